@@ -1,0 +1,151 @@
+/*
+ * rnnwave_sm100.h -- C-ABI of librnnwave_sm100.so, the B200 (sm_100a) implementation of the
+ * rnnwave multi-layer LSTM forward/backward path.
+ *
+ * This is the drop-in boundary under the reference's C++ API. Each entry point replaces one
+ * piece of the reference interface (paths relative to /root/reference/proj/include/rnnwave):
+ *
+ *   rw_create / rw_destroy      <- Engine::Engine(const LadderConfig&)       engine.hpp:71-75
+ *                                  (validation: LadderConfig::validate      config.hpp:74-96)
+ *   rw_set_params               <- the std::vector<LayerParams>& argument of forward /
+ *                                  backward_data (params.hpp:18-25) + pretranspose
+ *                                  (params.hpp:55-61) -> device repack, once per upload
+ *   rw_forward                  <- Engine::forward                          engine.hpp:82-123
+ *   rw_backward_data            <- Engine::backward_data                    engine.hpp:128-172
+ *   rw_weight_update            <- Engine::weight_update                    engine.hpp:178-217
+ *   rw_get_tape                 <- ForwardTape / BackwardState fields        engine.hpp:36-60
+ *   rw_flop_count_cell          <- flop_count                                cells.hpp:65-68
+ *   rw_run_pass / rw_upload_*   device-resident timed path (bench::time_level
+ *                                  run_once, bench.hpp:141-159)
+ *
+ * Conventions: plain pointers and sizes, no torch/STL types. Host matrices are fp32
+ * column-major exactly like rnnwave::Matrix (element (r, c) at c*rows + r). Per-layer
+ * arrays are passed as `const float* const*` with `layers` entries. Every call returns an
+ * rw_status; on error rw_last_error(ctx) holds the message. Messages mirror the reference
+ * exceptions (substrings "expected", "training", "stale tape" -- test_engine.cpp:220-256).
+ * Host-pointer entry points are synchronous. A context is not re-entrant (like Engine,
+ * SPEC.md:251): use one per host thread.
+ */
+#ifndef RNNWAVE_SM100_H
+#define RNNWAVE_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rw_ctx rw_ctx;
+
+typedef enum {
+  RW_OK = 0,
+  RW_EINVAL = 1, /* bad argument / shape / call order   -> std::invalid_argument */
+  RW_ECUDA = 2,  /* CUDA runtime or kernel failure       -> std::runtime_error   */
+  RW_ENOMEM = 3, /* device allocation failed             -> std::runtime_error   */
+  RW_ENCCL = 4,  /* collective failure                   -> std::runtime_error   */
+  RW_ESTATE = 5  /* e.g. persistent-kernel timeout       -> std::runtime_error   */
+} rw_status;
+
+typedef enum {
+  RW_PREC_BF16 = 0,     /* bf16 tensor-core operands, fp32 accumulate + fp32 cell math   */
+  RW_PREC_FP32 = 1      /* fp32-parity: 3xTF32 split operands, fp32 accumulate           */
+} rw_precision;
+
+typedef enum {
+  RW_SCHED_AUTO = 0,       /* persistent wavefront when it fits on the GPU, else stepwise */
+  RW_SCHED_STEPWISE = 1,   /* one fused kernel per (layer, step), CUDA-graph wavefront    */
+  RW_SCHED_PERSISTENT = 2  /* one kernel per pass, resident weights, flag wavefront       */
+} rw_schedule;
+
+/* Mirrors LadderConfig (config.hpp:49-97) plus the device knobs. */
+typedef struct {
+  int layers;
+  int hidden;
+  int input;
+  int batch;
+  int steps;
+  int cell_kind;   /* CellKind: must be 3 (Lstm) -- the north-star path */
+  int opt_level;   /* validated 0..6 for API compatibility; selects no alternate path */
+  int batch_steps; /* validated (1..steps) like the reference */
+  int workers;     /* validated > 0; unused on the device */
+  uint64_t seed;
+  int precision;   /* rw_precision */
+  int schedule;    /* rw_schedule */
+} rw_config;
+
+typedef enum {
+  RW_TAPE_X0 = 0,     /* I x B*T          (layer ignored) */
+  RW_TAPE_H = 1,      /* H x B*(T+1)      per layer       */
+  RW_TAPE_C = 2,      /* H x B*(T+1)      per layer       */
+  RW_TAPE_GATES = 3,  /* 4H x B*T         per layer (i,f,o,c' post-activations) */
+  RW_TAPE_TANH_C = 4, /* H x B*T          per layer       */
+  RW_TAPE_DGW = 5,    /* 4H x B*T         per layer (BackwardState::dgw_seq) */
+  RW_TAPE_Y = 6       /* H x B*T          (layer ignored) */
+} rw_tape;
+
+/* Validates like LadderConfig::validate; allocates every device buffer for the config. */
+int rw_create(const rw_config* cfg, int device, rw_ctx** out);
+void rw_destroy(rw_ctx* ctx);
+const char* rw_last_error(const rw_ctx* ctx);
+/* Static error text when rw_create itself fails (no context). */
+const char* rw_create_error(void);
+
+/* Layer parameters in the reference layout: W (4H x I_l), R (4H x H), b (4H, may be NULL =
+ * zeros). Host pointers; triggers the device repack for that layer. */
+int rw_set_params(rw_ctx* ctx, int layer, const float* W, const float* R, const float* b);
+
+/* Engine::forward. x: I x B*T host. h0/c0: NULL or `layers` host pointers of H x B.
+ * y: H x B*T host output (may be NULL). training != 0 records the tape for backward.
+ * Returns the tape generation id in *tape_id (may be NULL). */
+int rw_forward(rw_ctx* ctx, const float* x, int training, const float* const* h0,
+               const float* const* c0, float* y, uint64_t* tape_id);
+
+/* Engine::backward_data on tape `tape_id` (must be the context's latest training tape).
+ * dy: H x B*T host. dx0: I x B*T. dh0/dc0: `layers` pointers of H x B (any may be NULL). */
+int rw_backward_data(rw_ctx* ctx, uint64_t tape_id, const float* dy, float* dx0,
+                     float* const* dh0, float* const* dc0);
+
+/* Engine::weight_update: dW (4H x I_l), dR (4H x H), db (4H) per layer (NULL = skip). */
+int rw_weight_update(rw_ctx* ctx, uint64_t tape_id, float* const* dW, float* const* dR,
+                     float* const* db);
+
+/* Materialise one tape tensor (reference layout, unpadded) into a host buffer. */
+int rw_get_tape(rw_ctx* ctx, int which, int layer, float* host);
+
+/* ---- device-resident timed path (bench) ---- */
+/* Upload the synthetic x (I x B*T) and dy (H x B*T) once (host pointers). */
+int rw_upload_inputs(rw_ctx* ctx, const float* x, const float* dy);
+/* One pass on the device, inputs already resident: 0 = forward (inference), 1 = backward
+ * (backward_data + weight_update on the resident tape), 2 = both (training forward +
+ * backward_data + weight_update). Enqueued on `stream` (cudaStream_t, NULL = legacy default)
+ * and returns without synchronising. */
+int rw_run_pass(rw_ctx* ctx, int pass, void* stream);
+/* Wait for the context's work; reports kernel faults / persistent-kernel timeouts. */
+int rw_sync(rw_ctx* ctx);
+/* Enable per-phase CUDA-event timing of rw_run_pass (0 = off). When on, rw_phase_times
+ * returns the accumulated milliseconds and launch counts of the phases since the last reset:
+ * out_ms[0..5] = {repack/convert, fwd recurrent, bwd recurrent, weight-grad GEMMs,
+ * dx0 GEMM, db reduce}; out_launches likewise. */
+int rw_set_profiling(rw_ctx* ctx, int on);
+int rw_phase_times(rw_ctx* ctx, double* out_ms, int* out_launches, int n, int reset);
+/* The schedule the context actually uses for forward/backward (rw_schedule values), and the
+ * split-K factors chosen. */
+int rw_describe(rw_ctx* ctx, int* fwd_sched, int* bwd_sched, int* fwd_ksplit, int* bwd_ksplit);
+
+/* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
+int64_t rw_flop_count_cell(int hidden, int input, int batch);
+
+/* ---- unit-test hook: one tcgen05 GEMM on device pointers ----
+ * D (M x N, fp32, column-major, ldd) = A * B^T where A is M x K and B is N x K.
+ * a_mn_major=0: A stored K-major (element (m,k) at m*lda + k); 1: MN-major (k*lda + m).
+ * Likewise B. Operands are fp32 on the device and converted to the precision's operand
+ * planes internally. M, N, K must be multiples of 128/64/64. */
+int rw_test_gemm(int precision, int a_mn_major, int b_mn_major, int M, int N, int K,
+                 const float* dA, long long lda, const float* dB, long long ldb, float* dD,
+                 long long ldd, int bn);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

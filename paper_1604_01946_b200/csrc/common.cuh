@@ -1,0 +1,66 @@
+// common.cuh -- shared definitions between the sm_100a kernels and the host runtime.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace rw {
+
+// Operand precision of the tensor-core GEMMs. Accumulation and all pointwise cell math
+// are fp32 in both modes.
+//   kBF16  : operands rounded to bf16 (kind::f16), 1 plane.
+//   kTF32x3: operands split x = hi + lo, hi = tf32(x) (round-to-nearest), lo = x - hi, and
+//            D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::tf32), 2 planes -- the fp32-parity
+//            mode (normwise error ~1e-6 vs the fp32 reference engine).
+enum Prec : int { kBF16 = 0, kTF32x3 = 1 };
+
+struct PrecBF16 {
+  static constexpr int kPlanes = 1;
+  static constexpr int kElem = 2;
+  static constexpr int kAtomK = 64;  // elements per 128-byte swizzle row
+  static constexpr int kUmmaK = 16;
+  static constexpr uint32_t kFmt = 1;
+  static constexpr bool kTF32 = false;
+  static constexpr int kCombos = 1;
+};
+struct PrecTF32x3 {
+  static constexpr int kPlanes = 2;
+  static constexpr int kElem = 4;
+  static constexpr int kAtomK = 32;
+  static constexpr int kUmmaK = 8;
+  static constexpr uint32_t kFmt = 2;
+  static constexpr bool kTF32 = true;
+  static constexpr int kCombos = 3;
+};
+
+constexpr int kTileM = 128;      // UMMA M (cta_group::1)
+constexpr int kRowBytes = 128;   // one SWIZZLE_128B row
+constexpr int kUnitsPerFwdTile = 32;  // forward tile = 32 hidden units x 4 gates
+
+// Gate-interleaved row order used by every forward operand/accumulator:
+// row rho = tile*128 + g*32 + j  <->  gate g of hidden unit u = tile*32 + j.
+__host__ __device__ inline int rho_of(int g, int u) { return (u >> 5) * 128 + g * 32 + (u & 31); }
+__host__ __device__ inline int rho_gate(int rho) { return (rho & 127) >> 5; }
+__host__ __device__ inline int rho_unit(int rho) { return (rho >> 7) * 32 + (rho & 31); }
+
+// Output index mapping of the generic GEMM epilogue.
+enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1 };
+enum ColMode : int { kColIdentity = 0, kColBatchUnpad = 1 };
+
+// One (grouped) GEMM problem: D[MxN] = A[MxK] * B[NxK]^T, fp32 out.
+struct GemmDesc {
+  const CUtensorMap* a[2];
+  const CUtensorMap* b[2];
+  int M, N, K;         // tile-space dims (K multiple of the k-block)
+  int a_k_off, b_k_off;  // K coordinate offsets inside the A / B tensors
+  float* d;
+  long long ldd;
+  int row_mode, col_mode;
+  int H, Hp, B, Bp;    // for the unpermute / unpad maps
+  int m_valid, n_valid;  // identity-mode bounds
+  int accumulate;      // D += result instead of D = result
+};
+
+}  // namespace rw

@@ -1,0 +1,177 @@
+// gemm_tc.cuh -- warp-specialised tcgen05 GEMM for sm_100a (K1/K5/K6 of SURVEY §2.2):
+//   D[M x N] (fp32) = A[M x K] * B[N x K]^T
+// A and B are read from HBM/L2 by TMA into SWIZZLE_128B shared-memory stages (either
+// operand K-major or MN-major), multiplied by tcgen05.mma with the accumulator in TMEM,
+// and written by a 4-warp epilogue (tcgen05.ld -> registers -> coalesced global stores)
+// that can un-permute gate-interleaved rows and strip batch padding on the fly.
+//
+// Roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator,
+// warp 3 idle, warps 4..7 epilogue (warp w reads TMEM lane quarter w%4).
+// blockIdx.z indexes a table of GemmDesc so several independent GEMMs (e.g. dW and dR of
+// every layer) run as one grouped launch.
+#pragma once
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace rw {
+
+template <class P, bool kMN>
+struct OperandTile {
+  // Issue the TMA loads of one k-block of an operand tile (rows x kAtomK elements) into
+  // `dst` (rows * 128 bytes). K-major: one box {kAtomK, rows} at (k, row0).
+  // MN-major: rows / kAtomK boxes {kAtomK (along MN), kAtomK (K rows)} stacked at
+  // kAtomK * 128-byte strides (the UMMA LBO).
+  static __device__ __forceinline__ void load(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                              int row0, int rows, int k0) {
+    if constexpr (!kMN) {
+      tma_load_2d(dst, m, bar, k0, row0);
+    } else {
+      for (int c = 0; c < rows / P::kAtomK; ++c)
+        tma_load_2d(static_cast<uint8_t*>(dst) + c * P::kAtomK * kRowBytes, m, bar,
+                    row0 + c * P::kAtomK, k0);
+    }
+  }
+  // UMMA descriptor of k-substep kk (0 .. kAtomK/kUmmaK-1) of a tile at smem address s.
+  static __device__ __forceinline__ uint64_t desc(uint32_t s, int kk) {
+    if constexpr (!kMN) {
+      return sdesc_sw128(s + kk * P::kUmmaK * P::kElem, 16, 1024);
+    } else {
+      return sdesc_sw128(s + kk * P::kUmmaK * kRowBytes, P::kAtomK * kRowBytes, 1024);
+    }
+  }
+};
+
+__device__ __forceinline__ int gemm_out_row(const GemmDesc& g, int m) {
+  if (g.row_mode == kRowGateUnperm) {
+    const int u = rho_unit(m);
+    return u < g.H ? rho_gate(m) * g.H + u : -1;
+  }
+  return m < g.m_valid ? m : -1;
+}
+__device__ __forceinline__ long long gemm_out_col(const GemmDesc& g, int n) {
+  if (g.col_mode == kColBatchUnpad) {
+    const int t = n / g.Bp, b = n - t * g.Bp;
+    return b < g.B ? (long long)t * g.B + b : -1;
+  }
+  return n < g.n_valid ? n : -1;
+}
+
+template <class P, bool kAMN, bool kBMN>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm_tc(const GemmDesc* __restrict__ table, int bn, int stages) {
+  const GemmDesc& g = table[blockIdx.z];
+  const int m0 = blockIdx.x * kTileM;
+  const int n0 = blockIdx.y * bn;
+  if (m0 >= g.M || n0 >= g.N) return;
+  const int nkb = g.K / P::kAtomK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int a_bytes = kTileM * kRowBytes;
+  const int b_bytes = bn * kRowBytes;
+  const int stage_bytes = P::kPlanes * (a_bytes + b_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tmem_full = empty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)bn) tmem_cols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < P::kPlanes; ++p) {
+      prefetch_tmap(g.a[p]);
+      prefetch_tmap(g.b[p]);
+    }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], stage_bytes);
+      uint8_t* st = smem + s * stage_bytes;
+      const int k = kb * P::kAtomK;
+      for (int p = 0; p < P::kPlanes; ++p) {
+        OperandTile<P, kAMN>::load(st + p * a_bytes, g.a[p], &full[s], m0, kTileM, k + g.a_k_off);
+        OperandTile<P, kBMN>::load(st + P::kPlanes * a_bytes + p * b_bytes, g.b[p], &full[s], n0,
+                                   bn, k + g.b_k_off);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread)
+    const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, bn);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(&full[s], (kb / stages) & 1);
+      tc_fence_after();
+      const uint32_t st = smem_u32(smem + s * stage_bytes);
+      for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+        for (int c = 0; c < P::kCombos; ++c) {
+          // combos: (hi,hi), (hi,lo), (lo,hi); bf16 has only (hi,hi)
+          const int pa = (c == 2) ? 1 : 0;
+          const int pb = (c == 1) ? 1 : 0;
+          const uint64_t ad = OperandTile<P, kAMN>::desc(st + pa * a_bytes, kk);
+          const uint64_t bd = OperandTile<P, kBMN>::desc(st + P::kPlanes * a_bytes + pb * b_bytes, kk);
+          umma<P::kTF32>(tmem_base, ad, bd, idesc, (kb | kk | c) != 0);
+        }
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tmem_full);
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int m = m0 + q * 32 + lane;
+    const int orow = m < g.M ? gemm_out_row(g, m) : -1;
+    for (int c0 = 0; c0 < bn; c0 += 8) {
+      uint32_t v[8];
+      tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + c0, v);
+      tmem_ld_wait();
+      if (orow < 0) continue;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = n0 + c0 + j;
+        if (n >= g.N) break;
+        const long long oc = gemm_out_col(g, n);
+        if (oc < 0) continue;
+        float* dst = g.d + oc * g.ldd + orow;
+        const float val = __uint_as_float(v[j]);
+        *dst = g.accumulate ? *dst + val : val;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+}  // namespace rw

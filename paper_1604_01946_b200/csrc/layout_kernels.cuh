@@ -1,0 +1,133 @@
+// layout_kernels.cuh -- the HBM-bound layout kernels around the tensor-core path:
+//   K7 repack (params.hpp:55-61 pretranspose, re-imagined): reference column-major gate-
+//     stacked W/R (4H x I) -> padded, gate-interleaved, K-major operand planes;
+//   activation padding/conversion (x, h0, c0 -> padded tapes and operand planes);
+//   un-padding of tapes for read-back; the bias-gradient reduction.
+#pragma once
+
+#include "common.cuh"
+
+namespace rw {
+
+__device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long long idx, float v) {
+  if (prec == kBF16) {
+    static_cast<__nv_bfloat16*>(p0)[idx] = __float2bfloat16_rn(v);
+  } else {
+    uint32_t hi;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
+    const float fh = __uint_as_float(hi);
+    static_cast<float*>(p0)[idx] = fh;
+    static_cast<float*>(p1)[idx] = v - fh;
+  }
+}
+
+// Forward operand of layer l: rows rho (4Hp), K = [0, Ipl) from W, [Ipl, Ipl+Hp) from R.
+__global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__ R, int H, int I,
+                          int Hp, int Ipl, int prec, void* p0, void* p1) {
+  const long long K = Ipl + Hp;
+  const long long total = 4LL * Hp * K;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int rho = (int)(e / K);
+    const int k = (int)(e - rho * K);
+    const int g = rho_gate(rho), u = rho_unit(rho);
+    float v = 0.0f;
+    if (u < H) {
+      const long long row = (long long)g * H + u;
+      if (k < Ipl) {
+        if (k < I) v = W[(long long)k * 4 * H + row];
+      } else if (k - Ipl < H) {
+        v = R[(long long)(k - Ipl) * 4 * H + row];
+      }
+    }
+    store_planes(prec, p0, p1, e, v);
+  }
+}
+
+// Backward operand of layer l: rows = units (Hp), K = [W_{l+1}^T (4Hp, rho order)] ++
+// [R_l^T (4Hp, rho order)]; Wup may be null (top layer). Both sources are 4H x H.
+__global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict__ R, int H,
+                          int Hp, int prec, void* p0, void* p1) {
+  const int G4p = 4 * Hp;
+  const long long K = (Wup ? 2LL : 1LL) * G4p;
+  const long long total = (long long)Hp * K;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int u = (int)(e / K);
+    const int k = (int)(e - u * K);
+    const float* M = (Wup && k < G4p) ? Wup : R;
+    const int rho = k % G4p;
+    const int g = rho_gate(rho), up = rho_unit(rho);
+    float v = 0.0f;
+    if (u < H && up < H) v = M[(long long)u * 4 * H + (long long)g * H + up];
+    store_planes(prec, p0, p1, e, v);
+  }
+}
+
+// dx0 operand: W_0^T, rows = input features (Ip), K = 4Hp in rho order.
+__global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, int Ip, int prec,
+                           void* p0, void* p1) {
+  const int G4p = 4 * Hp;
+  const long long total = (long long)Ip * G4p;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / G4p);
+    const int rho = (int)(e - (long long)i * G4p);
+    const int g = rho_gate(rho), u = rho_unit(rho);
+    float v = 0.0f;
+    if (i < I && u < H) v = W0[(long long)i * 4 * H + (long long)g * H + u];
+    store_planes(prec, p0, p1, e, v);
+  }
+}
+
+// Reference-order padded bias: dst[g*Hp + u] = b[g*H + u].
+__global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* dst) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * Hp) return;
+  const int g = e / Hp, u = e - g * Hp;
+  dst[e] = (u < H && b) ? b[g * H + u] : 0.0f;
+}
+
+// Column-block padding: src is R x (nblk*B) column-major, dst is Rp x (nblk*Bp) starting at
+// column dst_col_off. Writes an fp32 copy and/or operand planes.
+__global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk, int Rp, int Bp,
+                           long long dst_col_off, float* dst_f32, int prec, void* p0, void* p1) {
+  const long long total = (long long)Rp * Bp * nblk;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long col = e / Rp;
+    const int r = (int)(e - col * Rp);
+    const int t = (int)(col / Bp), b = (int)(col - (long long)t * Bp);
+    const float v = (src && r < R && b < B) ? src[((long long)t * B + b) * R + r] : 0.0f;
+    const long long di = (dst_col_off + col) * Rp + r;
+    if (dst_f32) dst_f32[di] = v;
+    if (p0) store_planes(prec, p0, p1, di, v);
+  }
+}
+
+// Inverse: dst (G*R x nblk*B) from src (G*Rp x nblk*Bp at src_col_off); G gate blocks.
+__global__ void k_unpad_cols(const float* __restrict__ src, int Rp, int Bp, long long src_col_off,
+                             int G, int R, int B, int nblk, float* __restrict__ dst) {
+  const long long rows = (long long)G * R;
+  const long long total = rows * B * nblk;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long col = e / rows;
+    const int rr = (int)(e - col * rows);
+    const int g = rr / R, r = rr - g * R;
+    const int t = (int)(col / B), b = (int)(col - (long long)t * B);
+    dst[e] = src[(src_col_off + (long long)t * Bp + b) * G * Rp + (long long)g * Rp + r];
+  }
+}
+
+// db[g*H + u] = sum over partial slices (fixed order) of dbp[slice][g*Hp + u].
+__global__ void k_db_reduce(const float* __restrict__ dbp, int slices, int H, int Hp, float* db) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * H) return;
+  const int g = e / H, u = e - g * H;
+  float acc = 0.0f;
+  for (int s = 0; s < slices; ++s) acc += dbp[(long long)s * 4 * Hp + g * Hp + u];
+  db[e] = acc;
+}
+
+}  // namespace rw

@@ -1,0 +1,677 @@
+// lstm_step.cuh -- the fused recurrent kernels (SURVEY K2/K3 forward, K4 backward).
+//
+// Forward, per (layer l, step t, 128-row tile of gate-interleaved units):
+//     Z = [W_l | R_l] . [x_{l,t} ; h_{l,t-1}]          (tcgen05, K = I_l + H)
+//     i,f,o = sigmoid, c' = tanh, c = f c_prev + i c', h = o tanh(c)   (epilogue)
+// The LSTM cell of cells.hpp:227-260 is fused into the GEMM epilogue; the input GEMM
+// W.x (engine.hpp:347-365) is fused into the same accumulator (K concatenation).
+// Backward, per (layer l, step t, 128-unit tile):
+//     dh = [W_{l+1}^T | R_l^T] . [dG_{l+1,t} ; dG_{l,t+1}]  (+ dy for the top layer)
+//     dG_t, carry_c = cells.hpp:424-447 chain                (epilogue)
+// i.e. output_gemm of the layer above (engine.hpp:564-585) and recurrent_backward_gemm
+// (engine.hpp:538-560) share one accumulator and the pointwise backward runs on it.
+//
+// A tile's K range may be split over a cluster of `ksplit` CTAs (split-K); partial
+// accumulators are exchanged through distributed shared memory and every CTA runs the
+// cell epilogue for 1/ksplit of the batch columns.
+//
+// Two launch modes share the code:
+//   stepwise   : one launch per (layer, step); weights streamed by TMA every step;
+//                ordering comes from the stream/graph.
+//   persistent : one launch for all layers and steps (wavefront); each CTA owns
+//                one (layer, tile, k-slice), keeps its weight slice resident in shared
+//                memory, and waits on gpu-scope per-(layer, step) completion counters
+//                (release/acquire) instead of kernel boundaries.
+#pragma once
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace rw {
+
+constexpr int kMaxLayers = 16;
+constexpr int kXChunk = 64;  // batch columns per epilogue exchange chunk
+
+struct FwdLayer {
+  const CUtensorMap* a[2];   // [W|R] gate-interleaved rows, K-major: {Ipl + Hp, 4Hp}
+  const CUtensorMap* bx[2];  // layer input operand, K-major: {Ipl, cols}
+  const CUtensorMap* bh[2];  // own hidden operand, K-major: {Hp, Bp(T+1)}
+  int Ipl;
+  int bx_col_off;            // x_op: 0; h_op[l-1]: Bp (block t+1 holds h_t)
+  const float* bias;         // 4Hp, row g*Hp + u
+  float* h;                  // Hp x Bp(T+1)
+  float* c;                  // Hp x Bp(T+1)
+  void* hop[2];              // operand planes, Hp x Bp(T+1)
+  float* gates;              // 4Hp x Bp T (row g*Hp + u), null in inference
+  float* tanhc;              // Hp x Bp T, null in inference
+  uint32_t* flags;           // [T] completion counters
+};
+
+struct BwdLayer {
+  const CUtensorMap* a[2];   // [W_{l+1}^T | R_l^T] rows = units, K-major: {Kb, Hp}
+  const CUtensorMap* bup[2]; // dG operand of layer l+1, K-major: {4Hp, Bp T}
+  const CUtensorMap* bg[2];  // dG operand of layer l,   K-major: {4Hp, Bp T}
+  int has_up;
+  const float* dy;           // raw dy (H x B T), top layer only
+  const float* gates;
+  const float* tanhc;
+  const float* c;
+  float* dg;                 // fp32 dG tape, 4Hp x Bp T, row g*Hp + u
+  void* dgop[2];             // operand planes, row rho
+  float* carry_c;            // Hp x Bp
+  float* dbp;                // [ceil(Bp/64)*ksplit][4Hp] bias-gradient partial sums
+  float* dh0;                // Hp x Bp
+  float* dc0;                // Hp x Bp
+  uint32_t* flags;           // [T]
+};
+
+struct RecParams {
+  int L, H, Hp, B, Bp, T;
+  int ksplit;
+  int tiles;          // tiles per layer
+  int layer_base;     // layer of blockIdx.y == 0
+  int t_first;        // first step of this launch (fwd: ascending, bwd: descending)
+  int n_steps;        // steps in this launch (bwd: may include the dh0 step t = -1)
+  int persistent;
+  int resident;
+  int stages;
+  uint32_t flag_target;
+  int* error;
+  unsigned long long timeout_ns;
+};
+
+// ------------------------------------------------------------------ small helpers
+template <class P>
+__device__ __forceinline__ void store_operand(void* const* planes, long long idx, float v) {
+  if constexpr (P::kPlanes == 1) {
+    static_cast<__nv_bfloat16*>(planes[0])[idx] = __float2bfloat16_rn(v);
+  } else {
+    uint32_t hi;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
+    const float fh = __uint_as_float(hi);
+    static_cast<float*>(planes[0])[idx] = fh;
+    static_cast<float*>(planes[1])[idx] = v - fh;
+  }
+}
+
+__device__ __forceinline__ float sigmoid_ref(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+// Spin until *flag >= target (gpu-scope acquire), bounded by a timeout that records an
+// error instead of hanging the device.
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
+                                          const RecParams& p) {
+  if (ld_acquire_gpu(flag) >= target) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
+  while (ld_acquire_gpu(flag) < target) {
+    nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (globaltimer() - t0 > p.timeout_ns) {
+      atomicExch(p.error, 1);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, 1000000;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait_cluster(bar, phase)) {
+  }
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, uint32_t rank) {
+  const uint32_t remote = map_dsmem(smem_u32(local_bar), rank);
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+// Shared-memory carve-up common to both directions.
+struct RecSmem {
+  uint8_t* a_res;      // resident A k-blocks (or A stages when streamed)
+  uint8_t* b_st;       // B stages
+  float* xbuf;         // [kXChunk][128] partial accumulators for the exchange
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* a_full;
+  uint64_t* tmem_full;
+  uint64_t* tmem_empty;
+  uint64_t* xready;
+  uint64_t* xfree;
+  uint32_t* tmem_slot;
+};
+
+template <class P>
+__device__ __forceinline__ RecSmem carve(uint8_t* smem, int a_bytes_total, int b_stage_bytes,
+                                         int stages) {
+  RecSmem s;
+  s.a_res = smem;
+  s.b_st = smem + a_bytes_total;
+  s.xbuf = reinterpret_cast<float*>(s.b_st + stages * b_stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s.xbuf + kXChunk * kTileM);
+  s.full = bars;
+  s.empty = bars + stages;
+  s.a_full = bars + 2 * stages;
+  s.tmem_full = s.a_full + 1;
+  s.tmem_empty = s.a_full + 2;
+  s.xready = s.a_full + 3;
+  s.xfree = s.a_full + 4;
+  s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 5);
+  return s;
+}
+
+// Host-side mirror of the carve-up size.
+inline size_t rec_smem_bytes(int planes, int a_kblocks_resident_or_stages, int n, int stages) {
+  const size_t a = size_t(a_kblocks_resident_or_stages) * planes * kTileM * kRowBytes;
+  const size_t b = size_t(stages) * planes * n * kRowBytes;
+  const size_t x = size_t(kXChunk) * kTileM * 4;
+  const size_t bars = (2 * stages + 6) * 8 + 16;
+  return 1024 + a + b + x + bars;
+}
+
+// The two-level cluster exchange of one column chunk: publish my partial tile, wait for all
+// ranks, return. xc counts exchanges (phase parity).
+__device__ __forceinline__ void exchange_publish(const RecSmem& s, int ks, uint32_t xc) {
+  named_bar_sync(1, 128);
+  if (ks > 1) {
+    if (threadIdx.x == 128) {
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      for (int r = 0; r < ks; ++r) mbar_arrive_remote(s.xready, r);
+    }
+    mbar_wait_cluster(s.xready, xc & 1);
+  }
+}
+__device__ __forceinline__ void exchange_release(const RecSmem& s, int ks) {
+  named_bar_sync(1, 128);
+  if (ks > 1 && threadIdx.x == 128) {
+    for (int r = 0; r < ks; ++r) mbar_arrive_remote(s.xfree, r);
+  }
+}
+__device__ __forceinline__ void exchange_acquire_buffer(const RecSmem& s, int ks, uint32_t xc) {
+  if (ks > 1 && xc > 0) mbar_wait_cluster(s.xfree, (xc - 1) & 1);
+}
+
+// Read the sum over the cluster of xbuf[idx] (fixed rank order => deterministic).
+__device__ __forceinline__ float xsum(const RecSmem& s, int ks, int idx) {
+  if (ks == 1) return s.xbuf[idx];
+  const uint32_t local = smem_u32(s.xbuf + idx);
+  float acc = ld_dsmem_f32(map_dsmem(local, 0));
+  for (int r = 1; r < ks; ++r) acc += ld_dsmem_f32(map_dsmem(local, r));
+  return acc;
+}
+
+// ====================================================================== forward kernel
+template <class P>
+__global__ void __launch_bounds__(256, 1)
+    k_lstm_fwd(const FwdLayer* __restrict__ layers, RecParams p) {
+  const int l = p.layer_base + blockIdx.y;
+  const FwdLayer& Ly = layers[l];
+  const int ks = p.ksplit;
+  const int rank = (int)(blockIdx.x % ks);
+  const int tile = (int)(blockIdx.x / ks);
+  const int N = p.Bp;
+  const int nkb0 = Ly.Ipl / P::kAtomK;
+  const int nkb = nkb0 + p.Hp / P::kAtomK;
+  const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
+  const int my_nkb = kb_hi - kb_lo;
+  const int a_bytes = kTileM * kRowBytes;           // one plane of one k-block
+  const int b_bytes = N * kRowBytes;
+  const int b_stage = P::kPlanes * b_bytes;
+  const int a_stage = P::kPlanes * a_bytes;
+  const int a_total = p.resident ? my_nkb * a_stage : p.stages * a_stage;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)N) tmem_cols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    mbar_init(S.a_full, 1);
+    mbar_init(S.tmem_full, 1);
+    mbar_init(S.tmem_empty, 128);
+    mbar_init(S.xready, ks);
+    mbar_init(S.xfree, ks);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(S.tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *S.tmem_slot;
+  const int row0 = tile * kTileM;
+
+  if (warp == 0 && lane == 0) {
+    // ================= TMA producer
+    for (int pl = 0; pl < P::kPlanes; ++pl) {
+      prefetch_tmap(Ly.a[pl]);
+      prefetch_tmap(Ly.bx[pl]);
+      prefetch_tmap(Ly.bh[pl]);
+    }
+    if (p.resident) {
+      mbar_arrive_expect_tx(S.a_full, my_nkb * a_stage);
+      for (int kb = kb_lo; kb < kb_hi; ++kb)
+        for (int pl = 0; pl < P::kPlanes; ++pl)
+          tma_load_2d(S.a_res + (kb - kb_lo) * a_stage + pl * a_bytes, Ly.a[pl], S.a_full,
+                      kb * P::kAtomK, row0);
+    }
+    uint32_t pc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      const int t = p.t_first + it;
+      bool x_ready = false, h_ready = false;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
+        const bool seg0 = kb < nkb0;
+        if (p.persistent) {
+          if (seg0 && !x_ready) {
+            if (l > 0) wait_flag(&layers[l - 1].flags[t], p.flag_target, p);
+            fence_proxy_async_global();
+            x_ready = true;
+          }
+          if (!seg0 && !h_ready) {
+            if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p);
+            fence_proxy_async_global();
+            h_ready = true;
+          }
+        }
+        const int s = pc % p.stages;
+        mbar_wait(&S.empty[s], ((pc / p.stages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&S.full[s], b_stage + (p.resident ? 0 : a_stage));
+        uint8_t* bst = S.b_st + s * b_stage;
+        for (int pl = 0; pl < P::kPlanes; ++pl) {
+          if (seg0)
+            tma_load_2d(bst + pl * b_bytes, Ly.bx[pl], &S.full[s], kb * P::kAtomK,
+                        Ly.bx_col_off + t * p.Bp);
+          else
+            tma_load_2d(bst + pl * b_bytes, Ly.bh[pl], &S.full[s], (kb - nkb0) * P::kAtomK,
+                        t * p.Bp);
+          if (!p.resident)
+            tma_load_2d(S.a_res + s * a_stage + pl * a_bytes, Ly.a[pl], &S.full[s],
+                        kb * P::kAtomK, row0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ================= MMA issuer
+    const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
+    if (p.resident) mbar_wait(S.a_full, 0);
+    tc_fence_after();
+    uint32_t pc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      if (it > 0) {
+        mbar_wait(S.tmem_empty, (it - 1) & 1);
+        tc_fence_after();
+      }
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
+        const int s = pc % p.stages;
+        mbar_wait(&S.full[s], (pc / p.stages) & 1);
+        tc_fence_after();
+        const uint32_t a_base =
+            smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
+        const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+          for (int c = 0; c < P::kCombos; ++c) {
+            const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
+            const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+            const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+            umma<P::kTF32>(tmem_base, ad, bd, idesc, (kb != kb_lo || kk | c) ? 1u : 0u);
+          }
+        }
+        umma_commit(&S.empty[s]);
+      }
+      umma_commit(S.tmem_full);
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
+    const int et = threadIdx.x - 128;     // 0..127
+    const int q = warp & 3;               // TMEM lane quarter == gate
+    const int j = et & 31;                // unit within tile (cell phase)
+    const int cg = et >> 5;               // column group (cell phase)
+    const int u = tile * kUnitsPerFwdTile + j;
+    const long long Hp = p.Hp, G4 = 4 * Hp;
+    uint32_t xc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      const int t = p.t_first + it;
+      mbar_wait(S.tmem_full, it & 1);
+      tc_fence_after();
+      for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
+        const int nc = min(kXChunk, N - n0);
+        exchange_acquire_buffer(S, ks, xc);
+        // partial accumulator rows q*32+lane, columns n0..n0+nc -> xbuf[n][row]
+        for (int c0 = 0; c0 < nc; c0 += 8) {
+          uint32_t v[8];
+          tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = __uint_as_float(v[jj]);
+        }
+        if (n0 + kXChunk >= N) {
+          tc_fence_before();
+          mbar_arrive(S.tmem_empty);
+        }
+        exchange_publish(S, ks, xc);
+        // my column slice of this chunk
+        const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
+        for (int cc = c_lo + cg; cc < c_hi; cc += 4) {
+          const int n = n0 + cc;
+          const float zi = xsum(S, ks, cc * kTileM + 0 * 32 + j);
+          const float zf = xsum(S, ks, cc * kTileM + 1 * 32 + j);
+          const float zo = xsum(S, ks, cc * kTileM + 2 * 32 + j);
+          const float zc = xsum(S, ks, cc * kTileM + 3 * 32 + j);
+          const float ai = zi + Ly.bias[u];
+          const float af = zf + Ly.bias[Hp + u];
+          const float ao = zo + Ly.bias[2 * Hp + u];
+          const float ac = zc + Ly.bias[3 * Hp + u];
+          const float iv = sigmoid_ref(ai);
+          const float fv = sigmoid_ref(af);
+          const float ov = sigmoid_ref(ao);
+          const float cb = tanhf(ac);
+          const long long col_prev = (long long)t * p.Bp + n;  // block t   (c_{t-1})
+          const long long col_new = col_prev + p.Bp;           // block t+1 (c_t, h_t)
+          const float cp = Ly.c[col_prev * Hp + u];
+          const float t1 = fv * cp;
+          const float t2 = iv * cb;
+          const float cv = t1 + t2;
+          const float tcv = tanhf(cv);
+          const float hv = ov * tcv;
+          Ly.c[col_new * Hp + u] = cv;
+          Ly.h[col_new * Hp + u] = hv;
+          store_operand<P>(Ly.hop, col_new * Hp + u, hv);
+          if (Ly.gates) {
+            float* gp = Ly.gates + col_prev * G4 + u;
+            gp[0] = iv;
+            gp[Hp] = fv;
+            gp[2 * Hp] = ov;
+            gp[3 * Hp] = cb;
+            Ly.tanhc[col_prev * Hp + u] = tcv;
+          }
+        }
+        exchange_release(S, ks);
+      }
+      if (p.persistent) {
+        fence_proxy_async_global();
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) red_release_gpu_add(&Ly.flags[t], 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();  // no CTA leaves while peers may still read its smem
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+// ====================================================================== backward kernel
+template <class P>
+__global__ void __launch_bounds__(256, 1)
+    k_lstm_bwd(const BwdLayer* __restrict__ layers, RecParams p) {
+  const int l = p.layer_base + blockIdx.y;
+  const BwdLayer& Ly = layers[l];
+  const int ks = p.ksplit;
+  const int rank = (int)(blockIdx.x % ks);
+  const int tile = (int)(blockIdx.x / ks);
+  const int N = p.Bp;
+  const int G4p = 4 * p.Hp;
+  const int nkb0 = Ly.has_up ? G4p / P::kAtomK : 0;
+  const int nkb = nkb0 + G4p / P::kAtomK;
+  const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
+  const int my_nkb = kb_hi - kb_lo;
+  const int a_bytes = kTileM * kRowBytes;
+  const int b_bytes = N * kRowBytes;
+  const int b_stage = P::kPlanes * b_bytes;
+  const int a_stage = P::kPlanes * a_bytes;
+  const int a_total = p.resident ? my_nkb * a_stage : p.stages * a_stage;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)N) tmem_cols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    mbar_init(S.a_full, 1);
+    mbar_init(S.tmem_full, 1);
+    mbar_init(S.tmem_empty, 128);
+    mbar_init(S.xready, ks);
+    mbar_init(S.xfree, ks);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(S.tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *S.tmem_slot;
+  const int row0 = tile * kTileM;
+
+  // k-blocks this CTA multiplies at step t: seg0 needs dG_{l+1,t} (t >= 0), seg1 needs
+  // dG_{l,t+1} (t+1 <= T-1). Step t == -1 is the dh0 = R^T dG_{l,0} step (seg1 only).
+  auto kb_active = [&](int kb, int t) {
+    if (kb < nkb0) return t >= 0;
+    return t + 1 <= p.T - 1;
+  };
+
+  if (warp == 0 && lane == 0) {
+    for (int pl = 0; pl < P::kPlanes; ++pl) {
+      prefetch_tmap(Ly.a[pl]);
+      prefetch_tmap(Ly.bg[pl]);
+      if (Ly.has_up) prefetch_tmap(Ly.bup[pl]);
+    }
+    if (p.resident) {
+      mbar_arrive_expect_tx(S.a_full, my_nkb * a_stage);
+      for (int kb = kb_lo; kb < kb_hi; ++kb)
+        for (int pl = 0; pl < P::kPlanes; ++pl)
+          tma_load_2d(S.a_res + (kb - kb_lo) * a_stage + pl * a_bytes, Ly.a[pl], S.a_full,
+                      kb * P::kAtomK, row0);
+    }
+    uint32_t pc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      const int t = p.t_first - it;
+      bool up_ready = false, own_ready = false;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+        if (!kb_active(kb, t)) continue;
+        const bool seg0 = kb < nkb0;
+        if (p.persistent) {
+          if (seg0 && !up_ready) {
+            wait_flag(&layers[l + 1].flags[t], p.flag_target, p);
+            fence_proxy_async_global();
+            up_ready = true;
+          }
+          if (!seg0 && !own_ready) {
+            wait_flag(&Ly.flags[t + 1], p.flag_target, p);
+            fence_proxy_async_global();
+            own_ready = true;
+          }
+        }
+        const int s = pc % p.stages;
+        mbar_wait(&S.empty[s], ((pc / p.stages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&S.full[s], b_stage + (p.resident ? 0 : a_stage));
+        uint8_t* bst = S.b_st + s * b_stage;
+        for (int pl = 0; pl < P::kPlanes; ++pl) {
+          if (seg0)
+            tma_load_2d(bst + pl * b_bytes, Ly.bup[pl], &S.full[s], kb * P::kAtomK, t * p.Bp);
+          else
+            tma_load_2d(bst + pl * b_bytes, Ly.bg[pl], &S.full[s], (kb - nkb0) * P::kAtomK,
+                        (t + 1) * p.Bp);
+          if (!p.resident)
+            tma_load_2d(S.a_res + s * a_stage + pl * a_bytes, Ly.a[pl], &S.full[s],
+                        kb * P::kAtomK, row0);
+        }
+        ++pc;
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
+    if (p.resident) mbar_wait(S.a_full, 0);
+    tc_fence_after();
+    uint32_t pc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      const int t = p.t_first - it;
+      if (it > 0) {
+        mbar_wait(S.tmem_empty, (it - 1) & 1);
+        tc_fence_after();
+      }
+      bool first = true;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
+        if (!kb_active(kb, t)) continue;
+        const int s = pc % p.stages;
+        mbar_wait(&S.full[s], (pc / p.stages) & 1);
+        tc_fence_after();
+        const uint32_t a_base =
+            smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
+        const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+          for (int c = 0; c < P::kCombos; ++c) {
+            const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
+            const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+            const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+            umma<P::kTF32>(tmem_base, ad, bd, idesc, first ? 0u : 1u);
+            first = false;
+          }
+        }
+        umma_commit(&S.empty[s]);
+        ++pc;
+      }
+      umma_commit(S.tmem_full);
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue: split-K exchange + LSTM backward (cells.hpp:424-447)
+    const int et = threadIdx.x - 128;
+    const int q = warp & 3;
+    const int u = row0 + et;           // hidden unit of this thread (cell phase)
+    const long long Hp = p.Hp, G4 = 4 * Hp;
+    uint32_t xc = 0;
+    for (int it = 0; it < p.n_steps; ++it) {
+      const int t = p.t_first - it;
+      bool any = false;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) any |= kb_active(kb, t);
+      mbar_wait(S.tmem_full, it & 1);
+      tc_fence_after();
+      for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
+        const int nc = min(kXChunk, N - n0);
+        exchange_acquire_buffer(S, ks, xc);
+        for (int c0 = 0; c0 < nc; c0 += 8) {
+          uint32_t v[8];
+          tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = any ? __uint_as_float(v[jj]) : 0.0f;
+        }
+        if (n0 + kXChunk >= N) {
+          tc_fence_before();
+          mbar_arrive(S.tmem_empty);
+        }
+        exchange_publish(S, ks, xc);
+        const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
+        if (u < p.Hp) {
+          float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
+          for (int cc = c_lo; cc < c_hi; ++cc) {
+            const int n = n0 + cc;
+            const float acc = xsum(S, ks, cc * kTileM + et);
+            if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170)
+              Ly.dh0[(long long)n * Hp + u] = acc;
+              Ly.dc0[(long long)n * Hp + u] = Ly.carry_c[(long long)n * Hp + u];
+              continue;
+            }
+            float dh = acc;
+            if (Ly.dy) {
+              const float dyv = (u < p.H && n < p.B) ? Ly.dy[((long long)t * p.B + n) * p.H + u] : 0.0f;
+              dh = dyv + acc;
+            }
+            const long long col = (long long)t * p.Bp + n;
+            const float* gp = Ly.gates + col * G4 + u;
+            const float pi = gp[0], pf = gp[Hp], po = gp[2 * Hp], pcb = gp[3 * Hp];
+            const float ptc = Ly.tanhc[col * Hp + u];
+            const float pcp = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+            float* ccar = Ly.carry_c + (long long)n * Hp + u;
+            const float dci = (t == p.T - 1) ? 0.0f : *ccar;
+            const float q1 = dh * po;
+            const float s0 = ptc * ptc;
+            const float s1 = 1.0f - s0;
+            const float q2 = q1 * s1;
+            const float dc = dci + q2;
+            const float a1 = dc * pcb, a2 = a1 * pi, a3 = 1.0f - pi;
+            const float b1 = dc * pcp, b2 = b1 * pf, b3 = 1.0f - pf;
+            const float c1 = dh * ptc, c2 = c1 * po, c3 = 1.0f - po;
+            const float d1 = dc * pi, d2 = pcb * pcb, d3 = 1.0f - d2;
+            const float gi = a2 * a3, gf = b2 * b3, go = c2 * c3, gc = d1 * d3;
+            *ccar = dc * pf;
+            float* dgp = Ly.dg + col * G4 + u;
+            dgp[0] = gi;
+            dgp[Hp] = gf;
+            dgp[2 * Hp] = go;
+            dgp[3 * Hp] = gc;
+            const long long ob = col * G4;
+            store_operand<P>(Ly.dgop, ob + rho_of(0, u), gi);
+            store_operand<P>(Ly.dgop, ob + rho_of(1, u), gf);
+            store_operand<P>(Ly.dgop, ob + rho_of(2, u), go);
+            store_operand<P>(Ly.dgop, ob + rho_of(3, u), gc);
+            si += gi;
+            sf += gf;
+            so += go;
+            sc += gc;
+          }
+          if (t >= 0 && Ly.dbp) {
+            float* d = Ly.dbp + (long long)((n0 / kXChunk) * ks + rank) * G4 + u;
+            d[0] += si;
+            d[Hp] += sf;
+            d[2 * Hp] += so;
+            d[3 * Hp] += sc;
+          }
+        }
+        exchange_release(S, ks);
+      }
+      if (p.persistent && t >= 0) {
+        fence_proxy_async_global();
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) red_release_gpu_add(&Ly.flags[t], 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+}  // namespace rw

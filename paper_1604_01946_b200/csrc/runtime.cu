@@ -1,0 +1,1128 @@
+// runtime.cu -- librnnwave_sm100.so: device context, buffers, TMA descriptors, schedule
+// selection (persistent wavefront vs. stepwise CUDA-graph wavefront), and the C-ABI of
+// include/rnnwave_sm100.h. Replaces the reference Engine internals (engine.hpp:219-665),
+// scheduler.hpp (wavefront executor) and thread_pool.hpp ("streams") with device-side
+// equivalents; the arithmetic lives in lstm_step.cuh / gemm_tc.cuh / layout_kernels.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rnnwave_sm100.h"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "layout_kernels.cuh"
+#include "lstm_step.cuh"
+
+using namespace rw;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct RwError {
+  int code;
+  std::string msg;
+};
+
+#define RW_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw RwError{e_ == cudaErrorMemoryAllocation ? RW_ENOMEM : RW_ECUDA,              \
+                    std::string(#call) + ": " + cudaGetErrorString(e_)};                  \
+  } while (0)
+
+[[noreturn]] void einval(const std::string& m) { throw RwError{RW_EINVAL, m}; }
+
+// ------------------------------------------------------------------ TMA encode (driver API)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RW_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw RwError{RW_ECUDA, "cuTensorMapEncodeTiled unavailable"};
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major tensor: `inner` contiguous elements per row, `outer` rows, box {bi, bo},
+// SWIZZLE_128B, OOB zero fill.
+CUtensorMap make_map(const void* base, int prec, long long inner, long long outer, int bi, int bo) {
+  CUtensorMap m;
+  const int elem = prec == kBF16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(inner * elem)};
+  cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m,
+                           prec == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char b[256];
+    snprintf(b, sizeof b, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld box=%dx%d",
+             (int)r, inner, outer, bi, bo);
+    throw RwError{RW_ECUDA, b};
+  }
+  return m;
+}
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = n;
+    if (n) RW_CUDA(cudaMalloc(&p, n));
+    if (n) RW_CUDA(cudaMemset(p, 0, n));
+  }
+  float* f() const { return static_cast<float*>(p); }
+};
+
+// An operand tensor: 1 (bf16) or 2 (tf32 hi/lo) planes of `elems` elements.
+struct Operand {
+  DevBuf plane[2];
+  void alloc(int prec, size_t elems) {
+    const int planes = prec == kBF16 ? 1 : 2;
+    const size_t eb = prec == kBF16 ? 2 : 4;
+    for (int i = 0; i < 2; ++i) plane[i].alloc(i < planes ? elems * eb : 0);
+  }
+  void* p(int i) const { return plane[i].p; }
+};
+
+int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+int round_up(int a, int b) { return ceil_div(a, b) * b; }
+int grid_for(long long n) { return (int)std::min<long long>(std::max<long long>(1, (n + 255) / 256), 148LL * 16); }
+
+constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA
+
+template <class P>
+struct KernelSet {
+  static void* fwd() { return (void*)k_lstm_fwd<P>; }
+  static void* bwd() { return (void*)k_lstm_bwd<P>; }
+};
+
+}  // namespace
+
+// ====================================================================== context
+struct rw_ctx {
+  rw_config cfg{};
+  int dev = 0;
+  int prec = kBF16, planes = 1, elem = 2, atomK = 64;
+  int L = 0, H = 0, I = 0, B = 0, T = 0, Hp = 0, Ip = 0, Bp = 0;
+  std::string err;
+
+  // parameters (reference layout, device) + packed operands
+  std::vector<DevBuf> W, R, bias_raw;
+  std::vector<Operand> wf, wb;
+  Operand w0t;
+  std::vector<DevBuf> bias;
+  bool params_set_all = false;
+  std::vector<char> params_set;
+  bool dirty = true;
+
+  // activations / tapes
+  DevBuf x_raw, dy_raw;
+  Operand x_op;
+  std::vector<DevBuf> h, c, gates, tanhc, dg, carry_c, dh0, dc0, dbp;
+  std::vector<Operand> hop, dgop;
+  DevBuf dx0, y_raw, stage;  // unpadded outputs / staging
+  std::vector<DevBuf> dW, dR, db;
+  DevBuf flags_f, flags_b, errflag;
+
+  // descriptors
+  std::vector<CUtensorMap> maps;  // host copy
+  DevBuf maps_dev;
+  DevBuf fwd_layers, bwd_layers, gemm_wg, gemm_dx;
+  int n_wg = 0;
+
+  // schedule
+  int fwd_sched = RW_SCHED_STEPWISE, bwd_sched = RW_SCHED_STEPWISE;
+  int ks_f = 1, ks_b = 1, res_f = 0, res_b = 0, st_f = 4, st_b = 4;
+  size_t smem_f = 0, smem_b = 0;
+  int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
+  size_t smem_wg = 0, smem_dx = 0;
+
+  // streams / events / graphs
+  cudaStream_t main = nullptr;
+  std::vector<cudaStream_t> ls;
+  std::vector<cudaEvent_t> lev;
+  cudaEvent_t fork_ev = nullptr;
+  cudaGraphExec_t graph_both = nullptr, graph_fwd = nullptr, graph_fwd_train = nullptr,
+                  graph_bwd = nullptr;
+
+  // state
+  uint64_t tape_gen = 0;
+  bool tape_training = false;
+  bool bwd_done = false;
+  bool inputs_uploaded = false;
+
+  // profiling
+  bool profiling = false;
+  double phase_ms[6] = {0};
+  int phase_n[6] = {0};
+
+  ~rw_ctx();
+};
+
+namespace {
+
+// ------------------------------------------------------------------ schedule selection
+struct RecPlan {
+  int sched, ks, resident, stages;
+  size_t smem;
+};
+
+int max_active_clusters(void* kernel, int ks, size_t smem, int ctas) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctas, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = ks;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// kb_max: largest per-tile k-block count over layers; tiles per layer; L layers.
+RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles, int L, int N,
+                       int sms, const char* env_ks) {
+  RecPlan pl{RW_SCHED_STEPWISE, 1, 0, 4, 0};
+  int forced_ks = 0;
+  if (const char* e = getenv(env_ks)) forced_ks = atoi(e);
+  if (want != RW_SCHED_STEPWISE) {
+    for (int ks : {8, 4, 2, 1}) {
+      if (forced_ks && ks != forced_ks) continue;
+      if (ks > kb_max) continue;
+      const long long ctas = (long long)L * tiles * ks;
+      if (ctas > sms) continue;
+      for (int resident : {1, 0}) {
+        const int kbr = resident ? ceil_div(kb_max, ks) : 0;
+        int stages = 4;
+        size_t smem = rec_smem_bytes(planes, resident ? kbr : stages, N, stages);
+        while (smem > (size_t)kSmemLimit && stages > 2) {
+          --stages;
+          smem = rec_smem_bytes(planes, resident ? kbr : stages, N, stages);
+        }
+        if (smem > (size_t)kSmemLimit) continue;
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ks > 1) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        const int clusters = max_active_clusters(kernel, ks, smem, (int)ctas);
+        if ((long long)clusters * ks < ctas) continue;
+        return RecPlan{RW_SCHED_PERSISTENT, ks, resident, stages, smem};
+      }
+    }
+    if (want == RW_SCHED_PERSISTENT) einval("persistent schedule does not fit this configuration on the device");
+  }
+  // stepwise: split K so one layer's launch covers a fair share of the SMs
+  int ks = 1;
+  while (ks < 8 && (long long)tiles * ks * 2 <= sms && ks * 2 <= kb_max) ks *= 2;
+  if (forced_ks) ks = forced_ks;
+  int stages = 4;
+  size_t smem = rec_smem_bytes(planes, stages, N, stages);
+  while (smem > (size_t)kSmemLimit && stages > 2) {
+    --stages;
+    smem = rec_smem_bytes(planes, stages, N, stages);
+  }
+  if (smem > (size_t)kSmemLimit) einval("batch too large for the recurrent kernel tile");
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ks > 1) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return RecPlan{RW_SCHED_STEPWISE, ks, 0, stages, smem};
+}
+
+template <class P>
+void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_x, int grid_y,
+                size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid_x, grid_y, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = rp.ksplit;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  void* args[2] = {const_cast<void**>(&layers), const_cast<RecParams*>(&rp)};
+  RW_CUDA(cudaLaunchKernelExC(&lc, kernel, args));
+}
+
+size_t gemm_smem(int planes, int bn, int stages) {
+  return 1024 + (size_t)stages * planes * (kTileM + bn) * kRowBytes + (2 * stages + 2) * 8 + 16;
+}
+
+template <class P, bool AMN, bool BMN>
+void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
+                 cudaStream_t s) {
+  const size_t smem = gemm_smem(P::kPlanes, bn, stages);
+  auto k = k_gemm_tc<P, AMN, BMN>;
+  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
+  k<<<grid, 256, smem, s>>>(table_dev, bn, stages);
+  RW_CUDA(cudaGetLastError());
+}
+
+int gemm_stages(int planes, int bn) {
+  int st = 6;
+  while (st > 2 && gemm_smem(planes, bn, st) > (size_t)kSmemLimit) --st;
+  return st;
+}
+
+// ------------------------------------------------------------------ setup
+void validate(const rw_config& c) {
+  auto pos = [](int v, const char* n) {
+    if (v <= 0) einval(std::string("LadderConfig: ") + n + " must be positive, got " + std::to_string(v));
+  };
+  pos(c.layers, "layers");
+  pos(c.hidden, "hidden");
+  pos(c.input, "input");
+  pos(c.batch, "batch");
+  pos(c.steps, "steps");
+  pos(c.batch_steps, "batch_steps");
+  pos(c.workers, "workers");
+  if (c.opt_level < 0 || c.opt_level > 6)
+    einval("LadderConfig: opt_level must be in 0..6, got " + std::to_string(c.opt_level));
+  if (c.batch_steps > c.steps)
+    einval("LadderConfig: batch_steps " + std::to_string(c.batch_steps) + " exceeds steps " + std::to_string(c.steps));
+  if (c.cell_kind != 3) einval("rnnwave_sm100: only CellKind::Lstm (3) is implemented on the device");
+  if (c.precision != RW_PREC_BF16 && c.precision != RW_PREC_FP32) einval("rnnwave_sm100: unknown precision");
+  if (c.layers > kMaxLayers) einval("rnnwave_sm100: at most 16 layers");
+}
+
+int add_map(rw_ctx* x, const CUtensorMap& m) {
+  x->maps.push_back(m);
+  return (int)x->maps.size() - 1;
+}
+
+void build(rw_ctx* x) {
+  const rw_config& c = x->cfg;
+  x->prec = c.precision == RW_PREC_BF16 ? kBF16 : kTF32x3;
+  x->planes = x->prec == kBF16 ? 1 : 2;
+  x->elem = x->prec == kBF16 ? 2 : 4;
+  x->atomK = x->prec == kBF16 ? 64 : 32;
+  x->L = c.layers;
+  x->H = c.hidden;
+  x->I = c.input;
+  x->B = c.batch;
+  x->T = c.steps;
+  x->Hp = round_up(x->H, 64);
+  x->Ip = round_up(x->I, 64);
+  x->Bp = round_up(x->B, 16);
+  const int L = x->L, Hp = x->Hp, Ip = x->Ip, Bp = x->Bp, T = x->T, H = x->H, I = x->I, B = x->B;
+  const long long G4p = 4LL * Hp;
+  const long long colsT = (long long)Bp * T, colsT1 = (long long)Bp * (T + 1);
+  if (Bp > 256) einval("rnnwave_sm100: batch > 256 per context is not supported (split the minibatch)");
+
+  RW_CUDA(cudaSetDevice(x->dev));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->dev);
+
+  x->W.resize(L);
+  x->R.resize(L);
+  x->bias_raw.resize(L);
+  x->wf.resize(L);
+  x->wb.resize(L);
+  x->bias.resize(L);
+  x->params_set.assign(L, 0);
+  x->h.resize(L);
+  x->c.resize(L);
+  x->gates.resize(L);
+  x->tanhc.resize(L);
+  x->dg.resize(L);
+  x->carry_c.resize(L);
+  x->dh0.resize(L);
+  x->dc0.resize(L);
+  x->dbp.resize(L);
+  x->hop.resize(L);
+  x->dgop.resize(L);
+  x->dW.resize(L);
+  x->dR.resize(L);
+  x->db.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
+    x->W[l].alloc(4ULL * H * Il * 4);
+    x->R[l].alloc(4ULL * H * H * 4);
+    x->bias_raw[l].alloc(4ULL * H * 4);
+    x->wf[l].alloc(x->prec, (size_t)G4p * (Ipl + Hp));
+    x->wb[l].alloc(x->prec, (size_t)Hp * ((l < L - 1 ? 2 : 1) * G4p));
+    x->bias[l].alloc(G4p * 4);
+    x->h[l].alloc((size_t)Hp * colsT1 * 4);
+    x->c[l].alloc((size_t)Hp * colsT1 * 4);
+    x->hop[l].alloc(x->prec, (size_t)Hp * colsT1);
+    x->gates[l].alloc((size_t)G4p * colsT * 4);
+    x->tanhc[l].alloc((size_t)Hp * colsT * 4);
+    x->dg[l].alloc((size_t)G4p * colsT * 4);
+    x->dgop[l].alloc(x->prec, (size_t)G4p * colsT);
+    x->carry_c[l].alloc((size_t)Hp * Bp * 4);
+    x->dh0[l].alloc((size_t)Hp * Bp * 4);
+    x->dc0[l].alloc((size_t)Hp * Bp * 4);
+    x->dW[l].alloc(4ULL * H * Il * 4);
+    x->dR[l].alloc(4ULL * H * H * 4);
+    x->db[l].alloc(4ULL * H * 4);
+  }
+  x->w0t.alloc(x->prec, (size_t)Ip * G4p);
+  x->x_raw.alloc((size_t)I * B * T * 4);
+  x->dy_raw.alloc((size_t)H * B * T * 4);
+  x->x_op.alloc(x->prec, (size_t)Ip * colsT);
+  x->dx0.alloc((size_t)I * B * T * 4);
+  x->y_raw.alloc((size_t)std::max(4LL * H, (long long)std::max(H, I)) * B * (T + 1) * 4);
+  x->flags_f.alloc((size_t)L * T * 4);
+  x->flags_b.alloc((size_t)L * T * 4);
+  x->errflag.alloc(16);
+
+  // ---- schedules
+  void* kf = x->prec == kBF16 ? KernelSet<PrecBF16>::fwd() : KernelSet<PrecTF32x3>::fwd();
+  void* kb = x->prec == kBF16 ? KernelSet<PrecBF16>::bwd() : KernelSet<PrecTF32x3>::bwd();
+  const int kbf_max = (std::max(Ip, Hp) + Hp) / x->atomK;
+  const int kbb_max = (int)((L > 1 ? 2 : 1) * G4p / x->atomK);
+  const int tiles_f = Hp / kUnitsPerFwdTile, tiles_b = ceil_div(Hp, kTileM);
+  RecPlan pf = plan_recurrent(kf, c.schedule, x->planes, kbf_max, tiles_f, L, Bp, sms, "RW_FWD_KSPLIT");
+  RecPlan pb = plan_recurrent(kb, c.schedule, x->planes, kbb_max, tiles_b, L, Bp, sms, "RW_BWD_KSPLIT");
+  x->fwd_sched = pf.sched;
+  x->ks_f = pf.ks;
+  x->res_f = pf.resident;
+  x->st_f = pf.stages;
+  x->smem_f = pf.smem;
+  x->bwd_sched = pb.sched;
+  x->ks_b = pb.ks;
+  x->res_b = pb.resident;
+  x->st_b = pb.stages;
+  x->smem_b = pb.smem;
+  int slices_b = ceil_div(Bp, kXChunk) * x->ks_b;
+  for (int l = 0; l < L; ++l) x->dbp[l].alloc((size_t)slices_b * G4p * 4);
+
+  // ---- tensor maps
+  const int aK = x->atomK, prec = x->prec;
+  std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
+      m_dgMN(2 * L);
+  int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2];
+  x->bn_dx = colsT >= 256 ? 256 : 128;
+  x->bn_wg = 128;
+  for (int p = 0; p < x->planes; ++p) {
+    for (int l = 0; l < L; ++l) {
+      const int Ipl = l == 0 ? Ip : Hp;
+      m_wf[2 * l + p] = add_map(x, make_map(x->wf[l].p(p), prec, Ipl + Hp, G4p, aK, kTileM));
+      m_wb[2 * l + p] = add_map(x, make_map(x->wb[l].p(p), prec, (l < L - 1 ? 2 : 1) * G4p, Hp, aK, kTileM));
+      m_hopK[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp));
+      m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
+      m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
+      m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
+    }
+    m_xK[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp));
+    m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
+    m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
+    m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, x->bn_dx));
+  }
+  x->maps_dev.alloc(x->maps.size() * sizeof(CUtensorMap));
+  RW_CUDA(cudaMemcpy(x->maps_dev.p, x->maps.data(), x->maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  const CUtensorMap* MD = static_cast<const CUtensorMap*>(x->maps_dev.p);
+  auto mp = [&](int idx, int p) -> const CUtensorMap* { return p < x->planes ? MD + idx : nullptr; };
+
+  // ---- per-layer descriptor tables
+  std::vector<FwdLayer> fl(L);
+  std::vector<BwdLayer> bl(L);
+  uint32_t* ff = static_cast<uint32_t*>(x->flags_f.p);
+  uint32_t* fb = static_cast<uint32_t*>(x->flags_b.p);
+  for (int l = 0; l < L; ++l) {
+    FwdLayer& F = fl[l];
+    for (int p = 0; p < 2; ++p) {
+      F.a[p] = mp(m_wf[2 * l + (p % x->planes)], p);
+      F.bx[p] = l == 0 ? mp(m_xK[p % x->planes], p) : mp(m_hopK[2 * (l - 1) + (p % x->planes)], p);
+      F.bh[p] = mp(m_hopK[2 * l + (p % x->planes)], p);
+      F.hop[p] = x->hop[l].p(p);
+    }
+    F.Ipl = l == 0 ? Ip : Hp;
+    F.bx_col_off = l == 0 ? 0 : Bp;
+    F.bias = x->bias[l].f();
+    F.h = x->h[l].f();
+    F.c = x->c[l].f();
+    F.gates = x->gates[l].f();
+    F.tanhc = x->tanhc[l].f();
+    F.flags = ff + (size_t)l * T;
+    BwdLayer& Bd = bl[l];
+    for (int p = 0; p < 2; ++p) {
+      Bd.a[p] = mp(m_wb[2 * l + (p % x->planes)], p);
+      Bd.bup[p] = l < L - 1 ? mp(m_dgK[2 * (l + 1) + (p % x->planes)], p) : nullptr;
+      Bd.bg[p] = mp(m_dgK[2 * l + (p % x->planes)], p);
+      Bd.dgop[p] = x->dgop[l].p(p);
+    }
+    Bd.has_up = l < L - 1;
+    Bd.dy = l == L - 1 ? x->dy_raw.f() : nullptr;
+    Bd.gates = x->gates[l].f();
+    Bd.tanhc = x->tanhc[l].f();
+    Bd.c = x->c[l].f();
+    Bd.dg = x->dg[l].f();
+    Bd.carry_c = x->carry_c[l].f();
+    Bd.dbp = x->dbp[l].f();
+    Bd.dh0 = x->dh0[l].f();
+    Bd.dc0 = x->dc0[l].f();
+    Bd.flags = fb + (size_t)l * T;
+  }
+  x->fwd_layers.alloc(sizeof(FwdLayer) * L);
+  x->bwd_layers.alloc(sizeof(BwdLayer) * L);
+  RW_CUDA(cudaMemcpy(x->fwd_layers.p, fl.data(), sizeof(FwdLayer) * L, cudaMemcpyHostToDevice));
+  RW_CUDA(cudaMemcpy(x->bwd_layers.p, bl.data(), sizeof(BwdLayer) * L, cudaMemcpyHostToDevice));
+
+  // ---- GEMM tables: weight gradients (grouped, MN-major A and B) and dx0 (K-major)
+  std::vector<GemmDesc> wg;
+  for (int l = 0; l < L; ++l) {
+    const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
+    GemmDesc d{};
+    for (int p = 0; p < 2; ++p) {
+      d.a[p] = mp(m_dgMN[2 * l + (p % x->planes)], p);
+      d.b[p] = l == 0 ? mp(m_xMN[p % x->planes], p) : mp(m_hopMN[2 * (l - 1) + (p % x->planes)], p);
+    }
+    d.M = (int)G4p;
+    d.N = Ipl;
+    d.K = (int)colsT;
+    d.a_k_off = 0;
+    d.b_k_off = l == 0 ? 0 : Bp;  // X_l = h_{l-1} blocks 1..T
+    d.d = x->dW[l].f();
+    d.ldd = 4LL * H;
+    d.row_mode = kRowGateUnperm;
+    d.col_mode = kColIdentity;
+    d.H = H;
+    d.Hp = Hp;
+    d.B = B;
+    d.Bp = Bp;
+    d.m_valid = 4 * H;
+    d.n_valid = Il;
+    wg.push_back(d);
+    GemmDesc r = d;
+    for (int p = 0; p < 2; ++p) r.b[p] = mp(m_hopMN[2 * l + (p % x->planes)], p);
+    r.N = Hp;
+    r.b_k_off = 0;  // Hprev = blocks 0..T-1
+    r.d = x->dR[l].f();
+    r.n_valid = H;
+    wg.push_back(r);
+  }
+  x->n_wg = (int)wg.size();
+  x->gemm_wg.alloc(sizeof(GemmDesc) * wg.size());
+  RW_CUDA(cudaMemcpy(x->gemm_wg.p, wg.data(), sizeof(GemmDesc) * wg.size(), cudaMemcpyHostToDevice));
+  GemmDesc dx{};
+  for (int p = 0; p < 2; ++p) {
+    dx.a[p] = mp(m_w0t[p % x->planes], p);
+    dx.b[p] = mp(m_dg0dx[p % x->planes], p);
+  }
+  dx.M = Ip;
+  dx.N = (int)colsT;
+  dx.K = (int)G4p;
+  dx.d = x->dx0.f();
+  dx.ldd = I;
+  dx.row_mode = kRowIdentity;
+  dx.col_mode = kColBatchUnpad;
+  dx.H = H;
+  dx.Hp = Hp;
+  dx.B = B;
+  dx.Bp = Bp;
+  dx.m_valid = I;
+  dx.n_valid = (int)colsT;
+  x->gemm_dx.alloc(sizeof(GemmDesc));
+  RW_CUDA(cudaMemcpy(x->gemm_dx.p, &dx, sizeof(GemmDesc), cudaMemcpyHostToDevice));
+  x->st_wg = gemm_stages(x->planes, x->bn_wg);
+  x->st_dx = gemm_stages(x->planes, x->bn_dx);
+
+  // ---- streams
+  RW_CUDA(cudaStreamCreateWithFlags(&x->main, cudaStreamNonBlocking));
+  x->ls.resize(L);
+  x->lev.resize(L);
+  for (int l = 0; l < L; ++l) {
+    RW_CUDA(cudaStreamCreateWithFlags(&x->ls[l], cudaStreamNonBlocking));
+    RW_CUDA(cudaEventCreateWithFlags(&x->lev[l], cudaEventDisableTiming));
+  }
+  RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
+}
+
+// ------------------------------------------------------------------ phases
+struct PhaseTimer {
+  rw_ctx* x;
+  int phase;
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  PhaseTimer(rw_ctx* ctx, int ph, cudaStream_t st) : x(ctx), phase(ph), s(st) {
+    if (!x->profiling) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~PhaseTimer() {
+    if (!x->profiling) return;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    x->phase_ms[phase] += ms;
+    x->phase_n[phase] += 1;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+void repack_params(rw_ctx* x, cudaStream_t s) {
+  if (!x->dirty) return;
+  const int L = x->L, H = x->H, I = x->I, Hp = x->Hp, Ip = x->Ip;
+  for (int l = 0; l < L; ++l) {
+    const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
+    k_pack_wf<<<grid_for(4LL * Hp * (Ipl + Hp)), 256, 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp, Ipl,
+                                                             x->prec, x->wf[l].p(0), x->wf[l].p(1));
+    const float* wup = l < L - 1 ? x->W[l + 1].f() : nullptr;
+    k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(wup, x->R[l].f(), H, Hp, x->prec,
+                                                             x->wb[l].p(0), x->wb[l].p(1));
+    k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f());
+  }
+  k_pack_w0t<<<grid_for((long long)Ip * 4 * Hp), 256, 0, s>>>(x->W[0].f(), H, I, Hp, Ip, x->prec,
+                                                             x->w0t.p(0), x->w0t.p(1));
+  RW_CUDA(cudaGetLastError());
+  x->dirty = false;
+}
+
+RecParams rec_params(rw_ctx* x, bool fwd) {
+  RecParams rp{};
+  rp.L = x->L;
+  rp.H = x->H;
+  rp.Hp = x->Hp;
+  rp.B = x->B;
+  rp.Bp = x->Bp;
+  rp.T = x->T;
+  rp.ksplit = fwd ? x->ks_f : x->ks_b;
+  rp.tiles = fwd ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
+  rp.stages = fwd ? x->st_f : x->st_b;
+  rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
+  rp.error = static_cast<int*>(x->errflag.p);
+  rp.timeout_ns = 20ULL * 1000000000ULL;
+  return rp;
+}
+
+// x_op / tapes for a forward: h/c block 0 from h0/c0 (already staged on device as raw H x B
+// per layer at stage + l*H*B) or zeros.
+void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev) {
+  const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
+  k_pad_cols<<<grid_for((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
+      x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
+  for (int l = 0; l < L; ++l) {
+    const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
+    const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
+    k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(h0, H, B, 1, Hp, Bp, 0, x->h[l].f(), x->prec,
+                                                           x->hop[l].p(0), x->hop[l].p(1));
+    k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
+                                                           nullptr, nullptr);
+  }
+  RW_CUDA(cudaGetLastError());
+}
+
+template <class P>
+void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
+  RecParams rp = rec_params(x, true);
+  void* kern = KernelSet<P>::fwd();
+  // inference: no gate tapes (null gates pointer patched via a second descriptor table is
+  // avoided by simply keeping the tapes; cost is HBM writes only)
+  (void)training;
+  if (x->fwd_sched == RW_SCHED_PERSISTENT) {
+    RW_CUDA(cudaMemsetAsync(x->flags_f.p, 0, x->flags_f.bytes, s));
+    rp.persistent = 1;
+    rp.resident = x->res_f;
+    rp.layer_base = 0;
+    rp.t_first = 0;
+    rp.n_steps = x->T;
+    launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, x->L, x->smem_f, s);
+    return;
+  }
+  // stepwise wavefront: layer l on stream ls[l]; step (l,t) waits for (l-1,t)
+  rp.persistent = 0;
+  rp.resident = 0;
+  rp.n_steps = 1;
+  RW_CUDA(cudaEventRecord(x->fork_ev, s));
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->fork_ev, 0));
+  for (int t = 0; t < x->T; ++t) {
+    for (int l = 0; l < x->L; ++l) {
+      if (l > 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l - 1], 0));
+      rp.layer_base = l;
+      rp.t_first = t;
+      launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, x->ls[l]);
+      RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
+    }
+  }
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
+}
+
+template <class P>
+void run_backward_rec(rw_ctx* x, cudaStream_t s) {
+  RecParams rp = rec_params(x, false);
+  void* kern = KernelSet<P>::bwd();
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
+  if (x->bwd_sched == RW_SCHED_PERSISTENT) {
+    RW_CUDA(cudaMemsetAsync(x->flags_b.p, 0, x->flags_b.bytes, s));
+    rp.persistent = 1;
+    rp.resident = x->res_b;
+    rp.layer_base = 0;
+    rp.t_first = x->T - 1;
+    rp.n_steps = x->T + 1;  // T steps + the dh0 step
+    launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, x->L, x->smem_b, s);
+    return;
+  }
+  rp.persistent = 0;
+  rp.resident = 0;
+  rp.n_steps = 1;
+  RW_CUDA(cudaEventRecord(x->fork_ev, s));
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->fork_ev, 0));
+  for (int t = x->T - 1; t >= -1; --t) {
+    for (int l = x->L - 1; l >= 0; --l) {
+      if (l < x->L - 1 && t >= 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l + 1], 0));
+      rp.layer_base = l;
+      rp.t_first = t;
+      launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_b, x->ls[l]);
+      RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
+    }
+  }
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
+}
+
+template <class P>
+void run_dx0(rw_ctx* x, cudaStream_t s) {
+  launch_gemm<P, false, false>(static_cast<const GemmDesc*>(x->gemm_dx.p), 1, x->Ip,
+                               x->Bp * x->T, x->bn_dx, x->st_dx, s);
+}
+
+template <class P>
+void run_weight_grads(rw_ctx* x, cudaStream_t s) {
+  launch_gemm<P, true, true>(static_cast<const GemmDesc*>(x->gemm_wg.p), x->n_wg, 4 * x->Hp,
+                             std::max(x->Hp, x->Ip), x->bn_wg, x->st_wg, s);
+}
+
+void run_db(rw_ctx* x, cudaStream_t s) {
+  const int slices = ceil_div(x->Bp, kXChunk) * x->ks_b;
+  for (int l = 0; l < x->L; ++l)
+    k_db_reduce<<<ceil_div(4 * x->H, 256), 256, 0, s>>>(x->dbp[l].f(), slices, x->H, x->Hp, x->db[l].f());
+  RW_CUDA(cudaGetLastError());
+}
+
+template <class P>
+void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
+  {
+    PhaseTimer pt(x, 0, s);
+    repack_params(x, s);
+    if (pass != 1) forward_prologue(x, s, nullptr, nullptr);
+  }
+  if (pass != 1) {
+    PhaseTimer pt(x, 1, s);
+    run_forward_rec<P>(x, s, pass == 2);
+  }
+  if (pass == 0) return;
+  {
+    PhaseTimer pt(x, 2, s);
+    run_backward_rec<P>(x, s);
+  }
+  {
+    PhaseTimer pt(x, 3, s);
+    run_weight_grads<P>(x, s);
+  }
+  {
+    PhaseTimer pt(x, 4, s);
+    run_dx0<P>(x, s);
+  }
+  {
+    PhaseTimer pt(x, 5, s);
+    run_db(x, s);
+  }
+}
+
+void check_error_flag(rw_ctx* x) {
+  int e = 0;
+  RW_CUDA(cudaMemcpy(&e, x->errflag.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (e) {
+    cudaMemset(x->errflag.p, 0, sizeof(int));
+    throw RwError{RW_ESTATE, "persistent recurrent kernel timed out waiting for a wavefront flag"};
+  }
+}
+
+void sync_all(rw_ctx* x) {
+  RW_CUDA(cudaStreamSynchronize(x->main));
+  RW_CUDA(cudaGetLastError());
+  check_error_flag(x);
+}
+
+void d2h_unpad(rw_ctx* x, const float* src, int Rp, int Bp, long long col_off, int G, int R, int B,
+               int nblk, float* host) {
+  const long long n = (long long)G * R * B * nblk;
+  k_unpad_cols<<<grid_for(n), 256, 0, x->main>>>(src, Rp, Bp, col_off, G, R, B, nblk, x->y_raw.f());
+  RW_CUDA(cudaGetLastError());
+  RW_CUDA(cudaMemcpyAsync(host, x->y_raw.p, n * 4, cudaMemcpyDeviceToHost, x->main));
+  RW_CUDA(cudaStreamSynchronize(x->main));
+}
+
+template <typename F>
+int guarded(rw_ctx* x, F&& f) {
+  try {
+    f();
+    return RW_OK;
+  } catch (const RwError& e) {
+    if (x) x->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    if (x) x->err = e.what();
+    return RW_ECUDA;
+  }
+}
+
+std::string g_create_err;
+
+}  // namespace
+
+rw_ctx::~rw_ctx() {
+  if (main) cudaStreamSynchronize(main);
+  for (auto s : ls) cudaStreamDestroy(s);
+  for (auto e : lev) cudaEventDestroy(e);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (main) cudaStreamDestroy(main);
+}
+
+// ====================================================================== C-ABI
+extern "C" {
+
+int rw_create(const rw_config* cfg, int device, rw_ctx** out) {
+  if (!cfg || !out) {
+    g_create_err = "rw_create: null argument";
+    return RW_EINVAL;
+  }
+  *out = nullptr;
+  rw_ctx* x = new rw_ctx();
+  x->cfg = *cfg;
+  x->dev = device;
+  int rc = guarded(x, [&] {
+    validate(*cfg);
+    build(x);
+  });
+  if (rc != RW_OK) {
+    g_create_err = x->err;
+    delete x;
+    return rc;
+  }
+  *out = x;
+  return RW_OK;
+}
+
+void rw_destroy(rw_ctx* ctx) { delete ctx; }
+
+const char* rw_last_error(const rw_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+const char* rw_create_error(void) { return g_create_err.c_str(); }
+
+int64_t rw_flop_count_cell(int hidden, int input, int batch) {
+  return 2LL * 4 * hidden * ((int64_t)input + hidden) * batch;
+}
+
+int rw_set_params(rw_ctx* x, int layer, const float* W, const float* R, const float* b) {
+  return guarded(x, [&] {
+    if (layer < 0 || layer >= x->L) einval("rw_set_params: layer " + std::to_string(layer) + " out of range");
+    if (!W || !R) einval("rw_set_params: W and R are required");
+    RW_CUDA(cudaSetDevice(x->dev));
+    const int Il = layer == 0 ? x->I : x->H;
+    RW_CUDA(cudaMemcpy(x->W[layer].p, W, 4ULL * x->H * Il * 4, cudaMemcpyHostToDevice));
+    RW_CUDA(cudaMemcpy(x->R[layer].p, R, 4ULL * x->H * x->H * 4, cudaMemcpyHostToDevice));
+    if (b)
+      RW_CUDA(cudaMemcpy(x->bias_raw[layer].p, b, 4ULL * x->H * 4, cudaMemcpyHostToDevice));
+    else
+      RW_CUDA(cudaMemset(x->bias_raw[layer].p, 0, 4ULL * x->H * 4));
+    x->params_set[layer] = 1;
+    x->dirty = true;
+  });
+}
+
+static void require_params(rw_ctx* x) {
+  for (int l = 0; l < x->L; ++l)
+    if (!x->params_set[l])
+      einval("engine: expected " + std::to_string(x->L) + " layer parameter sets, layer " +
+             std::to_string(l) + " was never set");
+}
+
+int rw_forward(rw_ctx* x, const float* xin, int training, const float* const* h0,
+               const float* const* c0, float* y, uint64_t* tape_id) {
+  return guarded(x, [&] {
+    if (!xin) einval("forward: x is null, expected " + std::to_string(x->I) + "x" + std::to_string(x->B * x->T));
+    require_params(x);
+    RW_CUDA(cudaSetDevice(x->dev));
+    const size_t hb = (size_t)x->H * x->B;
+    RW_CUDA(cudaMemcpyAsync(x->x_raw.p, xin, (size_t)x->I * x->B * x->T * 4, cudaMemcpyHostToDevice, x->main));
+    // stage h0 / c0 contiguously in y_raw (large enough: >= 2 * L * H * B is not guaranteed,
+    // so use dedicated temporaries)
+    DevBuf th0, tc0;
+    if (h0) {
+      th0.alloc(hb * x->L * 4);
+      for (int l = 0; l < x->L; ++l)
+        RW_CUDA(cudaMemcpy(th0.f() + l * hb, h0[l], hb * 4, cudaMemcpyHostToDevice));
+    }
+    if (c0) {
+      tc0.alloc(hb * x->L * 4);
+      for (int l = 0; l < x->L; ++l)
+        RW_CUDA(cudaMemcpy(tc0.f() + l * hb, c0[l], hb * 4, cudaMemcpyHostToDevice));
+    }
+    repack_params(x, x->main);
+    forward_prologue(x, x->main, h0 ? th0.f() : nullptr, c0 ? tc0.f() : nullptr);
+    if (x->prec == kBF16)
+      run_forward_rec<PrecBF16>(x, x->main, training != 0);
+    else
+      run_forward_rec<PrecTF32x3>(x, x->main, training != 0);
+    sync_all(x);
+    x->inputs_uploaded = false;
+    x->tape_gen += 1;
+    x->tape_training = training != 0;
+    x->bwd_done = false;
+    if (tape_id) *tape_id = x->tape_gen;
+    if (y) d2h_unpad(x, x->h[x->L - 1].f(), x->Hp, x->Bp, x->Bp, 1, x->H, x->B, x->T, y);
+  });
+}
+
+static void check_tape(rw_ctx* x, uint64_t id) {
+  if (id != x->tape_gen || x->tape_gen == 0)
+    einval("engine: stale tape, the device holds tape " + std::to_string(x->tape_gen) +
+           " but tape " + std::to_string(id) + " was passed");
+  if (!x->tape_training) einval("engine: tape was recorded without training mode");
+}
+
+int rw_backward_data(rw_ctx* x, uint64_t tape_id, const float* dy, float* dx0, float* const* dh0,
+                     float* const* dc0) {
+  return guarded(x, [&] {
+    check_tape(x, tape_id);
+    if (!dy) einval("backward_data: dy is null, expected " + std::to_string(x->H) + "x" + std::to_string(x->B * x->T));
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaMemcpyAsync(x->dy_raw.p, dy, (size_t)x->H * x->B * x->T * 4, cudaMemcpyHostToDevice, x->main));
+    repack_params(x, x->main);
+    if (x->prec == kBF16) {
+      run_backward_rec<PrecBF16>(x, x->main);
+      run_dx0<PrecBF16>(x, x->main);
+    } else {
+      run_backward_rec<PrecTF32x3>(x, x->main);
+      run_dx0<PrecTF32x3>(x, x->main);
+    }
+    sync_all(x);
+    x->bwd_done = true;
+    if (dx0) RW_CUDA(cudaMemcpy(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < x->L; ++l) {
+      if (dh0 && dh0[l]) d2h_unpad(x, x->dh0[l].f(), x->Hp, x->Bp, 0, 1, x->H, x->B, 1, dh0[l]);
+      if (dc0 && dc0[l]) d2h_unpad(x, x->dc0[l].f(), x->Hp, x->Bp, 0, 1, x->H, x->B, 1, dc0[l]);
+    }
+  });
+}
+
+int rw_weight_update(rw_ctx* x, uint64_t tape_id, float* const* dW, float* const* dR, float* const* db) {
+  return guarded(x, [&] {
+    check_tape(x, tape_id);
+    if (!x->bwd_done) einval("weight_update: backward state layer count mismatch (run backward_data on this tape first)");
+    RW_CUDA(cudaSetDevice(x->dev));
+    if (x->prec == kBF16)
+      run_weight_grads<PrecBF16>(x, x->main);
+    else
+      run_weight_grads<PrecTF32x3>(x, x->main);
+    run_db(x, x->main);
+    sync_all(x);
+    for (int l = 0; l < x->L; ++l) {
+      const int Il = l == 0 ? x->I : x->H;
+      if (dW && dW[l]) RW_CUDA(cudaMemcpy(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpy(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost));
+      if (db && db[l]) RW_CUDA(cudaMemcpy(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int rw_get_tape(rw_ctx* x, int which, int layer, float* host) {
+  return guarded(x, [&] {
+    if (!host) einval("rw_get_tape: null destination");
+    if (which != RW_TAPE_X0 && which != RW_TAPE_Y && (layer < 0 || layer >= x->L))
+      einval("rw_get_tape: layer out of range");
+    if (x->tape_gen == 0) einval("rw_get_tape: no forward pass has run");
+    RW_CUDA(cudaSetDevice(x->dev));
+    const int H = x->H, B = x->B, T = x->T, Hp = x->Hp, Bp = x->Bp;
+    switch (which) {
+      case RW_TAPE_X0:
+        RW_CUDA(cudaMemcpy(host, x->x_raw.p, (size_t)x->I * B * T * 4, cudaMemcpyDeviceToHost));
+        break;
+      case RW_TAPE_Y:
+        d2h_unpad(x, x->h[x->L - 1].f(), Hp, Bp, Bp, 1, H, B, T, host);
+        break;
+      case RW_TAPE_H:
+        d2h_unpad(x, x->h[layer].f(), Hp, Bp, 0, 1, H, B, T + 1, host);
+        break;
+      case RW_TAPE_C:
+        d2h_unpad(x, x->c[layer].f(), Hp, Bp, 0, 1, H, B, T + 1, host);
+        break;
+      case RW_TAPE_GATES:
+        if (!x->tape_training) einval("engine: tape was recorded without training mode");
+        d2h_unpad(x, x->gates[layer].f(), Hp, Bp, 0, 4, H, B, T, host);
+        break;
+      case RW_TAPE_TANH_C:
+        if (!x->tape_training) einval("engine: tape was recorded without training mode");
+        d2h_unpad(x, x->tanhc[layer].f(), Hp, Bp, 0, 1, H, B, T, host);
+        break;
+      case RW_TAPE_DGW:
+        if (!x->bwd_done) einval("rw_get_tape: no backward pass on the current tape");
+        d2h_unpad(x, x->dg[layer].f(), Hp, Bp, 0, 4, H, B, T, host);
+        break;
+      default:
+        einval("rw_get_tape: unknown tape id");
+    }
+  });
+}
+
+int rw_upload_inputs(rw_ctx* x, const float* xin, const float* dy) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaSetDevice(x->dev));
+    if (xin) RW_CUDA(cudaMemcpy(x->x_raw.p, xin, (size_t)x->I * x->B * x->T * 4, cudaMemcpyHostToDevice));
+    if (dy) RW_CUDA(cudaMemcpy(x->dy_raw.p, dy, (size_t)x->H * x->B * x->T * 4, cudaMemcpyHostToDevice));
+    x->inputs_uploaded = true;
+  });
+}
+
+int rw_run_pass(rw_ctx* x, int pass, void* stream) {
+  return guarded(x, [&] {
+    if (pass < 0 || pass > 2) einval("rw_run_pass: pass must be 0 (fwd), 1 (bwd) or 2 (both)");
+    require_params(x);
+    RW_CUDA(cudaSetDevice(x->dev));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
+    if (pass == 1 && (x->tape_gen == 0 || !x->tape_training))
+      einval("rw_run_pass: backward needs a training tape (run pass 2 once first)");
+    if (x->prec == kBF16)
+      enqueue_pass<PrecBF16>(x, pass, s);
+    else
+      enqueue_pass<PrecTF32x3>(x, pass, s);
+    if (pass != 1) {
+      x->tape_gen += 1;
+      x->tape_training = pass == 2;
+    }
+    x->bwd_done = pass != 0;
+  });
+}
+
+int rw_sync(rw_ctx* x) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaDeviceSynchronize());
+    RW_CUDA(cudaGetLastError());
+    check_error_flag(x);
+  });
+}
+
+int rw_set_profiling(rw_ctx* x, int on) {
+  return guarded(x, [&] { x->profiling = on != 0; });
+}
+
+int rw_phase_times(rw_ctx* x, double* out_ms, int* out_n, int n, int reset) {
+  return guarded(x, [&] {
+    for (int i = 0; i < n && i < 6; ++i) {
+      if (out_ms) out_ms[i] = x->phase_ms[i];
+      if (out_n) out_n[i] = x->phase_n[i];
+    }
+    if (reset)
+      for (int i = 0; i < 6; ++i) {
+        x->phase_ms[i] = 0;
+        x->phase_n[i] = 0;
+      }
+  });
+}
+
+int rw_describe(rw_ctx* x, int* fs, int* bs, int* kf, int* kb) {
+  return guarded(x, [&] {
+    if (fs) *fs = x->fwd_sched;
+    if (bs) *bs = x->bwd_sched;
+    if (kf) *kf = x->ks_f;
+    if (kb) *kb = x->ks_b;
+  });
+}
+
+int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const float* dA,
+                 long long lda, const float* dB, long long ldb, float* dD, long long ldd, int bn) {
+  return guarded(nullptr, [&] {
+    const int prec = precision == RW_PREC_BF16 ? kBF16 : kTF32x3;
+    const int aK = prec == kBF16 ? 64 : 32;
+    if (M % 128 || N % bn || K % 64 || (bn != 64 && bn != 128 && bn != 256)) einval("rw_test_gemm: bad shape");
+    // element counts of the stored operands
+    const long long a_elems = a_mn ? (long long)K * lda : (long long)M * lda;
+    const long long b_elems = b_mn ? (long long)K * ldb : (long long)N * ldb;
+    Operand A, Bo;
+    A.alloc(prec, a_elems);
+    Bo.alloc(prec, b_elems);
+    k_pad_cols<<<grid_for(a_elems), 256>>>(dA, (int)a_elems, 1, 1, (int)a_elems, 1, 0, nullptr, prec, A.p(0), A.p(1));
+    k_pad_cols<<<grid_for(b_elems), 256>>>(dB, (int)b_elems, 1, 1, (int)b_elems, 1, 0, nullptr, prec, Bo.p(0), Bo.p(1));
+    RW_CUDA(cudaGetLastError());
+    std::vector<CUtensorMap> maps;
+    for (int p = 0; p < (prec == kBF16 ? 1 : 2); ++p) {
+      maps.push_back(a_mn ? make_map(A.p(p), prec, lda, K, aK, aK) : make_map(A.p(p), prec, lda, M, aK, 128));
+      maps.push_back(b_mn ? make_map(Bo.p(p), prec, ldb, K, aK, aK) : make_map(Bo.p(p), prec, ldb, N, aK, bn));
+    }
+    DevBuf md;
+    md.alloc(maps.size() * sizeof(CUtensorMap));
+    RW_CUDA(cudaMemcpy(md.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    const CUtensorMap* MD = static_cast<const CUtensorMap*>(md.p);
+    GemmDesc g{};
+    g.a[0] = MD + 0;
+    g.b[0] = MD + 1;
+    if (prec != kBF16) {
+      g.a[1] = MD + 2;
+      g.b[1] = MD + 3;
+    }
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.d = dD;
+    g.ldd = ldd;
+    g.row_mode = kRowIdentity;
+    g.col_mode = kColIdentity;
+    g.m_valid = M;
+    g.n_valid = N;
+    DevBuf gd;
+    gd.alloc(sizeof(GemmDesc));
+    RW_CUDA(cudaMemcpy(gd.p, &g, sizeof g, cudaMemcpyHostToDevice));
+    const GemmDesc* G = static_cast<const GemmDesc*>(gd.p);
+    const int planes = prec == kBF16 ? 1 : 2;
+    const int st = gemm_stages(planes, bn);
+    if (prec == kBF16) {
+      if (!a_mn && !b_mn) launch_gemm<PrecBF16, false, false>(G, 1, M, N, bn, st, 0);
+      if (!a_mn && b_mn) launch_gemm<PrecBF16, false, true>(G, 1, M, N, bn, st, 0);
+      if (a_mn && !b_mn) launch_gemm<PrecBF16, true, false>(G, 1, M, N, bn, st, 0);
+      if (a_mn && b_mn) launch_gemm<PrecBF16, true, true>(G, 1, M, N, bn, st, 0);
+    } else {
+      if (!a_mn && !b_mn) launch_gemm<PrecTF32x3, false, false>(G, 1, M, N, bn, st, 0);
+      if (!a_mn && b_mn) launch_gemm<PrecTF32x3, false, true>(G, 1, M, N, bn, st, 0);
+      if (a_mn && !b_mn) launch_gemm<PrecTF32x3, true, false>(G, 1, M, N, bn, st, 0);
+      if (a_mn && b_mn) launch_gemm<PrecTF32x3, true, true>(G, 1, M, N, bn, st, 0);
+    }
+    RW_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+"""Host-side mirror of the reference rnnwave C++ API (proj/include/rnnwave), backed by the
+sm_100a library through its C-ABI.
+
+Same names, argument meaning and error behaviour as the reference, so parity tests read like
+the reference's own tests:
+
+    LadderConfig      config.hpp:49-97   (validate() raises ValueError with the same text)
+    LayerParams       params.hpp:18-25
+    init_params       params.hpp:31-51   (SplitMix64 streams 2l / 2l+1, U[-1/sqrt(H), 1/sqrt(H)])
+    pretranspose      params.hpp:55-61
+    make_input/make_dy verify.hpp:38-44  (streams 1000 / 1001)
+    Engine.forward / backward_data / weight_update   engine.hpp:82-217
+    ForwardTape / ForwardResult / BackwardState / Gradients   engine.hpp:36-67
+    flop_count        cells.hpp:65-68
+
+Matrices are numpy float32 arrays in Fortran (column-major) order with shape (rows, cols),
+i.e. exactly rnnwave::Matrix's memory layout. std::invalid_argument maps to ValueError and
+std::runtime_error to RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+_F = C.POINTER(C.c_float)
+
+CELL_LSTM = 3
+CELL_NAMES = {0: "rnn-tanh", 1: "rnn-relu", 2: "gru", 3: "lstm"}
+
+
+def _fp(a):
+    return None if a is None else a.ctypes.data_as(_F)
+
+
+def fmat(rows: int, cols: int) -> np.ndarray:
+    return np.zeros((rows, cols), dtype=np.float32, order="F")
+
+
+def as_matrix(a, rows: int | None = None, cols: int | None = None) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float32)
+    if a.ndim == 1 and rows is not None and cols is not None and a.size == rows * cols:
+        a = a.reshape((rows, cols), order="F")
+    return np.asfortranarray(a)
+
+
+# ------------------------------------------------------------------ config / params
+@dataclass
+class LadderConfig:
+    layers: int = 1
+    hidden: int = 1
+    input: int = 1
+    batch: int = 1
+    steps: int = 1
+    kind: int = CELL_LSTM
+    opt_level: int = 0
+    batch_steps: int = 1
+    workers: int = 1
+    seed: int = 0
+
+    def input_width(self, layer: int) -> int:
+        return self.input if layer == 0 else self.hidden
+
+    def effective_batch_steps(self) -> int:
+        return 1 if self.opt_level < 5 else min(self.batch_steps, self.steps)
+
+    def num_blocks(self) -> int:
+        s = self.effective_batch_steps()
+        return (self.steps + s - 1) // s
+
+    def validate(self) -> None:
+        for name in ("layers", "hidden", "input", "batch", "steps", "batch_steps", "workers"):
+            v = getattr(self, name)
+            if v <= 0:
+                raise ValueError(f"LadderConfig: {name} must be positive, got {v}")
+        if self.opt_level < 0 or self.opt_level > 6:
+            raise ValueError(f"LadderConfig: opt_level must be in 0..6, got {self.opt_level}")
+        if self.batch_steps > self.steps:
+            raise ValueError(f"LadderConfig: batch_steps {self.batch_steps} exceeds steps {self.steps}")
+
+
+def gate_count(kind: int) -> int:
+    return {0: 1, 1: 1, 2: 3, 3: 4}[kind]
+
+
+@dataclass
+class LayerParams:
+    w: np.ndarray
+    r: np.ndarray
+    bias: np.ndarray
+    wt: np.ndarray | None = None
+    rt: np.ndarray | None = None
+    transposed: bool = False
+
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _mix(z: np.ndarray) -> np.ndarray:
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def splitmix_symmetric(seed: int, stream: int, rng: float, n: int) -> np.ndarray:
+    """n draws of SplitMix64 stream `stream` of `seed` mapped to U[-rng, rng] (rng.hpp:13-48)."""
+    with np.errstate(over="ignore"):
+        s0 = _mix(np.array([np.uint64(seed) + np.uint64(stream) * _GOLDEN], dtype=np.uint64))[0]
+        idx = np.arange(1, n + 1, dtype=np.uint64)
+        z = _mix(s0 + idx * _GOLDEN)
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0**-53
+    return ((2.0 * u - 1.0) * rng).astype(np.float32)
+
+
+def init_params(cfg: LadderConfig) -> list[LayerParams]:
+    cfg.validate()
+    gh = gate_count(cfg.kind) * cfg.hidden
+    rng = 1.0 / np.sqrt(float(cfg.hidden))
+    out = []
+    for l in range(cfg.layers):
+        w = splitmix_symmetric(cfg.seed, 2 * l, rng, gh * cfg.input_width(l))
+        r = splitmix_symmetric(cfg.seed, 2 * l + 1, rng, gh * cfg.hidden)
+        out.append(LayerParams(w.reshape((gh, cfg.input_width(l)), order="F"),
+                               r.reshape((gh, cfg.hidden), order="F"),
+                               np.zeros(gh, np.float32)))
+    return out
+
+
+def pretranspose(params: list[LayerParams]) -> None:
+    for p in params:
+        p.wt = np.asfortranarray(p.w.T)
+        p.rt = np.asfortranarray(p.r.T)
+        p.transposed = True
+
+
+def random_matrix(rows: int, cols: int, seed: int, stream: int) -> np.ndarray:
+    return splitmix_symmetric(seed, stream, 1.0, rows * cols).reshape((rows, cols), order="F")
+
+
+def make_input(cfg: LadderConfig) -> np.ndarray:
+    return random_matrix(cfg.input, cfg.batch * cfg.steps, cfg.seed, 1000)
+
+
+def make_dy(cfg: LadderConfig) -> np.ndarray:
+    return random_matrix(cfg.hidden, cfg.batch * cfg.steps, cfg.seed, 1001)
+
+
+def flop_count(kind: int, hidden: int, inp: int, batch: int) -> int:
+    return 2 * gate_count(kind) * hidden * (inp + hidden) * batch
+
+
+# ------------------------------------------------------------------ results
+class _LazySeq:
+    """Per-layer tape tensors materialised from the device on first access."""
+
+    def __init__(self, fetch, n):
+        self._fetch, self._n, self._cache = fetch, n, {}
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, l):
+        if l < 0:
+            l += self._n
+        if not 0 <= l < self._n:
+            raise IndexError(l)
+        if l not in self._cache:
+            self._cache[l] = self._fetch(l)
+        return self._cache[l]
+
+    def __iter__(self):
+        return (self[l] for l in range(self._n))
+
+
+@dataclass
+class ForwardTape:
+    cfg: LadderConfig
+    training: bool
+    _engine: "Engine | None" = None
+    _id: int = 0
+    _x0: np.ndarray | None = None
+
+    @property
+    def x0(self) -> np.ndarray:
+        return self._x0
+
+    def _seq(self, which, rows, cols):
+        eng, tid = self._engine, self._id
+
+        def fetch(l):
+            eng._require_current(tid)
+            out = fmat(rows, cols)
+            eng._check(eng._L.rw_get_tape(eng._ctx, which, l, _fp(out)))
+            return out
+        return _LazySeq(fetch, self.cfg.layers)
+
+    @property
+    def h_seq(self):
+        c = self.cfg
+        if "_h" not in self.__dict__:
+            self.__dict__["_h"] = self._seq(_lib.RW_TAPE_H, c.hidden, c.batch * (c.steps + 1))
+        return self.__dict__["_h"]
+
+    @property
+    def c_seq(self):
+        c = self.cfg
+        if "_c" not in self.__dict__:
+            self.__dict__["_c"] = self._seq(_lib.RW_TAPE_C, c.hidden, c.batch * (c.steps + 1))
+        return self.__dict__["_c"]
+
+    @property
+    def gates_seq(self):
+        c = self.cfg
+        if not self.training:
+            return []
+        if "_g" not in self.__dict__:
+            self.__dict__["_g"] = self._seq(_lib.RW_TAPE_GATES, 4 * c.hidden, c.batch * c.steps)
+        return self.__dict__["_g"]
+
+    @property
+    def tanh_c_seq(self):
+        c = self.cfg
+        if not self.training:
+            return []
+        if "_t" not in self.__dict__:
+            self.__dict__["_t"] = self._seq(_lib.RW_TAPE_TANH_C, c.hidden, c.batch * c.steps)
+        return self.__dict__["_t"]
+
+
+@dataclass
+class ForwardResult:
+    y: np.ndarray
+    tape: ForwardTape
+
+
+@dataclass
+class BackwardState:
+    dx0: np.ndarray
+    dh0: list
+    dc0: list
+    _engine: "Engine | None" = None
+    _id: int = 0
+
+    @property
+    def dgw_seq(self):
+        if "_dg" not in self.__dict__:
+            eng, tid, c = self._engine, self._id, self._engine.cfg
+
+            def fetch(l):
+                eng._require_current(tid)
+                out = fmat(4 * c.hidden, c.batch * c.steps)
+                eng._check(eng._L.rw_get_tape(eng._ctx, _lib.RW_TAPE_DGW, l, _fp(out)))
+                return out
+            self.__dict__["_dg"] = _LazySeq(fetch, c.layers)
+        return self.__dict__["_dg"]
+
+
+@dataclass
+class Gradients:
+    dw: list = field(default_factory=list)
+    dr: list = field(default_factory=list)
+    db: list = field(default_factory=list)
+    dx0: np.ndarray | None = None
+
+
+# ------------------------------------------------------------------ engine
+PRECISIONS = {"bf16": _lib.RW_PREC_BF16, "fp32": _lib.RW_PREC_FP32}
+SCHEDULES = {"auto": _lib.RW_SCHED_AUTO, "stepwise": _lib.RW_SCHED_STEPWISE,
+             "persistent": _lib.RW_SCHED_PERSISTENT}
+
+
+class Engine:
+    """rnnwave::Engine on one B200. precision: 'fp32' (3xTF32 parity mode, the default like
+    the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent'."""
+
+    def __init__(self, cfg: LadderConfig, precision: str = "fp32", schedule: str = "auto",
+                 device: int = 0):
+        self.cfg = LadderConfig(**cfg.__dict__)
+        self.cfg.validate()
+        if self.cfg.kind != CELL_LSTM:
+            raise ValueError(f"rnnwave_sm100: only CellKind::Lstm is implemented on the device, "
+                             f"got {CELL_NAMES.get(self.cfg.kind, '?')}")
+        self.precision = precision
+        self.schedule = schedule
+        self._L = _lib.load()
+        c = self.cfg
+        rc = _lib.rw_config(c.layers, c.hidden, c.input, c.batch, c.steps, c.kind, c.opt_level,
+                            c.batch_steps, c.workers, c.seed, PRECISIONS[precision],
+                            SCHEDULES[schedule])
+        h = C.c_void_p()
+        st = self._L.rw_create(C.byref(rc), device, C.byref(h))
+        if st != 0:
+            msg = self._L.rw_create_error().decode()
+            raise (ValueError if st == _lib.RW_EINVAL else RuntimeError)(msg)
+        self._ctx = h
+        self._tape_id = 0
+        self._bwd_id = 0
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx:
+            self._L.rw_destroy(ctx)
+            self._ctx = None
+
+    def close(self):
+        self.__del__()
+
+    def config(self) -> LadderConfig:
+        return self.cfg
+
+    def set_trace_sink(self, sink) -> None:  # engine.hpp:79 (trace recording: see DESIGN.md)
+        self._trace_sink = sink
+
+    # -- plumbing
+    def _check(self, status: int) -> None:
+        if status == 0:
+            return
+        msg = self._L.rw_last_error(self._ctx).decode()
+        raise (ValueError if status == _lib.RW_EINVAL else RuntimeError)(msg)
+
+    def _require_current(self, tid: int) -> None:
+        if tid != self._tape_id:
+            raise ValueError("engine: stale tape, the device no longer holds this tape")
+
+    def _check_params(self, params) -> None:
+        c = self.cfg
+        if len(params) != c.layers:
+            raise ValueError(f"engine: expected {c.layers} layer parameter sets, got {len(params)}")
+        gh = 4 * c.hidden
+        for l, p in enumerate(params):
+            if (p.w.shape != (gh, c.input_width(l)) or p.r.shape != (gh, c.hidden)
+                    or np.asarray(p.bias).size != gh):
+                raise ValueError(f"engine: layer {l} parameter shapes do not match the configuration")
+
+    def set_params(self, params) -> None:
+        self._check_params(params)
+        for l, p in enumerate(params):
+            w = as_matrix(p.w)
+            r = as_matrix(p.r)
+            b = np.ascontiguousarray(p.bias, dtype=np.float32)
+            self._check(self._L.rw_set_params(self._ctx, l, _fp(w), _fp(r), _fp(b)))
+
+    # -- reference API
+    def forward(self, params, x, training: bool, h0=None, c0=None) -> ForwardResult:
+        c = self.cfg
+        bt = c.batch * c.steps
+        x = as_matrix(x)
+        if x.shape != (c.input, bt):
+            raise ValueError(f"forward: x is {x.shape[0]}x{x.shape[1]}, expected {c.input}x{bt}")
+        self.set_params(params)
+        if c.opt_level >= 4:
+            pretranspose(params)
+        if h0 is not None and len(h0) != c.layers:
+            raise ValueError("forward: h0 must supply one matrix per layer")
+        hs = [as_matrix(m, c.hidden, c.batch) for m in h0] if h0 is not None else None
+        cs = [as_matrix(m, c.hidden, c.batch) for m in c0] if c0 is not None else None
+        arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
+        y = fmat(c.hidden, bt)
+        tid = C.c_uint64()
+        self._check(self._L.rw_forward(self._ctx, _fp(x), int(bool(training)), arr(hs), arr(cs),
+                                       _fp(y), C.byref(tid)))
+        self._tape_id = tid.value
+        tape = ForwardTape(LadderConfig(**c.__dict__), bool(training), self, tid.value, x.copy(order="F"))
+        return ForwardResult(y, tape)
+
+    def _check_tape(self, tape: ForwardTape) -> None:
+        if not tape.training:
+            raise ValueError("engine: tape was recorded without training mode")
+        t, c = tape.cfg, self.cfg
+        if (t.layers, t.hidden, t.input, t.batch, t.steps, t.kind) != (
+                c.layers, c.hidden, c.input, c.batch, c.steps, c.kind):
+            raise ValueError("engine: stale tape, network dimensions differ")
+        if tape._engine is not self or tape._id != self._tape_id:
+            raise ValueError("engine: stale tape, the device no longer holds this tape")
+
+    def backward_data(self, params, tape: ForwardTape, dy) -> BackwardState:
+        c = self.cfg
+        self._check_params(params)
+        self._check_tape(tape)
+        bt = c.batch * c.steps
+        dy = as_matrix(dy)
+        if dy.shape != (c.hidden, bt):
+            raise ValueError(f"backward_data: dy is {dy.shape[0]}x{dy.shape[1]}, expected {c.hidden}x{bt}")
+        if c.opt_level >= 4:
+            pretranspose(params)
+        dx0 = fmat(c.input, bt)
+        dh0 = [fmat(c.hidden, c.batch) for _ in range(c.layers)]
+        dc0 = [fmat(c.hidden, c.batch) for _ in range(c.layers)]
+        arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst])  # noqa: E731
+        self._check(self._L.rw_backward_data(self._ctx, tape._id, _fp(dy), _fp(dx0), arr(dh0), arr(dc0)))
+        self._bwd_id = tape._id
+        return BackwardState(dx0, dh0, dc0, self, tape._id)
+
+    def weight_update(self, tape: ForwardTape, state: BackwardState) -> Gradients:
+        c = self.cfg
+        self._check_tape(tape)
+        if state._id != tape._id or len(state.dh0) != c.layers:
+            raise ValueError("weight_update: backward state layer count mismatch")
+        gh = 4 * c.hidden
+        dw = [fmat(gh, c.input_width(l)) for l in range(c.layers)]
+        dr = [fmat(gh, c.hidden) for _ in range(c.layers)]
+        db = [np.zeros(gh, np.float32) for _ in range(c.layers)]
+        arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst])  # noqa: E731
+        self._check(self._L.rw_weight_update(self._ctx, tape._id, arr(dw), arr(dr), arr(db)))
+        return Gradients(dw, dr, db, state.dx0)
+
+    # -- device-resident timed path (bench)
+    def upload_inputs(self, x, dy=None) -> None:
+        x = as_matrix(x)
+        dy = as_matrix(dy) if dy is not None else None
+        self._check(self._L.rw_upload_inputs(self._ctx, _fp(x), _fp(dy)))
+
+    def run_pass(self, kind: int, stream: int | None = None) -> None:
+        self._check(self._L.rw_run_pass(self._ctx, kind, C.c_void_p(stream or 0)))
+
+    def sync(self) -> None:
+        self._check(self._L.rw_sync(self._ctx))
+
+    def set_profiling(self, on: bool) -> None:
+        self._check(self._L.rw_set_profiling(self._ctx, int(on)))
+
+    def phase_times(self, reset: bool = True):
+        ms = (C.c_double * 6)()
+        n = (C.c_int * 6)()
+        self._check(self._L.rw_phase_times(self._ctx, ms, n, 6, int(reset)))
+        names = ["repack", "fwd_recurrent", "bwd_recurrent", "weight_grad_gemm", "dx0_gemm", "db_reduce"]
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
+
+    def describe(self) -> dict:
+        a, b, k1, k2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        self._check(self._L.rw_describe(self._ctx, C.byref(a), C.byref(b), C.byref(k1), C.byref(k2)))
+        names = {1: "stepwise", 2: "persistent"}
+        return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
+                "fwd_ksplit": k1.value, "bwd_ksplit": k2.value}

@@ -1,0 +1,91 @@
+"""GPU parity: the sm_100a engine vs the reference CPU engine (oracle/_ref, else the C
+restatement) on identical SplitMix64 weights and inputs, through the reference-shaped API.
+Tolerances: tests/parity.py."""
+import numpy as np
+import pytest
+
+from parity import assert_within, compare, make_case, run_device, run_reference
+
+pytestmark = pytest.mark.gpu
+
+from oracle import Dims  # noqa: E402
+
+SMALL = [
+    Dims(1, 5, 7, 3, 4),      # odd sizes: every dimension padded
+    Dims(2, 64, 64, 16, 8),
+    Dims(3, 96, 40, 20, 10),  # H not a multiple of 64, B not of 16
+    Dims(2, 130, 70, 33, 5),  # two forward tiles with a ragged last one, 3 batch blocks
+]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("schedule", ["stepwise", "persistent"])
+@pytest.mark.parametrize("dims", SMALL, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
+def test_small_configs(reference, precision, schedule, dims):
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(dims, seed=7, bias=True, state=True)
+    eng = Engine(c, precision=precision, schedule=schedule)
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), precision)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_config_b_full(reference, precision):
+    """The headline configuration (4L h512 mb64 T100, BASELINE.json configs[1]) at full size."""
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(Dims(4, 512, 512, 64, 100), seed=42)
+    eng = Engine(c, precision=precision)
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    rows = compare(dev, ref, c)
+    worst = assert_within(rows, precision)
+    print(f"config B {precision} {eng.describe()}: worst {worst}")
+
+
+def test_deterministic_repeat():
+    """Run-to-run bitwise identity on the device (the analogue of acceptance crit 8)."""
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(Dims(2, 128, 96, 24, 12), seed=3, bias=True)
+    eng = Engine(c, precision="bf16", schedule="persistent")
+    a = run_device(eng, params, x, dy, h0, c0)
+    b = run_device(eng, params, x, dy, h0, c0)
+    for k in a:
+        va = a[k] if isinstance(a[k], list) else [a[k]]
+        vb = b[k] if isinstance(b[k], list) else [b[k]]
+        for p, q in zip(va, vb):
+            assert np.array_equal(p, q), k
+
+
+def test_error_messages():
+    """Malformed calls raise with the reference's message substrings (test_engine.cpp:220-256)."""
+    from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_input, make_dy
+    cfg = LadderConfig(layers=2, hidden=4, input=4, batch=2, steps=2, seed=1, opt_level=1)
+    params = init_params(cfg)
+    eng = Engine(cfg)
+    with pytest.raises(ValueError, match="expected"):
+        eng.forward(params, np.zeros((3, 4), np.float32, order="F"), False)
+    x = make_input(cfg)
+    inference = eng.forward(params, x, False)
+    dy = make_dy(cfg)
+    with pytest.raises(ValueError, match="training"):
+        eng.backward_data(params, inference.tape, dy)
+    trained = eng.forward(params, x, True)
+    other = LadderConfig(**{**cfg.__dict__, "hidden": 8})
+    eng2 = Engine(other)
+    with pytest.raises(ValueError, match="stale tape"):
+        eng2.backward_data(init_params(other), trained.tape, make_dy(other))
+
+
+def test_zero_params_zero_output():
+    """test_engine.cpp:15-39: zero W/R => y == 0 exactly."""
+    from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_input
+    cfg = LadderConfig(layers=2, hidden=6, input=5, batch=3, steps=4, seed=3, batch_steps=2)
+    params = init_params(cfg)
+    for p in params:
+        p.w[:] = 0
+        p.r[:] = 0
+    for prec in ("fp32", "bf16"):
+        y = Engine(cfg, precision=prec).forward(params, make_input(cfg), False).y
+        assert np.all(y == 0.0)
