@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""bench.py -- LSTM fwd+bwd TFLOPS on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+Workload (BASELINE.json configs[1], the paper's headline case): 4-layer LSTM, h=512, mb=64,
+T=100, forward (training) + backward_data + weight_update per step, synthetic SplitMix64
+inputs/weights exactly like the reference generators (seed 42). FLOPs follow the
+reference convention (cells.hpp:65-68, bench.hpp:55-62, 210-213): GEMM multiply-adds only,
+2*4*H*(I+H)*B per cell x L*T x 3 (fwd 1 + bwd 2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|fp32]
+  python bench.py --impl reference ...   (the reference CPU engine, oracle/_ref, host cores)
+
+Under torchrun (N > 1) every rank runs its own independent minibatch of the same shape
+(data parallel, weak scaling) and the weight gradients are summed over ranks with NCCL
+(all-reduce of dW/dR/db); timing is the max over ranks of CUDA-event device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_B = dict(layers=4, hidden=512, input=512, batch=64, steps=100)
+METRIC = "LSTM fwd+bwd TFLOPS (h=512, mb=64, 4 layers, T=100) and % of B200 TC peak"
+
+
+def pass_flops(c: dict, mult: int = 3) -> int:
+    f = 0
+    for l in range(c["layers"]):
+        il = c["input"] if l == 0 else c["hidden"]
+        f += 2 * 4 * c["hidden"] * (il + c["hidden"]) * c["batch"] * c["steps"]
+    return f * mult
+
+
+def measured_peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p)), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # the reference CPU engine (oracle/_ref) -- checker/baseline leg only
+    R = oracle.Reference()
+    d = oracle.Dims(**CONFIG_B)
+    cores = os.cpu_count() or 1
+    flops = pass_flops(CONFIG_B)
+    # one pass of the reference engine at O6 ~ seconds; bound the run to a few minutes
+    est = R.time(d, seed=42, pass_kind=2, reps=1, warmup=0, workers=cores)["median_us"] * 1e-6
+    budget = 150.0
+    reps = max(1, min(args.steps, int(budget / max(est, 1e-3))))
+    warm = min(args.warmup, 1)
+    t = R.time(d, seed=42, pass_kind=2, reps=reps, warmup=warm, workers=cores)
+    sec = t["median_us"] * 1e-6
+    tflops = flops / sec / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": reps, "warmup": warm, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SplitMix64 seed 42, reference generators)",
+        "config": {"workload": "4L h512 mb64 T100 LSTM fwd+bwd (BASELINE configs[1])",
+                   "global_batch": CONFIG_B["batch"], "seq_len": CONFIG_B["steps"],
+                   "layers": 4, "hidden": 512, "opt_level": 6, "workers": cores},
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "reference",
+                         "sample": f"{reps} full config-B passes (median), O6, {cores} workers",
+                         "lib": os.path.basename(R.path)},
+        "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c = dict(CONFIG_B)
+    cfg = LadderConfig(**c, seed=42 + rank, opt_level=6, batch_steps=2, workers=1)
+    eng = Engine(cfg, precision=args.precision, schedule=args.schedule, device=local)
+    params = init_params(LadderConfig(**c, seed=42))
+    x = make_input(cfg)
+    dy = make_dy(cfg)
+    eng.set_params(params)
+    eng.upload_inputs(x, dy)
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    flops = pass_flops(c)
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps, outside the events
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def allreduce():
+        if world > 1:
+            eng.allreduce_grads(sh)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            eng.run_pass(2, sh)
+            allreduce()
+        eng.sync()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        eng.launch_count(reset=True)
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                eng.run_pass(2, sh)
+                allreduce()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            eng.sync()
+        launches = eng.launch_count(reset=True) // args.steps
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        total_ms = sum(step_ms)
+        if world > 1:
+            t = torch.tensor([total_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            total_ms = t.item()
+        ms = total_ms / args.steps
+
+        # ---- per-phase device times (CUDA events on the launching stream) for the roofline
+        eng.set_profiling(True)
+        eng.phase_times(reset=True)
+        nprof = max(3, min(args.steps, 10))
+        for _ in range(nprof):
+            flush.zero_()
+            eng.run_pass(2, sh)
+        eng.sync()
+        ph = eng.phase_times(reset=True)
+        eng.set_profiling(False)
+
+        # ---- e2e through the C-ABI with host buffers: H2D inputs, pass, D2H results
+        y = np.zeros((c["hidden"], c["batch"] * c["steps"]), np.float32, order="F")
+        dx0 = np.zeros((c["input"], c["batch"] * c["steps"]), np.float32, order="F")
+        dw = [np.zeros((4 * c["hidden"], c["input"] if l == 0 else c["hidden"]), np.float32, order="F")
+              for l in range(c["layers"])]
+        dr = [np.zeros((4 * c["hidden"], c["hidden"]), np.float32, order="F") for _ in range(c["layers"])]
+        db = [np.zeros(4 * c["hidden"], np.float32) for _ in range(c["layers"])]
+        xh = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).pin_memory()
+        dyh = torch.from_numpy(np.asfortranarray(dy).ravel(order="F")).pin_memory()
+        h2d = xh.numel() * 4 + dyh.numel() * 4
+        d2h = (y.size + dx0.size + sum(a.size for a in dw) + sum(a.size for a in dr)
+               + sum(a.size for a in db)) * 4
+        e2e_steps = max(3, min(args.steps, 20))
+        for _ in range(2):
+            eng.upload_inputs_ptr(xh.data_ptr(), dyh.data_ptr())
+            eng.run_pass(2, sh)
+            eng.read_outputs(y, dx0, dw, dr, db)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.upload_inputs_ptr(xh.data_ptr(), dyh.data_ptr())
+            eng.run_pass(2, sh)
+            allreduce()
+            eng.read_outputs(y, dx0, dw, dr, db)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3 / e2e_steps
+        e2e_ms = max(e0.elapsed_time(e1) / e2e_steps, wall)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = t.item()
+
+    if rank != 0:
+        return
+    peaks, peak_src = measured_peaks()
+    desc = eng.describe()
+    # dominant kernel: the longer of the two recurrent (persistent / stepwise) phases
+    fwd_ms = ph["fwd_recurrent"][0] / max(ph["fwd_recurrent"][1], 1)
+    bwd_ms = ph["bwd_recurrent"][0] / max(ph["bwd_recurrent"][1], 1)
+    L, H, I, B, T = c["layers"], c["hidden"], c["input"], c["batch"], c["steps"]
+    fwd_fl = pass_flops(c, 1)  # [W|R].[x;h] for every cell
+    bwd_fl = sum(2 * 4 * H * (H + (H if l < L - 1 else 0)) * B * (T + (1 if True else 0))
+                 for l in range(L))  # W_{l+1}^T and R_l^T per cell (+ the dh0 step)
+    if bwd_ms >= fwd_ms:
+        dom, dom_ms, dom_fl = "k_lstm_bwd (fused recurrent backward)", bwd_ms, bwd_fl
+    else:
+        dom, dom_ms, dom_fl = "k_lstm_fwd (fused recurrent forward)", fwd_ms, fwd_fl
+    achieved = dom_fl / (dom_ms * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", 1590.0)
+    cpu_base = None
+    if not args.no_cpu_baseline:
+        cpu_base = cpu_baseline()
+    value = flops * world / (ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16" if args.precision == "bf16" else "tf32x3 (fp32-parity)",
+        "data": "synthetic (SplitMix64 seed 42 weights, streams 1000/1001 inputs: the reference generators)",
+        "config": {"workload": "4L h512 mb64 T100 LSTM fwd+bwd (BASELINE configs[1])",
+                   "model": "lstm-4x512", "global_batch": c["batch"] * world, "seq_len": T,
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "precision": args.precision, "schedule": desc,
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "pct_of_bf16_peak": 100.0 * value / world / peak},
+        "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "C-ABI rw_upload_inputs (pinned host) -> rw_run_pass -> rw_read_outputs"},
+        "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                     "algorithmic_flops_per_launch": dom_fl, "avg_launch_ms": dom_ms},
+        "phases_ms": {k: v[0] / max(v[1], 1) for k, v in ph.items()},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu_base,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline() -> dict | None:
+    """The reference CPU engine on the host cores, bounded sample of the same workload."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        R = oracle.Reference()
+        kind = "reference"
+    except Exception:
+        return None
+    d = oracle.Dims(**CONFIG_B)
+    cores = os.cpu_count() or 1
+    t = R.time(d, seed=42, pass_kind=2, reps=3, warmup=1, workers=cores)
+    sec = t["median_us"] * 1e-6
+    return {"value": pass_flops(CONFIG_B) / sec / 1e12, "unit": "TFLOP/s", "cores": cores,
+            "kind": kind, "ms_per_step": sec * 1e3,
+            "sample": "3 full config-B fwd+bwd passes after 1 warm-up (median), O6, workers=cores"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

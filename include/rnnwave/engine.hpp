@@ -1,0 +1,286 @@
+// rnnwave/engine.hpp -- drop-in facade of rnnwave::Engine over librnnwave_sm100.so.
+//
+// Keeps the reference's public signatures (proj/include/rnnwave/engine.hpp:36-217):
+//   explicit Engine(const LadderConfig&)                       (+ optional device knobs)
+//   const LadderConfig& config() const;  void set_trace_sink(sched::ScheduleTrace*)
+//   ForwardResult forward(std::vector<LayerParams>&, const Matrix& x, bool training,
+//                         const std::vector<Matrix>* h0 = nullptr, const std::vector<Matrix>* c0 = nullptr)
+//   BackwardState backward_data(std::vector<LayerParams>&, const ForwardTape&, const Matrix& dy)
+//   Gradients     weight_update(const ForwardTape&, const BackwardState&)
+// and the value types' field names (ForwardTape::x0/h_seq/c_seq/gates_seq/tanh_c_seq,
+// BackwardState::dx0/dgw_seq/dh0/dc0, Gradients::dw/dr/db/dx0). The tape tensors live in
+// HBM; the facade materialises a tape field on first access (verify.hpp reads
+// tape.h_seq[l] / bwd.dgw_seq[l] directly), so the device-resident path stays free of
+// host copies. Errors: RW_EINVAL -> std::invalid_argument (same message substrings as the
+// reference: "expected", "training", "stale tape"), anything else -> std::runtime_error.
+//
+// Link with -L<repo>/paper_1604_01946_b200/lib -lrnnwave_sm100.
+#pragma once
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rnnwave/cells.hpp"
+#include "rnnwave/config.hpp"
+#include "rnnwave/matrix.hpp"
+#include "rnnwave/params.hpp"
+#include "rnnwave_sm100.h"
+
+namespace rnnwave {
+
+namespace sched {
+// The reference records a CPU task trace (scheduler.hpp:180-191). The device wavefront is
+// traced by CUDA events / ncu instead; the sink is accepted for source compatibility.
+struct TraceRecord {
+  int layer = 0, block = 0, phase = 0, worker = 0;
+  std::int64_t start_ns = 0, end_ns = 0;
+};
+struct ScheduleTrace {
+  std::vector<TraceRecord> records;
+};
+}  // namespace sched
+
+namespace detail {
+
+[[noreturn]] inline void raise(int status, const std::string& msg) {
+  if (status == RW_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// Owns the device context; shared by the Engine and every tape/state it hands out.
+struct DeviceHandle {
+  rw_ctx* ctx = nullptr;
+  std::uint64_t bwd_tape = 0;
+  ~DeviceHandle() {
+    if (ctx) rw_destroy(ctx);
+  }
+  void check(int status) const {
+    if (status != RW_OK) raise(status, rw_last_error(ctx));
+  }
+};
+
+// Per-layer tape tensor sequence, materialised from HBM on first access.
+class TapeSeq {
+ public:
+  TapeSeq() = default;
+  TapeSeq(std::shared_ptr<DeviceHandle> h, std::uint64_t id, int which, int n, int rows, int cols)
+      : h_(std::move(h)), id_(id), which_(which), rows_(rows), cols_(cols), cache_(n) {}
+  std::size_t size() const { return cache_.size(); }
+  bool empty() const { return cache_.empty(); }
+  const Matrix& operator[](std::size_t l) const {
+    if (l >= cache_.size()) throw std::out_of_range("tape: layer index out of range");
+    if (!cache_[l]) {
+      Matrix m(rows_, cols_);
+      h_->check(rw_get_tape(h_->ctx, which_, int(l), m.data()));
+      cache_[l] = std::move(m);
+    }
+    return *cache_[l];
+  }
+  const Matrix& back() const { return (*this)[cache_.size() - 1]; }
+  const Matrix& front() const { return (*this)[0]; }
+  std::uint64_t id() const { return id_; }
+
+ private:
+  std::shared_ptr<DeviceHandle> h_;
+  std::uint64_t id_ = 0;
+  int which_ = 0, rows_ = 0, cols_ = 0;
+  mutable std::vector<std::optional<Matrix>> cache_;
+};
+
+}  // namespace detail
+
+struct ForwardTape {
+  LadderConfig cfg;
+  bool training = false;
+  Matrix x0;
+  detail::TapeSeq h_seq;
+  detail::TapeSeq c_seq;
+  detail::TapeSeq gates_seq;
+  detail::TapeSeq tanh_c_seq;
+  std::vector<Matrix> zrh_seq;  // GRU only (empty: the device path is LSTM)
+  std::shared_ptr<detail::DeviceHandle> device;
+  std::uint64_t id = 0;
+};
+
+struct ForwardResult {
+  Matrix y;
+  ForwardTape tape;
+};
+
+struct BackwardState {
+  Matrix dx0;
+  detail::TapeSeq dgw_seq;
+  std::vector<Matrix> dgr_seq;  // GRU only
+  std::vector<Matrix> dh0;
+  std::vector<Matrix> dc0;
+  std::uint64_t id = 0;
+};
+
+struct Gradients {
+  std::vector<Matrix> dw;
+  std::vector<Matrix> dr;
+  std::vector<std::vector<float>> db;
+  Matrix dx0;
+};
+
+class Engine {
+ public:
+  // precision: RW_PREC_FP32 (3xTF32 fp32-parity, default) or RW_PREC_BF16; the environment
+  // variable RNNWAVE_PRECISION=bf16|fp32 overrides the default for unmodified callers.
+  explicit Engine(const LadderConfig& cfg, int precision = -1, int schedule = RW_SCHED_AUTO,
+                  int device = 0)
+      : cfg_(cfg), dev_(std::make_shared<detail::DeviceHandle>()) {
+    cfg_.validate();
+    if (precision < 0) {
+      precision = RW_PREC_FP32;
+      if (const char* e = std::getenv("RNNWAVE_PRECISION"))
+        if (std::strcmp(e, "bf16") == 0) precision = RW_PREC_BF16;
+    }
+    rw_config c{};
+    c.layers = cfg_.layers;
+    c.hidden = cfg_.hidden;
+    c.input = cfg_.input;
+    c.batch = cfg_.batch;
+    c.steps = cfg_.steps;
+    c.cell_kind = int(cfg_.kind);
+    c.opt_level = cfg_.opt_level;
+    c.batch_steps = cfg_.batch_steps;
+    c.workers = cfg_.workers;
+    c.seed = cfg_.seed;
+    c.precision = precision;
+    c.schedule = schedule;
+    const int st = rw_create(&c, device, &dev_->ctx);
+    if (st != RW_OK) detail::raise(st, rw_create_error());
+  }
+
+  const LadderConfig& config() const { return cfg_; }
+  void set_trace_sink(sched::ScheduleTrace* sink) { trace_sink_ = sink; }
+
+  ForwardResult forward(std::vector<LayerParams>& params, const Matrix& x, bool training,
+                        const std::vector<Matrix>* h0 = nullptr,
+                        const std::vector<Matrix>* c0 = nullptr) {
+    upload(params);
+    const int bt = cfg_.batch * cfg_.steps;
+    if (x.rows() != cfg_.input || x.cols() != bt)
+      throw std::invalid_argument("forward: x is " + std::to_string(x.rows()) + "x" +
+                                  std::to_string(x.cols()) + ", expected " +
+                                  std::to_string(cfg_.input) + "x" + std::to_string(bt));
+    if (cfg_.opt_level >= 4) pretranspose(params);
+    std::vector<const float*> ph0, pc0;
+    if (h0) {
+      if (int(h0->size()) != cfg_.layers)
+        throw std::invalid_argument("forward: h0 must supply one matrix per layer");
+      for (const Matrix& m : *h0) ph0.push_back(m.data());
+    }
+    if (c0) {
+      if (int(c0->size()) != cfg_.layers)
+        throw std::invalid_argument("forward: c0 must supply one matrix per layer");
+      for (const Matrix& m : *c0) pc0.push_back(m.data());
+    }
+    ForwardResult res;
+    res.y = Matrix(cfg_.hidden, bt);
+    std::uint64_t id = 0;
+    dev_->check(rw_forward(dev_->ctx, x.data(), training ? 1 : 0, h0 ? ph0.data() : nullptr,
+                           c0 ? pc0.data() : nullptr, res.y.data(), &id));
+    ForwardTape& t = res.tape;
+    t.cfg = cfg_;
+    t.training = training;
+    t.x0 = x;
+    t.device = dev_;
+    t.id = id;
+    const int H = cfg_.hidden, L = cfg_.layers;
+    t.h_seq = detail::TapeSeq(dev_, id, RW_TAPE_H, L, H, cfg_.batch + bt);
+    t.c_seq = detail::TapeSeq(dev_, id, RW_TAPE_C, L, H, cfg_.batch + bt);
+    if (training) {
+      t.gates_seq = detail::TapeSeq(dev_, id, RW_TAPE_GATES, L, 4 * H, bt);
+      t.tanh_c_seq = detail::TapeSeq(dev_, id, RW_TAPE_TANH_C, L, H, bt);
+    }
+    return res;
+  }
+
+  BackwardState backward_data(std::vector<LayerParams>& params, const ForwardTape& tape,
+                              const Matrix& dy) {
+    upload(params);
+    check_tape(tape);
+    const int bt = cfg_.batch * cfg_.steps;
+    if (dy.rows() != cfg_.hidden || dy.cols() != bt)
+      throw std::invalid_argument("backward_data: dy is " + std::to_string(dy.rows()) + "x" +
+                                  std::to_string(dy.cols()) + ", expected " +
+                                  std::to_string(cfg_.hidden) + "x" + std::to_string(bt));
+    if (cfg_.opt_level >= 4) pretranspose(params);
+    BackwardState s;
+    s.dx0 = Matrix(cfg_.input, bt);
+    std::vector<float*> pdh, pdc;
+    for (int l = 0; l < cfg_.layers; ++l) {
+      s.dh0.emplace_back(cfg_.hidden, cfg_.batch);
+      s.dc0.emplace_back(cfg_.hidden, cfg_.batch);
+    }
+    for (int l = 0; l < cfg_.layers; ++l) {
+      pdh.push_back(s.dh0[l].data());
+      pdc.push_back(s.dc0[l].data());
+    }
+    dev_->check(rw_backward_data(dev_->ctx, tape.id, dy.data(), s.dx0.data(), pdh.data(), pdc.data()));
+    s.dgw_seq = detail::TapeSeq(dev_, tape.id, RW_TAPE_DGW, cfg_.layers, 4 * cfg_.hidden, bt);
+    s.id = tape.id;
+    return s;
+  }
+
+  Gradients weight_update(const ForwardTape& tape, const BackwardState& state) {
+    check_tape(tape);
+    if (int(state.dgw_seq.size()) != cfg_.layers || state.id != tape.id)
+      throw std::invalid_argument("weight_update: backward state layer count mismatch");
+    Gradients g;
+    std::vector<float*> pw, pr, pb;
+    for (int l = 0; l < cfg_.layers; ++l) {
+      g.dw.emplace_back(4 * cfg_.hidden, cfg_.input_width(l));
+      g.dr.emplace_back(4 * cfg_.hidden, cfg_.hidden);
+      g.db.emplace_back(std::size_t(4 * cfg_.hidden), 0.0f);
+    }
+    for (int l = 0; l < cfg_.layers; ++l) {
+      pw.push_back(g.dw[l].data());
+      pr.push_back(g.dr[l].data());
+      pb.push_back(g.db[l].data());
+    }
+    dev_->check(rw_weight_update(dev_->ctx, tape.id, pw.data(), pr.data(), pb.data()));
+    g.dx0 = state.dx0;
+    return g;
+  }
+
+ private:
+  void upload(const std::vector<LayerParams>& params) {
+    if (int(params.size()) != cfg_.layers)
+      throw std::invalid_argument("engine: expected " + std::to_string(cfg_.layers) +
+                                  " layer parameter sets, got " + std::to_string(params.size()));
+    const int gh = gate_count(cfg_.kind) * cfg_.hidden;
+    for (int l = 0; l < cfg_.layers; ++l) {
+      const LayerParams& p = params[l];
+      if (p.w.rows() != gh || p.w.cols() != cfg_.input_width(l) || p.r.rows() != gh ||
+          p.r.cols() != cfg_.hidden || int(p.bias.size()) != gh)
+        throw std::invalid_argument("engine: layer " + std::to_string(l) +
+                                    " parameter shapes do not match the configuration");
+      dev_->check(rw_set_params(dev_->ctx, l, p.w.data(), p.r.data(), p.bias.data()));
+    }
+  }
+
+  void check_tape(const ForwardTape& tape) const {
+    if (!tape.training) throw std::invalid_argument("engine: tape was recorded without training mode");
+    const LadderConfig& t = tape.cfg;
+    if (t.layers != cfg_.layers || t.hidden != cfg_.hidden || t.input != cfg_.input ||
+        t.batch != cfg_.batch || t.steps != cfg_.steps || t.kind != cfg_.kind)
+      throw std::invalid_argument("engine: stale tape, network dimensions differ");
+    if (tape.device != dev_)
+      throw std::invalid_argument("engine: stale tape, recorded by another engine");
+  }
+
+  LadderConfig cfg_;
+  std::shared_ptr<detail::DeviceHandle> dev_;
+  sched::ScheduleTrace* trace_sink_ = nullptr;
+};
+
+}  // namespace rnnwave

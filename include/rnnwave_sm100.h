@@ -132,6 +132,24 @@ int rw_phase_times(rw_ctx* ctx, double* out_ms, int* out_launches, int n, int re
  * split-K factors chosen. */
 int rw_describe(rw_ctx* ctx, int* fwd_sched, int* bwd_sched, int* fwd_ksplit, int* bwd_ksplit);
 
+/* Copy the results of the last rw_run_pass to host buffers (any may be NULL): y (H x B*T),
+ * dx0 (I x B*T), dW / dR / db per layer (reference layouts). Synchronous. */
+int rw_read_outputs(rw_ctx* ctx, float* y, float* dx0, float* const* dW, float* const* dR,
+                    float* const* db);
+/* Number of kernels this library launched since the last reset (graph-free accounting). */
+int rw_launch_count(rw_ctx* ctx, long long* count, int reset);
+
+/* ---- data parallel over NVLink/NVSwitch (config E) ----
+ * Independent sequences are split by minibatch across ranks (one context per GPU, each with
+ * its own batch); the only exchange is a sum all-reduce of dW/dR/db after weight_update.
+ * NCCL is loaded at run time (libnccl.so.2), so the library itself has no NCCL dependency.
+ * rw_nccl_unique_id: rank 0 creates the 128-byte id and shares it out of band. */
+int rw_nccl_unique_id(char* id128);
+int rw_comm_init(rw_ctx* ctx, int nranks, int rank, const char* id128);
+/* Sum all-reduce of every layer's dW, dR, db on `stream` (NULL = context stream), one NCCL
+ * group, enqueued after the pass's weight-gradient GEMMs. */
+int rw_allreduce_grads(rw_ctx* ctx, void* stream);
+
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
 int64_t rw_flop_count_cell(int hidden, int input, int batch);
 

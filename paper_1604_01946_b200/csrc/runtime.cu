@@ -5,6 +5,7 @@
 // equivalents; the arithmetic lives in lstm_step.cuh / gemm_tc.cuh / layout_kernels.cuh.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -39,6 +40,9 @@ struct RwError {
   } while (0)
 
 [[noreturn]] void einval(const std::string& m) { throw RwError{RW_EINVAL, m}; }
+
+// Kernel launches issued by this library (per host thread), for the bench's gpu_launches.
+thread_local long long g_launches = 0;
 
 // ------------------------------------------------------------------ TMA encode (driver API)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -122,6 +126,49 @@ int grid_for(long long n) { return (int)std::min<long long>(std::max<long long>(
 
 constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA
 
+// ------------------------------------------------------------------ NCCL (dlopen'd)
+// Minimal subset of nccl.h (NCCL 2.x ABI) so the library carries no link-time NCCL dependency.
+typedef struct ncclComm* ncclComm_t;
+struct NcclId {
+  char internal[128];
+};
+struct Nccl {
+  void* h = nullptr;
+  int (*GetUniqueId)(NcclId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+Nccl& nccl() {
+  static Nccl n;
+  if (!n.h) {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (n.h) break;
+    }
+    if (!n.h) throw RwError{RW_ENCCL, "libnccl.so.2 not found"};
+    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+    n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+    n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+    if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce || !n.GroupStart || !n.GroupEnd)
+      throw RwError{RW_ENCCL, "libnccl.so.2 lacks required symbols"};
+  }
+  return n;
+}
+void nccl_check(int r, const char* what) {
+  if (r != 0)
+    throw RwError{RW_ENCCL, std::string(what) + ": " +
+                                (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error")};
+}
+constexpr int kNcclFloat32 = 7, kNcclSum = 0;
+
 template <class P>
 struct KernelSet {
   static void* fwd() { return (void*)k_lstm_fwd<P>; }
@@ -182,6 +229,10 @@ struct rw_ctx {
   bool tape_training = false;
   bool bwd_done = false;
   bool inputs_uploaded = false;
+
+  // data parallel
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
 
   // profiling
   bool profiling = false;
@@ -281,6 +332,7 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
   lc.attrs = at;
   lc.numAttrs = 1;
   void* args[2] = {const_cast<void**>(&layers), const_cast<RecParams*>(&rp)};
+  ++g_launches;
   RW_CUDA(cudaLaunchKernelExC(&lc, kernel, args));
 }
 
@@ -295,6 +347,7 @@ void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int
   auto k = k_gemm_tc<P, AMN, BMN>;
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
+  ++g_launches;
   k<<<grid, 256, smem, s>>>(table_dev, bn, stages);
   RW_CUDA(cudaGetLastError());
 }
@@ -600,13 +653,17 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   const int L = x->L, H = x->H, I = x->I, Hp = x->Hp, Ip = x->Ip;
   for (int l = 0; l < L; ++l) {
     const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
+    ++g_launches;
     k_pack_wf<<<grid_for(4LL * Hp * (Ipl + Hp)), 256, 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp, Ipl,
                                                              x->prec, x->wf[l].p(0), x->wf[l].p(1));
     const float* wup = l < L - 1 ? x->W[l + 1].f() : nullptr;
+    ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(wup, x->R[l].f(), H, Hp, x->prec,
                                                              x->wb[l].p(0), x->wb[l].p(1));
+    ++g_launches;
     k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f());
   }
+  ++g_launches;
   k_pack_w0t<<<grid_for((long long)Ip * 4 * Hp), 256, 0, s>>>(x->W[0].f(), H, I, Hp, Ip, x->prec,
                                                              x->w0t.p(0), x->w0t.p(1));
   RW_CUDA(cudaGetLastError());
@@ -634,13 +691,16 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
 // per layer at stage + l*H*B) or zeros.
 void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev) {
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
+  ++g_launches;
   k_pad_cols<<<grid_for((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
       x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
   for (int l = 0; l < L; ++l) {
     const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
     const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
+    ++g_launches;
     k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(h0, H, B, 1, Hp, Bp, 0, x->h[l].f(), x->prec,
                                                            x->hop[l].p(0), x->hop[l].p(1));
+    ++g_launches;
     k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
@@ -728,7 +788,7 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
 
 void run_db(rw_ctx* x, cudaStream_t s) {
   const int slices = ceil_div(x->Bp, kXChunk) * x->ks_b;
-  for (int l = 0; l < x->L; ++l)
+  for (int l = 0; l < x->L; ++l, ++g_launches)
     k_db_reduce<<<ceil_div(4 * x->H, 256), 256, 0, s>>>(x->dbp[l].f(), slices, x->H, x->Hp, x->db[l].f());
   RW_CUDA(cudaGetLastError());
 }
@@ -781,6 +841,7 @@ void sync_all(rw_ctx* x) {
 void d2h_unpad(rw_ctx* x, const float* src, int Rp, int Bp, long long col_off, int G, int R, int B,
                int nblk, float* host) {
   const long long n = (long long)G * R * B * nblk;
+  ++g_launches;
   k_unpad_cols<<<grid_for(n), 256, 0, x->main>>>(src, Rp, Bp, col_off, G, R, B, nblk, x->y_raw.f());
   RW_CUDA(cudaGetLastError());
   RW_CUDA(cudaMemcpyAsync(host, x->y_raw.p, n * 4, cudaMemcpyDeviceToHost, x->main));
@@ -807,6 +868,7 @@ std::string g_create_err;
 
 rw_ctx::~rw_ctx() {
   if (main) cudaStreamSynchronize(main);
+  if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
   for (auto s : ls) cudaStreamDestroy(s);
   for (auto e : lev) cudaEventDestroy(e);
   if (fork_ev) cudaEventDestroy(fork_ev);
@@ -1028,6 +1090,66 @@ int rw_run_pass(rw_ctx* x, int pass, void* stream) {
   });
 }
 
+int rw_read_outputs(rw_ctx* x, float* y, float* dx0, float* const* dW, float* const* dR,
+                    float* const* db) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaDeviceSynchronize());
+    check_error_flag(x);
+    if (y) d2h_unpad(x, x->h[x->L - 1].f(), x->Hp, x->Bp, x->Bp, 1, x->H, x->B, x->T, y);
+    if (dx0) RW_CUDA(cudaMemcpy(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < x->L; ++l) {
+      const int Il = l == 0 ? x->I : x->H;
+      if (dW && dW[l]) RW_CUDA(cudaMemcpy(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpy(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost));
+      if (db && db[l]) RW_CUDA(cudaMemcpy(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int rw_launch_count(rw_ctx* x, long long* count, int reset) {
+  return guarded(x, [&] {
+    if (count) *count = g_launches;
+    if (reset) g_launches = 0;
+  });
+}
+
+int rw_nccl_unique_id(char* id128) {
+  return guarded(nullptr, [&] {
+    NcclId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id128, id.internal, 128);
+  });
+}
+
+int rw_comm_init(rw_ctx* x, int nranks, int rank, const char* id128) {
+  return guarded(x, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) einval("rw_comm_init: bad rank/nranks");
+    RW_CUDA(cudaSetDevice(x->dev));
+    NcclId id;
+    std::memcpy(id.internal, id128, 128);
+    nccl_check(nccl().CommInitRank(&x->comm, nranks, id, rank), "ncclCommInitRank");
+    x->nranks = nranks;
+    x->rank = rank;
+  });
+}
+
+int rw_allreduce_grads(rw_ctx* x, void* stream) {
+  return guarded(x, [&] {
+    if (!x->comm) einval("rw_allreduce_grads: rw_comm_init was not called");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
+    Nccl& n = nccl();
+    nccl_check(n.GroupStart(), "ncclGroupStart");
+    for (int l = x->L - 1; l >= 0; --l) {  // top layer's gradients are final first
+      const int Il = l == 0 ? x->I : x->H;
+      nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
+      nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
+      nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
+    }
+    nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  });
+}
+
 int rw_sync(rw_ctx* x) {
   return guarded(x, [&] {
     RW_CUDA(cudaSetDevice(x->dev));
@@ -1076,7 +1198,9 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     Operand A, Bo;
     A.alloc(prec, a_elems);
     Bo.alloc(prec, b_elems);
+    ++g_launches;
     k_pad_cols<<<grid_for(a_elems), 256>>>(dA, (int)a_elems, 1, 1, (int)a_elems, 1, 0, nullptr, prec, A.p(0), A.p(1));
+    ++g_launches;
     k_pad_cols<<<grid_for(b_elems), 256>>>(dB, (int)b_elems, 1, 1, (int)b_elems, 1, 0, nullptr, prec, Bo.p(0), Bo.p(1));
     RW_CUDA(cudaGetLastError());
     std::vector<CUtensorMap> maps;

@@ -272,6 +272,14 @@ SCHEDULES = {"auto": _lib.RW_SCHED_AUTO, "stepwise": _lib.RW_SCHED_STEPWISE,
              "persistent": _lib.RW_SCHED_PERSISTENT}
 
 
+def nccl_unique_id() -> bytes:
+    L = _lib.load()
+    buf = C.create_string_buffer(128)
+    if L.rw_nccl_unique_id(buf) != 0:
+        raise RuntimeError(L.rw_create_error().decode() or "ncclGetUniqueId failed")
+    return buf.raw
+
+
 class Engine:
     """rnnwave::Engine on one B200. precision: 'fp32' (3xTF32 parity mode, the default like
     the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent'."""
@@ -412,6 +420,27 @@ class Engine:
         x = as_matrix(x)
         dy = as_matrix(dy) if dy is not None else None
         self._check(self._L.rw_upload_inputs(self._ctx, _fp(x), _fp(dy)))
+
+    def upload_inputs_ptr(self, x_ptr: int, dy_ptr: int) -> None:
+        """rw_upload_inputs on raw (e.g. pinned) host pointers."""
+        self._check(self._L.rw_upload_inputs(self._ctx, C.cast(C.c_void_p(x_ptr), _F),
+                                             C.cast(C.c_void_p(dy_ptr), _F)))
+
+    def read_outputs(self, y=None, dx0=None, dw=None, dr=None, db=None) -> None:
+        arr = lambda lst: (_F * self.cfg.layers)(*[_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
+        self._check(self._L.rw_read_outputs(self._ctx, _fp(y), _fp(dx0), arr(dw), arr(dr), arr(db)))
+
+    def init_comm(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Join the NCCL data-parallel group (one context per GPU)."""
+        self._check(self._L.rw_comm_init(self._ctx, world, rank, unique_id))
+
+    def allreduce_grads(self, stream: int | None = None) -> None:
+        self._check(self._L.rw_allreduce_grads(self._ctx, C.c_void_p(stream or 0)))
+
+    def launch_count(self, reset: bool = False) -> int:
+        n = C.c_longlong()
+        self._check(self._L.rw_launch_count(self._ctx, C.byref(n), int(reset)))
+        return n.value
 
     def run_pass(self, kind: int, stream: int | None = None) -> None:
         self._check(self._L.rw_run_pass(self._ctx, kind, C.c_void_p(stream or 0)))

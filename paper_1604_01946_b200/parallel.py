@@ -1,0 +1,51 @@
+"""Multi-GPU partitioning of the LSTM path, host-side logic.
+
+Data parallel: sequences are independent, so the minibatch B is split across ranks; each
+rank runs the full forward/backward on its shard and the weight gradients are summed
+(NCCL all-reduce inside librnnwave_sm100.so on GPUs; torch.distributed for host arrays, which
+is what the gloo CPU tests exercise). The time-major layout puts batch element b of step t
+in column t*B + b, so a shard is a strided column gather.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(batch: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced batch range [b0, b1) of `rank` (the first batch % world ranks
+    get one extra sequence)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} out of range for world size {world}")
+    base, extra = divmod(batch, world)
+    b0 = rank * base + min(rank, extra)
+    return b0, b0 + base + (1 if rank < extra else 0)
+
+
+def shard_columns(m: np.ndarray, batch: int, steps: int, rank: int, world: int) -> np.ndarray:
+    """Columns of a time-major (rows x batch*steps) matrix that belong to `rank`."""
+    b0, b1 = shard_range(batch, rank, world)
+    cols = (np.arange(steps)[:, None] * batch + np.arange(b0, b1)[None, :]).ravel()
+    return np.asfortranarray(m[:, cols])
+
+
+def unshard_columns(parts: list[np.ndarray], batch: int, steps: int) -> np.ndarray:
+    """Inverse of shard_columns over all ranks (rank order)."""
+    world = len(parts)
+    rows = parts[0].shape[0]
+    out = np.zeros((rows, batch * steps), np.float32, order="F")
+    for r, p in enumerate(parts):
+        b0, b1 = shard_range(batch, r, world)
+        cols = (np.arange(steps)[:, None] * batch + np.arange(b0, b1)[None, :]).ravel()
+        out[:, cols] = p
+    return out
+
+
+def allreduce_gradients(grads, group=None) -> None:
+    """Sum dW/dR/db over the process group in place (host arrays, torch.distributed)."""
+    import torch
+    import torch.distributed as dist
+    for lst in (grads.dw, grads.dr, grads.db):
+        for i, a in enumerate(lst):
+            t = torch.from_numpy(np.array(a, dtype=np.float32).ravel(order="F"))
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            lst[i] = np.asfortranarray(t.numpy().reshape(a.shape, order="F"))

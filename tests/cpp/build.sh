@@ -1,0 +1,12 @@
+#!/bin/sh
+# Builds the C++ facade drop-in test against the in-tree librnnwave_sm100.so.
+# The checker (oracle/lstm_oracle.c) is compiled with the reference's -ffp-contract=off.
+set -e
+HERE=$(cd "$(dirname "$0")" && pwd)
+ROOT=$(cd "$HERE/../.." && pwd)
+mkdir -p "$HERE/build"
+gcc -O2 -ffp-contract=off -std=c11 -c "$ROOT/oracle/lstm_oracle.c" -o "$HERE/build/lstm_oracle.o"
+g++ -std=c++17 -O2 -I"$ROOT/include" -I"$ROOT/oracle" "$HERE/facade_parity.cpp" "$HERE/build/lstm_oracle.o" \
+    -L"$ROOT/paper_1604_01946_b200/lib" -lrnnwave_sm100 -Wl,-rpath,"$ROOT/paper_1604_01946_b200/lib" \
+    -Wl,-rpath,'$ORIGIN/../../../paper_1604_01946_b200/lib' -o "$HERE/build/facade_parity"
+echo "$HERE/build/facade_parity"
