@@ -120,6 +120,34 @@ __global__ void k_unpad_cols(const float* __restrict__ src, int Rp, int Bp, long
   }
 }
 
+// Plane-wise transpose for the tf32 weight-gradient operands: src is column-major R x C
+// (element (r, c) at c*R + r), dst is row-major R x C (element (r, c) at r*C + c), i.e. the
+// K-major layout over the time-batch dimension. 32x32 shared-memory tiles, coalesced both ways.
+__global__ void k_transpose_planes(const float* __restrict__ s0, const float* __restrict__ s1,
+                                   int R, long long C, float* __restrict__ d0,
+                                   float* __restrict__ d1) {
+  __shared__ float tile[2][32][33];
+  const long long c0 = (long long)blockIdx.x * 32;
+  const int r0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const long long c = c0 + j;
+    const int r = r0 + threadIdx.x;
+    if (c < C && r < R) {
+      tile[0][j][threadIdx.x] = s0[c * R + r];
+      if (s1) tile[1][j][threadIdx.x] = s1[c * R + r];
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = r0 + j;
+    const long long c = c0 + threadIdx.x;
+    if (c < C && r < R) {
+      d0[(long long)r * C + c] = tile[0][threadIdx.x][j];
+      if (s1) d1[(long long)r * C + c] = tile[1][threadIdx.x][j];
+    }
+  }
+}
+
 // db[g*H + u] = sum over partial slices (fixed order) of dbp[slice][g*Hp + u].
 __global__ void k_db_reduce(const float* __restrict__ dbp, int slices, int H, int Hp, float* db) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

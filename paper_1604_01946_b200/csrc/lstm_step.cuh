@@ -98,8 +98,9 @@ __device__ __forceinline__ float sigmoid_ref(float x) { return 1.0f / (1.0f + ex
 
 // Spin until *flag >= target (gpu-scope acquire), bounded by a timeout that records an
 // error instead of hanging the device.
+// `code` identifies the wait for the host-side error message.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
-                                          const RecParams& p) {
+                                          const RecParams& p, int code) {
   if (ld_acquire_gpu(flag) >= target) return;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
@@ -107,10 +108,15 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
     nanosleep(ns);
     if (ns < 256) ns <<= 1;
     if (globaltimer() - t0 > p.timeout_ns) {
-      atomicExch(p.error, 1);
+      atomicCAS(p.error, 0, code);
+      atomicMax(p.error + 1, (int)ld_acquire_gpu(flag));
       return;
     }
   }
+}
+// error code: 1<<30 | dir<<28 | layer<<20 | (t+2)<<4 | which
+__device__ __forceinline__ int wait_code(int dir, int l, int t, int which) {
+  return (1 << 30) | (dir << 28) | (l << 20) | ((t + 2) << 4) | which;
 }
 
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t phase) {
@@ -283,12 +289,12 @@ __global__ void __launch_bounds__(256, 1)
         const bool seg0 = kb < nkb0;
         if (p.persistent) {
           if (seg0 && !x_ready) {
-            if (l > 0) wait_flag(&layers[l - 1].flags[t], p.flag_target, p);
+            if (l > 0) wait_flag(&layers[l - 1].flags[t], p.flag_target, p, wait_code(0, l, t, 1));
             fence_proxy_async_global();
             x_ready = true;
           }
           if (!seg0 && !h_ready) {
-            if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p);
+            if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p, wait_code(0, l, t, 2));
             fence_proxy_async_global();
             h_ready = true;
           }
@@ -508,12 +514,12 @@ __global__ void __launch_bounds__(256, 1)
         const bool seg0 = kb < nkb0;
         if (p.persistent) {
           if (seg0 && !up_ready) {
-            wait_flag(&layers[l + 1].flags[t], p.flag_target, p);
+            wait_flag(&layers[l + 1].flags[t], p.flag_target, p, wait_code(1, l, t, 1));
             fence_proxy_async_global();
             up_ready = true;
           }
           if (!seg0 && !own_ready) {
-            wait_flag(&Ly.flags[t + 1], p.flag_target, p);
+            wait_flag(&Ly.flags[t + 1], p.flag_target, p, wait_code(1, l, t, 2));
             fence_proxy_async_global();
             own_ready = true;
           }

@@ -199,6 +199,10 @@ struct rw_ctx {
   Operand x_op;
   std::vector<DevBuf> h, c, gates, tanhc, dg, carry_c, dh0, dc0, dbp;
   std::vector<Operand> hop, dgop;
+  // tf32 only: K-major (time-batch contiguous) copies for the weight-gradient GEMMs, since
+  // tcgen05 kind::tf32 cannot read these operands MN-major with the 128B swizzle we use
+  std::vector<Operand> dgT, hT;
+  Operand xT;
   DevBuf dx0, y_raw, stage;  // unpadded outputs / staging
   std::vector<DevBuf> dW, dR, db;
   DevBuf flags_f, flags_b, errflag;
@@ -451,6 +455,16 @@ void build(rw_ctx* x) {
     x->db[l].alloc(4ULL * H * 4);
   }
   x->w0t.alloc(x->prec, (size_t)Ip * G4p);
+  const bool kmajor_wg = x->prec != kBF16;
+  if (kmajor_wg) {
+    x->dgT.resize(L);
+    x->hT.resize(L);
+    for (int l = 0; l < L; ++l) {
+      x->dgT[l].alloc(x->prec, (size_t)G4p * colsT);
+      x->hT[l].alloc(x->prec, (size_t)Hp * colsT1);
+    }
+    x->xT.alloc(x->prec, (size_t)Ip * colsT);
+  }
   x->x_raw.alloc((size_t)I * B * T * 4);
   x->dy_raw.alloc((size_t)H * B * T * 4);
   x->x_op.alloc(x->prec, (size_t)Ip * colsT);
@@ -485,7 +499,8 @@ void build(rw_ctx* x) {
   const int aK = x->atomK, prec = x->prec;
   std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
       m_dgMN(2 * L);
-  int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2];
+  int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
+  std::vector<int> m_dgT(2 * L), m_hT(2 * L);
   x->bn_dx = colsT >= 256 ? 256 : 128;
   x->bn_wg = 128;
   for (int p = 0; p < x->planes; ++p) {
@@ -497,6 +512,13 @@ void build(rw_ctx* x) {
       m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
       m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
+    }
+    if (kmajor_wg) {
+      for (int l = 0; l < L; ++l) {
+        m_dgT[2 * l + p] = add_map(x, make_map(x->dgT[l].p(p), prec, colsT, G4p, aK, kTileM));
+        m_hT[2 * l + p] = add_map(x, make_map(x->hT[l].p(p), prec, colsT1, Hp, aK, x->bn_wg));
+      }
+      m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, x->bn_wg));
     }
     m_xK[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp));
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
@@ -559,8 +581,14 @@ void build(rw_ctx* x) {
     const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
     GemmDesc d{};
     for (int p = 0; p < 2; ++p) {
-      d.a[p] = mp(m_dgMN[2 * l + (p % x->planes)], p);
-      d.b[p] = l == 0 ? mp(m_xMN[p % x->planes], p) : mp(m_hopMN[2 * (l - 1) + (p % x->planes)], p);
+      const int q = p % x->planes;
+      if (kmajor_wg) {
+        d.a[p] = mp(m_dgT[2 * l + q], p);
+        d.b[p] = l == 0 ? mp(m_xT[q], p) : mp(m_hT[2 * (l - 1) + q], p);
+      } else {
+        d.a[p] = mp(m_dgMN[2 * l + q], p);
+        d.b[p] = l == 0 ? mp(m_xMN[q], p) : mp(m_hopMN[2 * (l - 1) + q], p);
+      }
     }
     d.M = (int)G4p;
     d.N = Ipl;
@@ -579,7 +607,8 @@ void build(rw_ctx* x) {
     d.n_valid = Il;
     wg.push_back(d);
     GemmDesc r = d;
-    for (int p = 0; p < 2; ++p) r.b[p] = mp(m_hopMN[2 * l + (p % x->planes)], p);
+    for (int p = 0; p < 2; ++p)
+      r.b[p] = kmajor_wg ? mp(m_hT[2 * l + (p % x->planes)], p) : mp(m_hopMN[2 * l + (p % x->planes)], p);
     r.N = Hp;
     r.b_k_off = 0;  // Hprev = blocks 0..T-1
     r.d = x->dR[l].f();
@@ -684,6 +713,7 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.error = static_cast<int*>(x->errflag.p);
   rp.timeout_ns = 20ULL * 1000000000ULL;
+  if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) rp.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
   return rp;
 }
 
@@ -780,10 +810,29 @@ void run_dx0(rw_ctx* x, cudaStream_t s) {
                                x->Bp * x->T, x->bn_dx, x->st_dx, s);
 }
 
+void transpose_planes(rw_ctx* x, const Operand& src, int R, long long C, Operand& dst, cudaStream_t s) {
+  dim3 grid(ceil_div(C, 32), ceil_div(R, 32));
+  ++g_launches;
+  k_transpose_planes<<<grid, dim3(32, 8), 0, s>>>(src.plane[0].f(), src.plane[1].f(), R, C,
+                                                  dst.plane[0].f(), dst.plane[1].f());
+}
+
 template <class P>
 void run_weight_grads(rw_ctx* x, cudaStream_t s) {
-  launch_gemm<P, true, true>(static_cast<const GemmDesc*>(x->gemm_wg.p), x->n_wg, 4 * x->Hp,
-                             std::max(x->Hp, x->Ip), x->bn_wg, x->st_wg, s);
+  const GemmDesc* t = static_cast<const GemmDesc*>(x->gemm_wg.p);
+  const int M = 4 * x->Hp, N = std::max(x->Hp, x->Ip);
+  if constexpr (P::kPlanes == 2) {
+    const long long colsT = (long long)x->Bp * x->T;
+    for (int l = 0; l < x->L; ++l) {
+      transpose_planes(x, x->dgop[l], 4 * x->Hp, colsT, x->dgT[l], s);
+      transpose_planes(x, x->hop[l], x->Hp, colsT + x->Bp, x->hT[l], s);
+    }
+    transpose_planes(x, x->x_op, x->Ip, colsT, x->xT, s);
+    RW_CUDA(cudaGetLastError());
+    launch_gemm<P, false, false>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
+  } else {
+    launch_gemm<P, true, true>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
+  }
 }
 
 void run_db(rw_ctx* x, cudaStream_t s) {
@@ -824,11 +873,17 @@ void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
 }
 
 void check_error_flag(rw_ctx* x) {
-  int e = 0;
-  RW_CUDA(cudaMemcpy(&e, x->errflag.p, sizeof(int), cudaMemcpyDeviceToHost));
-  if (e) {
-    cudaMemset(x->errflag.p, 0, sizeof(int));
-    throw RwError{RW_ESTATE, "persistent recurrent kernel timed out waiting for a wavefront flag"};
+  int e[2] = {0, 0};
+  RW_CUDA(cudaMemcpy(e, x->errflag.p, sizeof e, cudaMemcpyDeviceToHost));
+  if (e[0]) {
+    cudaMemset(x->errflag.p, 0, sizeof e);
+    char b[256];
+    snprintf(b, sizeof b,
+             "persistent recurrent kernel timed out waiting for a wavefront flag "
+             "(%s layer %d step %d, %s flag, last seen count %d)",
+             (e[0] >> 28 & 3) ? "backward" : "forward", (e[0] >> 20) & 0xff,
+             ((e[0] >> 4) & 0xffff) - 2, (e[0] & 15) == 1 ? "neighbour-layer" : "own-layer", e[1]);
+    throw RwError{RW_ESTATE, b};
   }
 }
 
