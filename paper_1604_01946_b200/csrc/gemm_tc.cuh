@@ -57,14 +57,21 @@ __device__ __forceinline__ long long gemm_out_col(const GemmDesc& g, int n) {
   return n < g.n_valid ? n : -1;
 }
 
-template <class P, bool kAMN, bool kBMN>
+// kChunkBN > 0 enables "promotion" for the fp32-parity mode: the K loop is cut into chunks of
+// `chunk_kb` k-blocks, each accumulated into one of two TMEM buffers, and the epilogue drains
+// every chunk into fp32 registers (round-to-nearest adds). The tensor core's accumulation
+// of long K chains loses ~K*2^-24 (measured 5e-5 at K = 6400); chunking bounds that to the
+// chunk length while the next chunk's MMAs run into the other buffer.
+template <class P, bool kAMN, bool kBMN, int kChunkBN>
 __global__ void __launch_bounds__(256, 1)
-    k_gemm_tc(const GemmDesc* __restrict__ table, int bn, int stages) {
+    k_gemm_tc(const GemmDesc* __restrict__ table, int bn, int stages, int chunk_kb) {
   const GemmDesc& g = table[blockIdx.z];
   const int m0 = blockIdx.x * kTileM;
   const int n0 = blockIdx.y * bn;
   if (m0 >= g.M || n0 >= g.N) return;
-  const int nkb = g.K / P::kAtomK;
+  const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;  // OOB K is zero-filled by TMA
+  const int ckb = (kChunkBN > 0 && chunk_kb > 0) ? chunk_kb : nkb;
+  const int nchunks = (nkb + ckb - 1) / ckb;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -74,20 +81,25 @@ __global__ void __launch_bounds__(256, 1)
   const int stage_bytes = P::kPlanes * (a_bytes + b_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
   uint64_t* empty = full + stages;
-  uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + stages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int nbuf = kChunkBN > 0 ? 2 : 1;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)bn) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(bn * nbuf)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 128);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -124,45 +136,88 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
     const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, bn);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % stages;
-      mbar_wait(&full[s], (kb / stages) & 1);
-      tc_fence_after();
-      const uint32_t st = smem_u32(smem + s * stage_bytes);
-      for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
-        for (int c = 0; c < P::kCombos; ++c) {
-          // combos: (hi,hi), (hi,lo), (lo,hi); bf16 has only (hi,hi)
-          const int pa = (c == 2) ? 1 : 0;
-          const int pb = (c == 1) ? 1 : 0;
-          const uint64_t ad = OperandTile<P, kAMN>::desc(st + pa * a_bytes, kk);
-          const uint64_t bd = OperandTile<P, kBMN>::desc(st + P::kPlanes * a_bytes + pb * b_bytes, kk);
-          umma<P::kTF32>(tmem_base, ad, bd, idesc, (kb | kk | c) != 0);
-        }
+    int kb = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1;
+      if (c >= 2) {
+        mbar_wait(&tmem_empty[buf], ((c >> 1) - 1) & 1);
+        tc_fence_after();
       }
-      umma_commit(&empty[s]);
+      const uint32_t acc = tmem_base + buf * bn;
+      const int kb_end = min(nkb, (c + 1) * ckb);
+      for (int k0 = kb; kb < kb_end; ++kb) {
+        const int s = kb % stages;
+        mbar_wait(&full[s], (kb / stages) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * stage_bytes);
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+          for (int cb = 0; cb < P::kCombos; ++cb) {
+            // combos: (hi,hi), (hi,lo), (lo,hi); bf16 has only (hi,hi)
+            const int pa = (cb == 2) ? 1 : 0;
+            const int pb = (cb == 1) ? 1 : 0;
+            const uint64_t ad = OperandTile<P, kAMN>::desc(st + pa * a_bytes, kk);
+            const uint64_t bd = OperandTile<P, kBMN>::desc(st + P::kPlanes * a_bytes + pb * b_bytes, kk);
+            umma<P::kTF32>(acc, ad, bd, idesc, (kb != k0 || kk | cb) ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&tmem_full[buf]);
     }
-    umma_commit(tmem_full);
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
     const int q = warp & 3;
     const int m = m0 + q * 32 + lane;
     const int orow = m < g.M ? gemm_out_row(g, m) : -1;
-    for (int c0 = 0; c0 < bn; c0 += 8) {
-      uint32_t v[8];
-      tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + c0, v);
-      tmem_ld_wait();
-      if (orow < 0) continue;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    if constexpr (kChunkBN > 0) {
+      float accum[kChunkBN];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int n = n0 + c0 + j;
-        if (n >= g.N) break;
-        const long long oc = gemm_out_col(g, n);
-        if (oc < 0) continue;
-        float* dst = g.d + oc * g.ldd + orow;
-        const float val = __uint_as_float(v[j]);
-        *dst = g.accumulate ? *dst + val : val;
+      for (int i = 0; i < kChunkBN; ++i) accum[i] = 0.0f;
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait(&tmem_full[buf], (c >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < kChunkBN; c0 += 8) {
+          uint32_t v[8];
+          tmem_ld_32x32b_x8(tmem_base + lane_off + buf * bn + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) accum[c0 + j] += __uint_as_float(v[j]);
+        }
+        tc_fence_before();
+        mbar_arrive(&tmem_empty[buf]);
+      }
+      if (orow >= 0) {
+#pragma unroll
+        for (int j = 0; j < kChunkBN; ++j) {
+          const int n = n0 + j;
+          if (n >= g.N) break;
+          const long long oc = gemm_out_col(g, n);
+          if (oc < 0) continue;
+          float* dst = g.d + oc * g.ldd + orow;
+          *dst = g.accumulate ? *dst + accum[j] : accum[j];
+        }
+      }
+    } else {
+      mbar_wait(&tmem_full[0], 0);
+      tc_fence_after();
+      for (int c0 = 0; c0 < bn; c0 += 8) {
+        uint32_t v[8];
+        tmem_ld_32x32b_x8(tmem_base + lane_off + c0, v);
+        tmem_ld_wait();
+        if (orow < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n = n0 + c0 + j;
+          if (n >= g.N) break;
+          const long long oc = gemm_out_col(g, n);
+          if (oc < 0) continue;
+          float* dst = g.d + oc * g.ldd + orow;
+          const float val = __uint_as_float(v[j]);
+          *dst = g.accumulate ? *dst + val : val;
+        }
       }
     }
   }

@@ -78,7 +78,17 @@ struct RecParams {
   uint32_t flag_target;
   int* error;
   unsigned long long timeout_ns;
+  unsigned int* progress;  // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
 };
+
+// Debug progress word: (step iteration << 12) | (role marker); volatile store to mapped
+// host memory so the host can print where a stuck persistent kernel is waiting.
+__device__ __forceinline__ void progress(const RecParams& p, int role, int it, int marker) {
+  if (p.progress) {
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
+    *(volatile unsigned*)(p.progress + cta * 4 + role) = (unsigned(it + 2) << 12) | unsigned(marker);
+  }
+}
 
 // ------------------------------------------------------------------ small helpers
 template <class P>
@@ -284,16 +294,19 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
+      progress(p, 0, it, 1);
       bool x_ready = false, h_ready = false;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const bool seg0 = kb < nkb0;
         if (p.persistent) {
           if (seg0 && !x_ready) {
+            progress(p, 0, it, 2);
             if (l > 0) wait_flag(&layers[l - 1].flags[t], p.flag_target, p, wait_code(0, l, t, 1));
             fence_proxy_async_global();
             x_ready = true;
           }
           if (!seg0 && !h_ready) {
+            progress(p, 0, it, 3);
             if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p, wait_code(0, l, t, 2));
             fence_proxy_async_global();
             h_ready = true;
@@ -323,10 +336,12 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
+      progress(p, 1, it, 1);
       if (it > 0) {
         mbar_wait(S.tmem_empty, (it - 1) & 1);
         tc_fence_after();
       }
+      progress(p, 1, it, 2);
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const int s = pc % p.stages;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
@@ -357,11 +372,14 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
+      if (et == 0) progress(p, 2, it, 1);
       mbar_wait(S.tmem_full, it & 1);
       tc_fence_after();
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
+        if (et == 0) progress(p, 2, it, 2);
         exchange_acquire_buffer(S, ks, xc);
+        if (et == 0) progress(p, 2, it, 3);
         // partial accumulator rows q*32+lane, columns n0..n0+nc -> xbuf[n][row]
         for (int c0 = 0; c0 < nc; c0 += 8) {
           uint32_t v[8];
@@ -375,7 +393,9 @@ __global__ void __launch_bounds__(256, 1)
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
+        if (et == 0) progress(p, 2, it, 4);
         exchange_publish(S, ks, xc);
+        if (et == 0) progress(p, 2, it, 5);
         // my column slice of this chunk
         const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
         for (int cc = c_lo + cg; cc < c_hi; cc += 4) {
@@ -413,6 +433,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         exchange_release(S, ks);
+        if (et == 0) progress(p, 2, it, 6);
       }
       if (p.persistent) {
         fence_proxy_async_global();
@@ -508,17 +529,20 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
+      progress(p, 0, it, 1);
       bool up_ready = false, own_ready = false;
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
         const bool seg0 = kb < nkb0;
         if (p.persistent) {
           if (seg0 && !up_ready) {
+            progress(p, 0, it, 2);
             wait_flag(&layers[l + 1].flags[t], p.flag_target, p, wait_code(1, l, t, 1));
             fence_proxy_async_global();
             up_ready = true;
           }
           if (!seg0 && !own_ready) {
+            progress(p, 0, it, 3);
             wait_flag(&Ly.flags[t + 1], p.flag_target, p, wait_code(1, l, t, 2));
             fence_proxy_async_global();
             own_ready = true;
@@ -548,10 +572,12 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
+      progress(p, 1, it, 1);
       if (it > 0) {
         mbar_wait(S.tmem_empty, (it - 1) & 1);
         tc_fence_after();
       }
+      progress(p, 1, it, 2);
       bool first = true;
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
@@ -586,11 +612,14 @@ __global__ void __launch_bounds__(256, 1)
       const int t = p.t_first - it;
       bool any = false;
       for (int kb = kb_lo; kb < kb_hi; ++kb) any |= kb_active(kb, t);
+      if (et == 0) progress(p, 2, it, 1);
       mbar_wait(S.tmem_full, it & 1);
       tc_fence_after();
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
+        if (et == 0) progress(p, 2, it, 2);
         exchange_acquire_buffer(S, ks, xc);
+        if (et == 0) progress(p, 2, it, 3);
         for (int c0 = 0; c0 < nc; c0 += 8) {
           uint32_t v[8];
           tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, v);
@@ -603,7 +632,9 @@ __global__ void __launch_bounds__(256, 1)
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
+        if (et == 0) progress(p, 2, it, 4);
         exchange_publish(S, ks, xc);
+        if (et == 0) progress(p, 2, it, 5);
         const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
         if (u < p.Hp) {
           float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
@@ -662,6 +693,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         exchange_release(S, ks);
+        if (et == 0) progress(p, 2, it, 6);
       }
       if (p.persistent && t >= 0) {
         fence_proxy_async_global();

@@ -6,6 +6,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
+
+#include <chrono>
 
 #include <algorithm>
 #include <cstdarg>
@@ -225,8 +228,9 @@ struct rw_ctx {
   std::vector<cudaStream_t> ls;
   std::vector<cudaEvent_t> lev;
   cudaEvent_t fork_ev = nullptr;
-  cudaGraphExec_t graph_both = nullptr, graph_fwd = nullptr, graph_fwd_train = nullptr,
-                  graph_bwd = nullptr;
+  cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};  // per pass kind
+  long long graph_launches[3] = {0, 0, 0};                   // kernels inside each graph
+  bool use_graphs = true;
 
   // state
   uint64_t tape_gen = 0;
@@ -237,6 +241,11 @@ struct rw_ctx {
   // data parallel
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+
+  // hang debugging (RW_DEBUG_HANG_S): mapped host progress words
+  unsigned int* progress_host = nullptr;
+  unsigned int* progress_dev = nullptr;
+  double hang_s = 0;
 
   // profiling
   bool profiling = false;
@@ -290,6 +299,7 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
         const int kbr = resident ? ceil_div(kb_max, ks) : 0;
         int stages = 4;
         size_t smem = rec_smem_bytes(planes, resident ? kbr : stages, N, stages);
+        if (const char* e = getenv("RW_MIN_SMEM_KB")) smem = std::max(smem, (size_t)atoi(e) * 1024);
         while (smem > (size_t)kSmemLimit && stages > 2) {
           --stages;
           smem = rec_smem_bytes(planes, resident ? kbr : stages, N, stages);
@@ -341,18 +351,28 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
 }
 
 size_t gemm_smem(int planes, int bn, int stages) {
-  return 1024 + (size_t)stages * planes * (kTileM + bn) * kRowBytes + (2 * stages + 2) * 8 + 16;
+  return 1024 + (size_t)stages * planes * (kTileM + bn) * kRowBytes + (2 * stages + 4) * 8 + 16;
 }
+
+// fp32-parity GEMMs accumulate in chunks of kPromoteKB k-blocks (= 256 K elements for tf32)
+// drained into fp32 registers; bf16 runs the whole K in TMEM.
+constexpr int kPromoteKB = 8;
 
 template <class P, bool AMN, bool BMN>
 void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
                  cudaStream_t s) {
   const size_t smem = gemm_smem(P::kPlanes, bn, stages);
-  auto k = k_gemm_tc<P, AMN, BMN>;
-  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
   ++g_launches;
-  k<<<grid, 256, smem, s>>>(table_dev, bn, stages);
+  if (P::kPlanes == 2 && bn == 64) {
+    auto k = k_gemm_tc<P, AMN, BMN, 64>;
+    RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, kPromoteKB);
+  } else {
+    auto k = k_gemm_tc<P, AMN, BMN, 0>;
+    RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, 0);
+  }
   RW_CUDA(cudaGetLastError());
 }
 
@@ -501,8 +521,8 @@ void build(rw_ctx* x) {
       m_dgMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
   std::vector<int> m_dgT(2 * L), m_hT(2 * L);
-  x->bn_dx = colsT >= 256 ? 256 : 128;
-  x->bn_wg = 128;
+  x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 64;
+  x->bn_wg = x->prec == kBF16 ? 128 : 64;
   for (int p = 0; p < x->planes; ++p) {
     for (int l = 0; l < L; ++l) {
       const int Ipl = l == 0 ? Ip : Hp;
@@ -650,6 +670,14 @@ void build(rw_ctx* x) {
     RW_CUDA(cudaEventCreateWithFlags(&x->lev[l], cudaEventDisableTiming));
   }
   RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
+  if (const char* e = getenv("RW_NO_GRAPHS")) x->use_graphs = atoi(e) == 0;
+  if (const char* e = getenv("RW_DEBUG_HANG_S")) {
+    x->hang_s = atof(e);
+    RW_CUDA(cudaHostAlloc((void**)&x->progress_host, 4 * 4096 * sizeof(unsigned), cudaHostAllocMapped));
+    std::memset(x->progress_host, 0, 4 * 4096 * sizeof(unsigned));
+    RW_CUDA(cudaHostGetDevicePointer((void**)&x->progress_dev, x->progress_host, 0));
+    x->use_graphs = false;
+  }
 }
 
 // ------------------------------------------------------------------ phases
@@ -712,6 +740,7 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.stages = fwd ? x->st_f : x->st_b;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.error = static_cast<int*>(x->errflag.p);
+  rp.progress = x->progress_dev;
   rp.timeout_ns = 20ULL * 1000000000ULL;
   if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) rp.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
   return rp;
@@ -843,11 +872,10 @@ void run_db(rw_ctx* x, cudaStream_t s) {
 }
 
 template <class P>
-void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
-  {
+void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
+  if (pass != 1) {
     PhaseTimer pt(x, 0, s);
-    repack_params(x, s);
-    if (pass != 1) forward_prologue(x, s, nullptr, nullptr);
+    forward_prologue(x, s, nullptr, nullptr);
   }
   if (pass != 1) {
     PhaseTimer pt(x, 1, s);
@@ -872,6 +900,44 @@ void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
   }
 }
 
+// A pass is a fixed DAG (descriptors live in HBM), so it is captured once per pass kind
+// into a CUDA graph and replayed: the stepwise schedule's ~2*L*T launches and the
+// per-layer fork/join events then cost one cudaGraphLaunch. Profiling mode runs eagerly so
+// per-phase CUDA events can bracket each phase on the stream.
+template <class P>
+void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
+  if (x->dirty) {
+    PhaseTimer pt(x, 0, s);
+    repack_params(x, s);
+  }
+  if (x->profiling || !x->use_graphs) {
+    enqueue_pass_body<P>(x, pass, s);
+    return;
+  }
+  if (!x->graphs[pass]) {
+    cudaStream_t cs = x->main;
+    RW_CUDA(cudaStreamSynchronize(cs));
+    const long long before = g_launches;
+    RW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_pass_body<P>(x, pass, cs);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(cs, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    RW_CUDA(cudaStreamEndCapture(cs, &g));
+    RW_CUDA(cudaGraphInstantiate(&x->graphs[pass], g, 0));
+    cudaGraphDestroy(g);
+    x->graph_launches[pass] = g_launches - before;
+    g_launches = before;
+  }
+  g_launches += x->graph_launches[pass];
+  RW_CUDA(cudaGraphLaunch(x->graphs[pass], s));
+}
+
 void check_error_flag(rw_ctx* x) {
   int e[2] = {0, 0};
   RW_CUDA(cudaMemcpy(e, x->errflag.p, sizeof e, cudaMemcpyDeviceToHost));
@@ -888,6 +954,24 @@ void check_error_flag(rw_ctx* x) {
 }
 
 void sync_all(rw_ctx* x) {
+  if (x->progress_host) {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (cudaStreamQuery(x->main) == cudaErrorNotReady) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > x->hang_s) {
+        fprintf(stderr, "rnnwave_sm100: stream not done after %.1f s; progress words (cta: prod mma epi):\n", el);
+        for (int c = 0; c < 4096; ++c) {
+          const unsigned* w = x->progress_host + 4 * c;
+          if (w[0] | w[1] | w[2])
+            fprintf(stderr, "  cta %4d: it%3d/m%u  it%3d/m%u  it%3d/m%u\n", c, int(w[0] >> 12) - 2, w[0] & 0xfff,
+                    int(w[1] >> 12) - 2, w[1] & 0xfff, int(w[2] >> 12) - 2, w[2] & 0xfff);
+        }
+        fflush(stderr);
+        _exit(3);
+      }
+      usleep(2000);
+    }
+  }
   RW_CUDA(cudaStreamSynchronize(x->main));
   RW_CUDA(cudaGetLastError());
   check_error_flag(x);
@@ -922,7 +1006,10 @@ std::string g_create_err;
 }  // namespace
 
 rw_ctx::~rw_ctx() {
+  if (progress_host) cudaFreeHost(progress_host);
   if (main) cudaStreamSynchronize(main);
+  for (auto& g : graphs)
+    if (g) cudaGraphExecDestroy(g);
   if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
   for (auto s : ls) cudaStreamDestroy(s);
   for (auto e : lev) cudaEventDestroy(e);

@@ -13,6 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 
 CASES = [
+    (2, 64, 64, 16, 8, "bf16", "persistent", "both-debug"),
+    (2, 64, 64, 16, 8, "bf16", "persistent", "both-onesm"),
+    (2, 130, 70, 33, 5, "fp32", "stepwise", "both"),
     # (L, H, I, B, T, precision, schedule, mode)
     (1, 5, 7, 3, 4, "bf16", "persistent", "both"),
     (2, 64, 64, 16, 8, "bf16", "persistent", "fwd"),
@@ -65,11 +68,16 @@ def child(spec):
 
 def main():
     filt = sys.argv[1] if len(sys.argv) > 1 else ""
-    env = dict(os.environ, RW_FLAG_TIMEOUT_MS="4000")
     for spec in CASES:
+        env = dict(os.environ, RW_FLAG_TIMEOUT_MS="4000")
         name = "L{}H{}I{}B{}T{}-{}-{}-{}".format(*spec)
         if filt not in name:
             continue
+        if spec[-1].endswith("-debug"):
+            env["RW_DEBUG_HANG_S"] = "15"
+        if spec[-1].endswith("-onesm"):
+            env["RW_MIN_SMEM_KB"] = "120"
+        spec = list(spec[:-1]) + [spec[-1].split("-")[0]]
         t0 = time.time()
         try:
             p = subprocess.run([sys.executable, __file__, "--child", json.dumps(spec)], env=env,
