@@ -74,6 +74,10 @@ struct RecParams {
   int n_steps;        // steps in this launch (bwd: may include the dh0 step t = -1)
   int persistent;
   int resident;
+  int a_slots;        // resident A k-block slots (identical in every CTA of a cluster, so
+                      // DSMEM offsets of xbuf / barriers match across ranks)
+  int acc_kb;         // k-blocks per TMEM accumulator (fp32 promotion); accumulators summed
+  int n_acc;          // in fp32 by the epilogue (1 = single accumulator)
   int stages;
   uint32_t flag_target;
   int* error;
@@ -148,6 +152,20 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, uint32_t
   const uint32_t remote = map_dsmem(smem_u32(local_bar), rank);
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
+}
+
+// Sum of `n` TMEM accumulators (N columns apart) for 8 columns of this thread's lane, in fp32
+// with round-to-nearest adds (n == 0 -> zeros: no k-block of this CTA was active).
+__device__ __forceinline__ void load_acc_sum(uint32_t taddr, int N, int n, float (&a)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 0.0f;
+  for (int i = 0; i < n; ++i) {
+    uint32_t v[8];
+    tmem_ld_32x32b_x8(taddr + i * N, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = i == 0 ? __uint_as_float(v[j]) : a[j] + __uint_as_float(v[j]);
+  }
 }
 
 // Shared-memory carve-up common to both directions.
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(256, 1)
   const int b_bytes = N * kRowBytes;
   const int b_stage = P::kPlanes * b_bytes;
   const int a_stage = P::kPlanes * a_bytes;
-  const int a_total = p.resident ? my_nkb * a_stage : p.stages * a_stage;
+  const int a_total = p.resident ? p.a_slots * a_stage : p.stages * a_stage;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -250,7 +268,7 @@ __global__ void __launch_bounds__(256, 1)
   RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)N) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.stages; ++i) {
@@ -349,12 +367,14 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t a_base =
             smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
+        const int ai = (kb - kb_lo) / p.acc_kb;  // accumulator of this k-block
+        const bool fresh = (kb - kb_lo) % p.acc_kb == 0;
         for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
           for (int c = 0; c < P::kCombos; ++c) {
             const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
             const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
             const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            umma<P::kTF32>(tmem_base, ad, bd, idesc, (kb != kb_lo || kk | c) ? 1u : 0u);
+            umma<P::kTF32>(tmem_base + ai * N, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
           }
         }
         umma_commit(&S.empty[s]);
@@ -381,13 +401,12 @@ __global__ void __launch_bounds__(256, 1)
         exchange_acquire_buffer(S, ks, xc);
         if (et == 0) progress(p, 2, it, 3);
         // partial accumulator rows q*32+lane, columns n0..n0+nc -> xbuf[n][row]
+        const int n_used = (my_nkb + p.acc_kb - 1) / p.acc_kb;
         for (int c0 = 0; c0 < nc; c0 += 8) {
-          uint32_t v[8];
-          tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, v);
-          tmem_ld_wait();
+          float a[8];
+          load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = __uint_as_float(v[jj]);
+          for (int jj = 0; jj < 8; ++jj) S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = a[jj];
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();
@@ -471,7 +490,7 @@ __global__ void __launch_bounds__(256, 1)
   const int b_bytes = N * kRowBytes;
   const int b_stage = P::kPlanes * b_bytes;
   const int a_stage = P::kPlanes * a_bytes;
-  const int a_total = p.resident ? my_nkb * a_stage : p.stages * a_stage;
+  const int a_total = p.resident ? p.a_slots * a_stage : p.stages * a_stage;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -479,7 +498,7 @@ __global__ void __launch_bounds__(256, 1)
   RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)N) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.stages; ++i) {
@@ -578,9 +597,12 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
       }
       progress(p, 1, it, 2);
-      bool first = true;
+      int nact = 0;  // active k-blocks so far this step
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
+        const int ai = nact / p.acc_kb;
+        const bool fresh = nact % p.acc_kb == 0;
+        ++nact;
         const int s = pc % p.stages;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
@@ -592,8 +614,7 @@ __global__ void __launch_bounds__(256, 1)
             const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
             const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
             const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            umma<P::kTF32>(tmem_base, ad, bd, idesc, first ? 0u : 1u);
-            first = false;
+            umma<P::kTF32>(tmem_base + ai * N, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
           }
         }
         umma_commit(&S.empty[s]);
@@ -610,8 +631,9 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
-      bool any = false;
-      for (int kb = kb_lo; kb < kb_hi; ++kb) any |= kb_active(kb, t);
+      int nact = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb) nact += kb_active(kb, t) ? 1 : 0;
+      const int n_used = (nact + p.acc_kb - 1) / p.acc_kb;
       if (et == 0) progress(p, 2, it, 1);
       mbar_wait(S.tmem_full, it & 1);
       tc_fence_after();
@@ -621,12 +643,10 @@ __global__ void __launch_bounds__(256, 1)
         exchange_acquire_buffer(S, ks, xc);
         if (et == 0) progress(p, 2, it, 3);
         for (int c0 = 0; c0 < nc; c0 += 8) {
-          uint32_t v[8];
-          tmem_ld_32x32b_x8(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, v);
-          tmem_ld_wait();
+          float a[8];
+          load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = any ? __uint_as_float(v[jj]) : 0.0f;
+          for (int jj = 0; jj < 8; ++jj) S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = a[jj];
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();

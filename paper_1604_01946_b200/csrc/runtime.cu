@@ -219,6 +219,7 @@ struct rw_ctx {
   // schedule
   int fwd_sched = RW_SCHED_STEPWISE, bwd_sched = RW_SCHED_STEPWISE;
   int ks_f = 1, ks_b = 1, res_f = 0, res_b = 0, st_f = 4, st_b = 4;
+  int slots_f = 0, slots_b = 0, acckb_f = 1, acckb_b = 1, nacc_f = 1, nacc_b = 1;
   size_t smem_f = 0, smem_b = 0;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
   size_t smem_wg = 0, smem_dx = 0;
@@ -261,6 +262,7 @@ namespace {
 struct RecPlan {
   int sched, ks, resident, stages;
   size_t smem;
+  int a_slots;
 };
 
 int max_active_clusters(void* kernel, int ks, size_t smem, int ctas) {
@@ -299,6 +301,8 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
         const int kbr = resident ? ceil_div(kb_max, ks) : 0;
         int stages = 4;
         size_t smem = rec_smem_bytes(planes, resident ? kbr : stages, N, stages);
+        // one CTA per SM: co-resident persistent CTAs must never contend for TMEM columns
+        smem = std::max(smem, (size_t)116 * 1024);
         if (const char* e = getenv("RW_MIN_SMEM_KB")) smem = std::max(smem, (size_t)atoi(e) * 1024);
         while (smem > (size_t)kSmemLimit && stages > 2) {
           --stages;
@@ -309,7 +313,7 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
         if (ks > 1) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         const int clusters = max_active_clusters(kernel, ks, smem, (int)ctas);
         if ((long long)clusters * ks < ctas) continue;
-        return RecPlan{RW_SCHED_PERSISTENT, ks, resident, stages, smem};
+        return RecPlan{RW_SCHED_PERSISTENT, ks, resident, stages, smem, resident ? kbr : 0};
       }
     }
     if (want == RW_SCHED_PERSISTENT) einval("persistent schedule does not fit this configuration on the device");
@@ -327,7 +331,7 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
   if (smem > (size_t)kSmemLimit) einval("batch too large for the recurrent kernel tile");
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (ks > 1) cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return RecPlan{RW_SCHED_STEPWISE, ks, 0, stages, smem};
+  return RecPlan{RW_SCHED_STEPWISE, ks, 0, stages, smem, 0};
 }
 
 template <class P>
@@ -507,11 +511,24 @@ void build(rw_ctx* x) {
   x->res_f = pf.resident;
   x->st_f = pf.stages;
   x->smem_f = pf.smem;
+  x->slots_f = pf.a_slots;
   x->bwd_sched = pb.sched;
   x->ks_b = pb.ks;
   x->res_b = pb.resident;
   x->st_b = pb.stages;
   x->smem_b = pb.smem;
+  x->slots_b = pb.a_slots;
+  // fp32-parity: accumulate every kAccKB k-blocks in a separate TMEM accumulator (<= 512 cols)
+  auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc) {
+    acc_kb = kb_per_cta > 0 ? kb_per_cta : 1;
+    n_acc = 1;
+    if (x->prec == kBF16) return;
+    acc_kb = 8;
+    while ((long long)ceil_div(kb_per_cta, acc_kb) * Bp > 512) acc_kb *= 2;
+    n_acc = std::max(1, ceil_div(kb_per_cta, acc_kb));
+  };
+  acc_plan(ceil_div(kbf_max, x->ks_f), x->acckb_f, x->nacc_f);
+  acc_plan(ceil_div(kbb_max, x->ks_b), x->acckb_b, x->nacc_b);
   int slices_b = ceil_div(Bp, kXChunk) * x->ks_b;
   for (int l = 0; l < L; ++l) x->dbp[l].alloc((size_t)slices_b * G4p * 4);
 
@@ -738,6 +755,9 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.ksplit = fwd ? x->ks_f : x->ks_b;
   rp.tiles = fwd ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
   rp.stages = fwd ? x->st_f : x->st_b;
+  rp.a_slots = fwd ? x->slots_f : x->slots_b;
+  rp.acc_kb = fwd ? x->acckb_f : x->acckb_b;
+  rp.n_acc = fwd ? x->nacc_f : x->nacc_b;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.error = static_cast<int*>(x->errflag.p);
   rp.progress = x->progress_dev;
@@ -1334,6 +1354,7 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     const int prec = precision == RW_PREC_BF16 ? kBF16 : kTF32x3;
     const int aK = prec == kBF16 ? 64 : 32;
     if (M % 128 || N % bn || K % 64 || (bn != 64 && bn != 128 && bn != 256)) einval("rw_test_gemm: bad shape");
+    if (prec != kBF16 && (a_mn || b_mn)) einval("rw_test_gemm: tf32 operands must be K-major");
     // element counts of the stored operands
     const long long a_elems = a_mn ? (long long)K * lda : (long long)M * lda;
     const long long b_elems = b_mn ? (long long)K * ldb : (long long)N * ldb;

@@ -13,20 +13,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 
 CASES = [
-    (2, 64, 64, 16, 8, "bf16", "persistent", "both-debug"),
-    (2, 64, 64, 16, 8, "bf16", "persistent", "both-onesm"),
-    (2, 130, 70, 33, 5, "fp32", "stepwise", "both"),
     # (L, H, I, B, T, precision, schedule, mode)
-    (1, 5, 7, 3, 4, "bf16", "persistent", "both"),
-    (2, 64, 64, 16, 8, "bf16", "persistent", "fwd"),
-    (2, 64, 64, 16, 8, "bf16", "persistent", "both"),
-    (2, 64, 64, 16, 8, "bf16", "stepwise", "both"),
-    (2, 64, 64, 16, 8, "fp32", "stepwise", "both"),
-    (2, 64, 64, 16, 8, "fp32", "persistent", "both"),
-    (3, 96, 40, 20, 10, "bf16", "persistent", "both"),
-    (2, 130, 70, 33, 5, "fp32", "stepwise", "both"),
+    (2, 64, 64, 16, 8, "bf16", "persistent", "both-debug"),
+    (3, 96, 40, 20, 10, "bf16", "persistent", "both-debug"),
+    (2, 130, 70, 33, 5, "bf16", "persistent", "both-debug"),
+    (2, 130, 70, 33, 5, "fp32", "persistent", "both-debug"),
     (4, 512, 512, 64, 100, "bf16", "persistent", "both"),
     (4, 512, 512, 64, 100, "fp32", "auto", "both"),
+    (4, 512, 512, 64, 100, "bf16", "stepwise", "both"),
+    (4, 1024, 1024, 16, 200, "bf16", "auto", "both"),
+    (4, 2048, 2048, 64, 100, "bf16", "auto", "both"),
 ]
 
 

@@ -34,11 +34,20 @@ def _run(prec, amn, bmn, M, N, K, bn):
     return err.item()
 
 
-@pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("amn,bmn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("prec,amn,bmn", [(0, 0, 0), (0, 0, 1), (0, 1, 0), (0, 1, 1), (1, 0, 0)])
 def test_gemm_majors(prec, amn, bmn):
+    # MN-major operands are used with bf16 only: kind::tf32 reads 32-bit MN-major tiles with a
+    # different swizzle atom, so the fp32-parity path feeds K-major (transposed) copies instead
     err = _run(prec, amn, bmn, 256, 256, 512, 128)
     assert err < TOL[prec], err
+
+
+def test_tf32_mn_major_rejected():
+    from paper_1604_01946_b200 import _lib
+    L = _lib.load()
+    d = torch.zeros(128 * 128, device="cuda")
+    assert L.rw_test_gemm(1, 1, 0, 128, 128, 64, d.data_ptr(), 128, d.data_ptr(), 64,
+                          d.data_ptr(), 128, 128) == 1
 
 
 @pytest.mark.parametrize("prec", [0, 1])
@@ -52,3 +61,9 @@ def test_gemm_large_k():
     # the weight-gradient shape class: long K (B*T), MN-major operands
     err = _run(0, 1, 1, 512, 256, 6400, 128)
     assert err < TOL[0], err
+
+
+def test_gemm_large_k_fp32_promotion():
+    # fp32-parity at K = 6400: chunked accumulation keeps the error at fp32 level
+    err = _run(1, 0, 0, 256, 128, 6400, 64)
+    assert err < 2e-6, err
