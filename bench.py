@@ -150,6 +150,12 @@ def run_ours(args) -> None:
     dy = make_dy(cfg)
     eng.set_params(params)
     eng.upload_inputs(x, dy)
+    if world > 1:
+        from paper_1604_01946_b200.engine import nccl_unique_id
+        import torch.distributed as dist
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        eng.init_comm(rank, world, box[0])
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     flops = pass_flops(c)

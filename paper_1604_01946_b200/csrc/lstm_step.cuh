@@ -83,7 +83,17 @@ struct RecParams {
   int* error;
   unsigned long long timeout_ns;
   unsigned int* progress;  // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
+  unsigned long long* trace;  // optional [cta][n_steps][4] %globaltimer stamps (RW_TRACE)
 };
+
+// Trace stamps per (CTA, step): 0 producer starts waiting for its inputs, 1 inputs ready
+// (flags acquired), 2 accumulator ready in TMEM (epilogue wakes), 3 step published.
+__device__ __forceinline__ void trace_stamp(const RecParams& p, int it, int what) {
+  if (p.trace) {
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
+    p.trace[((unsigned long long)cta * p.n_steps + it) * 4 + what] = globaltimer();
+  }
+}
 
 // Debug progress word: (step iteration << 12) | (role marker); volatile store to mapped
 // host memory so the host can print where a stuck persistent kernel is waiting.
@@ -115,12 +125,13 @@ __device__ __forceinline__ float sigmoid_ref(float x) { return 1.0f / (1.0f + ex
 // `code` identifies the wait for the host-side error message.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
                                           const RecParams& p, int code) {
-  if (ld_acquire_gpu(flag) >= target) return;
+  for (int i = 0; i < 4096; ++i)
+    if (ld_acquire_gpu(flag) >= target) return;
   const uint64_t t0 = globaltimer();
   uint32_t ns = 32;
   while (ld_acquire_gpu(flag) < target) {
     nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+    if (ns < 128) ns <<= 1;
     if (globaltimer() - t0 > p.timeout_ns) {
       atomicCAS(p.error, 0, code);
       atomicMax(p.error + 1, (int)ld_acquire_gpu(flag));
@@ -137,7 +148,7 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t ph
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(phase)
@@ -313,6 +324,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
       progress(p, 0, it, 1);
+      trace_stamp(p, it, 0);
       bool x_ready = false, h_ready = false;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const bool seg0 = kb < nkb0;
@@ -346,6 +358,7 @@ __global__ void __launch_bounds__(256, 1)
                         kb * P::kAtomK, row0);
         }
       }
+      trace_stamp(p, it, 1);
     }
   } else if (warp == 1 && lane == 0) {
     // ================= MMA issuer
@@ -395,6 +408,7 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) progress(p, 2, it, 1);
       mbar_wait(S.tmem_full, it & 1);
       tc_fence_after();
+      if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
         if (et == 0) progress(p, 2, it, 2);
@@ -455,11 +469,16 @@ __global__ void __launch_bounds__(256, 1)
         if (et == 0) progress(p, 2, it, 6);
       }
       if (p.persistent) {
+        // publish step t: every writer orders its generic stores before later async-proxy
+        // (TMA) reads, the CTA barrier collects them, one thread releases at gpu scope
         fence_proxy_async_global();
-        __threadfence();
         named_bar_sync(1, 128);
-        if (et == 0) red_release_gpu_add(&Ly.flags[t], 1);
+        if (et == 0) {
+          __threadfence();
+          red_release_gpu_add(&Ly.flags[t], 1);
+        }
       }
+      if (et == 0) trace_stamp(p, it, 3);
     }
   }
   tc_fence_before();
@@ -549,6 +568,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
       progress(p, 0, it, 1);
+      trace_stamp(p, it, 0);
       bool up_ready = false, own_ready = false;
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
@@ -583,6 +603,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         ++pc;
       }
+      trace_stamp(p, it, 1);
     }
   } else if (warp == 1 && lane == 0) {
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
@@ -637,6 +658,7 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) progress(p, 2, it, 1);
       mbar_wait(S.tmem_full, it & 1);
       tc_fence_after();
+      if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
         if (et == 0) progress(p, 2, it, 2);
@@ -717,10 +739,13 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (p.persistent && t >= 0) {
         fence_proxy_async_global();
-        __threadfence();
         named_bar_sync(1, 128);
-        if (et == 0) red_release_gpu_add(&Ly.flags[t], 1);
+        if (et == 0) {
+          __threadfence();
+          red_release_gpu_add(&Ly.flags[t], 1);
+        }
       }
+      if (et == 0) trace_stamp(p, it, 3);
     }
   }
   tc_fence_before();

@@ -243,6 +243,10 @@ struct rw_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
 
+  // device trace (RW_TRACE=<csv path>): globaltimer stamps of the persistent kernels
+  DevBuf trace_f, trace_b;
+  std::string trace_path;
+
   // hang debugging (RW_DEBUG_HANG_S): mapped host progress words
   unsigned int* progress_host = nullptr;
   unsigned int* progress_dev = nullptr;
@@ -360,7 +364,7 @@ size_t gemm_smem(int planes, int bn, int stages) {
 
 // fp32-parity GEMMs accumulate in chunks of kPromoteKB k-blocks (= 256 K elements for tf32)
 // drained into fp32 registers; bf16 runs the whole K in TMEM.
-constexpr int kPromoteKB = 8;
+constexpr int kPromoteKB = 2;
 
 template <class P, bool AMN, bool BMN>
 void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
@@ -523,7 +527,7 @@ void build(rw_ctx* x) {
     acc_kb = kb_per_cta > 0 ? kb_per_cta : 1;
     n_acc = 1;
     if (x->prec == kBF16) return;
-    acc_kb = 8;
+    acc_kb = 2;
     while ((long long)ceil_div(kb_per_cta, acc_kb) * Bp > 512) acc_kb *= 2;
     n_acc = std::max(1, ceil_div(kb_per_cta, acc_kb));
   };
@@ -688,6 +692,12 @@ void build(rw_ctx* x) {
   }
   RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
   if (const char* e = getenv("RW_NO_GRAPHS")) x->use_graphs = atoi(e) == 0;
+  if (const char* e = getenv("RW_TRACE")) {
+    x->trace_path = e;
+    const size_t ctas = 4096;
+    x->trace_f.alloc(ctas * (T + 1) * 4 * 8);
+    x->trace_b.alloc(ctas * (T + 2) * 4 * 8);
+  }
   if (const char* e = getenv("RW_DEBUG_HANG_S")) {
     x->hang_s = atof(e);
     RW_CUDA(cudaHostAlloc((void**)&x->progress_host, 4 * 4096 * sizeof(unsigned), cudaHostAllocMapped));
@@ -761,6 +771,8 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.error = static_cast<int*>(x->errflag.p);
   rp.progress = x->progress_dev;
+  rp.trace = nullptr;
+  if (!x->trace_path.empty()) rp.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
   rp.timeout_ns = 20ULL * 1000000000ULL;
   if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) rp.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
   return rp;
@@ -1312,12 +1324,48 @@ int rw_allreduce_grads(rw_ctx* x, void* stream) {
   });
 }
 
+// Write the persistent kernels' step stamps as CSV in the reference trace schema
+// (scheduler.hpp:411-417): task_layer,task_block,phase,worker,start_ns,end_ns, with
+// task_block = step, worker = CTA index within the layer, phase = fwd|bwd, and three spans
+// per (CTA, step): wait (inputs), mma (inputs ready -> accumulator), epilogue (-> published).
+void dump_trace(rw_ctx* x) {
+  if (x->trace_path.empty()) return;
+  FILE* f = fopen(x->trace_path.c_str(), "w");
+  if (!f) return;
+  fprintf(f, "task_layer,task_block,phase,worker,span,start_ns,end_ns\n");
+  for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 ? x->fwd_sched : x->bwd_sched) != RW_SCHED_PERSISTENT) continue;
+    const int steps = dir == 0 ? x->T : x->T + 1;
+    const int ks = dir == 0 ? x->ks_f : x->ks_b;
+    const int tiles = dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
+    const int per_layer = tiles * ks;
+    std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 4);
+    cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ULL;
+    for (auto v : h)
+      if (v && v < t0) t0 = v;
+    for (int l = 0; l < x->L; ++l)
+      for (int w = 0; w < per_layer; ++w)
+        for (int it = 0; it < steps; ++it) {
+          const unsigned long long* s = &h[(((size_t)l * per_layer + w) * steps + it) * 4];
+          const int t = dir == 0 ? it : x->T - 1 - it;
+          const char* ph = dir == 0 ? "fwd" : "bwd";
+          const char* names[3] = {"wait", "mma", "epilogue"};
+          for (int k = 0; k < 3; ++k)
+            if (s[k] && s[k + 1])
+              fprintf(f, "%d,%d,%s,%d,%s,%llu,%llu\n", l, t, ph, w, names[k], s[k] - t0, s[k + 1] - t0);
+        }
+  }
+  fclose(f);
+}
+
 int rw_sync(rw_ctx* x) {
   return guarded(x, [&] {
     RW_CUDA(cudaSetDevice(x->dev));
     RW_CUDA(cudaDeviceSynchronize());
     RW_CUDA(cudaGetLastError());
     check_error_flag(x);
+    dump_trace(x);
   });
 }
 

@@ -89,3 +89,27 @@ def test_zero_params_zero_output():
     for prec in ("fp32", "bf16"):
         y = Engine(cfg, precision=prec).forward(params, make_input(cfg), False).y
         assert np.all(y == 0.0)
+
+
+def test_nccl_single_rank_plumbing():
+    """rw_nccl_unique_id / rw_comm_init / rw_allreduce_grads on a 1-rank communicator leave
+    the gradients unchanged (the multi-rank sum is exercised by bench.py under torchrun and
+    its host logic by tests/test_dist_gloo.py)."""
+    from paper_1604_01946_b200 import Engine
+    from paper_1604_01946_b200.engine import nccl_unique_id
+    c, params, x, dy, h0, c0 = make_case(Dims(2, 64, 64, 16, 4), seed=11)
+    eng = Engine(c, precision="bf16")
+    eng.set_params(params)
+    eng.upload_inputs(x, dy)
+    eng.run_pass(2)
+    eng.sync()
+    L = c.layers
+    before = [np.zeros((256, 64), np.float32, order="F") for _ in range(L)]
+    eng.read_outputs(dw=before)
+    eng.init_comm(0, 1, nccl_unique_id())
+    eng.allreduce_grads()
+    eng.sync()
+    after = [np.zeros((256, 64), np.float32, order="F") for _ in range(L)]
+    eng.read_outputs(dw=after)
+    for a, b in zip(before, after):
+        assert np.array_equal(a, b)
