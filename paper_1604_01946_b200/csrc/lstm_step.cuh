@@ -11,9 +11,11 @@
 // i.e. output_gemm of the layer above (engine.hpp:564-585) and recurrent_backward_gemm
 // (engine.hpp:538-560) share one accumulator and the pointwise backward runs on it.
 //
-// A tile's K range may be split over a cluster of `ksplit` CTAs (split-K); partial
-// accumulators are exchanged through distributed shared memory and every CTA runs the
-// cell epilogue for 1/ksplit of the batch columns.
+// A tile's K range may be split over a cluster of `ksplit` CTAs (split-K). Each CTA owns
+// 1/ksplit of the batch columns for the cell epilogue: after its MMAs it pushes every
+// partial-accumulator column to the owning CTA's receive buffer with st.shared::cluster
+// (fire-and-forget DSMEM stores), signals with a release-arrive on every rank's mbarrier,
+// and then reduces only local shared memory (fixed rank order: deterministic).
 //
 // Two launch modes share the code:
 //   stepwise   : one launch per (layer, step); weights streamed by TMA every step;
@@ -22,6 +24,9 @@
 //                one (layer, tile, k-slice), keeps its weight slice resident in shared
 //                memory, and waits on gpu-scope per-(layer, step) completion counters
 //                (release/acquire) instead of kernel boundaries.
+//
+// Threads: 384 = warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator, warp 3 idle,
+// warps 4..11 epilogue (warp w and w+4 share TMEM lane quarter w%4 and split the columns).
 #pragma once
 
 #include "common.cuh"
@@ -30,7 +35,10 @@
 namespace rw {
 
 constexpr int kMaxLayers = 16;
-constexpr int kXChunk = 64;  // batch columns per epilogue exchange chunk
+constexpr int kXChunk = 64;        // batch columns per epilogue exchange chunk
+constexpr int kRecThreads = 384;
+constexpr int kEpiThreads = 256;
+constexpr int kEpiBase = 128;      // first epilogue thread
 
 struct FwdLayer {
   const CUtensorMap* a[2];   // [W|R] gate-interleaved rows, K-major: {Ipl + Hp, 4Hp}
@@ -59,7 +67,7 @@ struct BwdLayer {
   float* dg;                 // fp32 dG tape, 4Hp x Bp T, row g*Hp + u
   void* dgop[2];             // operand planes, row rho
   float* carry_c;            // Hp x Bp
-  float* dbp;                // [ceil(Bp/64)*ksplit][4Hp] bias-gradient partial sums
+  float* dbp;                // [ceil(Bp/64)*ksplit*2][4Hp] bias-gradient partial sums
   float* dh0;                // Hp x Bp
   float* dc0;                // Hp x Bp
   uint32_t* flags;           // [T]
@@ -75,19 +83,19 @@ struct RecParams {
   int persistent;
   int resident;
   int a_slots;        // resident A k-block slots (identical in every CTA of a cluster, so
-                      // DSMEM offsets of xbuf / barriers match across ranks)
+                      // DSMEM offsets of the receive buffer / barriers match across ranks)
   int acc_kb;         // k-blocks per TMEM accumulator (fp32 promotion); accumulators summed
   int n_acc;          // in fp32 by the epilogue (1 = single accumulator)
   int stages;
   uint32_t flag_target;
   int* error;
   unsigned long long timeout_ns;
-  unsigned int* progress;  // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
+  unsigned int* progress;     // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
   unsigned long long* trace;  // optional [cta][n_steps][4] %globaltimer stamps (RW_TRACE)
 };
 
 // Trace stamps per (CTA, step): 0 producer starts waiting for its inputs, 1 inputs ready
-// (flags acquired), 2 accumulator ready in TMEM (epilogue wakes), 3 step published.
+// (flags acquired, loads issued), 2 accumulator ready in TMEM, 3 step published.
 __device__ __forceinline__ void trace_stamp(const RecParams& p, int it, int what) {
   if (p.trace) {
     const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -118,11 +126,30 @@ __device__ __forceinline__ void store_operand(void* const* planes, long long idx
   }
 }
 
-__device__ __forceinline__ float sigmoid_ref(float x) { return 1.0f / (1.0f + expf(-x)); }
+// Activations. fp32-parity mode keeps the reference's accurate libm chain
+// (sigmoid = 1/(1+exp(-x)), cells.hpp:30; tanh); bf16 mode uses the SFU approximations
+// (relative error ~2^-11, far below the bf16 operand rounding it already carries).
+template <class P>
+__device__ __forceinline__ float act_sigmoid(float x) {
+  if constexpr (P::kPlanes == 1) {
+    return __fdividef(1.0f, 1.0f + __expf(-x));
+  } else {
+    return 1.0f / (1.0f + expf(-x));
+  }
+}
+template <class P>
+__device__ __forceinline__ float act_tanh(float x) {
+  if constexpr (P::kPlanes == 1) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  } else {
+    return tanhf(x);
+  }
+}
 
 // Spin until *flag >= target (gpu-scope acquire), bounded by a timeout that records an
-// error instead of hanging the device.
-// `code` identifies the wait for the host-side error message.
+// error instead of hanging the device. `code` identifies the wait for the host message.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
                                           const RecParams& p, int code) {
   for (int i = 0; i < 4096; ++i)
@@ -164,6 +191,9 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, uint32_t
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
+__device__ __forceinline__ void st_dsmem_f32(uint32_t cluster_addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v));
+}
 
 // Sum of `n` TMEM accumulators (N columns apart) for 8 columns of this thread's lane, in fp32
 // with round-to-nearest adds (n == 0 -> zeros: no k-block of this CTA was active).
@@ -183,7 +213,7 @@ __device__ __forceinline__ void load_acc_sum(uint32_t taddr, int N, int n, float
 struct RecSmem {
   uint8_t* a_res;      // resident A k-blocks (or A stages when streamed)
   uint8_t* b_st;       // B stages
-  float* xbuf;         // [kXChunk][128] partial accumulators for the exchange
+  float* xr;           // receive buffer [ksplit][kXChunk/ksplit][128] of partial columns
   uint64_t* full;
   uint64_t* empty;
   uint64_t* a_full;
@@ -194,14 +224,13 @@ struct RecSmem {
   uint32_t* tmem_slot;
 };
 
-template <class P>
 __device__ __forceinline__ RecSmem carve(uint8_t* smem, int a_bytes_total, int b_stage_bytes,
                                          int stages) {
   RecSmem s;
   s.a_res = smem;
   s.b_st = smem + a_bytes_total;
-  s.xbuf = reinterpret_cast<float*>(s.b_st + stages * b_stage_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s.xbuf + kXChunk * kTileM);
+  s.xr = reinterpret_cast<float*>(s.b_st + stages * b_stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s.xr + kXChunk * kTileM);
   s.full = bars;
   s.empty = bars + stages;
   s.a_full = bars + 2 * stages;
@@ -222,40 +251,108 @@ inline size_t rec_smem_bytes(int planes, int a_kblocks_resident_or_stages, int n
   return 1024 + a + b + x + bars;
 }
 
-// The two-level cluster exchange of one column chunk: publish my partial tile, wait for all
-// ranks, return. xc counts exchanges (phase parity).
-__device__ __forceinline__ void exchange_publish(const RecSmem& s, int ks, uint32_t xc) {
-  named_bar_sync(1, 128);
+// ---- split-K exchange of one column chunk (xc counts exchanges: mbarrier phase parity) ----
+// 1. wait until every rank finished reading the previous chunk (xfree), 2. push partial
+// columns into their owners' receive buffers, 3. publish (bar + release-arrive on all
+// ranks), 4. wait for all ranks' pushes (acquire). After reducing: release (xfree).
+__device__ __forceinline__ void xchg_wait_free(const RecSmem& s, int ks, uint32_t xc) {
+  if (ks > 1 && xc > 0) mbar_wait_cluster(s.xfree, (xc - 1) & 1);
+}
+// Thread (quarter q, lane) pushes the 8 columns c0..c0+7 of its accumulator row.
+__device__ __forceinline__ void xchg_push8(const RecSmem& s, int ks, int rank, int nco, int q,
+                                           int lane, int c0, const float (&a)[8]) {
+  const int row = q * 32 + lane;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + j;
+    const int owner = c / nco;
+    float* dst = s.xr + ((rank * nco) + (c - owner * nco)) * kTileM + row;
+    if (owner == rank)
+      *dst = a[j];
+    else
+      st_dsmem_f32(map_dsmem(smem_u32(dst), owner), a[j]);
+  }
+}
+__device__ __forceinline__ void xchg_publish(const RecSmem& s, int ks, uint32_t xc) {
+  named_bar_sync(1, kEpiThreads);
   if (ks > 1) {
-    if (threadIdx.x == 128) {
+    if (threadIdx.x == kEpiBase) {
       asm volatile("fence.acq_rel.cluster;" ::: "memory");
       for (int r = 0; r < ks; ++r) mbar_arrive_remote(s.xready, r);
     }
     mbar_wait_cluster(s.xready, xc & 1);
   }
 }
-__device__ __forceinline__ void exchange_release(const RecSmem& s, int ks) {
-  named_bar_sync(1, 128);
-  if (ks > 1 && threadIdx.x == 128) {
+__device__ __forceinline__ void xchg_release(const RecSmem& s, int ks) {
+  named_bar_sync(1, kEpiThreads);
+  if (ks > 1 && threadIdx.x == kEpiBase) {
     for (int r = 0; r < ks; ++r) mbar_arrive_remote(s.xfree, r);
   }
 }
-__device__ __forceinline__ void exchange_acquire_buffer(const RecSmem& s, int ks, uint32_t xc) {
-  if (ks > 1 && xc > 0) mbar_wait_cluster(s.xfree, (xc - 1) & 1);
+// Reduced accumulator value of owned column cl, row `row` (fixed rank order).
+__device__ __forceinline__ float xchg_sum(const RecSmem& s, int ks, int nco, int cl, int row) {
+  float acc = s.xr[cl * kTileM + row];
+  for (int r = 1; r < ks; ++r) acc += s.xr[(r * nco + cl) * kTileM + row];
+  return acc;
 }
 
-// Read the sum over the cluster of xbuf[idx] (fixed rank order => deterministic).
-__device__ __forceinline__ float xsum(const RecSmem& s, int ks, int idx) {
-  if (ks == 1) return s.xbuf[idx];
-  const uint32_t local = smem_u32(s.xbuf + idx);
-  float acc = ld_dsmem_f32(map_dsmem(local, 0));
-  for (int r = 1; r < ks; ++r) acc += ld_dsmem_f32(map_dsmem(local, r));
-  return acc;
+// Common prologue: barriers, TMEM allocation, cluster rendezvous.
+__device__ __forceinline__ uint32_t rec_setup(const RecSmem& S, const RecParams& p, int ks,
+                                              uint32_t tmem_cols) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    mbar_init(S.a_full, 1);
+    mbar_init(S.tmem_full, 1);
+    mbar_init(S.tmem_empty, kEpiThreads);
+    mbar_init(S.xready, ks);
+    mbar_init(S.xfree, ks);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(S.tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
+  tc_fence_after();
+  return *S.tmem_slot;
+}
+
+__device__ __forceinline__ void rec_teardown(int ks, uint32_t tmem_base, uint32_t tmem_cols) {
+  tc_fence_before();
+  __syncthreads();
+  if (ks > 1) cluster_sync();  // no CTA leaves while peers may still write its smem
+  if ((threadIdx.x >> 5) == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(tmem_cols));
+  }
+}
+
+// MMA issue of one k-block (all kk substeps, all precision combos) into accumulator acc.
+template <class P>
+__device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32_t b_base,
+                                           int a_bytes, int b_bytes, uint32_t idesc,
+                                           bool fresh) {
+  for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+    for (int c = 0; c < P::kCombos; ++c) {
+      const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
+      const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+      const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+      umma<P::kTF32>(acc, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
+    }
+  }
 }
 
 // ====================================================================== forward kernel
 template <class P>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_fwd(const FwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
   const FwdLayer& Ly = layers[l];
@@ -276,34 +373,11 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
+  const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < p.stages; ++i) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], 1);
-    }
-    mbar_init(S.a_full, 1);
-    mbar_init(S.tmem_full, 1);
-    mbar_init(S.tmem_empty, 128);
-    mbar_init(S.xready, ks);
-    mbar_init(S.xfree, ks);
-    fence_barrier_init();
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(S.tmem_slot)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (ks > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
-  tc_fence_after();
-  const uint32_t tmem_base = *S.tmem_slot;
+  const uint32_t tmem_base = rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
   if (warp == 0 && lane == 0) {
@@ -377,31 +451,27 @@ __global__ void __launch_bounds__(256, 1)
         const int s = pc % p.stages;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
-        const uint32_t a_base =
-            smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
+        const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
         const int ai = (kb - kb_lo) / p.acc_kb;  // accumulator of this k-block
-        const bool fresh = (kb - kb_lo) % p.acc_kb == 0;
-        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
-          for (int c = 0; c < P::kCombos; ++c) {
-            const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
-            const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            umma<P::kTF32>(tmem_base + ai * N, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
-          }
-        }
+        mma_kblock<P>(tmem_base + ai * N, a_base, b_base, a_bytes, b_bytes, idesc,
+                      (kb - kb_lo) % p.acc_kb == 0);
         umma_commit(&S.empty[s]);
       }
       umma_commit(S.tmem_full);
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
-    const int et = threadIdx.x - 128;     // 0..127
-    const int q = warp & 3;               // TMEM lane quarter == gate
-    const int j = et & 31;                // unit within tile (cell phase)
-    const int cg = et >> 5;               // column group (cell phase)
+    const int et = threadIdx.x - kEpiBase;  // 0..255
+    const int q = warp & 3;                 // TMEM lane quarter == gate
+    const int half = (warp - 4) >> 2;       // which half of the chunk's columns to drain
+    const int j = et & 31;                  // unit within tile (cell phase)
+    const int cg = et >> 5;                 // column group 0..7 (cell phase)
     const int u = tile * kUnitsPerFwdTile + j;
     const long long Hp = p.Hp, G4 = 4 * Hp;
+    const float bi = Ly.bias[u], bf = Ly.bias[Hp + u], bo = Ly.bias[2 * Hp + u],
+                bc = Ly.bias[3 * Hp + u];
+    const int n_used = (my_nkb + p.acc_kb - 1) / p.acc_kb;
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
@@ -411,48 +481,45 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
-        if (et == 0) progress(p, 2, it, 2);
-        exchange_acquire_buffer(S, ks, xc);
-        if (et == 0) progress(p, 2, it, 3);
-        // partial accumulator rows q*32+lane, columns n0..n0+nc -> xbuf[n][row]
-        const int n_used = (my_nkb + p.acc_kb - 1) / p.acc_kb;
-        for (int c0 = 0; c0 < nc; c0 += 8) {
+        const int nco = nc / ks;  // columns of this chunk owned by each rank
+        xchg_wait_free(S, ks, xc);
+        for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = a[jj];
+          xchg_push8(S, ks, rank, nco, q, lane, c0, a);
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
-        if (et == 0) progress(p, 2, it, 4);
-        exchange_publish(S, ks, xc);
-        if (et == 0) progress(p, 2, it, 5);
-        // my column slice of this chunk
-        const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
-        for (int cc = c_lo + cg; cc < c_hi; cc += 4) {
-          const int n = n0 + cc;
-          const float zi = xsum(S, ks, cc * kTileM + 0 * 32 + j);
-          const float zf = xsum(S, ks, cc * kTileM + 1 * 32 + j);
-          const float zo = xsum(S, ks, cc * kTileM + 2 * 32 + j);
-          const float zc = xsum(S, ks, cc * kTileM + 3 * 32 + j);
-          const float ai = zi + Ly.bias[u];
-          const float af = zf + Ly.bias[Hp + u];
-          const float ao = zo + Ly.bias[2 * Hp + u];
-          const float ac = zc + Ly.bias[3 * Hp + u];
-          const float iv = sigmoid_ref(ai);
-          const float fv = sigmoid_ref(af);
-          const float ov = sigmoid_ref(ao);
-          const float cb = tanhf(ac);
-          const long long col_prev = (long long)t * p.Bp + n;  // block t   (c_{t-1})
-          const long long col_new = col_prev + p.Bp;           // block t+1 (c_t, h_t)
-          const float cp = Ly.c[col_prev * Hp + u];
-          const float t1 = fv * cp;
+        xchg_publish(S, ks, xc);
+        // cell phase: owned columns cl = cg + 8k, unit j; loads first, then math
+        float cp[8];
+        const long long colb = (long long)t * p.Bp + n0 + rank * nco;  // block t, owned base
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int cl = cg + 8 * k;
+          cp[k] = cl < nco ? Ly.c[(colb + cl) * Hp + u] : 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int cl = cg + 8 * k;
+          if (cl >= nco) break;
+          const float ai = xchg_sum(S, ks, nco, cl, 0 * 32 + j) + bi;
+          const float af = xchg_sum(S, ks, nco, cl, 1 * 32 + j) + bf;
+          const float ao = xchg_sum(S, ks, nco, cl, 2 * 32 + j) + bo;
+          const float ac = xchg_sum(S, ks, nco, cl, 3 * 32 + j) + bc;
+          const float iv = act_sigmoid<P>(ai);
+          const float fv = act_sigmoid<P>(af);
+          const float ov = act_sigmoid<P>(ao);
+          const float cb = act_tanh<P>(ac);
+          const float t1 = fv * cp[k];
           const float t2 = iv * cb;
           const float cv = t1 + t2;
-          const float tcv = tanhf(cv);
+          const float tcv = act_tanh<P>(cv);
           const float hv = ov * tcv;
+          const long long col_prev = colb + cl;       // block t   (c_{t-1})
+          const long long col_new = col_prev + p.Bp;  // block t+1 (c_t, h_t)
           Ly.c[col_new * Hp + u] = cv;
           Ly.h[col_new * Hp + u] = hv;
           store_operand<P>(Ly.hop, col_new * Hp + u, hv);
@@ -465,14 +532,13 @@ __global__ void __launch_bounds__(256, 1)
             Ly.tanhc[col_prev * Hp + u] = tcv;
           }
         }
-        exchange_release(S, ks);
-        if (et == 0) progress(p, 2, it, 6);
+        xchg_release(S, ks);
       }
       if (p.persistent) {
-        // publish step t: every writer orders its generic stores before later async-proxy
-        // (TMA) reads, the CTA barrier collects them, one thread releases at gpu scope
+        // publish step t: writers order their generic stores before later async-proxy (TMA)
+        // reads, the CTA barrier collects them, one thread releases at gpu scope
         fence_proxy_async_global();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           __threadfence();
           red_release_gpu_add(&Ly.flags[t], 1);
@@ -481,18 +547,12 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) trace_stamp(p, it, 3);
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (ks > 1) cluster_sync();  // no CTA leaves while peers may still read its smem
-  if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(tmem_cols));
-  }
+  rec_teardown(ks, tmem_base, tmem_cols);
 }
 
 // ====================================================================== backward kernel
 template <class P>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_bwd(const BwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
   const BwdLayer& Ly = layers[l];
@@ -514,34 +574,11 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  RecSmem S = carve<P>(smem, a_total, b_stage, p.stages);
+  const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < p.stages; ++i) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], 1);
-    }
-    mbar_init(S.a_full, 1);
-    mbar_init(S.tmem_full, 1);
-    mbar_init(S.tmem_empty, 128);
-    mbar_init(S.xready, ks);
-    mbar_init(S.xfree, ks);
-    fence_barrier_init();
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(S.tmem_slot)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (ks > 1) cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *S.tmem_slot;
+  const uint32_t tmem_base = rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
   // k-blocks this CTA multiplies at step t: seg0 needs dG_{l+1,t} (t >= 0), seg1 needs
@@ -621,23 +658,14 @@ __global__ void __launch_bounds__(256, 1)
       int nact = 0;  // active k-blocks so far this step
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
-        const int ai = nact / p.acc_kb;
-        const bool fresh = nact % p.acc_kb == 0;
-        ++nact;
         const int s = pc % p.stages;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
-        const uint32_t a_base =
-            smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
+        const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
-        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
-          for (int c = 0; c < P::kCombos; ++c) {
-            const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
-            const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-            umma<P::kTF32>(tmem_base + ai * N, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
-          }
-        }
+        mma_kblock<P>(tmem_base + (nact / p.acc_kb) * N, a_base, b_base, a_bytes, b_bytes, idesc,
+                      nact % p.acc_kb == 0);
+        ++nact;
         umma_commit(&S.empty[s]);
         ++pc;
       }
@@ -645,9 +673,12 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM backward (cells.hpp:424-447)
-    const int et = threadIdx.x - 128;
+    const int et = threadIdx.x - kEpiBase;
     const int q = warp & 3;
-    const int u = row0 + et;           // hidden unit of this thread (cell phase)
+    const int half = (warp - 4) >> 2;
+    const int ul = et & 127;            // unit within the tile (cell phase)
+    const int hh = et >> 7;             // column parity (cell phase)
+    const int u = row0 + ul;
     const long long Hp = p.Hp, G4 = 4 * Hp;
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
@@ -661,85 +692,98 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
-        if (et == 0) progress(p, 2, it, 2);
-        exchange_acquire_buffer(S, ks, xc);
-        if (et == 0) progress(p, 2, it, 3);
-        for (int c0 = 0; c0 < nc; c0 += 8) {
+        const int nco = nc / ks;
+        xchg_wait_free(S, ks, xc);
+        for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) S.xbuf[(c0 + jj) * kTileM + q * 32 + lane] = a[jj];
+          xchg_push8(S, ks, rank, nco, q, lane, c0, a);
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
-        if (et == 0) progress(p, 2, it, 4);
-        exchange_publish(S, ks, xc);
-        if (et == 0) progress(p, 2, it, 5);
-        const int c_lo = rank * nc / ks, c_hi = (rank + 1) * nc / ks;
+        xchg_publish(S, ks, xc);
+        const long long cbase = (long long)n0 + rank * nco;  // first owned batch column
         if (u < p.Hp) {
           float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
-          for (int cc = c_lo; cc < c_hi; ++cc) {
-            const int n = n0 + cc;
-            const float acc = xsum(S, ks, cc * kTileM + et);
-            if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170)
-              Ly.dh0[(long long)n * Hp + u] = acc;
-              Ly.dc0[(long long)n * Hp + u] = Ly.carry_c[(long long)n * Hp + u];
-              continue;
+          // owned columns cl = hh + 2k, processed 8 at a time: all loads first, then math
+          for (int kb8 = 0; kb8 * 16 < nco; ++kb8) {
+            float acc[8], pi[8], pf[8], po[8], pcb[8], ptc[8], pcp[8], dci[8], dyv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int cl = hh + 2 * (kb8 * 8 + k);
+              acc[k] = pi[k] = pf[k] = po[k] = pcb[k] = ptc[k] = pcp[k] = dci[k] = dyv[k] = 0.0f;
+              if (cl >= nco) continue;
+              acc[k] = xchg_sum(S, ks, nco, cl, ul);
+              const long long n = cbase + cl;
+              if (t < 0) {
+                dci[k] = Ly.carry_c[n * Hp + u];
+                continue;
+              }
+              const long long col = (long long)t * p.Bp + n;
+              const float* gp = Ly.gates + col * G4 + u;
+              pi[k] = gp[0];
+              pf[k] = gp[Hp];
+              po[k] = gp[2 * Hp];
+              pcb[k] = gp[3 * Hp];
+              ptc[k] = Ly.tanhc[col * Hp + u];
+              pcp[k] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+              dci[k] = (t == p.T - 1) ? 0.0f : Ly.carry_c[n * Hp + u];
+              if (Ly.dy && u < p.H && n < p.B) dyv[k] = Ly.dy[((long long)t * p.B + n) * p.H + u];
             }
-            float dh = acc;
-            if (Ly.dy) {
-              const float dyv = (u < p.H && n < p.B) ? Ly.dy[((long long)t * p.B + n) * p.H + u] : 0.0f;
-              dh = dyv + acc;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int cl = hh + 2 * (kb8 * 8 + k);
+              if (cl >= nco) break;
+              const long long n = cbase + cl;
+              if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170)
+                Ly.dh0[n * Hp + u] = acc[k];
+                Ly.dc0[n * Hp + u] = dci[k];
+                continue;
+              }
+              const float dh = Ly.dy ? dyv[k] + acc[k] : acc[k];
+              const float q1 = dh * po[k];
+              const float s0 = ptc[k] * ptc[k];
+              const float s1 = 1.0f - s0;
+              const float q2 = q1 * s1;
+              const float dc = dci[k] + q2;
+              const float a1 = dc * pcb[k], a2 = a1 * pi[k], a3 = 1.0f - pi[k];
+              const float b1 = dc * pcp[k], b2 = b1 * pf[k], b3 = 1.0f - pf[k];
+              const float c1 = dh * ptc[k], c2 = c1 * po[k], c3 = 1.0f - po[k];
+              const float d1 = dc * pi[k], d2 = pcb[k] * pcb[k], d3 = 1.0f - d2;
+              const float gi = a2 * a3, gf = b2 * b3, go = c2 * c3, gc = d1 * d3;
+              Ly.carry_c[n * Hp + u] = dc * pf[k];
+              const long long col = (long long)t * p.Bp + n;
+              float* dgp = Ly.dg + col * G4 + u;
+              dgp[0] = gi;
+              dgp[Hp] = gf;
+              dgp[2 * Hp] = go;
+              dgp[3 * Hp] = gc;
+              const long long ob = col * G4;
+              store_operand<P>(Ly.dgop, ob + rho_of(0, u), gi);
+              store_operand<P>(Ly.dgop, ob + rho_of(1, u), gf);
+              store_operand<P>(Ly.dgop, ob + rho_of(2, u), go);
+              store_operand<P>(Ly.dgop, ob + rho_of(3, u), gc);
+              si += gi;
+              sf += gf;
+              so += go;
+              sc += gc;
             }
-            const long long col = (long long)t * p.Bp + n;
-            const float* gp = Ly.gates + col * G4 + u;
-            const float pi = gp[0], pf = gp[Hp], po = gp[2 * Hp], pcb = gp[3 * Hp];
-            const float ptc = Ly.tanhc[col * Hp + u];
-            const float pcp = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
-            float* ccar = Ly.carry_c + (long long)n * Hp + u;
-            const float dci = (t == p.T - 1) ? 0.0f : *ccar;
-            const float q1 = dh * po;
-            const float s0 = ptc * ptc;
-            const float s1 = 1.0f - s0;
-            const float q2 = q1 * s1;
-            const float dc = dci + q2;
-            const float a1 = dc * pcb, a2 = a1 * pi, a3 = 1.0f - pi;
-            const float b1 = dc * pcp, b2 = b1 * pf, b3 = 1.0f - pf;
-            const float c1 = dh * ptc, c2 = c1 * po, c3 = 1.0f - po;
-            const float d1 = dc * pi, d2 = pcb * pcb, d3 = 1.0f - d2;
-            const float gi = a2 * a3, gf = b2 * b3, go = c2 * c3, gc = d1 * d3;
-            *ccar = dc * pf;
-            float* dgp = Ly.dg + col * G4 + u;
-            dgp[0] = gi;
-            dgp[Hp] = gf;
-            dgp[2 * Hp] = go;
-            dgp[3 * Hp] = gc;
-            const long long ob = col * G4;
-            store_operand<P>(Ly.dgop, ob + rho_of(0, u), gi);
-            store_operand<P>(Ly.dgop, ob + rho_of(1, u), gf);
-            store_operand<P>(Ly.dgop, ob + rho_of(2, u), go);
-            store_operand<P>(Ly.dgop, ob + rho_of(3, u), gc);
-            si += gi;
-            sf += gf;
-            so += go;
-            sc += gc;
           }
           if (t >= 0 && Ly.dbp) {
-            float* d = Ly.dbp + (long long)((n0 / kXChunk) * ks + rank) * G4 + u;
+            float* d = Ly.dbp + (long long)(((n0 / kXChunk) * ks + rank) * 2 + hh) * G4 + u;
             d[0] += si;
             d[Hp] += sf;
             d[2 * Hp] += so;
             d[3 * Hp] += sc;
           }
         }
-        exchange_release(S, ks);
-        if (et == 0) progress(p, 2, it, 6);
+        xchg_release(S, ks);
       }
       if (p.persistent && t >= 0) {
         fence_proxy_async_global();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           __threadfence();
           red_release_gpu_add(&Ly.flags[t], 1);
@@ -748,13 +792,7 @@ __global__ void __launch_bounds__(256, 1)
       if (et == 0) trace_stamp(p, it, 3);
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (ks > 1) cluster_sync();
-  if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(tmem_cols));
-  }
+  rec_teardown(ks, tmem_base, tmem_cols);
 }
 
 }  // namespace rw

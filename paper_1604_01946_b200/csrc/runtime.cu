@@ -272,7 +272,7 @@ struct RecPlan {
 int max_active_clusters(void* kernel, int ks, size_t smem, int ctas) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctas, 1, 1);
-  lc.blockDim = dim3(256, 1, 1);
+  lc.blockDim = dim3(kRecThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -343,7 +343,7 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
                 size_t smem, cudaStream_t s) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid_x, grid_y, 1);
-  lc.blockDim = dim3(256, 1, 1);
+  lc.blockDim = dim3(kRecThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
   cudaLaunchAttribute at[1];
@@ -533,7 +533,7 @@ void build(rw_ctx* x) {
   };
   acc_plan(ceil_div(kbf_max, x->ks_f), x->acckb_f, x->nacc_f);
   acc_plan(ceil_div(kbb_max, x->ks_b), x->acckb_b, x->nacc_b);
-  int slices_b = ceil_div(Bp, kXChunk) * x->ks_b;
+  int slices_b = ceil_div(Bp, kXChunk) * x->ks_b * 2;
   for (int l = 0; l < L; ++l) x->dbp[l].alloc((size_t)slices_b * G4p * 4);
 
   // ---- tensor maps
@@ -897,7 +897,7 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
 }
 
 void run_db(rw_ctx* x, cudaStream_t s) {
-  const int slices = ceil_div(x->Bp, kXChunk) * x->ks_b;
+  const int slices = ceil_div(x->Bp, kXChunk) * x->ks_b * 2;
   for (int l = 0; l < x->L; ++l, ++g_launches)
     k_db_reduce<<<ceil_div(4 * x->H, 256), 256, 0, s>>>(x->dbp[l].f(), slices, x->H, x->Hp, x->db[l].f());
   RW_CUDA(cudaGetLastError());
