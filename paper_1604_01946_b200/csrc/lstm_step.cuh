@@ -91,15 +91,16 @@ struct RecParams {
   int* error;
   unsigned long long timeout_ns;
   unsigned int* progress;     // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
-  unsigned long long* trace;  // optional [cta][n_steps][4] %globaltimer stamps (RW_TRACE)
+  unsigned long long* trace;  // optional [cta][n_steps][8] %globaltimer stamps (RW_TRACE)
 };
 
 // Trace stamps per (CTA, step): 0 producer starts waiting for its inputs, 1 inputs ready
-// (flags acquired, loads issued), 2 accumulator ready in TMEM, 3 step published.
+// (flags acquired, loads issued), 2 accumulator ready in TMEM, 3 partials pushed, 4 exchange
+// complete, 5 cell math + stores done, 6 exchange buffer released, 7 step published.
 __device__ __forceinline__ void trace_stamp(const RecParams& p, int it, int what) {
   if (p.trace) {
     const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
-    p.trace[((unsigned long long)cta * p.n_steps + it) * 4 + what] = globaltimer();
+    p.trace[((unsigned long long)cta * p.n_steps + it) * 8 + what] = globaltimer();
   }
 }
 
@@ -492,7 +493,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
         xchg_publish(S, ks, xc);
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 4);
         // cell phase: owned columns cl = cg + 8k, unit j; loads first, then math
         float cp[8];
         const long long colb = (long long)t * p.Bp + n0 + rank * nco;  // block t, owned base
@@ -532,7 +535,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             Ly.tanhc[col_prev * Hp + u] = tcv;
           }
         }
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 5);
         xchg_release(S, ks);
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 6);
       }
       if (p.persistent) {
         // publish step t: writers order their generic stores before later async-proxy (TMA)
@@ -544,7 +549,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           red_release_gpu_add(&Ly.flags[t], 1);
         }
       }
-      if (et == 0) trace_stamp(p, it, 3);
+      if (et == 0) trace_stamp(p, it, 7);
     }
   }
   rec_teardown(ks, tmem_base, tmem_cols);
@@ -703,7 +708,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
         xchg_publish(S, ks, xc);
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 4);
         const long long cbase = (long long)n0 + rank * nco;  // first owned batch column
         if (u < p.Hp) {
           float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
@@ -779,7 +786,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             d[3 * Hp] += sc;
           }
         }
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 5);
         xchg_release(S, ks);
+        if (et == 0 && n0 == 0) trace_stamp(p, it, 6);
       }
       if (p.persistent && t >= 0) {
         fence_proxy_async_global();
@@ -789,7 +798,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           red_release_gpu_add(&Ly.flags[t], 1);
         }
       }
-      if (et == 0) trace_stamp(p, it, 3);
+      if (et == 0) trace_stamp(p, it, 7);
     }
   }
   rec_teardown(ks, tmem_base, tmem_cols);

@@ -695,8 +695,8 @@ void build(rw_ctx* x) {
   if (const char* e = getenv("RW_TRACE")) {
     x->trace_path = e;
     const size_t ctas = 4096;
-    x->trace_f.alloc(ctas * (T + 1) * 4 * 8);
-    x->trace_b.alloc(ctas * (T + 2) * 4 * 8);
+    x->trace_f.alloc(ctas * (T + 1) * 8 * 8);
+    x->trace_b.alloc(ctas * (T + 2) * 8 * 8);
   }
   if (const char* e = getenv("RW_DEBUG_HANG_S")) {
     x->hang_s = atof(e);
@@ -1339,19 +1339,19 @@ void dump_trace(rw_ctx* x) {
     const int ks = dir == 0 ? x->ks_f : x->ks_b;
     const int tiles = dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
     const int per_layer = tiles * ks;
-    std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 4);
+    std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 8);
     cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ULL;
     for (auto v : h)
       if (v && v < t0) t0 = v;
+    const char* names[7] = {"wait", "mma", "push", "xchg", "cells", "release", "publish"};
     for (int l = 0; l < x->L; ++l)
       for (int w = 0; w < per_layer; ++w)
         for (int it = 0; it < steps; ++it) {
-          const unsigned long long* s = &h[(((size_t)l * per_layer + w) * steps + it) * 4];
+          const unsigned long long* s = &h[(((size_t)l * per_layer + w) * steps + it) * 8];
           const int t = dir == 0 ? it : x->T - 1 - it;
           const char* ph = dir == 0 ? "fwd" : "bwd";
-          const char* names[3] = {"wait", "mma", "epilogue"};
-          for (int k = 0; k < 3; ++k)
+          for (int k = 0; k < 7; ++k)
             if (s[k] && s[k + 1])
               fprintf(f, "%d,%d,%s,%d,%s,%llu,%llu\n", l, t, ph, w, names[k], s[k] - t0, s[k + 1] - t0);
         }

@@ -19,7 +19,7 @@ def summarize(path):
         d = int(r["end_ns"]) - int(r["start_ns"])
         spans[(r["phase"], r["span"])].append(d)
         key = (r["phase"], int(r["task_layer"]), int(r["task_block"]))
-        if r["span"] == "epilogue":
+        if r["span"] == "publish":
             by_step[key][1] = max(by_step[key][1], int(r["end_ns"]))
         if r["span"] == "wait":
             by_step[key][0] = min(by_step[key][0], int(r["start_ns"]))
