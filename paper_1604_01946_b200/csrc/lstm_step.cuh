@@ -153,19 +153,26 @@ __device__ __forceinline__ float act_tanh(float x) {
 // error instead of hanging the device. `code` identifies the wait for the host message.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
                                           const RecParams& p, int code) {
-  for (int i = 0; i < 4096; ++i)
-    if (ld_acquire_gpu(flag) >= target) return;
-  const uint64_t t0 = globaltimer();
-  uint32_t ns = 32;
-  while (ld_acquire_gpu(flag) < target) {
-    nanosleep(ns);
-    if (ns < 128) ns <<= 1;
-    if (globaltimer() - t0 > p.timeout_ns) {
-      atomicCAS(p.error, 0, code);
-      atomicMax(p.error + 1, (int)ld_acquire_gpu(flag));
-      return;
+  // Poll with relaxed loads (an acquire load per iteration would invalidate the SM's L1 each
+  // time, CCTL.IVALL, slowing every other warp on the SM); one acquire once satisfied.
+  bool ok = false;
+#pragma unroll 1
+  for (int i = 0; i < 2048 && !ok; ++i) ok = ld_relaxed_gpu(flag) >= target;
+  if (!ok) {
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 32;
+#pragma unroll 1
+    while (ld_relaxed_gpu(flag) < target) {
+      nanosleep(ns);
+      if (ns < 128) ns <<= 1;
+      if (globaltimer() - t0 > p.timeout_ns) {
+        atomicCAS(p.error, 0, code);
+        atomicMax(p.error + 1, (int)ld_relaxed_gpu(flag));
+        return;
+      }
     }
   }
+  (void)ld_acquire_gpu(flag);
 }
 // error code: 1<<30 | dir<<28 | layer<<20 | (t+2)<<4 | which
 __device__ __forceinline__ int wait_code(int dir, int l, int t, int which) {
@@ -184,6 +191,7 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t ph
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+#pragma unroll 1
   while (!mbar_try_wait_cluster(bar, phase)) {
   }
 }

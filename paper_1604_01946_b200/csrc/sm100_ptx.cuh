@@ -66,6 +66,7 @@ RW_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   return ok != 0;
 }
 RW_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
+#pragma unroll 1
   while (!mbar_try_wait(bar, phase)) {
   }
 }
@@ -209,6 +210,13 @@ RW_DEVICE float4 ld_dsmem_f32x4(uint32_t cluster_saddr) {
 RW_DEVICE uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Relaxed gpu-scope load: observes other SMs' writes (bypasses L1) without the L1
+// invalidation (CCTL.IVALL) an acquire load carries -- for spin loops.
+RW_DEVICE uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 RW_DEVICE void red_release_gpu_add(uint32_t* p, uint32_t v) {
