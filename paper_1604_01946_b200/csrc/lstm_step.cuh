@@ -204,6 +204,15 @@ __device__ __forceinline__ void st_dsmem_f32(uint32_t cluster_addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v));
 }
 
+__device__ __forceinline__ float lds_f32(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(float* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
+}
+
 // Sum of `n` TMEM accumulators (N columns apart) for 8 columns of this thread's lane, in fp32
 // with round-to-nearest adds (n == 0 -> zeros: no k-block of this CTA was active).
 __device__ __forceinline__ void load_acc_sum(uint32_t taddr, int N, int n, float (&a)[8]) {
@@ -277,7 +286,7 @@ __device__ __forceinline__ void xchg_push8(const RecSmem& s, int ks, int rank, i
     const int owner = c / nco;
     float* dst = s.xr + ((rank * nco) + (c - owner * nco)) * kTileM + row;
     if (owner == rank)
-      *dst = a[j];
+      sts_f32(dst, a[j]);
     else
       st_dsmem_f32(map_dsmem(smem_u32(dst), owner), a[j]);
   }
@@ -300,8 +309,8 @@ __device__ __forceinline__ void xchg_release(const RecSmem& s, int ks) {
 }
 // Reduced accumulator value of owned column cl, row `row` (fixed rank order).
 __device__ __forceinline__ float xchg_sum(const RecSmem& s, int ks, int nco, int cl, int row) {
-  float acc = s.xr[cl * kTileM + row];
-  for (int r = 1; r < ks; ++r) acc += s.xr[(r * nco + cl) * kTileM + row];
+  float acc = lds_f32(s.xr + cl * kTileM + row);
+  for (int r = 1; r < ks; ++r) acc += lds_f32(s.xr + (r * nco + cl) * kTileM + row);
   return acc;
 }
 
@@ -364,7 +373,15 @@ template <class P>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_fwd(const FwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
-  const FwdLayer& Ly = layers[l];
+  // The descriptor is read after every barrier; keep it in shared memory (global reloads
+  // would go to L2 because cluster/gpu-scope acquires invalidate L1).
+  __shared__ FwdLayer Ly;
+  __shared__ const uint32_t* x_flags;
+  if (threadIdx.x == 0) {
+    Ly = layers[l];
+    x_flags = l > 0 ? layers[l - 1].flags : nullptr;
+  }
+  __syncthreads();
   const int ks = p.ksplit;
   const int rank = (int)(blockIdx.x % ks);
   const int tile = (int)(blockIdx.x / ks);
@@ -414,7 +431,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (p.persistent) {
           if (seg0 && !x_ready) {
             progress(p, 0, it, 2);
-            if (l > 0) wait_flag(&layers[l - 1].flags[t], p.flag_target, p, wait_code(0, l, t, 1));
+            if (l > 0) wait_flag(&x_flags[t], p.flag_target, p, wait_code(0, l, t, 1));
             fence_proxy_async_global();
             x_ready = true;
           }
@@ -568,7 +585,13 @@ template <class P>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_bwd(const BwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
-  const BwdLayer& Ly = layers[l];
+  __shared__ BwdLayer Ly;
+  __shared__ const uint32_t* up_flags;
+  if (threadIdx.x == 0) {
+    Ly = layers[l];
+    up_flags = Ly.has_up ? layers[l + 1].flags : nullptr;
+  }
+  __syncthreads();
   const int ks = p.ksplit;
   const int rank = (int)(blockIdx.x % ks);
   const int tile = (int)(blockIdx.x / ks);
@@ -626,7 +649,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (p.persistent) {
           if (seg0 && !up_ready) {
             progress(p, 0, it, 2);
-            wait_flag(&layers[l + 1].flags[t], p.flag_target, p, wait_code(1, l, t, 1));
+            wait_flag(&up_flags[t], p.flag_target, p, wait_code(1, l, t, 1));
             fence_proxy_async_global();
             up_ready = true;
           }
