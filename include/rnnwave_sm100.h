@@ -162,6 +162,10 @@ int rw_test_gemm(int precision, int a_mn_major, int b_mn_major, int M, int N, in
                  const float* dA, long long lda, const float* dB, long long ldb, float* dD,
                  long long ldd, int bn);
 
+/* Average device time (ms) of the last rw_test_gemm call's GEMM kernel; with the environment
+ * variable RW_TEST_GEMM_REPS=n the kernel is repeated n times after one warm-up. */
+float rw_test_gemm_last_ms(void);
+
 #ifdef __cplusplus
 }
 #endif

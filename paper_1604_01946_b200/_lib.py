@@ -23,7 +23,7 @@ EXPORTS = [
     "rw_backward_data", "rw_weight_update", "rw_get_tape", "rw_upload_inputs", "rw_run_pass",
     "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count",
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_flop_count_cell",
-    "rw_test_gemm",
+    "rw_test_gemm", "rw_test_gemm_last_ms",
 ]
 
 
@@ -81,5 +81,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_flop_count_cell.restype = C.c_int64
     L.rw_test_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                                C.c_longlong, vp, C.c_longlong, vp, C.c_longlong, C.c_int]
+    L.rw_test_gemm_last_ms.argtypes = []
+    L.rw_test_gemm_last_ms.restype = C.c_float
     _lib = L
     return L

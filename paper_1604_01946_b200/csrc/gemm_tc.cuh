@@ -62,10 +62,40 @@ __device__ __forceinline__ long long gemm_out_col(const GemmDesc& g, int n) {
 // every chunk into fp32 registers (round-to-nearest adds). The tensor core's accumulation
 // of long K chains loses ~K*2^-24 (measured 5e-5 at K = 6400); chunking bounds that to the
 // chunk length while the next chunk's MMAs run into the other buffer.
+// Output column iterator (no per-element division): yields the destination column of
+// n0, n0+1, ... or -1 for padding columns.
+struct ColCursor {
+  int unpad, Bp, B, n_valid, b;
+  long long t_base, n;
+  __device__ __forceinline__ ColCursor(const GemmDesc& g, int n0)
+      : unpad(g.col_mode == kColBatchUnpad), Bp(g.Bp), B(g.B), n_valid(g.n_valid), n(n0) {
+    const int t = unpad ? n0 / g.Bp : 0;
+    b = unpad ? n0 - t * g.Bp : 0;
+    t_base = (long long)t * g.B;
+  }
+  __device__ __forceinline__ long long next() {
+    long long r;
+    if (unpad) {
+      r = b < B ? t_base + b : -1;
+      if (++b == Bp) {
+        b = 0;
+        t_base += B;
+      }
+    } else {
+      r = n < n_valid ? n : -1;
+      ++n;
+    }
+    return r;
+  }
+};
+
 template <class P, bool kAMN, bool kBMN, int kChunkBN>
 __global__ void __launch_bounds__(256, 1)
     k_gemm_tc(const GemmDesc* __restrict__ table, int bn, int stages, int chunk_kb) {
-  const GemmDesc& g = table[blockIdx.z];
+  // descriptor in shared memory: the epilogue reads it per element
+  __shared__ GemmDesc g;
+  if (threadIdx.x == 0) g = table[blockIdx.z];
+  __syncthreads();
   const int m0 = blockIdx.x * kTileM;
   const int n0 = blockIdx.y * bn;
   if (m0 >= g.M || n0 >= g.N) return;
@@ -190,19 +220,27 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&tmem_empty[buf]);
       }
       if (orow >= 0) {
+        ColCursor cc(g, n0);
+        float* const drow = g.d + orow;
+        const long long ldd = g.ldd;
+        const bool accum_out = g.accumulate != 0;
 #pragma unroll
         for (int j = 0; j < kChunkBN; ++j) {
-          const int n = n0 + j;
-          if (n >= g.N) break;
-          const long long oc = gemm_out_col(g, n);
+          if (n0 + j >= g.N) break;
+          const long long oc = cc.next();
           if (oc < 0) continue;
-          float* dst = g.d + oc * g.ldd + orow;
-          *dst = g.accumulate ? *dst + accum[j] : accum[j];
+          float* dst = drow + oc * ldd;
+          *dst = accum_out ? *dst + accum[j] : accum[j];
         }
       }
     } else {
       mbar_wait(&tmem_full[0], 0);
       tc_fence_after();
+      ColCursor cc(g, n0);
+      float* const drow = g.d + (orow < 0 ? 0 : orow);
+      const long long ldd = g.ldd;
+      const bool accum_out = g.accumulate != 0;
+      const int nlim = min(bn, g.N - n0);
       for (int c0 = 0; c0 < bn; c0 += 8) {
         uint32_t v[8];
         tmem_ld_32x32b_x8(tmem_base + lane_off + c0, v);
@@ -210,13 +248,12 @@ __global__ void __launch_bounds__(256, 1)
         if (orow < 0) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int n = n0 + c0 + j;
-          if (n >= g.N) break;
-          const long long oc = gemm_out_col(g, n);
+          if (c0 + j >= nlim) break;
+          const long long oc = cc.next();
           if (oc < 0) continue;
-          float* dst = g.d + oc * g.ldd + orow;
+          float* dst = drow + oc * ldd;
           const float val = __uint_as_float(v[j]);
-          *dst = g.accumulate ? *dst + val : val;
+          *dst = accum_out ? *dst + val : val;
         }
       }
     }

@@ -155,9 +155,12 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
                                           const RecParams& p, int code) {
   // Poll with relaxed loads (an acquire load per iteration would invalidate the SM's L1 each
   // time, CCTL.IVALL, slowing every other warp on the SM); one acquire once satisfied.
-  bool ok = false;
+  bool ok = ld_relaxed_gpu(flag) >= target;
 #pragma unroll 1
-  for (int i = 0; i < 2048 && !ok; ++i) ok = ld_relaxed_gpu(flag) >= target;
+  for (int i = 0; i < 4096 && !ok; ++i) {
+    nanosleep(20);
+    ok = ld_relaxed_gpu(flag) >= target;
+  }
   if (!ok) {
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
@@ -183,10 +186,10 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t ph
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(kSuspendHintNs)
       : "memory");
   return ok != 0;
 }
@@ -277,13 +280,14 @@ __device__ __forceinline__ void xchg_wait_free(const RecSmem& s, int ks, uint32_
   if (ks > 1 && xc > 0) mbar_wait_cluster(s.xfree, (xc - 1) & 1);
 }
 // Thread (quarter q, lane) pushes the 8 columns c0..c0+7 of its accumulator row.
+// inv = ceil(2^16 / nco): (c * inv) >> 16 == c / nco exactly for c < 64 (no integer divide).
 __device__ __forceinline__ void xchg_push8(const RecSmem& s, int ks, int rank, int nco, int q,
-                                           int lane, int c0, const float (&a)[8]) {
+                                           int lane, int c0, const float (&a)[8], uint32_t inv) {
   const int row = q * 32 + lane;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int c = c0 + j;
-    const int owner = c / nco;
+    const int owner = (int)((uint32_t(c) * inv) >> 16);
     float* dst = s.xr + ((rank * nco) + (c - owner * nco)) * kTileM + row;
     if (owner == rank)
       sts_f32(dst, a[j]);
@@ -508,11 +512,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
         const int nco = nc / ks;  // columns of this chunk owned by each rank
+        const uint32_t inv = (65536u + nco - 1) / nco;
         xchg_wait_free(S, ks, xc);
         for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
-          xchg_push8(S, ks, rank, nco, q, lane, c0, a);
+          xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();
@@ -729,11 +734,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
         const int nco = nc / ks;
+        const uint32_t inv = (65536u + nco - 1) / nco;
         xchg_wait_free(S, ks, xc);
         for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
-          xchg_push8(S, ks, rank, nco, q, lane, c0, a);
+          xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();

@@ -1396,6 +1396,9 @@ int rw_describe(rw_ctx* x, int* fs, int* bs, int* kf, int* kb) {
   });
 }
 
+static float g_test_gemm_ms = 0.0f;
+float rw_test_gemm_last_ms(void) { return g_test_gemm_ms; }
+
 int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const float* dA,
                  long long lda, const float* dB, long long ldb, float* dD, long long ldd, int bn) {
   return guarded(nullptr, [&] {
@@ -1445,6 +1448,13 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     const GemmDesc* G = static_cast<const GemmDesc*>(gd.p);
     const int planes = prec == kBF16 ? 1 : 2;
     const int st = gemm_stages(planes, bn);
+    const char* reps_env = getenv("RW_TEST_GEMM_REPS");
+    const int reps = reps_env ? std::max(1, atoi(reps_env)) : 1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int rep = 0; rep <= reps; ++rep) {
+    if (rep == 1) cudaEventRecord(e0, 0);
     if (prec == kBF16) {
       if (!a_mn && !b_mn) launch_gemm<PrecBF16, false, false>(G, 1, M, N, bn, st, 0);
       if (!a_mn && b_mn) launch_gemm<PrecBF16, false, true>(G, 1, M, N, bn, st, 0);
@@ -1456,7 +1466,13 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
       if (a_mn && !b_mn) launch_gemm<PrecTF32x3, true, false>(G, 1, M, N, bn, st, 0);
       if (a_mn && b_mn) launch_gemm<PrecTF32x3, true, true>(G, 1, M, N, bn, st, 0);
     }
+    }
+    cudaEventRecord(e1, 0);
     RW_CUDA(cudaDeviceSynchronize());
+    cudaEventElapsedTime(&g_test_gemm_ms, e0, e1);
+    g_test_gemm_ms /= reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 

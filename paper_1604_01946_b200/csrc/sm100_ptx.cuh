@@ -40,6 +40,10 @@ RW_DEVICE uint64_t globaltimer() {
 }
 
 // ------------------------------------------------------------------ mbarrier
+// try_wait suspend-time hint (the waiting thread sleeps in hardware until the phase completes
+// or this many ns pass); keeps waiting warps from spinning on issue slots the working warps
+// of the SM need. Same order of magnitude as CUTLASS's barrier wait.
+constexpr uint32_t kSuspendHintNs = 10000000;
 RW_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -58,10 +62,10 @@ RW_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(kSuspendHintNs)
       : "memory");
   return ok != 0;
 }
