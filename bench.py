@@ -29,6 +29,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG_B = dict(layers=4, hidden=512, input=512, batch=64, steps=100)
+# BASELINE.json configs by SURVEY §8(d) letter; only B is the bench line, the others are sweep /
+# parity cases (--config for the profiles/ sweep tables).
+CONFIGS = {
+    "A": dict(layers=1, hidden=512, input=512, batch=64, steps=100),
+    "B": CONFIG_B,
+    "C128": dict(layers=4, hidden=128, input=128, batch=64, steps=100),
+    "C256": dict(layers=4, hidden=256, input=256, batch=64, steps=100),
+    "C1024": dict(layers=4, hidden=1024, input=1024, batch=64, steps=100),
+    "C2048": dict(layers=4, hidden=2048, input=2048, batch=64, steps=100),
+    "D1": dict(layers=1, hidden=1024, input=1024, batch=16, steps=200),
+    "D4": dict(layers=4, hidden=1024, input=1024, batch=16, steps=200),
+    "E": dict(layers=8, hidden=2048, input=2048, batch=256, steps=100),
+}
 METRIC = "LSTM fwd+bwd TFLOPS (h=512, mb=64, 4 layers, T=100) and % of B200 TC peak"
 
 
@@ -142,7 +155,7 @@ def run_ours(args) -> None:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    c = dict(CONFIG_B)
+    c = dict(CONFIGS[args.config])
     cfg = LadderConfig(**c, seed=42 + rank, opt_level=6, batch_steps=2, workers=1)
     eng = Engine(cfg, precision=args.precision, schedule=args.schedule, device=local)
     params = init_params(LadderConfig(**c, seed=42))
@@ -264,7 +277,7 @@ def run_ours(args) -> None:
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", 1590.0)
     cpu_base = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and args.config == "B":
         cpu_base = cpu_baseline()
     value = flops * world / (ms * 1e-3) / 1e12
     line = {
@@ -280,8 +293,8 @@ def run_ours(args) -> None:
         "vs_baseline": None,
         "dtype": "bf16" if args.precision == "bf16" else "tf32x3 (fp32-parity)",
         "data": "synthetic (SplitMix64 seed 42 weights, streams 1000/1001 inputs: the reference generators)",
-        "config": {"workload": "4L h512 mb64 T100 LSTM fwd+bwd (BASELINE configs[1])",
-                   "model": "lstm-4x512", "global_batch": c["batch"] * world, "seq_len": T,
+        "config": {"workload": workload_name(args.config, c),
+                   "model": f"lstm-{c['layers']}x{c['hidden']}", "global_batch": c["batch"] * world, "seq_len": T,
                    "parallelism": f"dp{world}" if world > 1 else "single",
                    "precision": args.precision, "schedule": desc,
                    "l2": "flushed (256 MiB write) between timed steps",
@@ -299,6 +312,11 @@ def run_ours(args) -> None:
         "cpu_baseline": cpu_base,
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_name(key: str, c: dict) -> str:
+    base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM fwd+bwd"
+    return base + (" (BASELINE configs[1])" if key == "B" else f" (sweep config {key})")
 
 
 def cpu_baseline() -> dict | None:
@@ -326,8 +344,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
+                    help="SURVEY §8(d) config; B (the headline) unless sweeping")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

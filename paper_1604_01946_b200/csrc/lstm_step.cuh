@@ -151,16 +151,13 @@ __device__ __forceinline__ float act_tanh(float x) {
 
 // Spin until *flag >= target (gpu-scope acquire), bounded by a timeout that records an
 // error instead of hanging the device. `code` identifies the wait for the host message.
-__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
-                                          const RecParams& p, int code) {
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target, int* error,
+                                          unsigned long long timeout_ns, int code) {
   // Poll with relaxed loads (an acquire load per iteration would invalidate the SM's L1 each
   // time, CCTL.IVALL, slowing every other warp on the SM); one acquire once satisfied.
   bool ok = ld_relaxed_gpu(flag) >= target;
 #pragma unroll 1
-  for (int i = 0; i < 4096 && !ok; ++i) {
-    nanosleep(20);
-    ok = ld_relaxed_gpu(flag) >= target;
-  }
+  for (int i = 0; i < 65536 && !ok; ++i) ok = ld_relaxed_gpu(flag) >= target;
   if (!ok) {
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
@@ -168,14 +165,18 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
     while (ld_relaxed_gpu(flag) < target) {
       nanosleep(ns);
       if (ns < 128) ns <<= 1;
-      if (globaltimer() - t0 > p.timeout_ns) {
-        atomicCAS(p.error, 0, code);
-        atomicMax(p.error + 1, (int)ld_relaxed_gpu(flag));
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicCAS(error, 0, code);
+        atomicMax(error + 1, (int)ld_relaxed_gpu(flag));
         return;
       }
     }
   }
   (void)ld_acquire_gpu(flag);
+}
+__device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
+                                          const RecParams& p, int code) {
+  wait_flag(flag, target, p.error, p.timeout_ns, code);
 }
 // error code: 1<<30 | dir<<28 | layer<<20 | (t+2)<<4 | which
 __device__ __forceinline__ int wait_code(int dir, int l, int t, int which) {

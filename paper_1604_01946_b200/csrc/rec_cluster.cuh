@@ -1,0 +1,811 @@
+// rec_cluster.cuh -- persistent recurrent kernels with split roles per tile ("cluster"
+// schedule). bf16 operands, fp32 accumulation and cell math.
+//
+// Why: in a persistent wavefront the per-step critical path bounds small-H configs (config B:
+// 206 dependent steps). Measured on B200 (profiles/ubench/sync_ubench.cu): a gpu-scope flag
+// round trip costs ~1.7 us and a 16-CTA flag barrier ~1.4 us, while DSMEM bulk copies
+// (cp.async.bulk shared::cta -> shared::cluster, completion by complete_tx on the receiver's
+// mbarrier) move a 16-32 KB exchange in ~0.7-1.1 us with no separate handshake. So everything
+// that does not depend on the recurrence is taken off the critical path, and the exchange that
+// remains inside a tile uses bulk DSMEM copies.
+//
+// Per tile (forward: 32 units x 4 gates = 128 rho-rows; backward: 128 units) two clusters of
+// cs CTAs ("members") split the K range of the step's GEMM, each member keeping its
+// 128 x <=512 bf16 weight slice resident in shared memory (loaded once by TMA):
+//   * the CRITICAL cluster (kc active members) multiplies the recurrent operand
+//       forward : R_l . h_{l,t-1}                 (engine.hpp:368-387)
+//       backward: R_l^T . dG_{l,t+1}              (recurrent_backward_gemm, engine.hpp:538-560)
+//   * the OFF cluster (ko active members) multiplies the operand from the neighbouring layer
+//       forward : W_l . x_{l,t}   (x = h_{l-1,t})  (input_gemm, engine.hpp:347-365)
+//       backward: W_{l+1}^T . dG_{l+1,t}          (output_gemm, engine.hpp:564-585)
+//     which does not wait for this layer's previous step, so it runs ahead (up to kRing steps).
+// Inside a cluster each member drains its TMEM accumulator (128 rows x Bp, fp32) into a
+// staging buffer [owner][column][row] and pushes each owner's block with one bulk copy into
+// the owner's receive slot; owners sum in fixed member order (deterministic). The off cluster
+// writes its reduced partial to a global ring (offsum) and publishes a per-(layer, tile, step)
+// counter; the critical producer prefetches it with a bulk copy as soon as it is published.
+// Critical owners then form (x-part + h-part) + bias (forward, cells.hpp:240) or
+// d_above + carry_h (backward, cells.hpp:424), run the LSTM cell on their columns, publish the
+// bf16 operand (h_t / dG_t) with a gpu-scope release counter per (layer, step), and only then
+// write the fp32 tapes (h, c, gates, tanh(c) / dG), which nothing in the pass waits for.
+// Cell state (c forward; carry_c and the bias-gradient sums backward) stays in registers.
+//
+// Threads: 384 = warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM allocator, warp 3 idle,
+// warps 4..11 epilogue (warp w and w+4 share TMEM lane quarter w%4, split the columns).
+#pragma once
+
+#include "lstm_step.cuh"
+
+namespace rw {
+
+constexpr int kClKBlocks = 8;  // k-blocks (64 bf16) per member: 128 x 512 x 2 B = 128 KB resident
+constexpr int kClMaxN = 64;    // batch columns (Bp) this path supports
+constexpr int kRing = 4;       // off-partial ring depth (steps the off cluster may run ahead)
+
+struct ClParams {
+  int L, H, Hp, B, Bp, T;
+  int tiles;     // tiles per layer
+  int kc;        // active critical members per tile
+  int cs;        // cluster size = max(kc, ko over layers)
+  int ncomax;    // Bp / min(kc, min_l ko_l): receive-slot size (columns) of the carve-up
+  int stages;    // B-operand TMA stages
+  uint32_t flag_target;  // per-(layer, step) publications: tiles * kc
+  float* offsum;         // [L][tiles][kRing][Bp][128] reduced off partials
+  uint32_t* off_done;    // [L][tiles][T] publications by the off cluster (target ko_l)
+  uint32_t* consumed;    // [L][tiles][32] (one counter per 128 B): ring slots read by critical members
+  int* error;
+  unsigned long long timeout_ns;
+  unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
+  int trace_steps;
+};
+
+// Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
+// mapa names the same buffer in a peer).
+struct ClSmem {
+  uint8_t* a;     // resident A: kClKBlocks x 128 rows x 128 B
+  uint8_t* b;     // stages x Bp x 128 B   (forward critical: also the [nco][128] sum buffer)
+  float* rx;      // receive slots [cs-1][ncomax][128]
+  float* rxoff;   // critical: the off partial of the owned columns [ncomax][128]
+  float* st;      // staging [cs-1][ncomax][128] of pushes to peers
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* a_full;
+  uint64_t* tmem_full;   // [2]
+  uint64_t* tmem_empty;  // [2]
+  uint64_t* rx_full;     // peers' partials for this step arrived
+  uint64_t* push_free;   // every owner consumed this member's previous push
+  uint64_t* off_full;    // critical: off partial landed in rxoff
+  uint64_t* off_empty;   // critical: epilogue finished reading rxoff
+  uint32_t* tmem_slot;
+};
+
+__host__ __device__ inline size_t cl_slot_bytes(int ncomax) { return (size_t)ncomax * 128 * 4; }
+__host__ __device__ inline size_t cl_smem_bytes(int cs, int ncomax, int N, int stages) {
+  return 1024 + (size_t)kClKBlocks * kTileM * kRowBytes + (size_t)stages * N * kRowBytes +
+         (2 * (size_t)(cs - 1) + 1) * cl_slot_bytes(ncomax) + (2 * stages + 12) * 8 + 16;
+}
+
+__device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
+  ClSmem s;
+  const size_t slot = cl_slot_bytes(p.ncomax);
+  s.a = smem;
+  s.b = s.a + kClKBlocks * kTileM * kRowBytes;
+  s.rx = reinterpret_cast<float*>(s.b + p.stages * p.Bp * kRowBytes);
+  s.rxoff = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rx) + (p.cs - 1) * slot);
+  s.st = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rxoff) + slot);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.st) + (p.cs - 1) * slot);
+  s.full = bars;
+  s.empty = bars + p.stages;
+  s.a_full = bars + 2 * p.stages;
+  s.tmem_full = s.a_full + 1;
+  s.tmem_empty = s.a_full + 3;
+  s.rx_full = s.a_full + 5;
+  s.push_free = s.a_full + 6;
+  s.off_full = s.a_full + 7;
+  s.off_empty = s.a_full + 8;
+  s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 9);
+  return s;
+}
+
+__device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
+  if (p.trace) {
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
+    p.trace[((unsigned long long)cta * p.trace_steps + it) * 8 + what] = globaltimer();
+  }
+}
+
+// Bulk copy of `bytes` from local smem to the same-offset buffer of cluster rank `dst_rank`,
+// completing `bytes` of transaction count on that rank's mbarrier `bar` (local address).
+__device__ __forceinline__ void bulk_push(const void* dst_local, const void* src, uint32_t bytes,
+                                          uint64_t* bar_local, uint32_t dst_rank) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          map_dsmem(smem_u32(dst_local), dst_rank)),
+      "r"(smem_u32(src)), "r"(bytes), "r"(map_dsmem(smem_u32(bar_local), dst_rank))
+      : "memory");
+}
+// Bulk copy global -> local smem, completion on a local mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Receive slot of sender s at owner d (senders = every member but d, in member order).
+__device__ __forceinline__ int cl_slot(int s, int d) { return s < d ? s : s - 1; }
+
+// Load 8 accumulator columns of this thread's TMEM lane, or zeros if nothing was accumulated.
+__device__ __forceinline__ void cl_ld8(uint32_t taddr, bool have, float (&v)[8]) {
+  if (have) {
+    uint32_t r[8];
+    tmem_ld_32x32b_x8(taddr, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.0f;
+  }
+}
+
+// Common prologue: barriers, TMEM allocation (2 accumulators of N columns), cluster rendezvous.
+__device__ __forceinline__ uint32_t cl_setup(const ClSmem& S, const ClParams& p, uint32_t tmem_cols,
+                                             int n_act) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    mbar_init(S.a_full, 1);
+    mbar_init(&S.tmem_full[0], 1);
+    mbar_init(&S.tmem_full[1], 1);
+    mbar_init(&S.tmem_empty[0], kEpiThreads);
+    mbar_init(&S.tmem_empty[1], kEpiThreads);
+    mbar_init(S.rx_full, 1);
+    mbar_init(S.push_free, n_act > 1 ? n_act - 1 : 1);
+    mbar_init(S.off_full, 1);
+    mbar_init(S.off_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(S.tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peers' barriers initialised before any remote copy / arrive
+  tc_fence_after();
+  return *S.tmem_slot;
+}
+
+__device__ __forceinline__ void cl_teardown(uint32_t tmem_base, uint32_t tmem_cols) {
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while peers may still copy into its shared memory
+  if ((threadIdx.x >> 5) == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+  }
+}
+
+__device__ __forceinline__ void cl_load_a(const ClSmem& S, const CUtensorMap* a, int kb_lo, int kb_hi,
+                                          int row0) {
+  const int a_bytes = kTileM * kRowBytes;
+  mbar_arrive_expect_tx(S.a_full, (kb_hi - kb_lo) * a_bytes);
+  for (int kb = kb_lo; kb < kb_hi; ++kb)
+    tma_load_2d(S.a + (kb - kb_lo) * a_bytes, a, S.a_full, kb * 64, row0);
+}
+
+__device__ __forceinline__ void cl_mma_step(const ClSmem& S, uint32_t acc, int nkb, uint32_t idesc,
+                                            uint32_t& pc, int stages, int N) {
+  const int a_bytes = kTileM * kRowBytes, b_bytes = N * kRowBytes;
+  for (int k = 0; k < nkb; ++k, ++pc) {
+    const int s = pc % stages;
+    mbar_wait(&S.full[s], (pc / stages) & 1);
+    tc_fence_after();
+    mma_kblock<PrecBF16>(acc, smem_u32(S.a + k * a_bytes), smem_u32(S.b + s * b_bytes), a_bytes, b_bytes,
+                         idesc, k == 0);
+    umma_commit(&S.empty[s]);
+  }
+}
+
+// Producer: stream the k-blocks [kb_lo, kb_hi) of one step's B operand (map m, K offset
+// k0 - kb_lo*64, column col) through the stage ring.
+__device__ __forceinline__ void cl_load_b(const ClSmem& S, const CUtensorMap* m, int kb_lo, int kb_hi, int kofs,
+                                          int col, uint32_t& pc, int stages, int N) {
+  const int b_bytes = N * kRowBytes;
+  for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
+    const int s = pc % stages;
+    mbar_wait(&S.empty[s], ((pc / stages) & 1) ^ 1);
+    mbar_arrive_expect_tx(&S.full[s], b_bytes);
+    tma_load_2d(S.b + s * b_bytes, m, &S.full[s], (kb - kofs) * 64, col);
+  }
+}
+
+// Cluster-local split-K reduction of one step: push the columns owned by the other n_act-1
+// members, wait for theirs, and return this thread's owned columns summed in member order.
+// Thread (quarter q, lane) owns accumulator row q*32+lane; `half` picks its half of the owned
+// columns. v_out[i*8 + j] = owned column half*nco/2 + i*8 + j.
+template <int kChunks>
+__device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, int it, int m, int n_act,
+                                          int nco, uint32_t& rxc, float (&v_out)[kChunks * 8]) {
+  const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
+  const uint32_t taddr = tacc + (uint32_t(q * 32) << 16);
+  if (n_act > 1) {
+    if (it > 0) mbar_wait_cluster(S.push_free, (it - 1) & 1);  // owners consumed the previous push
+    for (int d = 0; d < n_act; ++d) {
+      if (d == m) continue;
+      float* blk = S.st + (size_t)cl_slot(d, m) * nco * kTileM;
+      for (int c0 = half * (nco >> 1); c0 < (half + 1) * (nco >> 1); c0 += 8) {
+        float v[8];
+        cl_ld8(taddr + d * nco + c0, have, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sts_f32(blk + (size_t)(c0 + j) * kTileM + row, v[j]);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, kEpiThreads);
+    if (et == 0) {
+      for (int d = 0; d < n_act; ++d) {
+        if (d == m) continue;
+        bulk_push(S.rx + (size_t)cl_slot(m, d) * nco * kTileM, S.st + (size_t)cl_slot(d, m) * nco * kTileM,
+                  (uint32_t)(nco * kTileM * 4), S.rx_full, (uint32_t)d);
+      }
+    }
+  }
+  const int own0 = m * nco;
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    float v[8];
+    cl_ld8(taddr + own0 + half * (nco >> 1) + i * 8, have, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = v[j];
+  }
+  tc_fence_before();
+  mbar_arrive(&S.tmem_empty[it & 1]);
+  if (n_act > 1) {
+    mbar_wait_cluster(S.rx_full, rxc & 1);
+    ++rxc;
+#pragma unroll
+    for (int i = 0; i < kChunks; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int cl = half * (nco >> 1) + i * 8 + j;
+        float acc = 0.0f;
+        for (int s = 0; s < n_act; ++s)
+          acc += s == m ? v_out[i * 8 + j] : lds_f32(S.rx + ((size_t)cl_slot(s, m) * nco + cl) * kTileM + row);
+        v_out[i * 8 + j] = acc;
+      }
+    }
+  }
+}
+
+// After every epilogue thread of the owner read the receive slots (named barrier): re-arm for
+// the next step and release the slots to the senders (one thread).
+__device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, int nco) {
+  if (n_act > 1) {
+    mbar_arrive_expect_tx(S.rx_full, (uint32_t)(n_act - 1) * nco * kTileM * 4);
+    for (int s = 0; s < n_act; ++s)
+      if (s != m) mbar_arrive_remote(S.push_free, (uint32_t)s);
+  }
+}
+
+// Off cluster epilogue of one step: reduce, then store the owned columns of the reduced partial
+// into ring slot it % kRing ([Bp][128] fp32) and publish it.
+template <int kChunks>
+__device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, int it, int m,
+                                            int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
+                                            const uint32_t* consumed) {
+  const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
+  float v[kChunks * 8];
+  cl_reduce<kChunks>(S, tacc, true, it, m, n_act, nco, rxc, v);
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0) {
+    cl_rx_next(S, m, n_act, nco);
+    // ring slot free once every critical member copied step it - kRing
+    if (it >= kRing)
+      wait_flag(consumed, (uint32_t)(p.kc * (it - kRing + 1)), p.error, p.timeout_ns,
+                (1 << 30) | (3 << 28) | (blockIdx.y << 20) | ((it + 2) << 4));
+  }
+  if (it >= kRing) named_bar_sync(2, kEpiThreads);
+  float* slot = ring + (size_t)(it % kRing) * p.Bp * kTileM;
+  const int c0 = m * nco + half * (nco >> 1);
+#pragma unroll
+  for (int i = 0; i < kChunks * 8; ++i) slot[(size_t)(c0 + i) * kTileM + row] = v[i];
+  fence_proxy_async_global();
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0) {
+    __threadfence();
+    red_release_gpu_add(done + it, 1);
+  }
+}
+
+template <int kChunks>
+__device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, int n_it,
+                                            int m, int n_act, float* ring, uint32_t* done,
+                                            const uint32_t* consumed) {
+  const int et = threadIdx.x - kEpiBase, N = p.Bp, nco = N / n_act;
+  uint32_t rxc = 0;
+  if (et == 0 && n_act > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(n_act - 1) * nco * kTileM * 4);
+  for (int it = 0; it < n_it; ++it) {
+    mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
+    tc_fence_after();
+    if (et == 0) cl_trace(p, it, 2);
+    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * N, it, m, n_act, nco, rxc, ring, done, consumed);
+    if (et == 0) cl_trace(p, it, 3);
+  }
+}
+
+// Critical producer: prefetch the off partial of step `it` into rxoff (owned columns).
+__device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p, const float* ring,
+                                             const uint32_t* done, uint32_t target, int it, int m, int nco,
+                                             uint32_t& offc, int code) {
+  if (offc > 0) mbar_wait(S.off_empty, (offc - 1) & 1);
+  wait_flag(done + it, target, p.error, p.timeout_ns, code);
+  fence_proxy_async_global();
+  const uint32_t bytes = (uint32_t)(nco * kTileM * 4);
+  mbar_arrive_expect_tx(S.off_full, bytes);
+  bulk_load(S.rxoff, ring + ((size_t)(it % kRing) * p.Bp + (size_t)m * nco) * kTileM, bytes, S.off_full);
+  ++offc;
+}
+
+// ====================================================================== forward
+// grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
+// R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
+template <int kChunks>
+__device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, int t, int m, int kc, int nco,
+                                           uint32_t& rxc, uint32_t offc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
+  float v[kChunks * 8];
+  cl_reduce<kChunks>(S, tacc, true, t, m, kc, nco, rxc, v);
+  mbar_wait(S.off_full, offc & 1);
+  float* sum = reinterpret_cast<float*>(S.b);
+#pragma unroll
+  for (int i = 0; i < kChunks * 8; ++i) {
+    const int cl = half * kChunks * 8 + i;
+    const float zw = lds_f32(S.rxoff + (size_t)cl * kTileM + row);
+    sts_f32(sum + (size_t)cl * kTileM + row, zw + v[i]);  // (zw + zr), cells.hpp:240
+  }
+}
+
+__global__ void __launch_bounds__(kRecThreads, 1)
+    k_cl_fwd(const FwdLayer* __restrict__ layers, ClParams p) {
+  const int l = blockIdx.y;
+  __shared__ FwdLayer Ly;
+  __shared__ const uint32_t* x_flags;
+  if (threadIdx.x == 0) {
+    Ly = layers[l];
+    x_flags = l > 0 ? layers[l - 1].flags : nullptr;
+  }
+  __syncthreads();
+  const int cs = p.cs, kc = p.kc, N = p.Bp;
+  const int m = (int)(blockIdx.x % cs), cl_id = (int)(blockIdx.x / cs);
+  const int tile = cl_id >> 1;
+  const bool crit = (cl_id & 1) == 0;
+  const int nkb_x = Ly.Ipl / 64, nkb_h = p.Hp / 64;
+  const int ko = (nkb_x + kClKBlocks - 1) / kClKBlocks;
+  const int n_act = crit ? kc : ko;
+  const bool active = m < n_act;
+  int kb_lo = 0, kb_hi = 0;
+  if (active) {
+    if (crit) {
+      kb_lo = nkb_x + m * nkb_h / kc;
+      kb_hi = nkb_x + (m + 1) * nkb_h / kc;
+    } else {
+      kb_lo = m * nkb_x / ko;
+      kb_hi = (m + 1) * nkb_x / ko;
+    }
+  }
+  const int nkb = kb_hi - kb_lo;
+  const int nco = N / n_act;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const ClSmem S = cl_carve(smem, p);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)(2 * N)) tmem_cols <<= 1;
+  const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
+  const int row0 = tile * kTileM;
+  const size_t lt = (size_t)l * p.tiles + tile;
+  float* ring = p.offsum + lt * kRing * N * kTileM;
+  uint32_t* done = p.off_done + lt * p.T;
+  uint32_t* consumed = p.consumed + lt * 32;
+
+  if (active && warp == 0 && lane == 0) {
+    // ================= TMA producer
+    prefetch_tmap(Ly.a[0]);
+    prefetch_tmap(crit ? Ly.bh[0] : Ly.bx[0]);
+    cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
+    uint32_t pc = 0, offc = 0;
+    for (int t = 0; t < p.T; ++t) {
+      cl_trace(p, t, 0);
+      if (crit) {
+        // the off partial is usually published already: fetch it before waiting for h_{t-1}
+        const bool early = ld_relaxed_gpu(done + t) >= (uint32_t)ko;
+        if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, t, m, nco, offc, wait_code(0, l, t, 3));
+        if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
+        fence_proxy_async_global();
+        cl_trace(p, t, 1);
+        cl_load_b(S, Ly.bh[0], kb_lo, kb_hi, nkb_x, t * N, pc, p.stages, N);
+        if (!early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, t, m, nco, offc, wait_code(0, l, t, 3));
+      } else {
+        if (l > 0) wait_flag(&x_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
+        fence_proxy_async_global();
+        cl_trace(p, t, 1);
+        cl_load_b(S, Ly.bx[0], kb_lo, kb_hi, 0, Ly.bx_col_off + t * N, pc, p.stages, N);
+      }
+    }
+  } else if (active && warp == 1 && lane == 0) {
+    // ================= MMA issuer
+    const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
+    mbar_wait(S.a_full, 0);
+    tc_fence_after();
+    uint32_t pc = 0;
+    for (int t = 0; t < p.T; ++t) {
+      const int ab = t & 1;
+      if (t >= 2) {
+        mbar_wait(&S.tmem_empty[ab], ((t >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      cl_mma_step(S, tmem_base + ab * N, nkb, idesc, pc, p.stages, N);
+      umma_commit(&S.tmem_full[ab]);
+    }
+  } else if (active && warp >= 4) {
+    const int et = threadIdx.x - kEpiBase;
+    if (!crit) {
+      switch (nco >> 4) {
+        case 4: cl_off_loop<4>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
+        default: cl_off_loop<1>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
+      }
+    } else {
+      // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
+      const int j = et & 31, cg = et >> 5;  // cell phase: unit j of the tile, column group cg
+      const int u = tile * kUnitsPerFwdTile + j;
+      const long long Hp = p.Hp, G4 = 4 * Hp;
+      const int own0 = m * nco;
+      const float bi = Ly.bias[u], bf = Ly.bias[Hp + u], bo = Ly.bias[2 * Hp + u], bc = Ly.bias[3 * Hp + u];
+      float creg[kClMaxN / 8];  // c_{t-1} of owned columns cl = cg + 8k (c tape block 0 = c0)
+#pragma unroll
+      for (int k = 0; k < kClMaxN / 8; ++k) {
+        const int cl = cg + 8 * k;
+        creg[k] = cl < nco ? Ly.c[(long long)(own0 + cl) * Hp + u] : 0.0f;
+      }
+      const float* sum = reinterpret_cast<const float*>(S.b);
+      uint32_t rxc = 0;
+      if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
+      for (int t = 0; t < p.T; ++t) {
+        mbar_wait(&S.tmem_full[t & 1], (t >> 1) & 1);
+        tc_fence_after();
+        if (et == 0) cl_trace(p, t, 2);
+        const uint32_t tacc = tmem_base + (t & 1) * N;
+        switch (nco >> 4) {
+          case 4: cl_fwd_sum<4>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
+          case 3: cl_fwd_sum<3>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
+          case 2: cl_fwd_sum<2>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
+          default: cl_fwd_sum<1>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
+        }
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          cl_trace(p, t, 4);
+          mbar_arrive(S.off_empty);
+          red_release_gpu_add(consumed, 1);  // ring slot t copied into rxoff
+          cl_rx_next(S, m, kc, nco);
+        }
+        // cell phase, operand store first (the critical output)
+        float hv[kClMaxN / 8], cv[kClMaxN / 8], iv[kClMaxN / 8], fv[kClMaxN / 8], ov[kClMaxN / 8],
+            cb[kClMaxN / 8], tcv[kClMaxN / 8];
+        const long long colp = (long long)t * N + own0;  // block t (c_{t-1}), owned base
+#pragma unroll
+        for (int k = 0; k < kClMaxN / 8; ++k) {
+          const int cl = cg + 8 * k;
+          if (cl >= nco) break;
+          const float ai = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
+          const float af = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
+          const float ao = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j) + bo;
+          const float ac = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j) + bc;
+          iv[k] = act_sigmoid<PrecBF16>(ai);
+          fv[k] = act_sigmoid<PrecBF16>(af);
+          ov[k] = act_sigmoid<PrecBF16>(ao);
+          cb[k] = act_tanh<PrecBF16>(ac);
+          const float t1 = fv[k] * creg[k];
+          const float t2 = iv[k] * cb[k];
+          cv[k] = t1 + t2;
+          tcv[k] = act_tanh<PrecBF16>(cv[k]);
+          hv[k] = ov[k] * tcv[k];
+          creg[k] = cv[k];
+          static_cast<__nv_bfloat16*>(Ly.hop[0])[(colp + N + cl) * Hp + u] = __float2bfloat16_rn(hv[k]);
+        }
+        // publish h_t (all operand stores of this CTA, then one gpu-scope release)
+        fence_proxy_async_global();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          __threadfence();
+          red_release_gpu_add(&Ly.flags[t], 1);
+          cl_trace(p, t, 5);
+        }
+        // tapes (read only after the pass)
+#pragma unroll
+        for (int k = 0; k < kClMaxN / 8; ++k) {
+          const int cl = cg + 8 * k;
+          if (cl >= nco) break;
+          const long long col_prev = colp + cl, col_new = col_prev + N;
+          Ly.c[col_new * Hp + u] = cv[k];
+          Ly.h[col_new * Hp + u] = hv[k];
+          if (Ly.gates) {
+            float* gp = Ly.gates + col_prev * G4 + u;
+            gp[0] = iv[k];
+            gp[Hp] = fv[k];
+            gp[2 * Hp] = ov[k];
+            gp[3 * Hp] = cb[k];
+            Ly.tanhc[col_prev * Hp + u] = tcv[k];
+          }
+        }
+        if (et == 0) cl_trace(p, t, 6);
+      }
+    }
+  }
+  cl_teardown(tmem_base, tmem_cols);
+}
+
+// ====================================================================== backward
+// grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
+// R^T.dG_{l,t+1}, 1 off W_{l+1}^T.dG_{l+1,t}; the top layer has no off cluster and adds dy).
+// Critical steps t = T-1 .. -1 (t = -1: dh0 = R^T dG_{l,0}, dc0 = carry; engine.hpp:163-170),
+// off steps t = T-1 .. 0. Iteration it <-> t = T-1-it.
+template <int kChunks>
+__device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
+                                            uint32_t tmem_base, int tile, int m, int ko, uint32_t* consumed) {
+  const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
+  const int N = p.Bp, kc = p.kc, nco = N / kc;
+  const int u = tile * kTileM + row;
+  const bool uok = u < p.Hp;
+  const long long Hp = p.Hp, G4 = 4 * Hp;
+  const int cbase = m * nco + half * (nco >> 1);  // first batch column of this thread
+  float carry[kChunks * 8];
+#pragma unroll
+  for (int i = 0; i < kChunks * 8; ++i) carry[i] = 0.0f;
+  float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
+  uint32_t rxc = 0, offc = 0;
+  if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
+  for (int it = 0; it <= p.T; ++it) {
+    const int t = p.T - 1 - it;
+    const bool off = ko > 0 && t >= 0;
+    const bool have = t <= p.T - 2;  // an R^T.dG_{t+1} product was accumulated
+    float pi[8], pf[8], po[8], pcb[8], ptc[8], pcp[8], dyv[8];
+    auto load_tapes = [&](int i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        pi[j] = pf[j] = po[j] = pcb[j] = ptc[j] = pcp[j] = dyv[j] = 0.0f;
+        const long long n = cbase + i * 8 + j;
+        if (t < 0 || !uok) continue;
+        const long long col = (long long)t * N + n;
+        const float* gp = Ly.gates + col * G4 + u;
+        pi[j] = gp[0];
+        pf[j] = gp[Hp];
+        po[j] = gp[2 * Hp];
+        pcb[j] = gp[3 * Hp];
+        ptc[j] = Ly.tanhc[col * Hp + u];
+        pcp[j] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+        if (Ly.dy && u < p.H && n < p.B) dyv[j] = Ly.dy[((long long)t * p.B + n) * p.H + u];
+      }
+    };
+    load_tapes(0);  // independent of this step's GEMM: in flight while we wait
+    mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
+    tc_fence_after();
+    if (et == 0) cl_trace(p, it, 2);
+    float acc[kChunks * 8];
+    cl_reduce<kChunks>(S, tmem_base + (it & 1) * N, have, it, m, kc, nco, rxc, acc);
+    float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
+    if (off) {
+      mbar_wait(S.off_full, offc & 1);
+#pragma unroll
+      for (int i = 0; i < kChunks * 8; ++i)
+        dab[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
+    }
+    named_bar_sync(1, kEpiThreads);
+    if (et == 0) {
+      cl_trace(p, it, 4);
+      if (off) {
+        mbar_arrive(S.off_empty);
+        red_release_gpu_add(consumed, 1);
+      }
+      cl_rx_next(S, m, kc, nco);
+    }
+    if (off) ++offc;
+    if (t < 0) {  // dh0 / dc0
+      if (uok) {
+#pragma unroll
+        for (int i = 0; i < kChunks * 8; ++i) {
+          const long long n = cbase + i;
+          Ly.dh0[n * Hp + u] = acc[i];
+          Ly.dc0[n * Hp + u] = carry[i];
+        }
+      }
+      break;
+    }
+    float g_i[kChunks * 8], g_f[kChunks * 8], g_o[kChunks * 8], g_c[kChunks * 8];
+#pragma unroll
+    for (int i = 0; i < kChunks; ++i) {
+      if (i > 0) load_tapes(i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = i * 8 + j;
+        // cells.hpp:424-447 operation order; dh = d_above + carry_h
+        const float dh = off ? dab[k] + acc[k] : (Ly.dy ? dyv[j] + acc[k] : acc[k]);
+        const float q1 = dh * po[j];
+        const float s0 = ptc[j] * ptc[j];
+        const float s1 = 1.0f - s0;
+        const float q2 = q1 * s1;
+        const float dc = carry[k] + q2;
+        const float a1 = dc * pcb[j], a2 = a1 * pi[j], a3 = 1.0f - pi[j];
+        const float b1 = dc * pcp[j], b2 = b1 * pf[j], b3 = 1.0f - pf[j];
+        const float c1 = dh * ptc[j], c2 = c1 * po[j], c3 = 1.0f - po[j];
+        const float d1 = dc * pi[j], d2 = pcb[j] * pcb[j], d3 = 1.0f - d2;
+        g_i[k] = a2 * a3;
+        g_f[k] = b2 * b3;
+        g_o[k] = c2 * c3;
+        g_c[k] = d1 * d3;
+        carry[k] = dc * pf[j];
+        if (uok) {
+          const long long ob = ((long long)t * N + cbase + k) * G4;
+          __nv_bfloat16* op = static_cast<__nv_bfloat16*>(Ly.dgop[0]);
+          op[ob + rho_of(0, u)] = __float2bfloat16_rn(g_i[k]);
+          op[ob + rho_of(1, u)] = __float2bfloat16_rn(g_f[k]);
+          op[ob + rho_of(2, u)] = __float2bfloat16_rn(g_o[k]);
+          op[ob + rho_of(3, u)] = __float2bfloat16_rn(g_c[k]);
+        }
+      }
+    }
+    // publish dG_{l,t}
+    fence_proxy_async_global();
+    named_bar_sync(1, kEpiThreads);
+    if (et == 0) {
+      __threadfence();
+      red_release_gpu_add(&Ly.flags[t], 1);
+      cl_trace(p, it, 5);
+    }
+    if (uok) {
+#pragma unroll
+      for (int k = 0; k < kChunks * 8; ++k) {
+        float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
+        dgp[0] = g_i[k];
+        dgp[Hp] = g_f[k];
+        dgp[2 * Hp] = g_o[k];
+        dgp[3 * Hp] = g_c[k];
+        si += g_i[k];
+        sf += g_f[k];
+        so += g_o[k];
+        sc += g_c[k];
+      }
+    }
+    if (et == 0) cl_trace(p, it, 6);
+  }
+  if (uok && Ly.dbp) {
+    float* d = Ly.dbp + (long long)(m * 2 + half) * G4 + u;
+    d[0] = si;
+    d[Hp] = sf;
+    d[2 * Hp] = so;
+    d[3 * Hp] = sc;
+  }
+}
+
+__global__ void __launch_bounds__(kRecThreads, 1)
+    k_cl_bwd(const BwdLayer* __restrict__ layers, ClParams p) {
+  const int l = blockIdx.y;
+  __shared__ BwdLayer Ly;
+  __shared__ const uint32_t* up_flags;
+  if (threadIdx.x == 0) {
+    Ly = layers[l];
+    up_flags = Ly.has_up ? layers[l + 1].flags : nullptr;
+  }
+  __syncthreads();
+  const int cs = p.cs, kc = p.kc, N = p.Bp;
+  const int m = (int)(blockIdx.x % cs), cl_id = (int)(blockIdx.x / cs);
+  const int tile = cl_id >> 1;
+  const bool crit = (cl_id & 1) == 0;
+  const int G4p = 4 * p.Hp;
+  const int nkb_up = Ly.has_up ? G4p / 64 : 0, nkb_r = G4p / 64;
+  const int ko = (nkb_up + kClKBlocks - 1) / kClKBlocks;
+  const int n_act = crit ? kc : ko;
+  if (n_act == 0) return;  // whole cluster idle (top layer's off cluster): nobody waits on it
+  const bool active = m < n_act;
+  int kb_lo = 0, kb_hi = 0;
+  if (active) {
+    if (crit) {
+      kb_lo = nkb_up + m * nkb_r / kc;
+      kb_hi = nkb_up + (m + 1) * nkb_r / kc;
+    } else {
+      kb_lo = m * nkb_up / ko;
+      kb_hi = (m + 1) * nkb_up / ko;
+    }
+  }
+  const int nkb = kb_hi - kb_lo;
+  const int nco = N / n_act;
+  const int n_it = crit ? p.T + 1 : p.T;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const ClSmem S = cl_carve(smem, p);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < (uint32_t)(2 * N)) tmem_cols <<= 1;
+  const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
+  const int row0 = tile * kTileM;
+  const size_t lt = (size_t)l * p.tiles + tile;
+  float* ring = p.offsum + lt * kRing * N * kTileM;
+  uint32_t* done = p.off_done + lt * p.T;
+  uint32_t* consumed = p.consumed + lt * 32;
+
+  if (active && warp == 0 && lane == 0) {
+    prefetch_tmap(Ly.a[0]);
+    prefetch_tmap(crit ? Ly.bg[0] : Ly.bup[0]);
+    cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
+    uint32_t pc = 0, offc = 0;
+    for (int it = 0; it < n_it; ++it) {
+      const int t = p.T - 1 - it;
+      cl_trace(p, it, 0);
+      if (crit) {
+        const bool off = ko > 0 && t >= 0;
+        const bool early = off && ld_relaxed_gpu(done + it) >= (uint32_t)ko;
+        if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
+        if (t <= p.T - 2) {
+          wait_flag(&Ly.flags[t + 1], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 2));
+          fence_proxy_async_global();
+          cl_trace(p, it, 1);
+          cl_load_b(S, Ly.bg[0], kb_lo, kb_hi, nkb_up, (t + 1) * N, pc, p.stages, N);
+        }
+        if (off && !early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
+      } else {
+        wait_flag(&up_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
+        fence_proxy_async_global();
+        cl_trace(p, it, 1);
+        cl_load_b(S, Ly.bup[0], kb_lo, kb_hi, 0, t * N, pc, p.stages, N);
+      }
+    }
+  } else if (active && warp == 1 && lane == 0) {
+    const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
+    mbar_wait(S.a_full, 0);
+    tc_fence_after();
+    uint32_t pc = 0;
+    for (int it = 0; it < n_it; ++it) {
+      const int t = p.T - 1 - it;
+      const int ab = it & 1;
+      if (it >= 2) {
+        mbar_wait(&S.tmem_empty[ab], ((it >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      if (!crit || t <= p.T - 2) cl_mma_step(S, tmem_base + ab * N, nkb, idesc, pc, p.stages, N);
+      umma_commit(&S.tmem_full[ab]);
+    }
+  } else if (active && warp >= 4) {
+    if (!crit) {
+      switch (nco >> 4) {
+        case 4: cl_off_loop<4>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
+        default: cl_off_loop<1>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
+      }
+    } else {
+      switch (nco >> 4) {
+        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
+        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
+        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
+        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
+      }
+    }
+  }
+  cl_teardown(tmem_base, tmem_cols);
+}
+
+}  // namespace rw

@@ -23,6 +23,7 @@
 #include "gemm_tc.cuh"
 #include "layout_kernels.cuh"
 #include "lstm_step.cuh"
+#include "rec_cluster.cuh"
 
 using namespace rw;
 
@@ -172,6 +173,11 @@ void nccl_check(int r, const char* what) {
 }
 constexpr int kNcclFloat32 = 7, kNcclSum = 0;
 
+struct ClPlan {
+  int kc = 0, cs = 0, ncomax = 0, stages = 0;
+  size_t smem = 0;
+};
+
 template <class P>
 struct KernelSet {
   static void* fwd() { return (void*)k_lstm_fwd<P>; }
@@ -221,6 +227,9 @@ struct rw_ctx {
   int ks_f = 1, ks_b = 1, res_f = 0, res_b = 0, st_f = 4, st_b = 4;
   int slots_f = 0, slots_b = 0, acckb_f = 1, acckb_b = 1, nacc_f = 1, nacc_b = 1;
   size_t smem_f = 0, smem_b = 0;
+  // cluster schedule (rec_cluster.cuh)
+  ClPlan cl_f, cl_b;
+  DevBuf cl_offsum, cl_done, cl_consumed;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
   size_t smem_wg = 0, smem_dx = 0;
 
@@ -356,6 +365,38 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
   void* args[2] = {const_cast<void**>(&layers), const_cast<RecParams*>(&rp)};
   ++g_launches;
   RW_CUDA(cudaLaunchKernelExC(&lc, kernel, args));
+}
+
+// Cluster schedule (rec_cluster.cuh): per tile a critical cluster (kc members) and an off
+// cluster (ko_l members per layer), each member holding <= 512 K of its weight slice. Returns
+// false when the shape does not fit (batch > 64, owned columns not a multiple of 16, too many
+// CTAs, shared memory, or clusters not co-resident).
+bool plan_cluster(void* kernel, bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
+                  ClPlan& out) {
+  if (Bp > kClMaxN || Bp % kc || (Bp / kc) % 16) return false;
+  int cs = kc, komin = kc;
+  for (int k : ko) {
+    if (k == 0) continue;
+    if (Bp % k || (Bp / k) % 16) return false;
+    cs = std::max(cs, k);
+    komin = std::min(komin, k);
+  }
+  if (cs > 8 || (long long)L * tiles * 2 * cs > sms) return false;
+  const int ncomax = Bp / komin;
+  const int min_stages = fwd ? 4 : 2;  // forward critical: the sum buffer aliases the B stages
+  int stages = kClKBlocks;
+  size_t smem = cl_smem_bytes(cs, ncomax, Bp, stages);
+  while (smem > (size_t)kSmemLimit && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, Bp, --stages);
+  if (smem > (size_t)kSmemLimit) return false;
+  if (fwd && (size_t)stages * Bp * kRowBytes < (size_t)(Bp / kc) * kTileM * 4) return false;
+  smem = std::max(smem, (size_t)116 * 1024);  // one CTA per SM
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if ((long long)max_active_clusters(kernel, cs, smem, L * tiles * 2 * cs) < (long long)L * tiles * 2) return false;
+  out = ClPlan{kc, cs, ncomax, stages, smem};
+  return true;
 }
 
 size_t gemm_smem(int planes, int bn, int stages) {
@@ -508,8 +549,25 @@ void build(rw_ctx* x) {
   const int kbf_max = (std::max(Ip, Hp) + Hp) / x->atomK;
   const int kbb_max = (int)((L > 1 ? 2 : 1) * G4p / x->atomK);
   const int tiles_f = Hp / kUnitsPerFwdTile, tiles_b = ceil_div(Hp, kTileM);
-  RecPlan pf = plan_recurrent(kf, c.schedule, x->planes, kbf_max, tiles_f, L, Bp, sms, "RW_FWD_KSPLIT");
-  RecPlan pb = plan_recurrent(kb, c.schedule, x->planes, kbb_max, tiles_b, L, Bp, sms, "RW_BWD_KSPLIT");
+  // cluster schedule first (bf16): forward kc = K-slices of R.h, ko = of W.x; backward kc =
+  // K-slices of R^T.dG, ko = of W_{l+1}^T.dG (none for a single layer)
+  ClPlan cpf, cpb;
+  bool cl_f = false, cl_b = false;
+  if (x->prec == kBF16 && (c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER)) {
+    const int kc_f = ceil_div(Hp / 64, kClKBlocks);
+    std::vector<int> ko_f(L), ko_b(L);
+    for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
+    cl_f = plan_cluster((void*)k_cl_fwd, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
+    const int kc_b = ceil_div(4 * Hp / 64, kClKBlocks);
+    for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
+    cl_b = plan_cluster((void*)k_cl_bwd, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
+  }
+  if (c.schedule == RW_SCHED_CLUSTER && !(cl_f && cl_b))
+    einval("cluster schedule does not fit this configuration (bf16, batch <= 64, owned columns multiple of 16, "
+           "CTAs and clusters co-resident)");
+  const int want = c.schedule == RW_SCHED_CLUSTER ? RW_SCHED_AUTO : c.schedule;
+  RecPlan pf = plan_recurrent(kf, want, x->planes, kbf_max, tiles_f, L, Bp, sms, "RW_FWD_KSPLIT");
+  RecPlan pb = plan_recurrent(kb, want, x->planes, kbb_max, tiles_b, L, Bp, sms, "RW_BWD_KSPLIT");
   x->fwd_sched = pf.sched;
   x->ks_f = pf.ks;
   x->res_f = pf.resident;
@@ -522,6 +580,22 @@ void build(rw_ctx* x) {
   x->st_b = pb.stages;
   x->smem_b = pb.smem;
   x->slots_b = pb.a_slots;
+  if (cl_f) {
+    x->fwd_sched = RW_SCHED_CLUSTER;
+    x->cl_f = cpf;
+    x->ks_f = cpf.kc;
+  }
+  if (cl_b) {
+    x->bwd_sched = RW_SCHED_CLUSTER;
+    x->cl_b = cpb;
+    x->ks_b = cpb.kc;  // bias-gradient partial slices = kc members x 2 column halves
+  }
+  if (cl_f || cl_b) {
+    const size_t lt = (size_t)L * std::max(Hp / kUnitsPerFwdTile, ceil_div(Hp, kTileM));
+    x->cl_offsum.alloc(lt * kRing * Bp * kTileM * 4);
+    x->cl_done.alloc(lt * T * 4);
+    x->cl_consumed.alloc(lt * 32 * 4);
+  }
   // fp32-parity: accumulate every kAccKB k-blocks in a separate TMEM accumulator (<= 512 cols)
   auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc) {
     acc_kb = kb_per_cta > 0 ? kb_per_cta : 1;
@@ -798,8 +872,61 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   RW_CUDA(cudaGetLastError());
 }
 
+ClParams cl_params(rw_ctx* x, bool fwd) {
+  ClParams p{};
+  p.L = x->L;
+  p.H = x->H;
+  p.Hp = x->Hp;
+  p.B = x->B;
+  p.Bp = x->Bp;
+  p.T = x->T;
+  const ClPlan& pl = fwd ? x->cl_f : x->cl_b;
+  p.tiles = fwd ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
+  p.kc = pl.kc;
+  p.cs = pl.cs;
+  p.ncomax = pl.ncomax;
+  p.stages = pl.stages;
+  p.flag_target = (uint32_t)(p.tiles * p.kc);
+  p.offsum = x->cl_offsum.f();
+  p.off_done = static_cast<uint32_t*>(x->cl_done.p);
+  p.consumed = static_cast<uint32_t*>(x->cl_consumed.p);
+  p.error = static_cast<int*>(x->errflag.p);
+  p.timeout_ns = 20ULL * 1000000000ULL;
+  if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) p.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
+  p.trace = nullptr;
+  if (!x->trace_path.empty()) p.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
+  p.trace_steps = fwd ? x->T : x->T + 1;
+  return p;
+}
+
+void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams& p, int L, size_t smem,
+                    cudaStream_t s) {
+  RW_CUDA(cudaMemsetAsync(x->cl_done.p, 0, x->cl_done.bytes, s));
+  RW_CUDA(cudaMemsetAsync(x->cl_consumed.p, 0, x->cl_consumed.bytes, s));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(p.tiles * 2 * p.cs, L, 1);
+  lc.blockDim = dim3(kRecThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  void* args[2] = {const_cast<void**>(&layers), const_cast<ClParams*>(&p)};
+  ++g_launches;
+  RW_CUDA(cudaLaunchKernelExC(&lc, kernel, args));
+}
+
 template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
+  if (x->fwd_sched == RW_SCHED_CLUSTER) {
+    RW_CUDA(cudaMemsetAsync(x->flags_f.p, 0, x->flags_f.bytes, s));
+    launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->L, x->cl_f.smem, s);
+    return;
+  }
   RecParams rp = rec_params(x, true);
   void* kern = KernelSet<P>::fwd();
   // inference: no gate tapes (null gates pointer patched via a second descriptor table is
@@ -838,6 +965,11 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   RecParams rp = rec_params(x, false);
   void* kern = KernelSet<P>::bwd();
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
+  if (x->bwd_sched == RW_SCHED_CLUSTER) {
+    RW_CUDA(cudaMemsetAsync(x->flags_b.p, 0, x->flags_b.bytes, s));
+    launch_cluster(x, (void*)k_cl_bwd, x->bwd_layers.p, cl_params(x, false), x->L, x->cl_b.smem, s);
+    return;
+  }
   if (x->bwd_sched == RW_SCHED_PERSISTENT) {
     RW_CUDA(cudaMemsetAsync(x->flags_b.p, 0, x->flags_b.bytes, s));
     rp.persistent = 1;
@@ -1334,6 +1466,32 @@ void dump_trace(rw_ctx* x) {
   if (!f) return;
   fprintf(f, "task_layer,task_block,phase,worker,span,start_ns,end_ns\n");
   for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 ? x->fwd_sched : x->bwd_sched) == RW_SCHED_CLUSTER) {
+      // stamps: 0 step start, 1 operand published, 2 accumulator ready, 3 partial pushed (off
+      // members), 4 partials reduced, 5 operand published, 6 tapes written
+      const int steps = dir == 0 ? x->T : x->T + 1;
+      const int per_layer = (dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM)) * 2 *
+                            (dir == 0 ? x->cl_f.cs : x->cl_b.cs);
+      std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 8);
+      cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ULL;
+      for (auto v : h)
+        if (v && v < t0) t0 = v;
+      const int from[7] = {0, 1, 2, 2, 4, 5, 1};
+      const int to[7] = {1, 2, 3, 4, 5, 6, 3};
+      const char* names[7] = {"wait", "mma", "push", "reduce", "publish", "tapes", "offstep"};
+      for (int l = 0; l < x->L; ++l)
+        for (int w = 0; w < per_layer; ++w)
+          for (int it = 0; it < steps; ++it) {
+            const unsigned long long* st = &h[(((size_t)l * per_layer + w) * steps + it) * 8];
+            const int t = dir == 0 ? it : x->T - 1 - it;
+            for (int k = 0; k < 7; ++k)
+              if (st[from[k]] && st[to[k]])
+                fprintf(f, "%d,%d,%s,%d,%s,%llu,%llu\n", l, t, dir == 0 ? "fwd" : "bwd", w, names[k],
+                        st[from[k]] - t0, st[to[k]] - t0);
+          }
+      continue;
+    }
     if ((dir == 0 ? x->fwd_sched : x->bwd_sched) != RW_SCHED_PERSISTENT) continue;
     const int steps = dir == 0 ? x->T : x->T + 1;
     const int ks = dir == 0 ? x->ks_f : x->ks_b;

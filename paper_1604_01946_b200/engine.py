@@ -269,7 +269,7 @@ class Gradients:
 # ------------------------------------------------------------------ engine
 PRECISIONS = {"bf16": _lib.RW_PREC_BF16, "fp32": _lib.RW_PREC_FP32}
 SCHEDULES = {"auto": _lib.RW_SCHED_AUTO, "stepwise": _lib.RW_SCHED_STEPWISE,
-             "persistent": _lib.RW_SCHED_PERSISTENT}
+             "persistent": _lib.RW_SCHED_PERSISTENT, "cluster": _lib.RW_SCHED_CLUSTER}
 
 
 def nccl_unique_id() -> bytes:
@@ -282,7 +282,7 @@ def nccl_unique_id() -> bytes:
 
 class Engine:
     """rnnwave::Engine on one B200. precision: 'fp32' (3xTF32 parity mode, the default like
-    the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent'."""
+    the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent' | 'cluster'."""
 
     def __init__(self, cfg: LadderConfig, precision: str = "fp32", schedule: str = "auto",
                  device: int = 0):
@@ -461,6 +461,6 @@ class Engine:
     def describe(self) -> dict:
         a, b, k1, k2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         self._check(self._L.rw_describe(self._ctx, C.byref(a), C.byref(b), C.byref(k1), C.byref(k2)))
-        names = {1: "stepwise", 2: "persistent"}
+        names = {1: "stepwise", 2: "persistent", 3: "cluster"}
         return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
                 "fwd_ksplit": k1.value, "bwd_ksplit": k2.value}

@@ -19,15 +19,54 @@ SMALL = [
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-@pytest.mark.parametrize("schedule", ["stepwise", "persistent"])
+@pytest.mark.parametrize("schedule", ["stepwise", "persistent", "cluster"])
 @pytest.mark.parametrize("dims", SMALL, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
 def test_small_configs(reference, precision, schedule, dims):
     from paper_1604_01946_b200 import Engine
     c, params, x, dy, h0, c0 = make_case(dims, seed=7, bias=True, state=True)
-    eng = Engine(c, precision=precision, schedule=schedule)
+    eng = make_engine(Engine, c, precision, schedule)
     dev = run_device(eng, params, x, dy, h0, c0)
     ref = run_reference(reference, c, params, x, dy, h0, c0)
     assert_within(compare(dev, ref, c), precision)
+
+
+def make_engine(Engine, c, precision, schedule):
+    """The cluster schedule is bf16-only and shape-gated (rec_cluster.cuh): skip where the
+    runtime reports that it does not fit rather than testing a fallback under its name."""
+    if schedule == "cluster" and precision != "bf16":
+        pytest.skip("cluster schedule is bf16 only")
+    try:
+        eng = Engine(c, precision=precision, schedule=schedule)
+    except ValueError as e:
+        if schedule == "cluster" and "does not fit" in str(e):
+            pytest.skip(str(e))
+        raise
+    d = eng.describe()
+    if schedule == "cluster":
+        assert d["fwd_schedule"] == d["bwd_schedule"] == "cluster", d
+    return eng
+
+
+# shapes the cluster schedule takes (incl. split critical members, kc > 1, and several
+# off-critical members): run fwd+bwd parity on each
+CLUSTER = [
+    Dims(2, 256, 256, 64, 12),   # bwd kc = 2 (4H = 1024): critical peers exchange partials
+    Dims(2, 512, 512, 64, 6),    # config-B shape, short: fwd cs = 2, bwd kc = 4, cs = 8
+    Dims(3, 512, 300, 64, 7),    # bwd kc = 4, cs = 8; layer-0 input narrower than H
+    Dims(1, 512, 512, 64, 9),    # single layer: backward has no off-critical members
+    Dims(2, 384, 1000, 48, 5),   # forward ko = 2 (I = 1000 -> two W.x members), nco = 48
+]
+
+
+@pytest.mark.parametrize("dims", CLUSTER, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
+def test_cluster_configs(reference, dims):
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(dims, seed=17, bias=True, state=True)
+    eng = make_engine(Engine, c, "bf16", "cluster")
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    worst = assert_within(compare(dev, ref, c), "bf16")
+    print(f"cluster {dims}: {eng.describe()} worst {worst}")
 
 
 @pytest.mark.slow
@@ -44,11 +83,12 @@ def test_config_b_full(reference, precision):
     print(f"config B {precision} {eng.describe()}: worst {worst}")
 
 
-def test_deterministic_repeat():
+@pytest.mark.parametrize("schedule", ["persistent", "cluster"])
+def test_deterministic_repeat(schedule):
     """Run-to-run bitwise identity on the device (the analogue of acceptance crit 8)."""
     from paper_1604_01946_b200 import Engine
-    c, params, x, dy, h0, c0 = make_case(Dims(2, 128, 96, 24, 12), seed=3, bias=True)
-    eng = Engine(c, precision="bf16", schedule="persistent")
+    c, params, x, dy, h0, c0 = make_case(Dims(2, 128, 96, 32, 12), seed=3, bias=True)
+    eng = make_engine(Engine, c, "bf16", schedule)
     a = run_device(eng, params, x, dy, h0, c0)
     b = run_device(eng, params, x, dy, h0, c0)
     for k in a:
