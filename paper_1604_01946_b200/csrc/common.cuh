@@ -45,6 +45,14 @@ __host__ __device__ inline int rho_of(int g, int u) { return (u >> 5) * 128 + g 
 __host__ __device__ inline int rho_gate(int rho) { return (rho & 127) >> 5; }
 __host__ __device__ inline int rho_unit(int rho) { return (rho >> 7) * 32 + (rho & 31); }
 
+// Byte offset of element (k, n) inside one step block of a pre-swizzled operand: k-blocks of
+// 64 K-elements, each Bp rows of 128 B with the 16-B chunks XOR-permuted by row % 8 -- exactly
+// the shared-memory image TMA SWIZZLE_128B produces for a {64, Bp} box, so a consumer fetches
+// a k-block with one contiguous 1-D bulk copy (rec_cluster.cuh).
+__host__ __device__ inline long long sw_off(int k, int n, int Bp) {
+  return (long long)(k >> 6) * Bp * 128 + n * 128 + ((((k >> 3) & 7) ^ (n & 7)) << 4) + (k & 7) * 2;
+}
+
 // Output index mapping of the generic GEMM epilogue.
 enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1 };
 enum ColMode : int { kColIdentity = 0, kColBatchUnpad = 1 };

@@ -34,11 +34,18 @@ struct OperandTile {
   }
   // UMMA descriptor of k-substep kk (0 .. kAtomK/kUmmaK-1) of a tile at smem address s.
   static __device__ __forceinline__ uint64_t desc(uint32_t s, int kk) {
+    return desc_add(base(s), kk * kk_bytes());
+  }
+  // Descriptor of the tile at smem address s (k-substep 0) and the byte stride of a k-substep.
+  static __device__ __forceinline__ uint64_t base(uint32_t s) {
     if constexpr (!kMN) {
-      return sdesc_sw128(s + kk * P::kUmmaK * P::kElem, 16, 1024);
+      return sdesc_sw128(s, 16, 1024);
     } else {
-      return sdesc_sw128(s + kk * P::kUmmaK * kRowBytes, P::kAtomK * kRowBytes, 1024);
+      return sdesc_sw128(s, P::kAtomK * kRowBytes, 1024);
     }
+  }
+  static __device__ __forceinline__ constexpr uint32_t kk_bytes() {
+    return kMN ? P::kUmmaK * kRowBytes : P::kUmmaK * P::kElem;
   }
 };
 
@@ -166,6 +173,9 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
     const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, bn);
+    // stage-0 descriptors, advanced by adds (sm100_ptx.cuh desc_add)
+    const uint64_t a_d0 = OperandTile<P, kAMN>::base(smem_u32(smem));
+    const uint64_t b_d0 = OperandTile<P, kBMN>::base(smem_u32(smem + P::kPlanes * a_bytes));
     int kb = 0;
     for (int c = 0; c < nchunks; ++c) {
       const int buf = c & 1;
@@ -179,14 +189,16 @@ __global__ void __launch_bounds__(256, 1)
         const int s = kb % stages;
         mbar_wait(&full[s], (kb / stages) & 1);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + s * stage_bytes);
+        const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
+#pragma unroll
         for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+#pragma unroll
           for (int cb = 0; cb < P::kCombos; ++cb) {
             // combos: (hi,hi), (hi,lo), (lo,hi); bf16 has only (hi,hi)
             const int pa = (cb == 2) ? 1 : 0;
             const int pb = (cb == 1) ? 1 : 0;
-            const uint64_t ad = OperandTile<P, kAMN>::desc(st + pa * a_bytes, kk);
-            const uint64_t bd = OperandTile<P, kBMN>::desc(st + P::kPlanes * a_bytes + pb * b_bytes, kk);
+            const uint64_t ad = desc_add(a_s, pa * a_bytes + kk * OperandTile<P, kAMN>::kk_bytes());
+            const uint64_t bd = desc_add(b_s, pb * b_bytes + kk * OperandTile<P, kBMN>::kk_bytes());
             umma<P::kTF32>(acc, ad, bd, idesc, (kb != k0 || kk | cb) ? 1u : 0u);
           }
         }

@@ -105,6 +105,21 @@ __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk
   }
 }
 
+// Plain K-major bf16 operand (column c = t*Bp + n holds K contiguous elements) -> swizzled step
+// blocks (block t at t * K * Bp * 2 bytes), columns [c0, c0 + ncols).
+__global__ void k_swizzle_op(const __nv_bfloat16* __restrict__ src, int K, int Bp, long long c0, long long ncols,
+                             uint8_t* __restrict__ dst) {
+  const long long total = (long long)K * ncols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long c = c0 + e / K;
+    const int k = (int)(e % K);
+    const long long t = c / Bp;
+    const int n = (int)(c - t * Bp);
+    *reinterpret_cast<__nv_bfloat16*>(dst + t * (long long)K * Bp * 2 + sw_off(k, n, Bp)) = src[c * K + k];
+  }
+}
+
 // Inverse: dst (G*R x nblk*B) from src (G*Rp x nblk*Bp at src_col_off); G gate blocks.
 __global__ void k_unpad_cols(const float* __restrict__ src, int Rp, int Bp, long long src_col_off,
                              int G, int R, int B, int nblk, float* __restrict__ dst) {

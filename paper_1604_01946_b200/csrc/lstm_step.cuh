@@ -53,6 +53,10 @@ struct FwdLayer {
   float* gates;              // 4Hp x Bp T (row g*Hp + u), null in inference
   float* tanhc;              // Hp x Bp T, null in inference
   uint32_t* flags;           // [T] completion counters
+  // cluster schedule: pre-swizzled bf16 operand step blocks (layout_kernels.cuh sw_off)
+  uint8_t* hsw;              // own h: block t+1 = h_t, block 0 = h0 (Hp x Bp per block)
+  const uint8_t* bxsw;       // layer input: x (blocks 0..T-1, Ipl x Bp) or hsw of layer l-1 (+1 block)
+  int bx_blk_off;
 };
 
 struct BwdLayer {
@@ -71,6 +75,9 @@ struct BwdLayer {
   float* dh0;                // Hp x Bp
   float* dc0;                // Hp x Bp
   uint32_t* flags;           // [T]
+  // cluster schedule: pre-swizzled bf16 dG step blocks (4Hp x Bp per block, K index rho)
+  uint8_t* dgsw;
+  const uint8_t* bupsw;      // dgsw of layer l+1
 };
 
 struct RecParams {
@@ -133,7 +140,10 @@ __device__ __forceinline__ void store_operand(void* const* planes, long long idx
 template <class P>
 __device__ __forceinline__ float act_sigmoid(float x) {
   if constexpr (P::kPlanes == 1) {
-    return __fdividef(1.0f, 1.0f + __expf(-x));
+    // sigma(x) = 0.5 + 0.5 tanh(x/2): one MUFU.TANH instead of EX2 + RCP
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(0.5f * x));
+    return fmaf(0.5f, y, 0.5f);
   } else {
     return 1.0f / (1.0f + expf(-x));
   }
@@ -363,11 +373,14 @@ template <class P>
 __device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32_t b_base,
                                            int a_bytes, int b_bytes, uint32_t idesc,
                                            bool fresh) {
+  const uint64_t a0 = sdesc_sw128(a_base, 16, 1024), b0 = sdesc_sw128(b_base, 16, 1024);
+#pragma unroll
   for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
+#pragma unroll
     for (int c = 0; c < P::kCombos; ++c) {
       const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
-      const uint64_t ad = sdesc_sw128(a_base + pa * a_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
-      const uint64_t bd = sdesc_sw128(b_base + pb * b_bytes + kk * P::kUmmaK * P::kElem, 16, 1024);
+      const uint64_t ad = desc_add(a0, pa * a_bytes + kk * P::kUmmaK * P::kElem);
+      const uint64_t bd = desc_add(b0, pb * b_bytes + kk * P::kUmmaK * P::kElem);
       umma<P::kTF32>(acc, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
     }
   }

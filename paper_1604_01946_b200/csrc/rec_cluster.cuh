@@ -41,6 +41,11 @@ namespace rw {
 constexpr int kClKBlocks = 8;  // k-blocks (64 bf16) per member: 128 x 512 x 2 B = 128 KB resident
 constexpr int kClMaxN = 64;    // batch columns (Bp) this path supports
 constexpr int kRing = 4;       // off-partial ring depth (steps the off cluster may run ahead)
+// MMA issue: a single issuing warp sustains only ~90 cycles per tcgen05.mma regardless of N
+// (profiles/ubench/mma_ubench.cu), which at N = Bp = 64 is ~3x the tensor core's own time. Two
+// warps (1 and 3) issue the two halves of a step's k-blocks into separate accumulators, and
+// the epilogue adds them (acc0 + acc1, fixed order).
+constexpr int kIssuers = 2;
 
 struct ClParams {
   int L, H, Hp, B, Bp, T;
@@ -57,6 +62,7 @@ struct ClParams {
   unsigned long long timeout_ns;
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
   int trace_steps;
+  int debug;  // RW_CL_DEBUG bits (timing experiments only; results invalid): 1 = skip fwd tapes
 };
 
 // Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
@@ -110,7 +116,7 @@ __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
 __device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
   if (p.trace) {
     const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
-    p.trace[((unsigned long long)cta * p.trace_steps + it) * 8 + what] = globaltimer();
+    p.trace[((unsigned long long)cta * p.trace_steps + it) * 16 + what] = globaltimer();
   }
 }
 
@@ -136,14 +142,16 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // Receive slot of sender s at owner d (senders = every member but d, in member order).
 __device__ __forceinline__ int cl_slot(int s, int d) { return s < d ? s : s - 1; }
 
-// Load 8 accumulator columns of this thread's TMEM lane, or zeros if nothing was accumulated.
-__device__ __forceinline__ void cl_ld8(uint32_t taddr, bool have, float (&v)[8]) {
+// Load 8 accumulator columns of this thread's TMEM lane: acc0 (+ acc1, `two` accumulators N
+// columns apart, the two issuers' halves of K), or zeros if nothing was accumulated.
+__device__ __forceinline__ void cl_ld8(uint32_t taddr, bool have, float (&v)[8], bool two = false, int N = 0) {
   if (have) {
-    uint32_t r[8];
+    uint32_t r[8], r2[8];
     tmem_ld_32x32b_x8(taddr, r);
+    if (two) tmem_ld_32x32b_x8(taddr + N, r2);
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+    for (int j = 0; j < 8; ++j) v[j] = two ? __uint_as_float(r[j]) + __uint_as_float(r2[j]) : __uint_as_float(r[j]);
   } else {
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = 0.0f;
@@ -160,8 +168,8 @@ __device__ __forceinline__ uint32_t cl_setup(const ClSmem& S, const ClParams& p,
       mbar_init(&S.empty[i], 1);
     }
     mbar_init(S.a_full, 1);
-    mbar_init(&S.tmem_full[0], 1);
-    mbar_init(&S.tmem_full[1], 1);
+    mbar_init(&S.tmem_full[0], kIssuers);
+    mbar_init(&S.tmem_full[1], kIssuers);
     mbar_init(&S.tmem_empty[0], kEpiThreads);
     mbar_init(&S.tmem_empty[1], kEpiThreads);
     mbar_init(S.rx_full, 1);
@@ -200,29 +208,44 @@ __device__ __forceinline__ void cl_load_a(const ClSmem& S, const CUtensorMap* a,
     tma_load_2d(S.a + (kb - kb_lo) * a_bytes, a, S.a_full, kb * 64, row0);
 }
 
-__device__ __forceinline__ void cl_mma_step(const ClSmem& S, uint32_t acc, int nkb, uint32_t idesc,
-                                            uint32_t& pc, int stages, int N) {
+// MMA issuers: warps 1 (j = 0) and 3 (j = 1), each converged; elect.sync inside the instruction
+// blocks picks the issuing lane (sm100_ptx.cuh umma_bf16_warp). Issuer j multiplies its half of
+// the step's k-blocks into accumulator `acc` (= its own TMEM columns).
+__device__ __forceinline__ int cl_half0(int nkb) { return (nkb + 1) >> 1; }
+__device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, int it, uint32_t acc, int nkb,
+                                            uint32_t idesc, uint32_t& pc, int stages, int N, int j) {
   const int a_bytes = kTileM * kRowBytes, b_bytes = N * kRowBytes;
-  for (int k = 0; k < nkb; ++k, ++pc) {
-    const int s = pc % stages;
-    mbar_wait(&S.full[s], (pc / stages) & 1);
+  const bool l0 = (threadIdx.x & 31) == 0;
+  const uint64_t a0 = sdesc_sw128(smem_u32(S.a), 16, 1024), b0 = sdesc_sw128(smem_u32(S.b), 16, 1024);
+  const int h0 = cl_half0(nkb);
+  const int k_lo = j == 0 ? 0 : h0, k_hi = j == 0 ? h0 : nkb;
+  for (int k = k_lo; k < k_hi; ++k) {
+    const uint32_t q = pc + k;
+    const uint32_t s = q % stages;
+    mbar_wait(&S.full[s], (q / stages) & 1);
     tc_fence_after();
-    mma_kblock<PrecBF16>(acc, smem_u32(S.a + k * a_bytes), smem_u32(S.b + s * b_bytes), a_bytes, b_bytes,
-                         idesc, k == 0);
-    umma_commit(&S.empty[s]);
+    if (l0 && k < 8) cl_trace(p, it, 8 + k);  // arrival of each k-block (slots 8..15)
+    if (l0 && k == nkb - 1) cl_trace(p, it, 7);
+    const uint64_t ad = desc_add(a0, k * a_bytes), bd = desc_add(b0, s * b_bytes);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)  // 4 x K=16 per 64-element k-block (32 bytes along K)
+      umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, kk * 32), idesc, (k != k_lo || kk) ? 1u : 0u);
+    umma_commit_warp(&S.empty[s]);
   }
+  pc += nkb;
 }
 
-// Producer: stream the k-blocks [kb_lo, kb_hi) of one step's B operand (map m, K offset
-// k0 - kb_lo*64, column col) through the stage ring.
-__device__ __forceinline__ void cl_load_b(const ClSmem& S, const CUtensorMap* m, int kb_lo, int kb_hi, int kofs,
-                                          int col, uint32_t& pc, int stages, int N) {
+// Producer (one thread): stream the k-blocks [kb_lo, kb_hi) of one step's B operand through the
+// stage ring. `blk` is the operand's pre-swizzled step block (sw_off layout); k-block kb sits at
+// (kb - kofs) * N * 128 bytes, already in the SWIZZLE_128B smem image: one 1-D bulk copy each.
+__device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, int kb_lo, int kb_hi, int kofs,
+                                          uint32_t& pc, int stages, int N) {
   const int b_bytes = N * kRowBytes;
   for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
     const int s = pc % stages;
     mbar_wait(&S.empty[s], ((pc / stages) & 1) ^ 1);
     mbar_arrive_expect_tx(&S.full[s], b_bytes);
-    tma_load_2d(S.b + s * b_bytes, m, &S.full[s], (kb - kofs) * 64, col);
+    bulk_load(S.b + s * b_bytes, blk + (size_t)(kb - kofs) * b_bytes, b_bytes, &S.full[s]);
   }
 }
 
@@ -231,8 +254,8 @@ __device__ __forceinline__ void cl_load_b(const ClSmem& S, const CUtensorMap* m,
 // Thread (quarter q, lane) owns accumulator row q*32+lane; `half` picks its half of the owned
 // columns. v_out[i*8 + j] = owned column half*nco/2 + i*8 + j.
 template <int kChunks>
-__device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, int it, int m, int n_act,
-                                          int nco, uint32_t& rxc, float (&v_out)[kChunks * 8]) {
+__device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, bool two, int N, int it, int m,
+                                          int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8]) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const uint32_t taddr = tacc + (uint32_t(q * 32) << 16);
@@ -243,7 +266,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
       float* blk = S.st + (size_t)cl_slot(d, m) * nco * kTileM;
       for (int c0 = half * (nco >> 1); c0 < (half + 1) * (nco >> 1); c0 += 8) {
         float v[8];
-        cl_ld8(taddr + d * nco + c0, have, v);
+        cl_ld8(taddr + d * nco + c0, have, v, two, N);
 #pragma unroll
         for (int j = 0; j < 8; ++j) sts_f32(blk + (size_t)(c0 + j) * kTileM + row, v[j]);
       }
@@ -259,12 +282,17 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
     }
   }
   const int own0 = m * nco;
+  if (have) {
 #pragma unroll
-  for (int i = 0; i < kChunks; ++i) {
-    float v[8];
-    cl_ld8(taddr + own0 + half * (nco >> 1) + i * 8, have, v);
+    for (int i = 0; i < kChunks; ++i) {
+      float v[8];
+      cl_ld8(taddr + own0 + half * (nco >> 1) + i * 8, true, v, two, N);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = v[j];
+      for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = v[j];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kChunks * 8; ++i) v_out[i] = 0.0f;
   }
   tc_fence_before();
   mbar_arrive(&S.tmem_empty[it & 1]);
@@ -298,13 +326,13 @@ __device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, in
 // Off cluster epilogue of one step: reduce, then store the owned columns of the reduced partial
 // into ring slot it % kRing ([Bp][128] fp32) and publish it.
 template <int kChunks>
-__device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, int it, int m,
-                                            int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
+__device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, bool two, int it,
+                                            int m, int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
                                             const uint32_t* consumed) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<kChunks>(S, tacc, true, it, m, n_act, nco, rxc, v);
+  cl_reduce<kChunks>(S, tacc, true, two, p.Bp, it, m, n_act, nco, rxc, v);
   named_bar_sync(1, kEpiThreads);
   if (et == 0) {
     cl_rx_next(S, m, n_act, nco);
@@ -320,15 +348,12 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
   for (int i = 0; i < kChunks * 8; ++i) slot[(size_t)(c0 + i) * kTileM + row] = v[i];
   fence_proxy_async_global();
   named_bar_sync(1, kEpiThreads);
-  if (et == 0) {
-    __threadfence();
-    red_release_gpu_add(done + it, 1);
-  }
+  if (et == 0) red_release_gpu_add(done + it, 1);
 }
 
 template <int kChunks>
-__device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, int n_it,
-                                            int m, int n_act, float* ring, uint32_t* done,
+__device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, bool two,
+                                            int n_it, int m, int n_act, float* ring, uint32_t* done,
                                             const uint32_t* consumed) {
   const int et = threadIdx.x - kEpiBase, N = p.Bp, nco = N / n_act;
   uint32_t rxc = 0;
@@ -337,7 +362,7 @@ __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, 
     mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
-    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * N, it, m, n_act, nco, rxc, ring, done, consumed);
+    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed);
     if (et == 0) cl_trace(p, it, 3);
   }
 }
@@ -359,12 +384,12 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
 template <int kChunks>
-__device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, int t, int m, int kc, int nco,
-                                           uint32_t& rxc, uint32_t offc) {
+__device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
+                                           int nco, uint32_t& rxc, uint32_t offc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<kChunks>(S, tacc, true, t, m, kc, nco, rxc, v);
+  cl_reduce<kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v);
   mbar_wait(S.off_full, offc & 1);
   float* sum = reinterpret_cast<float*>(S.b);
 #pragma unroll
@@ -404,6 +429,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     }
   }
   const int nkb = kb_hi - kb_lo;
+  const bool two = nkb - cl_half0(nkb) > 0;  // the second issuer accumulated something
   const int nco = N / n_act;
 
   extern __shared__ uint8_t smem_raw[];
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const ClSmem S = cl_carve(smem, p);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(2 * N)) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
   const int row0 = tile * kTileM;
   const size_t lt = (size_t)l * p.tiles + tile;
@@ -420,9 +446,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   uint32_t* consumed = p.consumed + lt * 32;
 
   if (active && warp == 0 && lane == 0) {
-    // ================= TMA producer
+    // ================= producer: resident A (TMA), then per step the operand (bulk copies)
     prefetch_tmap(Ly.a[0]);
-    prefetch_tmap(crit ? Ly.bh[0] : Ly.bx[0]);
     cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
     uint32_t pc = 0, offc = 0;
     for (int t = 0; t < p.T; ++t) {
@@ -434,17 +459,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.bh[0], kb_lo, kb_hi, nkb_x, t * N, pc, p.stages, N);
+        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, nkb_x, pc, p.stages, N);
         if (!early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, t, m, nco, offc, wait_code(0, l, t, 3));
       } else {
         if (l > 0) wait_flag(&x_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.bx[0], kb_lo, kb_hi, 0, Ly.bx_col_off + t * N, pc, p.stages, N);
+        cl_load_b(S, Ly.bxsw + (size_t)(Ly.bx_blk_off + t) * Ly.Ipl * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
       }
     }
-  } else if (active && warp == 1 && lane == 0) {
-    // ================= MMA issuer
+  } else if (active && (warp == 1 || warp == 3)) {
+    // ================= MMA issuers (whole warps, elected lane issues); j = half of the k-blocks
+    const int j = warp == 3 ? 1 : 0;
     const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
     mbar_wait(S.a_full, 0);
     tc_fence_after();
@@ -455,17 +481,17 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_empty[ab], ((t >> 1) - 1) & 1);
         tc_fence_after();
       }
-      cl_mma_step(S, tmem_base + ab * N, nkb, idesc, pc, p.stages, N);
-      umma_commit(&S.tmem_full[ab]);
+      cl_mma_step(S, p, t, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j);
+      umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
     const int et = threadIdx.x - kEpiBase;
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
-        default: cl_off_loop<1>(S, p, tmem_base, p.T, m, n_act, ring, done, consumed); break;
+        case 4: cl_off_loop<4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
+        default: cl_off_loop<1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
       }
     } else {
       // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
@@ -487,24 +513,24 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_full[t & 1], (t >> 1) & 1);
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
-        const uint32_t tacc = tmem_base + (t & 1) * N;
+        const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
         switch (nco >> 4) {
-          case 4: cl_fwd_sum<4>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
-          case 3: cl_fwd_sum<3>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
-          case 2: cl_fwd_sum<2>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
-          default: cl_fwd_sum<1>(S, tacc, t, m, kc, nco, rxc, (uint32_t)t); break;
+          case 4: cl_fwd_sum<4>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
+          case 3: cl_fwd_sum<3>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
+          case 2: cl_fwd_sum<2>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
+          default: cl_fwd_sum<1>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
         }
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
           mbar_arrive(S.off_empty);
-          red_release_gpu_add(consumed, 1);  // ring slot t copied into rxoff
           cl_rx_next(S, m, kc, nco);
         }
         // cell phase, operand store first (the critical output)
         float hv[kClMaxN / 8], cv[kClMaxN / 8], iv[kClMaxN / 8], fv[kClMaxN / 8], ov[kClMaxN / 8],
             cb[kClMaxN / 8], tcv[kClMaxN / 8];
         const long long colp = (long long)t * N + own0;  // block t (c_{t-1}), owned base
+        uint8_t* hblk = Ly.hsw + (size_t)(t + 1) * p.Hp * N * 2;  // h_t: block t+1
 #pragma unroll
         for (int k = 0; k < kClMaxN / 8; ++k) {
           const int cl = cg + 8 * k;
@@ -523,24 +549,27 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tcv[k] = act_tanh<PrecBF16>(cv[k]);
           hv[k] = ov[k] * tcv[k];
           creg[k] = cv[k];
-          static_cast<__nv_bfloat16*>(Ly.hop[0])[(colp + N + cl) * Hp + u] = __float2bfloat16_rn(hv[k]);
+          *reinterpret_cast<__nv_bfloat16*>(hblk + sw_off(u, own0 + cl, N)) = __float2bfloat16_rn(hv[k]);
         }
+        if (et == 0) cl_trace(p, t, 3);
         // publish h_t (all operand stores of this CTA, then one gpu-scope release)
         fence_proxy_async_global();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
-          __threadfence();
-          red_release_gpu_add(&Ly.flags[t], 1);
+          red_release_gpu_add(&Ly.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
+          red_relaxed_gpu_add(consumed, 1);      // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
         }
-        // tapes (read only after the pass)
+        // tapes (read only after the pass; the plain bf16 h feeds the weight-gradient GEMMs)
 #pragma unroll
         for (int k = 0; k < kClMaxN / 8; ++k) {
+          if (p.debug & 1) break;
           const int cl = cg + 8 * k;
           if (cl >= nco) break;
           const long long col_prev = colp + cl, col_new = col_prev + N;
           Ly.c[col_new * Hp + u] = cv[k];
           Ly.h[col_new * Hp + u] = hv[k];
+          static_cast<__nv_bfloat16*>(Ly.hop[0])[col_new * Hp + u] = __float2bfloat16_rn(hv[k]);
           if (Ly.gates) {
             float* gp = Ly.gates + col_prev * G4 + u;
             gp[0] = iv[k];
@@ -564,7 +593,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 // off steps t = T-1 .. 0. Iteration it <-> t = T-1-it.
 template <int kChunks>
 __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
-                                            uint32_t tmem_base, int tile, int m, int ko, uint32_t* consumed) {
+                                            uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const int N = p.Bp, kc = p.kc, nco = N / kc;
@@ -605,7 +634,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     float acc[kChunks * 8];
-    cl_reduce<kChunks>(S, tmem_base + (it & 1) * N, have, it, m, kc, nco, rxc, acc);
+    cl_reduce<kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc);
     float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
       mbar_wait(S.off_full, offc & 1);
@@ -616,10 +645,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     named_bar_sync(1, kEpiThreads);
     if (et == 0) {
       cl_trace(p, it, 4);
-      if (off) {
-        mbar_arrive(S.off_empty);
-        red_release_gpu_add(consumed, 1);
-      }
+      if (off) mbar_arrive(S.off_empty);
       cl_rx_next(S, m, kc, nco);
     }
     if (off) ++offc;
@@ -658,26 +684,33 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         g_c[k] = d1 * d3;
         carry[k] = dc * pf[j];
         if (uok) {
-          const long long ob = ((long long)t * N + cbase + k) * G4;
-          __nv_bfloat16* op = static_cast<__nv_bfloat16*>(Ly.dgop[0]);
-          op[ob + rho_of(0, u)] = __float2bfloat16_rn(g_i[k]);
-          op[ob + rho_of(1, u)] = __float2bfloat16_rn(g_f[k]);
-          op[ob + rho_of(2, u)] = __float2bfloat16_rn(g_o[k]);
-          op[ob + rho_of(3, u)] = __float2bfloat16_rn(g_c[k]);
+          uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
+          const int n = cbase + k;
+          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(0, u), n, N)) = __float2bfloat16_rn(g_i[k]);
+          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(1, u), n, N)) = __float2bfloat16_rn(g_f[k]);
+          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(2, u), n, N)) = __float2bfloat16_rn(g_o[k]);
+          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(3, u), n, N)) = __float2bfloat16_rn(g_c[k]);
         }
       }
     }
+    if (et == 0) cl_trace(p, it, 3);
     // publish dG_{l,t}
     fence_proxy_async_global();
     named_bar_sync(1, kEpiThreads);
     if (et == 0) {
-      __threadfence();
       red_release_gpu_add(&Ly.flags[t], 1);
+      if (off) red_relaxed_gpu_add(consumed, 1);
       cl_trace(p, it, 5);
     }
     if (uok) {
 #pragma unroll
       for (int k = 0; k < kChunks * 8; ++k) {
+        const long long ob = ((long long)t * N + cbase + k) * G4;
+        __nv_bfloat16* op = static_cast<__nv_bfloat16*>(Ly.dgop[0]);
+        op[ob + rho_of(0, u)] = __float2bfloat16_rn(g_i[k]);
+        op[ob + rho_of(1, u)] = __float2bfloat16_rn(g_f[k]);
+        op[ob + rho_of(2, u)] = __float2bfloat16_rn(g_o[k]);
+        op[ob + rho_of(3, u)] = __float2bfloat16_rn(g_c[k]);
         float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
         dgp[0] = g_i[k];
         dgp[Hp] = g_f[k];
@@ -731,6 +764,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     }
   }
   const int nkb = kb_hi - kb_lo;
+  const bool two = nkb - cl_half0(nkb) > 0;  // the second issuer accumulated something
   const int nco = N / n_act;
   const int n_it = crit ? p.T + 1 : p.T;
 
@@ -739,7 +773,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const ClSmem S = cl_carve(smem, p);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(2 * N)) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
   const int row0 = tile * kTileM;
   const size_t lt = (size_t)l * p.tiles + tile;
@@ -749,31 +783,31 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 
   if (active && warp == 0 && lane == 0) {
     prefetch_tmap(Ly.a[0]);
-    prefetch_tmap(crit ? Ly.bg[0] : Ly.bup[0]);
     cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
     uint32_t pc = 0, offc = 0;
     for (int it = 0; it < n_it; ++it) {
       const int t = p.T - 1 - it;
+      const bool off = crit && ko > 0 && t >= 0;
+      const bool load = !crit || t <= p.T - 2;
       cl_trace(p, it, 0);
-      if (crit) {
-        const bool off = ko > 0 && t >= 0;
-        const bool early = off && ld_relaxed_gpu(done + it) >= (uint32_t)ko;
-        if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
-        if (t <= p.T - 2) {
+      const bool early = off && ld_relaxed_gpu(done + it) >= (uint32_t)ko;
+      if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
+      if (load) {
+        if (crit)
           wait_flag(&Ly.flags[t + 1], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 2));
-          fence_proxy_async_global();
-          cl_trace(p, it, 1);
-          cl_load_b(S, Ly.bg[0], kb_lo, kb_hi, nkb_up, (t + 1) * N, pc, p.stages, N);
-        }
-        if (off && !early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
-      } else {
-        wait_flag(&up_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
+        else
+          wait_flag(&up_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, it, 1);
-        cl_load_b(S, Ly.bup[0], kb_lo, kb_hi, 0, t * N, pc, p.stages, N);
+        if (crit)
+          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, nkb_up, pc, p.stages, N);
+        else
+          cl_load_b(S, Ly.bupsw + (size_t)t * G4p * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
       }
+      if (off && !early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
     }
-  } else if (active && warp == 1 && lane == 0) {
+  } else if (active && (warp == 1 || warp == 3)) {
+    const int j = warp == 3 ? 1 : 0;
     const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
     mbar_wait(S.a_full, 0);
     tc_fence_after();
@@ -785,23 +819,23 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_empty[ab], ((it >> 1) - 1) & 1);
         tc_fence_after();
       }
-      if (!crit || t <= p.T - 2) cl_mma_step(S, tmem_base + ab * N, nkb, idesc, pc, p.stages, N);
-      umma_commit(&S.tmem_full[ab]);
+      if (!crit || t <= p.T - 2) cl_mma_step(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j);
+      umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
-        default: cl_off_loop<1>(S, p, tmem_base, n_it, m, n_act, ring, done, consumed); break;
+        case 4: cl_off_loop<4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
+        default: cl_off_loop<1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
       }
     } else {
       switch (nco >> 4) {
-        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
-        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
-        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
-        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, tile, m, ko, consumed); break;
+        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
+        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
+        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
+        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
       }
     }
   }

@@ -230,6 +230,8 @@ struct rw_ctx {
   // cluster schedule (rec_cluster.cuh)
   ClPlan cl_f, cl_b;
   DevBuf cl_offsum, cl_done, cl_consumed;
+  std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
+  DevBuf xsw;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
   size_t smem_wg = 0, smem_dx = 0;
 
@@ -596,6 +598,15 @@ void build(rw_ctx* x) {
     x->cl_done.alloc(lt * T * 4);
     x->cl_consumed.alloc(lt * 32 * 4);
   }
+  if (cl_f) {
+    x->hsw.resize(L);
+    for (int l = 0; l < L; ++l) x->hsw[l].alloc((size_t)Hp * colsT1 * 2);
+    x->xsw.alloc((size_t)Ip * colsT * 2);
+  }
+  if (cl_b) {
+    x->dgsw.resize(L);
+    for (int l = 0; l < L; ++l) x->dgsw[l].alloc((size_t)G4p * colsT * 2);
+  }
   // fp32-parity: accumulate every kAccKB k-blocks in a separate TMEM accumulator (<= 512 cols)
   auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc) {
     acc_kb = kb_per_cta > 0 ? kb_per_cta : 1;
@@ -666,6 +677,11 @@ void build(rw_ctx* x) {
     F.gates = x->gates[l].f();
     F.tanhc = x->tanhc[l].f();
     F.flags = ff + (size_t)l * T;
+    if (!x->hsw.empty()) {
+      F.hsw = static_cast<uint8_t*>(x->hsw[l].p);
+      F.bxsw = l == 0 ? static_cast<const uint8_t*>(x->xsw.p) : static_cast<const uint8_t*>(x->hsw[l - 1].p);
+      F.bx_blk_off = l == 0 ? 0 : 1;
+    }
     BwdLayer& Bd = bl[l];
     for (int p = 0; p < 2; ++p) {
       Bd.a[p] = mp(m_wb[2 * l + (p % x->planes)], p);
@@ -684,6 +700,10 @@ void build(rw_ctx* x) {
     Bd.dh0 = x->dh0[l].f();
     Bd.dc0 = x->dc0[l].f();
     Bd.flags = fb + (size_t)l * T;
+    if (!x->dgsw.empty()) {
+      Bd.dgsw = static_cast<uint8_t*>(x->dgsw[l].p);
+      Bd.bupsw = l < L - 1 ? static_cast<const uint8_t*>(x->dgsw[l + 1].p) : nullptr;
+    }
   }
   x->fwd_layers.alloc(sizeof(FwdLayer) * L);
   x->bwd_layers.alloc(sizeof(BwdLayer) * L);
@@ -769,8 +789,8 @@ void build(rw_ctx* x) {
   if (const char* e = getenv("RW_TRACE")) {
     x->trace_path = e;
     const size_t ctas = 4096;
-    x->trace_f.alloc(ctas * (T + 1) * 8 * 8);
-    x->trace_b.alloc(ctas * (T + 2) * 8 * 8);
+    x->trace_f.alloc(ctas * (T + 1) * 16 * 8);
+    x->trace_b.alloc(ctas * (T + 2) * 16 * 8);
   }
   if (const char* e = getenv("RW_DEBUG_HANG_S")) {
     x->hang_s = atof(e);
@@ -869,6 +889,15 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
     k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
+  if (x->fwd_sched == RW_SCHED_CLUSTER) {  // pre-swizzled operand images of x and h0
+    const long long colsT = (long long)Bp * x->T;
+    ++g_launches;
+    k_swizzle_op<<<grid_for((long long)x->Ip * colsT), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x->x_op.p(0)), x->Ip, Bp, 0, colsT, static_cast<uint8_t*>(x->xsw.p));
+    for (int l = 0; l < L; ++l, ++g_launches)
+      k_swizzle_op<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
+                                                               Hp, Bp, 0, Bp, static_cast<uint8_t*>(x->hsw[l].p));
+  }
   RW_CUDA(cudaGetLastError());
 }
 
@@ -896,6 +925,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.trace = nullptr;
   if (!x->trace_path.empty()) p.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
   p.trace_steps = fwd ? x->T : x->T + 1;
+  if (const char* e = getenv("RW_CL_DEBUG")) p.debug = atoi(e);
   return p;
 }
 
@@ -1472,20 +1502,30 @@ void dump_trace(rw_ctx* x) {
       const int steps = dir == 0 ? x->T : x->T + 1;
       const int per_layer = (dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM)) * 2 *
                             (dir == 0 ? x->cl_f.cs : x->cl_b.cs);
-      std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 8);
+      std::vector<unsigned long long> h((size_t)x->L * per_layer * steps * 16);
       cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost);
       unsigned long long t0 = ~0ULL;
       for (auto v : h)
         if (v && v < t0) t0 = v;
-      const int from[7] = {0, 1, 2, 2, 4, 5, 1};
-      const int to[7] = {1, 2, 3, 4, 5, 6, 3};
-      const char* names[7] = {"wait", "mma", "push", "reduce", "publish", "tapes", "offstep"};
+      // critical members (cluster index even): wait 0-1, load 1-7, mma 7-2, reduce 2-4,
+      // cell 4-3, publish 3-5, tapes 5-6; off members: offload 1-7, offmma 7-2, offstep 2-3
+      const int cs = dir == 0 ? x->cl_f.cs : x->cl_b.cs;
+      const int fromc[15] = {0, 1, 7, 2, 4, 3, 5, 1, 1, 1, 1, 1, 1, 1, 1};
+      const int toc[15] = {1, 7, 2, 4, 3, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15};
+      const char* namec[15] = {"wait", "load", "mma", "reduce", "cell", "publish", "tapes", "kb0",
+                               "kb1", "kb2", "kb3", "kb4", "kb5", "kb6", "kb7"};
+      const int fromo[9] = {1, 7, 2, 1}, too[9] = {7, 2, 3, 8};
+      const char* nameo[9] = {"offload", "offmma", "offstep", "offkb0"};
       for (int l = 0; l < x->L; ++l)
         for (int w = 0; w < per_layer; ++w)
           for (int it = 0; it < steps; ++it) {
-            const unsigned long long* st = &h[(((size_t)l * per_layer + w) * steps + it) * 8];
+            const unsigned long long* st = &h[(((size_t)l * per_layer + w) * steps + it) * 16];
             const int t = dir == 0 ? it : x->T - 1 - it;
-            for (int k = 0; k < 7; ++k)
+            const bool critm = ((w / cs) & 1) == 0;
+            const int* from = critm ? fromc : fromo;
+            const int* to = critm ? toc : too;
+            const char* const* names = critm ? namec : nameo;
+            for (int k = 0; k < (critm ? 15 : 4); ++k)
               if (st[from[k]] && st[to[k]])
                 fprintf(f, "%d,%d,%s,%d,%s,%llu,%llu\n", l, t, dir == 0 ? "fwd" : "bwd", w, names[k],
                         st[from[k]] - t0, st[to[k]] - t0);

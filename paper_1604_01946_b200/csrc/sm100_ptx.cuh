@@ -130,6 +130,27 @@ RW_DEVICE void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t id
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
   }
 }
+// Warp-converged variants: the whole warp executes them and elect.sync picks the issuing lane
+// inside the instruction block. Issued from a lane-0-only branch instead, every tcgen05.mma
+// gets wrapped in an ELECT/R2UR.BROADCAST waterfall loop whose fixed latencies bounded the
+// issue rate at ~155 cycles per MMA in the recurrent kernels (ncu source view: stall_wait).
+RW_DEVICE void umma_bf16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+RW_DEVICE void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 // Arrive (once) on `bar` when all previously issued tcgen05.mma of this thread complete.
 RW_DEVICE void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -174,6 +195,12 @@ RW_DEVICE uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
 }
+// Advance a shared-memory matrix descriptor by `bytes` (the start-address field, bits 0..13,
+// holds addr >> 4; shared memory < 256 KB never carries out of it). Lets the MMA issuer build
+// each descriptor with one 64-bit add instead of re-encoding (measured: re-encoding in the
+// uniform datapath bounded a single issuing thread at ~85-165 cycles per tcgen05.mma,
+// profiles/ubench/mma_ubench.cu).
+RW_DEVICE uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 // Instruction descriptor: fp32 accumulate; fmt 1 = bf16, 2 = tf32.
 __host__ __device__ constexpr uint32_t idesc_make(uint32_t fmt, bool a_mn_major, bool b_mn_major,
                                                   uint32_t M, uint32_t N) {
@@ -225,6 +252,9 @@ RW_DEVICE uint32_t ld_relaxed_gpu(const uint32_t* p) {
 }
 RW_DEVICE void red_release_gpu_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+RW_DEVICE void red_relaxed_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 RW_DEVICE void nanosleep(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
 
