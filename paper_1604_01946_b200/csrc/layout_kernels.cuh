@@ -106,17 +106,20 @@ __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk
 }
 
 // Plain K-major bf16 operand (column c = t*Bp + n holds K contiguous elements) -> swizzled step
-// blocks (block t at t * K * Bp * 2 bytes), columns [c0, c0 + ncols).
+// blocks (block t at t * K * Bp * 2 bytes), columns [c0, c0 + ncols). One thread per 8 consecutive
+// K elements: they form one 16-byte chunk in both layouts (sw_off permutes whole chunks).
 __global__ void k_swizzle_op(const __nv_bfloat16* __restrict__ src, int K, int Bp, long long c0, long long ncols,
                              uint8_t* __restrict__ dst) {
-  const long long total = (long long)K * ncols;
+  const int kc = K >> 3;
+  const long long total = (long long)kc * ncols;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long c = c0 + e / K;
-    const int k = (int)(e % K);
+    const long long c = c0 + e / kc;
+    const int k = (int)(e % kc) << 3;
     const long long t = c / Bp;
     const int n = (int)(c - t * Bp);
-    *reinterpret_cast<__nv_bfloat16*>(dst + t * (long long)K * Bp * 2 + sw_off(k, n, Bp)) = src[c * K + k];
+    *reinterpret_cast<uint4*>(dst + t * (long long)K * Bp * 2 + sw_off(k, n, Bp)) =
+        *reinterpret_cast<const uint4*>(src + c * K + k);
   }
 }
 

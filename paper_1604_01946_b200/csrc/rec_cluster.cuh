@@ -62,7 +62,8 @@ struct ClParams {
   unsigned long long timeout_ns;
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
   int trace_steps;
-  int debug;  // RW_CL_DEBUG bits (timing experiments only; results invalid): 1 = skip fwd tapes
+  int debug;  // RW_CL_DEBUG bits (timing experiments only; results invalid): 1 = skip fwd tapes,
+              // 4 = skip bwd tape loads, 8 = skip bwd operand stores
 };
 
 // Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
@@ -224,7 +225,7 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
     const uint32_t s = q % stages;
     mbar_wait(&S.full[s], (q / stages) & 1);
     tc_fence_after();
-    if (l0 && k < 8) cl_trace(p, it, 8 + k);  // arrival of each k-block (slots 8..15)
+    if (l0 && k == 0) cl_trace(p, it, 8);  // first k-block arrived
     if (l0 && k == nkb - 1) cl_trace(p, it, 7);
     const uint64_t ad = desc_add(a0, k * a_bytes), bd = desc_add(b0, s * b_bytes);
 #pragma unroll
@@ -255,12 +256,16 @@ __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, i
 // columns. v_out[i*8 + j] = owned column half*nco/2 + i*8 + j.
 template <int kChunks>
 __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, bool two, int N, int it, int m,
-                                          int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8]) {
+                                          int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8],
+                                          const ClParams* tp = nullptr) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const uint32_t taddr = tacc + (uint32_t(q * 32) << 16);
   if (n_act > 1) {
-    if (it > 0) mbar_wait_cluster(S.push_free, (it - 1) & 1);  // owners consumed the previous push
+    // owners consumed the previous push. CTA-scope waits here and below: a cluster-scope acquire
+    // makes every waiting thread invalidate L1 (CCTL.IVALL), ~2 us per step across 256 threads;
+    // the bulk copies' data is covered by the mbarrier's complete_tx (as for TMA loads).
+    if (it > 0) mbar_wait(S.push_free, (it - 1) & 1);
     for (int d = 0; d < n_act; ++d) {
       if (d == m) continue;
       float* blk = S.st + (size_t)cl_slot(d, m) * nco * kTileM;
@@ -273,6 +278,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
     }
     fence_proxy_async_smem();
     named_bar_sync(1, kEpiThreads);
+    if (tp && et == 0) cl_trace(*tp, it, 9);
     if (et == 0) {
       for (int d = 0; d < n_act; ++d) {
         if (d == m) continue;
@@ -296,30 +302,55 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
   }
   tc_fence_before();
   mbar_arrive(&S.tmem_empty[it & 1]);
+  if (tp && et == 0) cl_trace(*tp, it, 10);
   if (n_act > 1) {
-    mbar_wait_cluster(S.rx_full, rxc & 1);
+    mbar_wait(S.rx_full, rxc & 1);
     ++rxc;
+    if (tp && et == 0) cl_trace(*tp, it, 11);
+    // sum in member order s = 0 .. n_act-1 (own partial at s = m); each sender's 8 columns of a
+    // chunk are read as one batch of independent loads (a per-element volatile chain measured
+    // ~1.9 us per step); chunk by chunk to keep register pressure flat
+    const float* base = S.rx + (size_t)(half * (nco >> 1)) * kTileM + row;
 #pragma unroll
     for (int i = 0; i < kChunks; ++i) {
+      float acc[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int cl = half * (nco >> 1) + i * 8 + j;
-        float acc = 0.0f;
-        for (int s = 0; s < n_act; ++s)
-          acc += s == m ? v_out[i * 8 + j] : lds_f32(S.rx + ((size_t)cl_slot(s, m) * nco + cl) * kTileM + row);
-        v_out[i * 8 + j] = acc;
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+      for (int s = 0; s < n_act; ++s) {
+        if (s == m) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += v_out[i * 8 + j];
+        } else {
+          const float* src = base + ((size_t)cl_slot(s, m) * nco + i * 8) * kTileM;
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = src[(size_t)j * kTileM];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += v[j];
+        }
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = acc[j];
     }
   }
 }
 
 // After every epilogue thread of the owner read the receive slots (named barrier): re-arm for
 // the next step and release the slots to the senders (one thread).
+// The arrive is relaxed: a release would make this thread wait for all its outstanding global
+// stores (the previous step's tapes) first -- measured ~2 us on the backward's critical path.
+// The slots' values were consumed into registers before the barrier that precedes this call,
+// so the reads are complete before a sender's next bulk copy can overwrite them.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* local_bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   map_dsmem(smem_u32(local_bar), rank))
+               : "memory");
+}
 __device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, int nco) {
   if (n_act > 1) {
     mbar_arrive_expect_tx(S.rx_full, (uint32_t)(n_act - 1) * nco * kTileM * 4);
     for (int s = 0; s < n_act; ++s)
-      if (s != m) mbar_arrive_remote(S.push_free, (uint32_t)s);
+      if (s != m) mbar_arrive_remote_relaxed(S.push_free, (uint32_t)s);
   }
 }
 
@@ -617,7 +648,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       for (int j = 0; j < 8; ++j) {
         pi[j] = pf[j] = po[j] = pcb[j] = ptc[j] = pcp[j] = dyv[j] = 0.0f;
         const long long n = cbase + i * 8 + j;
-        if (t < 0 || !uok) continue;
+        if (t < 0 || !uok || (p.debug & 4)) continue;
         const long long col = (long long)t * N + n;
         const float* gp = Ly.gates + col * G4 + u;
         pi[j] = gp[0];
@@ -630,11 +661,25 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       }
     };
     load_tapes(0);  // independent of this step's GEMM: in flight while we wait
+    if (t >= 1) {
+      // pull next step's tape lines (gates x4, tanh(c), c of this warp's 32 units and its
+      // columns) from HBM into L2 now, so next step's loads are L2 hits
+      const long long tn = t - 1;
+      const int ub = tile * kTileM + q * 32;
+      for (int pi = lane; pi < kChunks * 8 * 6; pi += 32) {
+        const long long col = tn * N + cbase + pi / 6;
+        const int ty = pi % 6;
+        const float* a = ty < 4 ? Ly.gates + col * G4 + ty * Hp + ub
+                                : (ty == 4 ? Ly.tanhc : Ly.c) + col * Hp + ub;
+        if (ub < p.Hp) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
     mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     float acc[kChunks * 8];
-    cl_reduce<kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc);
+    cl_reduce<kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, &p);
+    if (et == 0) cl_trace(p, it, 12);
     float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
       mbar_wait(S.off_full, offc & 1);
@@ -642,6 +687,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       for (int i = 0; i < kChunks * 8; ++i)
         dab[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
     }
+    if (et == 0) cl_trace(p, it, 13);
     named_bar_sync(1, kEpiThreads);
     if (et == 0) {
       cl_trace(p, it, 4);
@@ -683,7 +729,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         g_o[k] = c2 * c3;
         g_c[k] = d1 * d3;
         carry[k] = dc * pf[j];
-        if (uok) {
+        if (uok && !(p.debug & 8)) {
           uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
           const int n = cbase + k;
           *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(0, u), n, N)) = __float2bfloat16_rn(g_i[k]);

@@ -892,10 +892,10 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   if (x->fwd_sched == RW_SCHED_CLUSTER) {  // pre-swizzled operand images of x and h0
     const long long colsT = (long long)Bp * x->T;
     ++g_launches;
-    k_swizzle_op<<<grid_for((long long)x->Ip * colsT), 256, 0, s>>>(
+    k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(x->x_op.p(0)), x->Ip, Bp, 0, colsT, static_cast<uint8_t*>(x->xsw.p));
     for (int l = 0; l < L; ++l, ++g_launches)
-      k_swizzle_op<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
+      k_swizzle_op<<<grid_for((long long)Hp / 8 * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
                                                                Hp, Bp, 0, Bp, static_cast<uint8_t*>(x->hsw[l].p));
   }
   RW_CUDA(cudaGetLastError());
@@ -1510,10 +1510,10 @@ void dump_trace(rw_ctx* x) {
       // critical members (cluster index even): wait 0-1, load 1-7, mma 7-2, reduce 2-4,
       // cell 4-3, publish 3-5, tapes 5-6; off members: offload 1-7, offmma 7-2, offstep 2-3
       const int cs = dir == 0 ? x->cl_f.cs : x->cl_b.cs;
-      const int fromc[15] = {0, 1, 7, 2, 4, 3, 5, 1, 1, 1, 1, 1, 1, 1, 1};
-      const int toc[15] = {1, 7, 2, 4, 3, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15};
-      const char* namec[15] = {"wait", "load", "mma", "reduce", "cell", "publish", "tapes", "kb0",
-                               "kb1", "kb2", "kb3", "kb4", "kb5", "kb6", "kb7"};
+      const int fromc[13] = {0, 1, 7, 2, 4, 3, 5, 1, 2, 9, 10, 11, 12};
+      const int toc[13] = {1, 7, 2, 4, 3, 5, 6, 8, 9, 10, 11, 12, 13};
+      const char* namec[13] = {"wait", "load", "mma", "reduce", "cell", "publish", "tapes", "kb0",
+                               "r_drain", "r_own", "r_peers", "r_sum", "r_off"};
       const int fromo[9] = {1, 7, 2, 1}, too[9] = {7, 2, 3, 8};
       const char* nameo[9] = {"offload", "offmma", "offstep", "offkb0"};
       for (int l = 0; l < x->L; ++l)
@@ -1525,7 +1525,7 @@ void dump_trace(rw_ctx* x) {
             const int* from = critm ? fromc : fromo;
             const int* to = critm ? toc : too;
             const char* const* names = critm ? namec : nameo;
-            for (int k = 0; k < (critm ? 15 : 4); ++k)
+            for (int k = 0; k < (critm ? 13 : 4); ++k)
               if (st[from[k]] && st[to[k]])
                 fprintf(f, "%d,%d,%s,%d,%s,%llu,%llu\n", l, t, dir == 0 ? "fwd" : "bwd", w, names[k],
                         st[from[k]] - t0, st[to[k]] - t0);
