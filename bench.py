@@ -63,47 +63,56 @@ def measured_peaks() -> tuple[dict, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML polled every 5 ms
+    from a thread (nvidia-smi -lms cannot go below ~100 ms, longer than a short timed region);
+    falls back to nvidia-smi when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+        self.gpu, self.rows, self.stop = gpu, [], threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+    def _poll(self):
+        while not self.stop.is_set():
+            try:
+                if self.nvml:
+                    sm = self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM)
+                    r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.rows.append((sm, self.max_mhz, r))
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True)
+                    sm, mx = (float(v) for v in out.stdout.split(","))
+                    self.rows.append((sm, mx, 0))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(2)
 
     def summary(self) -> dict:
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
-                          if r[5 + i].lower().startswith("active")})
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n, bit in self.REASONS.items() if r[2] & bit})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml 5 ms" if self.nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -270,10 +279,14 @@ def run_ours(args) -> None:
     fwd_fl = pass_flops(c, 1)  # [W|R].[x;h] for every cell
     bwd_fl = sum(2 * 4 * H * (H + (H if l < L - 1 else 0)) * B * (T + (1 if True else 0))
                  for l in range(L))  # W_{l+1}^T and R_l^T per cell (+ the dh0 step)
+    kern = {"cluster": ("k_cl_fwd", "k_cl_bwd"), "persistent": ("k_lstm_fwd", "k_lstm_bwd"),
+            "stepwise": ("k_lstm_fwd", "k_lstm_bwd")}
+    kf = kern.get(desc["fwd_schedule"], ("k_lstm_fwd",))[0]
+    kb = kern.get(desc["bwd_schedule"], ("", "k_lstm_bwd"))[1]
     if bwd_ms >= fwd_ms:
-        dom, dom_ms, dom_fl = "k_lstm_bwd (fused recurrent backward)", bwd_ms, bwd_fl
+        dom, dom_ms, dom_fl = f"{kb} (fused recurrent backward, {desc['bwd_schedule']})", bwd_ms, bwd_fl
     else:
-        dom, dom_ms, dom_fl = "k_lstm_fwd (fused recurrent forward)", fwd_ms, fwd_fl
+        dom, dom_ms, dom_fl = f"{kf} (fused recurrent forward, {desc['fwd_schedule']})", fwd_ms, fwd_fl
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops", 1590.0)
     cpu_base = None
@@ -340,7 +353,7 @@ def cpu_baseline() -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])

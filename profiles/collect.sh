@@ -16,7 +16,7 @@ if [[ $what == launches || $what == all ]]; then
       --log-file gpurun_out/launches.csv $B --steps 2 --warmup 1 > gpurun_out/launches.out 2>&1
 fi
 if [[ $what == full || $what == all ]]; then
-  for k in k_lstm_fwd k_lstm_bwd k_gemm_tc; do
+  for k in k_cl_fwd k_cl_bwd k_gemm_tc; do
     timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
         -o gpurun_out/prof_$k -f $B --steps 1 --warmup 1 > gpurun_out/prof_$k.out 2>&1
   done
