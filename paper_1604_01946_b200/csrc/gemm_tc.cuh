@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(256, 1)
                                    bn, k + g.b_k_off);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp converged; elect.sync picks the issuing lane)
     const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, bn);
     // stage-0 descriptors, advanced by adds (sm100_ptx.cuh desc_add)
     const uint64_t a_d0 = OperandTile<P, kAMN>::base(smem_u32(smem));
@@ -199,12 +199,12 @@ __global__ void __launch_bounds__(256, 1)
             const int pb = (cb == 1) ? 1 : 0;
             const uint64_t ad = desc_add(a_s, pa * a_bytes + kk * OperandTile<P, kAMN>::kk_bytes());
             const uint64_t bd = desc_add(b_s, pb * b_bytes + kk * OperandTile<P, kBMN>::kk_bytes());
-            umma<P::kTF32>(acc, ad, bd, idesc, (kb != k0 || kk | cb) ? 1u : 0u);
+            umma_warp<P::kTF32>(acc, ad, bd, idesc, (kb != k0 || kk | cb) ? 1u : 0u);
           }
         }
-        umma_commit(&empty[s]);
+        umma_commit_warp(&empty[s]);
       }
-      umma_commit(&tmem_full[buf]);
+      umma_commit_warp(&tmem_full[buf]);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global
@@ -275,6 +275,159 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(tmem_cols));
+  }
+}
+
+// ====================================================================== persistent GEMM (bf16)
+// k_gemm_p: one CTA per SM loops over the (problem, n-tile, m-tile) space of a grouped GEMM table
+// (m fastest, so CTAs running together share B tiles in L2). Tiles are 128 x BN (BN = 128 or
+// 256: at N = 256 a tcgen05.mma (128x256x16) takes 128 tensor cycles, more than a warp's ~90
+// cycle issue interval, so the tensor pipe -- not the issuer -- paces the loop). Two TMEM
+// accumulators (2 x BN columns) let the epilogue drain tile i while the MMAs of tile i+1 run.
+// Warps: 0 TMA producer, 1 MMA issuer (converged, elect.sync), 2 TMEM allocator, 3 idle,
+// 4..7 epilogue (TMEM lane quarter = warp % 4).
+template <bool kAMN, bool kBMN, int BN>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm_p(const GemmDesc* __restrict__ table, int count, int mt_max, int nt_max, int stages) {
+  using P = PrecBF16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int a_bytes = kTileM * kRowBytes;
+  constexpr int b_bytes = BN * kRowBytes;
+  constexpr int stage_bytes = a_bytes + b_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tmem_full = empty + stages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t tmem_cols = 2 * BN;
+  const long long ntiles = (long long)count * mt_max * nt_max;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  auto tile_of = [&](long long t, int& z, int& m0, int& n0) {
+    const int per = mt_max * nt_max;
+    z = (int)(t / per);
+    const int r = (int)(t - (long long)z * per);
+    n0 = (r / mt_max) * BN;
+    m0 = (r % mt_max) * kTileM;
+  };
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    uint32_t pc = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
+      for (int kb = 0; kb < nkb; ++kb, ++pc) {
+        const int s = pc % stages;
+        mbar_wait(&empty[s], ((pc / stages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        uint8_t* st = smem + s * stage_bytes;
+        const int k = kb * P::kAtomK;
+        OperandTile<P, kAMN>::load(st, g.a[0], &full[s], m0, kTileM, k + g.a_k_off);
+        OperandTile<P, kBMN>::load(st + a_bytes, g.b[0], &full[s], n0, BN, k + g.b_k_off);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (converged warp)
+    const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, BN);
+    const uint64_t a_d0 = OperandTile<P, kAMN>::base(smem_u32(smem));
+    const uint64_t b_d0 = OperandTile<P, kBMN>::base(smem_u32(smem + a_bytes));
+    uint32_t pc = 0, tc = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
+      const int buf = tc & 1;
+      if (tc >= 2) {
+        mbar_wait(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t acc = tmem_base + buf * BN;
+      for (int kb = 0; kb < nkb; ++kb, ++pc) {
+        const int s = pc % stages;
+        mbar_wait(&full[s], (pc / stages) & 1);
+        tc_fence_after();
+        const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
+#pragma unroll
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk)
+          umma_bf16_warp(acc, desc_add(a_s, kk * OperandTile<P, kAMN>::kk_bytes()),
+                         desc_add(b_s, kk * OperandTile<P, kBMN>::kk_bytes()), idesc, (kb | kk) ? 1u : 0u);
+        umma_commit_warp(&empty[s]);
+      }
+      umma_commit_warp(&tmem_full[buf]);
+      ++tc;
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global (overlaps the next tile's MMAs)
+    const int q = warp & 3;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    uint32_t tc = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int buf = tc & 1;
+      mbar_wait(&tmem_full[buf], (tc >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + q * 32 + lane;
+      const int orow = m < g.M ? gemm_out_row(g, m) : -1;
+      ColCursor cc(g, n0);
+      float* const drow = g.d + (orow < 0 ? 0 : orow);
+      const long long ldd = g.ldd;
+      const bool accum_out = g.accumulate != 0;
+      const int nlim = min(BN, g.N - n0);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[8], w[8];
+        tmem_ld_32x32b_x8(tmem_base + lane_off + buf * BN + c0, v);
+        tmem_ld_32x32b_x8(tmem_base + lane_off + buf * BN + c0 + 8, w);
+        tmem_ld_wait();
+        if (orow < 0 || c0 >= nlim) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (c0 + j >= nlim) break;
+          const long long oc = cc.next();
+          if (oc < 0) continue;
+          float* dst = drow + oc * ldd;
+          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]);
+          *dst = accum_out ? *dst + val : val;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tmem_empty[buf]);
+      ++tc;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 

@@ -47,17 +47,42 @@ constexpr int kRing = 4;       // off-partial ring depth (steps the off cluster 
 // the epilogue adds them (acc0 + acc1, fixed order).
 constexpr int kIssuers = 2;
 
+// The off-partial ring a critical layer group reads (in this GPU's memory; its writer -- an off
+// group -- may run on a peer GPU in the layer pipeline, then `sys` selects system-scope flags).
+// Counters are cumulative over passes: a pass's targets are epoch * (per-pass count).
+struct ClRing {
+  float* ring;         // [tiles][kRing][Bp][128] reduced off partials
+  uint32_t* done;      // [tiles][T] publications (ko per step per pass)
+  uint32_t* consumed;  // [tiles][32] ring slots copied by the critical members (kc per step per pass)
+  int ko;              // off members publishing per step (0: none -- backward top layer, uses dy)
+  int sys;
+};
+// An off-critical group (grid row y, role 1): W . operand for the rows of a target layer, written
+// into that layer's ring (possibly on a peer GPU: the layer pipeline's stage boundary).
+struct ClOff {
+  const CUtensorMap* a;      // weight map of the target layer; the group uses k-blocks [0, kdim/64)
+  int kdim;                  // operand K (forward I_l, backward 4Hp)
+  const uint8_t* op;         // operand pre-swizzled step blocks (sw_off), kdim x Bp each
+  int op_blk_off;            // step block of step t = op_blk_off + t
+  const uint32_t* op_flags;  // per-step publication counters of the operand (null: always ready)
+  float* ring;               // target layer's ring (ClRing fields)
+  uint32_t* done;
+  const uint32_t* consumed;
+  int sys;
+  int active;
+};
+
 struct ClParams {
   int L, H, Hp, B, Bp, T;
   int tiles;     // tiles per layer
   int kc;        // active critical members per tile
-  int cs;        // cluster size = max(kc, ko over layers)
-  int ncomax;    // Bp / min(kc, min_l ko_l): receive-slot size (columns) of the carve-up
+  int cs;        // cluster size = max(kc, ko over groups)
+  int ncomax;    // Bp / min(kc, min ko): receive-slot size (columns) of the carve-up
   int stages;    // B-operand TMA stages
-  uint32_t flag_target;  // per-(layer, step) publications: tiles * kc
-  float* offsum;         // [L][tiles][kRing][Bp][128] reduced off partials
-  uint32_t* off_done;    // [L][tiles][T] publications by the off cluster (target ko_l)
-  uint32_t* consumed;    // [L][tiles][32] (one counter per 128 B): ring slots read by critical members
+  int n_crit;    // critical layer groups (grid rows y < n_crit); rows may also carry off groups
+  const ClRing* cring;   // [n_crit]
+  const ClOff* offg;     // [gridDim.y]
+  const uint32_t* epoch; // pass counter (device, incremented before each launch)
   int* error;
   unsigned long long timeout_ns;
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
@@ -114,6 +139,8 @@ __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
   return s;
 }
 
+__global__ void k_epoch_inc(uint32_t* e) { *e += 1; }
+
 __device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
   if (p.trace) {
     const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
@@ -138,6 +165,45 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Flag operations at gpu or system scope (system: the counter is shared with a peer GPU).
+__device__ __forceinline__ uint32_t ld_relaxed_s(const uint32_t* p, bool sys) {
+  uint32_t v;
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_flag_s(const uint32_t* flag, uint32_t target, bool sys, int* error,
+                                            unsigned long long timeout_ns, int code) {
+  if (!sys) {
+    wait_flag(flag, target, error, timeout_ns, code);
+    return;
+  }
+  const uint64_t t0 = globaltimer();
+#pragma unroll 1
+  while (ld_relaxed_s(flag, true) < target) {
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicCAS(error, 0, code);
+      return;
+    }
+  }
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+}
+__device__ __forceinline__ void red_release_s(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    red_release_gpu_add(p, v);
+}
+__device__ __forceinline__ void red_relaxed_s(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    red_relaxed_gpu_add(p, v);
 }
 
 // Receive slot of sender s at owner d (senders = every member but d, in member order).
@@ -359,7 +425,7 @@ __device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, in
 template <int kChunks>
 __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, bool two, int it,
                                             int m, int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
-                                            const uint32_t* consumed) {
+                                            const uint32_t* consumed, bool sys, uint32_t epoch) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
@@ -367,10 +433,11 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
   named_bar_sync(1, kEpiThreads);
   if (et == 0) {
     cl_rx_next(S, m, n_act, nco);
-    // ring slot free once every critical member copied step it - kRing
+    // ring slot free once every critical member copied step it - kRing (of this pass; the
+    // previous passes' T steps are all consumed by then)
     if (it >= kRing)
-      wait_flag(consumed, (uint32_t)(p.kc * (it - kRing + 1)), p.error, p.timeout_ns,
-                (1 << 30) | (3 << 28) | (blockIdx.y << 20) | ((it + 2) << 4));
+      wait_flag_s(consumed, (uint32_t)(p.kc * ((epoch - 1) * p.T + (it - kRing + 1))), sys, p.error, p.timeout_ns,
+                  (1 << 30) | (3 << 28) | (blockIdx.y << 20) | ((it + 2) << 4));
   }
   if (it >= kRing) named_bar_sync(2, kEpiThreads);
   float* slot = ring + (size_t)(it % kRing) * p.Bp * kTileM;
@@ -379,13 +446,13 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
   for (int i = 0; i < kChunks * 8; ++i) slot[(size_t)(c0 + i) * kTileM + row] = v[i];
   fence_proxy_async_global();
   named_bar_sync(1, kEpiThreads);
-  if (et == 0) red_release_gpu_add(done + it, 1);
+  if (et == 0) red_release_s(done + it, 1, sys);
 }
 
 template <int kChunks>
 __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, bool two,
                                             int n_it, int m, int n_act, float* ring, uint32_t* done,
-                                            const uint32_t* consumed) {
+                                            const uint32_t* consumed, bool sys, uint32_t epoch) {
   const int et = threadIdx.x - kEpiBase, N = p.Bp, nco = N / n_act;
   uint32_t rxc = 0;
   if (et == 0 && n_act > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(n_act - 1) * nco * kTileM * 4);
@@ -393,7 +460,8 @@ __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, 
     mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
-    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed);
+    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed, sys,
+                         epoch);
     if (et == 0) cl_trace(p, it, 3);
   }
 }
@@ -401,9 +469,9 @@ __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, 
 // Critical producer: prefetch the off partial of step `it` into rxoff (owned columns).
 __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p, const float* ring,
                                              const uint32_t* done, uint32_t target, int it, int m, int nco,
-                                             uint32_t& offc, int code) {
+                                             uint32_t& offc, int code, bool sys) {
   if (offc > 0) mbar_wait(S.off_empty, (offc - 1) & 1);
-  wait_flag(done + it, target, p.error, p.timeout_ns, code);
+  wait_flag_s(done + it, target, sys, p.error, p.timeout_ns, code);
   fence_proxy_async_global();
   const uint32_t bytes = (uint32_t)(nco * kTileM * 4);
   mbar_arrive_expect_tx(S.off_full, bytes);
@@ -433,27 +501,41 @@ __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool 
 
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_fwd(const FwdLayer* __restrict__ layers, ClParams p) {
-  const int l = blockIdx.y;
-  __shared__ FwdLayer Ly;
-  __shared__ const uint32_t* x_flags;
-  if (threadIdx.x == 0) {
-    Ly = layers[l];
-    x_flags = l > 0 ? layers[l - 1].flags : nullptr;
-  }
-  __syncthreads();
+  const int y = blockIdx.y;
   const int cs = p.cs, kc = p.kc, N = p.Bp;
   const int m = (int)(blockIdx.x % cs), cl_id = (int)(blockIdx.x / cs);
   const int tile = cl_id >> 1;
   const bool crit = (cl_id & 1) == 0;
-  const int nkb_x = Ly.Ipl / 64, nkb_h = p.Hp / 64;
-  const int ko = (nkb_x + kClKBlocks - 1) / kClKBlocks;
+  // whole idle clusters leave at once (no peer waits on them)
+  if (crit ? y >= p.n_crit : !p.offg[y].active) return;
+  const int l = y;  // critical: layer y; off: the group's own target (descriptor)
+  __shared__ FwdLayer Ly;
+  __shared__ ClOff Og;
+  __shared__ ClRing Cr;
+  __shared__ uint32_t epoch_s;
+  if (threadIdx.x == 0) {
+    if (crit) {
+      Ly = layers[y];
+      Cr = p.cring[y];
+    } else {
+      Og = p.offg[y];
+    }
+    epoch_s = *p.epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = epoch_s;
+  const uint32_t flag_target = epoch * (uint32_t)(p.tiles * kc);
+  const int nkb_h = p.Hp / 64;
+  const int nkb_x = crit ? 0 : Og.kdim / 64;
+  const int ko = crit ? Cr.ko : (nkb_x + kClKBlocks - 1) / kClKBlocks;
   const int n_act = crit ? kc : ko;
   const bool active = m < n_act;
+  const int kofs = crit ? Ly.Ipl / 64 : 0;  // the critical slice sits after W's k-blocks in [W|R]
   int kb_lo = 0, kb_hi = 0;
   if (active) {
     if (crit) {
-      kb_lo = nkb_x + m * nkb_h / kc;
-      kb_hi = nkb_x + (m + 1) * nkb_h / kc;
+      kb_lo = kofs + m * nkb_h / kc;
+      kb_hi = kofs + (m + 1) * nkb_h / kc;
     } else {
       kb_lo = m * nkb_x / ko;
       kb_hi = (m + 1) * nkb_x / ko;
@@ -471,32 +553,37 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
   const int row0 = tile * kTileM;
-  const size_t lt = (size_t)l * p.tiles + tile;
-  float* ring = p.offsum + lt * kRing * N * kTileM;
-  uint32_t* done = p.off_done + lt * p.T;
-  uint32_t* consumed = p.consumed + lt * 32;
+  float* ring = crit ? Cr.ring : Og.ring;
+  uint32_t* done = crit ? Cr.done : Og.done;
+  uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
+  ring += (size_t)tile * kRing * N * kTileM;
+  done += (size_t)tile * p.T;
+  consumed += (size_t)tile * 32;
+  const bool sys = crit ? Cr.sys != 0 : Og.sys != 0;
+  const uint32_t done_target = epoch * (uint32_t)ko;
 
   if (active && warp == 0 && lane == 0) {
     // ================= producer: resident A (TMA), then per step the operand (bulk copies)
-    prefetch_tmap(Ly.a[0]);
-    cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
+    const CUtensorMap* amap = crit ? Ly.a[0] : Og.a;
+    prefetch_tmap(amap);
+    cl_load_a(S, amap, kb_lo, kb_hi, row0);
     uint32_t pc = 0, offc = 0;
     for (int t = 0; t < p.T; ++t) {
       cl_trace(p, t, 0);
       if (crit) {
         // the off partial is usually published already: fetch it before waiting for h_{t-1}
-        const bool early = ld_relaxed_gpu(done + t) >= (uint32_t)ko;
-        if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, t, m, nco, offc, wait_code(0, l, t, 3));
-        if (t > 0) wait_flag(&Ly.flags[t - 1], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
+        const bool early = ld_relaxed_s(done + t, sys) >= done_target;
+        if (early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
+        if (t > 0) wait_flag(&Ly.flags[t - 1], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, nkb_x, pc, p.stages, N);
-        if (!early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, t, m, nco, offc, wait_code(0, l, t, 3));
+        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N);
+        if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
       } else {
-        if (l > 0) wait_flag(&x_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
+        if (Og.op_flags) wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.bxsw + (size_t)(Ly.bx_blk_off + t) * Ly.Ipl * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
+        cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
       }
     }
   } else if (active && (warp == 1 || warp == 3)) {
@@ -519,10 +606,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const int et = threadIdx.x - kEpiBase;
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
-        default: cl_off_loop<1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed); break;
+        case 4: cl_off_loop<4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        default: cl_off_loop<1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
       }
     } else {
       // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
@@ -588,7 +675,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           red_release_gpu_add(&Ly.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
-          red_relaxed_gpu_add(consumed, 1);      // ring slot t was copied into rxoff
+          red_relaxed_s(consumed, 1, sys);       // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
         }
         // tapes (read only after the pass; the plain bf16 h feeds the weight-gradient GEMMs)
@@ -624,7 +711,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 // off steps t = T-1 .. 0. Iteration it <-> t = T-1-it.
 template <int kChunks>
 __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
-                                            uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed) {
+                                            uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed,
+                                            bool sys, uint32_t flag_target) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const int N = p.Bp, kc = p.kc, nco = N / kc;
@@ -745,7 +833,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     named_bar_sync(1, kEpiThreads);
     if (et == 0) {
       red_release_gpu_add(&Ly.flags[t], 1);
-      if (off) red_relaxed_gpu_add(consumed, 1);
+      if (off) red_relaxed_s(consumed, 1, sys);
       cl_trace(p, it, 5);
     }
     if (uok) {
@@ -781,32 +869,44 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_bwd(const BwdLayer* __restrict__ layers, ClParams p) {
-  const int l = blockIdx.y;
-  __shared__ BwdLayer Ly;
-  __shared__ const uint32_t* up_flags;
-  if (threadIdx.x == 0) {
-    Ly = layers[l];
-    up_flags = Ly.has_up ? layers[l + 1].flags : nullptr;
-  }
-  __syncthreads();
+  const int y = blockIdx.y;
   const int cs = p.cs, kc = p.kc, N = p.Bp;
   const int m = (int)(blockIdx.x % cs), cl_id = (int)(blockIdx.x / cs);
   const int tile = cl_id >> 1;
   const bool crit = (cl_id & 1) == 0;
+  if (crit ? y >= p.n_crit : !p.offg[y].active) return;  // idle cluster: nobody waits on it
+  const int l = y;
+  __shared__ BwdLayer Ly;
+  __shared__ ClOff Og;
+  __shared__ ClRing Cr;
+  __shared__ uint32_t epoch_s;
+  if (threadIdx.x == 0) {
+    if (crit) {
+      Ly = layers[y];
+      Cr = p.cring[y];
+    } else {
+      Og = p.offg[y];
+    }
+    epoch_s = *p.epoch;
+  }
+  __syncthreads();
+  const uint32_t epoch = epoch_s;
+  const uint32_t flag_target = epoch * (uint32_t)(p.tiles * kc);
   const int G4p = 4 * p.Hp;
-  const int nkb_up = Ly.has_up ? G4p / 64 : 0, nkb_r = G4p / 64;
-  const int ko = (nkb_up + kClKBlocks - 1) / kClKBlocks;
+  const int nkb_r = G4p / 64;
+  const int kofs = crit && Ly.has_up ? G4p / 64 : 0;  // R^T sits after W_{l+1}^T in [W_{l+1}^T | R_l^T]
+  const int nkb_o = crit ? 0 : Og.kdim / 64;
+  const int ko = crit ? Cr.ko : (nkb_o + kClKBlocks - 1) / kClKBlocks;
   const int n_act = crit ? kc : ko;
-  if (n_act == 0) return;  // whole cluster idle (top layer's off cluster): nobody waits on it
   const bool active = m < n_act;
   int kb_lo = 0, kb_hi = 0;
   if (active) {
     if (crit) {
-      kb_lo = nkb_up + m * nkb_r / kc;
-      kb_hi = nkb_up + (m + 1) * nkb_r / kc;
+      kb_lo = kofs + m * nkb_r / kc;
+      kb_hi = kofs + (m + 1) * nkb_r / kc;
     } else {
-      kb_lo = m * nkb_up / ko;
-      kb_hi = (m + 1) * nkb_up / ko;
+      kb_lo = m * nkb_o / ko;
+      kb_hi = (m + 1) * nkb_o / ko;
     }
   }
   const int nkb = kb_hi - kb_lo;
@@ -822,35 +922,40 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
   const int row0 = tile * kTileM;
-  const size_t lt = (size_t)l * p.tiles + tile;
-  float* ring = p.offsum + lt * kRing * N * kTileM;
-  uint32_t* done = p.off_done + lt * p.T;
-  uint32_t* consumed = p.consumed + lt * 32;
+  float* ring = crit ? Cr.ring : Og.ring;
+  uint32_t* done = crit ? Cr.done : Og.done;
+  uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
+  ring += (size_t)tile * kRing * N * kTileM;
+  done += (size_t)tile * p.T;
+  consumed += (size_t)tile * 32;
+  const bool sys = crit ? Cr.sys != 0 : Og.sys != 0;
+  const uint32_t done_target = epoch * (uint32_t)ko;
 
   if (active && warp == 0 && lane == 0) {
-    prefetch_tmap(Ly.a[0]);
-    cl_load_a(S, Ly.a[0], kb_lo, kb_hi, row0);
+    const CUtensorMap* amap = crit ? Ly.a[0] : Og.a;
+    prefetch_tmap(amap);
+    cl_load_a(S, amap, kb_lo, kb_hi, row0);
     uint32_t pc = 0, offc = 0;
     for (int it = 0; it < n_it; ++it) {
       const int t = p.T - 1 - it;
       const bool off = crit && ko > 0 && t >= 0;
       const bool load = !crit || t <= p.T - 2;
       cl_trace(p, it, 0);
-      const bool early = off && ld_relaxed_gpu(done + it) >= (uint32_t)ko;
-      if (early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
+      const bool early = off && ld_relaxed_s(done + it, sys) >= done_target;
+      if (early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
       if (load) {
         if (crit)
-          wait_flag(&Ly.flags[t + 1], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 2));
-        else
-          wait_flag(&up_flags[t], p.flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
+          wait_flag(&Ly.flags[t + 1], flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 2));
+        else if (Og.op_flags)
+          wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, it, 1);
         if (crit)
-          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, nkb_up, pc, p.stages, N);
+          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N);
         else
-          cl_load_b(S, Ly.bupsw + (size_t)t * G4p * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
+          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
       }
-      if (off && !early) cl_fetch_off(S, p, ring, done, (uint32_t)ko, it, m, nco, offc, wait_code(1, l, t, 3));
+      if (off && !early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
     }
   } else if (active && (warp == 1 || warp == 3)) {
     const int j = warp == 3 ? 1 : 0;
@@ -871,17 +976,17 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   } else if (active && warp >= 4) {
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
-        default: cl_off_loop<1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed); break;
+        case 4: cl_off_loop<4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 3: cl_off_loop<3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 2: cl_off_loop<2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        default: cl_off_loop<1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
       }
     } else {
       switch (nco >> 4) {
-        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
-        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
-        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
-        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, two, tile, m, ko, consumed); break;
+        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
+        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
+        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
+        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
       }
     }
   }

@@ -229,7 +229,12 @@ struct rw_ctx {
   size_t smem_f = 0, smem_b = 0;
   // cluster schedule (rec_cluster.cuh)
   ClPlan cl_f, cl_b;
-  DevBuf cl_offsum, cl_done, cl_consumed;
+  DevBuf cl_offsum, cl_done, cl_consumed;  // [L][tiles]... off-partial rings of this context's layers
+  DevBuf cl_epoch;                          // [2] pass counters (forward, backward)
+  DevBuf cl_ring_f, cl_ring_b, cl_off_f, cl_off_b;  // ClRing[L] / ClOff[rows] tables (device)
+  std::vector<ClRing> ring_f_h, ring_b_h;
+  std::vector<ClOff> off_f_h, off_b_h;
+  int rows_f = 0, rows_b = 0;               // grid rows (>= L: pipeline stages add boundary groups)
   std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
   DevBuf xsw;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
@@ -401,6 +406,17 @@ bool plan_cluster(void* kernel, bool fwd, int kc, const std::vector<int>& ko, in
   return true;
 }
 
+void upload_cluster_tables(rw_ctx* x) {
+  auto up = [](DevBuf& d, const void* h, size_t bytes) {
+    d.alloc(std::max<size_t>(bytes, 16));
+    if (bytes) RW_CUDA(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
+  };
+  up(x->cl_ring_f, x->ring_f_h.data(), x->ring_f_h.size() * sizeof(ClRing));
+  up(x->cl_ring_b, x->ring_b_h.data(), x->ring_b_h.size() * sizeof(ClRing));
+  up(x->cl_off_f, x->off_f_h.data(), x->off_f_h.size() * sizeof(ClOff));
+  up(x->cl_off_b, x->off_b_h.data(), x->off_b_h.size() * sizeof(ClOff));
+}
+
 size_t gemm_smem(int planes, int bn, int stages) {
   return 1024 + (size_t)stages * planes * (kTileM + bn) * kRowBytes + (2 * stages + 4) * 8 + 16;
 }
@@ -409,9 +425,38 @@ size_t gemm_smem(int planes, int bn, int stages) {
 // drained into fp32 registers; bf16 runs the whole K in TMEM.
 constexpr int kPromoteKB = 2;
 
+// bf16 grouped GEMMs go to the persistent kernel (gemm_tc.cuh k_gemm_p) unless RW_GEMM_OLD=1;
+// fp32-parity (3xTF32, chunked fp32 promotion) keeps the one-tile-per-CTA kernel.
+template <bool AMN, bool BMN, int BN>
+void launch_gemm_p(const GemmDesc* table_dev, int count, int M, int N, cudaStream_t s) {
+  const size_t stage = (size_t)(kTileM + BN) * kRowBytes;
+  int stages = 8;
+  auto smem_of = [&](int st) { return 1024 + st * stage + (2 * st + 4) * 8 + 16; };
+  while (stages > 2 && smem_of(stages) > (size_t)kSmemLimit) --stages;
+  const size_t smem = smem_of(stages);
+  const int mt = ceil_div(M, kTileM), nt = ceil_div(N, BN);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long tiles = (long long)count * mt * nt;
+  const int grid = (int)std::min<long long>(tiles, sms);
+  auto k = k_gemm_p<AMN, BMN, BN>;
+  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ++g_launches;
+  k<<<grid, 256, smem, s>>>(table_dev, count, mt, nt, stages);
+  RW_CUDA(cudaGetLastError());
+}
+
 template <class P, bool AMN, bool BMN>
 void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
                  cudaStream_t s) {
+  static const bool old = getenv("RW_GEMM_OLD") && atoi(getenv("RW_GEMM_OLD")) != 0;
+  if (P::kPlanes == 1 && !old && (bn == 128 || bn == 256)) {
+    if (bn == 256)
+      launch_gemm_p<AMN, BMN, 256>(table_dev, count, M, N, s);
+    else
+      launch_gemm_p<AMN, BMN, 128>(table_dev, count, M, N, s);
+    return;
+  }
   const size_t smem = gemm_smem(P::kPlanes, bn, stages);
   dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
   ++g_launches;
@@ -594,9 +639,10 @@ void build(rw_ctx* x) {
   }
   if (cl_f || cl_b) {
     const size_t lt = (size_t)L * std::max(Hp / kUnitsPerFwdTile, ceil_div(Hp, kTileM));
-    x->cl_offsum.alloc(lt * kRing * Bp * kTileM * 4);
-    x->cl_done.alloc(lt * T * 4);
-    x->cl_consumed.alloc(lt * 32 * 4);
+    // separate rings / counters per direction: counters are cumulative per direction's epoch
+    x->cl_offsum.alloc(2 * lt * kRing * Bp * kTileM * 4);
+    x->cl_done.alloc(2 * lt * T * 4);
+    x->cl_consumed.alloc(2 * lt * 32 * 4);
   }
   if (cl_f) {
     x->hsw.resize(L);
@@ -709,6 +755,66 @@ void build(rw_ctx* x) {
   x->bwd_layers.alloc(sizeof(BwdLayer) * L);
   RW_CUDA(cudaMemcpy(x->fwd_layers.p, fl.data(), sizeof(FwdLayer) * L, cudaMemcpyHostToDevice));
   RW_CUDA(cudaMemcpy(x->bwd_layers.p, bl.data(), sizeof(BwdLayer) * L, cudaMemcpyHostToDevice));
+
+  // ---- cluster schedule: per-layer off-partial rings and the off-critical group tables
+  if (cl_f || cl_b) {
+    x->cl_epoch.alloc(16);
+    const int tiles_fw = Hp / kUnitsPerFwdTile, tiles_bw = ceil_div(Hp, kTileM);
+    const size_t tmax = (size_t)std::max(tiles_fw, tiles_bw);
+    float* ob = x->cl_offsum.f();
+    uint32_t* db_ = static_cast<uint32_t*>(x->cl_done.p);
+    uint32_t* cb_ = static_cast<uint32_t*>(x->cl_consumed.p);
+    auto ring_of = [&](int l, int ko, int dir) {
+      const size_t ll = (size_t)dir * L + l;
+      ClRing r{};
+      r.ring = ob + ll * tmax * kRing * Bp * kTileM;
+      r.done = db_ + ll * tmax * T;
+      r.consumed = cb_ + ll * tmax * 32;
+      r.ko = ko;
+      r.sys = 0;
+      return r;
+    };
+    if (cl_f) {
+      x->ring_f_h.resize(L);
+      x->off_f_h.assign(L, ClOff{});
+      for (int l = 0; l < L; ++l) {
+        const int Ipl = l == 0 ? Ip : Hp;
+        x->ring_f_h[l] = ring_of(l, ceil_div(Ipl / 64, kClKBlocks), 0);
+        ClOff& o = x->off_f_h[l];
+        o.a = fl[l].a[0];
+        o.kdim = Ipl;
+        o.op = fl[l].bxsw;
+        o.op_blk_off = fl[l].bx_blk_off;
+        o.op_flags = l > 0 ? fl[l - 1].flags : nullptr;
+        o.ring = x->ring_f_h[l].ring;
+        o.done = x->ring_f_h[l].done;
+        o.consumed = x->ring_f_h[l].consumed;
+        o.active = 1;
+      }
+      x->rows_f = L;
+    }
+    if (cl_b) {
+      x->ring_b_h.resize(L);
+      x->off_b_h.assign(L, ClOff{});
+      for (int l = 0; l < L; ++l) {
+        const bool up = l < L - 1;
+        x->ring_b_h[l] = ring_of(l, up ? ceil_div(4 * Hp / 64, kClKBlocks) : 0, 1);
+        if (!up) continue;  // the top layer adds dy instead
+        ClOff& o = x->off_b_h[l];
+        o.a = bl[l].a[0];
+        o.kdim = 4 * Hp;
+        o.op = static_cast<const uint8_t*>(x->dgsw[l + 1].p);
+        o.op_blk_off = 0;
+        o.op_flags = bl[l + 1].flags;
+        o.ring = x->ring_b_h[l].ring;
+        o.done = x->ring_b_h[l].done;
+        o.consumed = x->ring_b_h[l].consumed;
+        o.active = 1;
+      }
+      x->rows_b = L;
+    }
+    upload_cluster_tables(x);
+  }
 
   // ---- GEMM tables: weight gradients (grouped, MN-major A and B) and dx0 (K-major)
   std::vector<GemmDesc> wg;
@@ -915,10 +1021,10 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.cs = pl.cs;
   p.ncomax = pl.ncomax;
   p.stages = pl.stages;
-  p.flag_target = (uint32_t)(p.tiles * p.kc);
-  p.offsum = x->cl_offsum.f();
-  p.off_done = static_cast<uint32_t*>(x->cl_done.p);
-  p.consumed = static_cast<uint32_t*>(x->cl_consumed.p);
+  p.n_crit = x->L;
+  p.cring = static_cast<const ClRing*>((fwd ? x->cl_ring_f : x->cl_ring_b).p);
+  p.offg = static_cast<const ClOff*>((fwd ? x->cl_off_f : x->cl_off_b).p);
+  p.epoch = static_cast<const uint32_t*>(x->cl_epoch.p) + (fwd ? 0 : 1);
   p.error = static_cast<int*>(x->errflag.p);
   p.timeout_ns = 20ULL * 1000000000ULL;
   if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) p.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
@@ -929,12 +1035,15 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   return p;
 }
 
-void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams& p, int L, size_t smem,
-                    cudaStream_t s) {
-  RW_CUDA(cudaMemsetAsync(x->cl_done.p, 0, x->cl_done.bytes, s));
-  RW_CUDA(cudaMemsetAsync(x->cl_consumed.p, 0, x->cl_consumed.bytes, s));
+// Counters of the cluster schedule are cumulative (targets = epoch * per-pass count), so no
+// per-pass memset races a pipeline neighbour that already writes into this context's rings.
+void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams& p, int rows, size_t smem,
+                    cudaStream_t s, bool fwd) {
+  ++g_launches;
+  k_epoch_inc<<<1, 1, 0, s>>>(static_cast<uint32_t*>(x->cl_epoch.p) + (fwd ? 0 : 1));
+  RW_CUDA(cudaGetLastError());
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(p.tiles * 2 * p.cs, L, 1);
+  lc.gridDim = dim3(p.tiles * 2 * p.cs, rows, 1);
   lc.blockDim = dim3(kRecThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
@@ -953,8 +1062,7 @@ void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams&
 template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
   if (x->fwd_sched == RW_SCHED_CLUSTER) {
-    RW_CUDA(cudaMemsetAsync(x->flags_f.p, 0, x->flags_f.bytes, s));
-    launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->L, x->cl_f.smem, s);
+    launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
     return;
   }
   RecParams rp = rec_params(x, true);
@@ -996,8 +1104,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   void* kern = KernelSet<P>::bwd();
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
   if (x->bwd_sched == RW_SCHED_CLUSTER) {
-    RW_CUDA(cudaMemsetAsync(x->flags_b.p, 0, x->flags_b.bytes, s));
-    launch_cluster(x, (void*)k_cl_bwd, x->bwd_layers.p, cl_params(x, false), x->L, x->cl_b.smem, s);
+    launch_cluster(x, (void*)k_cl_bwd, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
     return;
   }
   if (x->bwd_sched == RW_SCHED_PERSISTENT) {
