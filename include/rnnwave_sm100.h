@@ -120,8 +120,9 @@ int rw_get_tape(rw_ctx* ctx, int which, int layer, float* host);
 int rw_upload_inputs(rw_ctx* ctx, const float* x, const float* dy);
 /* One pass on the device, inputs already resident: 0 = forward (inference), 1 = backward
  * (backward_data + weight_update on the resident tape), 2 = both (training forward +
- * backward_data + weight_update). Enqueued on `stream` (cudaStream_t, NULL = legacy default)
- * and returns without synchronising. */
+ * backward_data + weight_update), 3 = forward recording a training tape (a later pass 1
+ * completes it). Enqueued on `stream` (cudaStream_t; NULL = the context's own stream) and
+ * returns without synchronising. */
 int rw_run_pass(rw_ctx* ctx, int pass, void* stream);
 /* Wait for the context's work; reports kernel faults / persistent-kernel timeouts. */
 int rw_sync(rw_ctx* ctx);
@@ -152,6 +153,34 @@ int rw_comm_init(rw_ctx* ctx, int nranks, int rank, const char* id128);
 /* Sum all-reduce of every layer's dW, dR, db on `stream` (NULL = context stream), one NCCL
  * group, enqueued after the pass's weight-gradient GEMMs. */
 int rw_allreduce_grads(rw_ctx* ctx, void* stream);
+
+/* ---- layer pipeline over NVLink (config E; SURVEY §8e "deep stacks split as a layer
+ * pipeline that hands off h_t per timestep peer-to-peer") ----
+ * Stage k is an ordinary context holding layers [l_k, l_k + L_k) (cfg.input = H for k > 0).
+ * At the stage boundary the cluster schedule's off-critical group of a layer -- the GEMM
+ * that does not depend on that layer's own recurrence -- runs on the stage that owns its
+ * operand and writes its per-step partial sums straight into the neighbour's ring over
+ * NVLink (system-scope release counters per step): forward, stage k computes
+ * W_{l_{k+1}} . h_{last,t} for stage k+1; backward, stage k+1 computes W_{l_{k+1}}^T . dG_t for
+ * stage k's last layer. After its forward, stage k also copies its last layer's h sequence
+ * into stage k+1's layer-input buffer (for stage k+1's dW of its first layer).
+ * Requires the cluster schedule (bf16) in both directions. Exported descriptors carry CUDA
+ * IPC handles (cross-process) and raw pointers (same-process stages, tests). */
+typedef struct {
+  char handle[5][64];     /* cudaIpcMemHandle_t of ring data / done / consumed / layer-input
+                             buffer / input-ready counter */
+  uint64_t offset[5];     /* byte offset of the region inside each exported allocation */
+  uint64_t ptr[5];        /* device pointers in the exporting process */
+  int64_t pid;            /* exporting process */
+  int device;             /* exporting device */
+  int ko;                 /* off members the ring expects per step */
+} rw_pp_ring;
+/* dir 0: the forward ring of my first layer (+ my layer-input buffer); dir 1: the backward
+ * ring of my last layer. */
+int rw_pp_export(rw_ctx* ctx, int dir, rw_pp_ring* out);
+/* dir 0: link to the NEXT stage's forward export; W_next is the next stage's first-layer W
+ * (4H x H, reference layout, host). dir 1: link to the PREVIOUS stage's backward export. */
+int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
 int64_t rw_flop_count_cell(int hidden, int input, int batch);

@@ -23,7 +23,7 @@ EXPORTS = [
     "rw_backward_data", "rw_weight_update", "rw_get_tape", "rw_upload_inputs", "rw_run_pass",
     "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count",
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_flop_count_cell",
-    "rw_test_gemm", "rw_test_gemm_last_ms",
+    "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link",
 ]
 
 
@@ -32,6 +32,11 @@ class rw_config(C.Structure):
                 ("steps", C.c_int), ("cell_kind", C.c_int), ("opt_level", C.c_int),
                 ("batch_steps", C.c_int), ("workers", C.c_int), ("seed", C.c_uint64),
                 ("precision", C.c_int), ("schedule", C.c_int)]
+
+
+class rw_pp_ring(C.Structure):
+    _fields_ = [("handle", (C.c_char * 64) * 5), ("offset", C.c_uint64 * 5), ("ptr", C.c_uint64 * 5),
+                ("pid", C.c_int64), ("device", C.c_int), ("ko", C.c_int)]
 
 
 _lib = None
@@ -81,6 +86,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_flop_count_cell.restype = C.c_int64
     L.rw_test_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                                C.c_longlong, vp, C.c_longlong, vp, C.c_longlong, C.c_int]
+    L.rw_pp_export.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring)]
+    L.rw_pp_link.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring), _F]
+    L.rw_pp_debug.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.rw_test_gemm_last_ms.argtypes = []
     L.rw_test_gemm_last_ms.restype = C.c_float
     _lib = L

@@ -79,6 +79,7 @@ struct ClParams {
   int cs;        // cluster size = max(kc, ko over groups)
   int ncomax;    // Bp / min(kc, min ko): receive-slot size (columns) of the carve-up
   int stages;    // B-operand TMA stages
+  int ring;      // off-partial ring depth (kRing; RW_PP_RING for the sequential pipeline test)
   int n_crit;    // critical layer groups (grid rows y < n_crit); rows may also carry off groups
   const ClRing* cring;   // [n_crit]
   const ClOff* offg;     // [gridDim.y]
@@ -87,6 +88,7 @@ struct ClParams {
   unsigned long long timeout_ns;
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
   int trace_steps;
+  int dir;    // 0 forward, 1 backward (error codes)
   int debug;  // RW_CL_DEBUG bits (timing experiments only; results invalid): 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores
 };
@@ -140,6 +142,24 @@ __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
 }
 
 __global__ void k_epoch_inc(uint32_t* e) { *e += 1; }
+// Layer pipeline: tell the next stage (system scope, its memory) that this forward's layer-input
+// copy landed; the next stage waits for its own forward epoch before its weight-gradient GEMMs.
+__global__ void k_pp_signal(uint32_t* peer_ready, const uint32_t* my_epoch) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_ready), "r"(*my_epoch) : "memory");
+}
+__global__ void k_pp_wait(const uint32_t* ready, const uint32_t* my_epoch, int* error, unsigned long long timeout_ns) {
+  const uint32_t e = *my_epoch;
+  const uint64_t t0 = globaltimer();
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicCAS(error, 0, (1 << 30) | (4 << 26));
+      return;
+    }
+  } while (v < e);
+}
 
 __device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
   if (p.trace) {
@@ -187,6 +207,7 @@ __device__ __forceinline__ void wait_flag_s(const uint32_t* flag, uint32_t targe
   while (ld_relaxed_s(flag, true) < target) {
     if (globaltimer() - t0 > timeout_ns) {
       atomicCAS(error, 0, code);
+      atomicMax(error + 1, (int)ld_relaxed_s(flag, true));
       return;
     }
   }
@@ -435,12 +456,12 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
     cl_rx_next(S, m, n_act, nco);
     // ring slot free once every critical member copied step it - kRing (of this pass; the
     // previous passes' T steps are all consumed by then)
-    if (it >= kRing)
-      wait_flag_s(consumed, (uint32_t)(p.kc * ((epoch - 1) * p.T + (it - kRing + 1))), sys, p.error, p.timeout_ns,
-                  (1 << 30) | (3 << 28) | (blockIdx.y << 20) | ((it + 2) << 4));
+    if (it >= p.ring)
+      wait_flag_s(consumed, (uint32_t)(p.kc * ((epoch - 1) * p.T + (it - p.ring + 1))), sys, p.error, p.timeout_ns,
+                  (1 << 30) | (p.dir << 28) | (blockIdx.y << 20) | ((it + 2) << 4) | 4);
   }
-  if (it >= kRing) named_bar_sync(2, kEpiThreads);
-  float* slot = ring + (size_t)(it % kRing) * p.Bp * kTileM;
+  if (it >= p.ring) named_bar_sync(2, kEpiThreads);
+  float* slot = ring + (size_t)(it % p.ring) * p.Bp * kTileM;
   const int c0 = m * nco + half * (nco >> 1);
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i) slot[(size_t)(c0 + i) * kTileM + row] = v[i];
@@ -475,7 +496,7 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
   fence_proxy_async_global();
   const uint32_t bytes = (uint32_t)(nco * kTileM * 4);
   mbar_arrive_expect_tx(S.off_full, bytes);
-  bulk_load(S.rxoff, ring + ((size_t)(it % kRing) * p.Bp + (size_t)m * nco) * kTileM, bytes, S.off_full);
+  bulk_load(S.rxoff, ring + ((size_t)(it % p.ring) * p.Bp + (size_t)m * nco) * kTileM, bytes, S.off_full);
   ++offc;
 }
 
@@ -556,7 +577,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   float* ring = crit ? Cr.ring : Og.ring;
   uint32_t* done = crit ? Cr.done : Og.done;
   uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
-  ring += (size_t)tile * kRing * N * kTileM;
+  ring += (size_t)tile * p.ring * N * kTileM;
   done += (size_t)tile * p.T;
   consumed += (size_t)tile * 32;
   const bool sys = crit ? Cr.sys != 0 : Og.sys != 0;
@@ -925,7 +946,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   float* ring = crit ? Cr.ring : Og.ring;
   uint32_t* done = crit ? Cr.done : Og.done;
   uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
-  ring += (size_t)tile * kRing * N * kTileM;
+  ring += (size_t)tile * p.ring * N * kTileM;
   done += (size_t)tile * p.T;
   consumed += (size_t)tile * 32;
   const bool sys = crit ? Cr.sys != 0 : Og.sys != 0;

@@ -231,10 +231,20 @@ struct rw_ctx {
   ClPlan cl_f, cl_b;
   DevBuf cl_offsum, cl_done, cl_consumed;  // [L][tiles]... off-partial rings of this context's layers
   DevBuf cl_epoch;                          // [2] pass counters (forward, backward)
+  int cl_ring = 4;                          // off-partial ring depth
   DevBuf cl_ring_f, cl_ring_b, cl_off_f, cl_off_b;  // ClRing[L] / ClOff[rows] tables (device)
   std::vector<ClRing> ring_f_h, ring_b_h;
   std::vector<ClOff> off_f_h, off_b_h;
   int rows_f = 0, rows_b = 0;               // grid rows (>= L: pipeline stages add boundary groups)
+  // layer pipeline (rw_pp_*): boundary groups, peer buffers
+  bool pp_prev = false, pp_next = false;     // linked to a previous / next stage
+  bool pp_exported_f = false, pp_exported_b = false;
+  DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
+  std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
+  DevBuf pp_maps_dev;
+  void* pp_next_xop = nullptr;               // next stage's layer-input operand (peer pointer)
+  uint32_t* pp_next_ready = nullptr;         // next stage's input-ready counter (peer pointer)
+  std::vector<void*> pp_opened;              // IPC-opened peer allocations
   std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
   DevBuf xsw;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
@@ -245,8 +255,8 @@ struct rw_ctx {
   std::vector<cudaStream_t> ls;
   std::vector<cudaEvent_t> lev;
   cudaEvent_t fork_ev = nullptr;
-  cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};  // per pass kind
-  long long graph_launches[3] = {0, 0, 0};                   // kernels inside each graph
+  cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // per pass kind
+  long long graph_launches[4] = {0, 0, 0, 0};                         // kernels inside each graph
   bool use_graphs = true;
 
   // state
@@ -640,7 +650,9 @@ void build(rw_ctx* x) {
   if (cl_f || cl_b) {
     const size_t lt = (size_t)L * std::max(Hp / kUnitsPerFwdTile, ceil_div(Hp, kTileM));
     // separate rings / counters per direction: counters are cumulative per direction's epoch
-    x->cl_offsum.alloc(2 * lt * kRing * Bp * kTileM * 4);
+    x->cl_ring = kRing;
+    if (const char* e = getenv("RW_PP_RING")) x->cl_ring = std::max(kRing, atoi(e));
+    x->cl_offsum.alloc(2 * lt * x->cl_ring * Bp * kTileM * 4);
     x->cl_done.alloc(2 * lt * T * 4);
     x->cl_consumed.alloc(2 * lt * 32 * 4);
   }
@@ -767,7 +779,7 @@ void build(rw_ctx* x) {
     auto ring_of = [&](int l, int ko, int dir) {
       const size_t ll = (size_t)dir * L + l;
       ClRing r{};
-      r.ring = ob + ll * tmax * kRing * Bp * kTileM;
+      r.ring = ob + ll * tmax * x->cl_ring * Bp * kTileM;
       r.done = db_ + ll * tmax * T;
       r.consumed = cb_ + ll * tmax * 32;
       r.ko = ko;
@@ -884,11 +896,16 @@ void build(rw_ctx* x) {
 
   // ---- streams
   RW_CUDA(cudaStreamCreateWithFlags(&x->main, cudaStreamNonBlocking));
-  x->ls.resize(L);
-  x->lev.resize(L);
-  for (int l = 0; l < L; ++l) {
-    RW_CUDA(cudaStreamCreateWithFlags(&x->ls[l], cudaStreamNonBlocking));
-    RW_CUDA(cudaEventCreateWithFlags(&x->lev[l], cudaEventDisableTiming));
+  // per-layer streams only for the stepwise wavefront: every stream takes a hardware work queue,
+  // and once a process has more streams than CUDA_DEVICE_MAX_CONNECTIONS (default 8) unrelated
+  // streams share queues -- which serialised two pipeline stages' persistent kernels
+  if (x->fwd_sched == RW_SCHED_STEPWISE || x->bwd_sched == RW_SCHED_STEPWISE) {
+    x->ls.resize(L);
+    x->lev.resize(L);
+    for (int l = 0; l < L; ++l) {
+      RW_CUDA(cudaStreamCreateWithFlags(&x->ls[l], cudaStreamNonBlocking));
+      RW_CUDA(cudaEventCreateWithFlags(&x->lev[l], cudaEventDisableTiming));
+    }
   }
   RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
   if (const char* e = getenv("RW_NO_GRAPHS")) x->use_graphs = atoi(e) == 0;
@@ -947,6 +964,11 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
     ++g_launches;
     k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f());
   }
+  if (x->pp_prev && x->wb_prev.p) {  // backward boundary group: [W_0^T | R_0^T] of this stage
+    ++g_launches;
+    k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
+                                                             x->wb_prev.p, nullptr);
+  }
   ++g_launches;
   k_pack_w0t<<<grid_for((long long)Ip * 4 * Hp), 256, 0, s>>>(x->W[0].f(), H, I, Hp, Ip, x->prec,
                                                              x->w0t.p(0), x->w0t.p(1));
@@ -982,9 +1004,11 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
 // per layer at stage + l*H*B) or zeros.
 void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev) {
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
-  ++g_launches;
-  k_pad_cols<<<grid_for((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
-      x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
+  if (!x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
+    ++g_launches;
+    k_pad_cols<<<grid_for((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
+        x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
+  }
   for (int l = 0; l < L; ++l) {
     const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
     const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
@@ -995,11 +1019,13 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
     k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
-  if (x->fwd_sched == RW_SCHED_CLUSTER) {  // pre-swizzled operand images of x and h0
+  if (x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled operand images of x and h0
     const long long colsT = (long long)Bp * x->T;
     ++g_launches;
     k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(x->x_op.p(0)), x->Ip, Bp, 0, colsT, static_cast<uint8_t*>(x->xsw.p));
+  }
+  if (x->fwd_sched == RW_SCHED_CLUSTER) {
     for (int l = 0; l < L; ++l, ++g_launches)
       k_swizzle_op<<<grid_for((long long)Hp / 8 * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
                                                                Hp, Bp, 0, Bp, static_cast<uint8_t*>(x->hsw[l].p));
@@ -1021,6 +1047,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.cs = pl.cs;
   p.ncomax = pl.ncomax;
   p.stages = pl.stages;
+  p.ring = x->cl_ring;
   p.n_crit = x->L;
   p.cring = static_cast<const ClRing*>((fwd ? x->cl_ring_f : x->cl_ring_b).p);
   p.offg = static_cast<const ClOff*>((fwd ? x->cl_off_f : x->cl_off_b).p);
@@ -1032,6 +1059,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   if (!x->trace_path.empty()) p.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
   p.trace_steps = fwd ? x->T : x->T + 1;
   if (const char* e = getenv("RW_CL_DEBUG")) p.debug = atoi(e);
+  p.dir = fwd ? 0 : 1;
   return p;
 }
 
@@ -1063,6 +1091,13 @@ template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
   if (x->fwd_sched == RW_SCHED_CLUSTER) {
     launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
+    if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
+      RW_CUDA(cudaMemcpyAsync(x->pp_next_xop, static_cast<uint8_t*>(x->hop[x->L - 1].p(0)) + (size_t)x->Hp * x->Bp * 2,
+                              (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
+      ++g_launches;
+      k_pp_signal<<<1, 1, 0, s>>>(x->pp_next_ready, static_cast<const uint32_t*>(x->cl_epoch.p));
+      RW_CUDA(cudaGetLastError());
+    }
     return;
   }
   RecParams rp = rec_params(x, true);
@@ -1149,6 +1184,12 @@ void transpose_planes(rw_ctx* x, const Operand& src, int R, long long C, Operand
 
 template <class P>
 void run_weight_grads(rw_ctx* x, cudaStream_t s) {
+  if (x->pp_prev) {  // layer input of a pipeline stage: copied in by the previous stage
+    ++g_launches;
+    const uint32_t* ep = static_cast<const uint32_t*>(x->cl_epoch.p);
+    k_pp_wait<<<1, 1, 0, s>>>(ep + 2, ep, static_cast<int*>(x->errflag.p), 20ULL * 1000000000ULL);
+    RW_CUDA(cudaGetLastError());
+  }
   const GemmDesc* t = static_cast<const GemmDesc*>(x->gemm_wg.p);
   const int M = 4 * x->Hp, N = std::max(x->Hp, x->Ip);
   if constexpr (P::kPlanes == 2) {
@@ -1180,9 +1221,9 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
   }
   if (pass != 1) {
     PhaseTimer pt(x, 1, s);
-    run_forward_rec<P>(x, s, pass == 2);
+    run_forward_rec<P>(x, s, pass >= 2);
   }
-  if (pass == 0) return;
+  if (pass == 0 || pass == 3) return;
   {
     PhaseTimer pt(x, 2, s);
     run_backward_rec<P>(x, s);
@@ -1249,7 +1290,9 @@ void check_error_flag(rw_ctx* x) {
              "persistent recurrent kernel timed out waiting for a wavefront flag "
              "(%s layer %d step %d, %s flag, last seen count %d)",
              (e[0] >> 28 & 3) ? "backward" : "forward", (e[0] >> 20) & 0xff,
-             ((e[0] >> 4) & 0xffff) - 2, (e[0] & 15) == 1 ? "neighbour-layer" : "own-layer", e[1]);
+             ((e[0] >> 4) & 0xffff) - 2,
+             (e[0] & 15) == 1 ? "neighbour-layer" : (e[0] & 15) == 3 ? "off-partial publication"
+                              : (e[0] & 15) == 4 ? "ring-slot consumed" : "own-layer", e[1]);
     throw RwError{RW_ESTATE, b};
   }
 }
@@ -1515,7 +1558,8 @@ int rw_upload_inputs(rw_ctx* x, const float* xin, const float* dy) {
 
 int rw_run_pass(rw_ctx* x, int pass, void* stream) {
   return guarded(x, [&] {
-    if (pass < 0 || pass > 2) einval("rw_run_pass: pass must be 0 (fwd), 1 (bwd) or 2 (both)");
+    if (pass < 0 || pass > 3)
+      einval("rw_run_pass: pass must be 0 (fwd), 1 (bwd), 2 (both) or 3 (fwd recording a training tape)");
     require_params(x);
     RW_CUDA(cudaSetDevice(x->dev));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
@@ -1527,9 +1571,9 @@ int rw_run_pass(rw_ctx* x, int pass, void* stream) {
       enqueue_pass<PrecTF32x3>(x, pass, s);
     if (pass != 1) {
       x->tape_gen += 1;
-      x->tape_training = pass == 2;
+      x->tape_training = pass >= 2;
     }
-    x->bwd_done = pass != 0;
+    x->bwd_done = pass == 1 || pass == 2;
   });
 }
 
@@ -1554,6 +1598,164 @@ int rw_launch_count(rw_ctx* x, long long* count, int reset) {
   return guarded(x, [&] {
     if (count) *count = g_launches;
     if (reset) g_launches = 0;
+  });
+}
+
+// ---------------------------------------------------------------- layer pipeline
+static void invalidate_graphs(rw_ctx* x) {
+  for (auto& g : x->graphs)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+static void export_region(rw_pp_ring* o, int i, const void* base, const void* region) {
+  cudaIpcMemHandle_t h;
+  RW_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(base)));
+  static_assert(sizeof(h) <= 64, "ipc handle");
+  memcpy(o->handle[i], &h, sizeof h);
+  o->offset[i] = (uint64_t)(static_cast<const uint8_t*>(region) - static_cast<const uint8_t*>(base));
+  o->ptr[i] = (uint64_t)(uintptr_t)region;
+}
+
+static void* open_region(rw_ctx* x, const rw_pp_ring* peer, int i) {
+  if (peer->pid == (int64_t)getpid()) {
+    if (peer->device != x->dev) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) RW_CUDA(e);
+      cudaGetLastError();
+    }
+    return reinterpret_cast<void*>((uintptr_t)peer->ptr[i]);
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, peer->handle[i], sizeof h);
+  void* base = nullptr;
+  RW_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  x->pp_opened.push_back(base);
+  return static_cast<uint8_t*>(base) + peer->offset[i];
+}
+
+extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
+  return guarded(x, [&] {
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+      einval("rw_pp_export: the layer pipeline needs the cluster schedule in both directions (bf16)");
+    if (dir != 0 && dir != 1) einval("rw_pp_export: dir must be 0 (forward) or 1 (backward)");
+    RW_CUDA(cudaSetDevice(x->dev));
+    memset(out, 0, sizeof *out);
+    out->pid = (int64_t)getpid();
+    out->device = x->dev;
+    ClRing& r = dir == 0 ? x->ring_f_h[0] : x->ring_b_h[x->L - 1];
+    if (dir == 1) r.ko = ceil_div(4 * x->Hp / 64, kClKBlocks);  // written by the next stage
+    r.sys = 1;
+    out->ko = r.ko;
+    export_region(out, 0, x->cl_offsum.p, r.ring);
+    export_region(out, 1, x->cl_done.p, r.done);
+    export_region(out, 2, x->cl_consumed.p, r.consumed);
+    if (dir == 0) {
+      export_region(out, 3, x->x_op.p(0), x->x_op.p(0));
+      export_region(out, 4, x->cl_epoch.p, static_cast<uint32_t*>(x->cl_epoch.p) + 2);
+      x->off_f_h[0].active = 0;  // the previous stage computes W_0 . x into this ring
+      x->pp_prev = true;
+      x->pp_exported_f = true;
+    } else {
+      x->pp_exported_b = true;
+    }
+    upload_cluster_tables(x);
+    invalidate_graphs(x);
+  });
+}
+
+extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const float* W_next) {
+  return guarded(x, [&] {
+    if (!peer) einval("rw_pp_link: peer descriptor is null");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+      einval("rw_pp_link: the layer pipeline needs the cluster schedule in both directions (bf16)");
+    RW_CUDA(cudaSetDevice(x->dev));
+    const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
+    const long long G4p = 4LL * Hp;
+    ClOff o{};
+    o.ring = static_cast<float*>(open_region(x, peer, 0));
+    o.done = static_cast<uint32_t*>(open_region(x, peer, 1));
+    o.consumed = static_cast<const uint32_t*>(open_region(x, peer, 2));
+    o.sys = 1;
+    o.active = 1;
+    if (dir == 0) {
+      if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
+      DevBuf wn;
+      wn.alloc(4ULL * H * H * 4);
+      RW_CUDA(cudaMemcpy(wn.p, W_next, 4ULL * H * H * 4, cudaMemcpyHostToDevice));
+      x->wf_next.alloc((size_t)G4p * (Hp + Hp) * 2);
+      ++g_launches;
+      k_pack_wf<<<grid_for(G4p * 2 * Hp), 256>>>(wn.f(), wn.f(), H, H, Hp, Hp, x->prec, x->wf_next.p, nullptr);
+      RW_CUDA(cudaGetLastError());
+      RW_CUDA(cudaDeviceSynchronize());
+      o.kdim = Hp;
+      o.op = static_cast<const uint8_t*>(x->hsw[L - 1].p);
+      o.op_blk_off = 1;
+      o.op_flags = static_cast<const uint32_t*>(x->flags_f.p) + (size_t)(L - 1) * T;
+      x->pp_maps[0] = make_map(x->wf_next.p, x->prec, Hp + Hp, G4p, aK, kTileM);
+      x->pp_next_xop = open_region(x, peer, 3);
+      x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
+      x->pp_next = true;
+    } else {
+      if (!x->pp_prev) einval("rw_pp_link: backward link needs this stage's forward ring exported first");
+      x->wb_prev.alloc((size_t)Hp * 2 * G4p * 2);
+      o.kdim = (int)G4p;
+      o.op = static_cast<const uint8_t*>(x->dgsw[0].p);
+      o.op_blk_off = 0;
+      o.op_flags = static_cast<const uint32_t*>(x->flags_b.p);
+      x->pp_maps[1] = make_map(x->wb_prev.p, x->prec, 2 * G4p, Hp, aK, kTileM);
+      x->dirty = true;  // repack_params packs [W_0^T | R_0^T] into wb_prev
+    }
+    // two fixed map slots [forward boundary, backward boundary], device copy allocated once
+    if (!x->pp_maps_dev.p) x->pp_maps_dev.alloc(2 * sizeof(CUtensorMap));
+    RW_CUDA(cudaMemcpy(x->pp_maps_dev.p, x->pp_maps.data(), 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    o.a = static_cast<const CUtensorMap*>(x->pp_maps_dev.p) + dir;
+    std::vector<ClOff>& offs = dir == 0 ? x->off_f_h : x->off_b_h;
+    offs.resize(L + 1);
+    offs[L] = o;
+    (dir == 0 ? x->rows_f : x->rows_b) = L + 1;
+    // the extra row must still be co-resident
+    const ClPlan& pl = dir == 0 ? x->cl_f : x->cl_b;
+    void* kern = dir == 0 ? (void*)k_cl_fwd : (void*)k_cl_bwd;
+    const int tiles = dir == 0 ? Hp / kUnitsPerFwdTile : ceil_div(Hp, kTileM);
+    const int clusters = max_active_clusters(kern, pl.cs, pl.smem, (L + 1) * tiles * 2 * pl.cs);
+    if (clusters < (L + 1) * tiles * 2) einval("rw_pp_link: the stage plus its boundary group does not fit on the GPU");
+    upload_cluster_tables(x);
+    invalidate_graphs(x);
+  });
+}
+
+// debug: counters of the boundary rings (pipeline bring-up): out[0..1] epochs (fwd, bwd),
+// out[2..4] forward ring of layer 0: done[0..1], consumed; out[6..8] backward ring of the last
+// layer: done[0..1], consumed; out[10..11] rows_f, rows_b; out[12..15] ko/sys of those rings.
+extern "C" int rw_pp_debug(rw_ctx* x, long long* out) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaDeviceSynchronize());
+    uint32_t e[3] = {0, 0, 0};
+    RW_CUDA(cudaMemcpy(e, x->cl_epoch.p, 12, cudaMemcpyDeviceToHost));
+    out[0] = e[0];
+    out[1] = e[1];
+    auto rd = [&](const uint32_t* p) {
+      uint32_t v = 0;
+      RW_CUDA(cudaMemcpy(&v, p, 4, cudaMemcpyDeviceToHost));
+      return (long long)v;
+    };
+    const ClRing& f = x->ring_f_h[0];
+    const ClRing& b = x->ring_b_h[x->L - 1];
+    out[2] = rd(f.done);
+    out[3] = rd(f.done + 1);
+    out[4] = rd(f.consumed);
+    out[6] = rd(b.done);
+    out[7] = rd(b.done + 1);
+    out[8] = rd(b.consumed);
+    out[10] = x->rows_f;
+    out[11] = x->rows_b;
+    out[12] = f.ko;
+    out[13] = f.sys;
+    out[14] = b.ko;
+    out[15] = b.sys;
   });
 }
 

@@ -437,6 +437,21 @@ class Engine:
     def allreduce_grads(self, stream: int | None = None) -> None:
         self._check(self._L.rw_allreduce_grads(self._ctx, C.c_void_p(stream or 0)))
 
+    # -- layer pipeline (rw_pp_*)
+    def pp_export(self, direction: int) -> bytes:
+        """Descriptor of this stage's boundary ring (0: forward ring of the first layer, also its
+        layer-input buffer; 1: backward ring of the last layer), to hand to the neighbour."""
+        r = _lib.rw_pp_ring()
+        self._check(self._L.rw_pp_export(self._ctx, direction, C.byref(r)))
+        return bytes(r)
+
+    def pp_link(self, direction: int, peer: bytes, w_next=None) -> None:
+        """0: link to the next stage's forward export (w_next = its first layer's W, 4H x H);
+        1: link to the previous stage's backward export."""
+        r = _lib.rw_pp_ring.from_buffer_copy(peer)
+        w = as_matrix(w_next) if w_next is not None else None
+        self._check(self._L.rw_pp_link(self._ctx, direction, C.byref(r), _fp(w)))
+
     def launch_count(self, reset: bool = False) -> int:
         n = C.c_longlong()
         self._check(self._L.rw_launch_count(self._ctx, C.byref(n), int(reset)))

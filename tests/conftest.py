@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# more hardware work queues than the default 8: tests create several engines (each with its own
+# stream) in one process, and layer-pipeline stages must run concurrently
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -1,0 +1,68 @@
+"""Layer pipeline: stages must reproduce the single-context run bit for bit -- the
+boundary layer's off-critical GEMM uses the same k-split and reduction order, only on the
+neighbour's GPU. On one GPU the stages run one after another with a ring as deep as T
+(RW_PP_RING, read when the contexts are created): forward of stage 0, 1, ..., then backward of
+the last stage down to stage 0. That exercises the whole data path (rings, counters, the
+layer-input copy and its ready flag) without needing the stages co-resident on the device."""
+import os
+
+import numpy as np
+import pytest
+
+from parity import make_case
+
+pytestmark = pytest.mark.gpu
+
+from oracle import Dims  # noqa: E402
+
+
+@pytest.mark.parametrize("dims,n", [(Dims(4, 128, 96, 32, 10), 2), (Dims(3, 64, 64, 16, 7), 3)],
+                         ids=["L4H128x2", "L3H64x3"])
+def test_pipeline_matches_single_context(dims, n, monkeypatch):
+    from paper_1604_01946_b200 import Engine
+    from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process
+    c, params, x, dy, _, _ = make_case(dims, seed=23, bias=True)
+    H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
+    ref = Engine(c, precision="bf16", schedule="cluster")
+    ref.set_params(params)
+    ref.upload_inputs(x, dy)
+    ref.run_pass(2)
+    ref.sync()
+    y_r = np.zeros((H, B * T), np.float32, order="F")
+    dx_r = np.zeros((I, B * T), np.float32, order="F")
+    dw_r = [np.zeros((4 * H, I if l == 0 else H), np.float32, order="F") for l in range(L)]
+    dr_r = [np.zeros((4 * H, H), np.float32, order="F") for _ in range(L)]
+    db_r = [np.zeros(4 * H, np.float32) for _ in range(L)]
+    ref.read_outputs(y_r, dx_r, dw_r, dr_r, db_r)
+
+    monkeypatch.setenv("RW_PP_RING", str(T))
+    stages = [PipelineStage(c, k, n) for k in range(n)]
+    for s in stages:
+        s.set_params(params)
+    link_in_process(stages, params)
+    zx = np.zeros((H, B * T), np.float32, order="F")
+    for k, s in enumerate(stages):
+        s.engine.upload_inputs(x if k == 0 else zx, dy if k == n - 1 else zx)
+    for rep in range(2):  # twice: the cumulative per-pass counters must carry over
+        for s in stages:          # forward, stage by stage (pass 3: training tape)
+            s.engine.run_pass(3)
+            s.engine.sync()
+        for s in reversed(stages):  # backward from the last stage down
+            s.engine.run_pass(1)
+            s.engine.sync()
+        for s in stages:
+            lo, cnt = s.first, s.count
+            y = np.zeros((H, B * T), np.float32, order="F")
+            dx = np.zeros((I if s.k == 0 else H, B * T), np.float32, order="F")
+            dw = [np.zeros_like(dw_r[l]) for l in range(lo, lo + cnt)]
+            dr = [np.zeros_like(dr_r[l]) for l in range(lo, lo + cnt)]
+            db = [np.zeros_like(db_r[l]) for l in range(lo, lo + cnt)]
+            s.engine.read_outputs(y, dx, dw, dr, db)
+            for j in range(cnt):
+                assert np.array_equal(dw[j], dw_r[lo + j]), (rep, "dW", lo + j)
+                assert np.array_equal(dr[j], dr_r[lo + j]), (rep, "dR", lo + j)
+                assert np.array_equal(db[j], db_r[lo + j]), (rep, "db", lo + j)
+            if s.k == n - 1:
+                assert np.array_equal(y, y_r), (rep, "y")
+            if s.k == 0:
+                assert np.array_equal(dx, dx_r), (rep, "dx0")
