@@ -615,7 +615,11 @@ void build(rw_ctx* x) {
     std::vector<int> ko_f(L), ko_b(L);
     for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
     cl_f = plan_cluster((void*)k_cl_fwd, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
-    const int kc_b = ceil_div(4 * Hp / 64, kClKBlocks);
+    // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
+    // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
+    const int nkb_r = 4 * Hp / 64;
+    int kc_b = ceil_div(nkb_r, kClKBlocks);
+    while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
     for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
     cl_b = plan_cluster((void*)k_cl_bwd, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
   }
