@@ -280,6 +280,7 @@ def run_ours(args) -> None:
     bwd_fl = sum(2 * 4 * H * (H + (H if l < L - 1 else 0)) * B * (T + (1 if True else 0))
                  for l in range(L))  # W_{l+1}^T and R_l^T per cell (+ the dh0 step)
     kern = {"cluster": ("k_cl_fwd", "k_cl_bwd"), "persistent": ("k_lstm_fwd", "k_lstm_bwd"),
+            "layerseq": ("k_gemm_p + k_lstm_fwd", "k_gemm_p + k_lstm_bwd"),
             "stepwise": ("k_lstm_fwd", "k_lstm_bwd")}
     kf = kern.get(desc["fwd_schedule"], ("k_lstm_fwd",))[0]
     kb = kern.get(desc["bwd_schedule"], ("", "k_lstm_bwd"))[1]
@@ -357,7 +358,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster", "layerseq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
                     help="SURVEY §8(d) config; B (the headline) unless sweeping")

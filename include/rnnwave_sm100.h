@@ -55,9 +55,12 @@ typedef enum {
   RW_SCHED_AUTO = 0,       /* cluster, else persistent, else stepwise: the first that fits */
   RW_SCHED_STEPWISE = 1,   /* one fused kernel per (layer, step), CUDA-graph wavefront    */
   RW_SCHED_PERSISTENT = 2, /* one kernel per pass, resident weights, flag wavefront       */
-  RW_SCHED_CLUSTER = 3     /* persistent with split roles per tile: off-critical W.x /
+  RW_SCHED_CLUSTER = 3,    /* persistent with split roles per tile: off-critical W.x /
                               W^T.dG members run ahead, partials exchanged by DSMEM bulk
                               copies (bf16, batch <= 64, hidden <= 512 per member slice) */
+  RW_SCHED_LAYERSEQ = 4    /* large hidden sizes: layer by layer, the input projections of all
+                              steps as one tcgen05 GEMM per layer (W.X_l; backward W_{l+1}^T.dG),
+                              then one fused recurrent-step kernel per step (R.h / R^T.dG only) */
 } rw_schedule;
 
 /* Mirrors LadderConfig (config.hpp:49-97) plus the device knobs. */

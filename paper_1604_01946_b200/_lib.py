@@ -14,7 +14,7 @@ _PF = C.POINTER(_F)
 
 RW_OK, RW_EINVAL, RW_ECUDA, RW_ENOMEM, RW_ENCCL, RW_ESTATE = range(6)
 RW_PREC_BF16, RW_PREC_FP32 = 0, 1
-RW_SCHED_AUTO, RW_SCHED_STEPWISE, RW_SCHED_PERSISTENT, RW_SCHED_CLUSTER = 0, 1, 2, 3
+RW_SCHED_AUTO, RW_SCHED_STEPWISE, RW_SCHED_PERSISTENT, RW_SCHED_CLUSTER, RW_SCHED_LAYERSEQ = 0, 1, 2, 3, 4
 RW_TAPE_X0, RW_TAPE_H, RW_TAPE_C, RW_TAPE_GATES, RW_TAPE_TANH_C, RW_TAPE_DGW, RW_TAPE_Y = range(7)
 
 # every symbol include/rnnwave_sm100.h declares (checked by tests/test_abi.py)

@@ -54,7 +54,7 @@ __host__ __device__ inline long long sw_off(int k, int n, int Bp) {
 }
 
 // Output index mapping of the generic GEMM epilogue.
-enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1 };
+enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1, kRowGatePad = 2 };
 enum ColMode : int { kColIdentity = 0, kColBatchUnpad = 1 };
 
 // One (grouped) GEMM problem: D[MxN] = A[MxK] * B[NxK]^T, fp32 out.
@@ -69,6 +69,7 @@ struct GemmDesc {
   int H, Hp, B, Bp;    // for the unpermute / unpad maps
   int m_valid, n_valid;  // identity-mode bounds
   int accumulate;      // D += result instead of D = result
+  int b_n_off;         // row (N) offset inside the B tensor (e.g. h_{l-1} starts at column block 1)
 };
 
 }  // namespace rw

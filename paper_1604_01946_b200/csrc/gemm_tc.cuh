@@ -54,6 +54,7 @@ __device__ __forceinline__ int gemm_out_row(const GemmDesc& g, int m) {
     const int u = rho_unit(m);
     return u < g.H ? rho_gate(m) * g.H + u : -1;
   }
+  if (g.row_mode == kRowGatePad) return rho_gate(m) * g.Hp + rho_unit(m);
   return m < g.m_valid ? m : -1;
 }
 __device__ __forceinline__ long long gemm_out_col(const GemmDesc& g, int n) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256, 1)
       const int k = kb * P::kAtomK;
       for (int p = 0; p < P::kPlanes; ++p) {
         OperandTile<P, kAMN>::load(st + p * a_bytes, g.a[p], &full[s], m0, kTileM, k + g.a_k_off);
-        OperandTile<P, kBMN>::load(st + P::kPlanes * a_bytes + p * b_bytes, g.b[p], &full[s], n0,
+        OperandTile<P, kBMN>::load(st + P::kPlanes * a_bytes + p * b_bytes, g.b[p], &full[s], n0 + g.b_n_off,
                                    bn, k + g.b_k_off);
       }
     }
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* st = smem + s * stage_bytes;
         const int k = kb * P::kAtomK;
         OperandTile<P, kAMN>::load(st, g.a[0], &full[s], m0, kTileM, k + g.a_k_off);
-        OperandTile<P, kBMN>::load(st + a_bytes, g.b[0], &full[s], n0, BN, k + g.b_k_off);
+        OperandTile<P, kBMN>::load(st + a_bytes, g.b[0], &full[s], n0 + g.b_n_off, BN, k + g.b_k_off);
       }
     }
   } else if (warp == 1) {

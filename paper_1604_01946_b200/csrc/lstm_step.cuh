@@ -57,6 +57,10 @@ struct FwdLayer {
   uint8_t* hsw;              // own h: block t+1 = h_t, block 0 = h0 (Hp x Bp per block)
   const uint8_t* bxsw;       // layer input: x (blocks 0..T-1, Ipl x Bp) or hsw of layer l-1 (+1 block)
   int bx_blk_off;
+  // layer-sequential schedule: the input projection W.x of every step was computed beforehand by
+  // one GEMM into this buffer (gate-major, [col][g*Hp + u]: the gates tape, which the cell
+  // overwrites in place); the step GEMM then covers only R.h_{t-1}
+  const float* zx;
 };
 
 struct BwdLayer {
@@ -78,6 +82,10 @@ struct BwdLayer {
   // cluster schedule: pre-swizzled bf16 dG step blocks (4Hp x Bp per block, K index rho)
   uint8_t* dgsw;
   const uint8_t* bupsw;      // dgsw of layer l+1
+  // layer-sequential schedule: d_above = W_{l+1}^T dG_{l+1} for every step from one GEMM
+  // ([col][u], Hp x Bp T); the step GEMM covers only R^T dG_{t+1}, at A k-block offset akofs
+  const float* dabove;
+  int akofs;
 };
 
 struct RecParams {
@@ -404,7 +412,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int rank = (int)(blockIdx.x % ks);
   const int tile = (int)(blockIdx.x / ks);
   const int N = p.Bp;
-  const int nkb0 = Ly.Ipl / P::kAtomK;
+  const bool zxm = Ly.zx != nullptr;
+  const int akofs = zxm ? Ly.Ipl / P::kAtomK : 0;  // A k-block of R (after W) in [W|R]
+  const int nkb0 = zxm ? 0 : Ly.Ipl / P::kAtomK;
   const int nkb = nkb0 + p.Hp / P::kAtomK;
   const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
   const int my_nkb = kb_hi - kb_lo;
@@ -436,7 +446,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       for (int kb = kb_lo; kb < kb_hi; ++kb)
         for (int pl = 0; pl < P::kPlanes; ++pl)
           tma_load_2d(S.a_res + (kb - kb_lo) * a_stage + pl * a_bytes, Ly.a[pl], S.a_full,
-                      kb * P::kAtomK, row0);
+                      (kb + akofs) * P::kAtomK, row0);
     }
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
@@ -473,7 +483,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                         t * p.Bp);
           if (!p.resident)
             tma_load_2d(S.a_res + s * a_stage + pl * a_bytes, Ly.a[pl], &S.full[s],
-                        kb * P::kAtomK, row0);
+                        (kb + akofs) * P::kAtomK, row0);
         }
       }
       trace_stamp(p, it, 1);
@@ -552,10 +562,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         for (int k = 0; k < 8; ++k) {
           const int cl = cg + 8 * k;
           if (cl >= nco) break;
-          const float ai = xchg_sum(S, ks, nco, cl, 0 * 32 + j) + bi;
-          const float af = xchg_sum(S, ks, nco, cl, 1 * 32 + j) + bf;
-          const float ao = xchg_sum(S, ks, nco, cl, 2 * 32 + j) + bo;
-          const float ac = xchg_sum(S, ks, nco, cl, 3 * 32 + j) + bc;
+          float zi = 0.0f, zf = 0.0f, zo = 0.0f, zc = 0.0f;
+          if (zxm) {  // (zw + zr) + b, cells.hpp:240
+            const float* zp = Ly.zx + (colb + cl) * G4 + u;
+            zi = zp[0];
+            zf = zp[Hp];
+            zo = zp[2 * Hp];
+            zc = zp[3 * Hp];
+          }
+          const float ai = (zxm ? zi + xchg_sum(S, ks, nco, cl, 0 * 32 + j) : xchg_sum(S, ks, nco, cl, 0 * 32 + j)) + bi;
+          const float af = (zxm ? zf + xchg_sum(S, ks, nco, cl, 1 * 32 + j) : xchg_sum(S, ks, nco, cl, 1 * 32 + j)) + bf;
+          const float ao = (zxm ? zo + xchg_sum(S, ks, nco, cl, 2 * 32 + j) : xchg_sum(S, ks, nco, cl, 2 * 32 + j)) + bo;
+          const float ac = (zxm ? zc + xchg_sum(S, ks, nco, cl, 3 * 32 + j) : xchg_sum(S, ks, nco, cl, 3 * 32 + j)) + bc;
           const float iv = act_sigmoid<P>(ai);
           const float fv = act_sigmoid<P>(af);
           const float ov = act_sigmoid<P>(ao);
@@ -616,7 +634,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int tile = (int)(blockIdx.x / ks);
   const int N = p.Bp;
   const int G4p = 4 * p.Hp;
-  const int nkb0 = Ly.has_up ? G4p / P::kAtomK : 0;
+  const bool dam = Ly.dabove != nullptr;
+  const int akofs = dam ? Ly.akofs : 0;
+  const int nkb0 = (Ly.has_up && !dam) ? G4p / P::kAtomK : 0;
   const int nkb = nkb0 + G4p / P::kAtomK;
   const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
   const int my_nkb = kb_hi - kb_lo;
@@ -654,7 +674,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       for (int kb = kb_lo; kb < kb_hi; ++kb)
         for (int pl = 0; pl < P::kPlanes; ++pl)
           tma_load_2d(S.a_res + (kb - kb_lo) * a_stage + pl * a_bytes, Ly.a[pl], S.a_full,
-                      kb * P::kAtomK, row0);
+                      (kb + akofs) * P::kAtomK, row0);
     }
     uint32_t pc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
@@ -691,7 +711,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                         (t + 1) * p.Bp);
           if (!p.resident)
             tma_load_2d(S.a_res + s * a_stage + pl * a_bytes, Ly.a[pl], &S.full[s],
-                        kb * P::kAtomK, row0);
+                        (kb + akofs) * P::kAtomK, row0);
         }
         ++pc;
       }
@@ -788,7 +808,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               ptc[k] = Ly.tanhc[col * Hp + u];
               pcp[k] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
               dci[k] = (t == p.T - 1) ? 0.0f : Ly.carry_c[n * Hp + u];
-              if (Ly.dy && u < p.H && n < p.B) dyv[k] = Ly.dy[((long long)t * p.B + n) * p.H + u];
+              if (dam)
+                dyv[k] = Ly.dabove[col * Hp + u];
+              else if (Ly.dy && u < p.H && n < p.B)
+                dyv[k] = Ly.dy[((long long)t * p.B + n) * p.H + u];
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -800,7 +823,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                 Ly.dc0[n * Hp + u] = dci[k];
                 continue;
               }
-              const float dh = Ly.dy ? dyv[k] + acc[k] : acc[k];
+              const float dh = (Ly.dy || dam) ? dyv[k] + acc[k] : acc[k];  // d_above + carry_h
               const float q1 = dh * po[k];
               const float s0 = ptc[k] * ptc[k];
               const float s1 = 1.0f - s0;

@@ -247,7 +247,8 @@ struct rw_ctx {
   std::vector<void*> pp_opened;              // IPC-opened peer allocations
   std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
   DevBuf xsw;
-  int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4;
+  int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4, bn_ls = 256;
+  DevBuf gemm_lsf, gemm_lsb, dabove;  // layer-sequential schedule
   size_t smem_wg = 0, smem_dx = 0;
 
   // streams / events / graphs
@@ -626,9 +627,23 @@ void build(rw_ctx* x) {
   if (c.schedule == RW_SCHED_CLUSTER && !(cl_f && cl_b))
     einval("cluster schedule does not fit this configuration (bf16, batch <= 64, owned columns multiple of 16, "
            "CTAs and clusters co-resident)");
-  const int want = c.schedule == RW_SCHED_CLUSTER ? RW_SCHED_AUTO : c.schedule;
-  RecPlan pf = plan_recurrent(kf, want, x->planes, kbf_max, tiles_f, L, Bp, sms, "RW_FWD_KSPLIT");
-  RecPlan pb = plan_recurrent(kb, want, x->planes, kbb_max, tiles_b, L, Bp, sms, "RW_BWD_KSPLIT");
+  int want = c.schedule == RW_SCHED_CLUSTER ? RW_SCHED_AUTO : c.schedule;
+  bool ls = c.schedule == RW_SCHED_LAYERSEQ;
+  // The layer-sequential schedule is opt-in: measured on B200 it is slower than the wavefront
+  // schedules at every configured shape (E: 147 vs 71 ms per pass; the per-step GEMM with the
+  // full batch as N moves ~1 MB of operands per CTA per step; profiles/r01/README.md).
+  if (ls) {
+    want = RW_SCHED_STEPWISE;
+    cl_f = cl_b = false;
+  }
+  RecPlan pf = plan_recurrent(kf, want, x->planes, ls ? Hp / x->atomK : kbf_max, tiles_f, ls ? 1 : L, Bp, sms,
+                              "RW_FWD_KSPLIT");
+  RecPlan pb = plan_recurrent(kb, want, x->planes, ls ? (int)(G4p / x->atomK) : kbb_max, tiles_b, ls ? 1 : L, Bp,
+                              sms, "RW_BWD_KSPLIT");
+  if (ls) {
+    pf.sched = pb.sched = RW_SCHED_LAYERSEQ;
+    x->dabove.alloc((size_t)Hp * colsT * 4);
+  }
   x->fwd_sched = pf.sched;
   x->ks_f = pf.ks;
   x->res_f = pf.resident;
@@ -678,8 +693,8 @@ void build(rw_ctx* x) {
     while ((long long)ceil_div(kb_per_cta, acc_kb) * Bp > 512) acc_kb *= 2;
     n_acc = std::max(1, ceil_div(kb_per_cta, acc_kb));
   };
-  acc_plan(ceil_div(kbf_max, x->ks_f), x->acckb_f, x->nacc_f);
-  acc_plan(ceil_div(kbb_max, x->ks_b), x->acckb_b, x->nacc_b);
+  acc_plan(ceil_div(ls ? Hp / x->atomK : kbf_max, x->ks_f), x->acckb_f, x->nacc_f);
+  acc_plan(ceil_div(ls ? (int)(G4p / x->atomK) : kbb_max, x->ks_b), x->acckb_b, x->nacc_b);
   int slices_b = ceil_div(Bp, kXChunk) * x->ks_b * 2;
   for (int l = 0; l < L; ++l) x->dbp[l].alloc((size_t)slices_b * G4p * 4);
 
@@ -688,6 +703,10 @@ void build(rw_ctx* x) {
   std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
       m_dgMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
+  // layer-sequential GEMMs: B operands (layer inputs / dG) as K-major boxes of bn_ls columns
+  x->bn_ls = x->prec == kBF16 ? 256 : 64;  // tf32: the chunked-promotion GEMM variant
+  int m_xLS[2] = {0, 0};
+  std::vector<int> m_hopLS(2 * L), m_dgLS(2 * L);
   std::vector<int> m_dgT(2 * L), m_hT(2 * L);
   x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 64;
   x->bn_wg = x->prec == kBF16 ? 128 : 64;
@@ -712,6 +731,13 @@ void build(rw_ctx* x) {
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
     m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
     m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, x->bn_dx));
+    if (ls) {
+      m_xLS[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, x->bn_ls));
+      for (int l = 0; l < L; ++l) {
+        m_hopLS[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, x->bn_ls));
+        m_dgLS[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, x->bn_ls));
+      }
+    }
   }
   x->maps_dev.alloc(x->maps.size() * sizeof(CUtensorMap));
   RW_CUDA(cudaMemcpy(x->maps_dev.p, x->maps.data(), x->maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
@@ -739,6 +765,7 @@ void build(rw_ctx* x) {
     F.gates = x->gates[l].f();
     F.tanhc = x->tanhc[l].f();
     F.flags = ff + (size_t)l * T;
+    F.zx = ls ? x->gates[l].f() : nullptr;  // the input GEMM writes W.x into the gates tape
     if (!x->hsw.empty()) {
       F.hsw = static_cast<uint8_t*>(x->hsw[l].p);
       F.bxsw = l == 0 ? static_cast<const uint8_t*>(x->xsw.p) : static_cast<const uint8_t*>(x->hsw[l - 1].p);
@@ -762,6 +789,10 @@ void build(rw_ctx* x) {
     Bd.dh0 = x->dh0[l].f();
     Bd.dc0 = x->dc0[l].f();
     Bd.flags = fb + (size_t)l * T;
+    if (ls && l < L - 1) {
+      Bd.dabove = x->dabove.f();
+      Bd.akofs = (int)(G4p / aK);  // R^T after W_{l+1}^T in the packed [W_{l+1}^T | R_l^T]
+    }
     if (!x->dgsw.empty()) {
       Bd.dgsw = static_cast<uint8_t*>(x->dgsw[l].p);
       Bd.bupsw = l < L - 1 ? static_cast<const uint8_t*>(x->dgsw[l + 1].p) : nullptr;
@@ -873,6 +904,57 @@ void build(rw_ctx* x) {
     wg.push_back(r);
   }
   x->n_wg = (int)wg.size();
+  if (ls) {  // per-layer input GEMMs (forward W_l.X_l, backward W_{l+1}^T.dG_{l+1})
+    std::vector<GemmDesc> lf(L), lb(L);
+    for (int l = 0; l < L; ++l) {
+      const int Ipl = l == 0 ? Ip : Hp;
+      GemmDesc& f = lf[l];
+      for (int p = 0; p < 2; ++p) {
+        const int q = p % x->planes;
+        f.a[p] = mp(m_wf[2 * l + q], p);
+        f.b[p] = l == 0 ? mp(m_xLS[q], p) : mp(m_hopLS[2 * (l - 1) + q], p);
+      }
+      f.M = (int)G4p;
+      f.N = (int)colsT;
+      f.K = Ipl;
+      f.b_n_off = l == 0 ? 0 : Bp;  // h_{l-1,t} is column block t+1
+      f.d = x->gates[l].f();
+      f.ldd = G4p;
+      f.row_mode = kRowGatePad;
+      f.col_mode = kColIdentity;
+      f.H = H;
+      f.Hp = Hp;
+      f.B = B;
+      f.Bp = Bp;
+      f.m_valid = (int)G4p;
+      f.n_valid = (int)colsT;
+      if (l < L - 1) {
+        GemmDesc& g = lb[l];
+        for (int p = 0; p < 2; ++p) {
+          const int q = p % x->planes;
+          g.a[p] = mp(m_wb[2 * l + q], p);
+          g.b[p] = mp(m_dgLS[2 * (l + 1) + q], p);
+        }
+        g.M = Hp;
+        g.N = (int)colsT;
+        g.K = (int)G4p;
+        g.d = x->dabove.f();
+        g.ldd = Hp;
+        g.row_mode = kRowIdentity;
+        g.col_mode = kColIdentity;
+        g.H = H;
+        g.Hp = Hp;
+        g.B = B;
+        g.Bp = Bp;
+        g.m_valid = Hp;
+        g.n_valid = (int)colsT;
+      }
+    }
+    x->gemm_lsf.alloc(sizeof(GemmDesc) * L);
+    x->gemm_lsb.alloc(sizeof(GemmDesc) * L);
+    RW_CUDA(cudaMemcpy(x->gemm_lsf.p, lf.data(), sizeof(GemmDesc) * L, cudaMemcpyHostToDevice));
+    RW_CUDA(cudaMemcpy(x->gemm_lsb.p, lb.data(), sizeof(GemmDesc) * L, cudaMemcpyHostToDevice));
+  }
   x->gemm_wg.alloc(sizeof(GemmDesc) * wg.size());
   RW_CUDA(cudaMemcpy(x->gemm_wg.p, wg.data(), sizeof(GemmDesc) * wg.size(), cudaMemcpyHostToDevice));
   GemmDesc dx{};
@@ -1093,6 +1175,23 @@ void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams&
 
 template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
+  if (x->fwd_sched == RW_SCHED_LAYERSEQ) {
+    RecParams rp = rec_params(x, true);
+    void* kern = KernelSet<P>::fwd();
+    rp.persistent = 0;
+    rp.resident = 0;
+    rp.n_steps = 1;
+    const GemmDesc* G = static_cast<const GemmDesc*>(x->gemm_lsf.p);
+    for (int l = 0; l < x->L; ++l) {
+      launch_gemm<P, false, false>(G + l, 1, 4 * x->Hp, x->Bp * x->T, x->bn_ls, gemm_stages(x->planes, x->bn_ls), s);
+      rp.layer_base = l;
+      for (int t = 0; t < x->T; ++t) {
+        rp.t_first = t;
+        launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, s);
+      }
+    }
+    return;
+  }
   if (x->fwd_sched == RW_SCHED_CLUSTER) {
     launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
     if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
@@ -1142,6 +1241,22 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   RecParams rp = rec_params(x, false);
   void* kern = KernelSet<P>::bwd();
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
+  if (x->bwd_sched == RW_SCHED_LAYERSEQ) {
+    rp.persistent = 0;
+    rp.resident = 0;
+    rp.n_steps = 1;
+    const GemmDesc* G = static_cast<const GemmDesc*>(x->gemm_lsb.p);
+    for (int l = x->L - 1; l >= 0; --l) {
+      if (l < x->L - 1)
+        launch_gemm<P, false, false>(G + l, 1, x->Hp, x->Bp * x->T, x->bn_ls, gemm_stages(x->planes, x->bn_ls), s);
+      rp.layer_base = l;
+      for (int t = x->T - 1; t >= -1; --t) {
+        rp.t_first = t;
+        launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_b, s);
+      }
+    }
+    return;
+  }
   if (x->bwd_sched == RW_SCHED_CLUSTER) {
     launch_cluster(x, (void*)k_cl_bwd, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
     return;

@@ -269,7 +269,8 @@ class Gradients:
 # ------------------------------------------------------------------ engine
 PRECISIONS = {"bf16": _lib.RW_PREC_BF16, "fp32": _lib.RW_PREC_FP32}
 SCHEDULES = {"auto": _lib.RW_SCHED_AUTO, "stepwise": _lib.RW_SCHED_STEPWISE,
-             "persistent": _lib.RW_SCHED_PERSISTENT, "cluster": _lib.RW_SCHED_CLUSTER}
+             "persistent": _lib.RW_SCHED_PERSISTENT, "cluster": _lib.RW_SCHED_CLUSTER,
+             "layerseq": _lib.RW_SCHED_LAYERSEQ}
 
 
 def nccl_unique_id() -> bytes:
@@ -476,6 +477,6 @@ class Engine:
     def describe(self) -> dict:
         a, b, k1, k2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         self._check(self._L.rw_describe(self._ctx, C.byref(a), C.byref(b), C.byref(k1), C.byref(k2)))
-        names = {1: "stepwise", 2: "persistent", 3: "cluster"}
+        names = {1: "stepwise", 2: "persistent", 3: "cluster", 4: "layerseq"}
         return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
                 "fwd_ksplit": k1.value, "bwd_ksplit": k2.value}

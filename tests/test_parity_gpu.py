@@ -19,7 +19,7 @@ SMALL = [
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-@pytest.mark.parametrize("schedule", ["stepwise", "persistent", "cluster"])
+@pytest.mark.parametrize("schedule", ["stepwise", "persistent", "cluster", "layerseq"])
 @pytest.mark.parametrize("dims", SMALL, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
 def test_small_configs(reference, precision, schedule, dims):
     from paper_1604_01946_b200 import Engine
@@ -67,6 +67,18 @@ def test_cluster_configs(reference, dims):
     ref = run_reference(reference, c, params, x, dy, h0, c0)
     worst = assert_within(compare(dev, ref, c), "bf16")
     print(f"cluster {dims}: {eng.describe()} worst {worst}")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_layerseq_large(reference, precision):
+    """Layer-sequential schedule at a larger hidden size with several split-K ranks."""
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(Dims(3, 1024, 768, 64, 6), seed=29, bias=True, state=True)
+    eng = Engine(c, precision=precision, schedule="layerseq")
+    assert eng.describe()["fwd_schedule"] == "layerseq"
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), precision)
 
 
 @pytest.mark.slow
