@@ -231,12 +231,17 @@ def run_ours(args) -> None:
         eng.set_profiling(False)
 
         # ---- e2e through the C-ABI with host buffers: H2D inputs, pass, D2H results
-        y = np.zeros((c["hidden"], c["batch"] * c["steps"]), np.float32, order="F")
-        dx0 = np.zeros((c["input"], c["batch"] * c["steps"]), np.float32, order="F")
-        dw = [np.zeros((4 * c["hidden"], c["input"] if l == 0 else c["hidden"]), np.float32, order="F")
-              for l in range(c["layers"])]
-        dr = [np.zeros((4 * c["hidden"], c["hidden"]), np.float32, order="F") for _ in range(c["layers"])]
-        db = [np.zeros(4 * c["hidden"], np.float32) for _ in range(c["layers"])]
+        def pinned(rows, cols=None):
+            """Column-major float32 host array in pinned (page-locked) memory: DMA at full rate."""
+            if cols is None:
+                return torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
+            return torch.zeros(cols, rows, dtype=torch.float32).pin_memory().numpy().T
+
+        y = pinned(c["hidden"], c["batch"] * c["steps"])
+        dx0 = pinned(c["input"], c["batch"] * c["steps"])
+        dw = [pinned(4 * c["hidden"], c["input"] if l == 0 else c["hidden"]) for l in range(c["layers"])]
+        dr = [pinned(4 * c["hidden"], c["hidden"]) for _ in range(c["layers"])]
+        db = [pinned(4 * c["hidden"]) for _ in range(c["layers"])]
         xh = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).pin_memory()
         dyh = torch.from_numpy(np.asfortranarray(dy).ravel(order="F")).pin_memory()
         h2d = xh.numel() * 4 + dyh.numel() * 4

@@ -1700,16 +1700,27 @@ int rw_read_outputs(rw_ctx* x, float* y, float* dx0, float* const* dW, float* co
                     float* const* db) {
   return guarded(x, [&] {
     RW_CUDA(cudaSetDevice(x->dev));
-    RW_CUDA(cudaDeviceSynchronize());
+    RW_CUDA(cudaDeviceSynchronize());  // the pass may have been enqueued on a caller's stream
     check_error_flag(x);
-    if (y) d2h_unpad(x, x->h[x->L - 1].f(), x->Hp, x->Bp, x->Bp, 1, x->H, x->B, x->T, y);
-    if (dx0) RW_CUDA(cudaMemcpy(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost));
+    // all copies queued on the context stream, one synchronisation (full DMA rate into pinned
+    // host buffers; pageable ones are staged by the driver)
+    cudaStream_t s = x->main;
+    if (y) {
+      const long long n = (long long)x->H * x->B * x->T;
+      ++g_launches;
+      k_unpad_cols<<<grid_for(n), 256, 0, s>>>(x->h[x->L - 1].f(), x->Hp, x->Bp, x->Bp, 1, x->H, x->B, x->T,
+                                               x->y_raw.f());
+      RW_CUDA(cudaGetLastError());
+      RW_CUDA(cudaMemcpyAsync(y, x->y_raw.p, n * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (dx0) RW_CUDA(cudaMemcpyAsync(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost, s));
     for (int l = 0; l < x->L; ++l) {
       const int Il = l == 0 ? x->I : x->H;
-      if (dW && dW[l]) RW_CUDA(cudaMemcpy(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost));
-      if (dR && dR[l]) RW_CUDA(cudaMemcpy(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost));
-      if (db && db[l]) RW_CUDA(cudaMemcpy(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost));
+      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost, s));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost, s));
+      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost, s));
     }
+    RW_CUDA(cudaStreamSynchronize(s));
   });
 }
 
