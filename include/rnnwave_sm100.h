@@ -127,6 +127,15 @@ int rw_upload_inputs(rw_ctx* ctx, const float* x, const float* dy);
  * completes it). Enqueued on `stream` (cudaStream_t; NULL = the context's own stream) and
  * returns without synchronising. */
 int rw_run_pass(rw_ctx* ctx, int pass, void* stream);
+/* One training step end to end with host buffers -- the public call a training loop makes:
+ * upload x and dy, forward + backward_data + weight_update, read back y, dx0, dW, dR, db (any
+ * output may be NULL). Asynchronous and pipelined: the next step's uploads overlap this
+ * step's compute and this step's read-back overlaps the next step's compute (pinned host
+ * memory for full DMA rate). Host outputs are complete after rw_train_wait; inputs must stay
+ * unchanged until the step's upload ran (rw_train_wait, or the next-but-one step). */
+int rw_train_step(rw_ctx* ctx, const float* x, const float* dy, float* y, float* dx0,
+                  float* const* dW, float* const* dR, float* const* db);
+int rw_train_wait(rw_ctx* ctx);
 /* Wait for the context's work; reports kernel faults / persistent-kernel timeouts. */
 int rw_sync(rw_ctx* ctx);
 /* Enable per-phase CUDA-event timing of rw_run_pass (0 = off). When on, rw_phase_times

@@ -24,6 +24,7 @@ EXPORTS = [
     "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count",
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link",
+    "rw_train_step", "rw_train_wait",
 ]
 
 
@@ -89,6 +90,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_pp_export.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring)]
     L.rw_pp_link.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring), _F]
     L.rw_pp_debug.argtypes = [vp, C.POINTER(C.c_longlong)]
+    L.rw_train_step.argtypes = [vp, _F, _F, _F, _F, _PF, _PF, _PF]
+    L.rw_train_wait.argtypes = [vp]
     L.rw_test_gemm_last_ms.argtypes = []
     L.rw_test_gemm_last_ms.restype = C.c_float
     _lib = L

@@ -253,6 +253,10 @@ struct rw_ctx {
 
   // streams / events / graphs
   cudaStream_t main = nullptr;
+  // rw_train_step: copy streams and the events that order the pipelined host round trip
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_x = nullptr, ev_y_staged = nullptr, ev_y_out = nullptr, ev_dy = nullptr,
+              ev_bwd = nullptr, ev_out = nullptr;
   std::vector<cudaStream_t> ls;
   std::vector<cudaEvent_t> lev;
   cudaEvent_t fork_ev = nullptr;
@@ -1478,6 +1482,10 @@ rw_ctx::~rw_ctx() {
   for (auto e : lev) cudaEventDestroy(e);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (main) cudaStreamDestroy(main);
+  if (cp_in) cudaStreamDestroy(cp_in);
+  if (cp_out) cudaStreamDestroy(cp_out);
+  for (cudaEvent_t e : {ev_fwd, ev_x, ev_y_staged, ev_y_out, ev_dy, ev_bwd, ev_out})
+    if (e) cudaEventDestroy(e);
 }
 
 // ====================================================================== C-ABI
@@ -1672,6 +1680,90 @@ int rw_upload_inputs(rw_ctx* x, const float* xin, const float* dy) {
     if (xin) RW_CUDA(cudaMemcpy(x->x_raw.p, xin, (size_t)x->I * x->B * x->T * 4, cudaMemcpyHostToDevice));
     if (dy) RW_CUDA(cudaMemcpy(x->dy_raw.p, dy, (size_t)x->H * x->B * x->T * 4, cudaMemcpyHostToDevice));
     x->inputs_uploaded = true;
+  });
+}
+
+// Pipelined training step with host buffers (the public end-to-end call; pinned host memory
+// gives full DMA rate). Inputs of step i+1 upload while step i computes, outputs of step i
+// download while step i+1 computes:
+//   cp_in : [wait fwd(i-1)] x -> x_raw                                   -> ev_x
+//   main  : [wait ev_x] forward (pass 3) -> ev_fwd; [wait y_out(i-1)] unpad y -> ev_y_staged
+//   cp_out: [wait ev_y_staged] y_raw -> y                                -> ev_y_out
+//   cp_in : [wait bwd(i-1)] dy -> dy_raw                                 -> ev_dy
+//   main  : [wait ev_dy, out(i-1)] backward + weight update (pass 1)     -> ev_bwd
+//   cp_out: [wait ev_bwd] dx0, dW, dR, db -> host                        -> ev_out
+// Host buffers are written asynchronously: they are complete after rw_train_wait.
+static void allreduce_grads(rw_ctx* x, cudaStream_t s);
+static void train_streams(rw_ctx* x) {
+  if (x->cp_in) return;
+  RW_CUDA(cudaStreamCreateWithFlags(&x->cp_in, cudaStreamNonBlocking));
+  RW_CUDA(cudaStreamCreateWithFlags(&x->cp_out, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&x->ev_fwd, &x->ev_x, &x->ev_y_staged, &x->ev_y_out, &x->ev_dy, &x->ev_bwd, &x->ev_out})
+    RW_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+}
+
+extern "C" int rw_train_step(rw_ctx* x, const float* xin, const float* dy, float* y, float* dx0, float* const* dW,
+                             float* const* dR, float* const* db) {
+  return guarded(x, [&] {
+    if (!xin || !dy) einval("rw_train_step: x and dy are required (expected host buffers)");
+    require_params(x);
+    RW_CUDA(cudaSetDevice(x->dev));
+    train_streams(x);
+    const size_t xb = (size_t)x->I * x->B * x->T * 4, yb = (size_t)x->H * x->B * x->T * 4;
+    RW_CUDA(cudaStreamWaitEvent(x->cp_in, x->ev_fwd, 0));
+    RW_CUDA(cudaMemcpyAsync(x->x_raw.p, xin, xb, cudaMemcpyHostToDevice, x->cp_in));
+    RW_CUDA(cudaEventRecord(x->ev_x, x->cp_in));
+    RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_x, 0));
+    if (x->prec == kBF16)
+      enqueue_pass<PrecBF16>(x, 3, x->main);
+    else
+      enqueue_pass<PrecTF32x3>(x, 3, x->main);
+    RW_CUDA(cudaEventRecord(x->ev_fwd, x->main));
+    if (y) {
+      RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_y_out, 0));
+      const long long n = (long long)x->H * x->B * x->T;
+      ++g_launches;
+      k_unpad_cols<<<grid_for(n), 256, 0, x->main>>>(x->h[x->L - 1].f(), x->Hp, x->Bp, x->Bp, 1, x->H, x->B, x->T,
+                                                     x->y_raw.f());
+      RW_CUDA(cudaGetLastError());
+      RW_CUDA(cudaEventRecord(x->ev_y_staged, x->main));
+      RW_CUDA(cudaStreamWaitEvent(x->cp_out, x->ev_y_staged, 0));
+      RW_CUDA(cudaMemcpyAsync(y, x->y_raw.p, yb, cudaMemcpyDeviceToHost, x->cp_out));
+      RW_CUDA(cudaEventRecord(x->ev_y_out, x->cp_out));
+    }
+    RW_CUDA(cudaStreamWaitEvent(x->cp_in, x->ev_bwd, 0));
+    RW_CUDA(cudaMemcpyAsync(x->dy_raw.p, dy, yb, cudaMemcpyHostToDevice, x->cp_in));
+    RW_CUDA(cudaEventRecord(x->ev_dy, x->cp_in));
+    RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_dy, 0));
+    RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_out, 0));
+    x->tape_gen += 1;
+    x->tape_training = true;
+    if (x->prec == kBF16)
+      enqueue_pass<PrecBF16>(x, 1, x->main);
+    else
+      enqueue_pass<PrecTF32x3>(x, 1, x->main);
+    x->bwd_done = true;
+    if (x->comm) allreduce_grads(x, x->main);  // data parallel: sum dW/dR/db before read-back
+    RW_CUDA(cudaEventRecord(x->ev_bwd, x->main));
+    RW_CUDA(cudaStreamWaitEvent(x->cp_out, x->ev_bwd, 0));
+    if (dx0) RW_CUDA(cudaMemcpyAsync(dx0, x->dx0.p, xb, cudaMemcpyDeviceToHost, x->cp_out));
+    for (int l = 0; l < x->L; ++l) {
+      const int Il = l == 0 ? x->I : x->H;
+      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost, x->cp_out));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
+      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
+    }
+    RW_CUDA(cudaEventRecord(x->ev_out, x->cp_out));
+  });
+}
+
+extern "C" int rw_train_wait(rw_ctx* x) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaStreamSynchronize(x->main));
+    if (x->cp_in) RW_CUDA(cudaStreamSynchronize(x->cp_in));
+    if (x->cp_out) RW_CUDA(cudaStreamSynchronize(x->cp_out));
+    check_error_flag(x);
   });
 }
 
@@ -1909,19 +2001,22 @@ int rw_comm_init(rw_ctx* x, int nranks, int rank, const char* id128) {
   });
 }
 
+static void allreduce_grads(rw_ctx* x, cudaStream_t s) {
+  Nccl& n = nccl();
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  for (int l = x->L - 1; l >= 0; --l) {  // top layer's gradients are final first
+    const int Il = l == 0 ? x->I : x->H;
+    nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
+    nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
+    nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
+  }
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+}
+
 int rw_allreduce_grads(rw_ctx* x, void* stream) {
   return guarded(x, [&] {
     if (!x->comm) einval("rw_allreduce_grads: rw_comm_init was not called");
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
-    Nccl& n = nccl();
-    nccl_check(n.GroupStart(), "ncclGroupStart");
-    for (int l = x->L - 1; l >= 0; --l) {  // top layer's gradients are final first
-      const int Il = l == 0 ? x->I : x->H;
-      nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
-      nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
-      nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
-    }
-    nccl_check(n.GroupEnd(), "ncclGroupEnd");
+    allreduce_grads(x, stream ? static_cast<cudaStream_t>(stream) : x->main);
   });
 }
 

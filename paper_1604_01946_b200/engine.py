@@ -431,6 +431,14 @@ class Engine:
         arr = lambda lst: (_F * self.cfg.layers)(*[_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
         self._check(self._L.rw_read_outputs(self._ctx, _fp(y), _fp(dx0), arr(dw), arr(dr), arr(db)))
 
+    def train_step(self, x, dy, y=None, dx0=None, dw=None, dr=None, db=None) -> None:
+        """rw_train_step: pipelined host round trip (outputs complete after train_wait)."""
+        arr = lambda lst: (_F * self.cfg.layers)(*[_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
+        self._check(self._L.rw_train_step(self._ctx, _fp(x), _fp(dy), _fp(y), _fp(dx0), arr(dw), arr(dr), arr(db)))
+
+    def train_wait(self) -> None:
+        self._check(self._L.rw_train_wait(self._ctx))
+
     def init_comm(self, rank: int, world: int, unique_id: bytes) -> None:
         """Join the NCCL data-parallel group (one context per GPU)."""
         self._check(self._L.rw_comm_init(self._ctx, world, rank, unique_id))

@@ -165,3 +165,33 @@ def test_nccl_single_rank_plumbing():
     eng.read_outputs(dw=after)
     for a, b in zip(before, after):
         assert np.array_equal(a, b)
+
+
+def test_train_step_matches_pass():
+    """rw_train_step (pipelined host round trip) returns what run_pass + read_outputs return,
+    bit for bit, also when several steps are in flight."""
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, _, _ = make_case(Dims(2, 256, 192, 32, 9), seed=31, bias=True)
+    H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
+    eng = Engine(c, precision="bf16")
+    eng.set_params(params)
+    eng.upload_inputs(x, dy)
+    eng.run_pass(2)
+    eng.sync()
+    shapes = dict(y=(H, B * T), dx0=(I, B * T))
+    ref = {k: np.zeros(v, np.float32, order="F") for k, v in shapes.items()}
+    rdw = [np.zeros((4 * H, I if l == 0 else H), np.float32, order="F") for l in range(L)]
+    rdr = [np.zeros((4 * H, H), np.float32, order="F") for _ in range(L)]
+    rdb = [np.zeros(4 * H, np.float32) for _ in range(L)]
+    eng.read_outputs(ref["y"], ref["dx0"], rdw, rdr, rdb)
+    got = {k: np.zeros(v, np.float32, order="F") for k, v in shapes.items()}
+    gdw = [np.zeros_like(a) for a in rdw]
+    gdr = [np.zeros_like(a) for a in rdr]
+    gdb = [np.zeros_like(a) for a in rdb]
+    xf, dyf = np.asfortranarray(x), np.asfortranarray(dy)
+    for _ in range(3):
+        eng.train_step(xf, dyf, got["y"], got["dx0"], gdw, gdr, gdb)
+    eng.train_wait()
+    assert np.array_equal(got["y"], ref["y"]) and np.array_equal(got["dx0"], ref["dx0"])
+    for a, b in zip(gdw + gdr + gdb, rdw + rdr + rdb):
+        assert np.array_equal(a, b)
