@@ -92,16 +92,18 @@ __global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* d
 // column dst_col_off. Writes an fp32 copy and/or operand planes.
 __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk, int Rp, int Bp,
                            long long dst_col_off, float* dst_f32, int prec, void* p0, void* p1) {
-  const long long total = (long long)Rp * Bp * nblk;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long col = e / Rp;
-    const int r = (int)(e - col * Rp);
-    const int t = (int)(col / Bp), b = (int)(col - (long long)t * Bp);
-    const float v = (src && r < R && b < B) ? src[((long long)t * B + b) * R + r] : 0.0f;
-    const long long di = (dst_col_off + col) * Rp + r;
-    if (dst_f32) dst_f32[di] = v;
-    if (p0) store_planes(prec, p0, p1, di, v);
+  // one column per block iteration, rows across threads: no per-element 64-bit division
+  const int ncols = Bp * nblk;
+  for (int col = blockIdx.x; col < ncols; col += gridDim.x) {
+    const int t = col / Bp, b = col - t * Bp;
+    const bool live = src && b < B;
+    const float* sc = live ? src + ((long long)t * B + b) * R : nullptr;
+    const long long d0 = (dst_col_off + col) * (long long)Rp;
+    for (int r = threadIdx.x; r < Rp; r += blockDim.x) {
+      const float v = (live && r < R) ? sc[r] : 0.0f;
+      if (dst_f32) dst_f32[d0 + r] = v;
+      if (p0) store_planes(prec, p0, p1, d0 + r, v);
+    }
   }
 }
 

@@ -126,6 +126,7 @@ struct Operand {
 
 int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 int round_up(int a, int b) { return ceil_div(a, b) * b; }
+int pad_grid(long long n) { (void)n; return 148 * 8; }  // k_pad_cols: one column per block iteration
 int grid_for(long long n) { return (int)std::min<long long>(std::max<long long>(1, (n + 255) / 256), 148LL * 16); }
 
 constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA
@@ -465,7 +466,10 @@ template <class P, bool AMN, bool BMN>
 void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
                  cudaStream_t s) {
   static const bool old = getenv("RW_GEMM_OLD") && atoi(getenv("RW_GEMM_OLD")) != 0;
-  if (P::kPlanes == 1 && !old && (bn == 128 || bn == 256)) {
+  // a single wave of tiles gains nothing from the persistent loop (measured: dx0 at config B
+  // 36 us one-tile-per-CTA vs 48 us persistent)
+  const long long tiles = (long long)count * ceil_div(M, kTileM) * ceil_div(N, bn);
+  if (P::kPlanes == 1 && !old && (bn == 128 || bn == 256) && tiles > 148) {
     if (bn == 256)
       launch_gemm_p<AMN, BMN, 256>(table_dev, count, M, N, s);
     else
@@ -1096,17 +1100,17 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
   if (!x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
     ++g_launches;
-    k_pad_cols<<<grid_for((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
+    k_pad_cols<<<pad_grid((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
         x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
   }
   for (int l = 0; l < L; ++l) {
     const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
     const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
     ++g_launches;
-    k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(h0, H, B, 1, Hp, Bp, 0, x->h[l].f(), x->prec,
+    k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(h0, H, B, 1, Hp, Bp, 0, x->h[l].f(), x->prec,
                                                            x->hop[l].p(0), x->hop[l].p(1));
     ++g_launches;
-    k_pad_cols<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
+    k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
   if (x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled operand images of x and h0
@@ -2145,9 +2149,9 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     A.alloc(prec, a_elems);
     Bo.alloc(prec, b_elems);
     ++g_launches;
-    k_pad_cols<<<grid_for(a_elems), 256>>>(dA, (int)a_elems, 1, 1, (int)a_elems, 1, 0, nullptr, prec, A.p(0), A.p(1));
+    k_pad_cols<<<pad_grid(a_elems), 256>>>(dA, (int)a_elems, 1, 1, (int)a_elems, 1, 0, nullptr, prec, A.p(0), A.p(1));
     ++g_launches;
-    k_pad_cols<<<grid_for(b_elems), 256>>>(dB, (int)b_elems, 1, 1, (int)b_elems, 1, 0, nullptr, prec, Bo.p(0), Bo.p(1));
+    k_pad_cols<<<pad_grid(b_elems), 256>>>(dB, (int)b_elems, 1, 1, (int)b_elems, 1, 0, nullptr, prec, Bo.p(0), Bo.p(1));
     RW_CUDA(cudaGetLastError());
     std::vector<CUtensorMap> maps;
     for (int p = 0; p < (prec == kBF16 ? 1 : 2); ++p) {
