@@ -354,9 +354,11 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
     }
     if (want == RW_SCHED_PERSISTENT) einval("persistent schedule does not fit this configuration on the device");
   }
-  // stepwise: split K so one layer's launch covers a fair share of the SMs
+  // stepwise: split K only while the L concurrently running layers (the wavefront) leave SMs
+  // idle -- the split-K exchange costs more than it gains once tiles x L fill the GPU
+  // (config E forward: ks 1 / 2 / 4 = 27 / 35 / 57 ms)
   int ks = 1;
-  while (ks < 8 && (long long)tiles * ks * 2 <= sms && ks * 2 <= kb_max) ks *= 2;
+  while (ks < 8 && (long long)tiles * L * ks * 2 <= sms && ks * 2 <= kb_max) ks *= 2;
   if (forced_ks) ks = forced_ks;
   int stages = 4;
   size_t smem = rec_smem_bytes(planes, stages, N, stages);
