@@ -19,13 +19,15 @@ namespace rw {
 template <class P, bool kMN>
 struct OperandTile {
   // Issue the TMA loads of one k-block of an operand tile (rows x kAtomK elements) into
-  // `dst` (rows * 128 bytes). K-major: one box {kAtomK, rows} at (k, row0).
+  // `dst` (rows * 128 bytes). K-major: boxes {kAtomK, min(rows, 128)} at (k, row0 + r) (GEMM
+  // operand maps are encoded with at most 128 box rows, see gemm_box_rows in runtime.cu).
   // MN-major: rows / kAtomK boxes {kAtomK (along MN), kAtomK (K rows)} stacked at
   // kAtomK * 128-byte strides (the UMMA LBO).
   static __device__ __forceinline__ void load(void* dst, const CUtensorMap* m, uint64_t* bar,
                                               int row0, int rows, int k0) {
     if constexpr (!kMN) {
-      tma_load_2d(dst, m, bar, k0, row0);
+      for (int r = 0; r < rows; r += 128)
+        tma_load_2d(static_cast<uint8_t*>(dst) + r * kRowBytes, m, bar, k0, row0 + r);
     } else {
       for (int c = 0; c < rows / P::kAtomK; ++c)
         tma_load_2d(static_cast<uint8_t*>(dst) + c * P::kAtomK * kRowBytes, m, bar,
@@ -429,6 +431,209 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+  }
+}
+
+// ====================================================================== 2-CTA persistent GEMM (bf16)
+// k_gemm_p2: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 with M = 256 (each CTA holds
+// its 128 rows of A) and N = 256 (each CTA holds half of the B tile): per SM a 64-K k-block
+// needs 16 KB of A + 16 KB of B instead of 16 + 32 KB, the difference between the ~60 B/cycle
+// an SM ingests from L2 (profiles/ubench/mma_ubench.cu) and what the tensor core consumes at
+// N = 256 (94 B/cycle per SM). The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads
+// complete on the leader's full barrier; commits multicast to both CTAs' barriers.
+namespace g2 {
+// shared::cluster address of the same object in the pair's leader (cluster rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) { return map_dsmem(smem_u32(p), 0); }
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar_any,
+                                                 int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_addr(bar_any)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void commit2_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+}  // namespace g2
+
+template <bool kAMN, bool kBMN>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm_p2(const GemmDesc* __restrict__ table, int count, int mt_max, int nt_max, int stages) {
+  using P = PrecBF16;
+  constexpr int BN = 256, BH = BN / 2;  // N per pair tile, per CTA half
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int a_bytes = kTileM * kRowBytes;
+  constexpr int b_bytes = BH * kRowBytes;
+  constexpr int stage_bytes = a_bytes + b_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);  // leader only
+  uint64_t* empty = full + stages;
+  uint64_t* tmem_full = empty + stages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;  // [2] leader only: one arrive per CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank() & 1;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr uint32_t tmem_cols = 2 * BN;
+  const long long ntiles = (long long)count * mt_max * nt_max;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  auto tile_of = [&](long long t, int& z, int& m0, int& n0) {
+    const int per = mt_max * nt_max;
+    z = (int)(t / per);
+    const int r = (int)(t - (long long)z * per);
+    n0 = (r / mt_max) * BN;
+    m0 = (r % mt_max) * (2 * kTileM);
+  };
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs; completion on the leader's full barrier)
+    uint32_t pc = 0;
+    for (long long t = pair; t < ntiles; t += npairs) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
+      for (int kb = 0; kb < nkb; ++kb, ++pc) {
+        const int s = pc % stages;
+        mbar_wait(&empty[s], ((pc / stages) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
+        uint8_t* st = smem + s * stage_bytes;
+        const int k = kb * P::kAtomK;
+        const int am = m0 + (int)rank * kTileM, bn = n0 + g.b_n_off + (int)rank * BH;
+        if constexpr (!kAMN) {
+          g2::tma_load_2d_pair(st, g.a[0], &full[s], k + g.a_k_off, am);
+        } else {
+          for (int c = 0; c < kTileM / P::kAtomK; ++c)
+            g2::tma_load_2d_pair(st + c * P::kAtomK * kRowBytes, g.a[0], &full[s], am + c * P::kAtomK, k + g.a_k_off);
+        }
+        if constexpr (!kBMN) {
+          g2::tma_load_2d_pair(st + a_bytes, g.b[0], &full[s], k + g.b_k_off, bn);
+        } else {
+          for (int c = 0; c < BH / P::kAtomK; ++c)
+            g2::tma_load_2d_pair(st + a_bytes + c * P::kAtomK * kRowBytes, g.b[0], &full[s], bn + c * P::kAtomK,
+                                 k + g.b_k_off);
+        }
+      }
+    }
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (leader, converged warp)
+    const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, 2 * kTileM, BN);
+    const uint64_t a_d0 = OperandTile<P, kAMN>::base(smem_u32(smem));
+    const uint64_t b_d0 = OperandTile<P, kBMN>::base(smem_u32(smem + a_bytes));
+    uint32_t pc = 0, tc = 0;
+    for (long long t = pair; t < ntiles; t += npairs) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
+      const int buf = tc & 1;
+      if (tc >= 2) {
+        mbar_wait(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t acc = tmem_base + buf * BN;
+      for (int kb = 0; kb < nkb; ++kb, ++pc) {
+        const int s = pc % stages;
+        mbar_wait(&full[s], (pc / stages) & 1);
+        tc_fence_after();
+        const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
+#pragma unroll
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk)
+          g2::umma2_warp(acc, desc_add(a_s, kk * OperandTile<P, kAMN>::kk_bytes()),
+                         desc_add(b_s, kk * OperandTile<P, kBMN>::kk_bytes()), idesc, (kb | kk) ? 1u : 0u);
+        g2::commit2_warp(&empty[s]);
+      }
+      g2::commit2_warp(&tmem_full[buf]);
+      ++tc;
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs: this CTA's 128 rows of the 256-row tile)
+    const int q = warp & 3;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    uint32_t tc = 0;
+    for (long long t = pair; t < ntiles; t += npairs) {
+      int z, m0, n0;
+      tile_of(t, z, m0, n0);
+      const GemmDesc& g = table[z];
+      if (m0 >= g.M || n0 >= g.N) continue;
+      const int buf = tc & 1;
+      mbar_wait(&tmem_full[buf], (tc >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + (int)rank * kTileM + q * 32 + lane;
+      const int orow = m < g.M ? gemm_out_row(g, m) : -1;
+      ColCursor cc(g, n0);
+      float* const drow = g.d + (orow < 0 ? 0 : orow);
+      const long long ldd = g.ldd;
+      const bool accum_out = g.accumulate != 0;
+      const int nlim = min(BN, g.N - n0);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[8], w[8];
+        tmem_ld_32x32b_x8(tmem_base + lane_off + buf * BN + c0, v);
+        tmem_ld_32x32b_x8(tmem_base + lane_off + buf * BN + c0 + 8, w);
+        tmem_ld_wait();
+        if (orow < 0 || c0 >= nlim) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (c0 + j >= nlim) break;
+          const long long oc = cc.next();
+          if (oc < 0) continue;
+          float* dst = drow + oc * ldd;
+          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]);
+          *dst = accum_out ? *dst + val : val;
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 128)  // one arrive per CTA on the leader's barrier
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(g2::leader_addr(&tmem_empty[buf]))
+                     : "memory");
+      ++tc;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 

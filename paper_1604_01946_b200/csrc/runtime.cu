@@ -67,6 +67,10 @@ EncodeTiledFn encode_fn() {
 
 // 2-D row-major tensor: `inner` contiguous elements per row, `outer` rows, box {bi, bo},
 // SWIZZLE_128B, OOB zero fill.
+// K-major GEMM operand boxes are at most 128 rows; OperandTile::load issues one box per 128 rows
+// (k_gemm_p2 loads half a 256-column B tile per CTA with the same map)
+inline int gemm_box_rows(int rows) { return rows < 128 ? rows : 128; }
+
 CUtensorMap make_map(const void* base, int prec, long long inner, long long outer, int bi, int bo) {
   CUtensorMap m;
   const int elem = prec == kBF16 ? 2 : 4;
@@ -464,13 +468,48 @@ void launch_gemm_p(const GemmDesc* table_dev, int count, int M, int N, cudaStrea
   RW_CUDA(cudaGetLastError());
 }
 
+template <bool AMN, bool BMN>
+void launch_gemm_p2(const GemmDesc* table_dev, int count, int M, int N, cudaStream_t s) {
+  const size_t stage = (size_t)(kTileM + 128) * kRowBytes;
+  int stages = 8;
+  auto smem_of = [&](int st) { return 1024 + st * stage + (2 * st + 4) * 8 + 16; };
+  while (stages > 2 && smem_of(stages) > (size_t)kSmemLimit) --stages;
+  const size_t smem = smem_of(stages);
+  const int mt = ceil_div(M, 2 * kTileM), nt = ceil_div(N, 256);
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long tiles = (long long)count * mt * nt;
+  const int pairs = (int)std::min<long long>(tiles, sms / 2);
+  auto k = k_gemm_p2<AMN, BMN>;
+  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(2 * pairs, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  ++g_launches;
+  RW_CUDA(cudaLaunchKernelEx(&lc, k, table_dev, count, mt, nt, stages));
+}
+
 template <class P, bool AMN, bool BMN>
 void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int stages,
                  cudaStream_t s) {
+  static const bool pair2 = !(getenv("RW_GEMM_2SM") && atoi(getenv("RW_GEMM_2SM")) == 0);
   static const bool old = getenv("RW_GEMM_OLD") && atoi(getenv("RW_GEMM_OLD")) != 0;
   // a single wave of tiles gains nothing from the persistent loop (measured: dx0 at config B
   // 36 us one-tile-per-CTA vs 48 us persistent)
   const long long tiles = (long long)count * ceil_div(M, kTileM) * ceil_div(N, bn);
+  if (P::kPlanes == 1 && !old && pair2 && bn == 256 && tiles > 148) {
+    launch_gemm_p2<AMN, BMN>(table_dev, count, M, N, s);
+    return;
+  }
   if (P::kPlanes == 1 && !old && (bn == 128 || bn == 256) && tiles > 148) {
     if (bn == 256)
       launch_gemm_p<AMN, BMN, 256>(table_dev, count, M, N, s);
@@ -733,19 +772,19 @@ void build(rw_ctx* x) {
     if (kmajor_wg) {
       for (int l = 0; l < L; ++l) {
         m_dgT[2 * l + p] = add_map(x, make_map(x->dgT[l].p(p), prec, colsT, G4p, aK, kTileM));
-        m_hT[2 * l + p] = add_map(x, make_map(x->hT[l].p(p), prec, colsT1, Hp, aK, x->bn_wg));
+        m_hT[2 * l + p] = add_map(x, make_map(x->hT[l].p(p), prec, colsT1, Hp, aK, gemm_box_rows(x->bn_wg)));
       }
-      m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, x->bn_wg));
+      m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, gemm_box_rows(x->bn_wg)));
     }
     m_xK[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp));
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
     m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
-    m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, x->bn_dx));
+    m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, gemm_box_rows(x->bn_dx)));
     if (ls) {
-      m_xLS[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, x->bn_ls));
+      m_xLS[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, gemm_box_rows(x->bn_ls)));
       for (int l = 0; l < L; ++l) {
-        m_hopLS[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, x->bn_ls));
-        m_dgLS[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, x->bn_ls));
+        m_hopLS[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, gemm_box_rows(x->bn_ls)));
+        m_dgLS[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, gemm_box_rows(x->bn_ls)));
       }
     }
   }
@@ -2158,7 +2197,7 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     std::vector<CUtensorMap> maps;
     for (int p = 0; p < (prec == kBF16 ? 1 : 2); ++p) {
       maps.push_back(a_mn ? make_map(A.p(p), prec, lda, K, aK, aK) : make_map(A.p(p), prec, lda, M, aK, 128));
-      maps.push_back(b_mn ? make_map(Bo.p(p), prec, ldb, K, aK, aK) : make_map(Bo.p(p), prec, ldb, N, aK, bn));
+      maps.push_back(b_mn ? make_map(Bo.p(p), prec, ldb, K, aK, aK) : make_map(Bo.p(p), prec, ldb, N, aK, gemm_box_rows(bn)));
     }
     DevBuf md;
     md.alloc(maps.size() * sizeof(CUtensorMap));
