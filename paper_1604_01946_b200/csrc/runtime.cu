@@ -1026,6 +1026,14 @@ void build(rw_ctx* x) {
   dx.n_valid = (int)colsT;
   x->gemm_dx.alloc(sizeof(GemmDesc));
   RW_CUDA(cudaMemcpy(x->gemm_dx.p, &dx, sizeof(GemmDesc), cudaMemcpyHostToDevice));
+  if (x->prec == kBF16) {
+    // 256-column tiles run as CTA pairs (k_gemm_p2: 1.17 vs 0.77 PFLOP/s at config E's dR shape,
+    // profiles/gemm_bench.py) once there are enough pair tiles to fill the SMs
+    const long long pair_tiles = (long long)x->n_wg * ceil_div(4 * x->Hp, 2 * kTileM) *
+                                 ceil_div(std::max(x->Hp, x->Ip), 256);
+    x->bn_wg = pair_tiles >= 148 ? 256 : 128;
+    if (const char* e = getenv("RW_BN_WG")) x->bn_wg = atoi(e);
+  }
   x->st_wg = gemm_stages(x->planes, x->bn_wg);
   x->st_dx = gemm_stages(x->planes, x->bn_dx);
 

@@ -18,7 +18,15 @@ SHAPES = [  # (name, prec, a_mn, b_mn, M, N, K, bn)
     ("dx0 bn128", 0, 0, 0, 512, 6400, 2048, 128),
     ("square 4096^3 K/K", 0, 0, 0, 4096, 4096, 4096, 256),
     ("tf32x3 wgrad K/K", 1, 0, 0, 2048, 512, 6400, 64),
+    ("config E wgrad one layer K/K", 0, 0, 0, 8192, 4096, 25600, 256),
+    ("config E wgrad one layer K/K bn128", 0, 0, 0, 8192, 4096, 25600, 128),
+    ("square 8192^3 K/K", 0, 0, 0, 8192, 8192, 8192, 256),
+    ("config E wgrad dR MN/MN bn256", 0, 1, 1, 8192, 2048, 25600, 256),
+    ("config E wgrad dR MN/MN bn128", 0, 1, 1, 8192, 2048, 25600, 128),
+    ("config C2048 wgrad dR MN/MN bn256", 0, 1, 1, 8192, 2048, 12800, 256),
 ]
+if os.environ.get("GEMM_ONLY"):
+    SHAPES = [s for s in SHAPES if os.environ["GEMM_ONLY"] in s[0]]
 out = []
 for name, prec, amn, bmn, M, N, K, bn in SHAPES:
     A = torch.randn(K, M, device="cuda") if amn else torch.randn(M, K, device="cuda")
