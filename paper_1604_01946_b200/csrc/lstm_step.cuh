@@ -234,6 +234,15 @@ __device__ __forceinline__ float lds_f32(const float* p) {
 __device__ __forceinline__ void sts_f32(float* p, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
 }
+__device__ __forceinline__ void sts_bf16(uint32_t a, float v) {
+  const __nv_bfloat16 b = __float2bfloat16_rn(v);
+  asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const uint16_t*>(&b)));
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 
 // Sum of `n` TMEM accumulators (N columns apart) for 8 columns of this thread's lane, in fp32
 // with round-to-nearest adds (n == 0 -> zeros: no k-block of this CTA was active).

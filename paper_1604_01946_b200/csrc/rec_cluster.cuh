@@ -376,13 +376,18 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
   }
   const int own0 = m * nco;
   if (have) {
+    // every chunk's TMEM loads in flight before one wait
+    uint32_t r[kChunks * 8], r2[kChunks * 8];
 #pragma unroll
     for (int i = 0; i < kChunks; ++i) {
-      float v[8];
-      cl_ld8(taddr + own0 + half * (nco >> 1) + i * 8, true, v, two, N);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = v[j];
+      uint32_t* ri = r + i * 8;
+      tmem_ld_32x32b_x8(taddr + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(ri));
+      if (two) tmem_ld_32x32b_x8(taddr + N + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(r2 + i * 8));
     }
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < kChunks * 8; ++i)
+      v_out[i] = two ? __uint_as_float(r[i]) + __uint_as_float(r2[i]) : __uint_as_float(r[i]);
   } else {
 #pragma unroll
     for (int i = 0; i < kChunks * 8; ++i) v_out[i] = 0.0f;
@@ -505,21 +510,28 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
 template <int kChunks>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
-                                           int nco, uint32_t& rxc, uint32_t offc) {
+                                           int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
   cl_reduce<kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v);
+  if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 9);
   mbar_wait(S.off_full, offc & 1);
+  if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 10);
   float* sum = reinterpret_cast<float*>(S.b);
+  // all loads, then all stores: the volatile ld/st.shared keep program order, so an interleaved
+  // ld -> st chain pays the smem latency per element (~0.6 us per step at 32 elements)
+  float zw[kChunks * 8];
 #pragma unroll
-  for (int i = 0; i < kChunks * 8; ++i) {
-    const int cl = half * kChunks * 8 + i;
-    const float zw = lds_f32(S.rxoff + (size_t)cl * kTileM + row);
-    sts_f32(sum + (size_t)cl * kTileM + row, zw + v[i]);  // (zw + zr), cells.hpp:240
-  }
+  for (int i = 0; i < kChunks * 8; ++i) zw[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
+#pragma unroll
+  for (int i = 0; i < kChunks * 8; ++i)
+    sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row, zw[i] + v[i]);  // (zw + zr), cells.hpp:240
 }
 
+// kCC: the critical members' owned columns / 16 (Bp / kc / 16), one instantiation each so the
+// register allocation of one variant does not spill another's hot loop
+template <int kCC>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_fwd(const FwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -646,6 +658,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         creg[k] = cl < nco ? Ly.c[(long long)(own0 + cl) * Hp + u] : 0.0f;
       }
       const float* sum = reinterpret_cast<const float*>(S.b);
+      // h_t staging after the gate sums, in the B ring: idle between this step's MMA and the
+      // next step's loads, which wait for this CTA's own publish
+      const uint32_t hstg = smem_u32(S.b + (size_t)N * kTileM * 4);
+      const bool staged = (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
       uint32_t rxc = 0;
       if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
       for (int t = 0; t < p.T; ++t) {
@@ -653,12 +669,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
         const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
-        switch (nco >> 4) {
-          case 4: cl_fwd_sum<4>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
-          case 3: cl_fwd_sum<3>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
-          case 2: cl_fwd_sum<2>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
-          default: cl_fwd_sum<1>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t); break;
-        }
+        cl_fwd_sum<kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p);
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
@@ -688,7 +699,19 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tcv[k] = act_tanh<PrecBF16>(cv[k]);
           hv[k] = ov[k] * tcv[k];
           creg[k] = cv[k];
-          *reinterpret_cast<__nv_bfloat16*>(hblk + sw_off(u, own0 + cl, N)) = __float2bfloat16_rn(hv[k]);
+          if (staged)
+            sts_bf16(hstg + (cl * 32 + j) * 2, hv[k]);
+          else
+            *reinterpret_cast<__nv_bfloat16*>(hblk + sw_off(u, own0 + cl, N)) = __float2bfloat16_rn(hv[k]);
+        }
+        if (staged) {
+          // the CTA's 32 units x nco columns as 16-byte chunks of the swizzled operand image:
+          // nco * 4 coalesced vector stores instead of 32 * nco scattered 2-byte ones
+          named_bar_sync(1, kEpiThreads);
+          for (int i = et; i < nco * 4; i += kEpiThreads) {
+            const uint4 v = lds_v4(hstg + i * 16);
+            *reinterpret_cast<uint4*>(hblk + sw_off(tile * kUnitsPerFwdTile + (i & 3) * 8, own0 + (i >> 2), N)) = v;
+          }
         }
         if (et == 0) cl_trace(p, t, 3);
         // publish h_t (all operand stores of this CTA, then one gpu-scope release)
@@ -746,6 +769,10 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   for (int i = 0; i < kChunks * 8; ++i) carry[i] = 0.0f;
   float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
   uint32_t rxc = 0, offc = 0;
+  // dG_t staging in the B ring (idle between this step's MMA and the next step's loads, which
+  // wait for this CTA's own publish): the tile's 8 k-blocks x nco rows of the swizzled image
+  const uint32_t dstg = smem_u32(S.b);
+  const bool staged = !(p.debug & 8) && (size_t)p.stages * N * kRowBytes >= (size_t)8 * nco * 128;
   if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
   for (int it = 0; it <= p.T; ++it) {
     const int t = p.T - 1 - it;
@@ -838,7 +865,16 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         g_o[k] = c2 * c3;
         g_c[k] = d1 * d3;
         carry[k] = dc * pf[j];
-        if (uok && !(p.debug & 8)) {
+        if (staged) {
+          // K offset within the tile's 8 k-blocks: rho_of(g, u) - 4 * tile * 128
+          const int n = cbase + k, nl = n - m * nco;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int kk = q * 128 + g * 32 + lane;
+            sts_bf16(dstg + ((kk >> 6) * nco + nl) * 128 + ((((kk >> 3) & 7) ^ (n & 7)) << 4) + (kk & 7) * 2,
+                     g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k]);
+          }
+        } else if (uok && !(p.debug & 8)) {
           uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
           const int n = cbase + k;
           *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(0, u), n, N)) = __float2bfloat16_rn(g_i[k]);
@@ -846,6 +882,17 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
           *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(2, u), n, N)) = __float2bfloat16_rn(g_o[k]);
           *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(3, u), n, N)) = __float2bfloat16_rn(g_c[k]);
         }
+      }
+    }
+    if (staged) {
+      // 8 k-blocks x nco rows x 128 B, each k-block's rows one contiguous run of the operand
+      named_bar_sync(1, kEpiThreads);
+      uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
+      const int kb0 = tile * 8, nkb = min(8, (int)(G4 / 64) - kb0), per = nco * 8;
+      for (int i = et; i < nkb * per; i += kEpiThreads) {
+        const int kb = i / per, r = i - kb * per;
+        const uint4 v = lds_v4(dstg + i * 16);
+        *reinterpret_cast<uint4*>(blk + ((size_t)(kb0 + kb) * N + m * nco) * 128 + (size_t)r * 16) = v;
       }
     }
     if (et == 0) cl_trace(p, it, 3);
@@ -888,6 +935,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   }
 }
 
+template <int kCC>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_bwd(const BwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -1003,12 +1051,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         default: cl_off_loop<1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
       }
     } else {
-      switch (nco >> 4) {
-        case 4: cl_bwd_crit<4>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
-        case 3: cl_bwd_crit<3>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
-        case 2: cl_bwd_crit<2>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
-        default: cl_bwd_crit<1>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target); break;
-      }
+      cl_bwd_crit<kCC>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
     }
   }
   cl_teardown(tmem_base, tmem_cols);

@@ -181,6 +181,7 @@ constexpr int kNcclFloat32 = 7, kNcclSum = 0;
 struct ClPlan {
   int kc = 0, cs = 0, ncomax = 0, stages = 0;
   size_t smem = 0;
+  void* kern = nullptr;  // the k_cl_fwd / k_cl_bwd instantiation for Bp / kc owned columns
 };
 
 template <class P>
@@ -400,9 +401,19 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
 // cluster (ko_l members per layer), each member holding <= 512 K of its weight slice. Returns
 // false when the shape does not fit (batch > 64, owned columns not a multiple of 16, too many
 // CTAs, shared memory, or clusters not co-resident).
-bool plan_cluster(void* kernel, bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
+void* cl_kernel(bool fwd, int nco) {
+  switch (nco >> 4) {
+    case 4: return fwd ? (void*)k_cl_fwd<4> : (void*)k_cl_bwd<4>;
+    case 3: return fwd ? (void*)k_cl_fwd<3> : (void*)k_cl_bwd<3>;
+    case 2: return fwd ? (void*)k_cl_fwd<2> : (void*)k_cl_bwd<2>;
+    default: return fwd ? (void*)k_cl_fwd<1> : (void*)k_cl_bwd<1>;
+  }
+}
+
+bool plan_cluster(bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
                   ClPlan& out) {
   if (Bp > kClMaxN || Bp % kc || (Bp / kc) % 16) return false;
+  void* kernel = cl_kernel(fwd, Bp / kc);
   int cs = kc, komin = kc;
   for (int k : ko) {
     if (k == 0) continue;
@@ -424,7 +435,7 @@ bool plan_cluster(void* kernel, bool fwd, int kc, const std::vector<int>& ko, in
     return false;
   }
   if ((long long)max_active_clusters(kernel, cs, smem, L * tiles * 2 * cs) < (long long)L * tiles * 2) return false;
-  out = ClPlan{kc, cs, ncomax, stages, smem};
+  out = ClPlan{kc, cs, ncomax, stages, smem, kernel};
   return true;
 }
 
@@ -664,14 +675,14 @@ void build(rw_ctx* x) {
     const int kc_f = ceil_div(Hp / 64, kClKBlocks);
     std::vector<int> ko_f(L), ko_b(L);
     for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
-    cl_f = plan_cluster((void*)k_cl_fwd, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
+    cl_f = plan_cluster(true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
     // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
     // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
     const int nkb_r = 4 * Hp / 64;
     int kc_b = ceil_div(nkb_r, kClKBlocks);
     while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
     for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
-    cl_b = plan_cluster((void*)k_cl_bwd, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
+    cl_b = plan_cluster(false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
   }
   if (c.schedule == RW_SCHED_CLUSTER && !(cl_f && cl_b))
     einval("cluster schedule does not fit this configuration (bf16, batch <= 64, owned columns multiple of 16, "
@@ -1250,7 +1261,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     return;
   }
   if (x->fwd_sched == RW_SCHED_CLUSTER) {
-    launch_cluster(x, (void*)k_cl_fwd, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
+    launch_cluster(x, x->cl_f.kern, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
     if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
       RW_CUDA(cudaMemcpyAsync(x->pp_next_xop, static_cast<uint8_t*>(x->hop[x->L - 1].p(0)) + (size_t)x->Hp * x->Bp * 2,
                               (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
@@ -1315,7 +1326,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     return;
   }
   if (x->bwd_sched == RW_SCHED_CLUSTER) {
-    launch_cluster(x, (void*)k_cl_bwd, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
+    launch_cluster(x, x->cl_b.kern, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
     return;
   }
   if (x->bwd_sched == RW_SCHED_PERSISTENT) {
@@ -1993,7 +2004,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     (dir == 0 ? x->rows_f : x->rows_b) = L + 1;
     // the extra row must still be co-resident
     const ClPlan& pl = dir == 0 ? x->cl_f : x->cl_b;
-    void* kern = dir == 0 ? (void*)k_cl_fwd : (void*)k_cl_bwd;
+    void* kern = pl.kern;
     const int tiles = dir == 0 ? Hp / kUnitsPerFwdTile : ceil_div(Hp, kTileM);
     const int clusters = max_active_clusters(kern, pl.cs, pl.smem, (L + 1) * tiles * 2 * pl.cs);
     if (clusters < (L + 1) * tiles * 2) einval("rw_pp_link: the stage plus its boundary group does not fit on the GPU");

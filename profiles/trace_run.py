@@ -42,6 +42,24 @@ def summarize(path):
                 lst.sort()
                 ticks += [abs(b[1] - a[1]) for a, b in zip(lst, lst[1:])]
             out[f"{ph}.tick_median_ns"] = statistics.median(ticks)
+    # flag propagation: last publish of (layer, t-1) over the layer's critical CTAs -> each
+    # CTA's wait end at t (forward; backward steps run t descending)
+    pub, seen = defaultdict(int), defaultdict(list)
+    for r in rows:
+        key = (r["phase"], int(r["task_layer"]), int(r["task_block"]))
+        if r["span"] == "publish":
+            pub[key] = max(pub[key], int(r["end_ns"]))
+        if r["span"] == "wait":
+            seen[key].append(int(r["end_ns"]))
+    for ph, d in (("fwd", -1), ("bwd", 1)):
+        props = []
+        for (p2, l, t), v in seen.items():
+            prev = pub.get((p2, l, t + d))
+            if p2 == ph and prev:
+                props += [x - prev for x in v]
+        if props:
+            out[f"{ph}.prop_from_last_publish_median_ns"] = statistics.median(props)
+            out[f"{ph}.prop_from_last_publish_min_ns"] = min(props)
     return out
 
 
