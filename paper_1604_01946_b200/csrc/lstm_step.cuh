@@ -231,6 +231,11 @@ __device__ __forceinline__ float lds_f32(const float* p) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
   return v;
 }
+__device__ __forceinline__ float lds_f32_at(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void sts_f32(float* p, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
 }
@@ -340,9 +345,14 @@ __device__ __forceinline__ void xchg_release(const RecSmem& s, int ks) {
   }
 }
 // Reduced accumulator value of owned column cl, row `row` (fixed rank order).
+// Not unrolled over ranks: the cell loop inlines this 4 x 8 times per chunk, and an unrolled
+// runtime-trip-count loop there grew the forward kernel to 15.6k instructions; the epilogue then
+// stalled on instruction fetch (ncu stall_no_inst 80 % of its samples, config E).
 __device__ __forceinline__ float xchg_sum(const RecSmem& s, int ks, int nco, int cl, int row) {
-  float acc = lds_f32(s.xr + cl * kTileM + row);
-  for (int r = 1; r < ks; ++r) acc += lds_f32(s.xr + (r * nco + cl) * kTileM + row);
+  const uint32_t a = smem_u32(s.xr) + (uint32_t)(cl * kTileM + row) * 4u;
+  float acc = lds_f32_at(a);
+#pragma unroll 1
+  for (int r = 1; r < ks; ++r) acc += lds_f32_at(a + (uint32_t)(r * nco * kTileM) * 4u);
   return acc;
 }
 
@@ -525,6 +535,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
+    // register copy of the descriptor: through the shared-memory one, every global store
+    // (a generic pointer that may alias it) forces a reload of the next pointer
+    const FwdLayer Le = Ly;
     const int et = threadIdx.x - kEpiBase;  // 0..255
     const int q = warp & 3;                 // TMEM lane quarter == gate
     const int half = (warp - 4) >> 2;       // which half of the chunk's columns to drain
@@ -532,8 +545,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const int cg = et >> 5;                 // column group 0..7 (cell phase)
     const int u = tile * kUnitsPerFwdTile + j;
     const long long Hp = p.Hp, G4 = 4 * Hp;
-    const float bi = Ly.bias[u], bf = Ly.bias[Hp + u], bo = Ly.bias[2 * Hp + u],
-                bc = Ly.bias[3 * Hp + u];
+    const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u],
+                bc = Le.bias[3 * Hp + u];
     const int n_used = (my_nkb + p.acc_kb - 1) / p.acc_kb;
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
@@ -565,7 +578,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int cl = cg + 8 * k;
-          cp[k] = cl < nco ? Ly.c[(colb + cl) * Hp + u] : 0.0f;
+          cp[k] = cl < nco ? Le.c[(colb + cl) * Hp + u] : 0.0f;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -573,16 +586,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           if (cl >= nco) break;
           float zi = 0.0f, zf = 0.0f, zo = 0.0f, zc = 0.0f;
           if (zxm) {  // (zw + zr) + b, cells.hpp:240
-            const float* zp = Ly.zx + (colb + cl) * G4 + u;
+            const float* zp = Le.zx + (colb + cl) * G4 + u;
             zi = zp[0];
             zf = zp[Hp];
             zo = zp[2 * Hp];
             zc = zp[3 * Hp];
           }
-          const float ai = (zxm ? zi + xchg_sum(S, ks, nco, cl, 0 * 32 + j) : xchg_sum(S, ks, nco, cl, 0 * 32 + j)) + bi;
-          const float af = (zxm ? zf + xchg_sum(S, ks, nco, cl, 1 * 32 + j) : xchg_sum(S, ks, nco, cl, 1 * 32 + j)) + bf;
-          const float ao = (zxm ? zo + xchg_sum(S, ks, nco, cl, 2 * 32 + j) : xchg_sum(S, ks, nco, cl, 2 * 32 + j)) + bo;
-          const float ac = (zxm ? zc + xchg_sum(S, ks, nco, cl, 3 * 32 + j) : xchg_sum(S, ks, nco, cl, 3 * 32 + j)) + bc;
+          const float si = xchg_sum(S, ks, nco, cl, 0 * 32 + j), sf = xchg_sum(S, ks, nco, cl, 1 * 32 + j);
+          const float so = xchg_sum(S, ks, nco, cl, 2 * 32 + j), sc = xchg_sum(S, ks, nco, cl, 3 * 32 + j);
+          const float ai = (zxm ? zi + si : si) + bi;
+          const float af = (zxm ? zf + sf : sf) + bf;
+          const float ao = (zxm ? zo + so : so) + bo;
+          const float ac = (zxm ? zc + sc : sc) + bc;
           const float iv = act_sigmoid<P>(ai);
           const float fv = act_sigmoid<P>(af);
           const float ov = act_sigmoid<P>(ao);
@@ -594,16 +609,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const float hv = ov * tcv;
           const long long col_prev = colb + cl;       // block t   (c_{t-1})
           const long long col_new = col_prev + p.Bp;  // block t+1 (c_t, h_t)
-          Ly.c[col_new * Hp + u] = cv;
-          Ly.h[col_new * Hp + u] = hv;
-          store_operand<P>(Ly.hop, col_new * Hp + u, hv);
-          if (Ly.gates) {
-            float* gp = Ly.gates + col_prev * G4 + u;
+          Le.c[col_new * Hp + u] = cv;
+          Le.h[col_new * Hp + u] = hv;
+          store_operand<P>(Le.hop, col_new * Hp + u, hv);
+          if (Le.gates) {
+            float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv;
             gp[Hp] = fv;
             gp[2 * Hp] = ov;
             gp[3 * Hp] = cb;
-            Ly.tanhc[col_prev * Hp + u] = tcv;
+            Le.tanhc[col_prev * Hp + u] = tcv;
           }
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 5);
@@ -617,7 +632,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           __threadfence();
-          red_release_gpu_add(&Ly.flags[t], 1);
+          red_release_gpu_add(&Le.flags[t], 1);
         }
       }
       if (et == 0) trace_stamp(p, it, 7);
@@ -756,6 +771,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       umma_commit(S.tmem_full);
     }
   } else if (warp >= 4) {
+    const BwdLayer Le = Ly;  // register copy (see the forward epilogue)
     // ================= epilogue: split-K exchange + LSTM backward (cells.hpp:424-447)
     const int et = threadIdx.x - kEpiBase;
     const int q = warp & 3;
@@ -805,22 +821,22 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               acc[k] = xchg_sum(S, ks, nco, cl, ul);
               const long long n = cbase + cl;
               if (t < 0) {
-                dci[k] = Ly.carry_c[n * Hp + u];
+                dci[k] = Le.carry_c[n * Hp + u];
                 continue;
               }
               const long long col = (long long)t * p.Bp + n;
-              const float* gp = Ly.gates + col * G4 + u;
+              const float* gp = Le.gates + col * G4 + u;
               pi[k] = gp[0];
               pf[k] = gp[Hp];
               po[k] = gp[2 * Hp];
               pcb[k] = gp[3 * Hp];
-              ptc[k] = Ly.tanhc[col * Hp + u];
-              pcp[k] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
-              dci[k] = (t == p.T - 1) ? 0.0f : Ly.carry_c[n * Hp + u];
+              ptc[k] = Le.tanhc[col * Hp + u];
+              pcp[k] = Le.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+              dci[k] = (t == p.T - 1) ? 0.0f : Le.carry_c[n * Hp + u];
               if (dam)
-                dyv[k] = Ly.dabove[col * Hp + u];
-              else if (Ly.dy && u < p.H && n < p.B)
-                dyv[k] = Ly.dy[((long long)t * p.B + n) * p.H + u];
+                dyv[k] = Le.dabove[col * Hp + u];
+              else if (Le.dy && u < p.H && n < p.B)
+                dyv[k] = Le.dy[((long long)t * p.B + n) * p.H + u];
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -828,11 +844,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               if (cl >= nco) break;
               const long long n = cbase + cl;
               if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170)
-                Ly.dh0[n * Hp + u] = acc[k];
-                Ly.dc0[n * Hp + u] = dci[k];
+                Le.dh0[n * Hp + u] = acc[k];
+                Le.dc0[n * Hp + u] = dci[k];
                 continue;
               }
-              const float dh = (Ly.dy || dam) ? dyv[k] + acc[k] : acc[k];  // d_above + carry_h
+              const float dh = (Le.dy || dam) ? dyv[k] + acc[k] : acc[k];  // d_above + carry_h
               const float q1 = dh * po[k];
               const float s0 = ptc[k] * ptc[k];
               const float s1 = 1.0f - s0;
@@ -843,26 +859,26 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               const float c1 = dh * ptc[k], c2 = c1 * po[k], c3 = 1.0f - po[k];
               const float d1 = dc * pi[k], d2 = pcb[k] * pcb[k], d3 = 1.0f - d2;
               const float gi = a2 * a3, gf = b2 * b3, go = c2 * c3, gc = d1 * d3;
-              Ly.carry_c[n * Hp + u] = dc * pf[k];
+              Le.carry_c[n * Hp + u] = dc * pf[k];
               const long long col = (long long)t * p.Bp + n;
-              float* dgp = Ly.dg + col * G4 + u;
+              float* dgp = Le.dg + col * G4 + u;
               dgp[0] = gi;
               dgp[Hp] = gf;
               dgp[2 * Hp] = go;
               dgp[3 * Hp] = gc;
               const long long ob = col * G4;
-              store_operand<P>(Ly.dgop, ob + rho_of(0, u), gi);
-              store_operand<P>(Ly.dgop, ob + rho_of(1, u), gf);
-              store_operand<P>(Ly.dgop, ob + rho_of(2, u), go);
-              store_operand<P>(Ly.dgop, ob + rho_of(3, u), gc);
+              store_operand<P>(Le.dgop, ob + rho_of(0, u), gi);
+              store_operand<P>(Le.dgop, ob + rho_of(1, u), gf);
+              store_operand<P>(Le.dgop, ob + rho_of(2, u), go);
+              store_operand<P>(Le.dgop, ob + rho_of(3, u), gc);
               si += gi;
               sf += gf;
               so += go;
               sc += gc;
             }
           }
-          if (t >= 0 && Ly.dbp) {
-            float* d = Ly.dbp + (long long)(((n0 / kXChunk) * ks + rank) * 2 + hh) * G4 + u;
+          if (t >= 0 && Le.dbp) {
+            float* d = Le.dbp + (long long)(((n0 / kXChunk) * ks + rank) * 2 + hh) * G4 + u;
             d[0] += si;
             d[Hp] += sf;
             d[2 * Hp] += so;
@@ -878,7 +894,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           __threadfence();
-          red_release_gpu_add(&Ly.flags[t], 1);
+          red_release_gpu_add(&Le.flags[t], 1);
         }
       }
       if (et == 0) trace_stamp(p, it, 7);

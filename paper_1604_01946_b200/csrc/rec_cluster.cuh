@@ -353,6 +353,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
     // makes every waiting thread invalidate L1 (CCTL.IVALL), ~2 us per step across 256 threads;
     // the bulk copies' data is covered by the mbarrier's complete_tx (as for TMA loads).
     if (it > 0) mbar_wait(S.push_free, (it - 1) & 1);
+#pragma unroll 1
     for (int d = 0; d < n_act; ++d) {
       if (d == m) continue;
       float* blk = S.st + (size_t)cl_slot(d, m) * nco * kTileM;
@@ -408,6 +409,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
       float acc[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+#pragma unroll 1
       for (int s = 0; s < n_act; ++s) {
         if (s == m) {
 #pragma unroll
@@ -646,16 +648,17 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       }
     } else {
       // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
+      const FwdLayer Le = Ly;  // register copy (see cl_bwd_crit)
       const int j = et & 31, cg = et >> 5;  // cell phase: unit j of the tile, column group cg
       const int u = tile * kUnitsPerFwdTile + j;
       const long long Hp = p.Hp, G4 = 4 * Hp;
       const int own0 = m * nco;
-      const float bi = Ly.bias[u], bf = Ly.bias[Hp + u], bo = Ly.bias[2 * Hp + u], bc = Ly.bias[3 * Hp + u];
+      const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u], bc = Le.bias[3 * Hp + u];
       float creg[kClMaxN / 8];  // c_{t-1} of owned columns cl = cg + 8k (c tape block 0 = c0)
 #pragma unroll
       for (int k = 0; k < kClMaxN / 8; ++k) {
         const int cl = cg + 8 * k;
-        creg[k] = cl < nco ? Ly.c[(long long)(own0 + cl) * Hp + u] : 0.0f;
+        creg[k] = cl < nco ? Le.c[(long long)(own0 + cl) * Hp + u] : 0.0f;
       }
       const float* sum = reinterpret_cast<const float*>(S.b);
       // h_t staging after the gate sums, in the B ring: idle between this step's MMA and the
@@ -680,7 +683,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         float hv[kClMaxN / 8], cv[kClMaxN / 8], iv[kClMaxN / 8], fv[kClMaxN / 8], ov[kClMaxN / 8],
             cb[kClMaxN / 8], tcv[kClMaxN / 8];
         const long long colp = (long long)t * N + own0;  // block t (c_{t-1}), owned base
-        uint8_t* hblk = Ly.hsw + (size_t)(t + 1) * p.Hp * N * 2;  // h_t: block t+1
+        uint8_t* hblk = Le.hsw + (size_t)(t + 1) * p.Hp * N * 2;  // h_t: block t+1
 #pragma unroll
         for (int k = 0; k < kClMaxN / 8; ++k) {
           const int cl = cg + 8 * k;
@@ -718,7 +721,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         fence_proxy_async_global();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
-          red_release_gpu_add(&Ly.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
+          red_release_gpu_add(&Le.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
           red_relaxed_s(consumed, 1, sys);       // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
         }
@@ -729,16 +732,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const int cl = cg + 8 * k;
           if (cl >= nco) break;
           const long long col_prev = colp + cl, col_new = col_prev + N;
-          Ly.c[col_new * Hp + u] = cv[k];
-          Ly.h[col_new * Hp + u] = hv[k];
-          static_cast<__nv_bfloat16*>(Ly.hop[0])[col_new * Hp + u] = __float2bfloat16_rn(hv[k]);
-          if (Ly.gates) {
-            float* gp = Ly.gates + col_prev * G4 + u;
+          Le.c[col_new * Hp + u] = cv[k];
+          Le.h[col_new * Hp + u] = hv[k];
+          static_cast<__nv_bfloat16*>(Le.hop[0])[col_new * Hp + u] = __float2bfloat16_rn(hv[k]);
+          if (Le.gates) {
+            float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv[k];
             gp[Hp] = fv[k];
             gp[2 * Hp] = ov[k];
             gp[3 * Hp] = cb[k];
-            Ly.tanhc[col_prev * Hp + u] = tcv[k];
+            Le.tanhc[col_prev * Hp + u] = tcv[k];
           }
         }
         if (et == 0) cl_trace(p, t, 6);
