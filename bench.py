@@ -290,7 +290,13 @@ def run_ours(args) -> None:
     else:
         dom, dom_ms, dom_fl = f"{kf} (fused recurrent forward, {desc['fwd_schedule']})", fwd_ms, fwd_fl
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
-    peak = peaks.get("bf16_tflops", 1590.0)
+    # burst peak for a kernel timed alone; the sustained (power-capped) one once the kernel runs
+    # long enough to hit the power limit (>= 10 ms: config E's recurrent kernels run at
+    # ~1.5 GHz under sw_power_cap, as does the sustained cuBLAS figure)
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    long_kernel = dom_ms >= 10.0
+    peak = peak_sus if long_kernel else peak_burst
     cpu_base = None
     if not args.no_cpu_baseline and args.config == "B":
         cpu_base = cpu_baseline()
@@ -313,14 +319,15 @@ def run_ours(args) -> None:
                    "parallelism": f"dp{world}" if world > 1 else "single",
                    "precision": args.precision, "schedule": desc,
                    "l2": "flushed (256 MiB write) between timed steps",
-                   "pct_of_bf16_peak": 100.0 * value / world / peak},
+                   "pct_of_bf16_peak": 100.0 * value / world / peak_burst,
+                   "pct_of_bf16_peak_sustained": 100.0 * value / world / peak_sus},
         "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "C-ABI rw_train_step (pinned host x, dy -> forward + backward_data + weight_update"
                         " -> y, dx0, dW, dR, db on the host; uploads/read-back pipelined against compute)"},
         "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
+                     "peak_source": f"{peak_src} bf16 {'sustained' if long_kernel else 'burst'} (MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_launch": dom_fl, "avg_launch_ms": dom_ms},
         "phases_ms": {k: v[0] / max(v[1], 1) for k, v in ph.items()},
         "gpu_launches": launches,

@@ -102,6 +102,7 @@ struct RecParams {
   int acc_kb;         // k-blocks per TMEM accumulator (fp32 promotion); accumulators summed
   int n_acc;          // in fp32 by the epilogue (1 = single accumulator)
   int stages;
+  int a_prefetch;     // streamed A: L2 prefetch distance in k-blocks (0 = off)
   uint32_t flag_target;
   int* error;
   unsigned long long timeout_ns;
@@ -473,8 +474,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       progress(p, 0, it, 1);
       trace_stamp(p, it, 0);
       bool x_ready = false, h_ready = false;
+      // streamed weights: pull the k-blocks a_prefetch ahead from HBM into L2 (the TMA loads
+      // behind them then hit L2; the stage ring alone keeps too few bytes in flight)
+      if (!p.resident)
+        for (int kp = kb_lo; kp < min(kb_hi, kb_lo + p.a_prefetch); ++kp)
+          for (int pl = 0; pl < P::kPlanes; ++pl) tma_prefetch_2d(Ly.a[pl], (kp + akofs) * P::kAtomK, row0);
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const bool seg0 = kb < nkb0;
+        if (!p.resident && kb + p.a_prefetch < kb_hi && p.a_prefetch > 0)
+          for (int pl = 0; pl < P::kPlanes; ++pl)
+            tma_prefetch_2d(Ly.a[pl], (kb + p.a_prefetch + akofs) * P::kAtomK, row0);
         if (p.persistent) {
           if (seg0 && !x_ready) {
             progress(p, 0, it, 2);
@@ -706,9 +715,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       progress(p, 0, it, 1);
       trace_stamp(p, it, 0);
       bool up_ready = false, own_ready = false;
+      // streamed weights: L2 prefetch a_prefetch k-blocks ahead, the first ones before the
+      // flag waits (the weights do not depend on them)
+      if (!p.resident)
+        for (int kp = kb_lo; kp < min(kb_hi, kb_lo + p.a_prefetch); ++kp)
+          if (kb_active(kp, t))
+            for (int pl = 0; pl < P::kPlanes; ++pl) tma_prefetch_2d(Ly.a[pl], (kp + akofs) * P::kAtomK, row0);
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
         const bool seg0 = kb < nkb0;
+        if (!p.resident && p.a_prefetch > 0 && kb + p.a_prefetch < kb_hi && kb_active(kb + p.a_prefetch, t))
+          for (int pl = 0; pl < P::kPlanes; ++pl)
+            tma_prefetch_2d(Ly.a[pl], (kb + p.a_prefetch + akofs) * P::kAtomK, row0);
         if (p.persistent) {
           if (seg0 && !up_ready) {
             progress(p, 0, it, 2);

@@ -305,9 +305,9 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
   const int a_bytes = kTileM * kRowBytes, b_bytes = N * kRowBytes;
   const bool l0 = (threadIdx.x & 31) == 0;
   const uint64_t a0 = sdesc_sw128(smem_u32(S.a), 16, 1024), b0 = sdesc_sw128(smem_u32(S.b), 16, 1024);
-  const int h0 = cl_half0(nkb);
-  const int k_lo = j == 0 ? 0 : h0, k_hi = j == 0 ? h0 : nkb;
-  for (int k = k_lo; k < k_hi; ++k) {
+  // interleaved: issuer j takes k-blocks j, j + 2, ... so both start on the first arrivals
+  const int k_lo = j;
+  for (int k = k_lo; k < nkb; k += kIssuers) {
     const uint32_t q = pc + k;
     const uint32_t s = q % stages;
     mbar_wait(&S.full[s], (q / stages) & 1);

@@ -1145,6 +1145,8 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.acc_kb = fwd ? x->acckb_f : x->acckb_b;
   rp.n_acc = fwd ? x->nacc_f : x->nacc_b;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
+  rp.a_prefetch = 0;  // measured: no gain at config E (0 4 8 16 32 -> 727 702 694 701 660 TFLOP/s)
+  if (const char* e = getenv("RW_A_PREFETCH")) rp.a_prefetch = atoi(e);
   rp.error = static_cast<int*>(x->errflag.p);
   rp.progress = x->progress_dev;
   rp.trace = nullptr;

@@ -79,6 +79,13 @@ RW_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
 RW_DEVICE void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
+// L2 prefetch of one 2-D box (no shared-memory destination, no completion).
+RW_DEVICE void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 // 2-D tiled load global -> shared, completion signalled on `bar` (complete_tx bytes).
 RW_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
                            int32_t c1) {

@@ -1,5 +1,5 @@
 """Run one config-B training pass with the device trace on (RW_TRACE) and summarise where a
-recurrent step's time goes. Usage (GPU box): python profiles/trace_run.py [bf16|fp32] [out.csv]
+recurrent step's time goes. Usage (GPU box): python profiles/trace_run.py [bf16|fp32] [out.csv] [bench config, default B]
 """
 import csv
 import os
@@ -68,7 +68,9 @@ def main():
     path = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", f"trace_{prec}.csv")
     os.environ["RW_TRACE"] = path
     from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
-    cfg = LadderConfig(layers=4, hidden=512, input=512, batch=64, steps=100, seed=42)
+    name = sys.argv[3] if len(sys.argv) > 3 else "B"
+    import bench
+    cfg = LadderConfig(**bench.CONFIGS[name], seed=42)
     eng = Engine(cfg, precision=prec)
     eng.set_params(init_params(cfg))
     eng.upload_inputs(make_input(cfg), make_dy(cfg))
