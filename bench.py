@@ -53,6 +53,48 @@ def pass_flops(c: dict, mult: int = 3) -> int:
     return f * mult
 
 
+# weights re-read every step (the streaming schedules) still come from L2 (126 MB) when they
+# fit in it; the cluster / persistent-resident schedules keep them in shared memory
+L2_WEIGHT_BYTES = 100 * 1024 * 1024
+
+
+def recurrent_bytes(c: dict, fwd: bool) -> int:
+    """Algorithmic HBM bytes of one recurrent launch: the bf16 weights --
+    once per pass when they fit on chip or in L2, else once per step (config E: 512 MB of
+    [W|R] per wavefront step, far beyond smem + L2) -- plus the fp32 tapes each cell must write (forward:
+    gates x4, c, h, tanh c + the bf16 h operand) or read and write (backward: gates x4, tanh c,
+    c read; dG fp32 x4 + bf16 x4 written)."""
+    L, H, I, B, T = c["layers"], c["hidden"], c["input"], c["batch"], c["steps"]
+    if fwd:
+        w = sum(4 * H * ((I if l == 0 else H) + H) * 2 for l in range(L))
+        steps, cell = T, 4 * (4 + 3) + 2
+    else:
+        w = sum(4 * H * (H + (H if l < L - 1 else 0)) * 2 for l in range(L))
+        steps, cell = T + 1, 4 * (4 + 2) + 4 * (4 + 2)
+    wt = w if w <= L2_WEIGHT_BYTES else w * steps
+    return wt + L * T * H * B * cell
+
+
+def ncu_traffic(kernel_prefix: str, config: str):
+    """DRAM bytes (read + write) of the kernel from the committed ncu --set full capture of this
+    config (profiles/r01/ncu_summary_<config>_v2.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01", f"ncu_summary_{config}_v2.json")
+    try:
+        summ = json.load(open(p))
+    except (OSError, ValueError):
+        return None
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for rows in summ.values():
+        for r in rows:
+            if isinstance(r, dict) and r.get("kernel", "").startswith(f"void {kernel_prefix}") and "dram_read" in r:
+                tot = 0.0
+                for k in ("dram_read", "dram_write"):
+                    v, u = r[k].split()
+                    tot += float(v) * unit.get(u, 1)
+                return tot
+    return None
+
+
 def measured_peaks() -> tuple[dict, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -287,8 +329,10 @@ def run_ours(args) -> None:
     kb = kern.get(desc["bwd_schedule"], ("", "k_lstm_bwd"))[1]
     if bwd_ms >= fwd_ms:
         dom, dom_ms, dom_fl = f"{kb} (fused recurrent backward, {desc['bwd_schedule']})", bwd_ms, bwd_fl
+        dom_k, dom_by = kb, recurrent_bytes(c, False)
     else:
         dom, dom_ms, dom_fl = f"{kf} (fused recurrent forward, {desc['fwd_schedule']})", fwd_ms, fwd_fl
+        dom_k, dom_by = kf, recurrent_bytes(c, True)
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     # burst peak for a kernel timed alone; the sustained (power-capped) one once the kernel runs
     # long enough to hit the power limit (>= 10 ms: config E's recurrent kernels run at
@@ -297,6 +341,10 @@ def run_ours(args) -> None:
     peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
     long_kernel = dom_ms >= 10.0
     peak = peak_sus if long_kernel else peak_burst
+    # binding roofline: the larger of flops / tensor peak and algorithmic bytes / HBM peak
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_bound = dom_by / (hbm_peak * 1e9) > dom_fl / (peak * 1e12)
+    traffic = ncu_traffic(dom_k.split()[0], args.config)
     cpu_base = None
     if not args.no_cpu_baseline and args.config == "B":
         cpu_base = cpu_baseline()
@@ -325,10 +373,17 @@ def run_ours(args) -> None:
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "C-ABI rw_train_step (pinned host x, dy -> forward + backward_data + weight_update"
                         " -> y, dx0, dW, dR, db on the host; uploads/read-back pipelined against compute)"},
-        "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "peak_source": f"{peak_src} bf16 {'sustained' if long_kernel else 'burst'} (MEASURED_PEAKS.json)",
-                     "algorithmic_flops_per_launch": dom_fl, "avg_launch_ms": dom_ms},
+        "roofline": ({"kernel": dom, "bound": "hbm", "achieved": dom_by / (dom_ms * 1e-3) / 1e9,
+                      "peak": hbm_peak, "unit": "GB/s", "frac": dom_by / (dom_ms * 1e-3) / 1e9 / hbm_peak,
+                      "traffic": traffic, "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+                      "algorithmic_bytes_per_launch": dom_by, "tensor_tflops": achieved,
+                      "tensor_frac": achieved / peak, "avg_launch_ms": dom_ms}
+                     if hbm_bound else
+                     {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
+                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                      "peak_source": f"{peak_src} bf16 {'sustained' if long_kernel else 'burst'} (MEASURED_PEAKS.json)",
+                      "algorithmic_flops_per_launch": dom_fl, "algorithmic_bytes_per_launch": dom_by,
+                      "avg_launch_ms": dom_ms}),
         "phases_ms": {k: v[0] / max(v[1], 1) for k, v in ph.items()},
         "gpu_launches": launches,
         "clocks": clk.summary(),

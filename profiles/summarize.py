@@ -1,7 +1,7 @@
 """Summarise ncu captures (gpurun_out/prof_*.ncu-rep) and the launch list (launches.csv) into
 the committed evidence under profiles/<round>/. Runs here (no GPU): needs `ncu` for -i.
 
-  python profiles/summarize.py r01 [gpurun_out]
+  python profiles/summarize.py r01 [gpurun_out] [output json name]
 """
 import csv
 import io
@@ -70,6 +70,7 @@ def launches(path):
 def main():
     rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
     src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
+    out_name = sys.argv[3] if len(sys.argv) > 3 else "ncu_summary.json"
     root = os.path.dirname(os.path.abspath(__file__))
     dst = os.path.join(root, rnd)
     os.makedirs(dst, exist_ok=True)
@@ -81,7 +82,7 @@ def main():
     if os.path.exists(lp):
         summary["launch_list"] = [
             {"kernel": k, "total_us": round(t, 2), "launches": n, "share": round(s, 4)} for k, t, n, s in launches(lp)]
-    with open(os.path.join(dst, "ncu_summary.json"), "w") as fh:
+    with open(os.path.join(dst, out_name), "w") as fh:
         json.dump(summary, fh, indent=1)
     for k, v in summary.items():
         print(k)
