@@ -89,8 +89,9 @@ struct ClParams {
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
   int trace_steps;
   int dir;    // 0 forward, 1 backward (error codes)
-  int debug;  // RW_CL_DEBUG bits (timing experiments only; results invalid): 1 = skip fwd tapes,
-              // 4 = skip bwd tape loads, 8 = skip bwd operand stores
+  int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 1 = skip fwd tapes,
+              // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
+              // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered
 };
 
 // Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
@@ -664,7 +665,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       // h_t staging after the gate sums, in the B ring: idle between this step's MMA and the
       // next step's loads, which wait for this CTA's own publish
       const uint32_t hstg = smem_u32(S.b + (size_t)N * kTileM * 4);
-      const bool staged = (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
+      // opt-in (RW_CL_DEBUG bit 16): measured at B forward 0.596 ms staged vs 0.589 scattered
+      const bool staged = (p.debug & 16) && (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
       uint32_t rxc = 0;
       if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
       for (int t = 0; t < p.T; ++t) {
@@ -775,7 +777,8 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   // dG_t staging in the B ring (idle between this step's MMA and the next step's loads, which
   // wait for this CTA's own publish): the tile's 8 k-blocks x nco rows of the swizzled image
   const uint32_t dstg = smem_u32(S.b);
-  const bool staged = !(p.debug & 8) && (size_t)p.stages * N * kRowBytes >= (size_t)8 * nco * 128;
+  // (measured at B: backward 0.880 ms staged vs 0.903 scattered; RW_CL_DEBUG bit 32 = scattered)
+  const bool staged = !(p.debug & 40) && (size_t)p.stages * N * kRowBytes >= (size_t)8 * nco * 128;
   if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
   for (int it = 0; it <= p.T; ++it) {
     const int t = p.T - 1 - it;
