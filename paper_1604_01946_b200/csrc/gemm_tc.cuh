@@ -441,36 +441,6 @@ __global__ void __launch_bounds__(256, 1)
 // an SM ingests from L2 (profiles/ubench/mma_ubench.cu) and what the tensor core consumes at
 // N = 256 (94 B/cycle per SM). The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads
 // complete on the leader's full barrier; commits multicast to both CTAs' barriers.
-namespace g2 {
-// shared::cluster address of the same object in the pair's leader (cluster rank 0)
-__device__ __forceinline__ uint32_t leader_addr(const void* p) { return map_dsmem(smem_u32(p), 0); }
-__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* m, uint64_t* bar_any,
-                                                 int32_t c0, int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_addr(bar_any)), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void umma2_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-// commit to the barrier at the same offset in both CTAs of the pair
-__device__ __forceinline__ void commit2_warp(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
-      ::"r"(smem_u32(bar)), "h"((uint16_t)3)
-      : "memory");
-}
-}  // namespace g2
 
 template <bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(256, 1)

@@ -61,6 +61,10 @@ struct FwdLayer {
   // one GEMM into this buffer (gate-major, [col][g*Hp + u]: the gates tape, which the cell
   // overwrites in place); the step GEMM then covers only R.h_{t-1}
   const float* zx;
+  // CTA-pair stepwise forward (k_lstm_fwd<_, true>): bf16 operand maps with Bp/2-row boxes, each
+  // CTA of a pair loading half of the batch columns
+  const CUtensorMap* bx2;
+  const CUtensorMap* bh2;
 };
 
 struct BwdLayer {
@@ -386,6 +390,41 @@ __device__ __forceinline__ uint32_t rec_setup(const RecSmem& S, const RecParams&
   return *S.tmem_slot;
 }
 
+// CTA-pair prologue / epilogue (cta_group::2 TMEM allocation in both CTAs of the pair).
+__device__ __forceinline__ uint32_t rec_setup_pair(const RecSmem& S, const RecParams& p, uint32_t tmem_cols) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.stages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    mbar_init(S.a_full, 1);
+    mbar_init(S.tmem_full, 1);
+    mbar_init(S.tmem_empty, kEpiThreads);
+    mbar_init(S.xready, 1);
+    mbar_init(S.xfree, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(S.tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers initialised before any load completes on them
+  tc_fence_after();
+  return *S.tmem_slot;
+}
+__device__ __forceinline__ void rec_teardown_pair(uint32_t tmem_base, uint32_t tmem_cols) {
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if ((threadIdx.x >> 5) == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+  }
+}
+
 __device__ __forceinline__ void rec_teardown(int ks, uint32_t tmem_base, uint32_t tmem_cols) {
   tc_fence_before();
   __syncthreads();
@@ -415,7 +454,11 @@ __device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32
 }
 
 // ====================================================================== forward kernel
-template <class P>
+// kPair (bf16, stepwise, ksplit 1): the CTAs of a cluster pair (tiles 2i, 2i+1) run
+// tcgen05.mma.cta_group::2 with M = 256; each CTA loads its own 128 A rows and half of the B
+// columns (Bp/2), so per SM a k-block moves 16 + Bp*64 bytes instead of 16K + Bp*128 -- the
+// per-SM operand ingress that bounds the step at large Bp (config E: 3 MB per CTA per step).
+template <class P, bool kPair = false>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_fwd(const FwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
@@ -439,7 +482,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
   const int my_nkb = kb_hi - kb_lo;
   const int a_bytes = kTileM * kRowBytes;           // one plane of one k-block
-  const int b_bytes = N * kRowBytes;
+  const int b_bytes = (kPair ? N / 2 : N) * kRowBytes;
   const int b_stage = P::kPlanes * b_bytes;
   const int a_stage = P::kPlanes * a_bytes;
   const int a_total = p.resident ? p.a_slots * a_stage : p.stages * a_stage;
@@ -451,10 +494,51 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
-  const uint32_t tmem_base = rec_setup(S, p, ks, tmem_cols);
+  const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
-  if (warp == 0 && lane == 0) {
+  if (kPair && warp <= 1) {
+   if constexpr (kPair) {
+    const uint32_t prank = cluster_ctarank() & 1;
+    const int nh = N / 2;
+    if (warp == 0 && lane == 0) {
+      // ============= TMA producer (both CTAs of the pair; completion on the leader's barrier)
+      prefetch_tmap(Ly.a[0]);
+      prefetch_tmap(Ly.bx2);
+      prefetch_tmap(Ly.bh2);
+      const int t = p.t_first;
+      uint32_t pc = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
+        const int s = pc % p.stages;
+        mbar_wait(&S.empty[s], ((pc / p.stages) & 1) ^ 1);
+        if (prank == 0) mbar_arrive_expect_tx(&S.full[s], 2 * (b_stage + a_stage));
+        uint8_t* bst = S.b_st + s * b_stage;
+        if (kb < nkb0)
+          g2::tma_load_2d_pair(bst, Ly.bx2, &S.full[s], kb * P::kAtomK, Ly.bx_col_off + t * p.Bp + (int)prank * nh);
+        else
+          g2::tma_load_2d_pair(bst, Ly.bh2, &S.full[s], (kb - nkb0) * P::kAtomK, t * p.Bp + (int)prank * nh);
+        g2::tma_load_2d_pair(S.a_res + s * a_stage, Ly.a[0], &S.full[s], (kb + akofs) * P::kAtomK, row0);
+      }
+    } else if (warp == 1 && prank == 0) {
+      // ============= MMA issuer (leader, converged warp): M = 256 over the pair, N = Bp
+      const uint32_t idesc = idesc_make(P::kFmt, false, false, 2 * kTileM, N);
+      uint32_t pc = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
+        const int s = pc % p.stages;
+        mbar_wait(&S.full[s], (pc / p.stages) & 1);
+        tc_fence_after();
+        const uint64_t a0 = sdesc_sw128(smem_u32(S.a_res + s * a_stage), 16, 1024);
+        const uint64_t b0 = sdesc_sw128(smem_u32(S.b_st + s * b_stage), 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk)
+          g2::umma2_warp(tmem_base, desc_add(a0, kk * 32), desc_add(b0, kk * 32), idesc,
+                         (kb != kb_lo || kk) ? 1u : 0u);
+        g2::commit2_warp(&S.empty[s]);
+      }
+      g2::commit2_warp(S.tmem_full);
+    }
+   }
+  } else if (!kPair && warp == 0 && lane == 0) {
     // ================= TMA producer
     for (int pl = 0; pl < P::kPlanes; ++pl) {
       prefetch_tmap(Ly.a[pl]);
@@ -516,7 +600,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       }
       trace_stamp(p, it, 1);
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (!kPair && warp == 1 && lane == 0) {
     // ================= MMA issuer
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
@@ -556,7 +640,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const long long Hp = p.Hp, G4 = 4 * Hp;
     const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u],
                 bc = Le.bias[3 * Hp + u];
-    const int n_used = (my_nkb + p.acc_kb - 1) / p.acc_kb;
+    const int n_used = kPair ? 1 : (my_nkb + p.acc_kb - 1) / p.acc_kb;
     uint32_t xc = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
@@ -647,7 +731,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       if (et == 0) trace_stamp(p, it, 7);
     }
   }
-  rec_teardown(ks, tmem_base, tmem_cols);
+  if constexpr (kPair)
+    rec_teardown_pair(tmem_base, tmem_cols);
+  else
+    rec_teardown(ks, tmem_base, tmem_cols);
 }
 
 // ====================================================================== backward kernel

@@ -244,6 +244,7 @@ struct rw_ctx {
   int rows_f = 0, rows_b = 0;               // grid rows (>= L: pipeline stages add boundary groups)
   // layer pipeline (rw_pp_*): boundary groups, peer buffers
   bool pp_prev = false, pp_next = false;     // linked to a previous / next stage
+  bool pair_f = false;                       // stepwise forward as CTA pairs (k_lstm_fwd<bf16, true>)
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
@@ -379,7 +380,7 @@ RecPlan plan_recurrent(void* kernel, int want, int planes, int kb_max, int tiles
 
 template <class P>
 void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_x, int grid_y,
-                size_t smem, cudaStream_t s) {
+                size_t smem, cudaStream_t s, int cluster = 0) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid_x, grid_y, 1);
   lc.blockDim = dim3(kRecThreads, 1, 1);
@@ -387,7 +388,7 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
   lc.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = rp.ksplit;
+  at[0].val.clusterDim.x = cluster > 0 ? cluster : rp.ksplit;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
@@ -716,6 +717,24 @@ void build(rw_ctx* x) {
   x->st_b = pb.stages;
   x->smem_b = pb.smem;
   x->slots_b = pb.a_slots;
+  // stepwise forward as CTA pairs (cta_group::2, M = 256, each CTA half of the batch columns):
+  // bf16, no split-K, an even tile count and Bp/2 a multiple of 16 (RW_FWD_PAIR=0 disables)
+  x->pair_f = x->prec == kBF16 && pf.sched == RW_SCHED_STEPWISE && !ls && !cl_f && pf.ks == 1 && tiles_f % 2 == 0 &&
+              Bp >= 64 && Bp % 32 == 0 && !(getenv("RW_FWD_PAIR") && atoi(getenv("RW_FWD_PAIR")) == 0);
+  if (x->pair_f) {
+    int st = 8;
+    size_t sm = rec_smem_bytes(1, st, Bp / 2, st);
+    while (sm > (size_t)kSmemLimit && st > 2) sm = rec_smem_bytes(1, --st, Bp / 2, st);
+    void* kp = (void*)k_lstm_fwd<PrecBF16, true>;
+    if (sm > (size_t)kSmemLimit ||
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+      cudaGetLastError();
+      x->pair_f = false;
+    } else {
+      x->st_f = st;
+      x->smem_f = sm;
+    }
+  }
   if (cl_f) {
     x->fwd_sched = RW_SCHED_CLUSTER;
     x->cl_f = cpf;
@@ -763,6 +782,8 @@ void build(rw_ctx* x) {
   std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
       m_dgMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
+  int m_xK2 = 0;  // CTA-pair forward: Bp/2-row boxes (bf16: one plane)
+  std::vector<int> m_hopK2(L);
   // layer-sequential GEMMs: B operands (layer inputs / dG) as K-major boxes of bn_ls columns
   x->bn_ls = x->prec == kBF16 ? 256 : 64;  // tf32: the chunked-promotion GEMM variant
   int m_xLS[2] = {0, 0};
@@ -776,6 +797,7 @@ void build(rw_ctx* x) {
       m_wf[2 * l + p] = add_map(x, make_map(x->wf[l].p(p), prec, Ipl + Hp, G4p, aK, kTileM));
       m_wb[2 * l + p] = add_map(x, make_map(x->wb[l].p(p), prec, (l < L - 1 ? 2 : 1) * G4p, Hp, aK, kTileM));
       m_hopK[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp));
+      if (x->pair_f) m_hopK2[l] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp / 2));
       m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
       m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
@@ -788,6 +810,7 @@ void build(rw_ctx* x) {
       m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, gemm_box_rows(x->bn_wg)));
     }
     m_xK[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp));
+    if (x->pair_f) m_xK2 = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp / 2));
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
     m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
     m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, gemm_box_rows(x->bn_dx)));
@@ -826,6 +849,8 @@ void build(rw_ctx* x) {
     F.tanhc = x->tanhc[l].f();
     F.flags = ff + (size_t)l * T;
     F.zx = ls ? x->gates[l].f() : nullptr;  // the input GEMM writes W.x into the gates tape
+    F.bx2 = x->pair_f ? MD + (l == 0 ? m_xK2 : m_hopK2[l - 1]) : nullptr;
+    F.bh2 = x->pair_f ? MD + m_hopK2[l] : nullptr;
     if (!x->hsw.empty()) {
       F.hsw = static_cast<uint8_t*>(x->hsw[l].p);
       F.bxsw = l == 0 ? static_cast<const uint8_t*>(x->xsw.p) : static_cast<const uint8_t*>(x->hsw[l - 1].p);
@@ -1289,6 +1314,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     return;
   }
   // stepwise wavefront: layer l on stream ls[l]; step (l,t) waits for (l-1,t)
+  if (x->pair_f) kern = (void*)k_lstm_fwd<PrecBF16, true>;
   rp.persistent = 0;
   rp.resident = 0;
   rp.n_steps = 1;
@@ -1299,7 +1325,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
       if (l > 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l - 1], 0));
       rp.layer_base = l;
       rp.t_first = t;
-      launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, x->ls[l]);
+      launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, x->ls[l], x->pair_f ? 2 : 0);
       RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
     }
   }
@@ -2191,6 +2217,13 @@ int rw_describe(rw_ctx* x, int* fs, int* bs, int* kf, int* kb) {
     if (bs) *bs = x->bwd_sched;
     if (kf) *kf = x->ks_f;
     if (kb) *kb = x->ks_b;
+  });
+}
+
+int rw_describe_variants(rw_ctx* x, int* fwd_pair, int* wgrad_bn) {
+  return guarded(x, [&] {
+    if (fwd_pair) *fwd_pair = x->pair_f ? 1 : 0;
+    if (wgrad_bn) *wgrad_bn = x->bn_wg;
   });
 }
 

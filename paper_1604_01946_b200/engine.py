@@ -486,5 +486,7 @@ class Engine:
         a, b, k1, k2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         self._check(self._L.rw_describe(self._ctx, C.byref(a), C.byref(b), C.byref(k1), C.byref(k2)))
         names = {1: "stepwise", 2: "persistent", 3: "cluster", 4: "layerseq"}
+        pair, bn = C.c_int(), C.c_int()
+        self._check(self._L.rw_describe_variants(self._ctx, C.byref(pair), C.byref(bn)))
         return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
-                "fwd_ksplit": k1.value, "bwd_ksplit": k2.value}
+                "fwd_ksplit": k1.value, "bwd_ksplit": k2.value, "fwd_pair": pair.value, "wgrad_bn": bn.value}

@@ -69,6 +69,23 @@ def test_cluster_configs(reference, dims):
     print(f"cluster {dims}: {eng.describe()} worst {worst}")
 
 
+# stepwise forward as CTA pairs (cta_group::2): bf16, no split-K (tiles x layers fill the GPU),
+# Bp >= 64; a ragged batch (250 -> Bp 256) and the input-width layer 0
+PAIRS = [Dims(3, 1024, 768, 64, 4), Dims(3, 1024, 512, 250, 3)]
+
+
+@pytest.mark.parametrize("dims", PAIRS, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
+def test_stepwise_pairs(reference, dims):
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(dims, seed=31, bias=True, state=True)
+    eng = Engine(c, precision="bf16", schedule="stepwise")
+    d = eng.describe()
+    assert d["fwd_schedule"] == "stepwise" and d["fwd_pair"] == 1 and d["fwd_ksplit"] == 1, d
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), "bf16")
+
+
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_layerseq_large(reference, precision):
     """Layer-sequential schedule at a larger hidden size with several split-K ranks."""
