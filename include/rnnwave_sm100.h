@@ -147,9 +147,10 @@ int rw_phase_times(rw_ctx* ctx, double* out_ms, int* out_launches, int n, int re
 /* The schedule the context actually uses for forward/backward (rw_schedule values), and the
  * split-K factors chosen. */
 int rw_describe(rw_ctx* ctx, int* fwd_sched, int* bwd_sched, int* fwd_ksplit, int* bwd_ksplit);
-/* Kernel variants chosen: fwd_pair = 1 when the stepwise forward runs as CTA pairs
- * (tcgen05 cta_group::2, M = 256); wgrad_bn = N tile of the weight-gradient GEMMs (256 = pairs). */
-int rw_describe_variants(rw_ctx* ctx, int* fwd_pair, int* wgrad_bn);
+/* Kernel variants chosen: pairs bit 0 = the stepwise forward, bit 1 = the persistent backward
+ * run as CTA pairs (tcgen05 cta_group::2, M = 256); wgrad_bn = N tile of the weight-gradient
+ * GEMMs (256 = pairs). */
+int rw_describe_variants(rw_ctx* ctx, int* pairs, int* wgrad_bn);
 
 /* Copy the results of the last rw_run_pass to host buffers (any may be NULL): y (H x B*T),
  * dx0 (I x B*T), dW / dR / db per layer (reference layouts). Synchronous. */

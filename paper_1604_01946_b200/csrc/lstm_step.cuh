@@ -90,6 +90,9 @@ struct BwdLayer {
   // ([col][u], Hp x Bp T); the step GEMM covers only R^T dG_{t+1}, at A k-block offset akofs
   const float* dabove;
   int akofs;
+  // CTA-pair persistent backward (k_lstm_bwd<_, true>): bf16 dG operand maps with Bp/2-row boxes
+  const CUtensorMap* bup2;
+  const CUtensorMap* bg2;
 };
 
 struct RecParams {
@@ -391,7 +394,8 @@ __device__ __forceinline__ uint32_t rec_setup(const RecSmem& S, const RecParams&
 }
 
 // CTA-pair prologue / epilogue (cta_group::2 TMEM allocation in both CTAs of the pair).
-__device__ __forceinline__ uint32_t rec_setup_pair(const RecSmem& S, const RecParams& p, uint32_t tmem_cols) {
+__device__ __forceinline__ uint32_t rec_setup_pair(const RecSmem& S, const RecParams& p, uint32_t tmem_cols,
+                                                   int tmem_empty_count = kEpiThreads) {
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < p.stages; ++i) {
@@ -400,7 +404,7 @@ __device__ __forceinline__ uint32_t rec_setup_pair(const RecSmem& S, const RecPa
     }
     mbar_init(S.a_full, 1);
     mbar_init(S.tmem_full, 1);
-    mbar_init(S.tmem_empty, kEpiThreads);
+    mbar_init(S.tmem_empty, tmem_empty_count);
     mbar_init(S.xready, 1);
     mbar_init(S.xfree, 1);
     fence_barrier_init();
@@ -738,7 +742,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 }
 
 // ====================================================================== backward kernel
-template <class P>
+// kPair (bf16, ksplit 1, streamed A): CTA pairs as in k_lstm_fwd<_, true>; the leader's
+// tmem_empty barrier collects one arrival per CTA before the next step's MMAs overwrite either
+// CTA's accumulator.
+template <class P, bool kPair = false>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_bwd(const BwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
@@ -761,7 +768,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int kb_lo = rank * nkb / ks, kb_hi = (rank + 1) * nkb / ks;
   const int my_nkb = kb_hi - kb_lo;
   const int a_bytes = kTileM * kRowBytes;
-  const int b_bytes = N * kRowBytes;
+  const int b_bytes = (kPair ? N / 2 : N) * kRowBytes;
   const int b_stage = P::kPlanes * b_bytes;
   const int a_stage = P::kPlanes * a_bytes;
   const int a_total = p.resident ? p.a_slots * a_stage : p.stages * a_stage;
@@ -773,7 +780,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
-  const uint32_t tmem_base = rec_setup(S, p, ks, tmem_cols);
+  // pair: the leader's tmem_empty takes one arrival per CTA (after its epilogue drained TMEM)
+  const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols, 2) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
   // k-blocks this CTA multiplies at step t: seg0 needs dG_{l+1,t} (t >= 0), seg1 needs
@@ -830,6 +838,20 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
         const int s = pc % p.stages;
         mbar_wait(&S.empty[s], ((pc / p.stages) & 1) ^ 1);
+        if constexpr (kPair) {
+          // both CTAs: own 128 A rows + half of the dG columns, completion on the leader's barrier
+          const uint32_t prank = cluster_ctarank() & 1;
+          const int nh = p.Bp / 2;
+          if (prank == 0) mbar_arrive_expect_tx(&S.full[s], 2 * (b_stage + a_stage));
+          uint8_t* bst = S.b_st + s * b_stage;
+          if (seg0)
+            g2::tma_load_2d_pair(bst, Ly.bup2, &S.full[s], kb * P::kAtomK, t * p.Bp + (int)prank * nh);
+          else
+            g2::tma_load_2d_pair(bst, Ly.bg2, &S.full[s], (kb - nkb0) * P::kAtomK, (t + 1) * p.Bp + (int)prank * nh);
+          g2::tma_load_2d_pair(S.a_res + s * a_stage, Ly.a[0], &S.full[s], (kb + akofs) * P::kAtomK, row0);
+          ++pc;
+          continue;
+        }
         mbar_arrive_expect_tx(&S.full[s], b_stage + (p.resident ? 0 : a_stage));
         uint8_t* bst = S.b_st + s * b_stage;
         for (int pl = 0; pl < P::kPlanes; ++pl) {
@@ -846,7 +868,39 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       }
       trace_stamp(p, it, 1);
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (kPair && warp == 1) {
+    if constexpr (kPair) {
+      if (cluster_ctarank() == 0) {
+        // ============= MMA issuer (leader, converged warp): M = 256 over the pair, N = Bp
+        const uint32_t idesc = idesc_make(P::kFmt, false, false, 2 * kTileM, N);
+        uint32_t pc = 0;
+        for (int it = 0; it < p.n_steps; ++it) {
+          const int t = p.t_first - it;
+          if (it > 0) {
+            mbar_wait(S.tmem_empty, (it - 1) & 1);  // both CTAs drained their accumulators
+            tc_fence_after();
+          }
+          bool first = true;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
+            if (!kb_active(kb, t)) continue;
+            const int s = pc % p.stages;
+            mbar_wait(&S.full[s], (pc / p.stages) & 1);
+            tc_fence_after();
+            const uint64_t a0 = sdesc_sw128(smem_u32(S.a_res + s * a_stage), 16, 1024);
+            const uint64_t b0 = sdesc_sw128(smem_u32(S.b_st + s * b_stage), 16, 1024);
+#pragma unroll
+            for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk)
+              g2::umma2_warp(tmem_base, desc_add(a0, kk * 32), desc_add(b0, kk * 32), idesc,
+                             (!first || kk) ? 1u : 0u);
+            g2::commit2_warp(&S.empty[s]);
+            first = false;
+            ++pc;
+          }
+          g2::commit2_warp(S.tmem_full);
+        }
+      }
+    }
+  } else if (!kPair && warp == 1 && lane == 0) {
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
     tc_fence_after();
@@ -907,7 +961,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
         if (n0 + kXChunk >= N) {
           tc_fence_before();
-          mbar_arrive(S.tmem_empty);
+          if constexpr (kPair) {
+            named_bar_sync(1, kEpiThreads);  // the whole CTA drained its TMEM accumulator
+            if (et == 0) mbar_arrive_remote(S.tmem_empty, 0);
+          } else {
+            mbar_arrive(S.tmem_empty);
+          }
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
         xchg_publish(S, ks, xc);
@@ -1005,7 +1064,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       if (et == 0) trace_stamp(p, it, 7);
     }
   }
-  rec_teardown(ks, tmem_base, tmem_cols);
+  if constexpr (kPair)
+    rec_teardown_pair(tmem_base, tmem_cols);
+  else
+    rec_teardown(ks, tmem_base, tmem_cols);
 }
 
 }  // namespace rw

@@ -245,6 +245,7 @@ struct rw_ctx {
   // layer pipeline (rw_pp_*): boundary groups, peer buffers
   bool pp_prev = false, pp_next = false;     // linked to a previous / next stage
   bool pair_f = false;                       // stepwise forward as CTA pairs (k_lstm_fwd<bf16, true>)
+  bool pair_b = false;                       // persistent backward as CTA pairs (k_lstm_bwd<bf16, true>)
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
@@ -735,6 +736,28 @@ void build(rw_ctx* x) {
       x->smem_f = sm;
     }
   }
+  // persistent backward as CTA pairs: bf16, no split-K, streamed weights, even tile count,
+  // and the pairs co-resident (RW_BWD_PAIR=0 disables)
+  x->pair_b = x->prec == kBF16 && pb.sched == RW_SCHED_PERSISTENT && !ls && !cl_b && pb.ks == 1 && !pb.resident &&
+              tiles_b % 2 == 0 && Bp >= 64 && Bp % 32 == 0 &&
+              !(getenv("RW_BWD_PAIR") && atoi(getenv("RW_BWD_PAIR")) == 0);
+  if (x->pair_b) {
+    int st = 8;
+    size_t sm = rec_smem_bytes(1, st, Bp / 2, st);
+    while (sm > (size_t)kSmemLimit && st > 2) sm = rec_smem_bytes(1, --st, Bp / 2, st);
+    sm = std::max(sm, (size_t)116 * 1024);
+    void* kp = (void*)k_lstm_bwd<PrecBF16, true>;
+    const int ctas = tiles_b * L;
+    if (sm > (size_t)kSmemLimit ||
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+        max_active_clusters(kp, 2, sm, ctas) * 2 < ctas) {
+      cudaGetLastError();
+      x->pair_b = false;
+    } else {
+      x->st_b = st;
+      x->smem_b = sm;
+    }
+  }
   if (cl_f) {
     x->fwd_sched = RW_SCHED_CLUSTER;
     x->cl_f = cpf;
@@ -783,7 +806,7 @@ void build(rw_ctx* x) {
       m_dgMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
   int m_xK2 = 0;  // CTA-pair forward: Bp/2-row boxes (bf16: one plane)
-  std::vector<int> m_hopK2(L);
+  std::vector<int> m_hopK2(L), m_dgK2(L);
   // layer-sequential GEMMs: B operands (layer inputs / dG) as K-major boxes of bn_ls columns
   x->bn_ls = x->prec == kBF16 ? 256 : 64;  // tf32: the chunked-promotion GEMM variant
   int m_xLS[2] = {0, 0};
@@ -800,6 +823,7 @@ void build(rw_ctx* x) {
       if (x->pair_f) m_hopK2[l] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp / 2));
       m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
+      if (x->pair_b) m_dgK2[l] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp / 2));
       m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
     }
     if (kmajor_wg) {
@@ -861,6 +885,8 @@ void build(rw_ctx* x) {
       Bd.a[p] = mp(m_wb[2 * l + (p % x->planes)], p);
       Bd.bup[p] = l < L - 1 ? mp(m_dgK[2 * (l + 1) + (p % x->planes)], p) : nullptr;
       Bd.bg[p] = mp(m_dgK[2 * l + (p % x->planes)], p);
+      Bd.bup2 = x->pair_b && l < L - 1 ? MD + m_dgK2[l + 1] : nullptr;
+      Bd.bg2 = x->pair_b ? MD + m_dgK2[l] : nullptr;
       Bd.dgop[p] = x->dgop[l].p(p);
     }
     Bd.has_up = l < L - 1;
@@ -1364,7 +1390,10 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     rp.layer_base = 0;
     rp.t_first = x->T - 1;
     rp.n_steps = x->T + 1;  // T steps + the dh0 step
-    launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, x->L, x->smem_b, s);
+    if (x->pair_b)
+      launch_rec<P>((void*)k_lstm_bwd<PrecBF16, true>, x->bwd_layers.p, rp, rp.tiles, x->L, x->smem_b, s, 2);
+    else
+      launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, x->L, x->smem_b, s);
     return;
   }
   rp.persistent = 0;
@@ -2222,7 +2251,7 @@ int rw_describe(rw_ctx* x, int* fs, int* bs, int* kf, int* kb) {
 
 int rw_describe_variants(rw_ctx* x, int* fwd_pair, int* wgrad_bn) {
   return guarded(x, [&] {
-    if (fwd_pair) *fwd_pair = x->pair_f ? 1 : 0;
+    if (fwd_pair) *fwd_pair = (x->pair_f ? 1 : 0) | (x->pair_b ? 2 : 0);
     if (wgrad_bn) *wgrad_bn = x->bn_wg;
   });
 }

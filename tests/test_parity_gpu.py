@@ -86,6 +86,24 @@ def test_stepwise_pairs(reference, dims):
     assert_within(compare(dev, ref, c), "bf16")
 
 
+# persistent backward as CTA pairs: needs ksplit 1 with every (layer, tile) CTA co-resident and
+# streamed weights -- many tiles x layers, e.g. 8 layers x 16 tiles at H = 2048
+BWD_PAIRS = [Dims(8, 2048, 2048, 64, 3), Dims(7, 1536, 700, 250, 2)]
+
+
+@pytest.mark.parametrize("dims", BWD_PAIRS, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
+def test_persistent_bwd_pairs(reference, dims):
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(dims, seed=37, bias=True, state=True)
+    eng = Engine(c, precision="bf16")
+    d = eng.describe()
+    if d["bwd_schedule"] != "persistent" or not d["bwd_pair"]:
+        pytest.skip(f"backward pairs not planned for this shape on this device: {d}")
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), "bf16")
+
+
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_layerseq_large(reference, precision):
     """Layer-sequential schedule at a larger hidden size with several split-K ranks."""
