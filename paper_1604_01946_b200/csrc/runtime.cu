@@ -268,8 +268,10 @@ struct rw_ctx {
   std::vector<cudaStream_t> ls;
   std::vector<cudaEvent_t> lev;
   cudaEvent_t fork_ev = nullptr;
-  cudaGraphExec_t graphs[4] = {nullptr, nullptr, nullptr, nullptr};  // per pass kind
-  long long graph_launches[4] = {0, 0, 0, 0};                         // kernels inside each graph
+  // per pass kind: 0-3 as rw_run_pass; internal 4 = backward recurrence only, 5 = the
+  // gradient GEMMs / reductions only (rw_train_step waits for the previous read-back between)
+  cudaGraphExec_t graphs[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  long long graph_launches[6] = {0, 0, 0, 0, 0, 0};                   // kernels inside each graph
   bool use_graphs = true;
 
   // state
@@ -1459,19 +1461,21 @@ void run_db(rw_ctx* x, cudaStream_t s) {
 
 template <class P>
 void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
-  if (pass != 1) {
+  const bool fwd = pass == 0 || pass == 2 || pass == 3;
+  if (fwd) {
     PhaseTimer pt(x, 0, s);
     forward_prologue(x, s, nullptr, nullptr);
   }
-  if (pass != 1) {
+  if (fwd) {
     PhaseTimer pt(x, 1, s);
     run_forward_rec<P>(x, s, pass >= 2);
   }
   if (pass == 0 || pass == 3) return;
-  {
+  if (pass != 5) {
     PhaseTimer pt(x, 2, s);
     run_backward_rec<P>(x, s);
   }
+  if (pass == 4) return;
   {
     PhaseTimer pt(x, 3, s);
     run_weight_grads<P>(x, s);
@@ -1856,13 +1860,19 @@ extern "C" int rw_train_step(rw_ctx* x, const float* xin, const float* dy, float
     RW_CUDA(cudaMemcpyAsync(x->dy_raw.p, dy, yb, cudaMemcpyHostToDevice, x->cp_in));
     RW_CUDA(cudaEventRecord(x->ev_dy, x->cp_in));
     RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_dy, 0));
-    RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_out, 0));
     x->tape_gen += 1;
     x->tape_training = true;
+    // the backward recurrence writes no read-back buffer: only the gradient phase waits for the
+    // previous step's read-back (ev_out), which thus overlaps this step's forward + recurrence
     if (x->prec == kBF16)
-      enqueue_pass<PrecBF16>(x, 1, x->main);
+      enqueue_pass<PrecBF16>(x, 4, x->main);
     else
-      enqueue_pass<PrecTF32x3>(x, 1, x->main);
+      enqueue_pass<PrecTF32x3>(x, 4, x->main);
+    RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_out, 0));
+    if (x->prec == kBF16)
+      enqueue_pass<PrecBF16>(x, 5, x->main);
+    else
+      enqueue_pass<PrecTF32x3>(x, 5, x->main);
     x->bwd_done = true;
     if (x->comm) allreduce_grads(x, x->main);  // data parallel: sum dW/dR/db before read-back
     RW_CUDA(cudaEventRecord(x->ev_bwd, x->main));
