@@ -148,8 +148,9 @@ int rw_phase_times(rw_ctx* ctx, double* out_ms, int* out_launches, int n, int re
  * split-K factors chosen. */
 int rw_describe(rw_ctx* ctx, int* fwd_sched, int* bwd_sched, int* fwd_ksplit, int* bwd_ksplit);
 /* Kernel variants chosen: pairs bit 0 = the stepwise forward, bit 1 = the persistent backward
- * run as CTA pairs (tcgen05 cta_group::2, M = 256); wgrad_bn = N tile of the weight-gradient
- * GEMMs (256 = pairs). */
+ * run as CTA pairs (tcgen05 cta_group::2, M = 256); bits 2 / 3 = the layer-sequential forward /
+ * backward run one persistent launch per layer; wgrad_bn = N tile of the weight-gradient GEMMs
+ * (256 = pairs). */
 int rw_describe_variants(rw_ctx* ctx, int* pairs, int* wgrad_bn);
 
 /* Copy the results of the last rw_run_pass to host buffers (any may be NULL): y (H x B*T),

@@ -246,6 +246,7 @@ struct rw_ctx {
   bool pp_prev = false, pp_next = false;     // linked to a previous / next stage
   bool pair_f = false;                       // stepwise forward as CTA pairs (k_lstm_fwd<bf16, true>)
   bool pair_b = false;                       // persistent backward as CTA pairs (k_lstm_bwd<bf16, true>)
+  bool ls_pers_f = false, ls_pers_b = false;  // layer-sequential: one persistent launch per layer
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
@@ -705,6 +706,11 @@ void build(rw_ctx* x) {
   RecPlan pb = plan_recurrent(kb, want, x->planes, ls ? (int)(G4p / x->atomK) : kbb_max, tiles_b, ls ? 1 : L, Bp,
                               sms, "RW_BWD_KSPLIT");
   if (ls) {
+    // persistent per-layer launches need every (tile, rank) CTA of a layer co-resident
+    const int cf = tiles_f * pf.ks, cb = tiles_b * pb.ks;
+    const bool lsp = !(getenv("RW_LS_PERSISTENT") && atoi(getenv("RW_LS_PERSISTENT")) == 0);
+    x->ls_pers_f = lsp && max_active_clusters(kf, pf.ks, pf.smem, cf) * pf.ks >= cf;
+    x->ls_pers_b = lsp && max_active_clusters(kb, pb.ks, pb.smem, cb) * pb.ks >= cb;
     pf.sched = pb.sched = RW_SCHED_LAYERSEQ;
     x->dabove.alloc((size_t)Hp * colsT * 4);
   }
@@ -1301,14 +1307,19 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
   if (x->fwd_sched == RW_SCHED_LAYERSEQ) {
     RecParams rp = rec_params(x, true);
     void* kern = KernelSet<P>::fwd();
-    rp.persistent = 0;
     rp.resident = 0;
-    rp.n_steps = 1;
+    // one persistent launch per layer (its tiles x ksplit CTAs co-resident, flag-synchronised
+    // steps, R streamed from L2 -- one layer's weights fit there) unless RW_LS_PERSISTENT=0:
+    // then one launch per step
+    const bool pers = x->ls_pers_f;
+    rp.persistent = pers ? 1 : 0;
+    rp.n_steps = pers ? x->T : 1;
+    if (pers) RW_CUDA(cudaMemsetAsync(x->flags_f.p, 0, x->flags_f.bytes, s));
     const GemmDesc* G = static_cast<const GemmDesc*>(x->gemm_lsf.p);
     for (int l = 0; l < x->L; ++l) {
       launch_gemm<P, false, false>(G + l, 1, 4 * x->Hp, x->Bp * x->T, x->bn_ls, gemm_stages(x->planes, x->bn_ls), s);
       rp.layer_base = l;
-      for (int t = 0; t < x->T; ++t) {
+      for (int t = 0; t < (pers ? 1 : x->T); ++t) {
         rp.t_first = t;
         launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, s);
       }
@@ -1366,15 +1377,17 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   void* kern = KernelSet<P>::bwd();
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
   if (x->bwd_sched == RW_SCHED_LAYERSEQ) {
-    rp.persistent = 0;
+    const bool pers = x->ls_pers_b;  // as in the forward
+    rp.persistent = pers ? 1 : 0;
     rp.resident = 0;
-    rp.n_steps = 1;
+    rp.n_steps = pers ? x->T + 1 : 1;
+    if (pers) RW_CUDA(cudaMemsetAsync(x->flags_b.p, 0, x->flags_b.bytes, s));
     const GemmDesc* G = static_cast<const GemmDesc*>(x->gemm_lsb.p);
     for (int l = x->L - 1; l >= 0; --l) {
       if (l < x->L - 1)
         launch_gemm<P, false, false>(G + l, 1, x->Hp, x->Bp * x->T, x->bn_ls, gemm_stages(x->planes, x->bn_ls), s);
       rp.layer_base = l;
-      for (int t = x->T - 1; t >= -1; --t) {
+      for (int t = x->T - 1; t >= (pers ? x->T - 1 : -1); --t) {
         rp.t_first = t;
         launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_b, s);
       }
@@ -2263,6 +2276,7 @@ int rw_describe_variants(rw_ctx* x, int* fwd_pair, int* wgrad_bn) {
   return guarded(x, [&] {
     if (fwd_pair) *fwd_pair = (x->pair_f ? 1 : 0) | (x->pair_b ? 2 : 0);
     if (wgrad_bn) *wgrad_bn = x->bn_wg;
+    if (fwd_pair) *fwd_pair |= (x->ls_pers_f ? 4 : 0) | (x->ls_pers_b ? 8 : 0);
   });
 }
 

@@ -490,4 +490,5 @@ class Engine:
         self._check(self._L.rw_describe_variants(self._ctx, C.byref(pair), C.byref(bn)))
         return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
                 "fwd_ksplit": k1.value, "bwd_ksplit": k2.value, "fwd_pair": pair.value & 1,
-                "bwd_pair": (pair.value >> 1) & 1, "wgrad_bn": bn.value}
+                "bwd_pair": (pair.value >> 1) & 1, "wgrad_bn": bn.value,
+                "layerseq_persistent": [(pair.value >> 2) & 1, (pair.value >> 3) & 1]}
