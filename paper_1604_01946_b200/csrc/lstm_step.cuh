@@ -452,7 +452,7 @@ __device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32
       const int pa = (c == 2) ? 1 : 0, pb = (c == 1) ? 1 : 0;
       const uint64_t ad = desc_add(a0, pa * a_bytes + kk * P::kUmmaK * P::kElem);
       const uint64_t bd = desc_add(b0, pb * b_bytes + kk * P::kUmmaK * P::kElem);
-      umma<P::kTF32>(acc, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
+      umma_warp<P::kTF32>(acc, ad, bd, idesc, (!fresh || kk | c) ? 1u : 0u);
     }
   }
 }
@@ -604,7 +604,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       }
       trace_stamp(p, it, 1);
     }
-  } else if (!kPair && warp == 1 && lane == 0) {
+  } else if (!kPair && warp == 1) {
+    // whole warp 1 (converged; elect.sync inside each MMA / commit): a lane-0-only issue branch
+    // costs an ELECT / R2UR waterfall per instruction (profiles/ubench/mma_ubench.cu)
     // ================= MMA issuer
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
@@ -626,9 +628,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         const int ai = (kb - kb_lo) / p.acc_kb;  // accumulator of this k-block
         mma_kblock<P>(tmem_base + ai * N, a_base, b_base, a_bytes, b_bytes, idesc,
                       (kb - kb_lo) % p.acc_kb == 0);
-        umma_commit(&S.empty[s]);
+        umma_commit_warp(&S.empty[s]);
       }
-      umma_commit(S.tmem_full);
+      umma_commit_warp(S.tmem_full);
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
@@ -900,7 +902,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
       }
     }
-  } else if (!kPair && warp == 1 && lane == 0) {
+  } else if (!kPair && warp == 1) {
+    // whole warp 1 (converged; elect.sync inside each MMA / commit): a lane-0-only issue branch
+    // costs an ELECT / R2UR waterfall per instruction (profiles/ubench/mma_ubench.cu)
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
     tc_fence_after();
@@ -924,10 +928,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mma_kblock<P>(tmem_base + (nact / p.acc_kb) * N, a_base, b_base, a_bytes, b_bytes, idesc,
                       nact % p.acc_kb == 0);
         ++nact;
-        umma_commit(&S.empty[s]);
+        umma_commit_warp(&S.empty[s]);
         ++pc;
       }
-      umma_commit(S.tmem_full);
+      umma_commit_warp(S.tmem_full);
     }
   } else if (warp >= 4) {
     const BwdLayer Le = Ly;  // register copy (see the forward epilogue)
