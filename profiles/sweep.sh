@@ -1,19 +1,24 @@
 #!/bin/bash
 # Run ON THE GPU BOX from the repo root: one bench.py line per configured shape (no CPU
-# baseline), summarised as a table on stdout. Usage: bash profiles/sweep.sh [configs...]
+# baseline), summarised as a table on stdout.
+# Usage: [PRECISION=bf16|fp32] bash profiles/sweep.sh [configs...]
 cfgs=${*:-"A B C128 C256 C1024 C2048 D1 D4 E"}
+prec=${PRECISION:-bf16}
 mkdir -p gpurun_out/sweep
 for c in $cfgs; do
   steps=20; [[ $c == E ]] && steps=10
-  timeout -s KILL 600 python bench.py --config $c --steps $steps --no-cpu-baseline > gpurun_out/sweep/$c.json 2> gpurun_out/sweep/$c.err
+  timeout -s KILL 900 python bench.py --config $c --steps $steps --precision $prec --no-cpu-baseline \
+      > gpurun_out/sweep/${c}_$prec.json 2> gpurun_out/sweep/${c}_$prec.err
 done
-python - $cfgs <<'PY'
+python - $prec $cfgs <<'PY'
 import json, sys
+prec = sys.argv[1]
+print(f"precision {prec}")
 print("| config | schedule (fwd / bwd) | ms / pass | TFLOP/s | e2e TFLOP/s | % burst / sustained peak | roofline bound, frac | SM MHz |")
 print("|---|---|---|---|---|---|---|---|")
-for c in sys.argv[1:]:
+for c in sys.argv[2:]:
     try:
-        d = json.loads(open(f"gpurun_out/sweep/{c}.json").read().strip().split("\n")[-1])
+        d = json.loads(open(f"gpurun_out/sweep/{c}_{prec}.json").read().strip().split("\n")[-1])
     except Exception as e:
         print(f"| {c} | failed: {e} |"); continue
     sc = d["config"]["schedule"]; r = d["roofline"]
