@@ -91,7 +91,8 @@ struct ClParams {
   int dir;    // 0 forward, 1 backward (error codes)
   int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
-              // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered
+              // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered,
+              // 64 = operand k-blocks copied one per bulk copy (not in pairs)
 };
 
 // Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
@@ -297,12 +298,19 @@ __device__ __forceinline__ void cl_load_a(const ClSmem& S, const CUtensorMap* a,
     tma_load_2d(S.a + (kb - kb_lo) * a_bytes, a, S.a_full, kb * 64, row0);
 }
 
+// k-blocks travel in pairs (one 2 x N x 128-byte copy into two adjacent stages, completion on
+// the even stage's barrier) when the ring and the step's k-block count are even: >= 16 KB bulk
+// copies ingest ~62 B/cycle per SM vs ~50 for 8 KB ones (profiles/ubench/mma_ubench.cu).
+__device__ __forceinline__ bool cl_pair_kb(const ClParams& p, int nkb) {
+  return !(p.debug & 64) && (p.stages % 2 == 0) && (nkb % 2 == 0);
+}
 // MMA issuers: warps 1 (j = 0) and 3 (j = 1), each converged; elect.sync inside the instruction
 // blocks picks the issuing lane (sm100_ptx.cuh umma_bf16_warp). Issuer j multiplies its half of
 // the step's k-blocks into accumulator `acc` (= its own TMEM columns).
 __device__ __forceinline__ int cl_half0(int nkb) { return (nkb + 1) >> 1; }
 __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, int it, uint32_t acc, int nkb,
                                             uint32_t idesc, uint32_t& pc, int stages, int N, int j) {
+  const bool pairs = cl_pair_kb(p, nkb);
   const int a_bytes = kTileM * kRowBytes, b_bytes = N * kRowBytes;
   const bool l0 = (threadIdx.x & 31) == 0;
   const uint64_t a0 = sdesc_sw128(smem_u32(S.a), 16, 1024), b0 = sdesc_sw128(smem_u32(S.b), 16, 1024);
@@ -311,7 +319,7 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
   for (int k = k_lo; k < nkb; k += kIssuers) {
     const uint32_t q = pc + k;
     const uint32_t s = q % stages;
-    mbar_wait(&S.full[s], (q / stages) & 1);
+    mbar_wait(&S.full[pairs ? (s & ~1u) : s], (q / stages) & 1);
     tc_fence_after();
     if (l0 && k == 0) cl_trace(p, it, 8);  // first k-block arrived
     if (l0 && k == nkb - 1) cl_trace(p, it, 7);
@@ -328,8 +336,18 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
 // stage ring. `blk` is the operand's pre-swizzled step block (sw_off layout); k-block kb sits at
 // (kb - kofs) * N * 128 bytes, already in the SWIZZLE_128B smem image: one 1-D bulk copy each.
 __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, int kb_lo, int kb_hi, int kofs,
-                                          uint32_t& pc, int stages, int N) {
+                                          uint32_t& pc, int stages, int N, bool pairs = false) {
   const int b_bytes = N * kRowBytes;
+  if (pairs) {
+    for (int kb = kb_lo; kb < kb_hi; kb += 2, pc += 2) {
+      const int s = pc % stages;  // even
+      mbar_wait(&S.empty[s], ((pc / stages) & 1) ^ 1);
+      mbar_wait(&S.empty[s + 1], ((pc / stages) & 1) ^ 1);
+      mbar_arrive_expect_tx(&S.full[s], 2 * b_bytes);
+      bulk_load(S.b + s * b_bytes, blk + (size_t)(kb - kofs) * b_bytes, 2 * b_bytes, &S.full[s]);
+    }
+    return;
+  }
   for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
     const int s = pc % stages;
     mbar_wait(&S.empty[s], ((pc / stages) & 1) ^ 1);
@@ -613,13 +631,14 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (t > 0) wait_flag(&Ly.flags[t - 1], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N);
+        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N, cl_pair_kb(p, nkb));
         if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
       } else {
         if (Og.op_flags) wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
+        cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N,
+                  cl_pair_kb(p, nkb));
       }
     }
   } else if (active && (warp == 1 || warp == 3)) {
@@ -1026,9 +1045,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         fence_proxy_async_global();
         cl_trace(p, it, 1);
         if (crit)
-          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N);
+          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N,
+                    cl_pair_kb(p, nkb));
         else
-          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N);
+          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N,
+                  cl_pair_kb(p, nkb));
       }
       if (off && !early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
     }

@@ -433,6 +433,8 @@ bool plan_cluster(bool fwd, int kc, const std::vector<int>& ko, int tiles, int L
   size_t smem = cl_smem_bytes(cs, ncomax, Bp, stages);
   while (smem > (size_t)kSmemLimit && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, Bp, --stages);
   if (smem > (size_t)kSmemLimit) return false;
+  // an even ring lets operand k-blocks travel in pairs (rec_cluster.cuh cl_pair_kb)
+  if (stages % 2 && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, Bp, --stages);
   if (fwd && (size_t)stages * Bp * kRowBytes < (size_t)(Bp / kc) * kTileM * 4) return false;
   smem = std::max(smem, (size_t)116 * 1024);  // one CTA per SM
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
