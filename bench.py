@@ -77,11 +77,15 @@ def recurrent_bytes(c: dict, fwd: bool) -> int:
 
 def ncu_traffic(kernel_prefix: str, config: str):
     """DRAM bytes (read + write) of the kernel from the committed ncu --set full capture of this
-    config (profiles/r01/ncu_summary_<config>_v2.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r01", f"ncu_summary_{config}_v2.json")
-    try:
-        summ = json.load(open(p))
-    except (OSError, ValueError):
+    config (profiles/r01/ncu_summary_<config>_v{3,2}.json), or None."""
+    summ = None
+    for ver in ("v3", "v2"):  # the newest committed capture of this config
+        try:
+            summ = json.load(open(os.path.join(ROOT, "profiles", "r01", f"ncu_summary_{config}_{ver}.json")))
+            break
+        except (OSError, ValueError):
+            continue
+    if summ is None:
         return None
     unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for rows in summ.values():
