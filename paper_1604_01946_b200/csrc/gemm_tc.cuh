@@ -442,11 +442,11 @@ __global__ void __launch_bounds__(256, 1)
 // N = 256 (94 B/cycle per SM). The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads
 // complete on the leader's full barrier; commits multicast to both CTAs' barriers.
 
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, int BN = 256>
 __global__ void __launch_bounds__(256, 1)
     k_gemm_p2(const GemmDesc* __restrict__ table, int count, int mt_max, int nt_max, int stages) {
   using P = PrecBF16;
-  constexpr int BN = 256, BH = BN / 2;  // N per pair tile, per CTA half
+  constexpr int BH = BN / 2;  // N per pair tile (128 or 256), per CTA half
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int a_bytes = kTileM * kRowBytes;

@@ -486,19 +486,19 @@ void launch_gemm_p(const GemmDesc* table_dev, int count, int M, int N, cudaStrea
   RW_CUDA(cudaGetLastError());
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int BN>
 void launch_gemm_p2(const GemmDesc* table_dev, int count, int M, int N, cudaStream_t s) {
-  const size_t stage = (size_t)(kTileM + 128) * kRowBytes;
+  const size_t stage = (size_t)(kTileM + BN / 2) * kRowBytes;
   int stages = 8;
   auto smem_of = [&](int st) { return 1024 + st * stage + (2 * st + 4) * 8 + 16; };
   while (stages > 2 && smem_of(stages) > (size_t)kSmemLimit) --stages;
   const size_t smem = smem_of(stages);
-  const int mt = ceil_div(M, 2 * kTileM), nt = ceil_div(N, 256);
+  const int mt = ceil_div(M, 2 * kTileM), nt = ceil_div(N, BN);
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long tiles = (long long)count * mt * nt;
   const int pairs = (int)std::min<long long>(tiles, sms / 2);
-  auto k = k_gemm_p2<AMN, BMN>;
+  auto k = k_gemm_p2<AMN, BMN, BN>;
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(2 * pairs, 1, 1);
@@ -525,7 +525,15 @@ void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int
   // 36 us one-tile-per-CTA vs 48 us persistent)
   const long long tiles = (long long)count * ceil_div(M, kTileM) * ceil_div(N, bn);
   if (P::kPlanes == 1 && !old && pair2 && bn == 256 && tiles > 148) {
-    launch_gemm_p2<AMN, BMN>(table_dev, count, M, N, s);
+    launch_gemm_p2<AMN, BMN, 256>(table_dev, count, M, N, s);
+    return;
+  }
+  // 128-column pair tiles (M = 256 x N = 128 per pair, half the TMEM): per SM a k-block moves
+  // 16 + 8 KB for 256 MMA cycles instead of 16 + 16 KB (RW_GEMM_2SM128=0 disables)
+  static const bool pair128 = !(getenv("RW_GEMM_2SM128") && atoi(getenv("RW_GEMM_2SM128")) == 0);
+  // (MN-major B only: a K-major B map has 128-row boxes, one CTA's half here is 64 rows)
+  if (P::kPlanes == 1 && !old && pair2 && pair128 && BMN && bn == 128 && tiles > 148) {
+    launch_gemm_p2<AMN, BMN, 128>(table_dev, count, M, N, s);
     return;
   }
   if (P::kPlanes == 1 && !old && (bn == 128 || bn == 256) && tiles > 148) {

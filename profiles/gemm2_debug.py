@@ -5,11 +5,12 @@ from paper_1604_01946_b200 import _lib
 L = _lib.load()
 M, N, K = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 amn, bmn = int(sys.argv[4]), int(sys.argv[5])
+bn = int(sys.argv[6]) if len(sys.argv) > 6 else 256
 torch.manual_seed(0)
 A = torch.randn(K, M, device="cuda") if amn else torch.randn(M, K, device="cuda")
 B = torch.randn(K, N, device="cuda") if bmn else torch.randn(N, K, device="cuda")
 D = torch.zeros(N, M, device="cuda")
-st = L.rw_test_gemm(0, amn, bmn, M, N, K, A.data_ptr(), M if amn else K, B.data_ptr(), N if bmn else K, D.data_ptr(), M, 256)
+st = L.rw_test_gemm(0, amn, bmn, M, N, K, A.data_ptr(), M if amn else K, B.data_ptr(), N if bmn else K, D.data_ptr(), M, bn)
 torch.cuda.synchronize()
 Ab = (A.t() if amn else A).to(torch.bfloat16).float()
 Bb = (B.t() if bmn else B).to(torch.bfloat16).float()
