@@ -247,6 +247,7 @@ struct rw_ctx {
   bool pair_f = false;                       // stepwise forward as CTA pairs (k_lstm_fwd<bf16, true>)
   bool pair_b = false;                       // persistent backward as CTA pairs (k_lstm_bwd<bf16, true>)
   bool ls_pers_f = false, ls_pers_b = false;  // layer-sequential: one persistent launch per layer
+  bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
@@ -1227,14 +1228,18 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
 
 // x_op / tapes for a forward: h/c block 0 from h0/c0 (already staged on device as raw H x B
 // per layer at stage + l*H*B) or zeros.
-void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev) {
+// `state`: also write block 0 (h0 / c0, zeros when null) of every layer's h, c, h-operand (and
+// its swizzled image). The graph-replayed passes leave it out: block 0 is written by nothing
+// else, so enqueue_pass re-zeroes it eagerly only after an rw_forward with explicit h0 / c0.
+void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev, bool state = true,
+                      bool inputs = true) {
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
-  if (!x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
+  if (inputs && !x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
         x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
   }
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < L && state; ++l) {
     const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
     const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
     ++g_launches;
@@ -1244,13 +1249,13 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
     k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
-  if (x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled operand images of x and h0
+  if (inputs && x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled operand images of x and h0
     const long long colsT = (long long)Bp * x->T;
     ++g_launches;
     k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(x->x_op.p(0)), x->Ip, Bp, 0, colsT, static_cast<uint8_t*>(x->xsw.p));
   }
-  if (x->fwd_sched == RW_SCHED_CLUSTER) {
+  if (state && x->fwd_sched == RW_SCHED_CLUSTER) {
     for (int l = 0; l < L; ++l, ++g_launches)
       k_swizzle_op<<<grid_for((long long)Hp / 8 * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
                                                                Hp, Bp, 0, Bp, static_cast<uint8_t*>(x->hsw[l].p));
@@ -1487,7 +1492,7 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
   const bool fwd = pass == 0 || pass == 2 || pass == 3;
   if (fwd) {
     PhaseTimer pt(x, 0, s);
-    forward_prologue(x, s, nullptr, nullptr);
+    forward_prologue(x, s, nullptr, nullptr, false);
   }
   if (fwd) {
     PhaseTimer pt(x, 1, s);
@@ -1522,6 +1527,10 @@ void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
   if (x->dirty) {
     PhaseTimer pt(x, 0, s);
     repack_params(x, s);
+  }
+  if ((pass == 0 || pass == 2 || pass == 3) && !x->state0_zero) {
+    forward_prologue(x, s, nullptr, nullptr, true, false);  // zero h0 / c0 blocks once
+    x->state0_zero = true;
   }
   if (x->profiling || !x->use_graphs) {
     enqueue_pass_body<P>(x, pass, s);
@@ -1717,6 +1726,7 @@ int rw_forward(rw_ctx* x, const float* xin, int training, const float* const* h0
     }
     repack_params(x, x->main);
     forward_prologue(x, x->main, h0 ? th0.f() : nullptr, c0 ? tc0.f() : nullptr);
+    x->state0_zero = !h0 && !c0;
     if (x->prec == kBF16)
       run_forward_rec<PrecBF16>(x, x->main, training != 0);
     else
@@ -2043,6 +2053,7 @@ extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
 }
 
 extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const float* W_next) {
+  x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
     if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)

@@ -230,3 +230,27 @@ def test_train_step_matches_pass():
     assert np.array_equal(got["y"], ref["y"]) and np.array_equal(got["dx0"], ref["dx0"])
     for a, b in zip(gdw + gdr + gdb, rdw + rdr + rdb):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("schedule", ["cluster", "persistent"])
+def test_state_blocks_restaged_after_explicit_h0(schedule):
+    """The graph-replayed passes do not rewrite the h0 / c0 blocks of the state tapes (block 0);
+    after an rw_forward with nonzero h0 / c0, the next zero-state pass must re-zero them: its
+    outputs equal a fresh context's bit for bit."""
+    from paper_1604_01946_b200 import Engine
+    from oracle import Dims
+    c, params, x, dy, h0, c0 = make_case(Dims(2, 256, 256, 64, 6), seed=41, bias=True, state=True)
+    outs = []
+    for pre in (False, True):
+        eng = make_engine(Engine, c, "bf16", schedule)
+        eng.set_params(params)
+        if pre:
+            eng.forward(params, x, True, h0, c0)  # nonzero block 0
+        eng.upload_inputs(x, dy)
+        eng.run_pass(2)
+        eng.sync()
+        y = np.zeros((c.hidden, c.batch * c.steps), dtype=np.float32, order="F")
+        dx0 = np.zeros((c.input, c.batch * c.steps), dtype=np.float32, order="F")
+        eng.read_outputs(y=y, dx0=dx0)
+        outs.append((y, dx0))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
