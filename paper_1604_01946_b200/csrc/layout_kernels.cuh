@@ -178,4 +178,42 @@ __global__ void k_db_reduce(const float* __restrict__ dbp, int slices, int H, in
   db[e] = acc;
 }
 
+// bf16 layer input in one pass: raw x (R x B per step, column-major) -> the padded plain
+// K-major operand (Rp x Bp per step) and its pre-swizzled step-block image (sw_off), 8
+// consecutive rows (one 16-byte chunk of either layout) per thread.
+__global__ void k_pad_swizzle_bf16(const float* __restrict__ src, int R, int B, int T, int Rp, int Bp,
+                                   __nv_bfloat16* __restrict__ plain, uint8_t* __restrict__ sw) {
+  const int kc = Rp >> 3;
+  const long long total = (long long)kc * Bp * T;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long col = e / kc;
+    const int k = (int)(e - col * kc) << 3;
+    const int t = (int)(col / Bp), b = (int)(col - (long long)t * Bp);
+    __align__(16) __nv_bfloat16 v[8];
+    const float* sc = src + ((long long)t * B + b) * R;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __float2bfloat16_rn((b < B && k + j < R) ? sc[k + j] : 0.0f);
+    const uint4 q = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(plain + col * Rp + k) = q;
+    *reinterpret_cast<uint4*>(sw + (long long)t * Rp * Bp * 2 + sw_off(k, b, Bp)) = q;
+  }
+}
+
+// All layers' bias-gradient reductions in one launch (blockIdx.y = layer within the group).
+constexpr int kDbGroup = 16;
+struct DbGroup {
+  const float* dbp[kDbGroup];
+  float* db[kDbGroup];
+};
+__global__ void k_db_reduce_layers(DbGroup grp, int slices, int H, int Hp) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 4 * H) return;
+  const float* dbp = grp.dbp[blockIdx.y];
+  const int g = e / H, u = e - g * H;
+  float acc = 0.0f;
+  for (int s = 0; s < slices; ++s) acc += dbp[(long long)s * 4 * Hp + g * Hp + u];
+  grp.db[blockIdx.y][e] = acc;
+}
+
 }  // namespace rw

@@ -1234,7 +1234,15 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
 void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev, bool state = true,
                       bool inputs = true) {
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
-  if (inputs && !x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
+  // cluster schedule (bf16): the plain operand and its swizzled image in one pass
+  const bool fused_x = inputs && !x->pp_prev && x->fwd_sched == RW_SCHED_CLUSTER && x->prec == kBF16 &&
+                       x->Ip % 8 == 0;
+  if (fused_x) {
+    ++g_launches;
+    k_pad_swizzle_bf16<<<grid_for((long long)x->Ip / 8 * Bp * x->T), 256, 0, s>>>(
+        x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, static_cast<__nv_bfloat16*>(x->x_op.p(0)),
+        static_cast<uint8_t*>(x->xsw.p));
+  } else if (inputs && !x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
         x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
@@ -1249,7 +1257,7 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
     k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
   }
-  if (inputs && x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled operand images of x and h0
+  if (inputs && !fused_x && x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled images of x
     const long long colsT = (long long)Bp * x->T;
     ++g_launches;
     k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT), 256, 0, s>>>(
@@ -1482,8 +1490,15 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
 
 void run_db(rw_ctx* x, cudaStream_t s) {
   const int slices = ceil_div(x->Bp, kXChunk) * x->ks_b * 2;
-  for (int l = 0; l < x->L; ++l, ++g_launches)
-    k_db_reduce<<<ceil_div(4 * x->H, 256), 256, 0, s>>>(x->dbp[l].f(), slices, x->H, x->Hp, x->db[l].f());
+  for (int l0 = 0; l0 < x->L; l0 += kDbGroup, ++g_launches) {
+    DbGroup grp{};
+    const int n = std::min(kDbGroup, x->L - l0);
+    for (int i = 0; i < n; ++i) {
+      grp.dbp[i] = x->dbp[l0 + i].f();
+      grp.db[i] = x->db[l0 + i].f();
+    }
+    k_db_reduce_layers<<<dim3(ceil_div(4 * x->H, 256), n), 256, 0, s>>>(grp, slices, x->H, x->Hp);
+  }
   RW_CUDA(cudaGetLastError());
 }
 
