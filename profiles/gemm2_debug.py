@@ -1,3 +1,6 @@
+"""One tcgen05 GEMM through rw_test_gemm against a torch fp32 reference of bf16-rounded inputs
+(scaled max error and kernel time). Usage: python profiles/gemm2_debug.py M N K a_mn b_mn [bn]
+(bn 256 with > 148 tiles selects the CTA-pair kernel k_gemm_p2)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

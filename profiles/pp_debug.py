@@ -1,3 +1,5 @@
+"""Layer-pipeline debugging on one GPU: two pipeline stages in one process run one after the
+other (RW_PP_RING = T), outputs compared with a single context. Paths are this container's."""
 import os, sys, time
 import os; os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests"); sys.path.insert(0, "/root/repo/oracle")
