@@ -437,7 +437,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
           const float* src = base + ((size_t)cl_slot(s, m) * nco + i * 8) * kTileM;
           float v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = src[(size_t)j * kTileM];
+          for (int j = 0; j < 8; ++j) v[j] = lds_f32(src + (size_t)j * kTileM);  // explicit ld.shared
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] += v[j];
         }
