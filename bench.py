@@ -389,6 +389,11 @@ def run_ours(args) -> None:
                       "algorithmic_flops_per_launch": dom_fl, "algorithmic_bytes_per_launch": dom_by,
                       "avg_launch_ms": dom_ms}),
         "phases_ms": {k: v[0] / max(v[1], 1) for k, v in ph.items()},
+        # SURVEY §8d's latency bound: the wavefront's dependent steps (T + L - 1 per direction,
+        # + the dh0 step backward) and the measured time per step of each recurrent phase
+        "critical_path": {"steps_fwd": T + L - 1, "steps_bwd": T + L,
+                          "us_per_step_fwd": 1e3 * fwd_ms / (T + L - 1),
+                          "us_per_step_bwd": 1e3 * bwd_ms / (T + L)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu_base,
