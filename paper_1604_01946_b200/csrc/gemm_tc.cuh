@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % stages;
-      mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+      mbar_wait_bounded(&empty[s], ((kb / stages) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], stage_bytes);
       uint8_t* st = smem + s * stage_bytes;
       const int k = kb * P::kAtomK;
@@ -183,14 +183,14 @@ __global__ void __launch_bounds__(256, 1)
     for (int c = 0; c < nchunks; ++c) {
       const int buf = c & 1;
       if (c >= 2) {
-        mbar_wait(&tmem_empty[buf], ((c >> 1) - 1) & 1);
+        mbar_wait_bounded(&tmem_empty[buf], ((c >> 1) - 1) & 1);
         tc_fence_after();
       }
       const uint32_t acc = tmem_base + buf * bn;
       const int kb_end = min(nkb, (c + 1) * ckb);
       for (int k0 = kb; kb < kb_end; ++kb) {
         const int s = kb % stages;
-        mbar_wait(&full[s], (kb / stages) & 1);
+        mbar_wait_bounded(&full[s], (kb / stages) & 1);
         tc_fence_after();
         const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
 #pragma unroll
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < kChunkBN; ++i) accum[i] = 0.0f;
       for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
-        mbar_wait(&tmem_full[buf], (c >> 1) & 1);
+        mbar_wait_bounded(&tmem_full[buf], (c >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < kChunkBN; c0 += 8) {
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     } else {
-      mbar_wait(&tmem_full[0], 0);
+      mbar_wait_bounded(&tmem_full[0], 0);
       tc_fence_after();
       ColCursor cc(g, n0);
       float* const drow = g.d + (orow < 0 ? 0 : orow);
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256, 1)
       const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
       for (int kb = 0; kb < nkb; ++kb, ++pc) {
         const int s = pc % stages;
-        mbar_wait(&empty[s], ((pc / stages) & 1) ^ 1);
+        mbar_wait_bounded(&empty[s], ((pc / stages) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         uint8_t* st = smem + s * stage_bytes;
         const int k = kb * P::kAtomK;
@@ -368,13 +368,13 @@ __global__ void __launch_bounds__(256, 1)
       const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
       const int buf = tc & 1;
       if (tc >= 2) {
-        mbar_wait(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
+        mbar_wait_bounded(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
         tc_fence_after();
       }
       const uint32_t acc = tmem_base + buf * BN;
       for (int kb = 0; kb < nkb; ++kb, ++pc) {
         const int s = pc % stages;
-        mbar_wait(&full[s], (pc / stages) & 1);
+        mbar_wait_bounded(&full[s], (pc / stages) & 1);
         tc_fence_after();
         const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
 #pragma unroll
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, 1)
       const GemmDesc& g = table[z];
       if (m0 >= g.M || n0 >= g.N) continue;
       const int buf = tc & 1;
-      mbar_wait(&tmem_full[buf], (tc >> 1) & 1);
+      mbar_wait_bounded(&tmem_full[buf], (tc >> 1) & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
       const int orow = m < g.M ? gemm_out_row(g, m) : -1;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256, 1)
       const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
       for (int kb = 0; kb < nkb; ++kb, ++pc) {
         const int s = pc % stages;
-        mbar_wait(&empty[s], ((pc / stages) & 1) ^ 1);
+        mbar_wait_bounded(&empty[s], ((pc / stages) & 1) ^ 1);
         if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * stage_bytes);
         uint8_t* st = smem + s * stage_bytes;
         const int k = kb * P::kAtomK;
@@ -537,13 +537,13 @@ __global__ void __launch_bounds__(256, 1)
       const int nkb = (g.K + P::kAtomK - 1) / P::kAtomK;
       const int buf = tc & 1;
       if (tc >= 2) {
-        mbar_wait(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
+        mbar_wait_bounded(&tmem_empty[buf], ((tc >> 1) - 1) & 1);
         tc_fence_after();
       }
       const uint32_t acc = tmem_base + buf * BN;
       for (int kb = 0; kb < nkb; ++kb, ++pc) {
         const int s = pc % stages;
-        mbar_wait(&full[s], (pc / stages) & 1);
+        mbar_wait_bounded(&full[s], (pc / stages) & 1);
         tc_fence_after();
         const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
 #pragma unroll
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(256, 1)
       const GemmDesc& g = table[z];
       if (m0 >= g.M || n0 >= g.N) continue;
       const int buf = tc & 1;
-      mbar_wait(&tmem_full[buf], (tc >> 1) & 1);
+      mbar_wait_bounded(&tmem_full[buf], (tc >> 1) & 1);
       tc_fence_after();
       const int m = m0 + (int)rank * kTileM + q * 32 + lane;
       const int orow = m < g.M ? gemm_out_row(g, m) : -1;

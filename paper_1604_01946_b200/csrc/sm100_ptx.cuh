@@ -74,6 +74,18 @@ RW_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
+// Bounded variant for the GEMM kernels (no flag protocol of their own): a wait that has not
+// completed after `kGemmWaitNs` traps, so a lost arrival surfaces as a launch error on the
+// host instead of a GPU that never returns.
+constexpr unsigned long long kGemmWaitNs = 20ULL * 1000000000ULL;
+RW_DEVICE void mbar_wait_bounded(uint64_t* bar, uint32_t phase) {
+  if (mbar_try_wait(bar, phase)) return;
+  const uint64_t t0 = globaltimer();
+#pragma unroll 1
+  while (!mbar_try_wait(bar, phase)) {
+    if (globaltimer() - t0 > kGemmWaitNs) __trap();
+  }
+}
 
 // ------------------------------------------------------------------ TMA
 RW_DEVICE void prefetch_tmap(const CUtensorMap* m) {
