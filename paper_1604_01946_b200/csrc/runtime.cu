@@ -832,6 +832,7 @@ void build(rw_ctx* x) {
   std::vector<int> m_hopLS(2 * L), m_dgLS(2 * L);
   std::vector<int> m_dgT(2 * L), m_hT(2 * L);
   x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 64;
+  if (const char* e = getenv("RW_BN_DX")) x->bn_dx = atoi(e);
   x->bn_wg = x->prec == kBF16 ? 128 : 64;
   for (int p = 0; p < x->planes; ++p) {
     for (int l = 0; l < L; ++l) {
