@@ -8,3 +8,4 @@ from .engine import (  # noqa: F401
     flop_count, gate_count, init_params, make_dy, make_input, pretranspose, random_matrix,
     splitmix_symmetric,
 )
+from . import param_io  # noqa: F401  (reference parameter files, param_io.hpp)

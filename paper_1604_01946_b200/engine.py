@@ -344,6 +344,15 @@ class Engine:
                     or np.asarray(p.bias).size != gh):
                 raise ValueError(f"engine: layer {l} parameter shapes do not match the configuration")
 
+    def load_params_file(self, path: str):
+        """Load a reference `save-params` file (param_io.hpp) into this context; returns the
+        parameters (needed again by forward / backward_data, as in the reference API)."""
+        from . import param_io
+        h, params = param_io.load_params(path)
+        param_io.check_matches(h, self.cfg)
+        self.set_params(params)
+        return params
+
     def set_params(self, params) -> None:
         self._check_params(params)
         for l, p in enumerate(params):
