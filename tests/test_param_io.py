@@ -76,3 +76,18 @@ def test_param_file_into_device_context_matches_reference(reference):
     dev = run_device(eng, params, x, dy, h0, c0)
     ref = run_reference(reference, c, params, x, dy, h0, c0)
     assert_within(compare(dev, ref, c), "fp32")
+
+
+def test_cpp_facade_param_io(tmp_path):
+    """The C++ facade's rnnwave/param_io.hpp (include/) reads the reference-written file
+    bit-exactly and writes it back byte-identically (tests/cpp/param_io_check.cpp)."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "pio"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "param_io_check.cpp"), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), FIX, str(tmp_path / "out.bin")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
