@@ -254,3 +254,27 @@ def test_state_blocks_restaged_after_explicit_h0(schedule):
         eng.read_outputs(y=y, dx0=dx0)
         outs.append((y, dx0))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch):
+    """RW_TRACE writes the recurrent kernels' stamps in the reference's trace schema; like the
+    reference's validate_trace, every dependency's end precedes its dependent's start
+    (profiles/validate_trace.py)."""
+    import importlib.util
+    import os as _os
+    from paper_1604_01946_b200 import Engine
+    from oracle import Dims
+    path = tmp_path / "trace.csv"
+    monkeypatch.setenv("RW_TRACE", str(path))
+    c, params, x, dy, h0, c0 = make_case(Dims(3, 512, 512, 64, 8), seed=43, bias=True, state=False)
+    eng = make_engine(Engine, c, "bf16", "cluster")
+    eng.set_params(params)
+    eng.upload_inputs(x, dy)
+    eng.run_pass(2)
+    eng.sync()
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("vt", _os.path.join(root, "profiles", "validate_trace.py"))
+    vt = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(vt)
+    assert path.exists()
+    assert vt.validate(str(path)) is None
