@@ -169,9 +169,10 @@ def run_reference(args) -> None:
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle  # the reference CPU engine (oracle/_ref) -- checker/baseline leg only
     R = oracle.Reference()
-    d = oracle.Dims(**CONFIG_B)
+    c = dict(CONFIGS[args.config])  # the same workload as our arm's line
+    d = oracle.Dims(**c)
     cores = os.cpu_count() or 1
-    flops = pass_flops(CONFIG_B)
+    flops = pass_flops(c)
     # one pass of the reference engine at O6 ~ seconds; bound the run to a few minutes
     est = R.time(d, seed=42, pass_kind=2, reps=1, warmup=0, workers=cores)["median_us"] * 1e-6
     budget = 150.0
@@ -185,11 +186,11 @@ def run_reference(args) -> None:
         "n_gpus": args.gpus, "steps": reps, "warmup": warm, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SplitMix64 seed 42, reference generators)",
-        "config": {"workload": "4L h512 mb64 T100 LSTM fwd+bwd (BASELINE configs[1])",
-                   "global_batch": CONFIG_B["batch"], "seq_len": CONFIG_B["steps"],
-                   "layers": 4, "hidden": 512, "opt_level": 6, "workers": cores},
+        "config": {"workload": workload_name(args.config, c),
+                   "global_batch": c["batch"], "seq_len": c["steps"],
+                   "layers": c["layers"], "hidden": c["hidden"], "opt_level": 6, "workers": cores},
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "reference",
-                         "sample": f"{reps} full config-B passes (median), O6, {cores} workers",
+                         "sample": f"{reps} full config-{args.config} passes (median), O6, {cores} workers",
                          "lib": os.path.basename(R.path)},
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
