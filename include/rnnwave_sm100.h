@@ -48,8 +48,19 @@ typedef enum {
 
 typedef enum {
   RW_PREC_BF16 = 0,     /* bf16 tensor-core operands, fp32 accumulate + fp32 cell math   */
-  RW_PREC_FP32 = 1      /* fp32-parity: 3xTF32 split operands, fp32 accumulate           */
+  RW_PREC_FP32 = 1      /* fp32-parity (normwise <= 1e-5 vs the fp32 reference): split
+                           operands, fp32 accumulate + accurate fp32 cell math. The operand
+                           format is chosen per shape: fp16x2 (hi + lo fp16 planes, 3 MMAs
+                           per product) on the cluster schedule, 3xTF32 elsewhere
+                           (rw_describe_precision) */
 } rw_precision;
+
+/* Operand format a context computes in (rw_describe_precision). */
+typedef enum {
+  RW_FMT_BF16 = 0,
+  RW_FMT_TF32X3 = 1,
+  RW_FMT_FP16X2 = 2
+} rw_operand_format;
 
 typedef enum {
   RW_SCHED_AUTO = 0,       /* cluster, else persistent, else stepwise: the first that fits */
@@ -152,6 +163,9 @@ int rw_describe(rw_ctx* ctx, int* fwd_sched, int* bwd_sched, int* fwd_ksplit, in
  * backward run one persistent launch per layer; wgrad_bn = N tile of the weight-gradient GEMMs
  * (256 = pairs). */
 int rw_describe_variants(rw_ctx* ctx, int* pairs, int* wgrad_bn);
+
+/* The operand format (rw_operand_format) the context's tensor-core GEMMs use. */
+int rw_describe_precision(rw_ctx* ctx, int* fmt);
 
 /* Copy the results of the last rw_run_pass to host buffers (any may be NULL): y (H x B*T),
  * dx0 (I x B*T), dW / dR / db per layer (reference layouts). Synchronous. */

@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -14,7 +15,23 @@ namespace rw {
 //   kTF32x3: operands split x = hi + lo, hi = tf32(x) (round-to-nearest), lo = x - hi, and
 //            D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::tf32), 2 planes -- the fp32-parity
 //            mode (normwise error ~1e-6 vs the fp32 reference engine).
-enum Prec : int { kBF16 = 0, kTF32x3 = 1 };
+//   kF16x2 : operands split x = hi + lo, hi = fp16_rn(x), lo = fp16_rn(x - hi) (22 significant
+//            bits), D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::f16, fp16 rate), 2 planes of 2
+//            bytes. The fp32-parity mode of the cluster schedule: half the bytes of 3xTF32 and
+//            twice its MMA rate, so the recurrent weights stay on chip (A_hi resident in shared
+//            memory, A_lo in tensor memory as the A operand of tcgen05.mma "TS"). Weight planes
+//            are stored pre-scaled by 2^kWScaleLog2 (exact) so their lo part stays a normal fp16;
+//            epilogues multiply weight products by 2^-kWScaleLog2. Activation lo parts are
+//            unscaled: a subnormal lo carries an absolute error <= 2^-25, far below the 1e-5
+//            normwise contract for operands of O(1) magnitude (profiles/ubench/f16x2_ts_check.cu:
+//            normwise 6.4e-7 at K = 512 vs an fp64 product). Range: |weights| < 255, |x|, |h|,
+//            |dG| < 65504.
+enum Prec : int { kBF16 = 0, kTF32x3 = 1, kF16x2 = 2 };
+constexpr int kWScaleLog2 = 8;
+
+__host__ __device__ constexpr int prec_planes(int prec) { return prec == kBF16 ? 1 : 2; }
+__host__ __device__ constexpr int prec_elem(int prec) { return prec == kTF32x3 ? 4 : 2; }
+__host__ __device__ constexpr int prec_atomk(int prec) { return prec == kTF32x3 ? 32 : 64; }
 
 struct PrecBF16 {
   static constexpr int kPlanes = 1;
@@ -34,6 +51,22 @@ struct PrecTF32x3 {
   static constexpr bool kTF32 = true;
   static constexpr int kCombos = 3;
 };
+
+struct PrecF16x2 {
+  static constexpr int kPlanes = 2;
+  static constexpr int kElem = 2;
+  static constexpr int kAtomK = 64;
+  static constexpr int kUmmaK = 16;
+  static constexpr uint32_t kFmt = 0;  // kind::f16 with fp16 inputs
+  static constexpr bool kTF32 = false;
+  static constexpr int kCombos = 3;
+};
+
+// fp16x2 split of v (already scaled): hi = fp16_rn(v), lo = fp16_rn(v - hi) (v - hi is exact in fp32).
+__device__ __forceinline__ void f16x2_split(float v, __half& hi, __half& lo) {
+  hi = __float2half_rn(v);
+  lo = __float2half_rn(v - __half2float(hi));
+}
 
 constexpr int kTileM = 128;      // UMMA M (cta_group::1)
 constexpr int kRowBytes = 128;   // one SWIZZLE_128B row
@@ -70,6 +103,7 @@ struct GemmDesc {
   int m_valid, n_valid;  // identity-mode bounds
   int accumulate;      // D += result instead of D = result
   int b_n_off;         // row (N) offset inside the B tensor (e.g. h_{l-1} starts at column block 1)
+  float alpha;         // D = alpha * A B^T (fp16x2 weight operands carry 2^kWScaleLog2); 0 means 1
 };
 
 }  // namespace rw

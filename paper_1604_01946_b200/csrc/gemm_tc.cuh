@@ -239,13 +239,15 @@ __global__ void __launch_bounds__(256, 1)
         float* const drow = g.d + orow;
         const long long ldd = g.ldd;
         const bool accum_out = g.accumulate != 0;
+        const float alpha = g.alpha != 0.0f ? g.alpha : 1.0f;
 #pragma unroll
         for (int j = 0; j < kChunkBN; ++j) {
           if (n0 + j >= g.N) break;
           const long long oc = cc.next();
           if (oc < 0) continue;
           float* dst = drow + oc * ldd;
-          *dst = accum_out ? *dst + accum[j] : accum[j];
+          const float val = accum[j] * alpha;
+          *dst = accum_out ? *dst + val : val;
         }
       }
     } else {
@@ -255,6 +257,7 @@ __global__ void __launch_bounds__(256, 1)
       float* const drow = g.d + (orow < 0 ? 0 : orow);
       const long long ldd = g.ldd;
       const bool accum_out = g.accumulate != 0;
+      const float alpha = g.alpha != 0.0f ? g.alpha : 1.0f;
       const int nlim = min(bn, g.N - n0);
       for (int c0 = 0; c0 < bn; c0 += 8) {
         uint32_t v[8];
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(256, 1)
           const long long oc = cc.next();
           if (oc < 0) continue;
           float* dst = drow + oc * ldd;
-          const float val = __uint_as_float(v[j]);
+          const float val = __uint_as_float(v[j]) * alpha;
           *dst = accum_out ? *dst + val : val;
         }
       }
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(256, 1)
       float* const drow = g.d + (orow < 0 ? 0 : orow);
       const long long ldd = g.ldd;
       const bool accum_out = g.accumulate != 0;
+      const float alpha = g.alpha != 0.0f ? g.alpha : 1.0f;
       const int nlim = min(BN, g.N - n0);
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[8], w[8];
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(256, 1)
           const long long oc = cc.next();
           if (oc < 0) continue;
           float* dst = drow + oc * ldd;
-          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]);
+          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]) * alpha;
           *dst = accum_out ? *dst + val : val;
         }
       }
@@ -574,6 +578,7 @@ __global__ void __launch_bounds__(256, 1)
       float* const drow = g.d + (orow < 0 ? 0 : orow);
       const long long ldd = g.ldd;
       const bool accum_out = g.accumulate != 0;
+      const float alpha = g.alpha != 0.0f ? g.alpha : 1.0f;
       const int nlim = min(BN, g.N - n0);
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[8], w[8];
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(256, 1)
           const long long oc = cc.next();
           if (oc < 0) continue;
           float* dst = drow + oc * ldd;
-          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]);
+          const float val = __uint_as_float(j < 8 ? v[j] : w[j - 8]) * alpha;
           *dst = accum_out ? *dst + val : val;
         }
       }

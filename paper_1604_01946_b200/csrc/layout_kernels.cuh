@@ -9,9 +9,16 @@
 
 namespace rw {
 
-__device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long long idx, float v) {
+// `wscale`: weight operands of the fp16x2 mode are stored as 2^kWScaleLog2 * W (common.cuh).
+__device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long long idx, float v,
+                                             bool wscale = false) {
   if (prec == kBF16) {
     static_cast<__nv_bfloat16*>(p0)[idx] = __float2bfloat16_rn(v);
+  } else if (prec == kF16x2) {
+    __half hi, lo;
+    f16x2_split(wscale ? v * (float)(1 << kWScaleLog2) : v, hi, lo);
+    static_cast<__half*>(p0)[idx] = hi;
+    static_cast<__half*>(p1)[idx] = lo;
   } else {
     uint32_t hi;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
@@ -22,17 +29,22 @@ __device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long 
 }
 
 // Forward operand of layer l: rows rho (4Hp), K = [0, Ipl) from W, [Ipl, Ipl+Hp) from R.
+// W and R are column-major (element (row, k) at k*4H + row), the operand is K-major (k
+// contiguous per rho row), so the kernel transposes through shared memory: a block moves a
+// tile of 32 rho rows (one gate of 32 consecutive units = 32 consecutive source rows) x 64 k,
+// reading 128-byte runs of the source columns and writing 64-element runs of the operand rows.
+// grid (ceil((Ipl + Hp) / 64), 4Hp / 32), block (32, 8).
 __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__ R, int H, int I,
                           int Hp, int Ipl, int prec, void* p0, void* p1) {
-  const long long K = Ipl + Hp;
-  const long long total = 4LL * Hp * K;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int rho = (int)(e / K);
-    const int k = (int)(e - rho * K);
-    const int g = rho_gate(rho), u = rho_unit(rho);
+  __shared__ float tile[64][33];
+  const int K = Ipl + Hp;
+  const int k0 = blockIdx.x * 64, rho0 = blockIdx.y * 32;
+  const int g = rho_gate(rho0), u0 = rho_unit(rho0);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int kk = ty; kk < 64; kk += 8) {
+    const int k = k0 + kk, u = u0 + tx;
     float v = 0.0f;
-    if (u < H) {
+    if (u < H && k < K) {
       const long long row = (long long)g * H + u;
       if (k < Ipl) {
         if (k < I) v = W[(long long)k * 4 * H + row];
@@ -40,7 +52,14 @@ __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__
         v = R[(long long)(k - Ipl) * 4 * H + row];
       }
     }
-    store_planes(prec, p0, p1, e, v);
+    tile[kk][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    for (int kk = tx; kk < 64; kk += 32) {
+      const int k = k0 + kk;
+      if (k < K) store_planes(prec, p0, p1, (long long)(rho0 + r) * K + k, tile[kk][r], true);
+    }
   }
 }
 
@@ -60,7 +79,7 @@ __global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict
     const int g = rho_gate(rho), up = rho_unit(rho);
     float v = 0.0f;
     if (u < H && up < H) v = M[(long long)u * 4 * H + (long long)g * H + up];
-    store_planes(prec, p0, p1, e, v);
+    store_planes(prec, p0, p1, e, v, true);
   }
 }
 
@@ -76,7 +95,7 @@ __global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, i
     const int g = rho_gate(rho), u = rho_unit(rho);
     float v = 0.0f;
     if (i < I && u < H) v = W0[(long long)i * 4 * H + (long long)g * H + u];
-    store_planes(prec, p0, p1, e, v);
+    store_planes(prec, p0, p1, e, v, true);
   }
 }
 
@@ -107,20 +126,27 @@ __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk
   }
 }
 
-// Plain K-major bf16 operand (column c = t*Bp + n holds K contiguous elements) -> swizzled step
-// blocks (block t at t * K * Bp * 2 bytes), columns [c0, c0 + ncols). One thread per 8 consecutive
-// K elements: they form one 16-byte chunk in both layouts (sw_off permutes whole chunks).
-__global__ void k_swizzle_op(const __nv_bfloat16* __restrict__ src, int K, int Bp, long long c0, long long ncols,
-                             uint8_t* __restrict__ dst) {
+// Plain K-major 16-bit operand planes (column c = t*Bp + n holds K contiguous elements) ->
+// swizzled step blocks, columns [c0, c0 + ncols). One plane (bf16): block t at t*K*Bp*2 bytes,
+// Bp rows per k-block. Two planes (fp16x2 hi, lo): block t at t*K*2Bp*2 bytes, each k-block
+// holds the hi rows then the lo rows (2Bp rows), so one bulk copy brings both planes of a
+// k-block (rec_cluster.cuh). One thread per 8 consecutive K elements of one plane: they form
+// one 16-byte chunk in both layouts (sw_off permutes whole chunks).
+__global__ void k_swizzle_op(const uint16_t* __restrict__ s0, const uint16_t* __restrict__ s1, int K, int Bp,
+                             long long c0, long long ncols, uint8_t* __restrict__ dst) {
   const int kc = K >> 3;
-  const long long total = (long long)kc * ncols;
+  const int planes = s1 ? 2 : 1, rows = planes * Bp;
+  const long long total = (long long)kc * ncols * planes;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long c = c0 + e / kc;
-    const int k = (int)(e % kc) << 3;
+    const int pl = (int)(e % planes);
+    const long long ee = e / planes;
+    const long long c = c0 + ee / kc;
+    const int k = (int)(ee % kc) << 3;
     const long long t = c / Bp;
     const int n = (int)(c - t * Bp);
-    *reinterpret_cast<uint4*>(dst + t * (long long)K * Bp * 2 + sw_off(k, n, Bp)) =
+    const uint16_t* src = pl ? s1 : s0;
+    *reinterpret_cast<uint4*>(dst + t * (long long)K * rows * 2 + sw_off(k, n + pl * Bp, rows)) =
         *reinterpret_cast<const uint4*>(src + c * K + k);
   }
 }

@@ -54,7 +54,7 @@ struct FwdLayer {
   float* tanhc;              // Hp x Bp T, null in inference
   uint32_t* flags;           // [T] completion counters
   // cluster schedule: pre-swizzled bf16 operand step blocks (layout_kernels.cuh sw_off)
-  uint8_t* hsw;              // own h: block t+1 = h_t, block 0 = h0 (Hp x Bp per block)
+  uint8_t* hsw;              // own h: block t+1 = h_t, block 0 = h0 (Hp x Bp per block; fp16x2: x 2 planes)
   const uint8_t* bxsw;       // layer input: x (blocks 0..T-1, Ipl x Bp) or hsw of layer l-1 (+1 block)
   int bx_blk_off;
   // layer-sequential schedule: the input projection W.x of every step was computed beforehand by
@@ -65,6 +65,10 @@ struct FwdLayer {
   // CTA of a pair loading half of the batch columns
   const CUtensorMap* bx2;
   const CUtensorMap* bh2;
+  // cluster schedule, fp16x2: the lo plane of [W|R] (K-major rows of alo_ld elements, alo_rows
+  // rows), copied once into tensor memory as the A operand of the lo x hi products
+  const uint16_t* alo;
+  int alo_ld, alo_rows;
 };
 
 struct BwdLayer {
@@ -93,6 +97,8 @@ struct BwdLayer {
   // CTA-pair persistent backward (k_lstm_bwd<_, true>): bf16 dG operand maps with Bp/2-row boxes
   const CUtensorMap* bup2;
   const CUtensorMap* bg2;
+  const uint16_t* alo;       // cluster schedule, fp16x2: lo plane of [W_{l+1}^T | R_l^T] (as FwdLayer)
+  int alo_ld, alo_rows;
 };
 
 struct RecParams {
@@ -141,6 +147,11 @@ template <class P>
 __device__ __forceinline__ void store_operand(void* const* planes, long long idx, float v) {
   if constexpr (P::kPlanes == 1) {
     static_cast<__nv_bfloat16*>(planes[0])[idx] = __float2bfloat16_rn(v);
+  } else if constexpr (!P::kTF32) {  // fp16x2
+    __half hi, lo;
+    f16x2_split(v, hi, lo);
+    static_cast<__half*>(planes[0])[idx] = hi;
+    static_cast<__half*>(planes[1])[idx] = lo;
   } else {
     uint32_t hi;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(v));
@@ -175,20 +186,25 @@ __device__ __forceinline__ float act_tanh(float x) {
   }
 }
 
-// Spin until *flag >= target (gpu-scope acquire), bounded by a timeout that records an
+// Counters are cumulative over passes (targets = epoch x per-pass count, all mod 2^32), so
+// "reached" is the wrap-safe signed distance, never a plain unsigned >=: after 2^32 arrivals the
+// counter restarts near 0 while the target is still large (or the target wraps first).
+__device__ __forceinline__ bool flag_reached(uint32_t v, uint32_t target) { return (int32_t)(v - target) >= 0; }
+
+// Spin until *flag reaches target (gpu-scope acquire), bounded by a timeout that records an
 // error instead of hanging the device. `code` identifies the wait for the host message.
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target, int* error,
                                           unsigned long long timeout_ns, int code) {
   // Poll with relaxed loads (an acquire load per iteration would invalidate the SM's L1 each
   // time, CCTL.IVALL, slowing every other warp on the SM); one acquire once satisfied.
-  bool ok = ld_relaxed_gpu(flag) >= target;
+  bool ok = flag_reached(ld_relaxed_gpu(flag), target);
 #pragma unroll 1
-  for (int i = 0; i < 65536 && !ok; ++i) ok = ld_relaxed_gpu(flag) >= target;
+  for (int i = 0; i < 65536 && !ok; ++i) ok = flag_reached(ld_relaxed_gpu(flag), target);
   if (!ok) {
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
 #pragma unroll 1
-    while (ld_relaxed_gpu(flag) < target) {
+    while (!flag_reached(ld_relaxed_gpu(flag), target)) {
       nanosleep(ns);
       if (ns < 128) ns <<= 1;
       if (globaltimer() - t0 > timeout_ns) {

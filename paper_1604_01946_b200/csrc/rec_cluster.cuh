@@ -1,5 +1,13 @@
 // rec_cluster.cuh -- persistent recurrent kernels with split roles per tile ("cluster"
-// schedule). bf16 operands, fp32 accumulation and cell math.
+// schedule). bf16 or fp16x2 (fp32-parity) operands, fp32 accumulation and
+// cell math.
+//
+// fp16x2 (common.cuh PrecF16x2): the resident weight slice is split A = A_hi + A_lo; A_hi stays
+// in shared memory exactly like the bf16 slice, A_lo lives in TENSOR MEMORY (copied once per
+// launch by the epilogue warps) and is the A operand of tcgen05.mma's TMEM-A form. Operand step
+// blocks carry both planes per k-block ([hi rows | lo rows], one bulk copy), and every K = 16 step
+// issues A_hi.B_hi, A_hi.B_lo, A_lo.B_hi into the same accumulator -- so the fp32-parity slices
+// need no more shared memory than bf16 ones and the same CTA count fits the GPU.
 //
 // Why: in a persistent wavefront the per-step critical path bounds small-H configs (config B:
 // 206 dependent steps). Measured on B200 (profiles/ubench/sync_ubench.cu): a gpu-scope flag
@@ -70,6 +78,8 @@ struct ClOff {
   const uint32_t* consumed;
   int sys;
   int active;
+  const uint16_t* alo;       // fp16x2: lo plane of the target layer's weights (FwdLayer::alo)
+  int alo_ld, alo_rows;
 };
 
 struct ClParams {
@@ -112,21 +122,24 @@ struct ClSmem {
   uint64_t* push_free;   // every owner consumed this member's previous push
   uint64_t* off_full;    // critical: off partial landed in rxoff
   uint64_t* off_empty;   // critical: epilogue finished reading rxoff
+  uint64_t* alo_full;    // fp16x2: A_lo copied into tensor memory (128 epilogue arrivals)
   uint32_t* tmem_slot;
 };
 
 __host__ __device__ inline size_t cl_slot_bytes(int ncomax) { return (size_t)ncomax * 128 * 4; }
-__host__ __device__ inline size_t cl_smem_bytes(int cs, int ncomax, int N, int stages) {
-  return 1024 + (size_t)kClKBlocks * kTileM * kRowBytes + (size_t)stages * N * kRowBytes +
+// `rows`: operand rows per stage (Bp, or 2 Bp for the two fp16x2 planes)
+__host__ __device__ inline size_t cl_smem_bytes(int cs, int ncomax, int rows, int stages) {
+  return 1024 + (size_t)kClKBlocks * kTileM * kRowBytes + (size_t)stages * rows * kRowBytes +
          (2 * (size_t)(cs - 1) + 1) * cl_slot_bytes(ncomax) + (2 * stages + 12) * 8 + 16;
 }
 
+template <class P>
 __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
   ClSmem s;
   const size_t slot = cl_slot_bytes(p.ncomax);
   s.a = smem;
   s.b = s.a + kClKBlocks * kTileM * kRowBytes;
-  s.rx = reinterpret_cast<float*>(s.b + p.stages * p.Bp * kRowBytes);
+  s.rx = reinterpret_cast<float*>(s.b + p.stages * P::kPlanes * p.Bp * kRowBytes);
   s.rxoff = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rx) + (p.cs - 1) * slot);
   s.st = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rxoff) + slot);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.st) + (p.cs - 1) * slot);
@@ -139,7 +152,8 @@ __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
   s.push_free = s.a_full + 6;
   s.off_full = s.a_full + 7;
   s.off_empty = s.a_full + 8;
-  s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 9);
+  s.alo_full = s.a_full + 9;
+  s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 10);
   return s;
 }
 
@@ -160,7 +174,7 @@ __global__ void k_pp_wait(const uint32_t* ready, const uint32_t* my_epoch, int* 
       atomicCAS(error, 0, (1 << 30) | (4 << 26));
       return;
     }
-  } while (v < e);
+  } while (!flag_reached(v, e));
 }
 
 __device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
@@ -206,7 +220,7 @@ __device__ __forceinline__ void wait_flag_s(const uint32_t* flag, uint32_t targe
   }
   const uint64_t t0 = globaltimer();
 #pragma unroll 1
-  while (ld_relaxed_s(flag, true) < target) {
+  while (!flag_reached(ld_relaxed_s(flag, true), target)) {
     if (globaltimer() - t0 > timeout_ns) {
       atomicCAS(error, 0, code);
       atomicMax(error + 1, (int)ld_relaxed_s(flag, true));
@@ -266,6 +280,7 @@ __device__ __forceinline__ uint32_t cl_setup(const ClSmem& S, const ClParams& p,
     mbar_init(S.push_free, n_act > 1 ? n_act - 1 : 1);
     mbar_init(S.off_full, 1);
     mbar_init(S.off_empty, 1);
+    mbar_init(S.alo_full, 128);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -298,6 +313,30 @@ __device__ __forceinline__ void cl_load_a(const ClSmem& S, const CUtensorMap* a,
     tma_load_2d(S.a + (kb - kb_lo) * a_bytes, a, S.a_full, kb * 64, row0);
 }
 
+// fp16x2: copy this member's A_lo slice (rows row0.., k-blocks [kb_lo, kb_lo + nkb)) from the
+// K-major lo plane into tensor memory columns [tmem_alo, tmem_alo + 32 nkb): two fp16 per
+// 32-bit column, one A row per TMEM lane. Run by the 128 threads of warps 4..7 (lane quarter =
+// warp % 4), once per launch; the MMA issuers wait for `alo_full`.
+__device__ __forceinline__ void cl_load_alo(const ClSmem& S, uint32_t tmem_alo, const uint16_t* alo, int ld,
+                                            int rows, int row0, int kb_lo, int nkb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, r = q * 32 + lane;
+  const bool ok = row0 + r < rows;
+  const uint4* src = reinterpret_cast<const uint4*>(alo + (size_t)(ok ? row0 + r : 0) * ld + (size_t)kb_lo * 64);
+  const uint32_t taddr = tmem_alo + (uint32_t(q * 32) << 16);
+  for (int c = 0; c < nkb * 32; c += 8) {
+    uint32_t v[8];
+    const uint4 a = ok ? src[c / 4] : make_uint4(0, 0, 0, 0);
+    const uint4 b = ok ? src[c / 4 + 1] : make_uint4(0, 0, 0, 0);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    tmem_st_32x32b_x8(taddr + c, v);
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  mbar_arrive(S.alo_full);
+}
+
 // k-blocks travel in pairs (one 2 x N x 128-byte copy into two adjacent stages, completion on
 // the even stage's barrier) when the ring and the step's k-block count are even: >= 16 KB bulk
 // copies ingest ~62 B/cycle per SM vs ~50 for 8 KB ones (profiles/ubench/mma_ubench.cu).
@@ -308,10 +347,14 @@ __device__ __forceinline__ bool cl_pair_kb(const ClParams& p, int nkb) {
 // blocks picks the issuing lane (sm100_ptx.cuh umma_bf16_warp). Issuer j multiplies its half of
 // the step's k-blocks into accumulator `acc` (= its own TMEM columns).
 __device__ __forceinline__ int cl_half0(int nkb) { return (nkb + 1) >> 1; }
+// fp16x2: per K = 16 step A_hi.B_hi, A_hi.B_lo (B_lo = the stage's second N rows) and
+// A_lo.B_hi with A_lo read from tensor memory at `tmem_alo` (k-block k at column k * 32).
+template <class P>
 __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, int it, uint32_t acc, int nkb,
-                                            uint32_t idesc, uint32_t& pc, int stages, int N, int j) {
+                                            uint32_t idesc, uint32_t& pc, int stages, int N, int j,
+                                            uint32_t tmem_alo) {
   const bool pairs = cl_pair_kb(p, nkb);
-  const int a_bytes = kTileM * kRowBytes, b_bytes = N * kRowBytes;
+  const int a_bytes = kTileM * kRowBytes, b_bytes = P::kPlanes * N * kRowBytes;
   const bool l0 = (threadIdx.x & 31) == 0;
   const uint64_t a0 = sdesc_sw128(smem_u32(S.a), 16, 1024), b0 = sdesc_sw128(smem_u32(S.b), 16, 1024);
   // interleaved: issuer j takes k-blocks j, j + 2, ... so both start on the first arrivals
@@ -325,8 +368,14 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
     if (l0 && k == nkb - 1) cl_trace(p, it, 7);
     const uint64_t ad = desc_add(a0, k * a_bytes), bd = desc_add(b0, s * b_bytes);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)  // 4 x K=16 per 64-element k-block (32 bytes along K)
-      umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, kk * 32), idesc, (k != k_lo || kk) ? 1u : 0u);
+    for (int kk = 0; kk < 4; ++kk) {  // 4 x K=16 per 64-element k-block (32 bytes along K)
+      const uint32_t acc_on = (k != k_lo || kk) ? 1u : 0u;
+      umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, kk * 32), idesc, acc_on);
+      if constexpr (P::kPlanes == 2) {
+        umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, N * kRowBytes + kk * 32), idesc, 1u);
+        umma_ts_f16_warp(acc, tmem_alo + k * 32 + kk * 8, desc_add(bd, kk * 32), idesc, 1u);
+      }
+    }
     umma_commit_warp(&S.empty[s]);
   }
   pc += nkb;
@@ -335,6 +384,7 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
 // Producer (one thread): stream the k-blocks [kb_lo, kb_hi) of one step's B operand through the
 // stage ring. `blk` is the operand's pre-swizzled step block (sw_off layout); k-block kb sits at
 // (kb - kofs) * N * 128 bytes, already in the SWIZZLE_128B smem image: one 1-D bulk copy each.
+// (fp16x2: N is the stage's row count, 2 Bp -- both planes of a k-block are adjacent in the image)
 __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, int kb_lo, int kb_hi, int kofs,
                                           uint32_t& pc, int stages, int N, bool pairs = false) {
   const int b_bytes = N * kRowBytes;
@@ -360,7 +410,9 @@ __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, i
 // members, wait for theirs, and return this thread's owned columns summed in member order.
 // Thread (quarter q, lane) owns accumulator row q*32+lane; `half` picks its half of the owned
 // columns. v_out[i*8 + j] = owned column half*nco/2 + i*8 + j.
-template <int kChunks>
+// fp16x2: the weight planes carry 2^kWScaleLog2 (common.cuh); the reduced sums are scaled back
+// here (exact), so everything downstream sees plain products.
+template <class P, int kChunks>
 __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, bool two, int N, int it, int m,
                                           int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8],
                                           const ClParams* tp = nullptr) {
@@ -446,6 +498,11 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
       for (int j = 0; j < 8; ++j) v_out[i * 8 + j] = acc[j];
     }
   }
+  if constexpr (P::kPlanes == 2) {
+    constexpr float kUnscale = 1.0f / (float)(1 << kWScaleLog2);
+#pragma unroll
+    for (int i = 0; i < kChunks * 8; ++i) v_out[i] *= kUnscale;
+  }
 }
 
 // After every epilogue thread of the owner read the receive slots (named barrier): re-arm for
@@ -469,14 +526,14 @@ __device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, in
 
 // Off cluster epilogue of one step: reduce, then store the owned columns of the reduced partial
 // into ring slot it % kRing ([Bp][128] fp32) and publish it.
-template <int kChunks>
+template <class P, int kChunks>
 __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, bool two, int it,
                                             int m, int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
                                             const uint32_t* consumed, bool sys, uint32_t epoch) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<kChunks>(S, tacc, true, two, p.Bp, it, m, n_act, nco, rxc, v);
+  cl_reduce<P, kChunks>(S, tacc, true, two, p.Bp, it, m, n_act, nco, rxc, v);
   named_bar_sync(1, kEpiThreads);
   if (et == 0) {
     cl_rx_next(S, m, n_act, nco);
@@ -496,7 +553,7 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
   if (et == 0) red_release_s(done + it, 1, sys);
 }
 
-template <int kChunks>
+template <class P, int kChunks>
 __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, bool two,
                                             int n_it, int m, int n_act, float* ring, uint32_t* done,
                                             const uint32_t* consumed, bool sys, uint32_t epoch) {
@@ -507,8 +564,8 @@ __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, 
     mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
-    cl_off_step<kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed, sys,
-                         epoch);
+    cl_off_step<P, kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed,
+                            sys, epoch);
     if (et == 0) cl_trace(p, it, 3);
   }
 }
@@ -529,13 +586,13 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // ====================================================================== forward
 // grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
-template <int kChunks>
+template <class P, int kChunks>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
                                            int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v);
+  cl_reduce<P, kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 9);
   mbar_wait(S.off_full, offc & 1);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 10);
@@ -552,7 +609,7 @@ __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool 
 
 // kCC: the critical members' owned columns / 16 (Bp / kc / 16), one instantiation each so the
 // register allocation of one variant does not spill another's hot loop
-template <int kCC>
+template <class P, int kCC>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_fwd(const FwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -601,12 +658,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const ClSmem S = cl_carve(smem, p);
+  const ClSmem S = cl_carve<P>(smem, p);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // 2 steps x 2 issuers of N accumulator columns (+ fp16x2: A_lo, 32 columns per k-block)
+  const uint32_t tmem_need = 4 * N + (P::kPlanes == 2 ? nkb * 32 : 0);
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
+  while (tmem_cols < tmem_need) tmem_cols <<= 1;
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
+  const uint32_t tmem_alo = tmem_base + 4 * N;
   const int row0 = tile * kTileM;
+  const int BR = P::kPlanes * N;  // operand rows per k-block (both fp16x2 planes)
   float* ring = crit ? Cr.ring : Og.ring;
   uint32_t* done = crit ? Cr.done : Og.done;
   uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
@@ -624,28 +685,30 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     uint32_t pc = 0, offc = 0;
     for (int t = 0; t < p.T; ++t) {
       cl_trace(p, t, 0);
+      // (fp16x2 step blocks hold both planes: BR rows per k-block)
       if (crit) {
         // the off partial is usually published already: fetch it before waiting for h_{t-1}
-        const bool early = ld_relaxed_s(done + t, sys) >= done_target;
+        const bool early = flag_reached(ld_relaxed_s(done + t, sys), done_target);
         if (early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
         if (t > 0) wait_flag(&Ly.flags[t - 1], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N, cl_pair_kb(p, nkb));
+        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR, cl_pair_kb(p, nkb));
         if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
       } else {
         if (Og.op_flags) wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N,
+        cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, p.stages, BR,
                   cl_pair_kb(p, nkb));
       }
     }
   } else if (active && (warp == 1 || warp == 3)) {
     // ================= MMA issuers (whole warps, elected lane issues); j = half of the k-blocks
     const int j = warp == 3 ? 1 : 0;
-    const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
+    const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     mbar_wait(S.a_full, 0);
+    if constexpr (P::kPlanes == 2) mbar_wait(S.alo_full, 0);
     tc_fence_after();
     uint32_t pc = 0;
     for (int t = 0; t < p.T; ++t) {
@@ -654,17 +717,22 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_empty[ab], ((t >> 1) - 1) & 1);
         tc_fence_after();
       }
-      cl_mma_step(S, p, t, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j);
+      cl_mma_step<P>(S, p, t, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j, tmem_alo);
       umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
     const int et = threadIdx.x - kEpiBase;
+    if constexpr (P::kPlanes == 2) {
+      if (warp < 8)
+        cl_load_alo(S, tmem_alo, crit ? Ly.alo : Og.alo, crit ? Ly.alo_ld : Og.alo_ld, crit ? Ly.alo_rows : Og.alo_rows,
+                    row0, kb_lo, nkb);
+    }
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        default: cl_off_loop<1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        default: cl_off_loop<P, 1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
       }
     } else {
       // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
@@ -685,7 +753,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       // next step's loads, which wait for this CTA's own publish
       const uint32_t hstg = smem_u32(S.b + (size_t)N * kTileM * 4);
       // opt-in (RW_CL_DEBUG bit 16): measured at B forward 0.596 ms staged vs 0.589 scattered
-      const bool staged = (p.debug & 16) && (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
+      const bool staged = P::kPlanes == 1 && (p.debug & 16) &&
+                          (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
       uint32_t rxc = 0;
       if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
       for (int t = 0; t < p.T; ++t) {
@@ -693,7 +762,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
         const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
-        cl_fwd_sum<kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p);
+        cl_fwd_sum<P, kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p);
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
@@ -704,7 +773,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         float hv[kClMaxN / 8], cv[kClMaxN / 8], iv[kClMaxN / 8], fv[kClMaxN / 8], ov[kClMaxN / 8],
             cb[kClMaxN / 8], tcv[kClMaxN / 8];
         const long long colp = (long long)t * N + own0;  // block t (c_{t-1}), owned base
-        uint8_t* hblk = Le.hsw + (size_t)(t + 1) * p.Hp * N * 2;  // h_t: block t+1
+        uint8_t* hblk = Le.hsw + (size_t)(t + 1) * p.Hp * BR * 2;  // h_t: block t+1
 #pragma unroll
         for (int k = 0; k < kClMaxN / 8; ++k) {
           const int cl = cg + 8 * k;
@@ -713,20 +782,26 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const float af = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
           const float ao = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j) + bo;
           const float ac = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j) + bc;
-          iv[k] = act_sigmoid<PrecBF16>(ai);
-          fv[k] = act_sigmoid<PrecBF16>(af);
-          ov[k] = act_sigmoid<PrecBF16>(ao);
-          cb[k] = act_tanh<PrecBF16>(ac);
+          iv[k] = act_sigmoid<P>(ai);
+          fv[k] = act_sigmoid<P>(af);
+          ov[k] = act_sigmoid<P>(ao);
+          cb[k] = act_tanh<P>(ac);
           const float t1 = fv[k] * creg[k];
           const float t2 = iv[k] * cb[k];
           cv[k] = t1 + t2;
-          tcv[k] = act_tanh<PrecBF16>(cv[k]);
+          tcv[k] = act_tanh<P>(cv[k]);
           hv[k] = ov[k] * tcv[k];
           creg[k] = cv[k];
-          if (staged)
+          if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block
+            __half hh, hl;
+            f16x2_split(hv[k], hh, hl);
+            *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
+            *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
+          } else if (staged) {
             sts_bf16(hstg + (cl * 32 + j) * 2, hv[k]);
-          else
+          } else {
             *reinterpret_cast<__nv_bfloat16*>(hblk + sw_off(u, own0 + cl, N)) = __float2bfloat16_rn(hv[k]);
+          }
         }
         if (staged) {
           // the CTA's 32 units x nco columns as 16-byte chunks of the swizzled operand image:
@@ -755,7 +830,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const long long col_prev = colp + cl, col_new = col_prev + N;
           Le.c[col_new * Hp + u] = cv[k];
           Le.h[col_new * Hp + u] = hv[k];
-          static_cast<__nv_bfloat16*>(Le.hop[0])[col_new * Hp + u] = __float2bfloat16_rn(hv[k]);
+          store_operand<P>(Le.hop, col_new * Hp + u, hv[k]);
           if (Le.gates) {
             float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv[k];
@@ -777,13 +852,14 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 // R^T.dG_{l,t+1}, 1 off W_{l+1}^T.dG_{l+1,t}; the top layer has no off cluster and adds dy).
 // Critical steps t = T-1 .. -1 (t = -1: dh0 = R^T dG_{l,0}, dc0 = carry; engine.hpp:163-170),
 // off steps t = T-1 .. 0. Iteration it <-> t = T-1-it.
-template <int kChunks>
+template <class P, int kChunks>
 __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
                                             uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed,
                                             bool sys, uint32_t flag_target) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const int N = p.Bp, kc = p.kc, nco = N / kc;
+  const int BR = P::kPlanes * N;  // operand rows per k-block (both fp16x2 planes)
   const int u = tile * kTileM + row;
   const bool uok = u < p.Hp;
   const long long Hp = p.Hp, G4 = 4 * Hp;
@@ -797,7 +873,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   // wait for this CTA's own publish): the tile's 8 k-blocks x nco rows of the swizzled image
   const uint32_t dstg = smem_u32(S.b);
   // (measured at B: backward 0.880 ms staged vs 0.903 scattered; RW_CL_DEBUG bit 32 = scattered)
-  const bool staged = !(p.debug & 40) && (size_t)p.stages * N * kRowBytes >= (size_t)8 * nco * 128;
+  const bool staged = !(p.debug & 40) && (size_t)p.stages * BR * kRowBytes >= (size_t)8 * P::kPlanes * nco * 128;
   if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
   for (int it = 0; it <= p.T; ++it) {
     const int t = p.T - 1 - it;
@@ -839,7 +915,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     float acc[kChunks * 8];
-    cl_reduce<kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, &p);
+    cl_reduce<P, kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, &p);
     if (et == 0) cl_trace(p, it, 12);
     float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
@@ -891,33 +967,53 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         g_c[k] = d1 * d3;
         carry[k] = dc * pf[j];
         if (staged) {
-          // K offset within the tile's 8 k-blocks: rho_of(g, u) - 4 * tile * 128
+          // K offset within the tile's 8 k-blocks: rho_of(g, u) - 4 * tile * 128; staging rows
+          // (k-block, plane, owned column) -- fp16x2 keeps each k-block's hi and lo runs adjacent
           const int n = cbase + k, nl = n - m * nco;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const int kk = q * 128 + g * 32 + lane;
-            sts_bf16(dstg + ((kk >> 6) * nco + nl) * 128 + ((((kk >> 3) & 7) ^ (n & 7)) << 4) + (kk & 7) * 2,
-                     g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k]);
+            const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+            const uint32_t so = ((((kk >> 3) & 7) ^ (n & 7)) << 4) + (kk & 7) * 2;
+            if constexpr (P::kPlanes == 2) {
+              __half hh, hl;
+              f16x2_split(gv, hh, hl);
+              const uint32_t r0 = ((kk >> 6) * 2) * nco + nl;
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + r0 * 128 + so), "h"(__half_as_ushort(hh)));
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + (r0 + nco) * 128 + so), "h"(__half_as_ushort(hl)));
+            } else {
+              sts_bf16(dstg + ((kk >> 6) * nco + nl) * 128 + so, gv);
+            }
           }
         } else if (uok && !(p.debug & 8)) {
-          uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
+          uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
           const int n = cbase + k;
-          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(0, u), n, N)) = __float2bfloat16_rn(g_i[k]);
-          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(1, u), n, N)) = __float2bfloat16_rn(g_f[k]);
-          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(2, u), n, N)) = __float2bfloat16_rn(g_o[k]);
-          *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(3, u), n, N)) = __float2bfloat16_rn(g_c[k]);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+            if constexpr (P::kPlanes == 2) {
+              __half hh, hl;
+              f16x2_split(gv, hh, hl);
+              *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), n, BR)) = hh;
+              *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), N + n, BR)) = hl;
+            } else {
+              *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(g, u), n, N)) = __float2bfloat16_rn(gv);
+            }
+          }
         }
       }
     }
     if (staged) {
-      // 8 k-blocks x nco rows x 128 B, each k-block's rows one contiguous run of the operand
+      // 8 k-blocks x (planes x) nco rows x 128 B, each (k-block, plane)'s rows one contiguous
+      // run of the operand image (fp16x2: hi rows at m*nco, lo rows at N + m*nco of the k-block)
       named_bar_sync(1, kEpiThreads);
-      uint8_t* blk = Ly.dgsw + (size_t)t * G4 * N * 2;
+      uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
       const int kb0 = tile * 8, nkb = min(8, (int)(G4 / 64) - kb0), per = nco * 8;
-      for (int i = et; i < nkb * per; i += kEpiThreads) {
-        const int kb = i / per, r = i - kb * per;
+      for (int i = et; i < nkb * P::kPlanes * per; i += kEpiThreads) {
+        const int kp = i / per, r = i - kp * per;  // kp = k-block * planes + plane
+        const int kb = kp / P::kPlanes, pl = kp - kb * P::kPlanes;
         const uint4 v = lds_v4(dstg + i * 16);
-        *reinterpret_cast<uint4*>(blk + ((size_t)(kb0 + kb) * N + m * nco) * 128 + (size_t)r * 16) = v;
+        *reinterpret_cast<uint4*>(blk + ((size_t)(kb0 + kb) * BR + pl * N + m * nco) * 128 + (size_t)r * 16) = v;
       }
     }
     if (et == 0) cl_trace(p, it, 3);
@@ -933,11 +1029,10 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 #pragma unroll
       for (int k = 0; k < kChunks * 8; ++k) {
         const long long ob = ((long long)t * N + cbase + k) * G4;
-        __nv_bfloat16* op = static_cast<__nv_bfloat16*>(Ly.dgop[0]);
-        op[ob + rho_of(0, u)] = __float2bfloat16_rn(g_i[k]);
-        op[ob + rho_of(1, u)] = __float2bfloat16_rn(g_f[k]);
-        op[ob + rho_of(2, u)] = __float2bfloat16_rn(g_o[k]);
-        op[ob + rho_of(3, u)] = __float2bfloat16_rn(g_c[k]);
+        store_operand<P>(Ly.dgop, ob + rho_of(0, u), g_i[k]);
+        store_operand<P>(Ly.dgop, ob + rho_of(1, u), g_f[k]);
+        store_operand<P>(Ly.dgop, ob + rho_of(2, u), g_o[k]);
+        store_operand<P>(Ly.dgop, ob + rho_of(3, u), g_c[k]);
         float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
         dgp[0] = g_i[k];
         dgp[Hp] = g_f[k];
@@ -960,7 +1055,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   }
 }
 
-template <int kCC>
+template <class P, int kCC>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_bwd(const BwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -1010,12 +1105,15 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const ClSmem S = cl_carve(smem, p);
+  const ClSmem S = cl_carve<P>(smem, p);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tmem_need = 4 * N + (P::kPlanes == 2 ? nkb * 32 : 0);  // as k_cl_fwd
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(4 * N)) tmem_cols <<= 1;  // 2 steps x 2 issuers
+  while (tmem_cols < tmem_need) tmem_cols <<= 1;
   const uint32_t tmem_base = cl_setup(S, p, tmem_cols, n_act);
+  const uint32_t tmem_alo = tmem_base + 4 * N;
   const int row0 = tile * kTileM;
+  const int BR = P::kPlanes * N;
   float* ring = crit ? Cr.ring : Og.ring;
   uint32_t* done = crit ? Cr.done : Og.done;
   uint32_t* consumed = crit ? Cr.consumed : const_cast<uint32_t*>(Og.consumed);
@@ -1035,7 +1133,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const bool off = crit && ko > 0 && t >= 0;
       const bool load = !crit || t <= p.T - 2;
       cl_trace(p, it, 0);
-      const bool early = off && ld_relaxed_s(done + it, sys) >= done_target;
+      const bool early = off && flag_reached(ld_relaxed_s(done + it, sys), done_target);
       if (early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
       if (load) {
         if (crit)
@@ -1045,18 +1143,19 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         fence_proxy_async_global();
         cl_trace(p, it, 1);
         if (crit)
-          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * N * 2, kb_lo, kb_hi, kofs, pc, p.stages, N,
+          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR,
                     cl_pair_kb(p, nkb));
         else
-          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * N * 2, kb_lo, kb_hi, 0, pc, p.stages, N,
-                  cl_pair_kb(p, nkb));
+          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, p.stages, BR,
+                    cl_pair_kb(p, nkb));
       }
       if (off && !early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
     }
   } else if (active && (warp == 1 || warp == 3)) {
     const int j = warp == 3 ? 1 : 0;
-    const uint32_t idesc = idesc_make(PrecBF16::kFmt, false, false, kTileM, N);
+    const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     mbar_wait(S.a_full, 0);
+    if constexpr (P::kPlanes == 2) mbar_wait(S.alo_full, 0);
     tc_fence_after();
     uint32_t pc = 0;
     for (int it = 0; it < n_it; ++it) {
@@ -1066,19 +1165,25 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_empty[ab], ((it >> 1) - 1) & 1);
         tc_fence_after();
       }
-      if (!crit || t <= p.T - 2) cl_mma_step(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j);
+      if (!crit || t <= p.T - 2)
+        cl_mma_step<P>(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j, tmem_alo);
       umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
+    if constexpr (P::kPlanes == 2) {
+      if (warp < 8)
+        cl_load_alo(S, tmem_alo, crit ? Ly.alo : Og.alo, crit ? Ly.alo_ld : Og.alo_ld, crit ? Ly.alo_rows : Og.alo_rows,
+                    row0, kb_lo, nkb);
+    }
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 3: cl_off_loop<3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 2: cl_off_loop<2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        default: cl_off_loop<1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        default: cl_off_loop<P, 1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
       }
     } else {
-      cl_bwd_crit<kCC>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
+      cl_bwd_crit<P, kCC>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
     }
   }
   cl_teardown(tmem_base, tmem_cols);

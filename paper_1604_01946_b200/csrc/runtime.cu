@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/rnnwave_sm100.h"
@@ -73,14 +74,15 @@ inline int gemm_box_rows(int rows) { return rows < 128 ? rows : 128; }
 
 CUtensorMap make_map(const void* base, int prec, long long inner, long long outer, int bi, int bo) {
   CUtensorMap m;
-  const int elem = prec == kBF16 ? 2 : 4;
+  const int elem = prec_elem(prec);
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)(inner * elem)};
   cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m,
-                           prec == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           prec == kBF16    ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                           : prec == kF16x2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            2, const_cast<void*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -117,12 +119,12 @@ struct DevBuf {
   float* f() const { return static_cast<float*>(p); }
 };
 
-// An operand tensor: 1 (bf16) or 2 (tf32 hi/lo) planes of `elems` elements.
+// An operand tensor: 1 (bf16) or 2 (tf32 / fp16 hi, lo) planes of `elems` elements.
 struct Operand {
   DevBuf plane[2];
   void alloc(int prec, size_t elems) {
-    const int planes = prec == kBF16 ? 1 : 2;
-    const size_t eb = prec == kBF16 ? 2 : 4;
+    const int planes = prec_planes(prec);
+    const size_t eb = prec_elem(prec);
     for (int i = 0; i < 2; ++i) plane[i].alloc(i < planes ? elems * eb : 0);
   }
   void* p(int i) const { return plane[i].p; }
@@ -189,6 +191,17 @@ struct KernelSet {
   static void* fwd() { return (void*)k_lstm_fwd<P>; }
   static void* bwd() { return (void*)k_lstm_bwd<P>; }
 };
+
+// Calls f(PrecX{}) for the context's operand format.
+template <class F>
+void by_prec(int prec, F&& f) {
+  if (prec == kBF16)
+    f(PrecBF16{});
+  else if (prec == kF16x2)
+    f(PrecF16x2{});
+  else
+    f(PrecTF32x3{});
+}
 
 }  // namespace
 
@@ -407,19 +420,27 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
 // cluster (ko_l members per layer), each member holding <= 512 K of its weight slice. Returns
 // false when the shape does not fit (batch > 64, owned columns not a multiple of 16, too many
 // CTAs, shared memory, or clusters not co-resident).
-void* cl_kernel(bool fwd, int nco) {
+template <class P>
+void* cl_kernel_p(bool fwd, int nco) {
   switch (nco >> 4) {
-    case 4: return fwd ? (void*)k_cl_fwd<4> : (void*)k_cl_bwd<4>;
-    case 3: return fwd ? (void*)k_cl_fwd<3> : (void*)k_cl_bwd<3>;
-    case 2: return fwd ? (void*)k_cl_fwd<2> : (void*)k_cl_bwd<2>;
-    default: return fwd ? (void*)k_cl_fwd<1> : (void*)k_cl_bwd<1>;
+    case 4: return fwd ? (void*)k_cl_fwd<P, 4> : (void*)k_cl_bwd<P, 4>;
+    case 3: return fwd ? (void*)k_cl_fwd<P, 3> : (void*)k_cl_bwd<P, 3>;
+    case 2: return fwd ? (void*)k_cl_fwd<P, 2> : (void*)k_cl_bwd<P, 2>;
+    default: return fwd ? (void*)k_cl_fwd<P, 1> : (void*)k_cl_bwd<P, 1>;
   }
 }
+void* cl_kernel(int prec, bool fwd, int nco) {
+  return prec == kF16x2 ? cl_kernel_p<PrecF16x2>(fwd, nco) : cl_kernel_p<PrecBF16>(fwd, nco);
+}
 
-bool plan_cluster(bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
+// prec: kBF16 or kF16x2 (two operand planes per stage; A_lo in tensor memory next to the
+// 4 x Bp accumulator columns, which fits 512 columns for Bp <= 64 and <= 8 k-blocks per member)
+bool plan_cluster(int prec, bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
                   ClPlan& out) {
   if (Bp > kClMaxN || Bp % kc || (Bp / kc) % 16) return false;
-  void* kernel = cl_kernel(fwd, Bp / kc);
+  if (prec == kF16x2 && 4 * Bp + kClKBlocks * 32 > 512) return false;
+  const int rows = prec_planes(prec) * Bp;  // operand rows per stage
+  void* kernel = cl_kernel(prec, fwd, Bp / kc);
   int cs = kc, komin = kc;
   for (int k : ko) {
     if (k == 0) continue;
@@ -431,12 +452,12 @@ bool plan_cluster(bool fwd, int kc, const std::vector<int>& ko, int tiles, int L
   const int ncomax = Bp / komin;
   const int min_stages = fwd ? 4 : 2;  // forward critical: the sum buffer aliases the B stages
   int stages = kClKBlocks;
-  size_t smem = cl_smem_bytes(cs, ncomax, Bp, stages);
-  while (smem > (size_t)kSmemLimit && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, Bp, --stages);
+  size_t smem = cl_smem_bytes(cs, ncomax, rows, stages);
+  while (smem > (size_t)kSmemLimit && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, rows, --stages);
   if (smem > (size_t)kSmemLimit) return false;
   // an even ring lets operand k-blocks travel in pairs (rec_cluster.cuh cl_pair_kb)
-  if (stages % 2 && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, Bp, --stages);
-  if (fwd && (size_t)stages * Bp * kRowBytes < (size_t)(Bp / kc) * kTileM * 4) return false;
+  if (stages % 2 && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, rows, --stages);
+  if (fwd && (size_t)stages * rows * kRowBytes < (size_t)(Bp / kc) * kTileM * 4) return false;
   smem = std::max(smem, (size_t)116 * 1024);  // one CTA per SM
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
@@ -462,9 +483,12 @@ size_t gemm_smem(int planes, int bn, int stages) {
   return 1024 + (size_t)stages * planes * (kTileM + bn) * kRowBytes + (2 * stages + 4) * 8 + 16;
 }
 
-// fp32-parity GEMMs accumulate in chunks of kPromoteKB k-blocks (= 256 K elements for tf32)
+// fp32-parity GEMMs accumulate in chunks of kPromoteKB k-blocks (3xTF32: 2 x 32 = 64 K elements;
+// fp16x2: kPromoteKB16 x 64 = 512, measured 6.4e-7 normwise for one 512-long chain,
+// profiles/ubench/f16x2_ts_check.cu)
 // drained into fp32 registers; bf16 runs the whole K in TMEM.
 constexpr int kPromoteKB = 2;
+constexpr int kPromoteKB16 = 8;
 
 // bf16 grouped GEMMs go to the persistent kernel (gemm_tc.cuh k_gemm_p) unless RW_GEMM_OLD=1;
 // fp32-parity (3xTF32, chunked fp32 promotion) keeps the one-tile-per-CTA kernel.
@@ -550,7 +574,7 @@ void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int
   if (P::kPlanes == 2 && bn == 64) {
     auto k = k_gemm_tc<P, AMN, BMN, 64>;
     RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, kPromoteKB);
+    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, P::kTF32 ? kPromoteKB : kPromoteKB16);
   } else {
     auto k = k_gemm_tc<P, AMN, BMN, 0>;
     RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -593,10 +617,6 @@ int add_map(rw_ctx* x, const CUtensorMap& m) {
 
 void build(rw_ctx* x) {
   const rw_config& c = x->cfg;
-  x->prec = c.precision == RW_PREC_BF16 ? kBF16 : kTF32x3;
-  x->planes = x->prec == kBF16 ? 1 : 2;
-  x->elem = x->prec == kBF16 ? 2 : 4;
-  x->atomK = x->prec == kBF16 ? 64 : 32;
   x->L = c.layers;
   x->H = c.hidden;
   x->I = c.input;
@@ -613,6 +633,45 @@ void build(rw_ctx* x) {
   RW_CUDA(cudaSetDevice(x->dev));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->dev);
+
+  // ---- cluster schedule first: forward kc = K-slices of R.h, ko = of W.x; backward kc =
+  // K-slices of R^T.dG, ko = of W_{l+1}^T.dG (none for a single layer). It also decides the
+  // operand format of the fp32-parity mode: fp16x2 when both directions fit the cluster path
+  // (rec_cluster.cuh), else 3xTF32 on the persistent / stepwise kernels (RW_FP32_TF32=1 forces
+  // the latter).
+  ClPlan cpf, cpb;
+  bool cl_f = false, cl_b = false;
+  auto try_cluster = [&](int prec) {
+    const int kc_f = ceil_div(Hp / 64, kClKBlocks);
+    std::vector<int> ko_f(L), ko_b(L);
+    for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
+    cl_f = plan_cluster(prec, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
+    // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
+    // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
+    const int nkb_r = 4 * Hp / 64;
+    int kc_b = ceil_div(nkb_r, kClKBlocks);
+    while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
+    for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
+    cl_b = plan_cluster(prec, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
+  };
+  const bool want_cl = c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER;
+  if (c.precision == RW_PREC_BF16) {
+    x->prec = kBF16;
+    if (want_cl) try_cluster(kBF16);
+  } else {
+    x->prec = kTF32x3;
+    const bool force_tf32 = getenv("RW_FP32_TF32") && atoi(getenv("RW_FP32_TF32")) != 0;
+    if (want_cl && !force_tf32) {
+      try_cluster(kF16x2);
+      if (cl_f && cl_b)
+        x->prec = kF16x2;
+      else
+        cl_f = cl_b = false;
+    }
+  }
+  x->planes = prec_planes(x->prec);
+  x->elem = prec_elem(x->prec);
+  x->atomK = prec_atomk(x->prec);
 
   x->W.resize(L);
   x->R.resize(L);
@@ -658,7 +717,7 @@ void build(rw_ctx* x) {
     x->db[l].alloc(4ULL * H * 4);
   }
   x->w0t.alloc(x->prec, (size_t)Ip * G4p);
-  const bool kmajor_wg = x->prec != kBF16;
+  const bool kmajor_wg = x->prec == kTF32x3;
   if (kmajor_wg) {
     x->dgT.resize(L);
     x->hT.resize(L);
@@ -678,30 +737,14 @@ void build(rw_ctx* x) {
   x->errflag.alloc(16);
 
   // ---- schedules
+  const bool f16x2 = x->prec == kF16x2;  // cluster kernels only (no persistent / stepwise variant)
   void* kf = x->prec == kBF16 ? KernelSet<PrecBF16>::fwd() : KernelSet<PrecTF32x3>::fwd();
   void* kb = x->prec == kBF16 ? KernelSet<PrecBF16>::bwd() : KernelSet<PrecTF32x3>::bwd();
   const int kbf_max = (std::max(Ip, Hp) + Hp) / x->atomK;
   const int kbb_max = (int)((L > 1 ? 2 : 1) * G4p / x->atomK);
   const int tiles_f = Hp / kUnitsPerFwdTile, tiles_b = ceil_div(Hp, kTileM);
-  // cluster schedule first (bf16): forward kc = K-slices of R.h, ko = of W.x; backward kc =
-  // K-slices of R^T.dG, ko = of W_{l+1}^T.dG (none for a single layer)
-  ClPlan cpf, cpb;
-  bool cl_f = false, cl_b = false;
-  if (x->prec == kBF16 && (c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER)) {
-    const int kc_f = ceil_div(Hp / 64, kClKBlocks);
-    std::vector<int> ko_f(L), ko_b(L);
-    for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
-    cl_f = plan_cluster(true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
-    // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
-    // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
-    const int nkb_r = 4 * Hp / 64;
-    int kc_b = ceil_div(nkb_r, kClKBlocks);
-    while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
-    for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
-    cl_b = plan_cluster(false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
-  }
   if (c.schedule == RW_SCHED_CLUSTER && !(cl_f && cl_b))
-    einval("cluster schedule does not fit this configuration (bf16, batch <= 64, owned columns multiple of 16, "
+    einval("cluster schedule does not fit this configuration (batch <= 64, owned columns multiple of 16, "
            "CTAs and clusters co-resident)");
   int want = c.schedule == RW_SCHED_CLUSTER ? RW_SCHED_AUTO : c.schedule;
   bool ls = c.schedule == RW_SCHED_LAYERSEQ;
@@ -712,10 +755,13 @@ void build(rw_ctx* x) {
     want = RW_SCHED_STEPWISE;
     cl_f = cl_b = false;
   }
-  RecPlan pf = plan_recurrent(kf, want, x->planes, ls ? Hp / x->atomK : kbf_max, tiles_f, ls ? 1 : L, Bp, sms,
-                              "RW_FWD_KSPLIT");
-  RecPlan pb = plan_recurrent(kb, want, x->planes, ls ? (int)(G4p / x->atomK) : kbb_max, tiles_b, ls ? 1 : L, Bp,
-                              sms, "RW_BWD_KSPLIT");
+  RecPlan pf{RW_SCHED_CLUSTER, 1, 0, 4, 0, 0}, pb{RW_SCHED_CLUSTER, 1, 0, 4, 0, 0};
+  if (!f16x2) {
+    pf = plan_recurrent(kf, want, x->planes, ls ? Hp / x->atomK : kbf_max, tiles_f, ls ? 1 : L, Bp, sms,
+                        "RW_FWD_KSPLIT");
+    pb = plan_recurrent(kb, want, x->planes, ls ? (int)(G4p / x->atomK) : kbb_max, tiles_b, ls ? 1 : L, Bp, sms,
+                        "RW_BWD_KSPLIT");
+  }
   if (ls) {
     // persistent per-layer launches need every (tile, rank) CTA of a layer co-resident
     const int cf = tiles_f * pf.ks, cb = tiles_b * pb.ks;
@@ -796,14 +842,14 @@ void build(rw_ctx* x) {
     x->cl_done.alloc(2 * lt * T * 4);
     x->cl_consumed.alloc(2 * lt * 32 * 4);
   }
-  if (cl_f) {
+  if (cl_f) {  // pre-swizzled 16-bit operand images (fp16x2: both planes per k-block)
     x->hsw.resize(L);
-    for (int l = 0; l < L; ++l) x->hsw[l].alloc((size_t)Hp * colsT1 * 2);
-    x->xsw.alloc((size_t)Ip * colsT * 2);
+    for (int l = 0; l < L; ++l) x->hsw[l].alloc((size_t)Hp * colsT1 * 2 * x->planes);
+    x->xsw.alloc((size_t)Ip * colsT * 2 * x->planes);
   }
   if (cl_b) {
     x->dgsw.resize(L);
-    for (int l = 0; l < L; ++l) x->dgsw[l].alloc((size_t)G4p * colsT * 2);
+    for (int l = 0; l < L; ++l) x->dgsw[l].alloc((size_t)G4p * colsT * 2 * x->planes);
   }
   // fp32-parity: accumulate every kAccKB k-blocks in a separate TMEM accumulator (<= 512 cols)
   auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc) {
@@ -895,6 +941,9 @@ void build(rw_ctx* x) {
     F.zx = ls ? x->gates[l].f() : nullptr;  // the input GEMM writes W.x into the gates tape
     F.bx2 = x->pair_f ? MD + (l == 0 ? m_xK2 : m_hopK2[l - 1]) : nullptr;
     F.bh2 = x->pair_f ? MD + m_hopK2[l] : nullptr;
+    F.alo = f16x2 ? static_cast<const uint16_t*>(x->wf[l].p(1)) : nullptr;
+    F.alo_ld = (l == 0 ? Ip : Hp) + Hp;
+    F.alo_rows = (int)G4p;
     if (!x->hsw.empty()) {
       F.hsw = static_cast<uint8_t*>(x->hsw[l].p);
       F.bxsw = l == 0 ? static_cast<const uint8_t*>(x->xsw.p) : static_cast<const uint8_t*>(x->hsw[l - 1].p);
@@ -907,6 +956,9 @@ void build(rw_ctx* x) {
       Bd.bg[p] = mp(m_dgK[2 * l + (p % x->planes)], p);
       Bd.bup2 = x->pair_b && l < L - 1 ? MD + m_dgK2[l + 1] : nullptr;
       Bd.bg2 = x->pair_b ? MD + m_dgK2[l] : nullptr;
+      Bd.alo = f16x2 ? static_cast<const uint16_t*>(x->wb[l].p(1)) : nullptr;
+      Bd.alo_ld = (int)((l < L - 1 ? 2 : 1) * G4p);
+      Bd.alo_rows = Hp;
       Bd.dgop[p] = x->dgop[l].p(p);
     }
     Bd.has_up = l < L - 1;
@@ -968,6 +1020,9 @@ void build(rw_ctx* x) {
         o.done = x->ring_f_h[l].done;
         o.consumed = x->ring_f_h[l].consumed;
         o.active = 1;
+        o.alo = fl[l].alo;
+        o.alo_ld = fl[l].alo_ld;
+        o.alo_rows = fl[l].alo_rows;
       }
       x->rows_f = L;
     }
@@ -988,6 +1043,9 @@ void build(rw_ctx* x) {
         o.done = x->ring_b_h[l].done;
         o.consumed = x->ring_b_h[l].consumed;
         o.active = 1;
+        o.alo = bl[l].alo;
+        o.alo_ld = bl[l].alo_ld;
+        o.alo_rows = bl[l].alo_rows;
       }
       x->rows_b = L;
     }
@@ -1105,6 +1163,7 @@ void build(rw_ctx* x) {
   dx.B = B;
   dx.Bp = Bp;
   dx.m_valid = I;
+  dx.alpha = f16x2 ? 1.0f / (float)(1 << kWScaleLog2) : 1.0f;  // W_0^T planes carry 2^kWScaleLog2
   dx.n_valid = (int)colsT;
   x->gemm_dx.alloc(sizeof(GemmDesc));
   RW_CUDA(cudaMemcpy(x->gemm_dx.p, &dx, sizeof(GemmDesc), cudaMemcpyHostToDevice));
@@ -1180,8 +1239,9 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   for (int l = 0; l < L; ++l) {
     const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
     ++g_launches;
-    k_pack_wf<<<grid_for(4LL * Hp * (Ipl + Hp)), 256, 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp, Ipl,
-                                                             x->prec, x->wf[l].p(0), x->wf[l].p(1));
+    k_pack_wf<<<dim3(ceil_div(Ipl + Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp,
+                                                                               Ipl, x->prec, x->wf[l].p(0),
+                                                                               x->wf[l].p(1));
     const float* wup = l < L - 1 ? x->W[l + 1].f() : nullptr;
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(wup, x->R[l].f(), H, Hp, x->prec,
@@ -1261,13 +1321,15 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   if (inputs && !fused_x && x->fwd_sched == RW_SCHED_CLUSTER && !x->pp_prev) {  // pre-swizzled images of x
     const long long colsT = (long long)Bp * x->T;
     ++g_launches;
-    k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT), 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(x->x_op.p(0)), x->Ip, Bp, 0, colsT, static_cast<uint8_t*>(x->xsw.p));
+    k_swizzle_op<<<grid_for((long long)x->Ip / 8 * colsT * x->planes), 256, 0, s>>>(
+        static_cast<const uint16_t*>(x->x_op.p(0)), static_cast<const uint16_t*>(x->x_op.p(1)), x->Ip, Bp, 0, colsT,
+        static_cast<uint8_t*>(x->xsw.p));
   }
   if (state && x->fwd_sched == RW_SCHED_CLUSTER) {
     for (int l = 0; l < L; ++l, ++g_launches)
-      k_swizzle_op<<<grid_for((long long)Hp / 8 * Bp), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x->hop[l].p(0)),
-                                                               Hp, Bp, 0, Bp, static_cast<uint8_t*>(x->hsw[l].p));
+      k_swizzle_op<<<grid_for((long long)Hp / 8 * Bp * x->planes), 256, 0, s>>>(
+          static_cast<const uint16_t*>(x->hop[l].p(0)), static_cast<const uint16_t*>(x->hop[l].p(1)), Hp, Bp, 0, Bp,
+          static_cast<uint8_t*>(x->hsw[l].p));
   }
   RW_CUDA(cudaGetLastError());
 }
@@ -1326,8 +1388,26 @@ void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams&
   RW_CUDA(cudaLaunchKernelExC(&lc, kernel, args));
 }
 
+void run_forward_cluster(rw_ctx* x, cudaStream_t s) {
+  launch_cluster(x, x->cl_f.kern, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
+  if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
+    RW_CUDA(cudaMemcpyAsync(x->pp_next_xop, static_cast<uint8_t*>(x->hop[x->L - 1].p(0)) + (size_t)x->Hp * x->Bp * 2,
+                            (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
+    ++g_launches;
+    k_pp_signal<<<1, 1, 0, s>>>(x->pp_next_ready, static_cast<const uint32_t*>(x->cl_epoch.p));
+    RW_CUDA(cudaGetLastError());
+  }
+}
+
 template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
+  if (x->fwd_sched == RW_SCHED_CLUSTER) {
+    run_forward_cluster(x, s);
+    return;
+  }
+  if constexpr (std::is_same_v<P, PrecF16x2>) {
+    throw RwError{RW_ECUDA, "internal: fp16x2 operands without the cluster schedule"};
+  } else {
   if (x->fwd_sched == RW_SCHED_LAYERSEQ) {
     RecParams rp = rec_params(x, true);
     void* kern = KernelSet<P>::fwd();
@@ -1347,17 +1427,6 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
         rp.t_first = t;
         launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, s);
       }
-    }
-    return;
-  }
-  if (x->fwd_sched == RW_SCHED_CLUSTER) {
-    launch_cluster(x, x->cl_f.kern, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
-    if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
-      RW_CUDA(cudaMemcpyAsync(x->pp_next_xop, static_cast<uint8_t*>(x->hop[x->L - 1].p(0)) + (size_t)x->Hp * x->Bp * 2,
-                              (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
-      ++g_launches;
-      k_pp_signal<<<1, 1, 0, s>>>(x->pp_next_ready, static_cast<const uint32_t*>(x->cl_epoch.p));
-      RW_CUDA(cudaGetLastError());
     }
     return;
   }
@@ -1393,13 +1462,21 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     }
   }
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
+  }  // P != PrecF16x2
 }
 
 template <class P>
 void run_backward_rec(rw_ctx* x, cudaStream_t s) {
+  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
+  if (x->bwd_sched == RW_SCHED_CLUSTER) {
+    launch_cluster(x, x->cl_b.kern, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
+    return;
+  }
+  if constexpr (std::is_same_v<P, PrecF16x2>) {
+    throw RwError{RW_ECUDA, "internal: fp16x2 operands without the cluster schedule"};
+  } else {
   RecParams rp = rec_params(x, false);
   void* kern = KernelSet<P>::bwd();
-  for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
   if (x->bwd_sched == RW_SCHED_LAYERSEQ) {
     const bool pers = x->ls_pers_b;  // as in the forward
     rp.persistent = pers ? 1 : 0;
@@ -1416,10 +1493,6 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
         launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_b, s);
       }
     }
-    return;
-  }
-  if (x->bwd_sched == RW_SCHED_CLUSTER) {
-    launch_cluster(x, x->cl_b.kern, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
     return;
   }
   if (x->bwd_sched == RW_SCHED_PERSISTENT) {
@@ -1450,6 +1523,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     }
   }
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
+  }  // P != PrecF16x2
 }
 
 template <class P>
@@ -1475,7 +1549,7 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
   }
   const GemmDesc* t = static_cast<const GemmDesc*>(x->gemm_wg.p);
   const int M = 4 * x->Hp, N = std::max(x->Hp, x->Ip);
-  if constexpr (P::kPlanes == 2) {
+  if constexpr (P::kTF32) {  // kind::tf32 reads these operands K-major only: transposed copies
     const long long colsT = (long long)x->Bp * x->T;
     for (int l = 0; l < x->L; ++l) {
       transpose_planes(x, x->dgop[l], 4 * x->Hp, colsT, x->dgT[l], s);
@@ -1743,10 +1817,7 @@ int rw_forward(rw_ctx* x, const float* xin, int training, const float* const* h0
     repack_params(x, x->main);
     forward_prologue(x, x->main, h0 ? th0.f() : nullptr, c0 ? tc0.f() : nullptr);
     x->state0_zero = !h0 && !c0;
-    if (x->prec == kBF16)
-      run_forward_rec<PrecBF16>(x, x->main, training != 0);
-    else
-      run_forward_rec<PrecTF32x3>(x, x->main, training != 0);
+    by_prec(x->prec, [&](auto tag) { run_forward_rec<decltype(tag)>(x, x->main, training != 0); });
     sync_all(x);
     x->inputs_uploaded = false;
     x->tape_gen += 1;
@@ -1772,13 +1843,10 @@ int rw_backward_data(rw_ctx* x, uint64_t tape_id, const float* dy, float* dx0, f
     RW_CUDA(cudaSetDevice(x->dev));
     RW_CUDA(cudaMemcpyAsync(x->dy_raw.p, dy, (size_t)x->H * x->B * x->T * 4, cudaMemcpyHostToDevice, x->main));
     repack_params(x, x->main);
-    if (x->prec == kBF16) {
-      run_backward_rec<PrecBF16>(x, x->main);
-      run_dx0<PrecBF16>(x, x->main);
-    } else {
-      run_backward_rec<PrecTF32x3>(x, x->main);
-      run_dx0<PrecTF32x3>(x, x->main);
-    }
+    by_prec(x->prec, [&](auto tag) {
+      run_backward_rec<decltype(tag)>(x, x->main);
+      run_dx0<decltype(tag)>(x, x->main);
+    });
     sync_all(x);
     x->bwd_done = true;
     if (dx0) RW_CUDA(cudaMemcpy(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost));
@@ -1794,10 +1862,7 @@ int rw_weight_update(rw_ctx* x, uint64_t tape_id, float* const* dW, float* const
     check_tape(x, tape_id);
     if (!x->bwd_done) einval("weight_update: backward state layer count mismatch (run backward_data on this tape first)");
     RW_CUDA(cudaSetDevice(x->dev));
-    if (x->prec == kBF16)
-      run_weight_grads<PrecBF16>(x, x->main);
-    else
-      run_weight_grads<PrecTF32x3>(x, x->main);
+    by_prec(x->prec, [&](auto tag) { run_weight_grads<decltype(tag)>(x, x->main); });
     run_db(x, x->main);
     sync_all(x);
     for (int l = 0; l < x->L; ++l) {
@@ -1888,10 +1953,7 @@ extern "C" int rw_train_step(rw_ctx* x, const float* xin, const float* dy, float
     RW_CUDA(cudaMemcpyAsync(x->x_raw.p, xin, xb, cudaMemcpyHostToDevice, x->cp_in));
     RW_CUDA(cudaEventRecord(x->ev_x, x->cp_in));
     RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_x, 0));
-    if (x->prec == kBF16)
-      enqueue_pass<PrecBF16>(x, 3, x->main);
-    else
-      enqueue_pass<PrecTF32x3>(x, 3, x->main);
+    by_prec(x->prec, [&](auto tag) { enqueue_pass<decltype(tag)>(x, 3, x->main); });
     RW_CUDA(cudaEventRecord(x->ev_fwd, x->main));
     if (y) {
       RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_y_out, 0));
@@ -1913,15 +1975,9 @@ extern "C" int rw_train_step(rw_ctx* x, const float* xin, const float* dy, float
     x->tape_training = true;
     // the backward recurrence writes no read-back buffer: only the gradient phase waits for the
     // previous step's read-back (ev_out), which thus overlaps this step's forward + recurrence
-    if (x->prec == kBF16)
-      enqueue_pass<PrecBF16>(x, 4, x->main);
-    else
-      enqueue_pass<PrecTF32x3>(x, 4, x->main);
+    by_prec(x->prec, [&](auto tag) { enqueue_pass<decltype(tag)>(x, 4, x->main); });
     RW_CUDA(cudaStreamWaitEvent(x->main, x->ev_out, 0));
-    if (x->prec == kBF16)
-      enqueue_pass<PrecBF16>(x, 5, x->main);
-    else
-      enqueue_pass<PrecTF32x3>(x, 5, x->main);
+    by_prec(x->prec, [&](auto tag) { enqueue_pass<decltype(tag)>(x, 5, x->main); });
     x->bwd_done = true;
     if (x->comm) allreduce_grads(x, x->main);  // data parallel: sum dW/dR/db before read-back
     RW_CUDA(cudaEventRecord(x->ev_bwd, x->main));
@@ -1956,10 +2012,7 @@ int rw_run_pass(rw_ctx* x, int pass, void* stream) {
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
     if (pass == 1 && (x->tape_gen == 0 || !x->tape_training))
       einval("rw_run_pass: backward needs a training tape (run pass 2 once first)");
-    if (x->prec == kBF16)
-      enqueue_pass<PrecBF16>(x, pass, s);
-    else
-      enqueue_pass<PrecTF32x3>(x, pass, s);
+    by_prec(x->prec, [&](auto tag) { enqueue_pass<decltype(tag)>(x, pass, s); });
     if (pass != 1) {
       x->tape_gen += 1;
       x->tape_training = pass >= 2;
@@ -2040,7 +2093,7 @@ static void* open_region(rw_ctx* x, const rw_pp_ring* peer, int i) {
 
 extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
   return guarded(x, [&] {
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16)
       einval("rw_pp_export: the layer pipeline needs the cluster schedule in both directions (bf16)");
     if (dir != 0 && dir != 1) einval("rw_pp_export: dir must be 0 (forward) or 1 (backward)");
     RW_CUDA(cudaSetDevice(x->dev));
@@ -2072,7 +2125,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
   x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16)
       einval("rw_pp_link: the layer pipeline needs the cluster schedule in both directions (bf16)");
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
@@ -2090,7 +2143,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
       RW_CUDA(cudaMemcpy(wn.p, W_next, 4ULL * H * H * 4, cudaMemcpyHostToDevice));
       x->wf_next.alloc((size_t)G4p * (Hp + Hp) * 2);
       ++g_launches;
-      k_pack_wf<<<grid_for(G4p * 2 * Hp), 256>>>(wn.f(), wn.f(), H, H, Hp, Hp, x->prec, x->wf_next.p, nullptr);
+      k_pack_wf<<<dim3(ceil_div(2 * Hp, 64), (int)(G4p / 32)), dim3(32, 8)>>>(wn.f(), wn.f(), H, H, Hp, Hp, x->prec,
+                                                                            x->wf_next.p, nullptr);
       RW_CUDA(cudaGetLastError());
       RW_CUDA(cudaDeviceSynchronize());
       o.kdim = Hp;
@@ -2309,6 +2363,12 @@ int rw_describe(rw_ctx* x, int* fs, int* bs, int* kf, int* kb) {
   });
 }
 
+int rw_describe_precision(rw_ctx* x, int* fmt) {
+  return guarded(x, [&] {
+    if (fmt) *fmt = x->prec;
+  });
+}
+
 int rw_describe_variants(rw_ctx* x, int* fwd_pair, int* wgrad_bn) {
   return guarded(x, [&] {
     if (fwd_pair) *fwd_pair = (x->pair_f ? 1 : 0) | (x->pair_b ? 2 : 0);
@@ -2323,10 +2383,11 @@ float rw_test_gemm_last_ms(void) { return g_test_gemm_ms; }
 int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const float* dA,
                  long long lda, const float* dB, long long ldb, float* dD, long long ldd, int bn) {
   return guarded(nullptr, [&] {
-    const int prec = precision == RW_PREC_BF16 ? kBF16 : kTF32x3;
-    const int aK = prec == kBF16 ? 64 : 32;
+    // precision 2 (test hook only): the fp16x2 split operands of the fp32-parity cluster path
+    const int prec = precision == RW_PREC_BF16 ? kBF16 : precision == 2 ? kF16x2 : kTF32x3;
+    const int aK = prec_atomk(prec);
     if (M % 128 || N % bn || K % 64 || (bn != 64 && bn != 128 && bn != 256)) einval("rw_test_gemm: bad shape");
-    if (prec != kBF16 && (a_mn || b_mn)) einval("rw_test_gemm: tf32 operands must be K-major");
+    if (prec == kTF32x3 && (a_mn || b_mn)) einval("rw_test_gemm: tf32 operands must be K-major");
     // element counts of the stored operands
     const long long a_elems = a_mn ? (long long)K * lda : (long long)M * lda;
     const long long b_elems = b_mn ? (long long)K * ldb : (long long)N * ldb;
@@ -2354,6 +2415,7 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
       g.a[1] = MD + 2;
       g.b[1] = MD + 3;
     }
+    g.alpha = 1.0f;
     g.M = M;
     g.N = N;
     g.K = K;
@@ -2367,7 +2429,7 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     gd.alloc(sizeof(GemmDesc));
     RW_CUDA(cudaMemcpy(gd.p, &g, sizeof g, cudaMemcpyHostToDevice));
     const GemmDesc* G = static_cast<const GemmDesc*>(gd.p);
-    const int planes = prec == kBF16 ? 1 : 2;
+    const int planes = prec_planes(prec);
     const int st = gemm_stages(planes, bn);
     const char* reps_env = getenv("RW_TEST_GEMM_REPS");
     const int reps = reps_env ? std::max(1, atoi(reps_env)) : 1;
@@ -2376,17 +2438,13 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     cudaEventCreate(&e1);
     for (int rep = 0; rep <= reps; ++rep) {
     if (rep == 1) cudaEventRecord(e0, 0);
-    if (prec == kBF16) {
-      if (!a_mn && !b_mn) launch_gemm<PrecBF16, false, false>(G, 1, M, N, bn, st, 0);
-      if (!a_mn && b_mn) launch_gemm<PrecBF16, false, true>(G, 1, M, N, bn, st, 0);
-      if (a_mn && !b_mn) launch_gemm<PrecBF16, true, false>(G, 1, M, N, bn, st, 0);
-      if (a_mn && b_mn) launch_gemm<PrecBF16, true, true>(G, 1, M, N, bn, st, 0);
-    } else {
-      if (!a_mn && !b_mn) launch_gemm<PrecTF32x3, false, false>(G, 1, M, N, bn, st, 0);
-      if (!a_mn && b_mn) launch_gemm<PrecTF32x3, false, true>(G, 1, M, N, bn, st, 0);
-      if (a_mn && !b_mn) launch_gemm<PrecTF32x3, true, false>(G, 1, M, N, bn, st, 0);
-      if (a_mn && b_mn) launch_gemm<PrecTF32x3, true, true>(G, 1, M, N, bn, st, 0);
-    }
+    by_prec(prec, [&](auto tag) {
+      using P = decltype(tag);
+      if (!a_mn && !b_mn) launch_gemm<P, false, false>(G, 1, M, N, bn, st, 0);
+      if (!a_mn && b_mn) launch_gemm<P, false, true>(G, 1, M, N, bn, st, 0);
+      if (a_mn && !b_mn) launch_gemm<P, true, false>(G, 1, M, N, bn, st, 0);
+      if (a_mn && b_mn) launch_gemm<P, true, true>(G, 1, M, N, bn, st, 0);
+    });
     }
     cudaEventRecord(e1, 0);
     RW_CUDA(cudaDeviceSynchronize());

@@ -175,6 +175,19 @@ RW_DEVICE void umma_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32
     umma_bf16_warp(tmem_d, adesc, bdesc, idesc, accumulate);
   }
 }
+// A operand from TENSOR MEMORY ("TS"): D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16. A is
+// M = 128 rows on the 128 lanes, K along the columns with two 16-bit elements per 32-bit column
+// (element k of the row in column k/2, even k in the low half): one K = 16 step reads 8 columns
+// (layout checked on B200 by profiles/ubench/f16x2_ts_check.cu).
+RW_DEVICE void umma_ts_f16_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 RW_DEVICE void umma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -211,6 +224,13 @@ RW_DEVICE void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[8]) {
         "=r"(v[7])
       : "r"(taddr));
 }
+// registers -> 8 consecutive 32-bit columns of this warp's 32 lanes (lane quarter = warp % 4)
+RW_DEVICE void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+RW_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 RW_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ UMMA descriptors

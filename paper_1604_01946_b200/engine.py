@@ -497,7 +497,10 @@ class Engine:
         names = {1: "stepwise", 2: "persistent", 3: "cluster", 4: "layerseq"}
         pair, bn = C.c_int(), C.c_int()
         self._check(self._L.rw_describe_variants(self._ctx, C.byref(pair), C.byref(bn)))
+        fmt = C.c_int()
+        self._check(self._L.rw_describe_precision(self._ctx, C.byref(fmt)))
         return {"fwd_schedule": names[a.value], "bwd_schedule": names[b.value],
+                "operands": {0: "bf16", 1: "tf32x3", 2: "fp16x2"}[fmt.value],
                 "fwd_ksplit": k1.value, "bwd_ksplit": k2.value, "fwd_pair": pair.value & 1,
                 "bwd_pair": (pair.value >> 1) & 1, "wgrad_bn": bn.value,
                 "layerseq_persistent": [(pair.value >> 2) & 1, (pair.value >> 3) & 1]}

@@ -31,10 +31,9 @@ def test_small_configs(reference, precision, schedule, dims):
 
 
 def make_engine(Engine, c, precision, schedule):
-    """The cluster schedule is bf16-only and shape-gated (rec_cluster.cuh): skip where the
-    runtime reports that it does not fit rather than testing a fallback under its name."""
-    if schedule == "cluster" and precision != "bf16":
-        pytest.skip("cluster schedule is bf16 only")
+    """The cluster schedule is shape-gated (rec_cluster.cuh): skip where the runtime reports
+    that it does not fit rather than testing a fallback under its name. In fp32-parity mode
+    it runs the fp16x2 operand format."""
     try:
         eng = Engine(c, precision=precision, schedule=schedule)
     except ValueError as e:
@@ -44,6 +43,7 @@ def make_engine(Engine, c, precision, schedule):
     d = eng.describe()
     if schedule == "cluster":
         assert d["fwd_schedule"] == d["bwd_schedule"] == "cluster", d
+        assert d["operands"] == ("bf16" if precision == "bf16" else "fp16x2"), d
     return eng
 
 
@@ -54,18 +54,20 @@ CLUSTER = [
     Dims(2, 512, 512, 64, 6),    # config-B shape, short: fwd cs = 2, bwd kc = 4, cs = 8
     Dims(3, 512, 300, 64, 7),    # bwd kc = 4, cs = 8; layer-0 input narrower than H
     Dims(1, 512, 512, 64, 9),    # single layer: backward has no off-critical members
-    Dims(2, 384, 1000, 48, 5),   # forward ko = 2 (I = 1000 -> two W.x members), nco = 48
+    Dims(2, 384, 1000, 64, 5),   # forward ko = 2 (I = 1000 -> two W.x members)
+    Dims(2, 256, 200, 60, 6),    # ragged batch (Bp = 64: padded columns carry zeros)
 ]
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("dims", CLUSTER, ids=lambda d: f"L{d.layers}H{d.hidden}I{d.input}B{d.batch}T{d.steps}")
-def test_cluster_configs(reference, dims):
+def test_cluster_configs(reference, dims, precision):
     from paper_1604_01946_b200 import Engine
     c, params, x, dy, h0, c0 = make_case(dims, seed=17, bias=True, state=True)
-    eng = make_engine(Engine, c, "bf16", "cluster")
+    eng = make_engine(Engine, c, precision, "cluster")
     dev = run_device(eng, params, x, dy, h0, c0)
     ref = run_reference(reference, c, params, x, dy, h0, c0)
-    worst = assert_within(compare(dev, ref, c), "bf16")
+    worst = assert_within(compare(dev, ref, c), precision)
     print(f"cluster {dims}: {eng.describe()} worst {worst}")
 
 
