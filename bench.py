@@ -7,7 +7,12 @@ inputs/weights exactly like the reference generators (seed 42). FLOPs follow the
 reference convention (cells.hpp:65-68, bench.hpp:55-62, 210-213): GEMM multiply-adds only,
 2*4*H*(I+H)*B per cell x L*T x 3 (fwd 1 + bwd 2).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|fp32]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp32|bf16] [--config B]
+
+The headline line is the fp32-parity mode (the reference computes in fp32; our split-operand
+tensor-core products meet its 1e-5 contract); bf16 is reported as a secondary key. Every timed
+step re-runs the K7 weight repack (the parameters are marked updated, as after an optimizer
+step), like the reference's per-pass pretranspose.
   python bench.py --impl reference ...   (the reference CPU engine, oracle/_ref, host cores)
 
 Under torchrun (N > 1) every rank runs its own independent minibatch of the same shape
@@ -58,30 +63,36 @@ def pass_flops(c: dict, mult: int = 3) -> int:
 L2_WEIGHT_BYTES = 100 * 1024 * 1024
 
 
-def recurrent_bytes(c: dict, fwd: bool) -> int:
-    """Algorithmic HBM bytes of one recurrent launch: the bf16 weights --
-    once per pass when they fit on chip or in L2, else once per step (config E: 512 MB of
-    [W|R] per wavefront step, far beyond smem + L2) -- plus the fp32 tapes each cell must write (forward:
-    gates x4, c, h, tanh c + the bf16 h operand) or read and write (backward: gates x4, tanh c,
-    c read; dG fp32 x4 + bf16 x4 written)."""
+def recurrent_bytes(c: dict, fwd: bool, planes: int = 1) -> int:
+    """Algorithmic HBM bytes of one recurrent launch: the 16-bit weight
+    operand planes (bf16: one; fp32-parity: hi + lo) -- once per pass when they fit on chip or
+    in L2, else once per step (config E: 512 MB of bf16 [W|R] per wavefront step, far beyond
+    smem + L2) -- plus the fp32 tapes each cell must write (forward: gates x4, c, h, tanh c + the
+    16-bit h operand planes) or read and write (backward: gates x4, tanh c, c read; dG fp32 x4 +
+    the 16-bit dG operand planes x4 written)."""
     L, H, I, B, T = c["layers"], c["hidden"], c["input"], c["batch"], c["steps"]
     if fwd:
         w = sum(4 * H * ((I if l == 0 else H) + H) * 2 for l in range(L))
-        steps, cell = T, 4 * (4 + 3) + 2
+        steps, cell = T, 4 * (4 + 3) + 2 * planes
     else:
         w = sum(4 * H * (H + (H if l < L - 1 else 0)) * 2 for l in range(L))
-        steps, cell = T + 1, 4 * (4 + 2) + 4 * (4 + 2)
+        steps, cell = T + 1, 4 * (4 + 2) + 4 * 4 + 4 * 2 * planes
+    w *= planes
     wt = w if w <= L2_WEIGHT_BYTES else w * steps
     return wt + L * T * H * B * cell
 
 
-def ncu_traffic(kernel_prefix: str, config: str):
-    """DRAM bytes (read + write) of the kernel from the committed ncu --set full capture of this
-    config (profiles/r01/ncu_summary_<config>_v{3,2}.json), or None."""
+def ncu_traffic(kernel_prefix: str, config: str, precision: str = "bf16"):
+    """DRAM bytes (read + write) of the kernel from the newest committed ncu --set full capture
+    of this config and precision (profiles/r02/ncu_summary_<config>_<precision>.json, else the
+    round-1 bf16 captures profiles/r01/ncu_summary_<config>_v{3,2}.json), or None."""
     summ = None
-    for ver in ("v3", "v2"):  # the newest committed capture of this config
+    cands = [("r02", f"ncu_summary_{config}_{precision}.json")]
+    if precision == "bf16":
+        cands += [("r01", f"ncu_summary_{config}_{v}.json") for v in ("v3", "v2")]
+    for rd, name in cands:
         try:
-            summ = json.load(open(os.path.join(ROOT, "profiles", "r01", f"ncu_summary_{config}_{ver}.json")))
+            summ = json.load(open(os.path.join(ROOT, "profiles", rd, name)))
             break
         except (OSError, ValueError):
             continue
@@ -161,6 +172,32 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml 5 ms" if self.nvml else "nvidia-smi"}
 
 
+# ----------------------------------------------------------------------------- shared
+def workload_name(key: str, c: dict) -> str:
+    base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM fwd+bwd"
+    return base + (" (BASELINE configs[1])" if key == "B" else f" (sweep config {key})")
+
+
+def config_dict(key: str, c: dict, world: int) -> dict:
+    """The `config` object both arms print (identical keys, so the driver can match them)."""
+    return {"workload": workload_name(key, c), "model": f"lstm-{c['layers']}x{c['hidden']}",
+            "global_batch": c["batch"] * world, "seq_len": c["steps"], "layers": c["layers"],
+            "hidden": c["hidden"], "parallelism": f"dp{world}" if world > 1 else "single",
+            "l2": "flushed (256 MiB write) between timed steps",
+            "per_step_work": "K7 repack (params updated in place) + forward (training) + "
+                             "backward_data + weight_update, like the reference's time_level pass"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
@@ -177,7 +214,7 @@ def run_reference(args) -> None:
     est = R.time(d, seed=42, pass_kind=2, reps=1, warmup=0, workers=cores)["median_us"] * 1e-6
     budget = 150.0
     reps = max(1, min(args.steps, int(budget / max(est, 1e-3))))
-    warm = min(args.warmup, 1)
+    warm = max(args.warmup, 3) if est * (reps + max(args.warmup, 3)) < 1.5 * budget else 1
     t = R.time(d, seed=42, pass_kind=2, reps=reps, warmup=warm, workers=cores)
     sec = t["median_us"] * 1e-6
     tflops = flops / sec / 1e12
@@ -186,34 +223,26 @@ def run_reference(args) -> None:
         "n_gpus": args.gpus, "steps": reps, "warmup": warm, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SplitMix64 seed 42, reference generators)",
-        "config": {"workload": workload_name(args.config, c),
-                   "global_batch": c["batch"], "seq_len": c["steps"],
-                   "layers": c["layers"], "hidden": c["hidden"], "opt_level": 6, "workers": cores},
+        "config": config_dict(args.config, c, 1),
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "reference",
                          "sample": f"{reps} full config-{args.config} passes (median), O6, {cores} workers",
-                         "lib": os.path.basename(R.path)},
+                         "cpu": cpu_model(), "lib": os.path.basename(R.path)},
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_ours(args) -> None:
+def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: bool = True) -> dict:
+    """Time one precision mode: K timed steps (repack + fwd + bwd + weight update), per-phase
+    device times, and the end-to-end host-buffer training call. Returns a partial line."""
     import numpy as np
     import torch
     from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     c = dict(CONFIGS[args.config])
     cfg = LadderConfig(**c, seed=42 + rank, opt_level=6, batch_steps=2, workers=1)
-    eng = Engine(cfg, precision=args.precision, schedule=args.schedule, device=local)
+    eng = Engine(cfg, precision=precision, schedule=args.schedule, device=local)
     params = init_params(LadderConfig(**c, seed=42))
     x = make_input(cfg)
     dy = make_dy(cfg)
@@ -227,19 +256,19 @@ def run_ours(args) -> None:
         eng.init_comm(rank, world, box[0])
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
-    flops = pass_flops(c)
 
     # L2 flush buffer (> 126 MB L2) written between timed steps, outside the events
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
-    def allreduce():
+    def step():
+        eng.params_updated()  # the parameters changed (optimizer): K7 repack inside the pass
+        eng.run_pass(2, sh)
         if world > 1:
             eng.allreduce_grads(sh)
 
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
-            eng.run_pass(2, sh)
-            allreduce()
+            step()
         eng.sync()
         torch.cuda.synchronize()
         if world > 1:
@@ -252,8 +281,7 @@ def run_ours(args) -> None:
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                eng.run_pass(2, sh)
-                allreduce()
+                step()
                 ev[i][1].record(stream)
             torch.cuda.synchronize()
             eng.sync()
@@ -272,60 +300,74 @@ def run_ours(args) -> None:
         nprof = max(3, min(args.steps, 10))
         for _ in range(nprof):
             flush.zero_()
+            eng.params_updated()
             eng.run_pass(2, sh)
         eng.sync()
         ph = eng.phase_times(reset=True)
         eng.set_profiling(False)
 
-        # ---- e2e through the C-ABI with host buffers: H2D inputs, pass, D2H results
-        def pinned(rows, cols=None):
-            """Column-major float32 host array in pinned (page-locked) memory: DMA at full rate."""
-            if cols is None:
-                return torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
-            return torch.zeros(cols, rows, dtype=torch.float32).pin_memory().numpy().T
+        e2e = None
+        if with_e2e:
+            def pinned(rows, cols=None):
+                """Column-major float32 host array in pinned (page-locked) memory."""
+                if cols is None:
+                    return torch.zeros(rows, dtype=torch.float32).pin_memory().numpy()
+                return torch.zeros(cols, rows, dtype=torch.float32).pin_memory().numpy().T
 
-        y = pinned(c["hidden"], c["batch"] * c["steps"])
-        dx0 = pinned(c["input"], c["batch"] * c["steps"])
-        dw = [pinned(4 * c["hidden"], c["input"] if l == 0 else c["hidden"]) for l in range(c["layers"])]
-        dr = [pinned(4 * c["hidden"], c["hidden"]) for _ in range(c["layers"])]
-        db = [pinned(4 * c["hidden"]) for _ in range(c["layers"])]
-        xh = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).pin_memory()
-        dyh = torch.from_numpy(np.asfortranarray(dy).ravel(order="F")).pin_memory()
-        h2d = xh.numel() * 4 + dyh.numel() * 4
-        d2h = (y.size + dx0.size + sum(a.size for a in dw) + sum(a.size for a in dr)
-               + sum(a.size for a in db)) * 4
-        # the public training call with host buffers: rw_train_step uploads x/dy, runs the pass
-        # (+ the DP gradient all-reduce) and reads y, dx0, dW, dR, db back, pipelined so the
-        # next step's uploads and this step's read-back overlap compute; timed by wall clock
-        # over the whole sequence including the final wait (device events cannot span streams)
-        e2e_steps = max(10, min(args.steps, 50))
-        xn, dyn = xh.numpy(), dyh.numpy()
-        for _ in range(3):
-            eng.train_step(xn, dyn, y, dx0, dw, dr, db)
-        eng.train_wait()
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            eng.train_step(xn, dyn, y, dx0, dw, dr, db)
-        eng.train_wait()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = t.item()
-
-    if rank != 0:
-        return
-    peaks, peak_src = measured_peaks()
+            y = pinned(c["hidden"], c["batch"] * c["steps"])
+            dx0 = pinned(c["input"], c["batch"] * c["steps"])
+            dw = [pinned(4 * c["hidden"], c["input"] if l == 0 else c["hidden"]) for l in range(c["layers"])]
+            dr = [pinned(4 * c["hidden"], c["hidden"]) for _ in range(c["layers"])]
+            db = [pinned(4 * c["hidden"]) for _ in range(c["layers"])]
+            xh = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).pin_memory()
+            dyh = torch.from_numpy(np.asfortranarray(dy).ravel(order="F")).pin_memory()
+            h2d = xh.numel() * 4 + dyh.numel() * 4
+            d2h = (y.size + dx0.size + sum(a.size for a in dw) + sum(a.size for a in dr)
+                   + sum(a.size for a in db)) * 4
+            # the public training call with host buffers: rw_train_step uploads x/dy, runs the
+            # pass (repack of the updated parameters included, + the DP all-reduce) and reads y,
+            # dx0, dW, dR, db back, pipelined so the next step's uploads and this step's read-back
+            # overlap compute; wall clock over the whole sequence including the final wait
+            e2e_steps = max(10, min(args.steps, 50))
+            xn, dyn = xh.numpy(), dyh.numpy()
+            for _ in range(3):
+                eng.params_updated()
+                eng.train_step(xn, dyn, y, dx0, dw, dr, db)
+            eng.train_wait()
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                eng.params_updated()
+                eng.train_step(xn, dyn, y, dx0, dw, dr, db)
+            eng.train_wait()
+            e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+            if world > 1:
+                t = torch.tensor([e2e_ms], device="cuda")
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                e2e_ms = t.item()
+            e2e = {"value": pass_flops(c) * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "path": "C-ABI rw_train_step (pinned host x, dy -> K7 repack + forward + backward_data"
+                           " + weight_update -> y, dx0, dW, dR, db on the host; uploads/read-back"
+                           " pipelined against compute)"}
     desc = eng.describe()
-    # dominant kernel: the longer of the two recurrent (persistent / stepwise) phases
+    eng.close()
+    return {"ms": ms, "ph": ph, "launches": launches, "clocks": clk.summary(), "e2e": e2e, "desc": desc}
+
+
+def roofline(args, m: dict, precision: str) -> tuple[dict, dict]:
+    c = dict(CONFIGS[args.config])
+    peaks, peak_src = measured_peaks()
+    desc, ph = m["desc"], m["ph"]
+    planes = 1 if precision == "bf16" else 2  # fp32-parity: hi and lo operand planes
+    # dominant kernel: the longer of the two recurrent (persistent / stepwise / cluster) phases
     fwd_ms = ph["fwd_recurrent"][0] / max(ph["fwd_recurrent"][1], 1)
     bwd_ms = ph["bwd_recurrent"][0] / max(ph["bwd_recurrent"][1], 1)
     L, H, I, B, T = c["layers"], c["hidden"], c["input"], c["batch"], c["steps"]
     fwd_fl = pass_flops(c, 1)  # [W|R].[x;h] for every cell
-    bwd_fl = sum(2 * 4 * H * (H + (H if l < L - 1 else 0)) * B * (T + (1 if True else 0))
+    bwd_fl = sum(2 * 4 * H * (H + (H if l < L - 1 else 0)) * B * (T + 1)
                  for l in range(L))  # W_{l+1}^T and R_l^T per cell (+ the dh0 step)
     kern = {"cluster": ("k_cl_fwd", "k_cl_bwd"), "persistent": ("k_lstm_fwd", "k_lstm_bwd"),
             "layerseq": ("k_gemm_p + k_lstm_fwd", "k_gemm_p + k_lstm_bwd"),
@@ -334,26 +376,76 @@ def run_ours(args) -> None:
     kb = kern.get(desc["bwd_schedule"], ("", "k_lstm_bwd"))[1]
     if bwd_ms >= fwd_ms:
         dom, dom_ms, dom_fl = f"{kb} (fused recurrent backward, {desc['bwd_schedule']})", bwd_ms, bwd_fl
-        dom_k, dom_by = kb, recurrent_bytes(c, False)
+        dom_k, dom_by = kb, recurrent_bytes(c, False, planes)
     else:
         dom, dom_ms, dom_fl = f"{kf} (fused recurrent forward, {desc['fwd_schedule']})", fwd_ms, fwd_fl
-        dom_k, dom_by = kf, recurrent_bytes(c, True)
+        dom_k, dom_by = kf, recurrent_bytes(c, True, planes)
     achieved = dom_fl / (dom_ms * 1e-3) / 1e12
     # burst peak for a kernel timed alone; the sustained (power-capped) one once the kernel runs
-    # long enough to hit the power limit (>= 10 ms: config E's recurrent kernels run at
-    # ~1.5 GHz under sw_power_cap, as does the sustained cuBLAS figure)
+    # long enough to hit the power limit (>= 10 ms)
     peak_burst = peaks.get("bf16_tflops", 1590.0)
     peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
     long_kernel = dom_ms >= 10.0
     peak = peak_sus if long_kernel else peak_burst
-    # binding roofline: the larger of flops / tensor peak and algorithmic bytes / HBM peak
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_bound = dom_by / (hbm_peak * 1e9) > dom_fl / (peak * 1e12)
-    traffic = ncu_traffic(dom_k.split()[0], args.config)
+    traffic = ncu_traffic(dom_k.split()[0], args.config, precision)
+    note = ("fp32-parity: each product is 3 tensor-core MMAs on split operands (hi.hi + hi.lo + "
+            "lo.hi), so the attainable ceiling is peak/3; frac is against the full dense bf16 peak"
+            if precision == "fp32" else "bf16 operands, fp32 accumulation")
+    if hbm_bound:
+        r = {"kernel": dom, "bound": "hbm", "achieved": dom_by / (dom_ms * 1e-3) / 1e9, "peak": hbm_peak,
+             "unit": "GB/s", "frac": dom_by / (dom_ms * 1e-3) / 1e9 / hbm_peak, "traffic": traffic,
+             "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+             "algorithmic_bytes_per_launch": dom_by, "tensor_tflops": achieved,
+             "tensor_frac": achieved / peak, "avg_launch_ms": dom_ms, "note": note}
+    else:
+        r = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+             "frac": achieved / peak, "traffic": traffic,
+             "peak_source": f"{peak_src} bf16 dense {'sustained' if long_kernel else 'burst'} (MEASURED_PEAKS.json)",
+             "algorithmic_flops_per_launch": dom_fl, "algorithmic_bytes_per_launch": dom_by,
+             "hbm_frac": dom_by / (dom_ms * 1e-3) / 1e9 / hbm_peak, "avg_launch_ms": dom_ms, "note": note}
+    crit = {"steps_fwd": T + L - 1, "steps_bwd": T + L,
+            "us_per_step_fwd": 1e3 * fwd_ms / (T + L - 1), "us_per_step_bwd": 1e3 * bwd_ms / (T + L)}
+    return r, crit
+
+
+def run_ours(args) -> None:
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c = dict(CONFIGS[args.config])
+    flops = pass_flops(c)
+    m = measure(args, args.precision, world, rank, local)
+    # the other precision mode, same workload, as a secondary key (bf16 is narrower arithmetic
+    # than the reference's fp32: never the headline)
+    other = "bf16" if args.precision == "fp32" else "fp32"
+    m2 = None if args.single_precision else measure(args, other, world, rank, local, with_e2e=True)
+    if rank != 0:
+        return
+    peaks, _ = measured_peaks()
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    rf, crit = roofline(args, m, args.precision)
     cpu_base = None
-    if not args.no_cpu_baseline and args.config == "B":
-        cpu_base = cpu_baseline()
-    value = flops * world / (ms * 1e-3) / 1e12
+    if not args.no_cpu_baseline and args.config in ("A", "B"):
+        cpu_base = cpu_baseline(args.config)
+    value = flops * world / (m["ms"] * 1e-3) / 1e12
+    dtype = {"bf16": "bf16", "fp32": "tf32x3 (fp32-parity)"}
+    operands = {"tf32x3": "3xTF32 split operands", "fp16x2": "fp16x2 split operands (hi + lo, 3 MMAs)",
+                "bf16": "bf16 operands"}
+    cfgd = config_dict(args.config, c, world)
+    cfgd.update({"precision": args.precision, "schedule": m["desc"],
+                 "operands": operands.get(m["desc"]["operands"], m["desc"]["operands"]),
+                 "pct_of_bf16_peak": 100.0 * value / world / peak_burst,
+                 "pct_of_bf16_peak_sustained": 100.0 * value / world / peak_sus})
     line = {
         "metric": METRIC,
         "value": value,
@@ -361,54 +453,38 @@ def run_ours(args) -> None:
         "n_gpus": world,
         "steps": args.steps,
         "warmup": max(args.warmup, 3),
-        "ms_per_step": ms,
+        "ms_per_step": m["ms"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16" if args.precision == "bf16" else "tf32x3 (fp32-parity)",
+        "dtype": dtype[args.precision],
         "data": "synthetic (SplitMix64 seed 42 weights, streams 1000/1001 inputs: the reference generators)",
-        "config": {"workload": workload_name(args.config, c),
-                   "model": f"lstm-{c['layers']}x{c['hidden']}", "global_batch": c["batch"] * world, "seq_len": T,
-                   "parallelism": f"dp{world}" if world > 1 else "single",
-                   "precision": args.precision, "schedule": desc,
-                   "l2": "flushed (256 MiB write) between timed steps",
-                   "pct_of_bf16_peak": 100.0 * value / world / peak_burst,
-                   "pct_of_bf16_peak_sustained": 100.0 * value / world / peak_sus},
-        "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "C-ABI rw_train_step (pinned host x, dy -> forward + backward_data + weight_update"
-                        " -> y, dx0, dW, dR, db on the host; uploads/read-back pipelined against compute)"},
-        "roofline": ({"kernel": dom, "bound": "hbm", "achieved": dom_by / (dom_ms * 1e-3) / 1e9,
-                      "peak": hbm_peak, "unit": "GB/s", "frac": dom_by / (dom_ms * 1e-3) / 1e9 / hbm_peak,
-                      "traffic": traffic, "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json)",
-                      "algorithmic_bytes_per_launch": dom_by, "tensor_tflops": achieved,
-                      "tensor_frac": achieved / peak, "avg_launch_ms": dom_ms}
-                     if hbm_bound else
-                     {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
-                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                      "peak_source": f"{peak_src} bf16 {'sustained' if long_kernel else 'burst'} (MEASURED_PEAKS.json)",
-                      "algorithmic_flops_per_launch": dom_fl, "algorithmic_bytes_per_launch": dom_by,
-                      "avg_launch_ms": dom_ms}),
-        "phases_ms": {k: v[0] / max(v[1], 1) for k, v in ph.items()},
+        "config": cfgd,
+        "e2e": m["e2e"],
+        "roofline": rf,
+        "phases_ms": {k: v[0] / max(v[1], 1) for k, v in m["ph"].items()},
         # SURVEY §8d's latency bound: the wavefront's dependent steps (T + L - 1 per direction,
         # + the dh0 step backward) and the measured time per step of each recurrent phase
-        "critical_path": {"steps_fwd": T + L - 1, "steps_bwd": T + L,
-                          "us_per_step_fwd": 1e3 * fwd_ms / (T + L - 1),
-                          "us_per_step_bwd": 1e3 * bwd_ms / (T + L)},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "critical_path": crit,
+        "gpu_launches": m["launches"],
+        "clocks": m["clocks"],
         "cpu_baseline": cpu_base,
     }
+    if m2 is not None:
+        rf2, crit2 = roofline(args, m2, other)
+        v2 = flops * world / (m2["ms"] * 1e-3) / 1e12
+        line[other] = {"dtype": dtype[other], "value": v2, "unit": "TFLOP/s", "ms_per_step": m2["ms"],
+                       "e2e": m2["e2e"], "schedule": m2["desc"], "roofline": rf2, "critical_path": crit2,
+                       "phases_ms": {k: v[0] / max(v[1], 1) for k, v in m2["ph"].items()},
+                       "pct_of_bf16_peak": 100.0 * v2 / world / peak_burst, "gpu_launches": m2["launches"],
+                       "clocks": m2["clocks"]}
     print(json.dumps(line), flush=True)
 
 
-def workload_name(key: str, c: dict) -> str:
-    base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM fwd+bwd"
-    return base + (" (BASELINE configs[1])" if key == "B" else f" (sweep config {key})")
-
-
-def cpu_baseline() -> dict | None:
-    """The reference CPU engine on the host cores, bounded sample of the same workload."""
+def cpu_baseline(key: str = "B") -> dict | None:
+    """The reference CPU engine on the host cores, bounded sample of the same workload: P = all
+    host threads and P = min(nproc, 2L) (the reference CLI's default worker count,
+    rnnwave.cpp:30-37)."""
     try:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle
@@ -416,13 +492,19 @@ def cpu_baseline() -> dict | None:
         kind = "reference"
     except Exception:
         return None
-    d = oracle.Dims(**CONFIG_B)
+    c = CONFIGS[key]
+    d = oracle.Dims(**c)
     cores = os.cpu_count() or 1
     t = R.time(d, seed=42, pass_kind=2, reps=3, warmup=1, workers=cores)
     sec = t["median_us"] * 1e-6
-    return {"value": pass_flops(CONFIG_B) / sec / 1e12, "unit": "TFLOP/s", "cores": cores,
-            "kind": kind, "ms_per_step": sec * 1e3,
-            "sample": "3 full config-B fwd+bwd passes after 1 warm-up (median), O6, workers=cores"}
+    p2 = min(cores, 2 * c["layers"])
+    t2 = R.time(d, seed=42, pass_kind=2, reps=3, warmup=1, workers=p2)
+    sec2 = t2["median_us"] * 1e-6
+    return {"value": pass_flops(c) / sec / 1e12, "unit": "TFLOP/s", "cores": cores,
+            "kind": kind, "ms_per_step": sec * 1e3, "cpu": cpu_model(),
+            "sample": f"3 full config-{key} fwd+bwd passes after 1 warm-up (median), O6, workers=cores",
+            "default_workers": {"workers": p2, "value": pass_flops(c) / sec2 / 1e12, "ms_per_step": sec2 * 1e3,
+                                "why": "min(nproc, 2L), the reference CLI default (rnnwave.cpp:30-37)"}}
 
 
 def main():
@@ -431,7 +513,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="fp32", choices=["bf16", "fp32"],
+                    help="headline precision: fp32 = the reference's fp32 contract (split-operand "
+                         "tensor-core products, parity <= 1e-5); the other mode is a secondary key")
+    ap.add_argument("--single-precision", action="store_true", help="skip the secondary precision")
     ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster", "layerseq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS),

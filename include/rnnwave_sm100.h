@@ -138,6 +138,10 @@ int rw_upload_inputs(rw_ctx* ctx, const float* x, const float* dy);
  * completes it). Enqueued on `stream` (cudaStream_t; NULL = the context's own stream) and
  * returns without synchronising. */
 int rw_run_pass(rw_ctx* ctx, int pass, void* stream);
+/* The device copy of the parameters was modified in place (as an optimizer step on the device
+ * does): the next pass re-runs the K7 repack inside its own stream work, like the reference's
+ * per-pass pretranspose (engine.hpp:92, 138). bench.py calls it before every timed pass. */
+int rw_params_updated(rw_ctx* ctx);
 /* One training step end to end with host buffers -- the public call a training loop makes:
  * upload x and dy, forward + backward_data + weight_update, read back y, dx0, dW, dR, db (any
  * output may be NULL). Asynchronous and pipelined: the next step's uploads overlap this

@@ -21,7 +21,7 @@ RW_TAPE_X0, RW_TAPE_H, RW_TAPE_C, RW_TAPE_GATES, RW_TAPE_TANH_C, RW_TAPE_DGW, RW
 EXPORTS = [
     "rw_create", "rw_destroy", "rw_last_error", "rw_create_error", "rw_set_params", "rw_forward",
     "rw_backward_data", "rw_weight_update", "rw_get_tape", "rw_upload_inputs", "rw_run_pass",
-    "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count",
+    "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count", "rw_params_updated",
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_describe_variants",
     "rw_describe_precision", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link",
@@ -83,6 +83,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_describe_precision.argtypes = [vp, C.POINTER(C.c_int)]
     L.rw_read_outputs.argtypes = [vp, _F, _F, _PF, _PF, _PF]
     L.rw_launch_count.argtypes = [vp, C.POINTER(C.c_longlong), C.c_int]
+    L.rw_params_updated.argtypes = [vp]
     L.rw_nccl_unique_id.argtypes = [C.c_char_p]
     L.rw_comm_init.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
     L.rw_allreduce_grads.argtypes = [vp, vp]

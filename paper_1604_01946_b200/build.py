@@ -35,22 +35,44 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each kernel family is its own translation unit (csrc/kernels_*.cu + runtime.cu), compiled
+    to objects in parallel and linked into one shared library."""
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
     cu = [s for s in sources() if s.endswith(".cu")]
+    compile_flags = [f for f in FLAGS if f not in ("-shared",)]
+    procs, objs = [], []
+    for src in cu:
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *ARCH, *compile_flags, "-c", "-I", os.path.join(ROOT, "include"), "-o", obj, src]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log_txt, failed = "", False
+    for cmd, pr in procs:
+        out, err = pr.communicate()
+        log_txt += " ".join(cmd) + "\n" + out + err
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(err[-8000:])
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *cu]
-    out = subprocess.run(cmd, capture_output=True, text=True)
+    if not failed:
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        log_txt += " ".join(cmd) + "\n" + out.stdout + out.stderr
+        if out.returncode != 0:
+            failed = True
+            sys.stderr.write(out.stderr[-8000:])
     log = os.path.join(LIBDIR, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + out.stdout + out.stderr)
-    if out.returncode != 0:
-        sys.stderr.write(out.stderr[-8000:])
+        f.write(log_txt)
+    if failed:
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(tmp, LIB)
     if verbose:
-        print(out.stderr[-4000:])
+        print(log_txt[-4000:])
     return LIB
 
 

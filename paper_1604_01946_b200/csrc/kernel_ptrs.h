@@ -1,0 +1,19 @@
+// kernel_ptrs.h -- host-side handles of the templated sm_100a kernels. Each family is
+// instantiated in its own translation unit (kernels_cl.cu, kernels_lstm.cu, kernels_gemm*.cu,
+// compiled in parallel) and reached from runtime.cu only through these pointers, which are
+// launched with cudaLaunchKernelExC.
+#pragma once
+
+namespace rw {
+
+// k_cl_fwd / k_cl_bwd<P, nco / 16> (rec_cluster.cuh); prec kBF16 or kF16x2
+void* cl_kernel_ptr(int prec, bool fwd, int nco);
+// k_lstm_fwd / k_lstm_bwd<P, pair> (lstm_step.cuh); prec kBF16 or kTF32x3 (pair: bf16 only)
+void* lstm_kernel_ptr(int prec, bool fwd, bool pair);
+// k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh), BNV 0 or 64
+void* gemm_tc_ptr(int prec, bool amn, bool bmn, int bnv);
+// k_gemm_p<AMN, BMN, BN> / k_gemm_p2<AMN, BMN, BN> (bf16), BN 128 or 256
+void* gemm_p_ptr(bool amn, bool bmn, int bn);
+void* gemm_p2_ptr(bool amn, bool bmn, int bn);
+
+}  // namespace rw

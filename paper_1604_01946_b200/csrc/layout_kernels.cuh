@@ -9,14 +9,15 @@
 
 namespace rw {
 
-// `wscale`: weight operands of the fp16x2 mode are stored as 2^kWScaleLog2 * W (common.cuh).
+// `f16scale`: fp16x2 operand planes carry a power-of-two scale (common.cuh: weights
+// 2^kWScaleLog2, h 2^kHScaleLog2, x 2^kXScaleLog2); other formats ignore it.
 __device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long long idx, float v,
-                                             bool wscale = false) {
+                                             float f16scale = 1.0f) {
   if (prec == kBF16) {
     static_cast<__nv_bfloat16*>(p0)[idx] = __float2bfloat16_rn(v);
   } else if (prec == kF16x2) {
     __half hi, lo;
-    f16x2_split(wscale ? v * (float)(1 << kWScaleLog2) : v, hi, lo);
+    f16x2_split(v * f16scale, hi, lo);
     static_cast<__half*>(p0)[idx] = hi;
     static_cast<__half*>(p1)[idx] = lo;
   } else {
@@ -58,7 +59,7 @@ __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__
   for (int r = ty; r < 32; r += 8) {
     for (int kk = tx; kk < 64; kk += 32) {
       const int k = k0 + kk;
-      if (k < K) store_planes(prec, p0, p1, (long long)(rho0 + r) * K + k, tile[kk][r], true);
+      if (k < K) store_planes(prec, p0, p1, (long long)(rho0 + r) * K + k, tile[kk][r], pow2f(kWScaleLog2));
     }
   }
 }
@@ -79,7 +80,7 @@ __global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict
     const int g = rho_gate(rho), up = rho_unit(rho);
     float v = 0.0f;
     if (u < H && up < H) v = M[(long long)u * 4 * H + (long long)g * H + up];
-    store_planes(prec, p0, p1, e, v, true);
+    store_planes(prec, p0, p1, e, v, pow2f(kWScaleLog2));
   }
 }
 
@@ -95,7 +96,7 @@ __global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, i
     const int g = rho_gate(rho), u = rho_unit(rho);
     float v = 0.0f;
     if (i < I && u < H) v = W0[(long long)i * 4 * H + (long long)g * H + u];
-    store_planes(prec, p0, p1, e, v, true);
+    store_planes(prec, p0, p1, e, v, pow2f(kWScaleLog2));
   }
 }
 
@@ -108,11 +109,14 @@ __global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* d
 }
 
 // Column-block padding: src is R x (nblk*B) column-major, dst is Rp x (nblk*Bp) starting at
-// column dst_col_off. Writes an fp32 copy and/or operand planes.
+// column dst_col_off. Writes an fp32 copy and/or operand planes (fp16x2: scaled by f16scale).
+// `amax` (optional): max |src| over the launch (float bits), the range check of scaled planes.
 __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk, int Rp, int Bp,
-                           long long dst_col_off, float* dst_f32, int prec, void* p0, void* p1) {
+                           long long dst_col_off, float* dst_f32, int prec, void* p0, void* p1,
+                           float f16scale = 1.0f, unsigned* amax = nullptr) {
   // one column per block iteration, rows across threads: no per-element 64-bit division
   const int ncols = Bp * nblk;
+  float mx = 0.0f;
   for (int col = blockIdx.x; col < ncols; col += gridDim.x) {
     const int t = col / Bp, b = col - t * Bp;
     const bool live = src && b < B;
@@ -120,9 +124,15 @@ __global__ void k_pad_cols(const float* __restrict__ src, int R, int B, int nblk
     const long long d0 = (dst_col_off + col) * (long long)Rp;
     for (int r = threadIdx.x; r < Rp; r += blockDim.x) {
       const float v = (live && r < R) ? sc[r] : 0.0f;
+      mx = fmaxf(mx, fabsf(v));
       if (dst_f32) dst_f32[d0 + r] = v;
-      if (p0) store_planes(prec, p0, p1, d0 + r, v);
+      if (p0) store_planes(prec, p0, p1, d0 + r, v, f16scale);
     }
+  }
+  if (amax) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.0f) atomicMax(amax, __float_as_uint(mx));
   }
 }
 

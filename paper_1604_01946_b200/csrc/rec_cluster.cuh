@@ -78,6 +78,7 @@ struct ClOff {
   const uint32_t* consumed;
   int sys;
   int active;
+  float unscale;             // fp16x2: 2^-(weight scale + operand scale) of this group's product
   const uint16_t* alo;       // fp16x2: lo plane of the target layer's weights (FwdLayer::alo)
   int alo_ld, alo_rows;
 };
@@ -99,6 +100,9 @@ struct ClParams {
   unsigned long long* trace;  // [cta][steps][8] (RW_TRACE)
   int trace_steps;
   int dir;    // 0 forward, 1 backward (error codes)
+  float unscale;  // critical groups, fp16x2: 2^-(kWScaleLog2 + kHScaleLog2) forward (R.h),
+                  // 2^-(kWScaleLog2 + kGScaleLog2) backward (R^T.dG); off groups: ClOff::unscale
+  unsigned* gmax; // backward: max |dG| of the pass (float bits; range check of the scaled dG planes)
   int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
               // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered,
@@ -155,26 +159,6 @@ __device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
   s.alo_full = s.a_full + 9;
   s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 10);
   return s;
-}
-
-__global__ void k_epoch_inc(uint32_t* e) { *e += 1; }
-// Layer pipeline: tell the next stage (system scope, its memory) that this forward's layer-input
-// copy landed; the next stage waits for its own forward epoch before its weight-gradient GEMMs.
-__global__ void k_pp_signal(uint32_t* peer_ready, const uint32_t* my_epoch) {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer_ready), "r"(*my_epoch) : "memory");
-}
-__global__ void k_pp_wait(const uint32_t* ready, const uint32_t* my_epoch, int* error, unsigned long long timeout_ns) {
-  const uint32_t e = *my_epoch;
-  const uint64_t t0 = globaltimer();
-  uint32_t v;
-  do {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
-    if (globaltimer() - t0 > timeout_ns) {
-      atomicCAS(error, 0, (1 << 30) | (4 << 26));
-      return;
-    }
-  } while (!flag_reached(v, e));
 }
 
 __device__ __forceinline__ void cl_trace(const ClParams& p, int it, int what) {
@@ -415,7 +399,7 @@ __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, i
 template <class P, int kChunks>
 __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, bool two, int N, int it, int m,
                                           int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8],
-                                          const ClParams* tp = nullptr) {
+                                          float unscale, const ClParams* tp = nullptr) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const uint32_t taddr = tacc + (uint32_t(q * 32) << 16);
@@ -499,9 +483,8 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
     }
   }
   if constexpr (P::kPlanes == 2) {
-    constexpr float kUnscale = 1.0f / (float)(1 << kWScaleLog2);
 #pragma unroll
-    for (int i = 0; i < kChunks * 8; ++i) v_out[i] *= kUnscale;
+    for (int i = 0; i < kChunks * 8; ++i) v_out[i] *= unscale;
   }
 }
 
@@ -529,11 +512,11 @@ __device__ __forceinline__ void cl_rx_next(const ClSmem& S, int m, int n_act, in
 template <class P, int kChunks>
 __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, uint32_t tacc, bool two, int it,
                                             int m, int n_act, int nco, uint32_t& rxc, float* ring, uint32_t* done,
-                                            const uint32_t* consumed, bool sys, uint32_t epoch) {
+                                            const uint32_t* consumed, bool sys, uint32_t epoch, float unscale) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<P, kChunks>(S, tacc, true, two, p.Bp, it, m, n_act, nco, rxc, v);
+  cl_reduce<P, kChunks>(S, tacc, true, two, p.Bp, it, m, n_act, nco, rxc, v, unscale);
   named_bar_sync(1, kEpiThreads);
   if (et == 0) {
     cl_rx_next(S, m, n_act, nco);
@@ -556,7 +539,7 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
 template <class P, int kChunks>
 __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, uint32_t tmem_base, bool two,
                                             int n_it, int m, int n_act, float* ring, uint32_t* done,
-                                            const uint32_t* consumed, bool sys, uint32_t epoch) {
+                                            const uint32_t* consumed, bool sys, uint32_t epoch, float unscale) {
   const int et = threadIdx.x - kEpiBase, N = p.Bp, nco = N / n_act;
   uint32_t rxc = 0;
   if (et == 0 && n_act > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(n_act - 1) * nco * kTileM * 4);
@@ -565,7 +548,7 @@ __device__ __forceinline__ void cl_off_loop(const ClSmem& S, const ClParams& p, 
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     cl_off_step<P, kChunks>(S, p, tmem_base + (it & 1) * 2 * N, two, it, m, n_act, nco, rxc, ring, done, consumed,
-                            sys, epoch);
+                            sys, epoch, unscale);
     if (et == 0) cl_trace(p, it, 3);
   }
 }
@@ -588,11 +571,11 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
 template <class P, int kChunks>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
-                                           int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp) {
+                                           int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp, float unscale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<P, kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v);
+  cl_reduce<P, kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v, unscale);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 9);
   mbar_wait(S.off_full, offc & 1);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 10);
@@ -729,10 +712,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     }
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
-        default: cl_off_loop<P, 1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        default: cl_off_loop<P, 1>(S, p, tmem_base, two, p.T, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
       }
     } else {
       // ================= critical epilogue: reduce + LSTM cell (cells.hpp:227-260)
@@ -762,7 +745,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
         const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
-        cl_fwd_sum<P, kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p);
+        cl_fwd_sum<P, kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p, p.unscale);
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
@@ -792,9 +775,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tcv[k] = act_tanh<P>(cv[k]);
           hv[k] = ov[k] * tcv[k];
           creg[k] = cv[k];
-          if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block
+          if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block (scaled, common.cuh)
             __half hh, hl;
-            f16x2_split(hv[k], hh, hl);
+            f16x2_split(hv[k] * pow2f(kHScaleLog2), hh, hl);
             *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
             *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
           } else if (staged) {
@@ -830,7 +813,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const long long col_prev = colp + cl, col_new = col_prev + N;
           Le.c[col_new * Hp + u] = cv[k];
           Le.h[col_new * Hp + u] = hv[k];
-          store_operand<P>(Le.hop, col_new * Hp + u, hv[k]);
+          store_operand<P>(Le.hop, col_new * Hp + u, P::kPlanes == 2 ? hv[k] * pow2f(kHScaleLog2) : hv[k]);
           if (Le.gates) {
             float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv[k];
@@ -868,6 +851,9 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i) carry[i] = 0.0f;
   float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
+  // fp16x2: the dG operand planes carry 2^kGScaleLog2 (common.cuh); the fp32 tapes do not
+  constexpr float kGS = P::kPlanes == 2 ? pow2f(kGScaleLog2) : 1.0f;
+  float gmax = 0.0f;
   uint32_t rxc = 0, offc = 0;
   // dG_t staging in the B ring (idle between this step's MMA and the next step's loads, which
   // wait for this CTA's own publish): the tile's 8 k-blocks x nco rows of the swizzled image
@@ -915,7 +901,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     float acc[kChunks * 8];
-    cl_reduce<P, kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, &p);
+    cl_reduce<P, kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, p.unscale, &p);
     if (et == 0) cl_trace(p, it, 12);
     float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
@@ -977,7 +963,8 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
             const uint32_t so = ((((kk >> 3) & 7) ^ (n & 7)) << 4) + (kk & 7) * 2;
             if constexpr (P::kPlanes == 2) {
               __half hh, hl;
-              f16x2_split(gv, hh, hl);
+              gmax = fmaxf(gmax, fabsf(gv));
+              f16x2_split(gv * kGS, hh, hl);
               const uint32_t r0 = ((kk >> 6) * 2) * nco + nl;
               asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + r0 * 128 + so), "h"(__half_as_ushort(hh)));
               asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + (r0 + nco) * 128 + so), "h"(__half_as_ushort(hl)));
@@ -993,7 +980,8 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
             const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
             if constexpr (P::kPlanes == 2) {
               __half hh, hl;
-              f16x2_split(gv, hh, hl);
+              gmax = fmaxf(gmax, fabsf(gv));
+              f16x2_split(gv * kGS, hh, hl);
               *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), n, BR)) = hh;
               *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), N + n, BR)) = hl;
             } else {
@@ -1029,10 +1017,10 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 #pragma unroll
       for (int k = 0; k < kChunks * 8; ++k) {
         const long long ob = ((long long)t * N + cbase + k) * G4;
-        store_operand<P>(Ly.dgop, ob + rho_of(0, u), g_i[k]);
-        store_operand<P>(Ly.dgop, ob + rho_of(1, u), g_f[k]);
-        store_operand<P>(Ly.dgop, ob + rho_of(2, u), g_o[k]);
-        store_operand<P>(Ly.dgop, ob + rho_of(3, u), g_c[k]);
+        store_operand<P>(Ly.dgop, ob + rho_of(0, u), g_i[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rho_of(1, u), g_f[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rho_of(2, u), g_o[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rho_of(3, u), g_c[k] * kGS);
         float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
         dgp[0] = g_i[k];
         dgp[Hp] = g_f[k];
@@ -1045,6 +1033,12 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       }
     }
     if (et == 0) cl_trace(p, it, 6);
+  }
+  if constexpr (P::kPlanes == 2) {
+    // range of the scaled dG planes: one atomic per warp (positive floats order as integers)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+    if (lane == 0 && p.gmax) atomicMax(p.gmax, __float_as_uint(gmax));
   }
   if (uok && Ly.dbp) {
     float* d = Ly.dbp + (long long)(m * 2 + half) * G4 + u;
@@ -1177,10 +1171,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     }
     if (!crit) {
       switch (nco >> 4) {
-        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
-        default: cl_off_loop<P, 1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch); break;
+        case 4: cl_off_loop<P, 4>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        case 3: cl_off_loop<P, 3>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        case 2: cl_off_loop<P, 2>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
+        default: cl_off_loop<P, 1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
       }
     } else {
       cl_bwd_crit<P, kCC>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);

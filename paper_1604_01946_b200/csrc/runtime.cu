@@ -24,7 +24,9 @@
 #include "gemm_tc.cuh"
 #include "layout_kernels.cuh"
 #include "lstm_step.cuh"
+#include "kernel_ptrs.h"
 #include "rec_cluster.cuh"
+#include "sync_kernels.cuh"
 
 using namespace rw;
 
@@ -188,8 +190,8 @@ struct ClPlan {
 
 template <class P>
 struct KernelSet {
-  static void* fwd() { return (void*)k_lstm_fwd<P>; }
-  static void* bwd() { return (void*)k_lstm_bwd<P>; }
+  static void* fwd() { return lstm_kernel_ptr(P::kTF32 ? kTF32x3 : kBF16, true, false); }
+  static void* bwd() { return lstm_kernel_ptr(P::kTF32 ? kTF32x3 : kBF16, false, false); }
 };
 
 // Calls f(PrecX{}) for the context's operand format.
@@ -420,18 +422,7 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
 // cluster (ko_l members per layer), each member holding <= 512 K of its weight slice. Returns
 // false when the shape does not fit (batch > 64, owned columns not a multiple of 16, too many
 // CTAs, shared memory, or clusters not co-resident).
-template <class P>
-void* cl_kernel_p(bool fwd, int nco) {
-  switch (nco >> 4) {
-    case 4: return fwd ? (void*)k_cl_fwd<P, 4> : (void*)k_cl_bwd<P, 4>;
-    case 3: return fwd ? (void*)k_cl_fwd<P, 3> : (void*)k_cl_bwd<P, 3>;
-    case 2: return fwd ? (void*)k_cl_fwd<P, 2> : (void*)k_cl_bwd<P, 2>;
-    default: return fwd ? (void*)k_cl_fwd<P, 1> : (void*)k_cl_bwd<P, 1>;
-  }
-}
-void* cl_kernel(int prec, bool fwd, int nco) {
-  return prec == kF16x2 ? cl_kernel_p<PrecF16x2>(fwd, nco) : cl_kernel_p<PrecBF16>(fwd, nco);
-}
+void* cl_kernel(int prec, bool fwd, int nco) { return cl_kernel_ptr(prec, fwd, nco); }
 
 // prec: kBF16 or kF16x2 (two operand planes per stage; A_lo in tensor memory next to the
 // 4 x Bp accumulator columns, which fits 512 columns for Bp <= 64 and <= 8 k-blocks per member)
@@ -504,11 +495,12 @@ void launch_gemm_p(const GemmDesc* table_dev, int count, int M, int N, cudaStrea
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long tiles = (long long)count * mt * nt;
   const int grid = (int)std::min<long long>(tiles, sms);
-  auto k = k_gemm_p<AMN, BMN, BN>;
+  void* k = gemm_p_ptr(AMN, BMN, BN);
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ++g_launches;
-  k<<<grid, 256, smem, s>>>(table_dev, count, mt, nt, stages);
-  RW_CUDA(cudaGetLastError());
+  void* args[5] = {const_cast<GemmDesc**>(&table_dev), &count, const_cast<int*>(&mt), const_cast<int*>(&nt),
+                   &stages};
+  RW_CUDA(cudaLaunchKernel(k, dim3(grid), dim3(256), args, smem, s));
 }
 
 template <bool AMN, bool BMN, int BN>
@@ -523,7 +515,7 @@ void launch_gemm_p2(const GemmDesc* table_dev, int count, int M, int N, cudaStre
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long tiles = (long long)count * mt * nt;
   const int pairs = (int)std::min<long long>(tiles, sms / 2);
-  auto k = k_gemm_p2<AMN, BMN, BN>;
+  void* k = gemm_p2_ptr(AMN, BMN, BN);
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(2 * pairs, 1, 1);
@@ -538,7 +530,9 @@ void launch_gemm_p2(const GemmDesc* table_dev, int count, int M, int N, cudaStre
   lc.attrs = at;
   lc.numAttrs = 1;
   ++g_launches;
-  RW_CUDA(cudaLaunchKernelEx(&lc, k, table_dev, count, mt, nt, stages));
+  void* args[5] = {const_cast<GemmDesc**>(&table_dev), &count, const_cast<int*>(&mt), const_cast<int*>(&nt),
+                   &stages};
+  RW_CUDA(cudaLaunchKernelExC(&lc, k, args));
 }
 
 template <class P, bool AMN, bool BMN>
@@ -571,16 +565,13 @@ void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int
   const size_t smem = gemm_smem(P::kPlanes, bn, stages);
   dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
   ++g_launches;
-  if (P::kPlanes == 2 && bn == 64) {
-    auto k = k_gemm_tc<P, AMN, BMN, 64>;
-    RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, P::kTF32 ? kPromoteKB : kPromoteKB16);
-  } else {
-    auto k = k_gemm_tc<P, AMN, BMN, 0>;
-    RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, s>>>(table_dev, bn, stages, 0);
-  }
-  RW_CUDA(cudaGetLastError());
+  const int prec = P::kPlanes == 1 ? kBF16 : P::kTF32 ? kTF32x3 : kF16x2;
+  const bool b64 = P::kPlanes == 2 && bn == 64;
+  void* k = gemm_tc_ptr(prec, AMN, BMN, b64 ? 64 : 0);
+  int promote = b64 ? (P::kTF32 ? kPromoteKB : kPromoteKB16) : 0;
+  RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[4] = {const_cast<GemmDesc**>(&table_dev), &bn, &stages, &promote};
+  RW_CUDA(cudaLaunchKernel(k, grid, dim3(256), args, smem, s));
 }
 
 int gemm_stages(int planes, int bn) {
@@ -734,7 +725,7 @@ void build(rw_ctx* x) {
   x->y_raw.alloc((size_t)std::max(4LL * H, (long long)std::max(H, I)) * B * (T + 1) * 4);
   x->flags_f.alloc((size_t)L * T * 4);
   x->flags_b.alloc((size_t)L * T * 4);
-  x->errflag.alloc(16);
+  x->errflag.alloc(32);  // [code, count, max|dG|, max|x|, max|h0|]
 
   // ---- schedules
   const bool f16x2 = x->prec == kF16x2;  // cluster kernels only (no persistent / stepwise variant)
@@ -791,7 +782,7 @@ void build(rw_ctx* x) {
     int st = 8;
     size_t sm = rec_smem_bytes(1, st, Bp / 2, st);
     while (sm > (size_t)kSmemLimit && st > 2) sm = rec_smem_bytes(1, --st, Bp / 2, st);
-    void* kp = (void*)k_lstm_fwd<PrecBF16, true>;
+    void* kp = lstm_kernel_ptr(kBF16, true, true);
     if (sm > (size_t)kSmemLimit ||
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
       cudaGetLastError();
@@ -811,7 +802,7 @@ void build(rw_ctx* x) {
     size_t sm = rec_smem_bytes(1, st, Bp / 2, st);
     while (sm > (size_t)kSmemLimit && st > 2) sm = rec_smem_bytes(1, --st, Bp / 2, st);
     sm = std::max(sm, (size_t)116 * 1024);
-    void* kp = (void*)k_lstm_bwd<PrecBF16, true>;
+    void* kp = lstm_kernel_ptr(kBF16, false, true);
     const int ctas = tiles_b * L;
     if (sm > (size_t)kSmemLimit ||
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
@@ -1020,6 +1011,8 @@ void build(rw_ctx* x) {
         o.done = x->ring_f_h[l].done;
         o.consumed = x->ring_f_h[l].consumed;
         o.active = 1;
+        // W.x (layer 0) or W.h_{l-1}: operand scales of the fp16x2 planes (common.cuh)
+        o.unscale = x->prec == kF16x2 ? pow2f(-(kWScaleLog2 + (l == 0 ? kXScaleLog2 : kHScaleLog2))) : 1.0f;
         o.alo = fl[l].alo;
         o.alo_ld = fl[l].alo_ld;
         o.alo_rows = fl[l].alo_rows;
@@ -1043,6 +1036,7 @@ void build(rw_ctx* x) {
         o.done = x->ring_b_h[l].done;
         o.consumed = x->ring_b_h[l].consumed;
         o.active = 1;
+        o.unscale = x->prec == kF16x2 ? pow2f(-(kWScaleLog2 + kGScaleLog2)) : 1.0f;  // W_{l+1}^T.dG
         o.alo = bl[l].alo;
         o.alo_ld = bl[l].alo_ld;
         o.alo_rows = bl[l].alo_rows;
@@ -1074,6 +1068,8 @@ void build(rw_ctx* x) {
     d.b_k_off = l == 0 ? 0 : Bp;  // X_l = h_{l-1} blocks 1..T
     d.d = x->dW[l].f();
     d.ldd = 4LL * H;
+    // fp16x2: dG planes carry 2^kGScaleLog2, x 2^kXScaleLog2, h 2^kHScaleLog2 (common.cuh)
+    d.alpha = x->prec == kF16x2 ? pow2f(-(kGScaleLog2 + (l == 0 ? kXScaleLog2 : kHScaleLog2))) : 1.0f;
     d.row_mode = kRowGateUnperm;
     d.col_mode = kColIdentity;
     d.H = H;
@@ -1088,6 +1084,7 @@ void build(rw_ctx* x) {
       r.b[p] = kmajor_wg ? mp(m_hT[2 * l + (p % x->planes)], p) : mp(m_hopMN[2 * l + (p % x->planes)], p);
     r.N = Hp;
     r.b_k_off = 0;  // Hprev = blocks 0..T-1
+    r.alpha = x->prec == kF16x2 ? pow2f(-(kGScaleLog2 + kHScaleLog2)) : 1.0f;
     r.d = x->dR[l].f();
     r.n_valid = H;
     wg.push_back(r);
@@ -1163,7 +1160,8 @@ void build(rw_ctx* x) {
   dx.B = B;
   dx.Bp = Bp;
   dx.m_valid = I;
-  dx.alpha = f16x2 ? 1.0f / (float)(1 << kWScaleLog2) : 1.0f;  // W_0^T planes carry 2^kWScaleLog2
+  // W_0^T planes carry 2^kWScaleLog2, the dG planes 2^kGScaleLog2
+  dx.alpha = f16x2 ? 1.0f / (float)(1 << (kWScaleLog2 + kGScaleLog2)) : 1.0f;
   dx.n_valid = (int)colsT;
   x->gemm_dx.alloc(sizeof(GemmDesc));
   RW_CUDA(cudaMemcpy(x->gemm_dx.p, &dx, sizeof(GemmDesc), cudaMemcpyHostToDevice));
@@ -1295,6 +1293,9 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
 void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const float* c0_dev, bool state = true,
                       bool inputs = true) {
   const int L = x->L, H = x->H, B = x->B, Hp = x->Hp, Bp = x->Bp;
+  // range records of the fp16x2 planes written below (max|x|, max|h0|; check_error_flag)
+  if (x->prec == kF16x2 && (inputs || state))
+    RW_CUDA(cudaMemsetAsync(static_cast<unsigned*>(x->errflag.p) + (inputs ? 3 : 4), 0, inputs && state ? 8 : 4, s));
   // cluster schedule (bf16): the plain operand and its swizzled image in one pass
   const bool fused_x = inputs && !x->pp_prev && x->fwd_sched == RW_SCHED_CLUSTER && x->prec == kBF16 &&
                        x->Ip % 8 == 0;
@@ -1306,14 +1307,16 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   } else if (inputs && !x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
-        x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1));
+        x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, 0, nullptr, x->prec, x->x_op.p(0), x->x_op.p(1),
+        pow2f(kXScaleLog2), static_cast<unsigned*>(x->errflag.p) + 3);
   }
   for (int l = 0; l < L && state; ++l) {
     const float* h0 = h0_dev ? h0_dev + (size_t)l * H * B : nullptr;
     const float* c0 = c0_dev ? c0_dev + (size_t)l * H * B : nullptr;
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(h0, H, B, 1, Hp, Bp, 0, x->h[l].f(), x->prec,
-                                                           x->hop[l].p(0), x->hop[l].p(1));
+                                                           x->hop[l].p(0), x->hop[l].p(1), pow2f(kHScaleLog2),
+                                                           static_cast<unsigned*>(x->errflag.p) + 4);
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)Hp * Bp), 256, 0, s>>>(c0, H, B, 1, Hp, Bp, 0, x->c[l].f(), x->prec,
                                                            nullptr, nullptr);
@@ -1361,6 +1364,9 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.trace_steps = fwd ? x->T : x->T + 1;
   if (const char* e = getenv("RW_CL_DEBUG")) p.debug = atoi(e);
   p.dir = fwd ? 0 : 1;
+  p.unscale = 1.0f;
+  if (x->prec == kF16x2) p.unscale = pow2f(-(kWScaleLog2 + (fwd ? kHScaleLog2 : kGScaleLog2)));
+  p.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
   return p;
 }
 
@@ -1369,7 +1375,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
 void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams& p, int rows, size_t smem,
                     cudaStream_t s, bool fwd) {
   ++g_launches;
-  k_epoch_inc<<<1, 1, 0, s>>>(static_cast<uint32_t*>(x->cl_epoch.p) + (fwd ? 0 : 1));
+  k_epoch_inc<<<1, 1, 0, s>>>(static_cast<uint32_t*>(x->cl_epoch.p) + (fwd ? 0 : 1), p.gmax);
   RW_CUDA(cudaGetLastError());
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(p.tiles * 2 * p.cs, rows, 1);
@@ -1446,7 +1452,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     return;
   }
   // stepwise wavefront: layer l on stream ls[l]; step (l,t) waits for (l-1,t)
-  if (x->pair_f) kern = (void*)k_lstm_fwd<PrecBF16, true>;
+  if (x->pair_f) kern = lstm_kernel_ptr(kBF16, true, true);
   rp.persistent = 0;
   rp.resident = 0;
   rp.n_steps = 1;
@@ -1503,7 +1509,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     rp.t_first = x->T - 1;
     rp.n_steps = x->T + 1;  // T steps + the dh0 step
     if (x->pair_b)
-      launch_rec<P>((void*)k_lstm_bwd<PrecBF16, true>, x->bwd_layers.p, rp, rp.tiles, x->L, x->smem_b, s, 2);
+      launch_rec<P>(lstm_kernel_ptr(kBF16, false, true), x->bwd_layers.p, rp, rp.tiles, x->L, x->smem_b, s, 2);
     else
       launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, x->L, x->smem_b, s);
     return;
@@ -1651,8 +1657,26 @@ void enqueue_pass(rw_ctx* x, int pass, cudaStream_t s) {
 }
 
 void check_error_flag(rw_ctx* x) {
-  int e[2] = {0, 0};
+  int e[5] = {0, 0, 0, 0, 0};
   RW_CUDA(cudaMemcpy(e, x->errflag.p, sizeof e, cudaMemcpyDeviceToHost));
+  if (x->prec == kF16x2) {
+    // fp16x2 operand range: the scaled planes must stay below fp16's 65504 (common.cuh)
+    const char* what[3] = {"a gate gradient dG", "an input x element", "an initial state h0 element"};
+    const int sc[3] = {kGScaleLog2, kXScaleLog2, kHScaleLog2};
+    for (int i = 0; i < 3; ++i) {
+      float v;
+      std::memcpy(&v, &e[2 + i], 4);
+      if (!(v * pow2f(sc[i]) < 65504.0f)) {
+        cudaMemset(static_cast<int*>(x->errflag.p) + 2 + i, 0, 4);
+        char b[256];
+        snprintf(b, sizeof b,
+                 "fp32-parity mode: %s of magnitude %g exceeds the fp16x2 operand range (< %g); results of "
+                 "this pass are invalid",
+                 what[i], v, 65504.0 / pow2f(sc[i]));
+        throw RwError{RW_ESTATE, b};
+      }
+    }
+  }
   if (e[0]) {
     cudaMemset(x->errflag.p, 0, sizeof e);
     char b[256];
@@ -2021,6 +2045,13 @@ int rw_run_pass(rw_ctx* x, int pass, void* stream) {
   });
 }
 
+int rw_params_updated(rw_ctx* x) {
+  return guarded(x, [&] {
+    require_params(x);
+    x->dirty = true;
+  });
+}
+
 int rw_read_outputs(rw_ctx* x, float* y, float* dx0, float* const* dW, float* const* dR,
                     float* const* db) {
   return guarded(x, [&] {
@@ -2136,6 +2167,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.consumed = static_cast<const uint32_t*>(open_region(x, peer, 2));
     o.sys = 1;
     o.active = 1;
+    o.unscale = 1.0f;  // bf16 only (above)
     if (dir == 0) {
       if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
       DevBuf wn;

@@ -478,6 +478,10 @@ class Engine:
     def run_pass(self, kind: int, stream: int | None = None) -> None:
         self._check(self._L.rw_run_pass(self._ctx, kind, C.c_void_p(stream or 0)))
 
+    def params_updated(self) -> None:
+        """The device parameters changed in place: the next pass repacks them (K7)."""
+        self._check(self._L.rw_params_updated(self._ctx))
+
     def sync(self) -> None:
         self._check(self._L.rw_sync(self._ctx))
 
