@@ -17,7 +17,9 @@
 // Link with -L<repo>/paper_1604_01946_b200/lib -lrnnwave_sm100.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <iterator>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -28,23 +30,13 @@
 
 #include "rnnwave/cells.hpp"
 #include "rnnwave/config.hpp"
+#include "rnnwave/gemm.hpp"
 #include "rnnwave/matrix.hpp"
 #include "rnnwave/params.hpp"
+#include "rnnwave/trace.hpp"
 #include "rnnwave_sm100.h"
 
 namespace rnnwave {
-
-namespace sched {
-// The reference records a CPU task trace (scheduler.hpp:180-191). The device wavefront is
-// traced by CUDA events / ncu instead; the sink is accepted for source compatibility.
-struct TraceRecord {
-  int layer = 0, block = 0, phase = 0, worker = 0;
-  std::int64_t start_ns = 0, end_ns = 0;
-};
-struct ScheduleTrace {
-  std::vector<TraceRecord> records;
-};
-}  // namespace sched
 
 namespace detail {
 
@@ -56,7 +48,8 @@ namespace detail {
 // Owns the device context; shared by the Engine and every tape/state it hands out.
 struct DeviceHandle {
   rw_ctx* ctx = nullptr;
-  std::uint64_t bwd_tape = 0;
+  std::uint64_t fwd_tape = 0;  // the forward tape the device holds (rw_forward's id)
+  std::uint64_t bwd_tape = 0;  // the tape whose backward state (dG) the device holds
   ~DeviceHandle() {
     if (ctx) rw_destroy(ctx);
   }
@@ -65,7 +58,10 @@ struct DeviceHandle {
   }
 };
 
-// Per-layer tape tensor sequence, materialised from HBM on first access.
+// Per-layer tape tensor sequence, materialised from HBM on first access. Like the reference's
+// std::vector<Matrix> fields it is indexable and iterable (range-for). A field first read after
+// the device moved on to a newer tape throws "stale tape" (the reference's value-type tapes keep
+// their data; here the data lives on the device until the next forward / backward).
 class TapeSeq {
  public:
   TapeSeq() = default;
@@ -76,15 +72,48 @@ class TapeSeq {
   const Matrix& operator[](std::size_t l) const {
     if (l >= cache_.size()) throw std::out_of_range("tape: layer index out of range");
     if (!cache_[l]) {
+      const std::uint64_t held = which_ == RW_TAPE_DGW ? h_->bwd_tape : h_->fwd_tape;
+      if (held != id_)
+        throw std::invalid_argument("engine: stale tape, the device no longer holds tape " + std::to_string(id_));
       Matrix m(rows_, cols_);
       h_->check(rw_get_tape(h_->ctx, which_, int(l), m.data()));
       cache_[l] = std::move(m);
     }
     return *cache_[l];
   }
+  const Matrix& at(std::size_t l) const { return (*this)[l]; }
   const Matrix& back() const { return (*this)[cache_.size() - 1]; }
   const Matrix& front() const { return (*this)[0]; }
   std::uint64_t id() const { return id_; }
+
+  class const_iterator {
+   public:
+    using value_type = Matrix;
+    using reference = const Matrix&;
+    using pointer = const Matrix*;
+    using difference_type = std::ptrdiff_t;
+    using iterator_category = std::forward_iterator_tag;
+    const_iterator(const TapeSeq* s, std::size_t i) : s_(s), i_(i) {}
+    reference operator*() const { return (*s_)[i_]; }
+    pointer operator->() const { return &(*s_)[i_]; }
+    const_iterator& operator++() {
+      ++i_;
+      return *this;
+    }
+    const_iterator operator++(int) {
+      const_iterator o = *this;
+      ++i_;
+      return o;
+    }
+    bool operator==(const const_iterator& o) const { return s_ == o.s_ && i_ == o.i_; }
+    bool operator!=(const const_iterator& o) const { return !(*this == o); }
+
+   private:
+    const TapeSeq* s_;
+    std::size_t i_;
+  };
+  const_iterator begin() const { return const_iterator(this, 0); }
+  const_iterator end() const { return const_iterator(this, cache_.size()); }
 
  private:
   std::shared_ptr<DeviceHandle> h_;
@@ -160,7 +189,12 @@ class Engine {
   }
 
   const LadderConfig& config() const { return cfg_; }
-  void set_trace_sink(sched::ScheduleTrace* sink) { trace_sink_ = sink; }
+  // engine.hpp:79-80: when set, every forward / backward_data deposits its schedule trace here
+  // (the device's per-step tasks, build_graph(L, T, 1) ids; rw_trace_records).
+  void set_trace_sink(sched::ScheduleTrace* sink) {
+    trace_sink_ = sink;
+    dev_->check(rw_trace_enable(dev_->ctx, sink ? 1 : 0));
+  }
 
   ForwardResult forward(std::vector<LayerParams>& params, const Matrix& x, bool training,
                         const std::vector<Matrix>* h0 = nullptr,
@@ -188,6 +222,8 @@ class Engine {
     std::uint64_t id = 0;
     dev_->check(rw_forward(dev_->ctx, x.data(), training ? 1 : 0, h0 ? ph0.data() : nullptr,
                            c0 ? pc0.data() : nullptr, res.y.data(), &id));
+    dev_->fwd_tape = id;
+    deposit_trace(0);
     ForwardTape& t = res.tape;
     t.cfg = cfg_;
     t.training = training;
@@ -226,6 +262,8 @@ class Engine {
       pdc.push_back(s.dc0[l].data());
     }
     dev_->check(rw_backward_data(dev_->ctx, tape.id, dy.data(), s.dx0.data(), pdh.data(), pdc.data()));
+    dev_->bwd_tape = tape.id;
+    deposit_trace(1);
     s.dgw_seq = detail::TapeSeq(dev_, tape.id, RW_TAPE_DGW, cfg_.layers, 4 * cfg_.hidden, bt);
     s.id = tape.id;
     return s;
@@ -253,6 +291,27 @@ class Engine {
   }
 
  private:
+  void deposit_trace(int direction) {
+    if (!trace_sink_) return;
+    int n = 0;
+    dev_->check(rw_trace_records(dev_->ctx, direction, nullptr, 0, &n));
+    std::vector<rw_trace_record> r(static_cast<std::size_t>(n));
+    dev_->check(rw_trace_records(dev_->ctx, direction, r.data(), n, &n));
+    trace_sink_->clear();
+    for (const rw_trace_record& t : r) {
+      sched::TraceRecord o;
+      o.task_id = t.task_id;
+      o.layer = t.layer;
+      o.block = t.block;
+      o.step_k = t.step_k;
+      o.phase = t.phase == 0 ? sched::TaskPhase::InputGemm : sched::TaskPhase::RecurrentStep;
+      o.worker = t.worker;
+      o.start_ns = t.start_ns;
+      o.end_ns = t.end_ns;
+      trace_sink_->push_back(o);
+    }
+  }
+
   void upload(const std::vector<LayerParams>& params) {
     if (int(params.size()) != cfg_.layers)
       throw std::invalid_argument("engine: expected " + std::to_string(cfg_.layers) +

@@ -218,6 +218,26 @@ int rw_pp_export(rw_ctx* ctx, int dir, rw_pp_ring* out);
 int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
+/* gemm (gemm.hpp:339-347, the reference's ordered fp32 GEMM) on the device: C (M x N) =
+ * alpha op(A) op(B) + beta C, host column-major buffers, op(X) = X^T when trans_x; 3xTF32 split
+ * operands on the tcgen05 tensor cores (fp32-parity, not bitwise equal to the CPU chain).
+ * Synchronous. */
+int rw_gemm(int trans_a, int trans_b, int M, int N, int K, float alpha, const float* A, long long lda,
+            const float* B, long long ldb, float beta, float* C, long long ldc);
+
+/* ---- schedule trace (Engine::set_trace_sink, engine.hpp:79-80; sched::TraceRecord,
+ * scheduler.hpp:180-192). rw_trace_enable(ctx, 1) makes the recurrent kernels record
+ * %globaltimer stamps; rw_trace_records returns the last pass's tasks of one direction (0
+ * forward, 1 backward) in the reference's task model with block width 1: task ids of
+ * build_graph(L, T, 1), phase 0 = INPUT_GEMM, 1 = RECURRENT_STEP, ns relative to the first
+ * record. *count receives the number of records (copies at most `capacity`). */
+typedef struct rw_trace_record {
+  int32_t task_id, layer, block, step_k, phase, worker;
+  int64_t start_ns, end_ns;
+} rw_trace_record;
+int rw_trace_enable(rw_ctx* ctx, int on);
+int rw_trace_records(rw_ctx* ctx, int direction, rw_trace_record* out, int capacity, int* count);
+
 int64_t rw_flop_count_cell(int hidden, int input, int batch);
 
 /* ---- unit-test hook: one tcgen05 GEMM on device pointers ----

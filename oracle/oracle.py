@@ -247,14 +247,15 @@ class Reference:
         H, B, T, G, L = cfg.hidden, cfg.batch, cfg.steps, 4 * cfg.hidden, cfg.layers
         training = training or dy is not None
         out = {"y": fmat(H, B * T)}
+        # tapes: True = every tape, "states" = h_seq / c_seq only (full-size parity runs)
         if tapes:
             out["h_seq"] = [fmat(H, B * (T + 1)) for _ in range(L)]
             out["c_seq"] = [fmat(H, B * (T + 1)) for _ in range(L)]
-            if training:
+            if training and tapes is True:
                 out["gates_seq"] = [fmat(G, B * T) for _ in range(L)]
                 out["tanh_c_seq"] = [fmat(H, B * T) for _ in range(L)]
         if dy is not None:
-            if tapes:
+            if tapes is True:
                 out["dgw_seq"] = [fmat(G, B * T) for _ in range(L)]
             out["dx0"] = fmat(cfg.input, B * T)
             out["dh0"] = [fmat(H, B) for _ in range(L)]

@@ -17,6 +17,11 @@ RW_PREC_BF16, RW_PREC_FP32 = 0, 1
 RW_SCHED_AUTO, RW_SCHED_STEPWISE, RW_SCHED_PERSISTENT, RW_SCHED_CLUSTER, RW_SCHED_LAYERSEQ = 0, 1, 2, 3, 4
 RW_TAPE_X0, RW_TAPE_H, RW_TAPE_C, RW_TAPE_GATES, RW_TAPE_TANH_C, RW_TAPE_DGW, RW_TAPE_Y = range(7)
 
+class rw_trace_record(C.Structure):
+    _fields_ = [("task_id", C.c_int32), ("layer", C.c_int32), ("block", C.c_int32), ("step_k", C.c_int32),
+                ("phase", C.c_int32), ("worker", C.c_int32), ("start_ns", C.c_int64), ("end_ns", C.c_int64)]
+
+
 # every symbol include/rnnwave_sm100.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "rw_create", "rw_destroy", "rw_last_error", "rw_create_error", "rw_set_params", "rw_forward",
@@ -25,7 +30,7 @@ EXPORTS = [
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_describe_variants",
     "rw_describe_precision", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link",
-    "rw_train_step", "rw_train_wait",
+    "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm",
 ]
 
 
@@ -96,6 +101,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_pp_debug.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.rw_train_step.argtypes = [vp, _F, _F, _F, _F, _PF, _PF, _PF]
     L.rw_train_wait.argtypes = [vp]
+    L.rw_trace_enable.argtypes = [vp, C.c_int]
+    L.rw_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, _F, C.c_longlong, _F,
+                          C.c_longlong, C.c_float, _F, C.c_longlong]
+    L.rw_trace_records.argtypes = [vp, C.c_int, C.POINTER(rw_trace_record), C.c_int, C.POINTER(C.c_int)]
     L.rw_test_gemm_last_ms.argtypes = []
     L.rw_test_gemm_last_ms.restype = C.c_float
     _lib = L

@@ -118,6 +118,7 @@ struct GemmDesc {
   int accumulate;      // D += result instead of D = result
   int b_n_off;         // row (N) offset inside the B tensor (e.g. h_{l-1} starts at column block 1)
   float alpha;         // D = alpha * A B^T (fp16x2 weight operands carry 2^kWScaleLog2); 0 means 1
+  int* error;          // the context's error word (bounded mbarrier waits, sm100_ptx.cuh)
 };
 
 }  // namespace rw

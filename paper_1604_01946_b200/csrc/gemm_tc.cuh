@@ -104,7 +104,10 @@ __global__ void __launch_bounds__(256, 1)
     k_gemm_tc(const GemmDesc* __restrict__ table, int bn, int stages, int chunk_kb) {
   // descriptor in shared memory: the epilogue reads it per element
   __shared__ GemmDesc g;
-  if (threadIdx.x == 0) g = table[blockIdx.z];
+  if (threadIdx.x == 0) {
+    g = table[blockIdx.z];
+    set_wait_error(g.error);
+  }
   __syncthreads();
   const int m0 = blockIdx.x * kTileM;
   const int n0 = blockIdx.y * bn;
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const int nbuf = kChunkBN > 0 ? 2 : 1;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(bn * nbuf)) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(P::kPlanes * bn * nbuf)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) {
@@ -175,7 +178,14 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp converged; elect.sync picks the issuing lane)
+    // Two-plane formats: the stage holds B_hi and B_lo as adjacent row runs (K-major rows, or
+    // MN-major 64-element chunks, at the same uniform stride), so (hi,hi) and (hi,lo) are ONE
+    // MMA over N = 2 bn into the buffer's two column halves, and (lo,hi) a second one of N = bn
+    // into the first half: 2 issues per K step instead of 3 (a warp issues one tcgen05.mma per
+    // ~84 cycles at N <= 128, profiles/r01/ubench_mma_ingress.txt), the epilogue sums the halves.
     const uint32_t idesc = idesc_make(P::kFmt, kAMN, kBMN, kTileM, bn);
+    const uint32_t idesc2 = idesc_make(P::kFmt, kAMN, kBMN, kTileM, P::kPlanes == 2 ? 2 * bn : bn);
+    const int bw = P::kPlanes * bn;  // accumulator columns per buffer
     // stage-0 descriptors, advanced by adds (sm100_ptx.cuh desc_add)
     const uint64_t a_d0 = OperandTile<P, kAMN>::base(smem_u32(smem));
     const uint64_t b_d0 = OperandTile<P, kBMN>::base(smem_u32(smem + P::kPlanes * a_bytes));
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait_bounded(&tmem_empty[buf], ((c >> 1) - 1) & 1);
         tc_fence_after();
       }
-      const uint32_t acc = tmem_base + buf * bn;
+      const uint32_t acc = tmem_base + buf * bw;
       const int kb_end = min(nkb, (c + 1) * ckb);
       for (int k0 = kb; kb < kb_end; ++kb) {
         const int s = kb % stages;
@@ -195,15 +205,10 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t a_s = desc_add(a_d0, s * stage_bytes), b_s = desc_add(b_d0, s * stage_bytes);
 #pragma unroll
         for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk) {
-#pragma unroll
-          for (int cb = 0; cb < P::kCombos; ++cb) {
-            // combos: (hi,hi), (hi,lo), (lo,hi); bf16 has only (hi,hi)
-            const int pa = (cb == 2) ? 1 : 0;
-            const int pb = (cb == 1) ? 1 : 0;
-            const uint64_t ad = desc_add(a_s, pa * a_bytes + kk * OperandTile<P, kAMN>::kk_bytes());
-            const uint64_t bd = desc_add(b_s, pb * b_bytes + kk * OperandTile<P, kBMN>::kk_bytes());
-            umma_warp<P::kTF32>(acc, ad, bd, idesc, (kb != k0 || kk | cb) ? 1u : 0u);
-          }
+          const uint64_t ad = desc_add(a_s, kk * OperandTile<P, kAMN>::kk_bytes());
+          const uint64_t bd = desc_add(b_s, kk * OperandTile<P, kBMN>::kk_bytes());
+          umma_warp<P::kTF32>(acc, ad, bd, idesc2, (kb != k0 || kk) ? 1u : 0u);
+          if constexpr (P::kPlanes == 2) umma_warp<P::kTF32>(acc, desc_add(ad, a_bytes), bd, idesc, 1u);
         }
         umma_commit_warp(&empty[s]);
       }
@@ -223,13 +228,16 @@ __global__ void __launch_bounds__(256, 1)
         const int buf = c & 1;
         mbar_wait_bounded(&tmem_full[buf], (c >> 1) & 1);
         tc_fence_after();
+        const uint32_t ab = tmem_base + lane_off + buf * P::kPlanes * kChunkBN;
 #pragma unroll
         for (int c0 = 0; c0 < kChunkBN; c0 += 8) {
-          uint32_t v[8];
-          tmem_ld_32x32b_x8(tmem_base + lane_off + buf * bn + c0, v);
+          uint32_t v[8], w[8];
+          tmem_ld_32x32b_x8(ab + c0, v);
+          if constexpr (P::kPlanes == 2) tmem_ld_32x32b_x8(ab + kChunkBN + c0, w);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) accum[c0 + j] += __uint_as_float(v[j]);
+          for (int j = 0; j < 8; ++j)
+            accum[c0 + j] += P::kPlanes == 2 ? __uint_as_float(v[j]) + __uint_as_float(w[j]) : __uint_as_float(v[j]);
         }
         tc_fence_before();
         mbar_arrive(&tmem_empty[buf]);
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(256, 1)
   const long long ntiles = (long long)count * mt_max * nt_max;
 
   if (threadIdx.x == 0) {
+    set_wait_error(table[0].error);  // every descriptor of a launch carries the same error word
     for (int i = 0; i < stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -468,6 +477,7 @@ __global__ void __launch_bounds__(256, 1)
   const long long ntiles = (long long)count * mt_max * nt_max;
 
   if (threadIdx.x == 0) {
+    set_wait_error(table[0].error);  // every descriptor of a launch carries the same error word
     for (int i = 0; i < stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);

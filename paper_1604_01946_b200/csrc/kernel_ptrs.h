@@ -10,7 +10,7 @@ namespace rw {
 void* cl_kernel_ptr(int prec, bool fwd, int nco);
 // k_lstm_fwd / k_lstm_bwd<P, pair> (lstm_step.cuh); prec kBF16 or kTF32x3 (pair: bf16 only)
 void* lstm_kernel_ptr(int prec, bool fwd, bool pair);
-// k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh), BNV 0 or 64
+// k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh): bf16 BNV 0; two-plane formats BNV = tile width 64 / 128
 void* gemm_tc_ptr(int prec, bool amn, bool bmn, int bnv);
 // k_gemm_p<AMN, BMN, BN> / k_gemm_p2<AMN, BMN, BN> (bf16), BN 128 or 256
 void* gemm_p_ptr(bool amn, bool bmn, int bn);

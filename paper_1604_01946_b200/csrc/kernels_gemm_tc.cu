@@ -4,9 +4,15 @@
 
 namespace rw {
 
+// bf16: one accumulation over the whole K (BNV 0); two-plane formats: chunked promotion with
+// BNV = the tile width (64 or 128)
 template <class P, bool AMN, bool BMN>
 static void* tc_ptr(int bnv) {
-  return bnv == 64 ? (void*)k_gemm_tc<P, AMN, BMN, 64> : (void*)k_gemm_tc<P, AMN, BMN, 0>;
+  if constexpr (P::kPlanes == 1) {
+    return (void*)k_gemm_tc<P, AMN, BMN, 0>;
+  } else {
+    return bnv == 128 ? (void*)k_gemm_tc<P, AMN, BMN, 128> : (void*)k_gemm_tc<P, AMN, BMN, 64>;
+  }
 }
 template <class P>
 static void* tc_ptr_p(bool amn, bool bmn, int bnv) {

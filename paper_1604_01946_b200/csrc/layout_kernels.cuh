@@ -252,4 +252,31 @@ __global__ void k_db_reduce_layers(DbGroup grp, int slices, int H, int Hp) {
   grp.db[blockIdx.y][e] = acc;
 }
 
+// rw_gemm operand packing: dst row r (of Rp), k (of Kp) = op(src)(r, k) -- zero outside the
+// rows x K source range -- as K-major operand planes. op(src)(r, k) = src[k * ld + r] when the
+// column-major source holds the rows x K operand directly, src[r * ld + k] when it holds its
+// transpose (gemm.hpp:339-347's trans flags).
+__global__ void k_pack_gemm_operand(const float* __restrict__ src, long long ld, int rows, int K, int trans,
+                                    int Rp, int Kp, int prec, void* p0, void* p1) {
+  const long long total = (long long)Rp * Kp;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / Kp), k = (int)(e - (long long)r * Kp);
+    float v = 0.0f;
+    if (r < rows && k < K) v = trans ? src[(long long)r * ld + k] : src[(long long)k * ld + r];
+    store_planes(prec, p0, p1, e, v);
+  }
+}
+// C = beta * C (column-major M x N, ldc) ahead of an accumulating GEMM (beta == 0: exact zeros,
+// like the reference's beta = 0 overwrite)
+__global__ void k_scale_cols(float* __restrict__ c, long long ldc, int M, int N, float beta) {
+  const long long total = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e / M, i = e - j * M;
+    float* p = c + j * ldc + i;
+    *p = beta == 0.0f ? 0.0f : beta * *p;
+  }
+}
+
 }  // namespace rw

@@ -114,6 +114,8 @@ struct RecParams {
                       // DSMEM offsets of the receive buffer / barriers match across ranks)
   int acc_kb;         // k-blocks per TMEM accumulator (fp32 promotion); accumulators summed
   int n_acc;          // in fp32 by the epilogue (1 = single accumulator)
+  int promo;          // 3xTF32 long K: promotion ring (promo_drain) -- acc_kb k-blocks per chunk,
+                      // n_acc slots after the fp32 sum region (TMEM: N x (1 + n_acc) columns)
   int stages;
   int a_prefetch;     // streamed A: L2 prefetch distance in k-blocks (0 = off)
   uint32_t flag_target;
@@ -299,8 +301,11 @@ struct RecSmem {
   uint64_t* tmem_empty;
   uint64_t* xready;
   uint64_t* xfree;
+  uint64_t* pfull;   // [kMaxPromoSlots] promotion ring: chunk accumulated (MMA commit)
+  uint64_t* pempty;  // [kMaxPromoSlots] chunk drained into the sum (kEpiThreads arrivals)
   uint32_t* tmem_slot;
 };
+constexpr int kMaxPromoSlots = 8;
 
 __device__ __forceinline__ RecSmem carve(uint8_t* smem, int a_bytes_total, int b_stage_bytes,
                                          int stages) {
@@ -316,7 +321,9 @@ __device__ __forceinline__ RecSmem carve(uint8_t* smem, int a_bytes_total, int b
   s.tmem_empty = s.a_full + 2;
   s.xready = s.a_full + 3;
   s.xfree = s.a_full + 4;
-  s.tmem_slot = reinterpret_cast<uint32_t*>(s.a_full + 5);
+  s.pfull = s.a_full + 5;
+  s.pempty = s.pfull + kMaxPromoSlots;
+  s.tmem_slot = reinterpret_cast<uint32_t*>(s.pempty + kMaxPromoSlots);
   return s;
 }
 
@@ -325,7 +332,7 @@ inline size_t rec_smem_bytes(int planes, int a_kblocks_resident_or_stages, int n
   const size_t a = size_t(a_kblocks_resident_or_stages) * planes * kTileM * kRowBytes;
   const size_t b = size_t(stages) * planes * n * kRowBytes;
   const size_t x = size_t(kXChunk) * kTileM * 4;
-  const size_t bars = (2 * stages + 6) * 8 + 16;
+  const size_t bars = (2 * stages + 6 + 2 * kMaxPromoSlots) * 8 + 16;
   return 1024 + a + b + x + bars;
 }
 
@@ -394,6 +401,10 @@ __device__ __forceinline__ uint32_t rec_setup(const RecSmem& S, const RecParams&
     mbar_init(S.tmem_empty, kEpiThreads);
     mbar_init(S.xready, ks);
     mbar_init(S.xfree, ks);
+    for (int i = 0; i < kMaxPromoSlots; ++i) {
+      mbar_init(&S.pfull[i], 1);
+      mbar_init(&S.pempty[i], kEpiThreads);
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -455,6 +466,54 @@ __device__ __forceinline__ void rec_teardown(int ks, uint32_t tmem_base, uint32_
   }
 }
 
+// ---- 3xTF32 promotion ring (RecParams::promo). The tensor core's fp32 accumulation loses
+// ~2^-27 of the running sum per MMA (measured: 5e-5 relative after K = 6400; at config C2048 the
+// backward's K = 16384 chains missed the 1e-5 contract by 2.5x), so long K ranges are cut into
+// chunks of acc_kb k-blocks, each accumulated into one of n_acc ring slots of TMEM while the
+// epilogue adds the previous chunk into an fp32 sum region (tcgen05.ld / add / tcgen05.st, fixed
+// order: deterministic). Slot handshake: pfull (MMA commit) / pempty (kEpiThreads arrivals).
+// Each thread touches only the TMEM cells it later reads in the step's final drain (its lane
+// row, its half of every kXChunk column chunk), so no cross-thread ordering is needed.
+__device__ __forceinline__ void promo_drain(const RecSmem& S, const RecParams& p, uint32_t tmem_base, int N,
+                                            int nchunks, uint32_t& ech) {
+  const int warp = threadIdx.x >> 5, q = warp & 3, half = (warp - 4) >> 2;
+  const uint32_t lane_off = uint32_t(q * 32) << 16;
+  for (int c = 0; c < nchunks; ++c, ++ech) {
+    const uint32_t slot = ech % (uint32_t)p.n_acc;
+    mbar_wait(&S.pfull[slot], (ech / (uint32_t)p.n_acc) & 1);
+    tc_fence_after();
+    const uint32_t src = tmem_base + lane_off + (1 + slot) * N, dst = tmem_base + lane_off;
+    for (int n0 = 0; n0 < N; n0 += kXChunk) {
+      const int nc = min(kXChunk, N - n0);
+      for (int c0 = n0 + half * (nc >> 1); c0 < n0 + (half + 1) * (nc >> 1); c0 += 8) {
+        uint32_t v[8], w[8];
+        tmem_ld_32x32b_x8(src + c0, v);
+        if (c > 0) tmem_ld_32x32b_x8(dst + c0, w);
+        tmem_ld_wait();
+        if (c > 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __float_as_uint(__uint_as_float(w[j]) + __uint_as_float(v[j]));
+        }
+        tmem_st_32x32b_x8(dst + c0, v);
+      }
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(&S.pempty[slot]);
+  }
+}
+// MMA side of the ring: called with the index (among this step's active k-blocks) of the
+// k-block about to be issued; returns its slot accumulator and whether it starts a chunk.
+__device__ __forceinline__ uint32_t promo_slot(const RecSmem& S, const RecParams& p, uint32_t tmem_base, int N,
+                                               int nact, uint32_t ch) {
+  const uint32_t slot = ch % (uint32_t)p.n_acc;
+  if (nact % p.acc_kb == 0 && ch >= (uint32_t)p.n_acc) {
+    mbar_wait(&S.pempty[slot], ((ch / (uint32_t)p.n_acc) - 1) & 1);
+    tc_fence_after();
+  }
+  return tmem_base + (1 + slot) * N;
+}
+
 // MMA issue of one k-block (all kk substeps, all precision combos) into accumulator acc.
 template <class P>
 __device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32_t b_base,
@@ -489,6 +548,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   if (threadIdx.x == 0) {
     Ly = layers[l];
     x_flags = l > 0 ? layers[l - 1].flags : nullptr;
+    set_wait_error(p.error);
   }
   __syncthreads();
   const int ks = p.ksplit;
@@ -513,7 +573,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * (p.n_acc + p.promo))) tmem_cols <<= 1;
   const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
@@ -627,26 +687,31 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
     tc_fence_after();
-    uint32_t pc = 0;
+    uint32_t pc = 0, ch = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       progress(p, 1, it, 1);
-      if (it > 0) {
+      if (it > 0 && !p.promo) {
         mbar_wait(S.tmem_empty, (it - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const int s = pc % p.stages;
+        const int nact = kb - kb_lo;
+        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, nact, ch)
+                                     : tmem_base + (nact / p.acc_kb) * N;  // accumulator of this k-block
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
-        const int ai = (kb - kb_lo) / p.acc_kb;  // accumulator of this k-block
-        mma_kblock<P>(tmem_base + ai * N, a_base, b_base, a_bytes, b_bytes, idesc,
-                      (kb - kb_lo) % p.acc_kb == 0);
+        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, nact % p.acc_kb == 0);
         umma_commit_warp(&S.empty[s]);
+        if (p.promo && ((nact + 1) % p.acc_kb == 0 || kb + 1 == kb_hi)) {
+          umma_commit_warp(&S.pfull[ch % (uint32_t)p.n_acc]);
+          ++ch;
+        }
       }
-      umma_commit_warp(S.tmem_full);
+      if (!p.promo) umma_commit_warp(S.tmem_full);
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
@@ -662,13 +727,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const long long Hp = p.Hp, G4 = 4 * Hp;
     const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u],
                 bc = Le.bias[3 * Hp + u];
-    const int n_used = kPair ? 1 : (my_nkb + p.acc_kb - 1) / p.acc_kb;
-    uint32_t xc = 0;
+    const int n_chunks = kPair ? 1 : (my_nkb + p.acc_kb - 1) / p.acc_kb;
+    const int n_used = p.promo ? (n_chunks > 0 ? 1 : 0) : n_chunks;
+    uint32_t xc = 0, ech = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
       if (et == 0) progress(p, 2, it, 1);
-      mbar_wait(S.tmem_full, it & 1);
-      tc_fence_after();
+      if (p.promo) {
+        promo_drain(S, p, tmem_base, N, n_chunks, ech);
+      } else {
+        mbar_wait(S.tmem_full, it & 1);
+        tc_fence_after();
+      }
       if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
@@ -680,7 +750,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
           xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
-        if (n0 + kXChunk >= N) {
+        if (n0 + kXChunk >= N && !p.promo) {
           tc_fence_before();
           mbar_arrive(S.tmem_empty);
         }
@@ -772,6 +842,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   if (threadIdx.x == 0) {
     Ly = layers[l];
     up_flags = Ly.has_up ? layers[l + 1].flags : nullptr;
+    set_wait_error(p.error);
   }
   __syncthreads();
   const int ks = p.ksplit;
@@ -797,7 +868,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(N * p.n_acc)) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * (p.n_acc + p.promo))) tmem_cols <<= 1;
   // pair: the leader's tmem_empty takes one arrival per CTA (after its epilogue drained TMEM)
   const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols, 2) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
@@ -924,30 +995,36 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
     if (p.resident) mbar_wait(S.a_full, 0);
     tc_fence_after();
-    uint32_t pc = 0;
+    uint32_t pc = 0, ch = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
       progress(p, 1, it, 1);
-      if (it > 0) {
+      if (it > 0 && !p.promo) {
         mbar_wait(S.tmem_empty, (it - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
+      int ntot = 0;  // active k-blocks of this step (the ring closes its last chunk on the last one)
+      for (int kb = kb_lo; kb < kb_hi; ++kb) ntot += kb_active(kb, t) ? 1 : 0;
       int nact = 0;  // active k-blocks so far this step
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
         const int s = pc % p.stages;
+        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, nact, ch) : tmem_base + (nact / p.acc_kb) * N;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
-        mma_kblock<P>(tmem_base + (nact / p.acc_kb) * N, a_base, b_base, a_bytes, b_bytes, idesc,
-                      nact % p.acc_kb == 0);
+        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, nact % p.acc_kb == 0);
         ++nact;
         umma_commit_warp(&S.empty[s]);
+        if (p.promo && (nact % p.acc_kb == 0 || nact == ntot)) {
+          umma_commit_warp(&S.pfull[ch % (uint32_t)p.n_acc]);
+          ++ch;
+        }
         ++pc;
       }
-      umma_commit_warp(S.tmem_full);
+      if (!p.promo) umma_commit_warp(S.tmem_full);
     }
   } else if (warp >= 4) {
     const BwdLayer Le = Ly;  // register copy (see the forward epilogue)
@@ -959,15 +1036,20 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const int hh = et >> 7;             // column parity (cell phase)
     const int u = row0 + ul;
     const long long Hp = p.Hp, G4 = 4 * Hp;
-    uint32_t xc = 0;
+    uint32_t xc = 0, ech = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
       int nact = 0;
       for (int kb = kb_lo; kb < kb_hi; ++kb) nact += kb_active(kb, t) ? 1 : 0;
-      const int n_used = (nact + p.acc_kb - 1) / p.acc_kb;
+      const int n_chunks = (nact + p.acc_kb - 1) / p.acc_kb;
+      const int n_used = (!kPair && p.promo) ? (n_chunks > 0 ? 1 : 0) : n_chunks;
       if (et == 0) progress(p, 2, it, 1);
-      mbar_wait(S.tmem_full, it & 1);
-      tc_fence_after();
+      if (!kPair && p.promo) {
+        promo_drain(S, p, tmem_base, N, n_chunks, ech);
+      } else {
+        mbar_wait(S.tmem_full, it & 1);
+        tc_fence_after();
+      }
       if (et == 0) trace_stamp(p, it, 2);
       for (int n0 = 0; n0 < N; n0 += kXChunk, ++xc) {
         const int nc = min(kXChunk, N - n0);
@@ -979,7 +1061,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
           xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
-        if (n0 + kXChunk >= N) {
+        if (n0 + kXChunk >= N && (kPair || !p.promo)) {
           tc_fence_before();
           if constexpr (kPair) {
             named_bar_sync(1, kEpiThreads);  // the whole CTA drained its TMEM accumulator

@@ -533,7 +533,10 @@ __device__ __forceinline__ void cl_off_step(const ClSmem& S, const ClParams& p, 
   for (int i = 0; i < kChunks * 8; ++i) slot[(size_t)(c0 + i) * kTileM + row] = v[i];
   fence_proxy_async_global();
   named_bar_sync(1, kEpiThreads);
-  if (et == 0) red_release_s(done + it, 1, sys);
+  if (et == 0) {
+    cl_trace(p, it, 15);  // task end (before the release: a consumer's start never precedes it)
+    red_release_s(done + it, 1, sys);
+  }
 }
 
 template <class P, int kChunks>
@@ -615,6 +618,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       Og = p.offg[y];
     }
     epoch_s = *p.epoch;
+    set_wait_error(p.error);
   }
   __syncthreads();
   const uint32_t epoch = epoch_s;
@@ -678,6 +682,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         cl_trace(p, t, 1);
         cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR, cl_pair_kb(p, nkb));
         if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
+        cl_trace(p, t, 14);  // task start: h_{t-1} and the off partial both available
       } else {
         if (Og.op_flags) wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
@@ -800,6 +805,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         fence_proxy_async_global();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
+          cl_trace(p, t, 15);  // task end, before the release
           red_release_gpu_add(&Le.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
           red_relaxed_s(consumed, 1, sys);       // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
@@ -1009,6 +1015,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     fence_proxy_async_global();
     named_bar_sync(1, kEpiThreads);
     if (et == 0) {
+      cl_trace(p, it, 15);  // task end, before the release
       red_release_gpu_add(&Ly.flags[t], 1);
       if (off) red_relaxed_s(consumed, 1, sys);
       cl_trace(p, it, 5);
@@ -1071,6 +1078,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       Og = p.offg[y];
     }
     epoch_s = *p.epoch;
+    set_wait_error(p.error);
   }
   __syncthreads();
   const uint32_t epoch = epoch_s;
@@ -1144,6 +1152,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                     cl_pair_kb(p, nkb));
       }
       if (off && !early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
+      if (crit) cl_trace(p, it, 14);  // task start: dG_{t+1} and the off partial (d_above) both available
     }
   } else if (active && (warp == 1 || warp == 3)) {
     const int j = warp == 3 ? 1 : 0;

@@ -119,6 +119,7 @@ struct DevBuf {
     if (n) RW_CUDA(cudaMemset(p, 0, n));
   }
   float* f() const { return static_cast<float*>(p); }
+  unsigned long long* u64() const { return static_cast<unsigned long long*>(p); }
 };
 
 // An operand tensor: 1 (bf16) or 2 (tf32 / fp16 hi, lo) planes of `elems` elements.
@@ -247,6 +248,7 @@ struct rw_ctx {
   int fwd_sched = RW_SCHED_STEPWISE, bwd_sched = RW_SCHED_STEPWISE;
   int ks_f = 1, ks_b = 1, res_f = 0, res_b = 0, st_f = 4, st_b = 4;
   int slots_f = 0, slots_b = 0, acckb_f = 1, acckb_b = 1, nacc_f = 1, nacc_b = 1;
+  int promo_f = 0, promo_b = 0;  // 3xTF32 promotion ring (lstm_step.cuh promo_drain)
   size_t smem_f = 0, smem_b = 0;
   // cluster schedule (rec_cluster.cuh)
   ClPlan cl_f, cl_b;
@@ -302,8 +304,10 @@ struct rw_ctx {
   int nranks = 1, rank = 0;
 
   // device trace (RW_TRACE=<csv path>): globaltimer stamps of the persistent kernels
-  DevBuf trace_f, trace_b;
-  std::string trace_path;
+  DevBuf trace_f, trace_b, trace_dx;  // device stamps (tracing on): [cta][steps][16] / dx0 GEMM span
+  bool tracing = false;
+  std::string trace_path;        // RW_TRACE: reference-schema CSV of every synced pass
+  std::string trace_spans_path;  // RW_TRACE_SPANS: per-CTA span profile (profiles/trace_run.py)
 
   // hang debugging (RW_DEBUG_HANG_S): mapped host progress words
   unsigned int* progress_host = nullptr;
@@ -565,10 +569,12 @@ void launch_gemm(const GemmDesc* table_dev, int count, int M, int N, int bn, int
   const size_t smem = gemm_smem(P::kPlanes, bn, stages);
   dim3 grid(ceil_div(M, kTileM), ceil_div(N, bn), count);
   ++g_launches;
+  // two-plane formats: the chunked-promotion variant, one instantiation per tile width
   const int prec = P::kPlanes == 1 ? kBF16 : P::kTF32 ? kTF32x3 : kF16x2;
-  const bool b64 = P::kPlanes == 2 && bn == 64;
-  void* k = gemm_tc_ptr(prec, AMN, BMN, b64 ? 64 : 0);
-  int promote = b64 ? (P::kTF32 ? kPromoteKB : kPromoteKB16) : 0;
+  const int chunk_bn = P::kPlanes == 2 ? bn : 0;
+  if (chunk_bn && chunk_bn != 64 && chunk_bn != 128) throw RwError{RW_ECUDA, "internal: two-plane GEMM tile width"};
+  void* k = gemm_tc_ptr(prec, AMN, BMN, chunk_bn);
+  int promote = chunk_bn ? (P::kTF32 ? kPromoteKB : kPromoteKB16) : 0;
   RW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[4] = {const_cast<GemmDesc**>(&table_dev), &bn, &stages, &promote};
   RW_CUDA(cudaLaunchKernel(k, grid, dim3(256), args, smem, s));
@@ -604,6 +610,19 @@ void validate(const rw_config& c) {
 int add_map(rw_ctx* x, const CUtensorMap& m) {
   x->maps.push_back(m);
   return (int)x->maps.size() - 1;
+}
+
+// Device stamp buffers of the recurrent kernels (RW_TRACE / rw_trace_enable): up to 4096 CTAs
+// x (T + 2) steps x 16 stamps per direction; the stepwise schedule stores one block of grid
+// CTAs per (layer, step) launch in the same buffers.
+void trace_alloc(rw_ctx* x) {
+  if (!x->trace_f.p) {
+    const size_t ctas = 4096;
+    x->trace_f.alloc(ctas * (x->T + 2) * 16 * 8);
+    x->trace_b.alloc(ctas * (x->T + 2) * 16 * 8);
+    x->trace_dx.alloc(16);
+  }
+  x->tracing = true;
 }
 
 void build(rw_ctx* x) {
@@ -842,17 +861,29 @@ void build(rw_ctx* x) {
     x->dgsw.resize(L);
     for (int l = 0; l < L; ++l) x->dgsw[l].alloc((size_t)G4p * colsT * 2 * x->planes);
   }
-  // fp32-parity: accumulate every kAccKB k-blocks in a separate TMEM accumulator (<= 512 cols)
-  auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc) {
+  // fp32-parity: accumulate every acc_kb k-blocks in a separate TMEM accumulator (<= 512 cols),
+  // summed in fp32 by the epilogue. When that would leave chains longer than kPromoKB k-blocks
+  // (large H: 512 / Bp accumulators cannot cover K), run the promotion ring instead: chunks of
+  // kPromoKB k-blocks in 512 / Bp - 1 ring slots, each added into an fp32 sum region as soon as it
+  // is complete (lstm_step.cuh promo_drain).
+  constexpr int kPromoKB = 8;  // 8 x 32 = 256 K elements per tensor-core accumulation chain
+  auto acc_plan = [&](int kb_per_cta, int& acc_kb, int& n_acc, int& promo) {
     acc_kb = kb_per_cta > 0 ? kb_per_cta : 1;
     n_acc = 1;
+    promo = 0;
     if (x->prec == kBF16) return;
     acc_kb = 2;
     while ((long long)ceil_div(kb_per_cta, acc_kb) * Bp > 512) acc_kb *= 2;
     n_acc = std::max(1, ceil_div(kb_per_cta, acc_kb));
+    const int slots = std::min(kMaxPromoSlots, 512 / Bp - 1);
+    if (acc_kb > kPromoKB && slots >= 1 && !getenv("RW_NO_PROMO")) {
+      acc_kb = kPromoKB;
+      n_acc = slots;
+      promo = 1;
+    }
   };
-  acc_plan(ceil_div(ls ? Hp / x->atomK : kbf_max, x->ks_f), x->acckb_f, x->nacc_f);
-  acc_plan(ceil_div(ls ? (int)(G4p / x->atomK) : kbb_max, x->ks_b), x->acckb_b, x->nacc_b);
+  acc_plan(ceil_div(ls ? Hp / x->atomK : kbf_max, x->ks_f), x->acckb_f, x->nacc_f, x->promo_f);
+  acc_plan(ceil_div(ls ? (int)(G4p / x->atomK) : kbb_max, x->ks_b), x->acckb_b, x->nacc_b, x->promo_b);
   int slices_b = ceil_div(Bp, kXChunk) * x->ks_b * 2;
   for (int l = 0; l < L; ++l) x->dbp[l].alloc((size_t)slices_b * G4p * 4);
 
@@ -868,9 +899,11 @@ void build(rw_ctx* x) {
   int m_xLS[2] = {0, 0};
   std::vector<int> m_hopLS(2 * L), m_dgLS(2 * L);
   std::vector<int> m_dgT(2 * L), m_hT(2 * L);
-  x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 64;
+  x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 128;
   if (const char* e = getenv("RW_BN_DX")) x->bn_dx = atoi(e);
-  x->bn_wg = x->prec == kBF16 ? 128 : 64;
+  // two-plane formats: (hi,hi)+(hi,lo) as one N = 2 bn MMA, 2 x 2 bn TMEM columns (gemm_tc.cuh)
+  x->bn_wg = 128;
+  if (const char* e = getenv("RW_BN_WG2"); e && x->prec != kBF16) x->bn_wg = atoi(e);
   for (int p = 0; p < x->planes; ++p) {
     for (int l = 0; l < L; ++l) {
       const int Ipl = l == 0 ? Ip : Hp;
@@ -1051,6 +1084,7 @@ void build(rw_ctx* x) {
   for (int l = 0; l < L; ++l) {
     const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
     GemmDesc d{};
+    d.error = static_cast<int*>(x->errflag.p);
     for (int p = 0; p < 2; ++p) {
       const int q = p % x->planes;
       if (kmajor_wg) {
@@ -1095,6 +1129,7 @@ void build(rw_ctx* x) {
     for (int l = 0; l < L; ++l) {
       const int Ipl = l == 0 ? Ip : Hp;
       GemmDesc& f = lf[l];
+      f.error = static_cast<int*>(x->errflag.p);
       for (int p = 0; p < 2; ++p) {
         const int q = p % x->planes;
         f.a[p] = mp(m_wf[2 * l + q], p);
@@ -1116,6 +1151,7 @@ void build(rw_ctx* x) {
       f.n_valid = (int)colsT;
       if (l < L - 1) {
         GemmDesc& g = lb[l];
+        g.error = static_cast<int*>(x->errflag.p);
         for (int p = 0; p < 2; ++p) {
           const int q = p % x->planes;
           g.a[p] = mp(m_wb[2 * l + q], p);
@@ -1144,6 +1180,7 @@ void build(rw_ctx* x) {
   x->gemm_wg.alloc(sizeof(GemmDesc) * wg.size());
   RW_CUDA(cudaMemcpy(x->gemm_wg.p, wg.data(), sizeof(GemmDesc) * wg.size(), cudaMemcpyHostToDevice));
   GemmDesc dx{};
+  dx.error = static_cast<int*>(x->errflag.p);
   for (int p = 0; p < 2; ++p) {
     dx.a[p] = mp(m_w0t[p % x->planes], p);
     dx.b[p] = mp(m_dg0dx[p % x->planes], p);
@@ -1191,12 +1228,9 @@ void build(rw_ctx* x) {
   }
   RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
   if (const char* e = getenv("RW_NO_GRAPHS")) x->use_graphs = atoi(e) == 0;
-  if (const char* e = getenv("RW_TRACE")) {
-    x->trace_path = e;
-    const size_t ctas = 4096;
-    x->trace_f.alloc(ctas * (T + 1) * 16 * 8);
-    x->trace_b.alloc(ctas * (T + 2) * 16 * 8);
-  }
+  if (const char* e = getenv("RW_TRACE")) x->trace_path = e;
+  if (const char* e = getenv("RW_TRACE_SPANS")) x->trace_spans_path = e;
+  if (!x->trace_path.empty() || !x->trace_spans_path.empty()) trace_alloc(x);
   if (const char* e = getenv("RW_DEBUG_HANG_S")) {
     x->hang_s = atof(e);
     RW_CUDA(cudaHostAlloc((void**)&x->progress_host, 4 * 4096 * sizeof(unsigned), cudaHostAllocMapped));
@@ -1273,13 +1307,14 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.a_slots = fwd ? x->slots_f : x->slots_b;
   rp.acc_kb = fwd ? x->acckb_f : x->acckb_b;
   rp.n_acc = fwd ? x->nacc_f : x->nacc_b;
+  rp.promo = fwd ? x->promo_f : x->promo_b;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.a_prefetch = 0;  // measured: no gain at config E (0 4 8 16 32 -> 727 702 694 701 660 TFLOP/s)
   if (const char* e = getenv("RW_A_PREFETCH")) rp.a_prefetch = atoi(e);
   rp.error = static_cast<int*>(x->errflag.p);
   rp.progress = x->progress_dev;
   rp.trace = nullptr;
-  if (!x->trace_path.empty()) rp.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
+  if (x->tracing) rp.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
   rp.timeout_ns = 20ULL * 1000000000ULL;
   if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) rp.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
   return rp;
@@ -1360,7 +1395,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.timeout_ns = 20ULL * 1000000000ULL;
   if (const char* e = getenv("RW_FLAG_TIMEOUT_MS")) p.timeout_ns = 1000000ULL * strtoull(e, nullptr, 10);
   p.trace = nullptr;
-  if (!x->trace_path.empty()) p.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
+  if (x->tracing) p.trace = static_cast<unsigned long long*>((fwd ? x->trace_f : x->trace_b).p);
   p.trace_steps = fwd ? x->T : x->T + 1;
   if (const char* e = getenv("RW_CL_DEBUG")) p.debug = atoi(e);
   p.dir = fwd ? 0 : 1;
@@ -1463,6 +1498,8 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
       if (l > 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l - 1], 0));
       rp.layer_base = l;
       rp.t_first = t;
+      // trace: one block of grid CTAs per (layer, step) launch (trace_records reads [l][t][cta])
+      if (x->tracing) rp.trace = x->trace_f.u64() + (size_t)(l * x->T + t) * rp.tiles * rp.ksplit * 8;
       launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, x->ls[l], x->pair_f ? 2 : 0);
       RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
     }
@@ -1524,6 +1561,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
       if (l < x->L - 1 && t >= 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l + 1], 0));
       rp.layer_base = l;
       rp.t_first = t;
+      if (x->tracing) rp.trace = x->trace_b.u64() + (size_t)(l * (x->T + 1) + (x->T - 1 - t)) * rp.tiles * rp.ksplit * 8;
       launch_rec<P>(kern, x->bwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_b, x->ls[l]);
       RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
     }
@@ -1534,8 +1572,10 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
 
 template <class P>
 void run_dx0(rw_ctx* x, cudaStream_t s) {
+  if (x->tracing) k_stamp<<<1, 1, 0, s>>>(x->trace_dx.u64());
   launch_gemm<P, false, false>(static_cast<const GemmDesc*>(x->gemm_dx.p), 1, x->Ip,
                                x->Bp * x->T, x->bn_dx, x->st_dx, s);
+  if (x->tracing) k_stamp<<<1, 1, 0, s>>>(x->trace_dx.u64() + 1);
 }
 
 void transpose_planes(rw_ctx* x, const Operand& src, int R, long long C, Operand& dst, cudaStream_t s) {
@@ -1687,6 +1727,9 @@ void check_error_flag(rw_ctx* x) {
              ((e[0] >> 4) & 0xffff) - 2,
              (e[0] & 15) == 1 ? "neighbour-layer" : (e[0] & 15) == 3 ? "off-partial publication"
                               : (e[0] & 15) == 4 ? "ring-slot consumed" : "own-layer", e[1]);
+    if (e[0] == kWaitTimeoutCode)
+      snprintf(b, sizeof b, "a kernel's pipeline barrier (TMA / MMA / exchange mbarrier) did not complete within %.0f s; "
+               "the launch was abandoned and its results are invalid", kWaitNs * 1e-9);
     throw RwError{RW_ESTATE, b};
   }
 }
@@ -1725,21 +1768,21 @@ void d2h_unpad(rw_ctx* x, const float* src, int Rp, int Bp, long long col_off, i
   RW_CUDA(cudaStreamSynchronize(x->main));
 }
 
+std::string g_create_err;  // rw_create / context-free calls (rw_gemm, rw_test_gemm): rw_last_error(NULL)
+
 template <typename F>
 int guarded(rw_ctx* x, F&& f) {
   try {
     f();
     return RW_OK;
   } catch (const RwError& e) {
-    if (x) x->err = e.msg;
+    (x ? x->err : g_create_err) = e.msg;
     return e.code;
   } catch (const std::exception& e) {
-    if (x) x->err = e.what();
+    (x ? x->err : g_create_err) = e.what();
     return RW_ECUDA;
   }
 }
-
-std::string g_create_err;
 
 }  // namespace
 
@@ -2287,13 +2330,154 @@ int rw_allreduce_grads(rw_ctx* x, void* stream) {
   });
 }
 
+// ---- schedule trace in the reference's task model (scheduler.hpp:96-155, 180-192), block width
+// 1: the device wavefront's unit of work is one step (INPUT_GEMM(l, t) = W_l.x_t, the W.x of
+// one step; RECURRENT_STEP(l, t)). Task ids follow build_graph(L, T, 1): input_id(l, j) =
+// l * 2T + j, recurrent_id(l, t) = l * 2T + T + t. Aggregated over the CTAs of a task: start =
+// the first CTA's "dependencies satisfied" stamp, end = the last CTA's stamp taken before its
+// release, so a consumer's start never precedes its producers' ends. The persistent / stepwise
+// kernels fuse W.x into the step's accumulator: their INPUT_GEMM records are the instant the step's
+// inputs were all available (zero length, ending where the step starts). Backward (the reversed
+// graph): INPUT_GEMM(l, t) is layer l's output GEMM W_l^T.dG_{l,t}, i.e. the off-critical group
+// of layer l - 1 (cluster) or fused into layer l - 1's step (persistent / stepwise); for l = 0
+// it is the dx0 GEMM, recorded once around the whole launch.
+struct TraceRec {
+  int task_id, layer, block, step_k, phase, worker;
+  long long start_ns, end_ns;
+};
+
+static std::vector<TraceRec> trace_records(rw_ctx* x, int dir) {
+  const int L = x->L, T = x->T, sched = dir == 0 ? x->fwd_sched : x->bwd_sched;
+  const int steps = dir == 0 ? T : T + 1;  // backward: + the dh0 step (not a reference task)
+  std::vector<TraceRec> out;
+  const unsigned long long kNone = ~0ULL;
+  struct Agg {
+    unsigned long long s = ~0ULL, e = 0;
+    int w = 0;
+    bool ok() const { return s != ~0ULL && e != 0; }
+  };
+  std::vector<Agg> rec((size_t)L * T), inp((size_t)L * T);
+  auto tof = [&](int it) { return dir == 0 ? it : T - 1 - it; };
+  if (sched == RW_SCHED_CLUSTER) {
+    const ClPlan& pl = dir == 0 ? x->cl_f : x->cl_b;
+    const int tiles = dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
+    const int gx = tiles * 2 * pl.cs, rows = dir == 0 ? x->rows_f : x->rows_b;
+    std::vector<unsigned long long> h((size_t)rows * gx * steps * 16);
+    RW_CUDA(cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int y = 0; y < std::min(rows, L); ++y)
+      for (int bx = 0; bx < gx; ++bx) {
+        const bool crit = ((bx / pl.cs) & 1) == 0;
+        const int lt = crit ? y : (dir == 0 ? y : y + 1);  // task layer
+        if (lt >= L) continue;
+        for (int it = 0; it < steps; ++it) {
+          const int t = tof(it);
+          if (t < 0) continue;
+          const unsigned long long* st = &h[(((size_t)y * gx + bx) * steps + it) * 16];
+          const unsigned long long a = crit ? st[14] : st[1], b = st[15];
+          if (!a || !b) continue;  // inactive member
+          Agg& g = (crit ? rec : inp)[(size_t)lt * T + t];
+          g.s = std::min(g.s, a);
+          if (b >= g.e) {
+            g.e = b;
+            g.w = bx;
+          }
+        }
+      }
+  } else if (sched == RW_SCHED_PERSISTENT || sched == RW_SCHED_STEPWISE) {
+    const int ks = dir == 0 ? x->ks_f : x->ks_b;
+    const bool pair = dir == 0 ? x->pair_f : x->pair_b;
+    const int tiles = dir == 0 ? x->Hp / kUnitsPerFwdTile : ceil_div(x->Hp, kTileM);
+    const int gx = pair && sched == RW_SCHED_PERSISTENT ? tiles : tiles * ks;
+    const bool stepwise = sched == RW_SCHED_STEPWISE;
+    std::vector<unsigned long long> h((size_t)L * gx * steps * 8);
+    RW_CUDA(cudaMemcpy(h.data(), (dir == 0 ? x->trace_f : x->trace_b).p, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; ++l)
+      for (int w = 0; w < gx; ++w)
+        for (int it = 0; it < steps; ++it) {
+          const int t = tof(it);
+          if (t < 0) continue;
+          const size_t i = stepwise ? (((size_t)l * steps + it) * gx + w) : (((size_t)l * gx + w) * steps + it);
+          const unsigned long long a = h[i * 8 + 1], b = h[i * 8 + 6];
+          if (!a || !b) continue;
+          Agg& g = rec[(size_t)l * T + t];
+          g.s = g.s == kNone ? a : std::max(g.s, a);  // all CTAs' inputs available (W.x fused)
+          if (b >= g.e) {
+            g.e = b;
+            g.w = w;
+          }
+        }
+    for (int l = 0; l < L; ++l)
+      for (int t = 0; t < T; ++t) {
+        const int host = dir == 0 ? l : l - 1;  // the step the input / output GEMM is fused into
+        if (host < 0) continue;
+        const Agg& r = rec[(size_t)host * T + t];
+        Agg& g = inp[(size_t)l * T + t];
+        g.s = r.s;
+        g.e = r.s;
+        g.w = r.w;
+      }
+  } else {
+    throw RwError{RW_EINVAL, "trace: records need the cluster, persistent or stepwise schedule"};
+  }
+  if (dir == 1) {  // INPUT_GEMM(0, t) of the backward: the dx0 GEMM
+    unsigned long long d[2] = {0, 0};
+    RW_CUDA(cudaMemcpy(d, x->trace_dx.p, 16, cudaMemcpyDeviceToHost));
+    for (int t = 0; t < T; ++t) inp[t] = Agg{d[0], d[1], 0};
+  }
+  unsigned long long t0 = kNone;
+  for (auto* v : {&rec, &inp})
+    for (const Agg& g : *v)
+      if (g.ok()) t0 = std::min(t0, g.s);
+  for (int l = 0; l < L; ++l)
+    for (int t = 0; t < T; ++t) {
+      const Agg& gi = inp[(size_t)l * T + t];
+      const Agg& gr = rec[(size_t)l * T + t];
+      if (gi.ok() || (gi.s != kNone && gi.s == gi.e))
+        out.push_back(TraceRec{l * 2 * T + t, l, t, 0, 0, gi.w, (long long)(gi.s - t0), (long long)(gi.e - t0)});
+      if (gr.ok())
+        out.push_back(TraceRec{l * 2 * T + T + t, l, t, 0, 1, gr.w, (long long)(gr.s - t0), (long long)(gr.e - t0)});
+    }
+  std::sort(out.begin(), out.end(), [](const TraceRec& a, const TraceRec& b) {
+    return a.start_ns != b.start_ns ? a.start_ns < b.start_ns : a.task_id < b.task_id;
+  });
+  return out;
+}
+
+// RW_TRACE=<csv>: the last synced pass's forward trace in write_trace_csv's schema
+// (scheduler.hpp:406-417), the backward one in <csv>.bwd.csv.
+static void dump_trace_csv(rw_ctx* x) {
+  if (x->trace_path.empty()) return;
+  for (int dir = 0; dir < 2; ++dir) {
+    std::vector<TraceRec> r;
+    try {
+      r = trace_records(x, dir);
+    } catch (const RwError&) {
+      continue;
+    }
+    if (r.empty()) continue;
+    const std::string path = dir == 0 ? x->trace_path : x->trace_path + ".bwd.csv";
+    FILE* f = fopen(path.c_str(), "w");
+    if (!f) continue;
+    fprintf(f, "task_layer,task_block,phase,worker,start_ns,end_ns\n");
+    for (const TraceRec& t : r) {
+      if (t.phase == 0)
+        fprintf(f, "%d,%d,INPUT_GEMM,%d,%lld,%lld\n", t.layer, t.block, t.worker, t.start_ns, t.end_ns);
+      else
+        fprintf(f, "%d,%d,RECURRENT_STEP(%d),%d,%lld,%lld\n", t.layer, t.block, t.step_k, t.worker, t.start_ns,
+                t.end_ns);
+    }
+    fclose(f);
+  }
+}
+
 // Write the persistent kernels' step stamps as CSV in the reference trace schema
 // (scheduler.hpp:411-417): task_layer,task_block,phase,worker,start_ns,end_ns, with
 // task_block = step, worker = CTA index within the layer, phase = fwd|bwd, and three spans
 // per (CTA, step): wait (inputs), mma (inputs ready -> accumulator), epilogue (-> published).
-void dump_trace(rw_ctx* x) {
-  if (x->trace_path.empty()) return;
-  FILE* f = fopen(x->trace_path.c_str(), "w");
+static void dump_trace(rw_ctx* x) {
+  dump_trace_csv(x);
+  if (x->trace_spans_path.empty()) return;
+  FILE* f = fopen(x->trace_spans_path.c_str(), "w");
   if (!f) return;
   fprintf(f, "task_layer,task_block,phase,worker,span,start_ns,end_ns\n");
   for (int dir = 0; dir < 2; ++dir) {
@@ -2368,6 +2552,34 @@ int rw_sync(rw_ctx* x) {
   });
 }
 
+int rw_trace_enable(rw_ctx* x, int on) {
+  return guarded(x, [&] {
+    RW_CUDA(cudaSetDevice(x->dev));
+    if (on && !x->tracing) {
+      trace_alloc(x);
+      invalidate_graphs(x);  // captured passes hold the (null) trace pointers
+    } else if (!on && x->tracing) {
+      x->tracing = false;
+      invalidate_graphs(x);
+    }
+  });
+}
+
+int rw_trace_records(rw_ctx* x, int direction, rw_trace_record* out, int capacity, int* count) {
+  return guarded(x, [&] {
+    if (!x->tracing) einval("rw_trace_records: tracing is off (rw_trace_enable)");
+    if (direction != 0 && direction != 1) einval("rw_trace_records: direction must be 0 (forward) or 1 (backward)");
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaStreamSynchronize(x->main));
+    const std::vector<TraceRec> r = trace_records(x, direction);
+    if (count) *count = (int)r.size();
+    for (int i = 0; i < (int)r.size() && out && i < capacity; ++i) {
+      const TraceRec& t = r[i];
+      out[i] = rw_trace_record{t.task_id, t.layer, t.block, t.step_k, t.phase, t.worker, t.start_ns, t.end_ns};
+    }
+  });
+}
+
 int rw_set_profiling(rw_ctx* x, int on) {
   return guarded(x, [&] { x->profiling = on != 0; });
 }
@@ -2409,6 +2621,85 @@ int rw_describe_variants(rw_ctx* x, int* fwd_pair, int* wgrad_bn) {
   });
 }
 
+// gemm (gemm.hpp:339-347) on the device: C = alpha op(A) op(B) + beta C with host column-major
+// buffers, 3xTF32 split operands (fp32-parity) on the tcgen05 GEMM with chunked fp32 promotion.
+int rw_gemm(int trans_a, int trans_b, int M, int N, int K, float alpha, const float* A, long long lda,
+            const float* B, long long ldb, float beta, float* C, long long ldc) {
+  return guarded(nullptr, [&] {
+    if (M < 0 || N < 0 || K < 0) einval("gemm: negative dimension");
+    if (M == 0 || N == 0) return;
+    if (!A || !B || !C) einval("gemm: null operand");
+    if (ldc < M || lda < (trans_a ? K : M) || ldb < (trans_b ? N : K)) einval("gemm: leading dimension too small");
+    const int prec = kTF32x3, aK = prec_atomk(prec), bn = 64;
+    const int Mp = round_up(M, kTileM), Np = round_up(N, bn), Kp = round_up(std::max(K, 1), aK);
+    const long long a_src = trans_a ? (long long)M * lda : (long long)std::max(K, 1) * lda;
+    const long long b_src = trans_b ? (long long)std::max(K, 1) * ldb : (long long)N * ldb;
+    DevBuf dA, dB, dC, errw;
+    dA.alloc(std::max<long long>(a_src, 1) * 4);
+    dB.alloc(std::max<long long>(b_src, 1) * 4);
+    dC.alloc((size_t)M * N * 4);
+    errw.alloc(16);
+    if (K > 0) {
+      RW_CUDA(cudaMemcpy(dA.p, A, (size_t)(trans_a ? (long long)(M - 1) * lda + K : (long long)(K - 1) * lda + M) * 4,
+                         cudaMemcpyHostToDevice));
+      RW_CUDA(cudaMemcpy(dB.p, B, (size_t)(trans_b ? (long long)(K - 1) * ldb + N : (long long)(N - 1) * ldb + K) * 4,
+                         cudaMemcpyHostToDevice));
+    }
+    RW_CUDA(cudaMemcpy2D(dC.p, (size_t)M * 4, C, (size_t)ldc * 4, (size_t)M * 4, N, cudaMemcpyHostToDevice));
+    ++g_launches;
+    k_scale_cols<<<grid_for((long long)M * N), 256>>>(dC.f(), M, M, N, beta);
+    if (K > 0 && alpha != 0.0f) {
+      Operand Ao, Bo;
+      Ao.alloc(prec, (size_t)Mp * Kp);
+      Bo.alloc(prec, (size_t)Np * Kp);
+      ++g_launches;
+      k_pack_gemm_operand<<<grid_for((long long)Mp * Kp), 256>>>(dA.f(), lda, M, K, trans_a, Mp, Kp, prec, Ao.p(0),
+                                                                  Ao.p(1));
+      // B' (N x K) = op(B)^T: op(B)(k, n) is B[n * ldb + k] (B stored K x N) or B[k * ldb + n] (stored N x K)
+      ++g_launches;
+      k_pack_gemm_operand<<<grid_for((long long)Np * Kp), 256>>>(dB.f(), ldb, N, K, trans_b ? 0 : 1, Np, Kp, prec,
+                                                                  Bo.p(0), Bo.p(1));
+      RW_CUDA(cudaGetLastError());
+      std::vector<CUtensorMap> maps;
+      for (int p = 0; p < 2; ++p) {
+        maps.push_back(make_map(Ao.p(p), prec, Kp, Mp, aK, kTileM));
+        maps.push_back(make_map(Bo.p(p), prec, Kp, Np, aK, gemm_box_rows(bn)));
+      }
+      DevBuf md;
+      md.alloc(maps.size() * sizeof(CUtensorMap));
+      RW_CUDA(cudaMemcpy(md.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      const CUtensorMap* MD = static_cast<const CUtensorMap*>(md.p);
+      GemmDesc g{};
+      g.error = static_cast<int*>(errw.p);
+      g.a[0] = MD + 0;
+      g.b[0] = MD + 1;
+      g.a[1] = MD + 2;
+      g.b[1] = MD + 3;
+      g.alpha = alpha;
+      g.accumulate = 1;
+      g.M = Mp;
+      g.N = Np;
+      g.K = Kp;
+      g.d = dC.f();
+      g.ldd = M;
+      g.row_mode = kRowIdentity;
+      g.col_mode = kColIdentity;
+      g.m_valid = M;
+      g.n_valid = N;
+      DevBuf gd;
+      gd.alloc(sizeof(GemmDesc));
+      RW_CUDA(cudaMemcpy(gd.p, &g, sizeof g, cudaMemcpyHostToDevice));
+      launch_gemm<PrecTF32x3, false, false>(static_cast<const GemmDesc*>(gd.p), 1, Mp, Np, bn,
+                                           gemm_stages(2, bn), 0);
+    }
+    RW_CUDA(cudaDeviceSynchronize());
+    int ew = 0;
+    RW_CUDA(cudaMemcpy(&ew, errw.p, 4, cudaMemcpyDeviceToHost));
+    if (ew) throw RwError{RW_ESTATE, "gemm: a pipeline barrier wait timed out"};
+    RW_CUDA(cudaMemcpy2D(C, (size_t)ldc * 4, dC.p, (size_t)M * 4, (size_t)M * 4, N, cudaMemcpyDeviceToHost));
+  });
+}
+
 static float g_test_gemm_ms = 0.0f;
 float rw_test_gemm_last_ms(void) { return g_test_gemm_ms; }
 
@@ -2419,6 +2710,7 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     const int prec = precision == RW_PREC_BF16 ? kBF16 : precision == 2 ? kF16x2 : kTF32x3;
     const int aK = prec_atomk(prec);
     if (M % 128 || N % bn || K % 64 || (bn != 64 && bn != 128 && bn != 256)) einval("rw_test_gemm: bad shape");
+    if (prec != kBF16 && bn == 256) einval("rw_test_gemm: two-plane operands take bn 64 or 128");
     if (prec == kTF32x3 && (a_mn || b_mn)) einval("rw_test_gemm: tf32 operands must be K-major");
     // element counts of the stored operands
     const long long a_elems = a_mn ? (long long)K * lda : (long long)M * lda;
@@ -2440,7 +2732,11 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     md.alloc(maps.size() * sizeof(CUtensorMap));
     RW_CUDA(cudaMemcpy(md.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     const CUtensorMap* MD = static_cast<const CUtensorMap*>(md.p);
+    DevBuf errw;
+    errw.alloc(16);
+    RW_CUDA(cudaMemset(errw.p, 0, 16));
     GemmDesc g{};
+    g.error = static_cast<int*>(errw.p);
     g.a[0] = MD + 0;
     g.b[0] = MD + 1;
     if (prec != kBF16) {
@@ -2480,6 +2776,9 @@ int rw_test_gemm(int precision, int a_mn, int b_mn, int M, int N, int K, const f
     }
     cudaEventRecord(e1, 0);
     RW_CUDA(cudaDeviceSynchronize());
+    int ew = 0;
+    RW_CUDA(cudaMemcpy(&ew, errw.p, 4, cudaMemcpyDeviceToHost));
+    if (ew) throw RwError{RW_ESTATE, "rw_test_gemm: a pipeline barrier wait timed out"};
     cudaEventElapsedTime(&g_test_gemm_ms, e0, e1);
     g_test_gemm_ms /= reps;
     cudaEventDestroy(e0);

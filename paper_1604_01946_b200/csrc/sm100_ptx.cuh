@@ -69,23 +69,35 @@ RW_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
-RW_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
-#pragma unroll 1
-  while (!mbar_try_wait(bar, phase)) {
-  }
-}
-// Bounded variant for the GEMM kernels (no flag protocol of their own): a wait that has not
-// completed after `kGemmWaitNs` traps, so a lost arrival surfaces as a launch error on the
-// host instead of a GPU that never returns.
-constexpr unsigned long long kGemmWaitNs = 20ULL * 1000000000ULL;
-RW_DEVICE void mbar_wait_bounded(uint64_t* bar, uint32_t phase) {
-  if (mbar_try_wait(bar, phase)) return;
+// Every mbarrier wait is bounded. A kernel stores its context's error word in `rw_wait_err`
+// (set_wait_error, before its first __syncthreads). A wait still incomplete after kWaitNs records
+// kWaitTimeoutCode there and returns; once the word is set, every later slow wait of the
+// launch returns too, so a lost arrival ends the launch within seconds and the host reports
+// RW_ESTATE (rw_sync) instead of a GPU that never returns or a sticky trap. Only a kernel
+// without an error word (none in this library) traps. The fast path is one try_wait.
+constexpr unsigned long long kWaitNs = 20ULL * 1000000000ULL;
+constexpr int kWaitTimeoutCode = (1 << 30) | (3 << 28) | 15;
+static __shared__ int* rw_wait_err;
+RW_DEVICE void set_wait_error(int* e) { rw_wait_err = e; }
+RW_DEVICE bool mbar_wait_slow(uint64_t* bar, uint32_t phase) {
   const uint64_t t0 = globaltimer();
+  int* const err = rw_wait_err;
 #pragma unroll 1
   while (!mbar_try_wait(bar, phase)) {
-    if (globaltimer() - t0 > kGemmWaitNs) __trap();
+    const uint64_t dt = globaltimer() - t0;
+    if (dt > 1000000ULL && err && *reinterpret_cast<volatile int*>(err) != 0) return false;  // abandoned launch
+    if (dt > kWaitNs) {
+      if (!err) __trap();
+      atomicCAS(err, 0, kWaitTimeoutCode);
+      return false;
+    }
   }
+  return true;
 }
+RW_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
+  if (!mbar_try_wait(bar, phase)) mbar_wait_slow(bar, phase);
+}
+RW_DEVICE void mbar_wait_bounded(uint64_t* bar, uint32_t phase) { mbar_wait(bar, phase); }
 
 // ------------------------------------------------------------------ TMA
 RW_DEVICE void prefetch_tmap(const CUtensorMap* m) {

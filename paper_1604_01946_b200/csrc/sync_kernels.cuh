@@ -30,4 +30,8 @@ __global__ void k_pp_wait(const uint32_t* ready, const uint32_t* my_epoch, int* 
   } while (!flag_reached(v, e));
 }
 
+// Device timestamp (%globaltimer ns) of a point in stream order: brackets launches that carry no
+// stamps of their own (the dx0 GEMM, the backward trace's INPUT_GEMM of layer 0).
+__global__ void k_stamp(unsigned long long* p) { *p = globaltimer(); }
+
 }  // namespace rw

@@ -231,6 +231,19 @@ class ForwardTape:
 
 
 @dataclass
+class TraceRecord:
+    """sched::TraceRecord (scheduler.hpp:180-192); phase "INPUT_GEMM" | "RECURRENT_STEP"."""
+    task_id: int
+    layer: int
+    block: int
+    step_k: int
+    phase: str
+    worker: int
+    start_ns: int
+    end_ns: int
+
+
+@dataclass
 class ForwardResult:
     y: np.ndarray
     tape: ForwardTape
@@ -320,8 +333,28 @@ class Engine:
     def config(self) -> LadderConfig:
         return self.cfg
 
-    def set_trace_sink(self, sink) -> None:  # engine.hpp:79 (trace recording: see DESIGN.md)
+    def set_trace_sink(self, sink) -> None:
+        """engine.hpp:79-80: when set (a list), every forward / backward_data replaces its contents
+        with the pass's schedule trace -- TraceRecord(task_id, layer, block, step_k, phase,
+        worker, start_ns, end_ns) per device task, ids of build_graph(L, T, 1)
+        (scheduler.hpp:96-155, 180-192; rw_trace_records)."""
         self._trace_sink = sink
+        self._check(self._L.rw_trace_enable(self._ctx, 1 if sink is not None else 0))
+
+    def trace_records(self, direction: int) -> list:
+        """The last pass's trace of one direction (0 forward, 1 backward)."""
+        n = C.c_int()
+        self._check(self._L.rw_trace_records(self._ctx, direction, None, 0, C.byref(n)))
+        buf = (_lib.rw_trace_record * max(n.value, 1))()
+        self._check(self._L.rw_trace_records(self._ctx, direction, buf, n.value, C.byref(n)))
+        return [TraceRecord(r.task_id, r.layer, r.block, r.step_k,
+                            "INPUT_GEMM" if r.phase == 0 else "RECURRENT_STEP", r.worker,
+                            r.start_ns, r.end_ns) for r in buf[:n.value]]
+
+    def _deposit_trace(self, direction: int) -> None:
+        sink = getattr(self, "_trace_sink", None)
+        if sink is not None:
+            sink[:] = self.trace_records(direction)
 
     # -- plumbing
     def _check(self, status: int) -> None:
@@ -381,6 +414,7 @@ class Engine:
         self._check(self._L.rw_forward(self._ctx, _fp(x), int(bool(training)), arr(hs), arr(cs),
                                        _fp(y), C.byref(tid)))
         self._tape_id = tid.value
+        self._deposit_trace(0)
         tape = ForwardTape(LadderConfig(**c.__dict__), bool(training), self, tid.value, x.copy(order="F"))
         return ForwardResult(y, tape)
 
@@ -410,6 +444,7 @@ class Engine:
         arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst])  # noqa: E731
         self._check(self._L.rw_backward_data(self._ctx, tape._id, _fp(dy), _fp(dx0), arr(dh0), arr(dc0)))
         self._bwd_id = tape._id
+        self._deposit_trace(1)
         return BackwardState(dx0, dh0, dc0, self, tape._id)
 
     def weight_update(self, tape: ForwardTape, state: BackwardState) -> Gradients:

@@ -1,4 +1,4 @@
-"""Run one config-B training pass with the device trace on (RW_TRACE) and summarise where a
+"""Run one config-B training pass with the device span trace on (RW_TRACE_SPANS) and summarise where a
 recurrent step's time goes. Usage (GPU box): python profiles/trace_run.py [bf16|fp32] [out.csv] [bench config, default B]
 """
 import csv
@@ -66,7 +66,7 @@ def summarize(path):
 def main():
     prec = sys.argv[1] if len(sys.argv) > 1 else "bf16"
     path = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", f"trace_{prec}.csv")
-    os.environ["RW_TRACE"] = path
+    os.environ["RW_TRACE_SPANS"] = path
     from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
     name = sys.argv[3] if len(sys.argv) > 3 else "B"
     import bench

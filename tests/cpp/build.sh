@@ -10,3 +10,12 @@ g++ -std=c++17 -O2 -I"$ROOT/include" -I"$ROOT/oracle" "$HERE/facade_parity.cpp" 
     -L"$ROOT/paper_1604_01946_b200/lib" -lrnnwave_sm100 -Wl,-rpath,"$ROOT/paper_1604_01946_b200/lib" \
     -Wl,-rpath,'$ORIGIN/../../../paper_1604_01946_b200/lib' -o "$HERE/build/facade_parity"
 echo "$HERE/build/facade_parity"
+# The reference's own harness (verify.hpp / oracle.hpp / scheduler.hpp, unmodified) against the
+# facade: only where the reference sources exist (this container); the binary travels to the box.
+REF=/root/reference/proj/include
+if [ -d "$REF/rnnwave" ]; then
+  g++ -std=c++20 -O2 -ffp-contract=off -I"$ROOT/include" -I"$REF" "$HERE/reference_harness.cpp" \
+      -L"$ROOT/paper_1604_01946_b200/lib" -lrnnwave_sm100 -pthread -Wl,-rpath,"$ROOT/paper_1604_01946_b200/lib" \
+      -Wl,-rpath,'$ORIGIN/../../../paper_1604_01946_b200/lib' -o "$HERE/build/reference_harness"
+  echo "$HERE/build/reference_harness"
+fi

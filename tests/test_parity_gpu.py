@@ -132,12 +132,14 @@ def test_config_b_full(reference, precision):
     print(f"config B {precision} {eng.describe()}: worst {worst}")
 
 
-@pytest.mark.parametrize("schedule", ["persistent", "cluster"])
-def test_deterministic_repeat(schedule):
-    """Run-to-run bitwise identity on the device (the analogue of acceptance crit 8)."""
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("schedule", ["stepwise", "persistent", "cluster", "layerseq"])
+def test_deterministic_repeat(schedule, precision):
+    """Run-to-run bitwise identity on the device (the analogue of acceptance crit 8): fixed
+    split-K reduction orders, no float atomics, in every schedule and both precisions."""
     from paper_1604_01946_b200 import Engine
     c, params, x, dy, h0, c0 = make_case(Dims(2, 128, 96, 32, 12), seed=3, bias=True)
-    eng = make_engine(Engine, c, "bf16", schedule)
+    eng = make_engine(Engine, c, precision, schedule)
     a = run_device(eng, params, x, dy, h0, c0)
     b = run_device(eng, params, x, dy, h0, c0)
     for k in a:
@@ -258,25 +260,48 @@ def test_state_blocks_restaged_after_explicit_h0(schedule):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
-def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch):
-    """RW_TRACE writes the recurrent kernels' stamps in the reference's trace schema; like the
-    reference's validate_trace, every dependency's end precedes its dependent's start
-    (profiles/validate_trace.py)."""
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("schedule", ["cluster", "persistent", "stepwise"])
+def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch, schedule, precision):
+    """set_trace_sink / RW_TRACE: the recurrent kernels' device stamps as the reference's schedule
+    trace (scheduler.hpp:180-192, 406-417). Like the reference's validate_trace, every task of
+    build_graph(L, T, 1) appears exactly once and every dependency ends before its dependent
+    starts -- forward and (reversed graph) backward (profiles/validate_trace.py)."""
+    import csv
     import importlib.util
     import os as _os
     from paper_1604_01946_b200 import Engine
     from oracle import Dims
     path = tmp_path / "trace.csv"
     monkeypatch.setenv("RW_TRACE", str(path))
-    c, params, x, dy, h0, c0 = make_case(Dims(3, 512, 512, 64, 8), seed=43, bias=True, state=False)
-    eng = make_engine(Engine, c, "bf16", "cluster")
-    eng.set_params(params)
-    eng.upload_inputs(x, dy)
-    eng.run_pass(2)
-    eng.sync()
+    c, params, x, dy, h0, c0 = make_case(Dims(3, 256, 192, 64, 8), seed=43, bias=True, state=False)
+    eng = make_engine(Engine, c, precision, schedule)
+    sink = []
+    eng.set_trace_sink(sink)
+    fwd = eng.forward(params, x, True)
+    fwd_sink = list(sink)
+    eng.backward_data(params, fwd.tape, dy)
     root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
     spec = importlib.util.spec_from_file_location("vt", _os.path.join(root, "profiles", "validate_trace.py"))
     vt = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(vt)
+
+    def rows(recs):
+        return [{"task_layer": r.layer, "task_block": r.block,
+                 "phase": "INPUT_GEMM" if r.phase == "INPUT_GEMM" else f"RECURRENT_STEP({r.step_k})",
+                 "worker": r.worker, "start_ns": r.start_ns, "end_ns": r.end_ns} for r in recs]
+    L, T = c.layers, c.steps
+    assert len(fwd_sink) == 2 * L * T and len(sink) == 2 * L * T
+    assert vt.validate_rows(rows(fwd_sink), L, T, "fwd") is None
+    assert vt.validate_rows(rows(sink), L, T, "bwd") is None
+    ids = sorted(r.task_id for r in fwd_sink)
+    assert ids == list(range(2 * L * T))  # build_graph(L, T, 1) ids, each once
+    # RW_TRACE wrote the same forward schedule (last synced forward) as CSV
+    eng.upload_inputs(x, dy)
+    eng.run_pass(0)
+    eng.sync()
     assert path.exists()
-    assert vt.validate(str(path)) is None
+    with open(path) as f:
+        hdr = f.readline().strip()
+    assert hdr == "task_layer,task_block,phase,worker,start_ns,end_ns"
+    assert vt.validate(str(path), L, T, "fwd") is None

@@ -1,5 +1,6 @@
-"""CPU: profiles/validate_trace.py flags a violated wavefront edge and accepts a consistent
-trace (synthetic CSVs in the device trace schema)."""
+"""CPU: profiles/validate_trace.py (the reference's validate_trace, scheduler.hpp:371-404, over
+build_graph(L, T, 1)) accepts a consistent trace in the write_trace_csv schema and reports
+missing / duplicate tasks and violated forward and backward edges (synthetic CSVs)."""
 import importlib.util
 import os
 
@@ -8,7 +9,22 @@ _spec = importlib.util.spec_from_file_location("vt", os.path.join(ROOT, "profile
 vt = importlib.util.module_from_spec(_spec)
 _spec.loader.exec_module(vt)
 
-HDR = "task_layer,task_block,phase,worker,span,start_ns,end_ns\n"
+HDR = "task_layer,task_block,phase,worker,start_ns,end_ns\n"
+
+
+def wavefront(L, T, reverse=False):
+    """A consistent schedule: task (l, t) at diagonal slot l + t (forward) or the mirror."""
+    rows = []
+    for l in range(L):
+        for t in range(T):
+            d = (l + t) if not reverse else ((L - 1 - l) + (T - 1 - t))
+            if not reverse:
+                rows.append((l, t, "INPUT_GEMM", 0, 100 * d, 100 * d + 10))
+                rows.append((l, t, "RECURRENT_STEP(0)", 1, 100 * d + 20, 100 * d + 90))
+            else:  # reversed graph: the output GEMM (INPUT_GEMM) runs after the step
+                rows.append((l, t, "RECURRENT_STEP(0)", 1, 100 * d, 100 * d + 60))
+                rows.append((l, t, "INPUT_GEMM", 0, 100 * d + 70, 100 * d + 90))
+    return rows
 
 
 def _write(tmp_path, rows):
@@ -17,24 +33,35 @@ def _write(tmp_path, rows):
     return str(p)
 
 
-def test_consistent_trace_passes(tmp_path):
-    rows = []
-    for t in range(3):
-        for w in range(2):
-            rows.append((0, t, "fwd", w, "wait", 100 * t, 100 * t + 10))
-            rows.append((0, t, "fwd", w, "publish", 100 * t + 50, 100 * t + 60 + w))
-    assert vt.validate(_write(tmp_path, rows)) is None
+def test_consistent_traces_pass(tmp_path):
+    assert vt.validate(_write(tmp_path, wavefront(3, 4)), 3, 4, "fwd") is None
+    assert vt.validate(_write(tmp_path, wavefront(3, 4, True)), 3, 4, "bwd") is None
+
+
+def test_missing_and_duplicate_tasks_are_reported(tmp_path):
+    rows = wavefront(2, 3)
+    v = vt.validate(_write(tmp_path, rows[:-1]), 2, 3)
+    assert v is not None and "records" in v
+    v = vt.validate(_write(tmp_path, rows[:-1] + [rows[0]]), 2, 3)
+    assert v is not None and "more than once" in v
 
 
 def test_violated_recurrence_edge_is_reported(tmp_path):
-    rows = [(0, 0, "fwd", 0, "publish", 50, 200), (0, 1, "fwd", 0, "wait", 100, 150),
-            (0, 1, "fwd", 0, "publish", 300, 310)]
-    v = vt.validate(_write(tmp_path, rows))
+    rows = wavefront(1, 3)
+    rows[1] = (0, 0, "RECURRENT_STEP(0)", 1, 20, 250)  # step 0 ends after step 1 starts
+    v = vt.validate(_write(tmp_path, rows), 1, 3)
     assert v is not None and "edge violated" in v
 
 
 def test_violated_layer_edge_is_reported(tmp_path):
-    rows = [(0, 0, "fwd", 0, "publish", 50, 200), (1, 0, "fwd", 0, "offload", 150, 160),
-            (1, 0, "fwd", 0, "publish", 300, 310)]
-    v = vt.validate(_write(tmp_path, rows))
-    assert v is not None and "off-critical" in v
+    rows = wavefront(2, 2)
+    rows = [r if not (r[0] == 1 and r[1] == 0 and r[2] == "INPUT_GEMM") else (1, 0, "INPUT_GEMM", 0, 50, 60)
+            for r in rows]  # layer 1's W.x_0 starts before layer 0's step 0 ends
+    v = vt.validate(_write(tmp_path, rows), 2, 2)
+    assert v is not None and "edge violated" in v
+
+
+def test_backward_edges_are_reversed(tmp_path):
+    # a forward-consistent trace violates the reversed graph
+    v = vt.validate(_write(tmp_path, wavefront(2, 3)), 2, 3, "bwd")
+    assert v is not None and "edge violated" in v
