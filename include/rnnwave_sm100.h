@@ -216,6 +216,9 @@ int rw_pp_export(rw_ctx* ctx, int dir, rw_pp_ring* out);
 /* dir 0: link to the NEXT stage's forward export; W_next is the next stage's first-layer W
  * (4H x H, reference layout, host). dir 1: link to the PREVIOUS stage's backward export. */
 int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next);
+/* The next stage's first-layer W (4H x H, reference layout) after a parameter update: the
+ * forward boundary group re-packs it with this stage's next pass. */
+int rw_pp_set_next_w(rw_ctx* ctx, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
 /* gemm (gemm.hpp:339-347, the reference's ordered fp32 GEMM) on the device: C (M x N) =

@@ -29,7 +29,7 @@ EXPORTS = [
     "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count", "rw_params_updated",
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_describe_variants",
     "rw_describe_precision", "rw_flop_count_cell",
-    "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link",
+    "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link", "rw_pp_set_next_w",
     "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm",
 ]
 
@@ -53,9 +53,27 @@ def lib_path() -> str:
     return _build.LIB
 
 
+def _nccl_hint() -> None:
+    """Point the library's lazy NCCL dlopen at the NCCL PyTorch links (the nvidia-nccl wheel), so
+    both share one libnccl.so.2 in a process (runtime.cu nccl())."""
+    if os.environ.get("RW_NCCL_PATH"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["RW_NCCL_PATH"] = p
+                return
+    except (ImportError, ValueError):
+        pass
+
+
 def load(build_if_missing: bool = True) -> C.CDLL:
     """Load (building first if needed and possible) the sm_100a library."""
     global _lib
+    _nccl_hint()
     if _lib is not None:
         return _lib
     path = lib_path()
@@ -98,6 +116,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                C.c_longlong, vp, C.c_longlong, vp, C.c_longlong, C.c_int]
     L.rw_pp_export.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring)]
     L.rw_pp_link.argtypes = [vp, C.c_int, C.POINTER(rw_pp_ring), _F]
+    L.rw_pp_set_next_w.argtypes = [vp, _F]
     L.rw_pp_debug.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.rw_train_step.argtypes = [vp, _F, _F, _F, _F, _PF, _PF, _PF]
     L.rw_train_wait.argtypes = [vp]

@@ -114,8 +114,12 @@ struct RecParams {
                       // DSMEM offsets of the receive buffer / barriers match across ranks)
   int acc_kb;         // k-blocks per TMEM accumulator (fp32 promotion); accumulators summed
   int n_acc;          // in fp32 by the epilogue (1 = single accumulator)
-  int promo;          // 3xTF32 long K: promotion ring (promo_drain) -- acc_kb k-blocks per chunk,
-                      // n_acc slots after the fp32 sum region (TMEM: N x (1 + n_acc) columns)
+  int promo;          // promotion ring (promo_drain) -- acc_kb k-blocks per chunk, n_acc slots after
+                      // the fp32 sum region (TMEM: N x (1 + n_acc) columns); chunks never straddle
+                      // the two K segments (fwd W.x | R.h, bwd W_{l+1}^T.dG | R^T.dG)
+  float us_in0, us_in, us_rec;  // fp16x2 unscale of a chunk's product (common.cuh): K segment 0 of
+                      // layer 0 / of layers >= 1, segment 1 -- applied by the drain (1 otherwise)
+  unsigned* gmax;     // backward, fp16x2: max |dG| of the pass (range check of the scaled planes)
   int stages;
   int a_prefetch;     // streamed A: L2 prefetch distance in k-blocks (0 = off)
   uint32_t flag_target;
@@ -145,6 +149,10 @@ __device__ __forceinline__ void progress(const RecParams& p, int role, int it, i
 }
 
 // ------------------------------------------------------------------ small helpers
+// fp16x2 split operands (common.cuh PrecF16x2): operand planes carry power-of-two scales
+template <class P>
+constexpr bool kF16Ops = P::kPlanes == 2 && !P::kTF32;
+
 template <class P>
 __device__ __forceinline__ void store_operand(void* const* planes, long long idx, float v) {
   if constexpr (P::kPlanes == 1) {
@@ -163,9 +171,29 @@ __device__ __forceinline__ void store_operand(void* const* planes, long long idx
   }
 }
 
-// Activations. fp32-parity mode keeps the reference's accurate libm chain
-// (sigmoid = 1/(1+exp(-x)), cells.hpp:30; tanh); bf16 mode uses the SFU approximations
-// (relative error ~2^-11, far below the bf16 operand rounding it already carries).
+// Activations (the reference's definitions: sigmoid = 1/(1+exp(-x)), cells.hpp:30; tanh).
+// bf16 mode: the SFU approximations (relative error ~2^-11, far below the bf16 operand rounding
+// it already carries). fp32-parity mode: exp with a two-constant ln2 range reduction and
+// a degree-6 polynomial on the reduced argument (|f| <= ln2/2; the Cephes expf coefficients,
+// ~1 ulp -- MUFU.EX2 alone measured 2e-5 normwise at config B), IEEE reciprocals, and
+// tanh(x) = sign(x) (1 - 2 / (1 + e^{2|x|})) above |x| = 0.625, Cephes' odd polynomial below
+// (relative error ~2e-7 throughout) -- a fraction of the fp32
+// rounding the 1e-5 contract allows, at a fraction of the instructions of libm expf / tanhf and
+// IEEE division.
+__device__ __forceinline__ float exp_rr(float x) {
+  x = fminf(fmaxf(x, -87.0f), 88.0f);
+  const float n = rintf(x * 1.44269504088896341f);
+  float f = fmaf(n, -0.693145751953125f, x);
+  f = fmaf(n, -1.428606765330187045e-06f, f);
+  float p = 1.9875691500e-4f;
+  p = fmaf(p, f, 1.3981999507e-3f);
+  p = fmaf(p, f, 8.3334519073e-3f);
+  p = fmaf(p, f, 4.1665795894e-2f);
+  p = fmaf(p, f, 1.6666665459e-1f);
+  p = fmaf(p, f, 5.0000001201e-1f);
+  const float e = fmaf(p, f * f, f) + 1.0f;
+  return e * __int_as_float(((int)n + 127) << 23);
+}
 template <class P>
 __device__ __forceinline__ float act_sigmoid(float x) {
   if constexpr (P::kPlanes == 1) {
@@ -174,7 +202,7 @@ __device__ __forceinline__ float act_sigmoid(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(0.5f * x));
     return fmaf(0.5f, y, 0.5f);
   } else {
-    return 1.0f / (1.0f + expf(-x));
+    return __frcp_rn(1.0f + exp_rr(-x));
   }
 }
 template <class P>
@@ -184,7 +212,18 @@ __device__ __forceinline__ float act_tanh(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
   } else {
-    return tanhf(x);
+    const float a = fabsf(x);
+    if (a < 0.625f) {  // Cephes tanhf odd polynomial (relative error ~1e-7)
+      const float z = x * x;
+      float p = -5.70498872745e-3f;
+      p = fmaf(p, z, 2.06390887954e-2f);
+      p = fmaf(p, z, -5.37397155531e-2f);
+      p = fmaf(p, z, 1.33314422036e-1f);
+      p = fmaf(p, z, -3.33332819422e-1f);
+      return fmaf(p * z, x, x);
+    }
+    const float t = fmaf(-2.0f, __frcp_rn(1.0f + exp_rr(2.0f * a)), 1.0f);
+    return copysignf(t, x);
   }
 }
 
@@ -474,12 +513,16 @@ __device__ __forceinline__ void rec_teardown(int ks, uint32_t tmem_base, uint32_
 // order: deterministic). Slot handshake: pfull (MMA commit) / pempty (kEpiThreads arrivals).
 // Each thread touches only the TMEM cells it later reads in the step's final drain (its lane
 // row, its half of every kXChunk column chunk), so no cross-thread ordering is needed.
+// `nc0` chunks of K segment 0 come first, then segment 1's; a chunk's product is scaled by `sc0` /
+// `sc1` (fp16x2 operand scales, exact powers of two) as it is added.
 __device__ __forceinline__ void promo_drain(const RecSmem& S, const RecParams& p, uint32_t tmem_base, int N,
-                                            int nchunks, uint32_t& ech) {
+                                            int nchunks, uint32_t& ech, int nc0 = 0, float sc0 = 1.0f,
+                                            float sc1 = 1.0f) {
   const int warp = threadIdx.x >> 5, q = warp & 3, half = (warp - 4) >> 2;
   const uint32_t lane_off = uint32_t(q * 32) << 16;
   for (int c = 0; c < nchunks; ++c, ++ech) {
     const uint32_t slot = ech % (uint32_t)p.n_acc;
+    const float sc = c < nc0 ? sc0 : sc1;
     mbar_wait(&S.pfull[slot], (ech / (uint32_t)p.n_acc) & 1);
     tc_fence_after();
     const uint32_t src = tmem_base + lane_off + (1 + slot) * N, dst = tmem_base + lane_off;
@@ -490,9 +533,10 @@ __device__ __forceinline__ void promo_drain(const RecSmem& S, const RecParams& p
         tmem_ld_32x32b_x8(src + c0, v);
         if (c > 0) tmem_ld_32x32b_x8(dst + c0, w);
         tmem_ld_wait();
-        if (c > 0) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = __float_as_uint(__uint_as_float(w[j]) + __uint_as_float(v[j]));
+        for (int j = 0; j < 8; ++j) {
+          const float x = __uint_as_float(v[j]) * sc;
+          v[j] = __float_as_uint(c > 0 ? __uint_as_float(w[j]) + x : x);
         }
         tmem_st_32x32b_x8(dst + c0, v);
       }
@@ -502,12 +546,12 @@ __device__ __forceinline__ void promo_drain(const RecSmem& S, const RecParams& p
     mbar_arrive(&S.pempty[slot]);
   }
 }
-// MMA side of the ring: called with the index (among this step's active k-blocks) of the
-// k-block about to be issued; returns its slot accumulator and whether it starts a chunk.
+// MMA side of the ring: the slot accumulator of chunk `ch` (waits for it to be drained when the
+// k-block about to be issued starts the chunk).
 __device__ __forceinline__ uint32_t promo_slot(const RecSmem& S, const RecParams& p, uint32_t tmem_base, int N,
-                                               int nact, uint32_t ch) {
+                                               bool start, uint32_t ch) {
   const uint32_t slot = ch % (uint32_t)p.n_acc;
-  if (nact % p.acc_kb == 0 && ch >= (uint32_t)p.n_acc) {
+  if (start && ch >= (uint32_t)p.n_acc) {
     mbar_wait(&S.pempty[slot], ((ch / (uint32_t)p.n_acc) - 1) & 1);
     tc_fence_after();
   }
@@ -688,6 +732,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     if (p.resident) mbar_wait(S.a_full, 0);
     tc_fence_after();
     uint32_t pc = 0, ch = 0;
+    const int s0_hi = min(kb_hi, nkb0);  // this CTA's K segment 0 (W.x) is [kb_lo, s0_hi)
     for (int it = 0; it < p.n_steps; ++it) {
       progress(p, 1, it, 1);
       if (it > 0 && !p.promo) {
@@ -698,15 +743,19 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const int s = pc % p.stages;
         const int nact = kb - kb_lo;
-        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, nact, ch)
+        // promotion chunks restart at the segment boundary (their products carry different scales)
+        const int iseg = kb < nkb0 ? kb - kb_lo : kb - max(kb_lo, nkb0);
+        const int nseg = kb < nkb0 ? s0_hi - kb_lo : kb_hi - max(kb_lo, nkb0);
+        const bool cstart = p.promo ? iseg % p.acc_kb == 0 : nact % p.acc_kb == 0;
+        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch)
                                      : tmem_base + (nact / p.acc_kb) * N;  // accumulator of this k-block
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
-        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, nact % p.acc_kb == 0);
+        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, cstart);
         umma_commit_warp(&S.empty[s]);
-        if (p.promo && ((nact + 1) % p.acc_kb == 0 || kb + 1 == kb_hi)) {
+        if (p.promo && ((iseg + 1) % p.acc_kb == 0 || iseg + 1 == nseg)) {
           umma_commit_warp(&S.pfull[ch % (uint32_t)p.n_acc]);
           ++ch;
         }
@@ -727,14 +776,17 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const long long Hp = p.Hp, G4 = 4 * Hp;
     const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u],
                 bc = Le.bias[3 * Hp + u];
-    const int n_chunks = kPair ? 1 : (my_nkb + p.acc_kb - 1) / p.acc_kb;
+    const int n_s0 = max(0, min(kb_hi, nkb0) - kb_lo), n_s1 = my_nkb - n_s0;  // k-blocks per K segment
+    const int nc0 = (n_s0 + p.acc_kb - 1) / p.acc_kb;
+    const int n_chunks = kPair ? 1 : p.promo ? nc0 + (n_s1 + p.acc_kb - 1) / p.acc_kb : (my_nkb + p.acc_kb - 1) / p.acc_kb;
     const int n_used = p.promo ? (n_chunks > 0 ? 1 : 0) : n_chunks;
+    const float sc0 = l == 0 ? p.us_in0 : p.us_in;
     uint32_t xc = 0, ech = 0;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
       if (et == 0) progress(p, 2, it, 1);
       if (p.promo) {
-        promo_drain(S, p, tmem_base, N, n_chunks, ech);
+        promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, sc0, p.us_rec);
       } else {
         mbar_wait(S.tmem_full, it & 1);
         tc_fence_after();
@@ -796,7 +848,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const long long col_new = col_prev + p.Bp;  // block t+1 (c_t, h_t)
           Le.c[col_new * Hp + u] = cv;
           Le.h[col_new * Hp + u] = hv;
-          store_operand<P>(Le.hop, col_new * Hp + u, hv);
+          store_operand<P>(Le.hop, col_new * Hp + u, kF16Ops<P> ? hv * pow2f(kHScaleLog2) : hv);
           if (Le.gates) {
             float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv;
@@ -1004,21 +1056,25 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
       }
       progress(p, 1, it, 2);
-      int ntot = 0;  // active k-blocks of this step (the ring closes its last chunk on the last one)
-      for (int kb = kb_lo; kb < kb_hi; ++kb) ntot += kb_active(kb, t) ? 1 : 0;
-      int nact = 0;  // active k-blocks so far this step
+      // active k-blocks of this step per K segment (the ring closes a chunk on each segment's last)
+      int nseg[2] = {0, 0};
+      for (int kb = kb_lo; kb < kb_hi; ++kb) nseg[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
+      int nact = 0, iseg[2] = {0, 0};  // active k-blocks so far this step (overall, per segment)
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
         const int s = pc % p.stages;
-        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, nact, ch) : tmem_base + (nact / p.acc_kb) * N;
+        const int sg = kb < nkb0 ? 0 : 1;
+        const bool cstart = p.promo ? iseg[sg] % p.acc_kb == 0 : nact % p.acc_kb == 0;
+        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch) : tmem_base + (nact / p.acc_kb) * N;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
-        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, nact % p.acc_kb == 0);
+        mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, cstart);
         ++nact;
+        ++iseg[sg];
         umma_commit_warp(&S.empty[s]);
-        if (p.promo && (nact % p.acc_kb == 0 || nact == ntot)) {
+        if (p.promo && (iseg[sg] % p.acc_kb == 0 || iseg[sg] == nseg[sg])) {
           umma_commit_warp(&S.pfull[ch % (uint32_t)p.n_acc]);
           ++ch;
         }
@@ -1037,15 +1093,19 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const int u = row0 + ul;
     const long long Hp = p.Hp, G4 = 4 * Hp;
     uint32_t xc = 0, ech = 0;
+    constexpr float kGS = kF16Ops<P> ? pow2f(kGScaleLog2) : 1.0f;  // dG operand plane scale
+    float gmax = 0.0f;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
-      int nact = 0;
-      for (int kb = kb_lo; kb < kb_hi; ++kb) nact += kb_active(kb, t) ? 1 : 0;
-      const int n_chunks = (nact + p.acc_kb - 1) / p.acc_kb;
+      int ns[2] = {0, 0};
+      for (int kb = kb_lo; kb < kb_hi; ++kb) ns[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
+      const int nact = ns[0] + ns[1];
+      const int nc0 = (ns[0] + p.acc_kb - 1) / p.acc_kb;
+      const int n_chunks = (!kPair && p.promo) ? nc0 + (ns[1] + p.acc_kb - 1) / p.acc_kb : (nact + p.acc_kb - 1) / p.acc_kb;
       const int n_used = (!kPair && p.promo) ? (n_chunks > 0 ? 1 : 0) : n_chunks;
       if (et == 0) progress(p, 2, it, 1);
       if (!kPair && p.promo) {
-        promo_drain(S, p, tmem_base, N, n_chunks, ech);
+        promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, p.us_in, p.us_rec);
       } else {
         mbar_wait(S.tmem_full, it & 1);
         tc_fence_after();
@@ -1133,10 +1193,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               dgp[2 * Hp] = go;
               dgp[3 * Hp] = gc;
               const long long ob = col * G4;
-              store_operand<P>(Le.dgop, ob + rho_of(0, u), gi);
-              store_operand<P>(Le.dgop, ob + rho_of(1, u), gf);
-              store_operand<P>(Le.dgop, ob + rho_of(2, u), go);
-              store_operand<P>(Le.dgop, ob + rho_of(3, u), gc);
+              store_operand<P>(Le.dgop, ob + rho_of(0, u), gi * kGS);
+              store_operand<P>(Le.dgop, ob + rho_of(1, u), gf * kGS);
+              store_operand<P>(Le.dgop, ob + rho_of(2, u), go * kGS);
+              store_operand<P>(Le.dgop, ob + rho_of(3, u), gc * kGS);
+              if constexpr (kF16Ops<P>) gmax = fmaxf(gmax, fmaxf(fmaxf(fabsf(gi), fabsf(gf)), fmaxf(fabsf(go), fabsf(gc))));
               si += gi;
               sf += gf;
               so += go;
@@ -1164,6 +1225,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
       }
       if (et == 0) trace_stamp(p, it, 7);
+    }
+    if constexpr (kF16Ops<P>) {  // range of the scaled dG planes (one atomic per warp)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+      if ((threadIdx.x & 31) == 0 && p.gmax) atomicMax(p.gmax, __float_as_uint(gmax));
     }
   }
   if constexpr (kPair)

@@ -741,8 +741,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       // next step's loads, which wait for this CTA's own publish
       const uint32_t hstg = smem_u32(S.b + (size_t)N * kTileM * 4);
       // opt-in (RW_CL_DEBUG bit 16): measured at B forward 0.596 ms staged vs 0.589 scattered
-      const bool staged = P::kPlanes == 1 && (p.debug & 16) &&
-                          (size_t)p.stages * N * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)nco * 64;
+      // (bf16), cell phase 5.3 vs 3.3 us (fp16x2, profiles/r02)
+      const bool staged = (p.debug & 16) != 0 &&
+                          (size_t)p.stages * BR * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)P::kPlanes * nco * 64;
       uint32_t rxc = 0;
       if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
       for (int t = 0; t < p.T; ++t) {
@@ -783,8 +784,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block (scaled, common.cuh)
             __half hh, hl;
             f16x2_split(hv[k] * pow2f(kHScaleLog2), hh, hl);
-            *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
-            *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
+            if (staged) {  // [plane][cl][32 units]
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(hstg + (cl * 32 + j) * 2), "h"(__half_as_ushort(hh)));
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(hstg + nco * 64 + (cl * 32 + j) * 2), "h"(__half_as_ushort(hl)));
+            } else {
+              *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
+              *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
+            }
           } else if (staged) {
             sts_bf16(hstg + (cl * 32 + j) * 2, hv[k]);
           } else {
@@ -792,12 +798,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           }
         }
         if (staged) {
-          // the CTA's 32 units x nco columns as 16-byte chunks of the swizzled operand image:
-          // nco * 4 coalesced vector stores instead of 32 * nco scattered 2-byte ones
+          // the CTA's 32 units x nco columns (x planes) as 16-byte chunks of the swizzled operand
+          // image: nco * 4 coalesced vector stores per plane instead of 32 * nco scattered 2-byte ones
           named_bar_sync(1, kEpiThreads);
-          for (int i = et; i < nco * 4; i += kEpiThreads) {
-            const uint4 v = lds_v4(hstg + i * 16);
-            *reinterpret_cast<uint4*>(hblk + sw_off(tile * kUnitsPerFwdTile + (i & 3) * 8, own0 + (i >> 2), N)) = v;
+          for (int i = et; i < P::kPlanes * nco * 4; i += kEpiThreads) {
+            const int pl = i >= nco * 4 ? 1 : 0, ii = i - pl * nco * 4;
+            const uint4 v = lds_v4(hstg + pl * nco * 64 + ii * 16);
+            *reinterpret_cast<uint4*>(hblk + sw_off(tile * kUnitsPerFwdTile + (ii & 3) * 8, pl * N + own0 + (ii >> 2), BR)) = v;
           }
         }
         if (et == 0) cl_trace(p, t, 3);

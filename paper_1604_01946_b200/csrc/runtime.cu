@@ -159,9 +159,16 @@ struct Nccl {
 Nccl& nccl() {
   static Nccl n;
   if (!n.h) {
+    // The NCCL the process already uses (e.g. PyTorch's), else RW_NCCL_PATH (the Python loader
+    // points it at the nvidia-nccl wheel PyTorch links), else the system one. Loaded RTLD_LOCAL:
+    // a second library with the same soname made global here would shadow a newer NCCL that a
+    // later import (libtorch_cuda) resolves its symbols against.
+    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!n.h)
+      if (const char* e = getenv("RW_NCCL_PATH")) n.h = dlopen(e, RTLD_NOW | RTLD_LOCAL);
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-      n.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
       if (n.h) break;
+      n.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     }
     if (!n.h) throw RwError{RW_ENCCL, "libnccl.so.2 not found"};
     n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
@@ -191,8 +198,9 @@ struct ClPlan {
 
 template <class P>
 struct KernelSet {
-  static void* fwd() { return lstm_kernel_ptr(P::kTF32 ? kTF32x3 : kBF16, true, false); }
-  static void* bwd() { return lstm_kernel_ptr(P::kTF32 ? kTF32x3 : kBF16, false, false); }
+  static constexpr int kPrec = P::kPlanes == 1 ? kBF16 : P::kTF32 ? kTF32x3 : kF16x2;
+  static void* fwd() { return lstm_kernel_ptr(kPrec, true, false); }
+  static void* bwd() { return lstm_kernel_ptr(kPrec, false, false); }
 };
 
 // Calls f(PrecX{}) for the context's operand format.
@@ -267,6 +275,7 @@ struct rw_ctx {
   bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
+  DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
   DevBuf pp_maps_dev;
   void* pp_next_xop = nullptr;               // next stage's layer-input operand (peer pointer)
@@ -645,10 +654,10 @@ void build(rw_ctx* x) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->dev);
 
   // ---- cluster schedule first: forward kc = K-slices of R.h, ko = of W.x; backward kc =
-  // K-slices of R^T.dG, ko = of W_{l+1}^T.dG (none for a single layer). It also decides the
-  // operand format of the fp32-parity mode: fp16x2 when both directions fit the cluster path
-  // (rec_cluster.cuh), else 3xTF32 on the persistent / stepwise kernels (RW_FP32_TF32=1 forces
-  // the latter).
+  // K-slices of R^T.dG, ko = of W_{l+1}^T.dG (none for a single layer). The fp32-parity mode
+  // computes with fp16x2 split operands on every schedule but the layer-sequential one (3xTF32
+  // there; RW_FP32_TF32=1 forces 3xTF32 everywhere): twice the MMA rate and half the operand
+  // bytes of 3xTF32, and half the tensor-core accumulation steps per K element.
   ClPlan cpf, cpb;
   bool cl_f = false, cl_b = false;
   auto try_cluster = [&](int prec) {
@@ -669,14 +678,12 @@ void build(rw_ctx* x) {
     x->prec = kBF16;
     if (want_cl) try_cluster(kBF16);
   } else {
-    x->prec = kTF32x3;
-    const bool force_tf32 = getenv("RW_FP32_TF32") && atoi(getenv("RW_FP32_TF32")) != 0;
+    const bool force_tf32 = (getenv("RW_FP32_TF32") && atoi(getenv("RW_FP32_TF32")) != 0) ||
+                            c.schedule == RW_SCHED_LAYERSEQ;
+    x->prec = force_tf32 ? kTF32x3 : kF16x2;
     if (want_cl && !force_tf32) {
       try_cluster(kF16x2);
-      if (cl_f && cl_b)
-        x->prec = kF16x2;
-      else
-        cl_f = cl_b = false;
+      if (!(cl_f && cl_b)) cl_f = cl_b = false;
     }
   }
   x->planes = prec_planes(x->prec);
@@ -747,9 +754,9 @@ void build(rw_ctx* x) {
   x->errflag.alloc(32);  // [code, count, max|dG|, max|x|, max|h0|]
 
   // ---- schedules
-  const bool f16x2 = x->prec == kF16x2;  // cluster kernels only (no persistent / stepwise variant)
-  void* kf = x->prec == kBF16 ? KernelSet<PrecBF16>::fwd() : KernelSet<PrecTF32x3>::fwd();
-  void* kb = x->prec == kBF16 ? KernelSet<PrecBF16>::bwd() : KernelSet<PrecTF32x3>::bwd();
+  const bool f16x2 = x->prec == kF16x2;
+  void* kf = lstm_kernel_ptr(x->prec, true, false);
+  void* kb = lstm_kernel_ptr(x->prec, false, false);
   const int kbf_max = (std::max(Ip, Hp) + Hp) / x->atomK;
   const int kbb_max = (int)((L > 1 ? 2 : 1) * G4p / x->atomK);
   const int tiles_f = Hp / kUnitsPerFwdTile, tiles_b = ceil_div(Hp, kTileM);
@@ -766,7 +773,7 @@ void build(rw_ctx* x) {
     cl_f = cl_b = false;
   }
   RecPlan pf{RW_SCHED_CLUSTER, 1, 0, 4, 0, 0}, pb{RW_SCHED_CLUSTER, 1, 0, 4, 0, 0};
-  if (!f16x2) {
+  if (!(cl_f && cl_b)) {
     pf = plan_recurrent(kf, want, x->planes, ls ? Hp / x->atomK : kbf_max, tiles_f, ls ? 1 : L, Bp, sms,
                         "RW_FWD_KSPLIT");
     pb = plan_recurrent(kb, want, x->planes, ls ? (int)(G4p / x->atomK) : kbb_max, tiles_b, ls ? 1 : L, Bp, sms,
@@ -872,6 +879,15 @@ void build(rw_ctx* x) {
     n_acc = 1;
     promo = 0;
     if (x->prec == kBF16) return;
+    if (x->prec == kF16x2) {
+      // fp16x2 always runs the ring: its drain applies each K segment's operand scales. 4 x 64 =
+      // 256 K elements (48 MMA accumulation steps) per chunk
+      acc_kb = 4;
+      if (const char* e = getenv("RW_PROMO_KB")) acc_kb = std::max(1, atoi(e));
+      n_acc = std::max(1, std::min(kMaxPromoSlots, 512 / Bp - 1));
+      promo = 1;
+      return;
+    }
     acc_kb = 2;
     while ((long long)ceil_div(kb_per_cta, acc_kb) * Bp > 512) acc_kb *= 2;
     n_acc = std::max(1, ceil_div(kb_per_cta, acc_kb));
@@ -1281,6 +1297,11 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
     ++g_launches;
     k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f());
   }
+  if (x->pp_next && x->wn_raw.p) {  // forward boundary group: the next stage's W_first (rw_pp_set_next_w)
+    ++g_launches;
+    k_pack_wf<<<dim3(ceil_div(2 * Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->wn_raw.f(), x->wn_raw.f(), H, H, Hp,
+                                                                           Hp, x->prec, x->wf_next.p, nullptr);
+  }
   if (x->pp_prev && x->wb_prev.p) {  // backward boundary group: [W_0^T | R_0^T] of this stage
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
@@ -1308,6 +1329,13 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   rp.acc_kb = fwd ? x->acckb_f : x->acckb_b;
   rp.n_acc = fwd ? x->nacc_f : x->nacc_b;
   rp.promo = fwd ? x->promo_f : x->promo_b;
+  rp.us_in0 = rp.us_in = rp.us_rec = 1.0f;
+  if (x->prec == kF16x2) {  // the drain's per-segment unscale (common.cuh operand scales)
+    rp.us_in0 = pow2f(-(kWScaleLog2 + (fwd ? kXScaleLog2 : kGScaleLog2)));
+    rp.us_in = pow2f(-(kWScaleLog2 + (fwd ? kHScaleLog2 : kGScaleLog2)));
+    rp.us_rec = pow2f(-(kWScaleLog2 + (fwd ? kHScaleLog2 : kGScaleLog2)));
+  }
+  rp.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
   rp.a_prefetch = 0;  // measured: no gain at config E (0 4 8 16 32 -> 727 702 694 701 660 TFLOP/s)
   if (const char* e = getenv("RW_A_PREFETCH")) rp.a_prefetch = atoi(e);
@@ -1446,9 +1474,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     run_forward_cluster(x, s);
     return;
   }
-  if constexpr (std::is_same_v<P, PrecF16x2>) {
-    throw RwError{RW_ECUDA, "internal: fp16x2 operands without the cluster schedule"};
-  } else {
+  {
   if (x->fwd_sched == RW_SCHED_LAYERSEQ) {
     RecParams rp = rec_params(x, true);
     void* kern = KernelSet<P>::fwd();
@@ -1505,7 +1531,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     }
   }
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
-  }  // P != PrecF16x2
+  }
 }
 
 template <class P>
@@ -1515,9 +1541,8 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     launch_cluster(x, x->cl_b.kern, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
     return;
   }
-  if constexpr (std::is_same_v<P, PrecF16x2>) {
-    throw RwError{RW_ECUDA, "internal: fp16x2 operands without the cluster schedule"};
-  } else {
+  {
+  if (x->prec == kF16x2) RW_CUDA(cudaMemsetAsync(static_cast<unsigned*>(x->errflag.p) + 2, 0, 4, s));  // max|dG|
   RecParams rp = rec_params(x, false);
   void* kern = KernelSet<P>::bwd();
   if (x->bwd_sched == RW_SCHED_LAYERSEQ) {
@@ -1567,7 +1592,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
     }
   }
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
-  }  // P != PrecF16x2
+  }
 }
 
 template <class P>
@@ -2213,15 +2238,10 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.unscale = 1.0f;  // bf16 only (above)
     if (dir == 0) {
       if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
-      DevBuf wn;
-      wn.alloc(4ULL * H * H * 4);
-      RW_CUDA(cudaMemcpy(wn.p, W_next, 4ULL * H * H * 4, cudaMemcpyHostToDevice));
+      x->wn_raw.alloc(4ULL * H * H * 4);
+      RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, 4ULL * H * H * 4, cudaMemcpyHostToDevice));
       x->wf_next.alloc((size_t)G4p * (Hp + Hp) * 2);
-      ++g_launches;
-      k_pack_wf<<<dim3(ceil_div(2 * Hp, 64), (int)(G4p / 32)), dim3(32, 8)>>>(wn.f(), wn.f(), H, H, Hp, Hp, x->prec,
-                                                                            x->wf_next.p, nullptr);
-      RW_CUDA(cudaGetLastError());
-      RW_CUDA(cudaDeviceSynchronize());
+      x->dirty = true;  // repack_params packs W_next into wf_next (again after rw_pp_set_next_w)
       o.kdim = Hp;
       o.op = static_cast<const uint8_t*>(x->hsw[L - 1].p);
       o.op_blk_off = 1;
@@ -2262,6 +2282,18 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
 // debug: counters of the boundary rings (pipeline bring-up): out[0..1] epochs (fwd, bwd),
 // out[2..4] forward ring of layer 0: done[0..1], consumed; out[6..8] backward ring of the last
 // layer: done[0..1], consumed; out[10..11] rows_f, rows_b; out[12..15] ko/sys of those rings.
+// The next stage's first-layer W changed (its parameters were updated): the forward boundary
+// group of this stage multiplies with it, so it is re-packed with this stage's next pass.
+extern "C" int rw_pp_set_next_w(rw_ctx* x, const float* W_next) {
+  return guarded(x, [&] {
+    if (!x->pp_next || !x->wn_raw.p) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
+    if (!W_next) einval("rw_pp_set_next_w: W_next is null");
+    RW_CUDA(cudaSetDevice(x->dev));
+    RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, 4ULL * x->H * x->H * 4, cudaMemcpyHostToDevice));
+    x->dirty = true;
+  });
+}
+
 extern "C" int rw_pp_debug(rw_ctx* x, long long* out) {
   return guarded(x, [&] {
     RW_CUDA(cudaDeviceSynchronize());

@@ -505,6 +505,11 @@ class Engine:
         w = as_matrix(w_next) if w_next is not None else None
         self._check(self._L.rw_pp_link(self._ctx, direction, C.byref(r), _fp(w)))
 
+    def pp_set_next_w(self, w_next) -> None:
+        """The next stage's first-layer W after a parameter update (rw_pp_set_next_w)."""
+        w = as_matrix(w_next)
+        self._check(self._L.rw_pp_set_next_w(self._ctx, _fp(w)))
+
     def launch_count(self, reset: bool = False) -> int:
         n = C.c_longlong()
         self._check(self._L.rw_launch_count(self._ctx, C.byref(n), int(reset)))

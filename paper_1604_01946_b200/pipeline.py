@@ -72,8 +72,12 @@ class PipelineStage:
         self.exports: dict[int, bytes] = {}
 
     def set_params(self, params) -> None:
-        """params: the full model's LayerParams; the stage takes its own slice."""
+        """params: the full model's LayerParams; the stage takes its own slice, and -- once linked
+        to a next stage -- that stage's first-layer W, which its forward boundary group multiplies
+        with (rw_pp_set_next_w: repacked with this stage's next pass)."""
         self.engine.set_params(params[self.first:self.first + self.count])
+        if self.plan.link_next and getattr(self, "_linked_next", False):
+            self.engine.pp_set_next_w(params[self.first + self.count].w)
 
     def export(self) -> dict[int, bytes]:
         if self.plan.export_fwd:
@@ -87,6 +91,7 @@ class PipelineStage:
         if self.plan.link_next:
             w_next = params[self.first + self.count].w
             self.engine.pp_link(0, next_exports[0], w_next)
+            self._linked_next = True
         if self.plan.link_prev:
             self.engine.pp_link(1, prev_exports[1])
 

@@ -1,0 +1,13 @@
+#!/bin/bash
+# GPU box: ncu evidence for the headline config (fp32-parity): the launch list of a short bench
+# run, and one --set full capture (with source) per hot kernel.
+# Usage: [KERNELS="k_cl_fwd k_cl_bwd"] [PREC=fp32] bash profiles/run_ncu.sh [extra bench args]
+mkdir -p gpurun_out
+PREC=${PREC:-fp32}
+B="python bench.py --no-cpu-baseline --single-precision --precision $PREC $*"
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/launches_$PREC.csv $B --steps 2 --warmup 1 > gpurun_out/launches_$PREC.out 2>&1
+for k in ${KERNELS:-k_cl_fwd k_cl_bwd}; do
+  timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 4 -c 1 \
+      -o gpurun_out/prof_${k}_$PREC -f $B --steps 1 --warmup 3 > gpurun_out/prof_${k}_$PREC.out 2>&1
+done

@@ -66,3 +66,55 @@ def test_pipeline_matches_single_context(dims, n, monkeypatch):
                 assert np.array_equal(y, y_r), (rep, "y")
             if s.k == 0:
                 assert np.array_equal(dx, dx_r), (rep, "dx0")
+
+
+def _single(c, params, x, dy):
+    from paper_1604_01946_b200 import Engine
+    H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
+    ref = Engine(c, precision="bf16", schedule="cluster")
+    ref.set_params(params)
+    ref.upload_inputs(x, dy)
+    ref.run_pass(2)
+    ref.sync()
+    y = np.zeros((H, B * T), np.float32, order="F")
+    dw = [np.zeros((4 * H, I if l == 0 else H), np.float32, order="F") for l in range(L)]
+    ref.read_outputs(y=y, dw=dw)
+    return y, dw
+
+
+def test_pipeline_follows_parameter_updates(monkeypatch):
+    """After the stages are linked, new parameters (an optimizer step) reach the forward boundary
+    group too (rw_pp_set_next_w): the next pass equals a fresh single context on the new
+    parameters, bit for bit (the boundary kept the link-time W)."""
+    from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process
+    c, params, x, dy, _, _ = make_case(Dims(4, 128, 96, 32, 6), seed=29, bias=True)
+    H, B, T, L, n = c.hidden, c.batch, c.steps, c.layers, 2
+    monkeypatch.setenv("RW_PP_RING", str(T))
+    stages = [PipelineStage(c, k, n) for k in range(n)]
+    for s in stages:
+        s.set_params(params)
+    link_in_process(stages, params)
+    zx = np.zeros((H, B * T), np.float32, order="F")
+    for k, s in enumerate(stages):
+        s.engine.upload_inputs(x if k == 0 else zx, dy if k == n - 1 else zx)
+
+    def run():
+        for s in stages:
+            s.engine.run_pass(3)
+            s.engine.sync()
+        for s in reversed(stages):
+            s.engine.run_pass(1)
+            s.engine.sync()
+        y = np.zeros((H, B * T), np.float32, order="F")
+        stages[-1].engine.read_outputs(y=y)
+        return y
+
+    run()
+    for p in params:  # "optimizer step"
+        p.w[:] = p.w * np.float32(0.9) + np.float32(0.01)
+        p.r[:] = p.r * np.float32(1.1)
+    for s in stages:
+        s.set_params(params)
+    y = run()
+    y_ref, _ = _single(c, params, x, dy)
+    assert np.array_equal(y, y_ref)
