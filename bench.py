@@ -173,6 +173,13 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- shared
+def job_flops(args, world: int) -> int:
+    """FLOPs of one step of the whole job: weak scaling runs `world` full minibatches, strong
+    scaling splits one across the ranks."""
+    f = pass_flops(CONFIGS[args.config])
+    return f if args.scaling == "strong" else f * world
+
+
 def workload_name(key: str, c: dict) -> str:
     base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM fwd+bwd"
     return base + (" (BASELINE configs[1])" if key == "B" else f" (sweep config {key})")
@@ -221,9 +228,11 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": reps, "warmup": warm, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SplitMix64 seed 42, reference generators)",
-        "config": config_dict(args.config, c, 1),
+        # the same job description as our arm's line (weak scaling: N minibatches, which the CPU
+        # engine processes at its per-minibatch rate)
+        "config": config_dict(args.config, c, 1 if args.scaling == "strong" else args.gpus),
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "reference",
                          "sample": f"{reps} full config-{args.config} passes (median), O6, {cores} workers",
                          "cpu": cpu_model(), "lib": os.path.basename(R.path)},
@@ -241,9 +250,13 @@ def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: b
     from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
 
     c = dict(CONFIGS[args.config])
+    if args.scaling == "strong" and world > 1:  # the global minibatch split across the ranks
+        from paper_1604_01946_b200.parallel import shard_range
+        b0, b1 = shard_range(c["batch"], rank, world)
+        c["batch"] = b1 - b0
     cfg = LadderConfig(**c, seed=42 + rank, opt_level=6, batch_steps=2, workers=1)
     eng = Engine(cfg, precision=precision, schedule=args.schedule, device=local)
-    params = init_params(LadderConfig(**c, seed=42))
+    params = init_params(LadderConfig(**{**c, "batch": CONFIGS[args.config]["batch"]}, seed=42))
     x = make_input(cfg)
     dy = make_dy(cfg)
     eng.set_params(params)
@@ -254,6 +267,7 @@ def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: b
         box = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         eng.init_comm(rank, world, box[0])
+        eng.comm_overlap(True)  # per-layer buckets all-reduced inside the pass, overlapped
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
 
@@ -347,7 +361,7 @@ def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: b
                 t = torch.tensor([e2e_ms], device="cuda")
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                 e2e_ms = t.item()
-            e2e = {"value": pass_flops(c) * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            e2e = {"value": job_flops(args, world) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                    "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "path": "C-ABI rw_train_step (pinned host x, dy -> K7 repack + forward + backward_data"
                            " + weight_update -> y, dx0, dW, dR, db on the host; uploads/read-back"
@@ -422,7 +436,6 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     c = dict(CONFIGS[args.config])
-    flops = pass_flops(c)
     m = measure(args, args.precision, world, rank, local)
     # the other precision mode, same workload, as a secondary key (bf16 is narrower arithmetic
     # than the reference's fp32: never the headline)
@@ -437,11 +450,11 @@ def run_ours(args) -> None:
     cpu_base = None
     if not args.no_cpu_baseline and args.config in ("A", "B"):
         cpu_base = cpu_baseline(args.config)
-    value = flops * world / (m["ms"] * 1e-3) / 1e12
+    value = job_flops(args, world) / (m["ms"] * 1e-3) / 1e12
     dtype = {"bf16": "bf16", "fp32": "tf32x3 (fp32-parity)"}
     operands = {"tf32x3": "3xTF32 split operands", "fp16x2": "fp16x2 split operands (hi + lo, 3 MMAs)",
                 "bf16": "bf16 operands"}
-    cfgd = config_dict(args.config, c, world)
+    cfgd = config_dict(args.config, c, 1 if args.scaling == "strong" else world)
     cfgd.update({"precision": args.precision, "schedule": m["desc"],
                  "operands": operands.get(m["desc"]["operands"], m["desc"]["operands"]),
                  "pct_of_bf16_peak": 100.0 * value / world / peak_burst,
@@ -455,7 +468,7 @@ def run_ours(args) -> None:
         "warmup": max(args.warmup, 3),
         "ms_per_step": m["ms"],
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": dtype[args.precision],
         "data": "synthetic (SplitMix64 seed 42 weights, streams 1000/1001 inputs: the reference generators)",
@@ -472,7 +485,7 @@ def run_ours(args) -> None:
     }
     if m2 is not None:
         rf2, crit2 = roofline(args, m2, other)
-        v2 = flops * world / (m2["ms"] * 1e-3) / 1e12
+        v2 = job_flops(args, world) / (m2["ms"] * 1e-3) / 1e12
         line[other] = {"dtype": dtype[other], "value": v2, "unit": "TFLOP/s", "ms_per_step": m2["ms"],
                        "e2e": m2["e2e"], "schedule": m2["desc"], "roofline": rf2, "critical_path": crit2,
                        "phases_ms": {k: v[0] / max(v[1], 1) for k, v in m2["ph"].items()},
@@ -519,6 +532,9 @@ def main():
     ap.add_argument("--single-precision", action="store_true", help="skip the secondary precision")
     ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster", "layerseq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU: weak = every rank its own full minibatch (data parallel); strong = "
+                         "the configuration's minibatch split across the ranks (e.g. --config E, B = 256)")
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
                     help="SURVEY §8(d) config; B (the headline) unless sweeping")
     args = ap.parse_args()

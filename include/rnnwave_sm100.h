@@ -188,6 +188,11 @@ int rw_comm_init(rw_ctx* ctx, int nranks, int rank, const char* id128);
 /* Sum all-reduce of every layer's dW, dR, db on `stream` (NULL = context stream), one NCCL
  * group, enqueued after the pass's weight-gradient GEMMs. */
 int rw_allreduce_grads(rw_ctx* ctx, void* stream);
+/* Overlapped gradient sums (on = 1): every later backward pass all-reduces each layer's bucket
+ * (dW_l, dR_l, db_l) inside the pass on a communication stream as soon as that layer's
+ * weight-gradient GEMMs finish (top layer first), overlapping the lower layers' GEMMs and the
+ * dx0 GEMM; rw_allreduce_grads then has nothing left to do. */
+int rw_comm_overlap(rw_ctx* ctx, int on);
 
 /* ---- layer pipeline over NVLink (config E; SURVEY §8e "deep stacks split as a layer
  * pipeline that hands off h_t per timestep peer-to-peer") ----

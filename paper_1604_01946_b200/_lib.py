@@ -27,7 +27,7 @@ EXPORTS = [
     "rw_create", "rw_destroy", "rw_last_error", "rw_create_error", "rw_set_params", "rw_forward",
     "rw_backward_data", "rw_weight_update", "rw_get_tape", "rw_upload_inputs", "rw_run_pass",
     "rw_sync", "rw_set_profiling", "rw_read_outputs", "rw_launch_count", "rw_params_updated",
-    "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_phase_times", "rw_describe", "rw_describe_variants",
+    "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_comm_overlap", "rw_phase_times", "rw_describe", "rw_describe_variants",
     "rw_describe_precision", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link", "rw_pp_set_next_w",
     "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm",
@@ -110,6 +110,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_nccl_unique_id.argtypes = [C.c_char_p]
     L.rw_comm_init.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
     L.rw_allreduce_grads.argtypes = [vp, vp]
+    L.rw_comm_overlap.argtypes = [vp, C.c_int]
     L.rw_flop_count_cell.argtypes = [C.c_int, C.c_int, C.c_int]
     L.rw_flop_count_cell.restype = C.c_int64
     L.rw_test_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,

@@ -173,27 +173,11 @@ __device__ __forceinline__ void store_operand(void* const* planes, long long idx
 
 // Activations (the reference's definitions: sigmoid = 1/(1+exp(-x)), cells.hpp:30; tanh).
 // bf16 mode: the SFU approximations (relative error ~2^-11, far below the bf16 operand rounding
-// it already carries). fp32-parity mode: exp with a two-constant ln2 range reduction and
-// a degree-6 polynomial on the reduced argument (|f| <= ln2/2; the Cephes expf coefficients,
-// ~1 ulp -- MUFU.EX2 alone measured 2e-5 normwise at config B), IEEE reciprocals, and
-// tanh(x) = sign(x) (1 - 2 / (1 + e^{2|x|})) above |x| = 0.625, Cephes' odd polynomial below
-// (relative error ~2e-7 throughout) -- a fraction of the fp32
-// rounding the 1e-5 contract allows, at a fraction of the instructions of libm expf / tanhf and
-// IEEE division.
-__device__ __forceinline__ float exp_rr(float x) {
-  x = fminf(fmaxf(x, -87.0f), 88.0f);
-  const float n = rintf(x * 1.44269504088896341f);
-  float f = fmaf(n, -0.693145751953125f, x);
-  f = fmaf(n, -1.428606765330187045e-06f, f);
-  float p = 1.9875691500e-4f;
-  p = fmaf(p, f, 1.3981999507e-3f);
-  p = fmaf(p, f, 8.3334519073e-3f);
-  p = fmaf(p, f, 4.1665795894e-2f);
-  p = fmaf(p, f, 1.6666665459e-1f);
-  p = fmaf(p, f, 5.0000001201e-1f);
-  const float e = fmaf(p, f * f, f) + 1.0f;
-  return e * __int_as_float(((int)n + 127) << 23);
-}
+// it already carries). fp32-parity mode: the accurate libm chain (expf, IEEE division, tanhf),
+// as the reference computes it. Measured alternatives (profiles/r02/README.md): MUFU.EX2 on a
+// range-reduced argument with an rcp.approx + Newton reciprocal was accurate enough but the
+// cell phase got slower (4.9-5.3 vs 3.3 us at config B), and tanh(x) = 1 - 2/(1 + e^{2x}) without
+// a small-|x| branch broke the 1e-5 contract (2e-5 normwise).
 template <class P>
 __device__ __forceinline__ float act_sigmoid(float x) {
   if constexpr (P::kPlanes == 1) {
@@ -202,7 +186,7 @@ __device__ __forceinline__ float act_sigmoid(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(0.5f * x));
     return fmaf(0.5f, y, 0.5f);
   } else {
-    return __frcp_rn(1.0f + exp_rr(-x));
+    return 1.0f / (1.0f + expf(-x));
   }
 }
 template <class P>
@@ -212,18 +196,7 @@ __device__ __forceinline__ float act_tanh(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
   } else {
-    const float a = fabsf(x);
-    if (a < 0.625f) {  // Cephes tanhf odd polynomial (relative error ~1e-7)
-      const float z = x * x;
-      float p = -5.70498872745e-3f;
-      p = fmaf(p, z, 2.06390887954e-2f);
-      p = fmaf(p, z, -5.37397155531e-2f);
-      p = fmaf(p, z, 1.33314422036e-1f);
-      p = fmaf(p, z, -3.33332819422e-1f);
-      return fmaf(p * z, x, x);
-    }
-    const float t = fmaf(-2.0f, __frcp_rn(1.0f + exp_rr(2.0f * a)), 1.0f);
-    return copysignf(t, x);
+    return tanhf(x);
   }
 }
 

@@ -103,7 +103,8 @@ struct ClParams {
   float unscale;  // critical groups, fp16x2: 2^-(kWScaleLog2 + kHScaleLog2) forward (R.h),
                   // 2^-(kWScaleLog2 + kGScaleLog2) backward (R^T.dG); off groups: ClOff::unscale
   unsigned* gmax; // backward: max |dG| of the pass (float bits; range check of the scaled dG planes)
-  int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 1 = skip fwd tapes,
+  int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 512 = fp16x2 forward
+              // without the lo-plane stores, 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
               // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered,
               // 64 = operand k-blocks copied one per bulk copy (not in pairs)
@@ -789,7 +790,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               asm volatile("st.shared.b16 [%0], %1;" ::"r"(hstg + nco * 64 + (cl * 32 + j) * 2), "h"(__half_as_ushort(hl)));
             } else {
               *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
-              *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
+              if (!(p.debug & 512))  // timing experiment (results invalid): hi plane only
+                *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
             }
           } else if (staged) {
             sts_bf16(hstg + (cl * 32 + j) * 2, hv[k]);

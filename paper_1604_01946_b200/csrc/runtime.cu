@@ -291,6 +291,12 @@ struct rw_ctx {
   cudaStream_t main = nullptr;
   // rw_train_step: copy streams and the events that order the pipelined host round trip
   cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  // data parallel, overlapped (rw_comm_overlap): per-layer gradient buckets all-reduced on `comm_s`
+  // as soon as that layer's weight-gradient GEMMs finish, while the lower layers' GEMMs and dx0 run
+  bool dp_overlap = false;
+  cudaStream_t comm_s = nullptr;
+  std::vector<cudaEvent_t> ev_layer;
+  cudaEvent_t ev_comm = nullptr;
   cudaEvent_t ev_fwd = nullptr, ev_x = nullptr, ev_y_staged = nullptr, ev_y_out = nullptr, ev_dy = nullptr,
               ev_bwd = nullptr, ev_out = nullptr;
   std::vector<cudaStream_t> ls;
@@ -492,7 +498,7 @@ size_t gemm_smem(int planes, int bn, int stages) {
 // profiles/ubench/f16x2_ts_check.cu)
 // drained into fp32 registers; bf16 runs the whole K in TMEM.
 constexpr int kPromoteKB = 2;
-constexpr int kPromoteKB16 = 8;
+constexpr int kPromoteKB16 = 4;
 
 // bf16 grouped GEMMs go to the persistent kernel (gemm_tc.cuh k_gemm_p) unless RW_GEMM_OLD=1;
 // fp32-parity (3xTF32, chunked fp32 promotion) keeps the one-tile-per-CTA kernel.
@@ -1610,6 +1616,18 @@ void transpose_planes(rw_ctx* x, const Operand& src, int R, long long C, Operand
                                                   dst.plane[0].f(), dst.plane[1].f());
 }
 
+// One layer's gradient bucket (dW_l, dR_l, db_l) summed over the data-parallel ranks.
+void allreduce_layer(rw_ctx* x, int l, cudaStream_t s) {
+  Nccl& n = nccl();
+  const int Il = l == 0 ? x->I : x->H;
+  nccl_check(n.GroupStart(), "ncclGroupStart");
+  nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
+  nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
+  nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
+  nccl_check(n.GroupEnd(), "ncclGroupEnd");
+}
+
+
 template <class P>
 void run_weight_grads(rw_ctx* x, cudaStream_t s) {
   if (x->pp_prev) {  // layer input of a pipeline stage: copied in by the previous stage
@@ -1628,10 +1646,25 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
     }
     transpose_planes(x, x->x_op, x->Ip, colsT, x->xT, s);
     RW_CUDA(cudaGetLastError());
-    launch_gemm<P, false, false>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
-  } else {
-    launch_gemm<P, true, true>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
   }
+  if (x->dp_overlap && x->comm) {
+    // data parallel, overlapped: the GEMM pair (dW_l, dR_l: descriptors 2l, 2l + 1) of one layer
+    // at a time, top layer first; its bucket is all-reduced on comm_s while the next runs
+    for (int l = x->L - 1; l >= 0; --l) {
+      if constexpr (P::kTF32)
+        launch_gemm<P, false, false>(t + 2 * l, 2, M, N, x->bn_wg, x->st_wg, s);
+      else
+        launch_gemm<P, true, true>(t + 2 * l, 2, M, N, x->bn_wg, x->st_wg, s);
+      RW_CUDA(cudaEventRecord(x->ev_layer[l], s));
+      RW_CUDA(cudaStreamWaitEvent(x->comm_s, x->ev_layer[l], 0));
+      allreduce_layer(x, l, x->comm_s);
+    }
+    return;
+  }
+  if constexpr (P::kTF32)
+    launch_gemm<P, false, false>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
+  else
+    launch_gemm<P, true, true>(t, x->n_wg, M, N, x->bn_wg, x->st_wg, s);
 }
 
 void run_db(rw_ctx* x, cudaStream_t s) {
@@ -1665,6 +1698,11 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
     run_backward_rec<P>(x, s);
   }
   if (pass == 4) return;
+  const bool overlap = x->dp_overlap && x->comm;
+  if (overlap) {  // db first: each layer's bucket (dW, dR, db) is complete after its GEMMs
+    PhaseTimer pt(x, 5, s);
+    run_db(x, s);
+  }
   {
     PhaseTimer pt(x, 3, s);
     run_weight_grads<P>(x, s);
@@ -1673,9 +1711,12 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
     PhaseTimer pt(x, 4, s);
     run_dx0<P>(x, s);
   }
-  {
+  if (!overlap) {
     PhaseTimer pt(x, 5, s);
     run_db(x, s);
+  } else {  // join: the pass completes when the last bucket is summed
+    RW_CUDA(cudaEventRecord(x->ev_comm, x->comm_s));
+    RW_CUDA(cudaStreamWaitEvent(s, x->ev_comm, 0));
   }
 }
 
@@ -1823,6 +1864,9 @@ rw_ctx::~rw_ctx() {
   if (main) cudaStreamDestroy(main);
   if (cp_in) cudaStreamDestroy(cp_in);
   if (cp_out) cudaStreamDestroy(cp_out);
+  if (comm_s) cudaStreamDestroy(comm_s);
+  for (cudaEvent_t e : ev_layer) cudaEventDestroy(e);
+  if (ev_comm) cudaEventDestroy(ev_comm);
   for (cudaEvent_t e : {ev_fwd, ev_x, ev_y_staged, ev_y_out, ev_dy, ev_bwd, ev_out})
     if (e) cudaEventDestroy(e);
 }
@@ -2344,6 +2388,7 @@ int rw_comm_init(rw_ctx* x, int nranks, int rank, const char* id128) {
 }
 
 static void allreduce_grads(rw_ctx* x, cudaStream_t s) {
+  if (x->dp_overlap) return;  // the pass already summed every bucket (rw_comm_overlap)
   Nccl& n = nccl();
   nccl_check(n.GroupStart(), "ncclGroupStart");
   for (int l = x->L - 1; l >= 0; --l) {  // top layer's gradients are final first
@@ -2353,6 +2398,24 @@ static void allreduce_grads(rw_ctx* x, cudaStream_t s) {
     nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// Overlapped data-parallel gradient sums: every later training pass all-reduces each layer's
+// bucket inside the pass, as soon as its weight-gradient GEMMs finish (top layer first), on a
+// communication stream, while the lower layers' GEMMs and the dx0 GEMM still run.
+extern "C" int rw_comm_overlap(rw_ctx* x, int on) {
+  return guarded(x, [&] {
+    if (on && !x->comm) einval("rw_comm_overlap: rw_comm_init was not called");
+    RW_CUDA(cudaSetDevice(x->dev));
+    if (on && !x->comm_s) {
+      RW_CUDA(cudaStreamCreateWithFlags(&x->comm_s, cudaStreamNonBlocking));
+      x->ev_layer.resize(x->L);
+      for (auto& e : x->ev_layer) RW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      RW_CUDA(cudaEventCreateWithFlags(&x->ev_comm, cudaEventDisableTiming));
+    }
+    if (x->dp_overlap != (on != 0)) invalidate_graphs(x);
+    x->dp_overlap = on != 0;
+  });
 }
 
 int rw_allreduce_grads(rw_ctx* x, void* stream) {

@@ -487,6 +487,10 @@ class Engine:
         """Join the NCCL data-parallel group (one context per GPU)."""
         self._check(self._L.rw_comm_init(self._ctx, world, rank, unique_id))
 
+    def comm_overlap(self, on: bool = True) -> None:
+        """Sum each layer's gradient bucket inside the pass, overlapped (rw_comm_overlap)."""
+        self._check(self._L.rw_comm_overlap(self._ctx, int(bool(on))))
+
     def allreduce_grads(self, stream: int | None = None) -> None:
         self._check(self._L.rw_allreduce_grads(self._ctx, C.c_void_p(stream or 0)))
 

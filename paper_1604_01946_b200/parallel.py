@@ -49,3 +49,30 @@ def allreduce_gradients(grads, group=None) -> None:
             t = torch.from_numpy(np.array(a, dtype=np.float32).ravel(order="F"))
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
             lst[i] = np.asfortranarray(t.numpy().reshape(a.shape, order="F"))
+
+
+def bucket_plan(layers: int, hidden: int, inp: int) -> list[tuple[int, int]]:
+    """The overlapped data-parallel all-reduce's buckets (rw_comm_overlap, runtime.cu): one per
+    layer, top layer first (its weight-gradient GEMMs finish first), as (layer, fp32 values):
+    dW_l (4H x I_l) + dR_l (4H x H) + db_l (4H)."""
+    G = 4 * hidden
+    return [(l, G * (inp if l == 0 else hidden) + G * hidden + G) for l in range(layers - 1, -1, -1)]
+
+
+def allreduce_gradients_bucketed(grads, group=None) -> None:
+    """Host twin of the overlapped device all-reduce: each layer's bucket (dW, dR, db) is summed
+    asynchronously in bucket_plan order, all in flight at once, then waited for; the result
+    equals allreduce_gradients bit for bit (same per-tensor sums)."""
+    import torch
+    import torch.distributed as dist
+    L = len(grads.dw)
+    plan = bucket_plan(L, grads.dr[0].shape[1], grads.dw[0].shape[1])
+    pending = []
+    for l, _ in plan:
+        for lst in (grads.dw, grads.dr, grads.db):
+            a = lst[l]
+            t = torch.from_numpy(np.array(a, dtype=np.float32).ravel(order="F"))
+            pending.append((lst, l, a.shape, t, dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group, async_op=True)))
+    for lst, l, shape, t, work in pending:
+        work.wait()
+        lst[l] = np.asfortranarray(t.numpy().reshape(shape, order="F"))

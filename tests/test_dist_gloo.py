@@ -98,3 +98,52 @@ def test_data_parallel_gradients_gloo():
             assert np.array_equal(got, res[1][idx][l])
             err = np.linalg.norm(got - ref[k][l]) / np.linalg.norm(ref[k][l])
             assert err < 1e-6, (k, l, err)
+
+
+def test_bucket_plan_top_layer_first():
+    from paper_1604_01946_b200.parallel import bucket_plan
+    plan = bucket_plan(3, 4, 5)
+    assert [l for l, _ in plan] == [2, 1, 0]
+    assert plan[-1][1] == 16 * 5 + 16 * 4 + 16 and plan[0][1] == 16 * 4 * 2 + 16
+
+
+def _bucket_worker(rank, world, port, result_q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_1604_01946_b200.engine import Gradients
+    from paper_1604_01946_b200.parallel import allreduce_gradients_bucketed
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(100 + rank)
+    L, H, I = 3, 8, 6
+    mk = lambda r, c: np.asfortranarray(rng.standard_normal((r, c)).astype(np.float32))  # noqa: E731
+    g = Gradients([mk(4 * H, I if l == 0 else H) for l in range(L)], [mk(4 * H, H) for _ in range(L)],
+                  [rng.standard_normal(4 * H).astype(np.float32) for _ in range(L)])
+    mine = Gradients([a.copy(order="F") for a in g.dw], [a.copy(order="F") for a in g.dr], [a.copy() for a in g.db])
+    allreduce_gradients_bucketed(g)
+    result_q.put((rank, mine, g))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bucketed_overlapped_allreduce_gloo():
+    """World size 2 over gloo: the overlapped per-layer buckets (all in flight at once, top layer
+    first, rw_comm_overlap's order) sum to exactly the per-tensor all-reduce."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    (_, a, ga), (_, b, gb) = res
+    for name in ("dw", "dr", "db"):
+        for la, lb, ra, rb in zip(getattr(a, name), getattr(b, name), getattr(ga, name), getattr(gb, name)):
+            want = (la.astype(np.float32) + lb.astype(np.float32))
+            assert np.array_equal(ra, want) and np.array_equal(rb, want)
