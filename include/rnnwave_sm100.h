@@ -96,8 +96,10 @@ typedef enum {
   RW_TAPE_C = 2,      /* H x B*(T+1)      per layer       */
   RW_TAPE_GATES = 3,  /* 4H x B*T         per layer (i,f,o,c' post-activations) */
   RW_TAPE_TANH_C = 4, /* H x B*T          per layer       */
-  RW_TAPE_DGW = 5,    /* 4H x B*T         per layer (BackwardState::dgw_seq) */
-  RW_TAPE_Y = 6       /* H x B*T          (layer ignored) */
+  RW_TAPE_DGW = 5,    /* G*H x B*T        per layer (BackwardState::dgw_seq) */
+  RW_TAPE_Y = 6,      /* H x B*T          (layer ignored) */
+  RW_TAPE_ZRH = 7,    /* H x B*T          per layer, GRU (ForwardTape::zrh_seq) */
+  RW_TAPE_DGR = 8     /* G*H x B*T        per layer, GRU (BackwardState::dgr_seq) */
 } rw_tape;
 
 /* Validates like LadderConfig::validate; allocates every device buffer for the config. */

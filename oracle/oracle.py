@@ -37,9 +37,15 @@ class Dims:
     input: int
     batch: int
     steps: int
+    kind: int = 3  # the reference's CellKind: 0 rnn-tanh, 1 rnn-relu, 2 gru, 3 lstm
 
     def input_width(self, l: int) -> int:
         return self.input if l == 0 else self.hidden
+
+
+def gate_count(kind: int) -> int:
+    """config.hpp:19-28: RNN 1, GRU 3, LSTM 4 (kind in the reference's CellKind order)."""
+    return {0: 1, 1: 1, 2: 3, 3: 4}[kind]
 
 
 def _dims(cfg) -> Dims:
@@ -109,20 +115,20 @@ class Restatement:
         G = 4 * d.hidden
         w = [fmat(G, d.input_width(l)) for l in range(d.layers)]
         r = [fmat(G, d.hidden) for _ in range(d.layers)]
-        self.lib.rwo_init_params(C.byref(_RwoDims(*d.__dict__.values())), seed,
+        self.lib.rwo_init_params(C.byref(_RwoDims(d.layers, d.hidden, d.input, d.batch, d.steps)), seed,
                                  _arr([_fp(a) for a in w]), _arr([_fp(a) for a in r]))
         return w, r
 
     def make_input(self, cfg, seed):
         d = _dims(cfg)
         x = fmat(d.input, d.batch * d.steps)
-        self.lib.rwo_make_input(C.byref(_RwoDims(*d.__dict__.values())), seed, _fp(x))
+        self.lib.rwo_make_input(C.byref(_RwoDims(d.layers, d.hidden, d.input, d.batch, d.steps)), seed, _fp(x))
         return x
 
     def make_dy(self, cfg, seed):
         d = _dims(cfg)
         dy = fmat(d.hidden, d.batch * d.steps)
-        self.lib.rwo_make_dy(C.byref(_RwoDims(*d.__dict__.values())), seed, _fp(dy))
+        self.lib.rwo_make_dy(C.byref(_RwoDims(d.layers, d.hidden, d.input, d.batch, d.steps)), seed, _fp(dy))
         return dy
 
     def flop_count_cell(self, hidden, inp, batch):
@@ -131,10 +137,12 @@ class Restatement:
     def run(self, cfg, w, r, b, x, h0=None, c0=None, dy=None, training=True):
         """Forward (+ backward_data + weight_update when dy is given). Returns a dict of
         Fortran-ordered float32 arrays named like the reference fields."""
+        if getattr(cfg, "kind", 3) != 3:
+            raise NotImplementedError("the C restatement covers the LSTM path; use Reference for GRU / RNN")
         d = _dims(cfg)
         H, B, T, G = d.hidden, d.batch, d.steps, 4 * d.hidden
         L = d.layers
-        dd = C.byref(_RwoDims(*d.__dict__.values()))
+        dd = C.byref(_RwoDims(d.layers, d.hidden, d.input, d.batch, d.steps))
         training = training or dy is not None
         out = {
             "h_seq": [fmat(H, B * (T + 1)) for _ in range(L)],
@@ -217,12 +225,13 @@ class Reference:
     def _cfg(cfg, opt_level=6, batch_steps=None, workers=None):
         s = batch_steps if batch_steps is not None else min(2, cfg.steps)
         wk = workers if workers is not None else min(os.cpu_count() or 1, 2 * cfg.layers)
-        arr = (C.c_int * 8)(cfg.layers, cfg.hidden, cfg.input, cfg.batch, cfg.steps,
-                            opt_level, s, wk)
+        kind = getattr(cfg, "kind", 3)  # the reference's CellKind (3 = LSTM)
+        arr = (C.c_int * 9)(cfg.layers, cfg.hidden, cfg.input, cfg.batch, cfg.steps,
+                            opt_level, s, wk, kind)
         return arr
 
     def init_params(self, cfg, seed):
-        G = 4 * cfg.hidden
+        G = gate_count(getattr(cfg, "kind", 3)) * cfg.hidden
         w = [fmat(G, cfg.input if l == 0 else cfg.hidden) for l in range(cfg.layers)]
         r = [fmat(G, cfg.hidden) for _ in range(cfg.layers)]
         self.lib.rwref_init_params(self._cfg(cfg), seed, _arr([_fp(a) for a in w]),
@@ -244,13 +253,16 @@ class Reference:
 
     def run(self, cfg, w, r, b, x, h0=None, c0=None, dy=None, training=True, tapes=True,
             opt_level=6, workers=None):
-        H, B, T, G, L = cfg.hidden, cfg.batch, cfg.steps, 4 * cfg.hidden, cfg.layers
+        H, B, T, L = cfg.hidden, cfg.batch, cfg.steps, cfg.layers
+        kind = getattr(cfg, "kind", 3)
+        G = gate_count(kind) * H
         training = training or dy is not None
         out = {"y": fmat(H, B * T)}
         # tapes: True = every tape, "states" = h_seq / c_seq only (full-size parity runs)
         if tapes:
             out["h_seq"] = [fmat(H, B * (T + 1)) for _ in range(L)]
-            out["c_seq"] = [fmat(H, B * (T + 1)) for _ in range(L)]
+            if kind == 3:
+                out["c_seq"] = [fmat(H, B * (T + 1)) for _ in range(L)]
             if training and tapes is True:
                 out["gates_seq"] = [fmat(G, B * T) for _ in range(L)]
                 out["tanh_c_seq"] = [fmat(H, B * T) for _ in range(L)]
@@ -259,11 +271,11 @@ class Reference:
                 out["dgw_seq"] = [fmat(G, B * T) for _ in range(L)]
             out["dx0"] = fmat(cfg.input, B * T)
             out["dh0"] = [fmat(H, B) for _ in range(L)]
-            out["dc0"] = [fmat(H, B) for _ in range(L)]
+            out["dc0"] = [fmat(H, B) for _ in range(L)] if kind == 3 else []
             out["dw"] = [fmat(G, cfg.input if l == 0 else H) for l in range(L)]
             out["dr"] = [fmat(G, H) for _ in range(L)]
             out["db"] = [np.zeros(G, np.float32) for _ in range(L)]
-        P = lambda k: _arr([_fp(a) for a in out[k]]) if k in out else None  # noqa: E731
+        P = lambda k: _arr([_fp(a) for a in out[k]]) if out.get(k) else None  # noqa: E731
         Q = lambda lst: _arr([_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
         err = C.create_string_buffer(512)
         rc = self.lib.rwref_run(self._cfg(cfg, opt_level, workers=workers), 0, Q(w), Q(r), Q(b),

@@ -24,10 +24,11 @@ using namespace rnnwave;
 
 namespace {
 
-// cfg[] = {layers, hidden, input, batch, steps, opt_level, batch_steps, workers}
+// cfg[] = {layers, hidden, input, batch, steps, opt_level, batch_steps, workers, kind}
+// (kind: the reference's CellKind order -- 0 rnn-tanh, 1 rnn-relu, 2 gru, 3 lstm)
 LadderConfig make_cfg(const int* c, std::uint64_t seed) {
   LadderConfig cfg;
-  cfg.kind = CellKind::Lstm;
+  cfg.kind = static_cast<CellKind>(c[8]);
   cfg.layers = c[0];
   cfg.hidden = c[1];
   cfg.input = c[2];
@@ -94,7 +95,7 @@ int rwref_run(const int* c, std::uint64_t seed, const float* const* w, const flo
               char* err, int errlen) {
   try {
     const LadderConfig cfg = make_cfg(c, seed);
-    const int H = cfg.hidden, B = cfg.batch, T = cfg.steps, G = 4 * H;
+    const int H = cfg.hidden, B = cfg.batch, T = cfg.steps, G = gate_count(cfg.kind) * H;
     std::vector<LayerParams> params(cfg.layers);
     for (int l = 0; l < cfg.layers; ++l) {
       params[l].w = get(w[l], G, cfg.input_width(l));
@@ -111,7 +112,7 @@ int rwref_run(const int* c, std::uint64_t seed, const float* const* w, const flo
     put(fwd.y, y);
     for (int l = 0; l < cfg.layers; ++l) {
       if (h_seq) put(fwd.tape.h_seq[l], h_seq[l]);
-      if (c_seq) put(fwd.tape.c_seq[l], c_seq[l]);
+      if (c_seq && !fwd.tape.c_seq.empty()) put(fwd.tape.c_seq[l], c_seq[l]);
       if (gates_seq && !fwd.tape.gates_seq.empty()) put(fwd.tape.gates_seq[l], gates_seq[l]);
       if (tanh_c_seq && !fwd.tape.tanh_c_seq.empty()) put(fwd.tape.tanh_c_seq[l], tanh_c_seq[l]);
     }
@@ -123,7 +124,7 @@ int rwref_run(const int* c, std::uint64_t seed, const float* const* w, const flo
     for (int l = 0; l < cfg.layers; ++l) {
       if (dgw_seq) put(bwd.dgw_seq[l], dgw_seq[l]);
       if (dh0) put(bwd.dh0[l], dh0[l]);
-      if (dc0) put(bwd.dc0[l], dc0[l]);
+      if (dc0 && !bwd.dc0.empty()) put(bwd.dc0[l], dc0[l]);
       if (dw) put(grads.dw[l], dw[l]);
       if (dr) put(grads.dr[l], dr[l]);
       if (db) std::memcpy(db[l], grads.db[l].data(), grads.db[l].size() * sizeof(float));
@@ -142,7 +143,7 @@ int rwref_oracle(const int* c, const float* const* w, const float* const* r,
                  double* const* dh0, double* const* dc0, char* err, int errlen) {
   try {
     const LadderConfig cfg = make_cfg(c, 0);
-    const int H = cfg.hidden, B = cfg.batch, T = cfg.steps, G = 4 * H;
+    const int H = cfg.hidden, B = cfg.batch, T = cfg.steps, G = gate_count(cfg.kind) * H;
     std::vector<LayerParams> params(cfg.layers);
     for (int l = 0; l < cfg.layers; ++l) {
       params[l].w = get(w[l], G, cfg.input_width(l));

@@ -15,7 +15,7 @@ _PF = C.POINTER(_F)
 RW_OK, RW_EINVAL, RW_ECUDA, RW_ENOMEM, RW_ENCCL, RW_ESTATE = range(6)
 RW_PREC_BF16, RW_PREC_FP32 = 0, 1
 RW_SCHED_AUTO, RW_SCHED_STEPWISE, RW_SCHED_PERSISTENT, RW_SCHED_CLUSTER, RW_SCHED_LAYERSEQ = 0, 1, 2, 3, 4
-RW_TAPE_X0, RW_TAPE_H, RW_TAPE_C, RW_TAPE_GATES, RW_TAPE_TANH_C, RW_TAPE_DGW, RW_TAPE_Y = range(7)
+RW_TAPE_X0, RW_TAPE_H, RW_TAPE_C, RW_TAPE_GATES, RW_TAPE_TANH_C, RW_TAPE_DGW, RW_TAPE_Y, RW_TAPE_ZRH, RW_TAPE_DGR = range(9)
 
 class rw_trace_record(C.Structure):
     _fields_ = [("task_id", C.c_int32), ("layer", C.c_int32), ("block", C.c_int32), ("step_k", C.c_int32),

@@ -82,6 +82,11 @@ __device__ __forceinline__ void f16x2_split(float v, __half& hi, __half& lo) {
   lo = __float2half_rn(v - __half2float(hi));
 }
 
+// Cell kinds (rw_config.cell_kind, the reference's CellKind order): the cluster kernels are
+// instantiated per class -- LSTM, GRU, RNN (tanh / relu selected at run time).
+enum CellKindDev : int { kCellRnnTanh = 0, kCellRnnRelu = 1, kCellGru = 2, kCellLstm = 3 };
+__host__ __device__ constexpr int cell_gates(int kind) { return kind == kCellLstm ? 4 : kind == kCellGru ? 3 : 1; }
+
 constexpr int kTileM = 128;      // UMMA M (cta_group::1)
 constexpr int kRowBytes = 128;   // one SWIZZLE_128B row
 constexpr int kUnitsPerFwdTile = 32;  // forward tile = 32 hidden units x 4 gates
@@ -119,6 +124,7 @@ struct GemmDesc {
   int b_n_off;         // row (N) offset inside the B tensor (e.g. h_{l-1} starts at column block 1)
   float alpha;         // D = alpha * A B^T (fp16x2 weight operands carry 2^kWScaleLog2); 0 means 1
   int* error;          // the context's error word (bounded mbarrier waits, sm100_ptx.cuh)
+  int gates;           // kRowGateUnperm: the cell's gate count (0 = 4)
 };
 
 }  // namespace rw

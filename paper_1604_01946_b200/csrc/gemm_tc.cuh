@@ -52,9 +52,9 @@ struct OperandTile {
 };
 
 __device__ __forceinline__ int gemm_out_row(const GemmDesc& g, int m) {
-  if (g.row_mode == kRowGateUnperm) {
-    const int u = rho_unit(m);
-    return u < g.H ? rho_gate(m) * g.H + u : -1;
+  if (g.row_mode == kRowGateUnperm) {  // gate slots g >= gates (GRU, RNN) hold no output row
+    const int u = rho_unit(m), gt = rho_gate(m);
+    return u < g.H && (g.gates == 0 || gt < g.gates) ? gt * g.H + u : -1;
   }
   if (g.row_mode == kRowGatePad) return rho_gate(m) * g.Hp + rho_unit(m);
   return m < g.m_valid ? m : -1;

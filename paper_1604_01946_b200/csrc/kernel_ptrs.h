@@ -4,10 +4,16 @@
 // launched with cudaLaunchKernelExC.
 #pragma once
 
+#include "common.cuh"
+
 namespace rw {
 
-// k_cl_fwd / k_cl_bwd<P, nco / 16> (rec_cluster.cuh); prec kBF16 or kF16x2
-void* cl_kernel_ptr(int prec, bool fwd, int nco);
+// k_cl_fwd / k_cl_bwd<P, nco / 16, cell class> (rec_cluster.cuh); prec kBF16 or kF16x2; kind
+// CellKindDev (one translation unit per cell class: kernels_cl*.cu)
+void* cl_kernel_ptr(int prec, bool fwd, int nco, int kind = kCellLstm);
+void* cl_kernel_ptr_lstm(int prec, bool fwd, int nco);
+void* cl_kernel_ptr_gru(int prec, bool fwd, int nco);
+void* cl_kernel_ptr_rnn(int prec, bool fwd, int nco);
 // k_lstm_fwd / k_lstm_bwd<P, pair> (lstm_step.cuh); prec kBF16, kF16x2 or kTF32x3 (pair: bf16 only)
 void* lstm_kernel_ptr(int prec, bool fwd, bool pair);
 // k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh): bf16 BNV 0; two-plane formats BNV = tile width 64 / 128

@@ -35,8 +35,10 @@ __device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long 
 // tile of 32 rho rows (one gate of 32 consecutive units = 32 consecutive source rows) x 64 k,
 // reading 128-byte runs of the source columns and writing 64-element runs of the operand rows.
 // grid (ceil((Ipl + Hp) / 64), 4Hp / 32), block (32, 8).
+// G: the cell's gate count (LSTM 4, GRU 3, RNN 1); gate slots g >= G of the 4-slot rho layout
+// stay zero (W and R are G*H x I column-major, gate blocks of H rows, cells.hpp:24-28).
 __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__ R, int H, int I,
-                          int Hp, int Ipl, int prec, void* p0, void* p1) {
+                          int Hp, int Ipl, int prec, void* p0, void* p1, int G = 4) {
   __shared__ float tile[64][33];
   const int K = Ipl + Hp;
   const int k0 = blockIdx.x * 64, rho0 = blockIdx.y * 32;
@@ -45,12 +47,12 @@ __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__
   for (int kk = ty; kk < 64; kk += 8) {
     const int k = k0 + kk, u = u0 + tx;
     float v = 0.0f;
-    if (u < H && k < K) {
+    if (u < H && k < K && g < G) {
       const long long row = (long long)g * H + u;
       if (k < Ipl) {
-        if (k < I) v = W[(long long)k * 4 * H + row];
+        if (k < I) v = W[(long long)k * G * H + row];
       } else if (k - Ipl < H) {
-        v = R[(long long)(k - Ipl) * 4 * H + row];
+        v = R[(long long)(k - Ipl) * G * H + row];
       }
     }
     tile[kk][tx] = v;
@@ -67,7 +69,7 @@ __global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__
 // Backward operand of layer l: rows = units (Hp), K = [W_{l+1}^T (4Hp, rho order)] ++
 // [R_l^T (4Hp, rho order)]; Wup may be null (top layer). Both sources are 4H x H.
 __global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict__ R, int H,
-                          int Hp, int prec, void* p0, void* p1) {
+                          int Hp, int prec, void* p0, void* p1, int G = 4) {
   const int G4p = 4 * Hp;
   const long long K = (Wup ? 2LL : 1LL) * G4p;
   const long long total = (long long)Hp * K;
@@ -79,14 +81,14 @@ __global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict
     const int rho = k % G4p;
     const int g = rho_gate(rho), up = rho_unit(rho);
     float v = 0.0f;
-    if (u < H && up < H) v = M[(long long)u * 4 * H + (long long)g * H + up];
+    if (u < H && up < H && g < G) v = M[(long long)u * G * H + (long long)g * H + up];
     store_planes(prec, p0, p1, e, v, pow2f(kWScaleLog2));
   }
 }
 
 // dx0 operand: W_0^T, rows = input features (Ip), K = 4Hp in rho order.
 __global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, int Ip, int prec,
-                           void* p0, void* p1) {
+                           void* p0, void* p1, int G = 4) {
   const int G4p = 4 * Hp;
   const long long total = (long long)Ip * G4p;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -95,17 +97,17 @@ __global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, i
     const int rho = (int)(e - (long long)i * G4p);
     const int g = rho_gate(rho), u = rho_unit(rho);
     float v = 0.0f;
-    if (i < I && u < H) v = W0[(long long)i * 4 * H + (long long)g * H + u];
+    if (i < I && u < H && g < G) v = W0[(long long)i * G * H + (long long)g * H + u];
     store_planes(prec, p0, p1, e, v, pow2f(kWScaleLog2));
   }
 }
 
 // Reference-order padded bias: dst[g*Hp + u] = b[g*H + u].
-__global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* dst) {
+__global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* dst, int G = 4) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 4 * Hp) return;
   const int g = e / Hp, u = e - g * Hp;
-  dst[e] = (u < H && b) ? b[g * H + u] : 0.0f;
+  dst[e] = (u < H && g < G && b) ? b[g * H + u] : 0.0f;
 }
 
 // Column-block padding: src is R x (nblk*B) column-major, dst is Rp x (nblk*Bp) starting at
@@ -242,9 +244,9 @@ struct DbGroup {
   const float* dbp[kDbGroup];
   float* db[kDbGroup];
 };
-__global__ void k_db_reduce_layers(DbGroup grp, int slices, int H, int Hp) {
+__global__ void k_db_reduce_layers(DbGroup grp, int slices, int H, int Hp, int G = 4) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= 4 * H) return;
+  if (e >= G * H) return;
   const float* dbp = grp.dbp[blockIdx.y];
   const int g = e / H, u = e - g * H;
   float acc = 0.0f;

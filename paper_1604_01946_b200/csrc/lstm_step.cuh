@@ -69,6 +69,7 @@ struct FwdLayer {
   // rows), copied once into tensor memory as the A operand of the lo x hi products
   const uint16_t* alo;
   int alo_ld, alo_rows;
+  float* zrh;                // GRU: R-side candidate pre-activation R_n h_{t-1} tape (Hp x Bp T)
 };
 
 struct BwdLayer {
@@ -99,6 +100,15 @@ struct BwdLayer {
   const CUtensorMap* bg2;
   const uint16_t* alo;       // cluster schedule, fp16x2: lo plane of [W_{l+1}^T | R_l^T] (as FwdLayer)
   int alo_ld, alo_rows;
+  // GRU / RNN (cluster schedule): the layer's h tape (GRU h_{t-1}, RNN h_t), the zrh tape, and the
+  // R-side gate gradients dgr (GRU only: they differ from dgw in the candidate gate) -- fp32 tape,
+  // operand planes (dR), and the pre-swizzled image the recurrence reads; dgsw then holds dgr and
+  // dgwsw the W-side image the layer below reads
+  const float* h;
+  const float* zrh;
+  float* dgr;
+  void* dgrop[2];
+  uint8_t* dgwsw;
 };
 
 struct RecParams {

@@ -103,6 +103,7 @@ struct ClParams {
   float unscale;  // critical groups, fp16x2: 2^-(kWScaleLog2 + kHScaleLog2) forward (R.h),
                   // 2^-(kWScaleLog2 + kGScaleLog2) backward (R^T.dG); off groups: ClOff::unscale
   unsigned* gmax; // backward: max |dG| of the pass (float bits; range check of the scaled dG planes)
+  int kind;       // cell kind (CellKindDev): the RNN variants share one instantiation
   int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 512 = fp16x2 forward
               // without the lo-plane stores, 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
@@ -573,7 +574,9 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // ====================================================================== forward
 // grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
-template <class P, int kChunks>
+// GRU (linear before reset, cells.hpp:283-333): the candidate gate keeps its two halves apart --
+// rows of gate slot 2 get W_n x, rows of the unused slot 3 get R_n h (written by the slot-2 threads).
+template <class P, int kChunks, int kKind = kCellLstm>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
                                            int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp, float unscale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -589,14 +592,25 @@ __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool 
   float zw[kChunks * 8];
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i) zw[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
+  if constexpr (kKind == kCellGru) {
+    if (q == 3) return;
+    if (q == 2) {
+#pragma unroll
+      for (int i = 0; i < kChunks * 8; ++i) {
+        sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row, zw[i]);
+        sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row + 32, v[i]);
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i)
     sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row, zw[i] + v[i]);  // (zw + zr), cells.hpp:240
 }
 
 // kCC: the critical members' owned columns / 16 (Bp / kc / 16), one instantiation each so the
-// register allocation of one variant does not spill another's hot loop
-template <class P, int kCC>
+// register allocation of one variant does not spill another's hot loop; kKind: the cell class
+template <class P, int kCC, int kKind = kCellLstm>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_fwd(const FwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -731,11 +745,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const long long Hp = p.Hp, G4 = 4 * Hp;
       const int own0 = m * nco;
       const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u], bc = Le.bias[3 * Hp + u];
-      float creg[kClMaxN / 8];  // c_{t-1} of owned columns cl = cg + 8k (c tape block 0 = c0)
+      // LSTM: c_{t-1} of owned columns cl = cg + 8k (c tape block 0 = c0); GRU: h_{t-1} (h0)
+      float creg[kClMaxN / 8];
 #pragma unroll
       for (int k = 0; k < kClMaxN / 8; ++k) {
         const int cl = cg + 8 * k;
-        creg[k] = cl < nco ? Le.c[(long long)(own0 + cl) * Hp + u] : 0.0f;
+        const float* st = kKind == kCellGru ? Le.h : Le.c;
+        creg[k] = (cl < nco && kKind != kCellRnnTanh) ? st[(long long)(own0 + cl) * Hp + u] : 0.0f;
       }
       const float* sum = reinterpret_cast<const float*>(S.b);
       // h_t staging after the gate sums, in the B ring: idle between this step's MMA and the
@@ -752,7 +768,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
         const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
-        cl_fwd_sum<P, kCC>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p, p.unscale);
+        cl_fwd_sum<P, kCC, kKind>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p, p.unscale);
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
@@ -768,20 +784,42 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         for (int k = 0; k < kClMaxN / 8; ++k) {
           const int cl = cg + 8 * k;
           if (cl >= nco) break;
-          const float ai = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
-          const float af = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
-          const float ao = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j) + bo;
-          const float ac = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j) + bc;
-          iv[k] = act_sigmoid<P>(ai);
-          fv[k] = act_sigmoid<P>(af);
-          ov[k] = act_sigmoid<P>(ao);
-          cb[k] = act_tanh<P>(ac);
-          const float t1 = fv[k] * creg[k];
-          const float t2 = iv[k] * cb[k];
-          cv[k] = t1 + t2;
-          tcv[k] = act_tanh<P>(cv[k]);
-          hv[k] = ov[k] * tcv[k];
-          creg[k] = cv[k];
+          if constexpr (kKind == kCellLstm) {
+            const float ai = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
+            const float af = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
+            const float ao = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j) + bo;
+            const float ac = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j) + bc;
+            iv[k] = act_sigmoid<P>(ai);
+            fv[k] = act_sigmoid<P>(af);
+            ov[k] = act_sigmoid<P>(ao);
+            cb[k] = act_tanh<P>(ac);
+            const float t1 = fv[k] * creg[k];
+            const float t2 = iv[k] * cb[k];
+            cv[k] = t1 + t2;
+            tcv[k] = act_tanh<P>(cv[k]);
+            hv[k] = ov[k] * tcv[k];
+            creg[k] = cv[k];
+          } else if constexpr (kKind == kCellGru) {  // cells.hpp:294-313 operation order
+            const float ar = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
+            const float au = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
+            const float zwn = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j);
+            const float zrn = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j);
+            iv[k] = act_sigmoid<P>(ar);  // r
+            fv[k] = act_sigmoid<P>(au);  // u
+            const float t1 = zwn + bo;   // W_n x + b_n
+            const float t2 = iv[k] * zrn;
+            const float an = t1 + t2;
+            ov[k] = act_tanh<P>(an);     // n
+            const float t3 = fv[k] * creg[k];
+            const float om = 1.0f - fv[k];
+            const float t4 = om * ov[k];
+            hv[k] = t3 + t4;
+            cb[k] = zrn;  // the zrh tape (R_n h_{t-1}, the backward's reset-gate input)
+            creg[k] = hv[k];
+          } else {  // RNN (cells.hpp:200-212)
+            const float a = lds_f32(sum + (size_t)cl * kTileM + j) + bi;
+            hv[k] = p.kind == kCellRnnRelu ? (a > 0.0f ? a : 0.0f) : act_tanh<P>(a);
+          }
           if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block (scaled, common.cuh)
             __half hh, hl;
             f16x2_split(hv[k] * pow2f(kHScaleLog2), hh, hl);
@@ -826,16 +864,20 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const int cl = cg + 8 * k;
           if (cl >= nco) break;
           const long long col_prev = colp + cl, col_new = col_prev + N;
-          Le.c[col_new * Hp + u] = cv[k];
+          if constexpr (kKind == kCellLstm) Le.c[col_new * Hp + u] = cv[k];
           Le.h[col_new * Hp + u] = hv[k];
           store_operand<P>(Le.hop, col_new * Hp + u, P::kPlanes == 2 ? hv[k] * pow2f(kHScaleLog2) : hv[k]);
-          if (Le.gates) {
+          if (Le.gates && kKind != kCellRnnTanh) {
             float* gp = Le.gates + col_prev * G4 + u;
             gp[0] = iv[k];
             gp[Hp] = fv[k];
             gp[2 * Hp] = ov[k];
-            gp[3 * Hp] = cb[k];
-            Le.tanhc[col_prev * Hp + u] = tcv[k];
+            if constexpr (kKind == kCellLstm) {
+              gp[3 * Hp] = cb[k];
+              Le.tanhc[col_prev * Hp + u] = tcv[k];
+            } else {
+              Le.zrh[col_prev * Hp + u] = cb[k];
+            }
           }
         }
         if (et == 0) cl_trace(p, t, 6);
@@ -850,7 +892,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 // R^T.dG_{l,t+1}, 1 off W_{l+1}^T.dG_{l+1,t}; the top layer has no off cluster and adds dy).
 // Critical steps t = T-1 .. -1 (t = -1: dh0 = R^T dG_{l,0}, dc0 = carry; engine.hpp:163-170),
 // off steps t = T-1 .. 0. Iteration it <-> t = T-1-it.
-template <class P, int kChunks>
+template <class P, int kChunks, int kKind = kCellLstm>
 __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
                                             uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed,
                                             bool sys, uint32_t flag_target) {
@@ -874,7 +916,9 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   // wait for this CTA's own publish): the tile's 8 k-blocks x nco rows of the swizzled image
   const uint32_t dstg = smem_u32(S.b);
   // (measured at B: backward 0.880 ms staged vs 0.903 scattered; RW_CL_DEBUG bit 32 = scattered)
-  const bool staged = !(p.debug & 40) && (size_t)p.stages * BR * kRowBytes >= (size_t)8 * P::kPlanes * nco * 128;
+  // GRU writes two images (dgr for the recurrence, dgw for the layer below): scattered stores
+  const bool staged = kKind != kCellGru && !(p.debug & 40) &&
+                      (size_t)p.stages * BR * kRowBytes >= (size_t)8 * P::kPlanes * nco * 128;
   if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
   for (int it = 0; it <= p.T; ++it) {
     const int t = p.T - 1 - it;
@@ -889,17 +933,27 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         if (t < 0 || !uok || (p.debug & 4)) continue;
         const long long col = (long long)t * N + n;
         const float* gp = Ly.gates + col * G4 + u;
-        pi[j] = gp[0];
-        pf[j] = gp[Hp];
-        po[j] = gp[2 * Hp];
-        pcb[j] = gp[3 * Hp];
-        ptc[j] = Ly.tanhc[col * Hp + u];
-        pcp[j] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+        if constexpr (kKind == kCellLstm) {
+          pi[j] = gp[0];
+          pf[j] = gp[Hp];
+          po[j] = gp[2 * Hp];
+          pcb[j] = gp[3 * Hp];
+          ptc[j] = Ly.tanhc[col * Hp + u];
+          pcp[j] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+        } else if constexpr (kKind == kCellGru) {
+          pi[j] = gp[0];                 // r
+          pf[j] = gp[Hp];                // u
+          po[j] = gp[2 * Hp];            // n
+          pcb[j] = Ly.zrh[col * Hp + u]; // R_n h_{t-1}
+          pcp[j] = Ly.h[col * Hp + u];   // h_{t-1}: block t of the h tape
+        } else {
+          pcp[j] = Ly.h[(col + N) * Hp + u];  // h_t: block t + 1
+        }
         if (Ly.dy && u < p.H && n < p.B) dyv[j] = Ly.dy[((long long)t * p.B + n) * p.H + u];
       }
     };
     load_tapes(0);  // independent of this step's GEMM: in flight while we wait
-    if (t >= 1) {
+    if (kKind == kCellLstm && t >= 1) {
       // pull next step's tape lines (gates x4, tanh(c), c of this warp's 32 units and its
       // columns) from HBM into L2 now, so next step's loads are L2 hits
       const long long tn = t - 1;
@@ -933,13 +987,13 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       cl_rx_next(S, m, kc, nco);
     }
     if (off) ++offc;
-    if (t < 0) {  // dh0 / dc0
+    if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170); GRU: dh0 = R^T dgr_0 + the direct term dh_0 u_0
       if (uok) {
 #pragma unroll
         for (int i = 0; i < kChunks * 8; ++i) {
           const long long n = cbase + i;
-          Ly.dh0[n * Hp + u] = acc[i];
-          Ly.dc0[n * Hp + u] = carry[i];
+          Ly.dh0[n * Hp + u] = kKind == kCellGru ? acc[i] + carry[i] : acc[i];
+          if constexpr (kKind == kCellLstm) Ly.dc0[n * Hp + u] = carry[i];
         }
       }
       break;
@@ -951,22 +1005,52 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int k = i * 8 + j;
-        // cells.hpp:424-447 operation order; dh = d_above + carry_h
-        const float dh = off ? dab[k] + acc[k] : (Ly.dy ? dyv[j] + acc[k] : acc[k]);
-        const float q1 = dh * po[j];
-        const float s0 = ptc[j] * ptc[j];
-        const float s1 = 1.0f - s0;
-        const float q2 = q1 * s1;
-        const float dc = carry[k] + q2;
-        const float a1 = dc * pcb[j], a2 = a1 * pi[j], a3 = 1.0f - pi[j];
-        const float b1 = dc * pcp[j], b2 = b1 * pf[j], b3 = 1.0f - pf[j];
-        const float c1 = dh * ptc[j], c2 = c1 * po[j], c3 = 1.0f - po[j];
-        const float d1 = dc * pi[j], d2 = pcb[j] * pcb[j], d3 = 1.0f - d2;
-        g_i[k] = a2 * a3;
-        g_f[k] = b2 * b3;
-        g_o[k] = c2 * c3;
-        g_c[k] = d1 * d3;
-        carry[k] = dc * pf[j];
+        // dh = d_above + carry_h (GRU: carry_h = R^T dgr_{t+1} + the direct term dh_{t+1} u_{t+1})
+        const float ch = kKind == kCellGru ? acc[k] + carry[k] : acc[k];
+        const float dh = off ? dab[k] + ch : (Ly.dy ? dyv[j] + ch : ch);
+        if constexpr (kKind == kCellLstm) {  // cells.hpp:424-447 operation order
+          const float q1 = dh * po[j];
+          const float s0 = ptc[j] * ptc[j];
+          const float s1 = 1.0f - s0;
+          const float q2 = q1 * s1;
+          const float dc = carry[k] + q2;
+          const float a1 = dc * pcb[j], a2 = a1 * pi[j], a3 = 1.0f - pi[j];
+          const float b1 = dc * pcp[j], b2 = b1 * pf[j], b3 = 1.0f - pf[j];
+          const float c1 = dh * ptc[j], c2 = c1 * po[j], c3 = 1.0f - po[j];
+          const float d1 = dc * pi[j], d2 = pcb[j] * pcb[j], d3 = 1.0f - d2;
+          g_i[k] = a2 * a3;
+          g_f[k] = b2 * b3;
+          g_o[k] = c2 * c3;
+          g_c[k] = d1 * d3;
+          carry[k] = dc * pf[j];
+        } else if constexpr (kKind == kCellGru) {  // cells.hpp:514-538 operation order
+          const float om = 1.0f - pf[j];
+          const float dn = dh * om;
+          const float s = po[j] * po[j];
+          const float s1 = 1.0f - s;
+          const float dnp = dn * s1;
+          const float tt = pcp[j] - po[j];
+          const float q = dh * tt;
+          const float q2 = q * pf[j];
+          const float dgu = q2 * om;
+          const float r0 = dnp * pcb[j];
+          const float r1 = r0 * pi[j];
+          const float r2 = 1.0f - pi[j];
+          g_i[k] = r1 * r2;     // dgw = dgr (reset gate)
+          g_f[k] = dgu;         // dgw = dgr (update gate)
+          g_o[k] = dnp;         // dgw (candidate); dgr = dnp r
+          g_c[k] = dnp * pi[j]; // slot 3 carries dgr of the candidate (slot 3 of dgw is zero)
+          carry[k] = dh * pf[j];
+        } else {  // RNN (cells.hpp:370-383)
+          if (p.kind == kCellRnnRelu) {
+            g_i[k] = pcp[j] > 0.0f ? dh : 0.0f;
+          } else {
+            const float s = pcp[j] * pcp[j];
+            const float s1 = 1.0f - s;
+            g_i[k] = dh * s1;
+          }
+          g_f[k] = g_o[k] = g_c[k] = 0.0f;
+        }
         if (staged) {
           // K offset within the tile's 8 k-blocks: rho_of(g, u) - 4 * tile * 128; staging rows
           // (k-block, plane, owned column) -- fp16x2 keeps each k-block's hi and lo runs adjacent
@@ -990,9 +1074,26 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
         } else if (uok && !(p.debug & 8)) {
           uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
           const int n = cbase + k;
+          if constexpr (kKind == kCellGru) {  // the W-side image (layer below): slots r, u, n, 0
+            uint8_t* wblk = Ly.dgwsw + (size_t)t * G4 * BR * 2;
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+              const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g_o[k];
+              if constexpr (P::kPlanes == 2) {
+                __half hh, hl;
+                f16x2_split(gv * kGS, hh, hl);
+                *reinterpret_cast<__half*>(wblk + sw_off(rho_of(g, u), n, BR)) = hh;
+                *reinterpret_cast<__half*>(wblk + sw_off(rho_of(g, u), N + n, BR)) = hl;
+              } else {
+                *reinterpret_cast<__nv_bfloat16*>(wblk + sw_off(rho_of(g, u), n, N)) = __float2bfloat16_rn(gv);
+              }
+            }
+          }
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+            // the R-side image (this layer's recurrence); GRU: slots r, u, n <- dgr (slot 3's value), 0
+            float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+            if (kKind == kCellGru) gv = g == 2 ? g_c[k] : g == 3 ? 0.0f : gv;
             if constexpr (P::kPlanes == 2) {
               __half hh, hl;
               gmax = fmaxf(gmax, fabsf(gv));
@@ -1033,19 +1134,30 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
 #pragma unroll
       for (int k = 0; k < kChunks * 8; ++k) {
         const long long ob = ((long long)t * N + cbase + k) * G4;
+        const float wc = kKind == kCellGru ? 0.0f : g_c[k];  // slot 3 of dgw (GRU: holds dgr_n)
         store_operand<P>(Ly.dgop, ob + rho_of(0, u), g_i[k] * kGS);
         store_operand<P>(Ly.dgop, ob + rho_of(1, u), g_f[k] * kGS);
         store_operand<P>(Ly.dgop, ob + rho_of(2, u), g_o[k] * kGS);
-        store_operand<P>(Ly.dgop, ob + rho_of(3, u), g_c[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rho_of(3, u), wc * kGS);
         float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
         dgp[0] = g_i[k];
         dgp[Hp] = g_f[k];
         dgp[2 * Hp] = g_o[k];
-        dgp[3 * Hp] = g_c[k];
+        dgp[3 * Hp] = wc;
+        if constexpr (kKind == kCellGru) {  // dgr: r, u as dgw, candidate dnp r (cells.hpp:527-529)
+          store_operand<P>(Ly.dgrop, ob + rho_of(0, u), g_i[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rho_of(1, u), g_f[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rho_of(2, u), g_c[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rho_of(3, u), 0.0f);
+          float* dgq = Ly.dgr + ((long long)t * N + cbase + k) * G4 + u;
+          dgq[0] = g_i[k];
+          dgq[Hp] = g_f[k];
+          dgq[2 * Hp] = g_c[k];
+        }
         si += g_i[k];
         sf += g_f[k];
         so += g_o[k];
-        sc += g_c[k];
+        sc += wc;
       }
     }
     if (et == 0) cl_trace(p, it, 6);
@@ -1065,7 +1177,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   }
 }
 
-template <class P, int kCC>
+template <class P, int kCC, int kKind = kCellLstm>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_cl_bwd(const BwdLayer* __restrict__ layers, ClParams p) {
   const int y = blockIdx.y;
@@ -1195,7 +1307,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         default: cl_off_loop<P, 1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
       }
     } else {
-      cl_bwd_crit<P, kCC>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
+      cl_bwd_crit<P, kCC, kKind>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
     }
   }
   cl_teardown(tmem_base, tmem_cols);

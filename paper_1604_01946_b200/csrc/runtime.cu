@@ -222,6 +222,7 @@ struct rw_ctx {
   int dev = 0;
   int prec = kBF16, planes = 1, elem = 2, atomK = 64;
   int L = 0, H = 0, I = 0, B = 0, T = 0, Hp = 0, Ip = 0, Bp = 0;
+  int kind = 3, G = 4;  // cell kind (rw_config.cell_kind: 0 RNN tanh, 1 RNN relu, 2 GRU, 3 LSTM), gates
   std::string err;
 
   // parameters (reference layout, device) + packed operands
@@ -282,6 +283,9 @@ struct rw_ctx {
   uint32_t* pp_next_ready = nullptr;         // next stage's input-ready counter (peer pointer)
   std::vector<void*> pp_opened;              // IPC-opened peer allocations
   std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
+  // GRU: zrh tapes, R-side gate gradients dgr (fp32 tape + operand planes), the W-side image dgwsw
+  std::vector<DevBuf> zrh, dgr, dgwsw;
+  std::vector<Operand> dgrop;
   DevBuf xsw;
   int bn_wg = 128, bn_dx = 128, st_wg = 4, st_dx = 4, bn_ls = 256;
   DevBuf gemm_lsf, gemm_lsb, dabove;  // layer-sequential schedule
@@ -441,16 +445,16 @@ void launch_rec(void* kernel, const void* layers, const RecParams& rp, int grid_
 // cluster (ko_l members per layer), each member holding <= 512 K of its weight slice. Returns
 // false when the shape does not fit (batch > 64, owned columns not a multiple of 16, too many
 // CTAs, shared memory, or clusters not co-resident).
-void* cl_kernel(int prec, bool fwd, int nco) { return cl_kernel_ptr(prec, fwd, nco); }
+void* cl_kernel(int prec, bool fwd, int nco, int kind = kCellLstm) { return cl_kernel_ptr(prec, fwd, nco, kind); }
 
 // prec: kBF16 or kF16x2 (two operand planes per stage; A_lo in tensor memory next to the
 // 4 x Bp accumulator columns, which fits 512 columns for Bp <= 64 and <= 8 k-blocks per member)
 bool plan_cluster(int prec, bool fwd, int kc, const std::vector<int>& ko, int tiles, int L, int Bp, int sms,
-                  ClPlan& out) {
+                  ClPlan& out, int kind = kCellLstm) {
   if (Bp > kClMaxN || Bp % kc || (Bp / kc) % 16) return false;
   if (prec == kF16x2 && 4 * Bp + kClKBlocks * 32 > 512) return false;
   const int rows = prec_planes(prec) * Bp;  // operand rows per stage
-  void* kernel = cl_kernel(prec, fwd, Bp / kc);
+  void* kernel = cl_kernel(prec, fwd, Bp / kc, kind);
   int cs = kc, komin = kc;
   for (int k : ko) {
     if (k == 0) continue;
@@ -617,7 +621,9 @@ void validate(const rw_config& c) {
     einval("LadderConfig: opt_level must be in 0..6, got " + std::to_string(c.opt_level));
   if (c.batch_steps > c.steps)
     einval("LadderConfig: batch_steps " + std::to_string(c.batch_steps) + " exceeds steps " + std::to_string(c.steps));
-  if (c.cell_kind != 3) einval("rnnwave_sm100: only CellKind::Lstm (3) is implemented on the device");
+  if (c.cell_kind < 0 || c.cell_kind > 3)
+    einval("LadderConfig: cell kind must be 0 (rnn-tanh), 1 (rnn-relu), 2 (gru) or 3 (lstm), got " +
+           std::to_string(c.cell_kind));
   if (c.precision != RW_PREC_BF16 && c.precision != RW_PREC_FP32) einval("rnnwave_sm100: unknown precision");
   if (c.layers > kMaxLayers) einval("rnnwave_sm100: at most 16 layers");
 }
@@ -650,6 +656,8 @@ void build(rw_ctx* x) {
   x->Hp = round_up(x->H, 64);
   x->Ip = round_up(x->I, 64);
   x->Bp = round_up(x->B, 16);
+  x->kind = c.cell_kind;
+  x->G = cell_gates(c.cell_kind);
   const int L = x->L, Hp = x->Hp, Ip = x->Ip, Bp = x->Bp, T = x->T, H = x->H, I = x->I, B = x->B;
   const long long G4p = 4LL * Hp;
   const long long colsT = (long long)Bp * T, colsT1 = (long long)Bp * (T + 1);
@@ -670,14 +678,14 @@ void build(rw_ctx* x) {
     const int kc_f = ceil_div(Hp / 64, kClKBlocks);
     std::vector<int> ko_f(L), ko_b(L);
     for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
-    cl_f = plan_cluster(prec, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf);
+    cl_f = plan_cluster(prec, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf, c.cell_kind);
     // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
     // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
     const int nkb_r = 4 * Hp / 64;
     int kc_b = ceil_div(nkb_r, kClKBlocks);
     while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
     for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
-    cl_b = plan_cluster(prec, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb);
+    cl_b = plan_cluster(prec, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb, c.cell_kind);
   };
   const bool want_cl = c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER;
   if (c.precision == RW_PREC_BF16) {
@@ -692,6 +700,14 @@ void build(rw_ctx* x) {
       if (!(cl_f && cl_b)) cl_f = cl_b = false;
     }
   }
+  // GRU and vanilla-RNN cells run on the cluster schedule only: their epilogues need the input and
+  // recurrent products apart (GRU's linear-before-reset candidate gate), which is that schedule's
+  // split of roles (rec_cluster.cuh); the other schedules fuse them into one accumulator
+  if (x->kind != kCellLstm && !(cl_f && cl_b))
+    einval(std::string("rnnwave_sm100: ") + (x->kind == kCellGru ? "GRU" : "RNN") +
+           " cells run on the cluster schedule, which does not fit this configuration (batch <= 64, owned "
+           "columns multiple of 16, CTAs and clusters co-resident" +
+           (c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER ? ")" : "; schedule must be auto or cluster)"));
   x->planes = prec_planes(x->prec);
   x->elem = prec_elem(x->prec);
   x->atomK = prec_atomk(x->prec);
@@ -874,6 +890,18 @@ void build(rw_ctx* x) {
     x->dgsw.resize(L);
     for (int l = 0; l < L; ++l) x->dgsw[l].alloc((size_t)G4p * colsT * 2 * x->planes);
   }
+  if (x->kind == kCellGru) {  // zrh tapes; dgr (fp32 + operand planes); the W-side dG images
+    x->zrh.resize(L);
+    x->dgr.resize(L);
+    x->dgrop.resize(L);
+    x->dgwsw.resize(L);
+    for (int l = 0; l < L; ++l) {
+      x->zrh[l].alloc((size_t)Hp * colsT * 4);
+      x->dgr[l].alloc((size_t)G4p * colsT * 4);
+      x->dgrop[l].alloc(x->prec, (size_t)G4p * colsT);
+      x->dgwsw[l].alloc((size_t)G4p * colsT * 2 * x->planes);
+    }
+  }
   // fp32-parity: accumulate every acc_kb k-blocks in a separate TMEM accumulator (<= 512 cols),
   // summed in fp32 by the epilogue. When that would leave chains longer than kPromoKB k-blocks
   // (large H: 512 / Bp accumulators cannot cover K), run the promotion ring instead: chunks of
@@ -912,7 +940,7 @@ void build(rw_ctx* x) {
   // ---- tensor maps
   const int aK = x->atomK, prec = x->prec;
   std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
-      m_dgMN(2 * L);
+      m_dgMN(2 * L), m_dgrMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
   int m_xK2 = 0;  // CTA-pair forward: Bp/2-row boxes (bf16: one plane)
   std::vector<int> m_hopK2(L), m_dgK2(L);
@@ -937,6 +965,8 @@ void build(rw_ctx* x) {
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
       if (x->pair_b) m_dgK2[l] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp / 2));
       m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
+      m_dgrMN[2 * l + p] = x->kind == kCellGru ? add_map(x, make_map(x->dgrop[l].p(p), prec, G4p, colsT, aK, aK))
+                                               : m_dgMN[2 * l + p];
     }
     if (kmajor_wg) {
       for (int l = 0; l < L; ++l) {
@@ -1026,6 +1056,18 @@ void build(rw_ctx* x) {
       Bd.dgsw = static_cast<uint8_t*>(x->dgsw[l].p);
       Bd.bupsw = l < L - 1 ? static_cast<const uint8_t*>(x->dgsw[l + 1].p) : nullptr;
     }
+    // GRU / RNN tapes (cluster schedule); for LSTM / RNN dgr is dgw (aliases)
+    Bd.h = x->h[l].f();
+    Bd.dgwsw = Bd.dgsw;
+    Bd.dgr = Bd.dg;
+    for (int p = 0; p < 2; ++p) Bd.dgrop[p] = Bd.dgop[p];
+    if (x->kind == kCellGru) {
+      fl[l].zrh = x->zrh[l].f();
+      Bd.zrh = x->zrh[l].f();
+      Bd.dgr = x->dgr[l].f();
+      Bd.dgwsw = static_cast<uint8_t*>(x->dgwsw[l].p);
+      for (int p = 0; p < 2; ++p) Bd.dgrop[p] = x->dgrop[l].p(p);
+    }
   }
   x->fwd_layers.alloc(sizeof(FwdLayer) * L);
   x->bwd_layers.alloc(sizeof(BwdLayer) * L);
@@ -1084,7 +1126,8 @@ void build(rw_ctx* x) {
         ClOff& o = x->off_b_h[l];
         o.a = bl[l].a[0];
         o.kdim = 4 * Hp;
-        o.op = static_cast<const uint8_t*>(x->dgsw[l + 1].p);
+        // W_{l+1}^T multiplies the W-side gradients of layer l + 1 (GRU: dgw, not dgr)
+        o.op = static_cast<const uint8_t*>(x->kind == kCellGru ? x->dgwsw[l + 1].p : x->dgsw[l + 1].p);
         o.op_blk_off = 0;
         o.op_flags = bl[l + 1].flags;
         o.ring = x->ring_b_h[l].ring;
@@ -1123,7 +1166,7 @@ void build(rw_ctx* x) {
     d.a_k_off = 0;
     d.b_k_off = l == 0 ? 0 : Bp;  // X_l = h_{l-1} blocks 1..T
     d.d = x->dW[l].f();
-    d.ldd = 4LL * H;
+    d.ldd = (long long)x->G * H;
     // fp16x2: dG planes carry 2^kGScaleLog2, x 2^kXScaleLog2, h 2^kHScaleLog2 (common.cuh)
     d.alpha = x->prec == kF16x2 ? pow2f(-(kGScaleLog2 + (l == 0 ? kXScaleLog2 : kHScaleLog2))) : 1.0f;
     d.row_mode = kRowGateUnperm;
@@ -1132,12 +1175,15 @@ void build(rw_ctx* x) {
     d.Hp = Hp;
     d.B = B;
     d.Bp = Bp;
-    d.m_valid = 4 * H;
+    d.m_valid = x->G * H;
+    d.gates = x->G;
     d.n_valid = Il;
     wg.push_back(d);
     GemmDesc r = d;
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < 2; ++p) {
       r.b[p] = kmajor_wg ? mp(m_hT[2 * l + (p % x->planes)], p) : mp(m_hopMN[2 * l + (p % x->planes)], p);
+      if (!kmajor_wg) r.a[p] = mp(m_dgrMN[2 * l + (p % x->planes)], p);  // dR = dgr h^T (GRU: dgr != dgw)
+    }
     r.N = Hp;
     r.b_k_off = 0;  // Hprev = blocks 0..T-1
     r.alpha = x->prec == kF16x2 ? pow2f(-(kGScaleLog2 + kHScaleLog2)) : 1.0f;
@@ -1295,13 +1341,13 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
     ++g_launches;
     k_pack_wf<<<dim3(ceil_div(Ipl + Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp,
                                                                                Ipl, x->prec, x->wf[l].p(0),
-                                                                               x->wf[l].p(1));
+                                                                               x->wf[l].p(1), x->G);
     const float* wup = l < L - 1 ? x->W[l + 1].f() : nullptr;
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(wup, x->R[l].f(), H, Hp, x->prec,
-                                                             x->wb[l].p(0), x->wb[l].p(1));
+                                                             x->wb[l].p(0), x->wb[l].p(1), x->G);
     ++g_launches;
-    k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f());
+    k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f(), x->G);
   }
   if (x->pp_next && x->wn_raw.p) {  // forward boundary group: the next stage's W_first (rw_pp_set_next_w)
     ++g_launches;
@@ -1315,7 +1361,7 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   }
   ++g_launches;
   k_pack_w0t<<<grid_for((long long)Ip * 4 * Hp), 256, 0, s>>>(x->W[0].f(), H, I, Hp, Ip, x->prec,
-                                                             x->w0t.p(0), x->w0t.p(1));
+                                                             x->w0t.p(0), x->w0t.p(1), x->G);
   RW_CUDA(cudaGetLastError());
   x->dirty = false;
 }
@@ -1436,6 +1482,7 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.unscale = 1.0f;
   if (x->prec == kF16x2) p.unscale = pow2f(-(kWScaleLog2 + (fwd ? kHScaleLog2 : kGScaleLog2)));
   p.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
+  p.kind = x->kind;
   return p;
 }
 
@@ -1621,9 +1668,9 @@ void allreduce_layer(rw_ctx* x, int l, cudaStream_t s) {
   Nccl& n = nccl();
   const int Il = l == 0 ? x->I : x->H;
   nccl_check(n.GroupStart(), "ncclGroupStart");
-  nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
-  nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
-  nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
+  nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, (unsigned long long)x->G * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
+  nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, (unsigned long long)x->G * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
+  nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, (unsigned long long)x->G * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
 }
 
@@ -1676,7 +1723,7 @@ void run_db(rw_ctx* x, cudaStream_t s) {
       grp.dbp[i] = x->dbp[l0 + i].f();
       grp.db[i] = x->db[l0 + i].f();
     }
-    k_db_reduce_layers<<<dim3(ceil_div(4 * x->H, 256), n), 256, 0, s>>>(grp, slices, x->H, x->Hp);
+    k_db_reduce_layers<<<dim3(ceil_div(x->G * x->H, 256), n), 256, 0, s>>>(grp, slices, x->H, x->Hp, x->G);
   }
   RW_CUDA(cudaGetLastError());
 }
@@ -1911,12 +1958,12 @@ int rw_set_params(rw_ctx* x, int layer, const float* W, const float* R, const fl
     if (!W || !R) einval("rw_set_params: W and R are required");
     RW_CUDA(cudaSetDevice(x->dev));
     const int Il = layer == 0 ? x->I : x->H;
-    RW_CUDA(cudaMemcpy(x->W[layer].p, W, 4ULL * x->H * Il * 4, cudaMemcpyHostToDevice));
-    RW_CUDA(cudaMemcpy(x->R[layer].p, R, 4ULL * x->H * x->H * 4, cudaMemcpyHostToDevice));
+    RW_CUDA(cudaMemcpy(x->W[layer].p, W, (unsigned long long)x->G * x->H * Il * 4, cudaMemcpyHostToDevice));
+    RW_CUDA(cudaMemcpy(x->R[layer].p, R, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyHostToDevice));
     if (b)
-      RW_CUDA(cudaMemcpy(x->bias_raw[layer].p, b, 4ULL * x->H * 4, cudaMemcpyHostToDevice));
+      RW_CUDA(cudaMemcpy(x->bias_raw[layer].p, b, (unsigned long long)x->G * x->H * 4, cudaMemcpyHostToDevice));
     else
-      RW_CUDA(cudaMemset(x->bias_raw[layer].p, 0, 4ULL * x->H * 4));
+      RW_CUDA(cudaMemset(x->bias_raw[layer].p, 0, (unsigned long long)x->G * x->H * 4));
     x->params_set[layer] = 1;
     x->dirty = true;
   });
@@ -1933,6 +1980,7 @@ int rw_forward(rw_ctx* x, const float* xin, int training, const float* const* h0
                const float* const* c0, float* y, uint64_t* tape_id) {
   return guarded(x, [&] {
     if (!xin) einval("forward: x is null, expected " + std::to_string(x->I) + "x" + std::to_string(x->B * x->T));
+    if (c0 && x->kind != kCellLstm) einval("forward: c0 supplied for a cell kind without cell state");
     require_params(x);
     RW_CUDA(cudaSetDevice(x->dev));
     const size_t hb = (size_t)x->H * x->B;
@@ -1988,7 +2036,7 @@ int rw_backward_data(rw_ctx* x, uint64_t tape_id, const float* dy, float* dx0, f
     if (dx0) RW_CUDA(cudaMemcpy(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost));
     for (int l = 0; l < x->L; ++l) {
       if (dh0 && dh0[l]) d2h_unpad(x, x->dh0[l].f(), x->Hp, x->Bp, 0, 1, x->H, x->B, 1, dh0[l]);
-      if (dc0 && dc0[l]) d2h_unpad(x, x->dc0[l].f(), x->Hp, x->Bp, 0, 1, x->H, x->B, 1, dc0[l]);
+      if (dc0 && dc0[l] && x->kind == kCellLstm) d2h_unpad(x, x->dc0[l].f(), x->Hp, x->Bp, 0, 1, x->H, x->B, 1, dc0[l]);
     }
   });
 }
@@ -2003,9 +2051,9 @@ int rw_weight_update(rw_ctx* x, uint64_t tape_id, float* const* dW, float* const
     sync_all(x);
     for (int l = 0; l < x->L; ++l) {
       const int Il = l == 0 ? x->I : x->H;
-      if (dW && dW[l]) RW_CUDA(cudaMemcpy(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost));
-      if (dR && dR[l]) RW_CUDA(cudaMemcpy(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost));
-      if (db && db[l]) RW_CUDA(cudaMemcpy(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost));
+      if (dW && dW[l]) RW_CUDA(cudaMemcpy(dW[l], x->dW[l].p, (unsigned long long)x->G * x->H * Il * 4, cudaMemcpyDeviceToHost));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpy(dR[l], x->dR[l].p, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyDeviceToHost));
+      if (db && db[l]) RW_CUDA(cudaMemcpy(db[l], x->db[l].p, (unsigned long long)x->G * x->H * 4, cudaMemcpyDeviceToHost));
     }
   });
 }
@@ -2029,19 +2077,31 @@ int rw_get_tape(rw_ctx* x, int which, int layer, float* host) {
         d2h_unpad(x, x->h[layer].f(), Hp, Bp, 0, 1, H, B, T + 1, host);
         break;
       case RW_TAPE_C:
+        if (x->kind != kCellLstm) einval("rw_get_tape: c_seq exists for LSTM cells only");
         d2h_unpad(x, x->c[layer].f(), Hp, Bp, 0, 1, H, B, T + 1, host);
+        break;
+      case RW_TAPE_ZRH:
+        if (x->kind != kCellGru) einval("rw_get_tape: zrh_seq exists for GRU cells only");
+        if (!x->tape_training) einval("engine: tape was recorded without training mode");
+        d2h_unpad(x, x->zrh[layer].f(), Hp, Bp, 0, 1, H, B, T, host);
+        break;
+      case RW_TAPE_DGR:
+        if (x->kind != kCellGru) einval("rw_get_tape: dgr_seq exists for GRU cells only");
+        if (!x->bwd_done) einval("rw_get_tape: no backward pass on the current tape");
+        d2h_unpad(x, x->dgr[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
         break;
       case RW_TAPE_GATES:
         if (!x->tape_training) einval("engine: tape was recorded without training mode");
-        d2h_unpad(x, x->gates[layer].f(), Hp, Bp, 0, 4, H, B, T, host);
+        d2h_unpad(x, x->gates[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
         break;
       case RW_TAPE_TANH_C:
+        if (x->kind != kCellLstm) einval("rw_get_tape: tanh_c_seq exists for LSTM cells only");
         if (!x->tape_training) einval("engine: tape was recorded without training mode");
         d2h_unpad(x, x->tanhc[layer].f(), Hp, Bp, 0, 1, H, B, T, host);
         break;
       case RW_TAPE_DGW:
         if (!x->bwd_done) einval("rw_get_tape: no backward pass on the current tape");
-        d2h_unpad(x, x->dg[layer].f(), Hp, Bp, 0, 4, H, B, T, host);
+        d2h_unpad(x, x->dg[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
         break;
       default:
         einval("rw_get_tape: unknown tape id");
@@ -2121,9 +2181,9 @@ extern "C" int rw_train_step(rw_ctx* x, const float* xin, const float* dy, float
     if (dx0) RW_CUDA(cudaMemcpyAsync(dx0, x->dx0.p, xb, cudaMemcpyDeviceToHost, x->cp_out));
     for (int l = 0; l < x->L; ++l) {
       const int Il = l == 0 ? x->I : x->H;
-      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost, x->cp_out));
-      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
-      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
+      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, (unsigned long long)x->G * x->H * Il * 4, cudaMemcpyDeviceToHost, x->cp_out));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
+      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, (unsigned long long)x->G * x->H * 4, cudaMemcpyDeviceToHost, x->cp_out));
     }
     RW_CUDA(cudaEventRecord(x->ev_out, x->cp_out));
   });
@@ -2184,9 +2244,9 @@ int rw_read_outputs(rw_ctx* x, float* y, float* dx0, float* const* dW, float* co
     if (dx0) RW_CUDA(cudaMemcpyAsync(dx0, x->dx0.p, (size_t)x->I * x->B * x->T * 4, cudaMemcpyDeviceToHost, s));
     for (int l = 0; l < x->L; ++l) {
       const int Il = l == 0 ? x->I : x->H;
-      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, 4ULL * x->H * Il * 4, cudaMemcpyDeviceToHost, s));
-      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, 4ULL * x->H * x->H * 4, cudaMemcpyDeviceToHost, s));
-      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, 4ULL * x->H * 4, cudaMemcpyDeviceToHost, s));
+      if (dW && dW[l]) RW_CUDA(cudaMemcpyAsync(dW[l], x->dW[l].p, (unsigned long long)x->G * x->H * Il * 4, cudaMemcpyDeviceToHost, s));
+      if (dR && dR[l]) RW_CUDA(cudaMemcpyAsync(dR[l], x->dR[l].p, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyDeviceToHost, s));
+      if (db && db[l]) RW_CUDA(cudaMemcpyAsync(db[l], x->db[l].p, (unsigned long long)x->G * x->H * 4, cudaMemcpyDeviceToHost, s));
     }
     RW_CUDA(cudaStreamSynchronize(s));
   });
@@ -2268,8 +2328,9 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
   x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16)
-      einval("rw_pp_link: the layer pipeline needs the cluster schedule in both directions (bf16)");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16 ||
+        x->kind != kCellLstm)
+      einval("rw_pp_link: the layer pipeline needs LSTM cells on the cluster schedule in both directions (bf16)");
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
     const long long G4p = 4LL * Hp;
@@ -2282,8 +2343,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.unscale = 1.0f;  // bf16 only (above)
     if (dir == 0) {
       if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
-      x->wn_raw.alloc(4ULL * H * H * 4);
-      RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, 4ULL * H * H * 4, cudaMemcpyHostToDevice));
+      x->wn_raw.alloc((size_t)x->G * H * H * 4);
+      RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, (size_t)x->G * H * H * 4, cudaMemcpyHostToDevice));
       x->wf_next.alloc((size_t)G4p * (Hp + Hp) * 2);
       x->dirty = true;  // repack_params packs W_next into wf_next (again after rw_pp_set_next_w)
       o.kdim = Hp;
@@ -2333,7 +2394,7 @@ extern "C" int rw_pp_set_next_w(rw_ctx* x, const float* W_next) {
     if (!x->pp_next || !x->wn_raw.p) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
     if (!W_next) einval("rw_pp_set_next_w: W_next is null");
     RW_CUDA(cudaSetDevice(x->dev));
-    RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, 4ULL * x->H * x->H * 4, cudaMemcpyHostToDevice));
+    RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyHostToDevice));
     x->dirty = true;
   });
 }
@@ -2393,9 +2454,9 @@ static void allreduce_grads(rw_ctx* x, cudaStream_t s) {
   nccl_check(n.GroupStart(), "ncclGroupStart");
   for (int l = x->L - 1; l >= 0; --l) {  // top layer's gradients are final first
     const int Il = l == 0 ? x->I : x->H;
-    nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, 4ULL * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
-    nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, 4ULL * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
-    nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, 4ULL * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
+    nccl_check(n.AllReduce(x->dW[l].p, x->dW[l].p, (unsigned long long)x->G * x->H * Il, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dW");
+    nccl_check(n.AllReduce(x->dR[l].p, x->dR[l].p, (unsigned long long)x->G * x->H * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce dR");
+    nccl_check(n.AllReduce(x->db[l].p, x->db[l].p, (unsigned long long)x->G * x->H, kNcclFloat32, kNcclSum, x->comm, s), "ncclAllReduce db");
   }
   nccl_check(n.GroupEnd(), "ncclGroupEnd");
 }

@@ -207,6 +207,8 @@ class ForwardTape:
     @property
     def c_seq(self):
         c = self.cfg
+        if c.kind != CELL_LSTM:  # engine.hpp:264: LSTM only
+            return []
         if "_c" not in self.__dict__:
             self.__dict__["_c"] = self._seq(_lib.RW_TAPE_C, c.hidden, c.batch * (c.steps + 1))
         return self.__dict__["_c"]
@@ -217,17 +219,27 @@ class ForwardTape:
         if not self.training:
             return []
         if "_g" not in self.__dict__:
-            self.__dict__["_g"] = self._seq(_lib.RW_TAPE_GATES, 4 * c.hidden, c.batch * c.steps)
+            self.__dict__["_g"] = self._seq(_lib.RW_TAPE_GATES, gate_count(c.kind) * c.hidden, c.batch * c.steps)
         return self.__dict__["_g"]
 
     @property
     def tanh_c_seq(self):
         c = self.cfg
-        if not self.training:
+        if not self.training or c.kind != CELL_LSTM:
             return []
         if "_t" not in self.__dict__:
             self.__dict__["_t"] = self._seq(_lib.RW_TAPE_TANH_C, c.hidden, c.batch * c.steps)
         return self.__dict__["_t"]
+
+    @property
+    def zrh_seq(self):
+        """GRU: R_n h_{t-1} per step (engine.hpp:44)."""
+        c = self.cfg
+        if not self.training or c.kind != 2:
+            return []
+        if "_z" not in self.__dict__:
+            self.__dict__["_z"] = self._seq(_lib.RW_TAPE_ZRH, c.hidden, c.batch * c.steps)
+        return self.__dict__["_z"]
 
 
 @dataclass
@@ -257,18 +269,30 @@ class BackwardState:
     _engine: "Engine | None" = None
     _id: int = 0
 
+    def _dseq(self, which):
+        eng, tid, c = self._engine, self._id, self._engine.cfg
+
+        def fetch(l):
+            eng._require_current(tid)
+            out = fmat(gate_count(c.kind) * c.hidden, c.batch * c.steps)
+            eng._check(eng._L.rw_get_tape(eng._ctx, which, l, _fp(out)))
+            return out
+        return _LazySeq(fetch, c.layers)
+
     @property
     def dgw_seq(self):
         if "_dg" not in self.__dict__:
-            eng, tid, c = self._engine, self._id, self._engine.cfg
-
-            def fetch(l):
-                eng._require_current(tid)
-                out = fmat(4 * c.hidden, c.batch * c.steps)
-                eng._check(eng._L.rw_get_tape(eng._ctx, _lib.RW_TAPE_DGW, l, _fp(out)))
-                return out
-            self.__dict__["_dg"] = _LazySeq(fetch, c.layers)
+            self.__dict__["_dg"] = self._dseq(_lib.RW_TAPE_DGW)
         return self.__dict__["_dg"]
+
+    @property
+    def dgr_seq(self):
+        """GRU: the R-side gate gradients (engine.hpp:57); empty for LSTM / RNN."""
+        if self._engine.cfg.kind != 2:
+            return []
+        if "_dr" not in self.__dict__:
+            self.__dict__["_dr"] = self._dseq(_lib.RW_TAPE_DGR)
+        return self.__dict__["_dr"]
 
 
 @dataclass
@@ -295,16 +319,18 @@ def nccl_unique_id() -> bytes:
 
 
 class Engine:
-    """rnnwave::Engine on one B200. precision: 'fp32' (3xTF32 parity mode, the default like
-    the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent' | 'cluster'."""
+    """rnnwave::Engine on one B200. precision: 'fp32' (the fp32-parity split-operand mode, the
+    default like the fp32 reference) or 'bf16'; schedule: 'auto' | 'stepwise' | 'persistent' |
+    'cluster' | 'layerseq'. Cell kinds: LSTM on every schedule; GRU (linear before reset) and
+    vanilla RNN (tanh / relu) on the cluster schedule (cells.hpp)."""
 
     def __init__(self, cfg: LadderConfig, precision: str = "fp32", schedule: str = "auto",
                  device: int = 0):
         self.cfg = LadderConfig(**cfg.__dict__)
         self.cfg.validate()
-        if self.cfg.kind != CELL_LSTM:
-            raise ValueError(f"rnnwave_sm100: only CellKind::Lstm is implemented on the device, "
-                             f"got {CELL_NAMES.get(self.cfg.kind, '?')}")
+        if self.cfg.kind not in CELL_NAMES:
+            raise ValueError(f"LadderConfig: cell kind must be 0 (rnn-tanh), 1 (rnn-relu), 2 (gru) or 3 (lstm), "
+                             f"got {self.cfg.kind}")
         self.precision = precision
         self.schedule = schedule
         self._L = _lib.load()
@@ -371,7 +397,7 @@ class Engine:
         c = self.cfg
         if len(params) != c.layers:
             raise ValueError(f"engine: expected {c.layers} layer parameter sets, got {len(params)}")
-        gh = 4 * c.hidden
+        gh = gate_count(c.kind) * c.hidden
         for l, p in enumerate(params):
             if (p.w.shape != (gh, c.input_width(l)) or p.r.shape != (gh, c.hidden)
                     or np.asarray(p.bias).size != gh):
@@ -406,6 +432,8 @@ class Engine:
             pretranspose(params)
         if h0 is not None and len(h0) != c.layers:
             raise ValueError("forward: h0 must supply one matrix per layer")
+        if c0 is not None and c.kind != CELL_LSTM:
+            raise ValueError("forward: c0 supplied for a cell kind without cell state")
         hs = [as_matrix(m, c.hidden, c.batch) for m in h0] if h0 is not None else None
         cs = [as_matrix(m, c.hidden, c.batch) for m in c0] if c0 is not None else None
         arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst]) if lst is not None else None  # noqa: E731
@@ -440,8 +468,8 @@ class Engine:
             pretranspose(params)
         dx0 = fmat(c.input, bt)
         dh0 = [fmat(c.hidden, c.batch) for _ in range(c.layers)]
-        dc0 = [fmat(c.hidden, c.batch) for _ in range(c.layers)]
-        arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst])  # noqa: E731
+        dc0 = [fmat(c.hidden, c.batch) for _ in range(c.layers)] if c.kind == CELL_LSTM else []  # engine.hpp:318
+        arr = lambda lst: (_F * c.layers)(*[_fp(a) for a in lst]) if lst else None  # noqa: E731
         self._check(self._L.rw_backward_data(self._ctx, tape._id, _fp(dy), _fp(dx0), arr(dh0), arr(dc0)))
         self._bwd_id = tape._id
         self._deposit_trace(1)
@@ -452,7 +480,7 @@ class Engine:
         self._check_tape(tape)
         if state._id != tape._id or len(state.dh0) != c.layers:
             raise ValueError("weight_update: backward state layer count mismatch")
-        gh = 4 * c.hidden
+        gh = gate_count(c.kind) * c.hidden
         dw = [fmat(gh, c.input_width(l)) for l in range(c.layers)]
         dr = [fmat(gh, c.hidden) for _ in range(c.layers)]
         db = [np.zeros(gh, np.float32) for _ in range(c.layers)]

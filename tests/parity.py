@@ -27,18 +27,21 @@ def errors(got, ref):
 
 def make_case(cfg, seed, bias=False, state=False):
     """SplitMix64 weights/inputs exactly like the reference (init_params, make_input/make_dy),
-    optionally with nonzero bias and initial states (SURVEY §8c asks for both)."""
+    optionally with nonzero bias and initial states (SURVEY §8c asks for both). cfg.kind (the
+    reference's CellKind, default LSTM) selects the cell; c0 exists for LSTM only."""
     from paper_1604_01946_b200 import engine as E
+    kind = getattr(cfg, "kind", 3)
     c = E.LadderConfig(layers=cfg.layers, hidden=cfg.hidden, input=cfg.input, batch=cfg.batch,
-                       steps=cfg.steps, seed=seed)
+                       steps=cfg.steps, seed=seed, kind=kind)
     params = E.init_params(c)
     if bias:
         for l, p in enumerate(params):
-            p.bias = E.splitmix_symmetric(seed, 300 + l, 0.5, 4 * c.hidden)
+            p.bias = E.splitmix_symmetric(seed, 300 + l, 0.5, E.gate_count(kind) * c.hidden)
     h0 = c0 = None
     if state:
         h0 = [E.random_matrix(c.hidden, c.batch, seed, 50 + l) for l in range(c.layers)]
-        c0 = [E.random_matrix(c.hidden, c.batch, seed, 60 + l) for l in range(c.layers)]
+        if kind == 3:
+            c0 = [E.random_matrix(c.hidden, c.batch, seed, 60 + l) for l in range(c.layers)]
     x = E.make_input(c)
     dy = E.make_dy(c)
     return c, params, x, dy, h0, c0
@@ -59,7 +62,8 @@ def run_device(eng, params, x, dy, h0, c0):
     out = {"y": fwd.y, "dx0": bwd.dx0, "dh0": bwd.dh0, "dc0": bwd.dc0, "dw": g.dw, "dr": g.dr,
            "db": g.db}
     out["hT"] = [fwd.tape.h_seq[l][:, c.batch * c.steps:] for l in range(c.layers)]
-    out["cT"] = [fwd.tape.c_seq[l][:, c.batch * c.steps:] for l in range(c.layers)]
+    if c.kind == 3:
+        out["cT"] = [fwd.tape.c_seq[l][:, c.batch * c.steps:] for l in range(c.layers)]
     return out
 
 
@@ -69,11 +73,14 @@ def compare(dev, refo, c):
     rows.append(("y",) + errors(dev["y"], refo["y"]))
     rows.append(("dx0",) + errors(dev["dx0"], refo["dx0"]))
     bt = c.batch * c.steps
+    lstm = getattr(c, "kind", 3) == 3
     for l in range(c.layers):
         rows.append((f"hT[{l}]",) + errors(dev["hT"][l], refo["h_seq"][l][:, bt:]))
-        rows.append((f"cT[{l}]",) + errors(dev["cT"][l], refo["c_seq"][l][:, bt:]))
+        if lstm:
+            rows.append((f"cT[{l}]",) + errors(dev["cT"][l], refo["c_seq"][l][:, bt:]))
         rows.append((f"dh0[{l}]",) + errors(dev["dh0"][l], refo["dh0"][l]))
-        rows.append((f"dc0[{l}]",) + errors(dev["dc0"][l], refo["dc0"][l]))
+        if lstm:
+            rows.append((f"dc0[{l}]",) + errors(dev["dc0"][l], refo["dc0"][l]))
         rows.append((f"dW[{l}]",) + errors(dev["dw"][l], refo["dw"][l]))
         rows.append((f"dR[{l}]",) + errors(dev["dr"][l], refo["dr"][l]))
         rows.append((f"db[{l}]",) + errors(dev["db"][l], refo["db"][l]))

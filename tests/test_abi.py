@@ -63,7 +63,7 @@ def _cfg(**kw):
     (dict(opt_level=7), "opt_level must be in 0..6"),
     (dict(hidden=0), "hidden must be positive"),
     (dict(batch_steps=5), "batch_steps 5 exceeds steps 4"),
-    (dict(cell_kind=2), "only CellKind::Lstm"),
+    (dict(cell_kind=7), "cell kind must be 0 (rnn-tanh), 1 (rnn-relu), 2 (gru) or 3 (lstm), got 7"),
     (dict(workers=0), "workers must be positive"),
 ])
 def test_create_validates_like_reference(kw, msg):
@@ -83,5 +83,5 @@ def test_python_config_validation_messages():
     from paper_1604_01946_b200 import Engine, LadderConfig
     with pytest.raises(ValueError, match="opt_level must be in 0..6, got 7"):
         Engine(LadderConfig(opt_level=7))
-    with pytest.raises(ValueError, match="only CellKind::Lstm"):
-        Engine(LadderConfig(kind=2))
+    with pytest.raises(ValueError, match="cell kind must be"):
+        Engine(LadderConfig(kind=5))
