@@ -164,8 +164,11 @@ __global__ void k_swizzle_op(const uint16_t* __restrict__ s0, const uint16_t* __
 }
 
 // Inverse: dst (G*R x nblk*B) from src (G*Rp x nblk*Bp at src_col_off); G gate blocks.
+// Gs: gate blocks per source column (the source's column stride is Gs * Rp; Gs >= G, e.g. the
+// 4-slot gates / dG tapes read back with G = 3 for GRU); 0 means G.
 __global__ void k_unpad_cols(const float* __restrict__ src, int Rp, int Bp, long long src_col_off,
-                             int G, int R, int B, int nblk, float* __restrict__ dst) {
+                             int G, int R, int B, int nblk, float* __restrict__ dst, int Gs = 0) {
+  if (Gs == 0) Gs = G;
   const long long rows = (long long)G * R;
   const long long total = rows * B * nblk;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -174,7 +177,7 @@ __global__ void k_unpad_cols(const float* __restrict__ src, int Rp, int Bp, long
     const int rr = (int)(e - col * rows);
     const int g = rr / R, r = rr - g * R;
     const int t = (int)(col / B), b = (int)(col - (long long)t * B);
-    dst[e] = src[(src_col_off + (long long)t * Bp + b) * G * Rp + (long long)g * Rp + r];
+    dst[e] = src[(src_col_off + (long long)t * Bp + b) * Gs * Rp + (long long)g * Rp + r];
   }
 }
 

@@ -81,6 +81,8 @@ struct ClOff {
   float unscale;             // fp16x2: 2^-(weight scale + operand scale) of this group's product
   const uint16_t* alo;       // fp16x2: lo plane of the target layer's weights (FwdLayer::alo)
   int alo_ld, alo_rows;
+  int ko;                    // members splitting K (the planner's choice: each owns Bp / ko columns,
+                             // a multiple of 16); 0: ceil(kdim / 512)
 };
 
 struct ClParams {
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const uint32_t flag_target = epoch * (uint32_t)(p.tiles * kc);
   const int nkb_h = p.Hp / 64;
   const int nkb_x = crit ? 0 : Og.kdim / 64;
-  const int ko = crit ? Cr.ko : (nkb_x + kClKBlocks - 1) / kClKBlocks;
+  const int ko = crit ? Cr.ko : (Og.ko ? Og.ko : (nkb_x + kClKBlocks - 1) / kClKBlocks);
   const int n_act = crit ? kc : ko;
   const bool active = m < n_act;
   const int kofs = crit ? Ly.Ipl / 64 : 0;  // the critical slice sits after W's k-blocks in [W|R]
@@ -1208,7 +1210,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int nkb_r = G4p / 64;
   const int kofs = crit && Ly.has_up ? G4p / 64 : 0;  // R^T sits after W_{l+1}^T in [W_{l+1}^T | R_l^T]
   const int nkb_o = crit ? 0 : Og.kdim / 64;
-  const int ko = crit ? Cr.ko : (nkb_o + kClKBlocks - 1) / kClKBlocks;
+  const int ko = crit ? Cr.ko : (Og.ko ? Og.ko : (nkb_o + kClKBlocks - 1) / kClKBlocks);
   const int n_act = crit ? kc : ko;
   const bool active = m < n_act;
   int kb_lo = 0, kb_hi = 0;

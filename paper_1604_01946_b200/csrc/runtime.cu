@@ -674,16 +674,27 @@ void build(rw_ctx* x) {
   // bytes of 3xTF32, and half the tensor-core accumulation steps per K element.
   ClPlan cpf, cpb;
   bool cl_f = false, cl_b = false;
+  std::vector<int> ko_f(L), ko_b(L);  // off-critical members per layer (the rings' publication counts)
   auto try_cluster = [&](int prec) {
     const int kc_f = ceil_div(Hp / 64, kClKBlocks);
-    std::vector<int> ko_f(L), ko_b(L);
-    for (int l = 0; l < L; ++l) ko_f[l] = ceil_div((l == 0 ? Ip : Hp) / 64, kClKBlocks);
+    auto fit = [&](int k, int nkb) {  // >= k members of <= 8 k-blocks that split Bp into 16s
+      while (k < 8 && k < nkb && !(Bp % k == 0 && (Bp / k) % 16 == 0)) ++k;
+      return k;
+    };
+    for (int l = 0; l < L; ++l) {
+      const int nkb = (l == 0 ? Ip : Hp) / 64;
+      ko_f[l] = fit(ceil_div(nkb, kClKBlocks), nkb);
+    }
     cl_f = plan_cluster(prec, true, kc_f, ko_f, Hp / kUnitsPerFwdTile, L, Bp, sms, cpf, c.cell_kind);
     // at least 4 critical members when the K range allows (>= 1 k-block each): small H would
     // otherwise leave one CTA per tile with Bp x 128 cells (measured 6x slower at H = 128)
     const int nkb_r = 4 * Hp / 64;
+    // the smallest member count covering K (<= 8 k-blocks each) that splits the batch into
+    // owned-column groups of a multiple of 16 (e.g. Bp = 48: 3 members), then doubled towards 4
+    auto splits = [&](int k) { return Bp % k == 0 && (Bp / k) % 16 == 0; };
     int kc_b = ceil_div(nkb_r, kClKBlocks);
-    while (kc_b < 4 && kc_b * 2 <= nkb_r && (Bp / (kc_b * 2)) % 16 == 0 && Bp % (kc_b * 2) == 0) kc_b *= 2;
+    while (kc_b <= 8 && kc_b <= nkb_r && !splits(kc_b)) ++kc_b;
+    while (kc_b < 4 && kc_b * 2 <= nkb_r && splits(kc_b * 2)) kc_b *= 2;
     for (int l = 0; l < L; ++l) ko_b[l] = l < L - 1 ? kc_b : 0;
     cl_b = plan_cluster(prec, false, kc_b, ko_b, ceil_div(Hp, kTileM), L, Bp, sms, cpb, c.cell_kind);
   };
@@ -1097,7 +1108,7 @@ void build(rw_ctx* x) {
       x->off_f_h.assign(L, ClOff{});
       for (int l = 0; l < L; ++l) {
         const int Ipl = l == 0 ? Ip : Hp;
-        x->ring_f_h[l] = ring_of(l, ceil_div(Ipl / 64, kClKBlocks), 0);
+        x->ring_f_h[l] = ring_of(l, ko_f[l], 0);
         ClOff& o = x->off_f_h[l];
         o.a = fl[l].a[0];
         o.kdim = Ipl;
@@ -1113,6 +1124,7 @@ void build(rw_ctx* x) {
         o.alo = fl[l].alo;
         o.alo_ld = fl[l].alo_ld;
         o.alo_rows = fl[l].alo_rows;
+        o.ko = ko_f[l];
       }
       x->rows_f = L;
     }
@@ -1121,7 +1133,7 @@ void build(rw_ctx* x) {
       x->off_b_h.assign(L, ClOff{});
       for (int l = 0; l < L; ++l) {
         const bool up = l < L - 1;
-        x->ring_b_h[l] = ring_of(l, up ? ceil_div(4 * Hp / 64, kClKBlocks) : 0, 1);
+        x->ring_b_h[l] = ring_of(l, up ? ko_b[l] : 0, 1);
         if (!up) continue;  // the top layer adds dy instead
         ClOff& o = x->off_b_h[l];
         o.a = bl[l].a[0];
@@ -1138,6 +1150,7 @@ void build(rw_ctx* x) {
         o.alo = bl[l].alo;
         o.alo_ld = bl[l].alo_ld;
         o.alo_rows = bl[l].alo_rows;
+        o.ko = ko_b[l];
       }
       x->rows_b = L;
     }
@@ -1872,10 +1885,10 @@ void sync_all(rw_ctx* x) {
 }
 
 void d2h_unpad(rw_ctx* x, const float* src, int Rp, int Bp, long long col_off, int G, int R, int B,
-               int nblk, float* host) {
+               int nblk, float* host, int Gs = 0) {
   const long long n = (long long)G * R * B * nblk;
   ++g_launches;
-  k_unpad_cols<<<grid_for(n), 256, 0, x->main>>>(src, Rp, Bp, col_off, G, R, B, nblk, x->y_raw.f());
+  k_unpad_cols<<<grid_for(n), 256, 0, x->main>>>(src, Rp, Bp, col_off, G, R, B, nblk, x->y_raw.f(), Gs);
   RW_CUDA(cudaGetLastError());
   RW_CUDA(cudaMemcpyAsync(host, x->y_raw.p, n * 4, cudaMemcpyDeviceToHost, x->main));
   RW_CUDA(cudaStreamSynchronize(x->main));
@@ -2088,11 +2101,11 @@ int rw_get_tape(rw_ctx* x, int which, int layer, float* host) {
       case RW_TAPE_DGR:
         if (x->kind != kCellGru) einval("rw_get_tape: dgr_seq exists for GRU cells only");
         if (!x->bwd_done) einval("rw_get_tape: no backward pass on the current tape");
-        d2h_unpad(x, x->dgr[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
+        d2h_unpad(x, x->dgr[layer].f(), Hp, Bp, 0, x->G, H, B, T, host, 4);
         break;
       case RW_TAPE_GATES:
         if (!x->tape_training) einval("engine: tape was recorded without training mode");
-        d2h_unpad(x, x->gates[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
+        d2h_unpad(x, x->gates[layer].f(), Hp, Bp, 0, x->G, H, B, T, host, 4);  // 4-slot tape
         break;
       case RW_TAPE_TANH_C:
         if (x->kind != kCellLstm) einval("rw_get_tape: tanh_c_seq exists for LSTM cells only");
@@ -2101,7 +2114,7 @@ int rw_get_tape(rw_ctx* x, int which, int layer, float* host) {
         break;
       case RW_TAPE_DGW:
         if (!x->bwd_done) einval("rw_get_tape: no backward pass on the current tape");
-        d2h_unpad(x, x->dg[layer].f(), Hp, Bp, 0, x->G, H, B, T, host);
+        d2h_unpad(x, x->dg[layer].f(), Hp, Bp, 0, x->G, H, B, T, host, 4);
         break;
       default:
         einval("rw_get_tape: unknown tape id");
@@ -2529,7 +2542,10 @@ static std::vector<TraceRec> trace_records(rw_ctx* x, int dir) {
           const int t = tof(it);
           if (t < 0) continue;
           const unsigned long long* st = &h[(((size_t)y * gx + bx) * steps + it) * 16];
-          const unsigned long long a = crit ? st[14] : st[1], b = st[15];
+          // start: the first operand k-block landed (stamp 8, the MMA issuer; after every
+          // dependency's release by a margin of the load latency, so cross-SM %globaltimer skew of
+          // a tick or two cannot invert an edge), else the dependencies-acquired stamp
+          const unsigned long long a = st[8] ? st[8] : (crit ? st[14] : st[1]), b = st[15];
           if (!a || !b) continue;  // inactive member
           Agg& g = (crit ? rec : inp)[(size_t)lt * T + t];
           g.s = std::min(g.s, a);

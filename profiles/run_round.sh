@@ -7,7 +7,7 @@ what=${*:-"tests bench"}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
 for w in $what; do
   case $w in
-    tests) export RW_PARITY_LOG=gpurun_out/parity.jsonl; timeout -s KILL ${PYTEST_TIMEOUT:-1500} python -m pytest ${PYTEST_FILES:-tests} -m gpu -q -rs -x ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
+    tests) export RW_PARITY_LOG=gpurun_out/parity.jsonl; timeout -s KILL ${PYTEST_TIMEOUT:-1500} python -m pytest ${PYTEST_FILES:-tests} -m gpu -q -rs ${PYTEST_X--x} ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
            echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
     bench) timeout -s KILL 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
            echo "bench rc=$?" >> gpurun_out/bench.err ;;

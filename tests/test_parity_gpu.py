@@ -292,8 +292,9 @@ def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch, schedule, p
                  "worker": r.worker, "start_ns": r.start_ns, "end_ns": r.end_ns} for r in recs]
     L, T = c.layers, c.steps
     assert len(fwd_sink) == 2 * L * T and len(sink) == 2 * L * T
-    assert vt.validate_rows(rows(fwd_sink), L, T, "fwd") is None
-    assert vt.validate_rows(rows(sink), L, T, "bwd") is None
+    # %globaltimer ticks are 32 ns and sampled per SM: allow two ticks of cross-SM skew
+    assert vt.validate_rows(rows(fwd_sink), L, T, "fwd", slack_ns=64) is None
+    assert vt.validate_rows(rows(sink), L, T, "bwd", slack_ns=64) is None
     ids = sorted(r.task_id for r in fwd_sink)
     assert ids == list(range(2 * L * T))  # build_graph(L, T, 1) ids, each once
     # RW_TRACE wrote the same forward schedule (last synced forward) as CSV
@@ -304,4 +305,4 @@ def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch, schedule, p
     with open(path) as f:
         hdr = f.readline().strip()
     assert hdr == "task_layer,task_block,phase,worker,start_ns,end_ns"
-    assert vt.validate(str(path), L, T, "fwd") is None
+    assert vt.validate(str(path), L, T, "fwd", slack_ns=64) is None
