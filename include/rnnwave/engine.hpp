@@ -72,7 +72,7 @@ class TapeSeq {
   const Matrix& operator[](std::size_t l) const {
     if (l >= cache_.size()) throw std::out_of_range("tape: layer index out of range");
     if (!cache_[l]) {
-      const std::uint64_t held = which_ == RW_TAPE_DGW ? h_->bwd_tape : h_->fwd_tape;
+      const std::uint64_t held = (which_ == RW_TAPE_DGW || which_ == RW_TAPE_DGR) ? h_->bwd_tape : h_->fwd_tape;
       if (held != id_)
         throw std::invalid_argument("engine: stale tape, the device no longer holds tape " + std::to_string(id_));
       Matrix m(rows_, cols_);
@@ -132,7 +132,7 @@ struct ForwardTape {
   detail::TapeSeq c_seq;
   detail::TapeSeq gates_seq;
   detail::TapeSeq tanh_c_seq;
-  std::vector<Matrix> zrh_seq;  // GRU only (empty: the device path is LSTM)
+  detail::TapeSeq zrh_seq;      // GRU only (engine.hpp:44)
   std::shared_ptr<detail::DeviceHandle> device;
   std::uint64_t id = 0;
 };
@@ -145,7 +145,7 @@ struct ForwardResult {
 struct BackwardState {
   Matrix dx0;
   detail::TapeSeq dgw_seq;
-  std::vector<Matrix> dgr_seq;  // GRU only
+  detail::TapeSeq dgr_seq;      // GRU only (engine.hpp:57)
   std::vector<Matrix> dh0;
   std::vector<Matrix> dc0;
   std::uint64_t id = 0;
@@ -213,6 +213,8 @@ class Engine {
       for (const Matrix& m : *h0) ph0.push_back(m.data());
     }
     if (c0) {
+      if (cfg_.kind != CellKind::Lstm)
+        throw std::invalid_argument("forward: c0 supplied for a cell kind without cell state");
       if (int(c0->size()) != cfg_.layers)
         throw std::invalid_argument("forward: c0 must supply one matrix per layer");
       for (const Matrix& m : *c0) pc0.push_back(m.data());
@@ -231,11 +233,14 @@ class Engine {
     t.device = dev_;
     t.id = id;
     const int H = cfg_.hidden, L = cfg_.layers;
+    const int G = gate_count(cfg_.kind);
+    const bool lstm = cfg_.kind == CellKind::Lstm, gru = cfg_.kind == CellKind::Gru;
     t.h_seq = detail::TapeSeq(dev_, id, RW_TAPE_H, L, H, cfg_.batch + bt);
-    t.c_seq = detail::TapeSeq(dev_, id, RW_TAPE_C, L, H, cfg_.batch + bt);
+    if (lstm) t.c_seq = detail::TapeSeq(dev_, id, RW_TAPE_C, L, H, cfg_.batch + bt);  // engine.hpp:264
     if (training) {
-      t.gates_seq = detail::TapeSeq(dev_, id, RW_TAPE_GATES, L, 4 * H, bt);
-      t.tanh_c_seq = detail::TapeSeq(dev_, id, RW_TAPE_TANH_C, L, H, bt);
+      t.gates_seq = detail::TapeSeq(dev_, id, RW_TAPE_GATES, L, G * H, bt);
+      if (lstm) t.tanh_c_seq = detail::TapeSeq(dev_, id, RW_TAPE_TANH_C, L, H, bt);
+      if (gru) t.zrh_seq = detail::TapeSeq(dev_, id, RW_TAPE_ZRH, L, H, bt);
     }
     return res;
   }
@@ -255,16 +260,19 @@ class Engine {
     std::vector<float*> pdh, pdc;
     for (int l = 0; l < cfg_.layers; ++l) {
       s.dh0.emplace_back(cfg_.hidden, cfg_.batch);
-      s.dc0.emplace_back(cfg_.hidden, cfg_.batch);
+      if (cfg_.kind == CellKind::Lstm) s.dc0.emplace_back(cfg_.hidden, cfg_.batch);  // engine.hpp:318
     }
     for (int l = 0; l < cfg_.layers; ++l) {
       pdh.push_back(s.dh0[l].data());
-      pdc.push_back(s.dc0[l].data());
+      if (cfg_.kind == CellKind::Lstm) pdc.push_back(s.dc0[l].data());
     }
-    dev_->check(rw_backward_data(dev_->ctx, tape.id, dy.data(), s.dx0.data(), pdh.data(), pdc.data()));
+    dev_->check(rw_backward_data(dev_->ctx, tape.id, dy.data(), s.dx0.data(), pdh.data(),
+                                 pdc.empty() ? nullptr : pdc.data()));
     dev_->bwd_tape = tape.id;
     deposit_trace(1);
-    s.dgw_seq = detail::TapeSeq(dev_, tape.id, RW_TAPE_DGW, cfg_.layers, 4 * cfg_.hidden, bt);
+    const int gh = gate_count(cfg_.kind) * cfg_.hidden;
+    s.dgw_seq = detail::TapeSeq(dev_, tape.id, RW_TAPE_DGW, cfg_.layers, gh, bt);
+    if (cfg_.kind == CellKind::Gru) s.dgr_seq = detail::TapeSeq(dev_, tape.id, RW_TAPE_DGR, cfg_.layers, gh, bt);
     s.id = tape.id;
     return s;
   }
@@ -276,9 +284,10 @@ class Engine {
     Gradients g;
     std::vector<float*> pw, pr, pb;
     for (int l = 0; l < cfg_.layers; ++l) {
-      g.dw.emplace_back(4 * cfg_.hidden, cfg_.input_width(l));
-      g.dr.emplace_back(4 * cfg_.hidden, cfg_.hidden);
-      g.db.emplace_back(std::size_t(4 * cfg_.hidden), 0.0f);
+      const int gh = gate_count(cfg_.kind) * cfg_.hidden;
+      g.dw.emplace_back(gh, cfg_.input_width(l));
+      g.dr.emplace_back(gh, cfg_.hidden);
+      g.db.emplace_back(std::size_t(gh), 0.0f);
     }
     for (int l = 0; l < cfg_.layers; ++l) {
       pw.push_back(g.dw[l].data());

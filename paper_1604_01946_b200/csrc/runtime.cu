@@ -2542,10 +2542,13 @@ static std::vector<TraceRec> trace_records(rw_ctx* x, int dir) {
           const int t = tof(it);
           if (t < 0) continue;
           const unsigned long long* st = &h[(((size_t)y * gx + bx) * steps + it) * 16];
-          // start: the first operand k-block landed (stamp 8, the MMA issuer; after every
-          // dependency's release by a margin of the load latency, so cross-SM %globaltimer skew of
-          // a tick or two cannot invert an edge), else the dependencies-acquired stamp
-          const unsigned long long a = st[8] ? st[8] : (crit ? st[14] : st[1]), b = st[15];
+          // start: for a recurrent step, the moment every input of its accumulation is in the CTA
+          // (the epilogue received the off partial: stamp 10 forward, 13 backward); for an input
+          // GEMM, its first operand k-block landed (stamp 8). Both trail the producers' releases by
+          // a load latency, so %globaltimer skew between SMs (a 32 ns tick or two) cannot invert an
+          // edge; the dependencies-acquired stamps (14 / 1) are the fallback.
+          const unsigned long long sa = crit ? st[dir == 0 ? 10 : 13] : st[8];
+          const unsigned long long a = sa ? sa : (crit ? st[14] : st[1]), b = st[15];
           if (!a || !b) continue;  // inactive member
           Agg& g = (crit ? rec : inp)[(size_t)lt * T + t];
           g.s = std::min(g.s, a);

@@ -6,13 +6,13 @@
 //   -I<repo>/include -I/root/reference/proj/include
 //
 // rnnwave/engine.hpp resolves to the facade (first on the path); verify.hpp / oracle.hpp /
-// scheduler.hpp / gemm.hpp to the reference's. Checks (LSTM: the device path's cell kind):
+// scheduler.hpp to the reference's. Checks:
 //   1. verify::check_determinism (verify.hpp:435-460), unmodified;
 //   2. verify::check_cross_level(CellKind::Lstm, ...) (verify.hpp:105-127), unmodified -- every
 //      opt_level runs the same device kernels, so this is the device's run-to-run identity;
-//   3. the LSTM draws of verify::check_oracle_agreement (verify.hpp:140-201): same SplitMix64
-//      draw sequence, same oracle::widen / forward / gradient, same thresholds (|y| <= 1e-4,
-//      |dW|, |dR|, |db| <= 1e-3); GRU / RNN draws are skipped (not on the device path);
+//   3. verify::check_oracle_agreement (verify.hpp:140-201), unmodified: 20 random draws over all
+//      four cell kinds (LSTM, GRU, RNN-tanh, RNN-relu) against the fp64 oracle, |y| <= 1e-4,
+//      |dW|, |dR|, |db| <= 1e-3 (the LSTM-draw restatement below stays as a second seed);
 //   4. set_trace_sink + sched::validate_trace (scheduler.hpp:371-404) on build_graph(L, T, 1)
 //      (forward) and reverse_graph (backward) over the device's trace.
 #include "rnnwave/engine.hpp"
@@ -128,7 +128,8 @@ int main(int argc, char** argv) {
   base.batch_steps = 2;
   base.seed = seed;
   fails += report(verify::check_cross_level(CellKind::Lstm, base, {1, 3}));
-  fails += report(lstm_oracle_agreement(20, seed));
+  fails += report(verify::check_oracle_agreement(20, seed));
+  fails += report(lstm_oracle_agreement(20, seed + 1));
   fails += report(device_trace(3, 6));
   std::printf("%s\n", fails ? "FAILED" : "ALL PASS");
   return fails ? 1 : 0;
