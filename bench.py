@@ -520,6 +520,94 @@ def cpu_baseline(key: str = "B") -> dict | None:
                                 "why": "min(nproc, 2L), the reference CLI default (rnnwave.cpp:30-37)"}}
 
 
+# ----------------------------------------------------------------------------- GPU ladder
+LADDER_LABELS = ["Naive", "Grouped GEMMs", "Streamed GEMMs", "Fused point-wise", "Pre-transpose",
+                 "Batching inputs", "Overlapping layers"]  # bench.hpp:30-32
+
+
+def run_ladder(args) -> None:
+    """The reference's run_ladder (bench.hpp:176-224) on the GPU: the seven rungs of the paper's
+    Table 1 as device variants (runtime.cu run_ladder_forward: O0-O4 on a stepwise context, O5 the
+    layer-sequential schedule, O6 the automatic wavefront), forward pass, median over reps, each
+    rung checked against O0 (equiv_ok: y within the precision's tolerance -- the reference's check
+    is bitwise, a tensor-core build's is a tolerance) and written in write_ladder_csv's schema
+    (bench.hpp:226-242)."""
+    import numpy as np
+    import torch
+    from paper_1604_01946_b200 import Engine, LadderConfig, init_params, make_dy, make_input
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity import TOL, errors
+    torch.cuda.set_device(0)
+    c = dict(CONFIGS[args.config])
+    cfg = LadderConfig(**c, seed=42, opt_level=6, batch_steps=2, workers=1)
+    params = init_params(cfg)
+    x, dy = make_input(cfg), make_dy(cfg)
+    engines = {"stepwise": Engine(cfg, precision=args.precision, schedule="stepwise"),
+               "layerseq": Engine(cfg, precision=args.precision, schedule="layerseq"),
+               "auto": Engine(cfg, precision=args.precision, schedule="auto")}
+    for e in engines.values():
+        e.set_params(params)
+        e.upload_inputs(x, dy)
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+
+    def run(level):
+        if level <= 4:
+            engines["stepwise"].ladder_pass(level, sh)
+            return engines["stepwise"]
+        e = engines["layerseq" if level == 5 else "auto"]
+        e.run_pass(0, sh)
+        return e
+
+    cells = c["layers"] * c["steps"]
+    flop_cell = 2 * 4 * c["hidden"] * (c["input"] + c["hidden"]) * c["batch"]
+    rows, y0, naive = [], None, None
+    with torch.cuda.stream(stream):
+        for level in range(7):
+            for _ in range(max(args.warmup, 2)):
+                e = run(level)
+            e.sync()
+            y = np.zeros((c["hidden"], c["batch"] * c["steps"]), np.float32, order="F")
+            e.read_outputs(y=y)
+            if y0 is None:
+                y0 = y
+            nw, sm = errors(y, y0)
+            tol = TOL[args.precision]
+            equiv = nw <= tol[0] and sm <= tol[1]
+            reps = max(3, min(args.steps, 20 if level <= 2 else 50))
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                run(level)
+                b.record(stream)
+                b.synchronize()
+                ts.append(a.elapsed_time(b) * 1e3)
+            med = statistics.median(ts)
+            us_cell = round(med / cells, 3)
+            if naive is None:
+                naive = us_cell
+            rows.append({"opt_level": level, "label": LADDER_LABELS[level], "us_per_cell": us_cell,
+                         "speedup_vs_naive": round(naive / us_cell, 3) if us_cell else 0.0,
+                         "gflops": flop_cell / (us_cell * 1000.0), "equiv_ok": bool(equiv),
+                         "y_normwise_vs_O0": nw, "schedule": engines["auto"].describe()["fwd_schedule"]
+                         if level == 6 else ("layerseq" if level == 5 else "stepwise")})
+    out = args.ladder_csv or os.path.join(ROOT, "gpurun_out", f"ladder_{args.config}_{args.precision}.csv")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as f:
+        f.write(f"# rnnwave run-ladder (B200, rnnwave_sm100): cell=lstm layers={c['layers']} hidden={c['hidden']} "
+                f"input={c['input']} batch={c['batch']} steps={c['steps']} batch_steps=2 workers=1 seed=42 "
+                f"pass=fwd reps=median precision={args.precision}\n")
+        f.write("# us_per_cell is the median over reps; gflops counts GEMM multiply-adds only "
+                "(2*G*H*(I+H)*B per cell, pass multiplier fwd=1 bwd=2 both=3)\n")
+        f.write("opt_level,label,us_per_cell,speedup_vs_naive,gflops,equiv_ok\n")
+        for r in rows:
+            f.write(f"{r['opt_level']},{r['label']},{r['us_per_cell']:.3f},{r['speedup_vs_naive']:.3f},"
+                    f"{r['gflops']:.3f},{'true' if r['equiv_ok'] else 'false'}\n")
+    print(json.dumps({"ladder": rows, "csv": out, "config": workload_name(args.config, c),
+                      "precision": args.precision}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -532,13 +620,18 @@ def main():
     ap.add_argument("--single-precision", action="store_true", help="skip the secondary precision")
     ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster", "layerseq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ladder", action="store_true", help="the GPU optimisation ladder (O0-O6) in the "
+                    "reference's run-ladder CSV schema instead of the bench line")
+    ap.add_argument("--ladder-csv", default=None)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="multi-GPU: weak = every rank its own full minibatch (data parallel); strong = "
                          "the configuration's minibatch split across the ranks (e.g. --config E, B = 256)")
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS),
                     help="SURVEY §8(d) config; B (the headline) unless sweeping")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.ladder:
+        run_ladder(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -228,6 +228,14 @@ int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next
 int rw_pp_set_next_w(rw_ctx* ctx, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */
+/* The GPU optimisation ladder (the reference's run_ladder, bench.hpp:30-32, 176-224): one
+ * inference forward pass of rung `level` 0..4 -- 0 naive (per-gate GEMMs on the reference-layout
+ * weights + the nine element-wise ops as nine launches), 1 grouped GEMMs, 2 streamed GEMMs (W.x
+ * on a second stream), 3 fused point-wise, 4 pre-transposed fused step kernels, layers in
+ * sequence. Rungs 5 / 6 are rw_run_pass on contexts with the layer-sequential / automatic
+ * schedule. The context must use the stepwise schedule and LSTM cells. */
+int rw_ladder_pass(rw_ctx* ctx, int level, void* stream);
+
 /* gemm (gemm.hpp:339-347, the reference's ordered fp32 GEMM) on the device: C (M x N) =
  * alpha op(A) op(B) + beta C, host column-major buffers, op(X) = X^T when trans_x; 3xTF32 split
  * operands on the tcgen05 tensor cores (fp32-parity, not bitwise equal to the CPU chain).

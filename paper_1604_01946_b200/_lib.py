@@ -30,7 +30,7 @@ EXPORTS = [
     "rw_nccl_unique_id", "rw_comm_init", "rw_allreduce_grads", "rw_comm_overlap", "rw_phase_times", "rw_describe", "rw_describe_variants",
     "rw_describe_precision", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link", "rw_pp_set_next_w",
-    "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm",
+    "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm", "rw_ladder_pass",
 ]
 
 
@@ -122,6 +122,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_train_step.argtypes = [vp, _F, _F, _F, _F, _PF, _PF, _PF]
     L.rw_train_wait.argtypes = [vp]
     L.rw_trace_enable.argtypes = [vp, C.c_int]
+    L.rw_ladder_pass.argtypes = [vp, C.c_int, vp]
     L.rw_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, _F, C.c_longlong, _F,
                           C.c_longlong, C.c_float, _F, C.c_longlong]
     L.rw_trace_records.argtypes = [vp, C.c_int, C.POINTER(rw_trace_record), C.c_int, C.POINTER(C.c_int)]

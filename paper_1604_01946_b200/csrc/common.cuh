@@ -106,7 +106,9 @@ __host__ __device__ inline long long sw_off(int k, int n, int Bp) {
 }
 
 // Output index mapping of the generic GEMM epilogue.
-enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1, kRowGatePad = 2 };
+// kRowGateRepad: reference gate-major rows g*H + u -> padded gate-major g*Hp + u (the ladder's
+// grouped GEMMs on the reference-layout weights)
+enum RowMode : int { kRowIdentity = 0, kRowGateUnperm = 1, kRowGatePad = 2, kRowGateRepad = 3 };
 enum ColMode : int { kColIdentity = 0, kColBatchUnpad = 1 };
 
 // One (grouped) GEMM problem: D[MxN] = A[MxK] * B[NxK]^T, fp32 out.
@@ -125,6 +127,7 @@ struct GemmDesc {
   float alpha;         // D = alpha * A B^T (fp16x2 weight operands carry 2^kWScaleLog2); 0 means 1
   int* error;          // the context's error word (bounded mbarrier waits, sm100_ptx.cuh)
   int gates;           // kRowGateUnperm: the cell's gate count (0 = 4)
+  int a_m_off;         // row (M) offset inside the A tensor (k_gemm_tc only: the ladder's per-gate GEMMs)
 };
 
 }  // namespace rw

@@ -57,6 +57,7 @@ __device__ __forceinline__ int gemm_out_row(const GemmDesc& g, int m) {
     return u < g.H && (g.gates == 0 || gt < g.gates) ? gt * g.H + u : -1;
   }
   if (g.row_mode == kRowGatePad) return rho_gate(m) * g.Hp + rho_unit(m);
+  if (g.row_mode == kRowGateRepad) return m < g.m_valid ? (m / g.H) * g.Hp + m % g.H : -1;
   return m < g.m_valid ? m : -1;
 }
 __device__ __forceinline__ long long gemm_out_col(const GemmDesc& g, int n) {
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(256, 1)
       uint8_t* st = smem + s * stage_bytes;
       const int k = kb * P::kAtomK;
       for (int p = 0; p < P::kPlanes; ++p) {
-        OperandTile<P, kAMN>::load(st + p * a_bytes, g.a[p], &full[s], m0, kTileM, k + g.a_k_off);
+        OperandTile<P, kAMN>::load(st + p * a_bytes, g.a[p], &full[s], m0 + g.a_m_off, kTileM, k + g.a_k_off);
         OperandTile<P, kBMN>::load(st + P::kPlanes * a_bytes + p * b_bytes, g.b[p], &full[s], n0 + g.b_n_off,
                                    bn, k + g.b_k_off);
       }

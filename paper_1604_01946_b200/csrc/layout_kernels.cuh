@@ -284,4 +284,82 @@ __global__ void k_scale_cols(float* __restrict__ c, long long ldc, int M, int N,
   }
 }
 
+// ---- the GPU optimisation ladder's point-wise stage (cells.hpp:261-279 is
+// the reference's unfused sequence, cells.hpp:227-260 the fused one). Padded gate-major fp32
+// matrices (gate g, unit u at row g*Hp + u), Hp x Bp per gate, column-major.
+enum EwOp : int { kEwAdd = 0, kEwAddBias = 1, kEwSigmoid = 2, kEwTanh = 3, kEwMul = 4 };
+// dst = op(a, b) over rows x cols (leading dimensions lda / ldb / ldd); kEwAddBias: b is a
+// per-row vector; kEwSigmoid / kEwTanh: unary on a. One launch per element-wise op: the
+// "Naive" .. "Streamed GEMMs" rungs run the nine-op LSTM sequence as nine launches (K8).
+__global__ void k_ew(int op, float* __restrict__ dst, int ldd, const float* __restrict__ a, int lda,
+                     const float* __restrict__ b, int ldb, int rows, int cols) {
+  const long long total = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / rows), r = (int)(e - (long long)c * rows);
+    const float x = a[(long long)c * lda + r];
+    float v;
+    switch (op) {
+      case kEwAdd: v = x + b[(long long)c * ldb + r]; break;
+      case kEwAddBias: v = x + b[r]; break;
+      case kEwSigmoid: v = 1.0f / (1.0f + expf(-x)); break;
+      case kEwTanh: v = tanhf(x); break;
+      default: v = x * b[(long long)c * ldb + r]; break;
+    }
+    dst[(long long)c * ldd + r] = v;
+  }
+}
+// Reference-layout gate-major weights (G*H x cols, column-major) -> operand planes with every
+// gate block padded to Hp rows (rows g*Hp + u; TMA tiles of one gate then start 128-byte aligned),
+// same column-major (MN-major A) orientation -- no transpose: the ladder's "not pre-transposed"
+// rungs read these.
+__global__ void k_pad_gates(const float* __restrict__ src, int G, int H, int Hp, int cols, int prec, void* p0,
+                            void* p1, float f16scale) {
+  const long long rows = (long long)G * Hp, total = rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e / rows;
+    const int r = (int)(e - c * rows), g = r / Hp, u = r - g * Hp;
+    const float v = u < H ? src[c * G * H + (long long)g * H + u] : 0.0f;
+    store_planes(prec, p0, p1, e, v, f16scale);
+  }
+}
+// h (Hp x Bp fp32) -> the operand planes of the next step's GEMM (fp16x2: scaled by 2^kHScaleLog2)
+__global__ void k_store_h_operand(const float* __restrict__ h, long long n, int prec, void* p0, void* p1) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    store_planes(prec, p0, p1, e, h[e], pow2f(kHScaleLog2));
+}
+// "Fused point-wise": the whole LSTM cell of cells.hpp:240-258 (same operation order) in one
+// launch: gates from zw + zr + b, c = f c_prev + i c', h = o tanh(c); writes c, h (tapes) and the
+// h operand planes.
+__global__ void k_lstm_cell_fused(const float* __restrict__ zw, const float* __restrict__ zr,
+                                  const float* __restrict__ bias, const float* __restrict__ c_prev,
+                                  float* __restrict__ c_out, float* __restrict__ h_out, int H, int Hp, int B,
+                                  int prec, void* p0, void* p1, long long op_off) {
+  const long long total = (long long)Hp * B;
+  const long long G4 = 4LL * Hp;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / Hp), u = (int)(e - (long long)c * Hp);
+    float hv = 0.0f, cv = 0.0f;
+    if (u < H) {
+      const float* w = zw + c * G4;
+      const float* r = zr + c * G4;
+      const float ai = (w[u] + r[u]) + bias[u];
+      const float af = (w[Hp + u] + r[Hp + u]) + bias[Hp + u];
+      const float ao = (w[2 * Hp + u] + r[2 * Hp + u]) + bias[2 * Hp + u];
+      const float ac = (w[3 * Hp + u] + r[3 * Hp + u]) + bias[3 * Hp + u];
+      const float iv = 1.0f / (1.0f + expf(-ai)), fv = 1.0f / (1.0f + expf(-af));
+      const float ov = 1.0f / (1.0f + expf(-ao)), cb = tanhf(ac);
+      const float t1 = fv * c_prev[e];
+      const float t2 = iv * cb;
+      cv = t1 + t2;
+      hv = ov * tanhf(cv);
+    }
+    c_out[e] = cv;
+    h_out[e] = hv;
+    store_planes(prec, p0, p1, op_off + e, hv, pow2f(kHScaleLog2));
+  }
+}
+
 }  // namespace rw

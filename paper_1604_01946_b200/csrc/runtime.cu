@@ -250,6 +250,22 @@ struct rw_ctx {
   // descriptors
   std::vector<CUtensorMap> maps;  // host copy
   DevBuf maps_dev;
+  int mi_xK[2] = {0, 0};          // map indices of the K-major x / h operands (the ladder's B operands)
+  std::vector<int> mi_hopK;
+  // ---- the GPU optimisation ladder (rw_ladder_pass), built on first use
+  struct Ladder {
+    bool ready = false;
+    std::vector<Operand> wraw, rraw;  // W_l, R_l in the reference layout (MN-major A operand planes)
+    DevBuf maps;                      // [wraw planes, rraw planes, x / h operand copies] per layer
+    DevBuf zw, zr, pre, gates, t1, t2;
+    DevBuf desc;                      // GemmDesc [l][t][kind]: W gate 0..3, R gate 0..3, W grouped, R grouped
+    std::vector<cudaEvent_t> ev;      // per (l, t): the W.x GEMM of the step finished (streamed rungs)
+    cudaStream_t side = nullptr;
+    ~Ladder() {
+      for (auto e : ev) cudaEventDestroy(e);
+      if (side) cudaStreamDestroy(side);
+    }
+  } ladder;
   DevBuf fwd_layers, bwd_layers, gemm_wg, gemm_dx;
   int n_wg = 0;
 
@@ -971,6 +987,8 @@ void build(rw_ctx* x) {
       m_wf[2 * l + p] = add_map(x, make_map(x->wf[l].p(p), prec, Ipl + Hp, G4p, aK, kTileM));
       m_wb[2 * l + p] = add_map(x, make_map(x->wb[l].p(p), prec, (l < L - 1 ? 2 : 1) * G4p, Hp, aK, kTileM));
       m_hopK[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp));
+      if (p == 0) x->mi_hopK.assign(2 * L, 0);
+      x->mi_hopK[2 * l + p] = m_hopK[2 * l + p];
       if (x->pair_f) m_hopK2[l] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp / 2));
       m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
@@ -987,6 +1005,7 @@ void build(rw_ctx* x) {
       m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, gemm_box_rows(x->bn_wg)));
     }
     m_xK[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp));
+    x->mi_xK[p] = m_xK[p];
     if (x->pair_f) m_xK2 = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, Bp / 2));
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
     m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
@@ -1659,6 +1678,191 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   }
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
   }
+}
+
+// ---- GPU optimisation ladder (the reference's run_ladder, bench.hpp:30-32,
+// 176-224): seven forward-pass rungs, each adding one optimisation of the paper's Table 1.
+//   O0 Naive            per step: 4 + 4 per-gate GEMMs (W_g.x_t, R_g.h_{t-1}) on the reference-
+//                       layout weights, then the nine element-wise ops of the unfused cell (K8)
+//                       as nine launches; layers and steps in sequence on one stream
+//   O1 Grouped GEMMs    one GEMM per operand for all gates (M = G H)
+//   O2 Streamed GEMMs   the W.x GEMMs on a second stream, running ahead of the recurrence
+//   O3 Fused point-wise the whole cell in one launch
+//   O4 Pre-transpose    the K7-packed K-major [W | R] and the fused GEMM + cell step kernel
+//                       (k_lstm_fwd), layers in sequence
+//   O5 Batching inputs  the layer-sequential schedule (one W.X GEMM per layer over all steps)
+//   O6 Overlapping layers the wavefront (cluster / persistent / stepwise)
+// O0-O4 run here on a context created with the stepwise schedule; O5 / O6 are rw_run_pass on
+// contexts with the layer-sequential / automatic schedule (bench.py --ladder).
+void ladder_init(rw_ctx* x) {
+  auto& Lr = x->ladder;
+  const int L = x->L, H = x->H, I = x->I, Hp = x->Hp, Bp = x->Bp, T = x->T, G = x->G, aK = x->atomK;
+  const long long G4p = 4LL * Hp;
+  Lr.wraw.resize(L);
+  Lr.rraw.resize(L);
+  std::vector<CUtensorMap> maps;
+  for (int l = 0; l < L; ++l) {
+    const int Il = l == 0 ? I : H;
+    Lr.wraw[l].alloc(x->prec, (size_t)G * Hp * Il);
+    Lr.rraw[l].alloc(x->prec, (size_t)G * Hp * H);
+    for (int p = 0; p < 2; ++p) {
+      const int q = p % x->planes;
+      maps.push_back(make_map(Lr.wraw[l].p(q), x->prec, (long long)G * Hp, Il, aK, aK));  // MN-major A
+      maps.push_back(make_map(Lr.rraw[l].p(q), x->prec, (long long)G * Hp, H, aK, aK));
+    }
+  }
+  // B operands (x_t, h_t column blocks), K-major with boxes of the GEMM's bn rows (the context's own
+  // maps use Bp-row boxes for the recurrent kernels); rows past the tensor are zero-filled and
+  // columns past Bp are computed but not written (n_valid)
+  const size_t nb = maps.size();
+  const int bn = Bp <= 64 ? 64 : 128;
+  const long long colsT = (long long)Bp * T, colsT1 = (long long)Bp * (T + 1);
+  for (int p = 0; p < 2; ++p) maps.push_back(make_map(x->x_op.p(p % x->planes), x->prec, x->Ip, colsT, aK, gemm_box_rows(bn)));
+  for (int l = 0; l < L; ++l)
+    for (int p = 0; p < 2; ++p)
+      maps.push_back(make_map(x->hop[l].p(p % x->planes), x->prec, Hp, colsT1, aK, gemm_box_rows(bn)));
+  Lr.maps.alloc(maps.size() * sizeof(CUtensorMap));
+  RW_CUDA(cudaMemcpy(Lr.maps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  const CUtensorMap* M = static_cast<const CUtensorMap*>(Lr.maps.p);
+  // maps per layer: [W plane 0, R plane 0, W plane 1, R plane 1]
+  auto mW = [&](int l, int p) { return p < x->planes ? M + 4 * l + 2 * p : nullptr; };
+  auto mR = [&](int l, int p) { return p < x->planes ? M + 4 * l + 2 * p + 1 : nullptr; };
+  auto mX = [&](int p) { return p < x->planes ? M + nb + p : nullptr; };
+  auto mH = [&](int l, int p) { return p < x->planes ? M + nb + 2 + 2 * l + p : nullptr; };
+  Lr.zw.alloc((size_t)G4p * Bp * T * 4);
+  Lr.zr.alloc((size_t)G4p * Bp * 4);
+  Lr.pre.alloc((size_t)G4p * Bp * 4);
+  Lr.gates.alloc((size_t)G4p * Bp * 4);
+  Lr.t1.alloc((size_t)Hp * Bp * 4);
+  Lr.t2.alloc((size_t)Hp * Bp * 4);
+  std::vector<GemmDesc> d((size_t)L * T * 10);
+  const bool f16 = x->prec == kF16x2;
+  for (int l = 0; l < L; ++l) {
+    const int Il = l == 0 ? I : H;
+    for (int t = 0; t < T; ++t)
+      for (int k = 0; k < 10; ++k) {
+        GemmDesc& g = d[((size_t)l * T + t) * 10 + k];
+        const bool w = k < 4 || k == 8, grouped = k >= 8;
+        const int gate = grouped ? 0 : (k & 3);
+        for (int p = 0; p < 2; ++p) {
+          g.a[p] = w ? mW(l, p) : mR(l, p);
+          g.b[p] = w ? (l == 0 ? mX(p) : mH(l - 1, p)) : mH(l, p);
+        }
+        g.error = static_cast<int*>(x->errflag.p);
+        g.a_m_off = grouped ? 0 : gate * Hp;
+        g.M = grouped ? G * Hp : round_up(H, kTileM);
+        g.N = Bp;
+        g.K = w ? Il : H;
+        g.b_n_off = w ? (l == 0 ? t * Bp : (t + 1) * Bp) : t * Bp;  // x_t, h_{l-1,t} (block t+1), h_{t-1}
+        g.d = (w ? Lr.zw.f() + (size_t)t * Bp * G4p : Lr.zr.f()) + (grouped ? 0 : (size_t)gate * Hp);
+        g.ldd = G4p;
+        g.row_mode = kRowIdentity;
+        g.col_mode = kColIdentity;
+        g.H = H;
+        g.Hp = Hp;
+        g.B = x->B;
+        g.Bp = Bp;
+        g.m_valid = grouped ? G * Hp : H;
+        g.n_valid = Bp;
+        g.alpha = f16 ? pow2f(-(kWScaleLog2 + (w && l == 0 ? kXScaleLog2 : kHScaleLog2))) : 1.0f;
+      }
+  }
+  Lr.desc.alloc(d.size() * sizeof(GemmDesc));
+  RW_CUDA(cudaMemcpy(Lr.desc.p, d.data(), d.size() * sizeof(GemmDesc), cudaMemcpyHostToDevice));
+  Lr.ev.resize((size_t)L * T);
+  for (auto& e : Lr.ev) RW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  RW_CUDA(cudaStreamCreateWithFlags(&Lr.side, cudaStreamNonBlocking));
+  Lr.ready = true;
+}
+
+template <class P>
+void run_ladder_forward(rw_ctx* x, int level, cudaStream_t s) {
+  if (!x->ladder.ready) ladder_init(x);
+  auto& Lr = x->ladder;
+  const int L = x->L, H = x->H, I = x->I, Hp = x->Hp, Bp = x->Bp, T = x->T, G = x->G;
+  const long long G4p = 4LL * Hp;
+  const int bn = Bp <= 64 ? 64 : 128;
+  const GemmDesc* D = static_cast<const GemmDesc*>(Lr.desc.p);
+  auto gemm = [&](int l, int t, int k, int count, cudaStream_t st) {
+    const GemmDesc* g = D + ((size_t)l * T + t) * 10 + k;
+    const int M = k >= 8 ? G * Hp : round_up(H, kTileM);
+    launch_gemm<P, true, false>(g, count, M, Bp, bn, gemm_stages(x->planes, bn), st);
+  };
+  // reference-layout operand planes of W, R (the "not pre-transposed" rungs read these)
+  if (level <= 3) {
+    for (int l = 0; l < L; ++l) {
+      const int Il = l == 0 ? I : H;
+      ++g_launches;
+      k_pad_gates<<<grid_for((long long)G * Hp * Il), 256, 0, s>>>(x->W[l].f(), G, H, Hp, Il, x->prec, Lr.wraw[l].p(0),
+                                                                    Lr.wraw[l].p(1), pow2f(kWScaleLog2));
+      ++g_launches;
+      k_pad_gates<<<grid_for((long long)G * Hp * H), 256, 0, s>>>(x->R[l].f(), G, H, Hp, H, x->prec, Lr.rraw[l].p(0),
+                                                                   Lr.rraw[l].p(1), pow2f(kWScaleLog2));
+    }
+  }
+  const int ew = grid_for((long long)G4p * Bp);
+  for (int l = 0; l < L; ++l) {
+    if (level == 4) {  // pre-transposed fused step kernels, layer after layer
+      RecParams rp = rec_params(x, true);
+      rp.persistent = 0;
+      rp.resident = 0;
+      rp.n_steps = 1;
+      rp.layer_base = l;
+      for (int t = 0; t < T; ++t) {
+        rp.t_first = t;
+        launch_rec<P>(KernelSet<P>::fwd(), x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, s,
+                      x->pair_f ? 2 : 0);
+      }
+      continue;
+    }
+    if (level >= 2) {  // streamed: every step's W.x on the side stream, ahead of the recurrence
+      RW_CUDA(cudaEventRecord(Lr.ev[(size_t)l * T], s));
+      RW_CUDA(cudaStreamWaitEvent(Lr.side, Lr.ev[(size_t)l * T], 0));  // layer l - 1 finished
+      for (int t = 0; t < T; ++t) {
+        gemm(l, t, 8, 1, Lr.side);
+        RW_CUDA(cudaEventRecord(Lr.ev[(size_t)l * T + t], Lr.side));
+      }
+    }
+    for (int t = 0; t < T; ++t) {
+      if (level == 0) {
+        for (int g = 0; g < G; ++g) gemm(l, t, g, 1, s);
+        for (int g = 0; g < G; ++g) gemm(l, t, 4 + g, 1, s);
+      } else {
+        if (level == 1) gemm(l, t, 8, 1, s);
+        gemm(l, t, 9, 1, s);
+        if (level >= 2) RW_CUDA(cudaStreamWaitEvent(s, Lr.ev[(size_t)l * T + t], 0));
+      }
+      const float* zwt = Lr.zw.f() + (size_t)t * Bp * G4p;
+      float* cprev = x->c[l].f() + (size_t)t * Bp * Hp;
+      float* cnew = cprev + (size_t)Bp * Hp;
+      float* hnew = x->h[l].f() + (size_t)(t + 1) * Bp * Hp;
+      const long long op_off = (long long)(t + 1) * Bp * Hp;
+      if (level == 3) {
+        ++g_launches;
+        k_lstm_cell_fused<<<grid_for((long long)Hp * Bp), 256, 0, s>>>(zwt, Lr.zr.f(), x->bias[l].f(), cprev, cnew, hnew,
+                                                                        H, Hp, Bp, x->prec, x->hop[l].p(0),
+                                                                        x->hop[l].p(1), op_off);
+        continue;
+      }
+      // the unfused cell: nine element-wise launches (cells.hpp:261-279 order)
+      float* pre = Lr.pre.f();
+      float* gt = Lr.gates.f();
+      g_launches += 10;
+      k_ew<<<ew, 256, 0, s>>>(kEwAdd, pre, (int)G4p, zwt, (int)G4p, Lr.zr.f(), (int)G4p, (int)G4p, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwAddBias, pre, (int)G4p, pre, (int)G4p, x->bias[l].f(), 0, (int)G4p, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwSigmoid, gt, (int)G4p, pre, (int)G4p, nullptr, 0, 3 * Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwTanh, gt + 3 * Hp, (int)G4p, pre + 3 * Hp, (int)G4p, nullptr, 0, Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwMul, Lr.t1.f(), Hp, gt + Hp, (int)G4p, cprev, Hp, Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwMul, Lr.t2.f(), Hp, gt, (int)G4p, gt + 3 * Hp, (int)G4p, Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwAdd, cnew, Hp, Lr.t1.f(), Hp, Lr.t2.f(), Hp, Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwTanh, Lr.t1.f(), Hp, cnew, Hp, nullptr, 0, Hp, Bp);
+      k_ew<<<ew, 256, 0, s>>>(kEwMul, hnew, Hp, gt + 2 * Hp, (int)G4p, Lr.t1.f(), Hp, Hp, Bp);
+      void* p0 = static_cast<uint8_t*>(x->hop[l].p(0)) + (size_t)op_off * x->elem;
+      void* p1 = x->hop[l].p(1) ? static_cast<uint8_t*>(x->hop[l].p(1)) + (size_t)op_off * x->elem : nullptr;
+      k_store_h_operand<<<ew, 256, 0, s>>>(hnew, (long long)Hp * Bp, x->prec, p0, p1);
+    }
+  }
+  RW_CUDA(cudaGetLastError());
 }
 
 template <class P>
@@ -2724,6 +2928,27 @@ int rw_sync(rw_ctx* x) {
     RW_CUDA(cudaGetLastError());
     check_error_flag(x);
     dump_trace(x);
+  });
+}
+
+// One forward pass (inference) of ladder rung `level` (0-4; run_ladder_forward); the context
+// must use the stepwise schedule for LSTM cells. Inputs: rw_upload_inputs; output y as for
+// rw_run_pass (rw_read_outputs).
+int rw_ladder_pass(rw_ctx* x, int level, void* stream) {
+  return guarded(x, [&] {
+    if (level < 0 || level > 4) einval("rw_ladder_pass: level must be 0..4 (5 / 6 are the layerseq / auto schedules)");
+    if (x->kind != kCellLstm) einval("rw_ladder_pass: the ladder runs LSTM cells");
+    if (x->fwd_sched != RW_SCHED_STEPWISE) einval("rw_ladder_pass: create the context with the stepwise schedule");
+    if (x->prec == kTF32x3 && level <= 3) einval("rw_ladder_pass: rungs 0-3 read MN-major operands (bf16 / fp16x2 only)");
+    require_params(x);
+    RW_CUDA(cudaSetDevice(x->dev));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : x->main;
+    if (x->dirty) repack_params(x, s);
+    forward_prologue(x, s, nullptr, nullptr, true);
+    by_prec(x->prec, [&](auto tag) { run_ladder_forward<decltype(tag)>(x, level, s); });
+    x->tape_gen += 1;
+    x->tape_training = false;
+    x->bwd_done = false;
   });
 }
 

@@ -554,6 +554,10 @@ class Engine:
         """The device parameters changed in place: the next pass repacks them (K7)."""
         self._check(self._L.rw_params_updated(self._ctx))
 
+    def ladder_pass(self, level: int, stream: int | None = None) -> None:
+        """One inference forward pass of GPU ladder rung 0..4 (rw_ladder_pass; stepwise context)."""
+        self._check(self._L.rw_ladder_pass(self._ctx, level, C.c_void_p(stream or 0)))
+
     def sync(self) -> None:
         self._check(self._L.rw_sync(self._ctx))
 

@@ -30,8 +30,19 @@ KEYS = [
 ]
 
 
+KEYS += [
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_cycles_active_pct"),
+    ("sm__ops_path_tensor_src_fp16_dst_fp32.avg.pct_of_peak_sustained_elapsed", "tensor_fp16_ops_pct"),
+    ("sm__ops_path_tensor_src_bf16_dst_fp32.avg.pct_of_peak_sustained_elapsed", "tensor_bf16_ops_pct"),
+]
+
+
 def ncu_raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep (read with ncu -i) or an already exported `--page raw --csv` file."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return []
@@ -76,12 +87,13 @@ def main():
     os.makedirs(dst, exist_ok=True)
     summary = {}
     for f in sorted(os.listdir(src)):
-        if f.startswith("prof_") and f.endswith(".ncu-rep"):
+        if f.startswith("prof_") and (f.endswith(".ncu-rep") or f.endswith("_raw.csv")):
             summary[f] = ncu_raw(os.path.join(src, f))
-    lp = os.path.join(src, "launches.csv")
-    if os.path.exists(lp):
-        summary["launch_list"] = [
-            {"kernel": k, "total_us": round(t, 2), "launches": n, "share": round(s, 4)} for k, t, n, s in launches(lp)]
+    for f in sorted(os.listdir(src)):
+        if f.startswith("launches") and f.endswith(".csv"):
+            summary["launch_list_" + f[:-4]] = [
+                {"kernel": k, "total_us": round(t, 2), "launches": n, "share": round(s, 4)}
+                for k, t, n, s in launches(os.path.join(src, f))]
     with open(os.path.join(dst, out_name), "w") as fh:
         json.dump(summary, fh, indent=1)
     for k, v in summary.items():
