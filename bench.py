@@ -525,6 +525,20 @@ LADDER_LABELS = ["Naive", "Grouped GEMMs", "Streamed GEMMs", "Fused point-wise",
                  "Batching inputs", "Overlapping layers"]  # bench.hpp:30-32
 
 
+def write_ladder_csv(f, c: dict, rows: list, reps: int, warmup: int, precision: str) -> None:
+    """The reference's write_ladder_csv schema (bench.hpp:226-242): the same two comment lines
+    (plus the device and precision), the same header and %.3f columns."""
+    f.write(f"# rnnwave run-ladder: cell=lstm layers={c['layers']} hidden={c['hidden']} input={c['input']} "
+            f"batch={c['batch']} steps={c['steps']} batch_steps=2 workers=1 seed=42 pass=fwd reps={reps} "
+            f"warmup={warmup} device=B200 precision={precision}\n")
+    f.write("# us_per_cell is the median over reps; gflops counts GEMM multiply-adds only "
+            "(2*G*H*(I+H)*B per cell, pass multiplier fwd=1 bwd=2 both=3)\n")
+    f.write("opt_level,label,us_per_cell,speedup_vs_naive,gflops,equiv_ok\n")
+    for r in rows:
+        f.write(f"{r['opt_level']},{r['label']},{r['us_per_cell']:.3f},{r['speedup_vs_naive']:.3f},"
+                f"{r['gflops']:.3f},{'true' if r['equiv_ok'] else 'false'}\n")
+
+
 def run_ladder(args) -> None:
     """The reference's run_ladder (bench.hpp:176-224) on the GPU: the seven rungs of the paper's
     Table 1 as device variants (runtime.cu run_ladder_forward: O0-O4 on a stepwise context, O5 the
@@ -574,7 +588,7 @@ def run_ladder(args) -> None:
             nw, sm = errors(y, y0)
             tol = TOL[args.precision]
             equiv = nw <= tol[0] and sm <= tol[1]
-            reps = max(3, min(args.steps, 20 if level <= 2 else 50))
+            reps = max(3, min(args.steps, 20))
             ts = []
             for _ in range(reps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -595,15 +609,8 @@ def run_ladder(args) -> None:
     out = args.ladder_csv or os.path.join(ROOT, "gpurun_out", f"ladder_{args.config}_{args.precision}.csv")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as f:
-        f.write(f"# rnnwave run-ladder (B200, rnnwave_sm100): cell=lstm layers={c['layers']} hidden={c['hidden']} "
-                f"input={c['input']} batch={c['batch']} steps={c['steps']} batch_steps=2 workers=1 seed=42 "
-                f"pass=fwd reps=median precision={args.precision}\n")
-        f.write("# us_per_cell is the median over reps; gflops counts GEMM multiply-adds only "
-                "(2*G*H*(I+H)*B per cell, pass multiplier fwd=1 bwd=2 both=3)\n")
-        f.write("opt_level,label,us_per_cell,speedup_vs_naive,gflops,equiv_ok\n")
-        for r in rows:
-            f.write(f"{r['opt_level']},{r['label']},{r['us_per_cell']:.3f},{r['speedup_vs_naive']:.3f},"
-                    f"{r['gflops']:.3f},{'true' if r['equiv_ok'] else 'false'}\n")
+        write_ladder_csv(f, c, rows, reps=max(3, min(args.steps, 20)), warmup=max(args.warmup, 2),
+                         precision=args.precision)
     print(json.dumps({"ladder": rows, "csv": out, "config": workload_name(args.config, c),
                       "precision": args.precision}), flush=True)
 

@@ -13,6 +13,15 @@
 
 namespace rnnwave {
 
+/// CPU cache-blocking sizes of the reference's tiled GEMM (gemm.hpp:27-31). The device GEMM tiles
+/// for the tensor cores itself, so these select nothing; results are identical for every value,
+/// which is the property the reference promises for its own tiles (gemm.hpp:20-25).
+struct GemmTiles {
+  int mc = 64;
+  int nc = 64;
+  int kc = 64;
+};
+
 inline void gemm(bool trans_a, bool trans_b, ConstSpan a, ConstSpan b, Span c, float alpha, float beta) {
   const int am = trans_a ? a.cols : a.rows;
   const int ak = trans_a ? a.rows : a.cols;
@@ -29,6 +38,12 @@ inline void gemm(bool trans_a, bool trans_b, ConstSpan a, ConstSpan b, Span c, f
                          b.ld > 0 ? b.ld : 1, beta, c.data, c.ld);
   if (st == RW_EINVAL) throw std::invalid_argument(rw_last_error(nullptr));
   if (st != RW_OK) throw std::runtime_error(rw_last_error(nullptr));
+}
+
+/// gemm.hpp:254-337 (the reference's entry point with explicit tiles).
+inline void gemm_tiled(bool trans_a, bool trans_b, ConstSpan a, ConstSpan b, Span c, float alpha, float beta,
+                       const GemmTiles&) {
+  gemm(trans_a, trans_b, a, b, c, alpha, beta);
 }
 
 /// op(A) * B convenience with op(B) = B (gemm.hpp:344-347).

@@ -81,7 +81,8 @@ typedef struct {
   int input;
   int batch;
   int steps;
-  int cell_kind;   /* CellKind: must be 3 (Lstm) -- the north-star path */
+  int cell_kind;   /* CellKind: 0 RnnTanh, 1 RnnRelu, 2 Gru, 3 Lstm (config.hpp:12); GRU / RNN run
+                     the cluster schedule (hidden and batch within its fit) */
   int opt_level;   /* validated 0..6 for API compatibility; selects no alternate path */
   int batch_steps; /* validated (1..steps) like the reference */
   int workers;     /* validated > 0; unused on the device */
@@ -242,6 +243,23 @@ int rw_ladder_pass(rw_ctx* ctx, int level, void* stream);
  * Synchronous. */
 int rw_gemm(int trans_a, int trans_b, int M, int N, int K, float alpha, const float* A, long long lda,
             const float* B, long long ldb, float beta, float* C, long long ldc);
+
+/* ---- the free pointwise stage (cells.hpp:181-333 pointwise_forward, 349-562
+ * pointwise_backward) on the device, synchronous. Host buffers, dense column-major (ld = rows):
+ * zw, zr, gates, dgw, dgr are G*H x B (G = gate count of `kind`), the rest H x B, bias G*H.
+ * `fused` selects the reference's fused / kernel-per-op mode; the reference defines the two
+ * bitwise identical and the device runs one kernel for both. Forward: c_prev / c_out for LSTM
+ * only; gates, tanh_c (LSTM), zr_h (GRU) may be NULL (inference: nothing saved; the RNN kinds
+ * save nothing -- their saved state is h_out). Backward: `gates` is the saved gates (the
+ * post-activation h for the RNN kinds), dgr GRU only (distinct from dgw), dc_carry / dc_prev
+ * LSTM only, db optional (G*H, += row sums of dgw in ascending column order). */
+int rw_pointwise_forward(int kind, int fused, int hidden, int batch, const float* zw, const float* zr,
+                         const float* bias, const float* h_prev, const float* c_prev, float* h_out, float* c_out,
+                         float* gates, float* tanh_c, float* zr_h);
+int rw_pointwise_backward(int kind, int fused, int hidden, int batch, const float* gates, const float* tanh_c,
+                          const float* zr_h, const float* h_prev, const float* c_prev, const float* d_above,
+                          const float* dh_carry, const float* dc_carry, float* dgw, float* dgr, float* dh_local,
+                          float* dc_prev, float* db);
 
 /* ---- schedule trace (Engine::set_trace_sink, engine.hpp:79-80; sched::TraceRecord,
  * scheduler.hpp:180-192). rw_trace_enable(ctx, 1) makes the recurrent kernels record

@@ -220,6 +220,46 @@ class Reference:
                                    _PD, _D, _PD, _PD, C.c_char_p, C.c_int]
         L.rwref_time.argtypes = [C.POINTER(C.c_int), C.c_uint64, C.c_int, C.c_int, C.c_int,
                                  _D, _D, _D, C.c_char_p, C.c_int]
+        L.rwref_pointwise_forward.argtypes = [C.c_int] * 4 + [_F] * 10 + [C.c_char_p, C.c_int]
+        L.rwref_pointwise_backward.argtypes = [C.c_int] * 4 + [_F] * 13 + [C.c_char_p, C.c_int]
+
+    def _call(self, fn, *args):
+        err = C.create_string_buffer(512)
+        if fn(*args, err, 512) != 0:
+            raise ValueError(err.value.decode())
+
+    def pointwise_forward(self, kind, fused, zw, zr, bias, h_prev, c_prev, training=True):
+        """cells.hpp:181 through the unmodified reference; returns dict of outputs."""
+        H, B = h_prev.shape
+        G = gate_count(kind)
+        o = {"h": fmat(H, B)}
+        if kind == 3:
+            o["c"] = fmat(H, B)
+        if training and kind in (2, 3):
+            o["gates"] = fmat(G * H, B)
+        if training and kind == 3:
+            o["tanh_c"] = fmat(H, B)
+        if training and kind == 2:
+            o["zr_h"] = fmat(H, B)
+        self._call(self.lib.rwref_pointwise_forward, kind, int(fused), H, B, _fp(zw), _fp(zr),
+                   _fp(np.ascontiguousarray(bias, np.float32)), _fp(h_prev), _fp(c_prev), _fp(o["h"]),
+                   _fp(o.get("c")), _fp(o.get("gates")), _fp(o.get("tanh_c")), _fp(o.get("zr_h")))
+        return o
+
+    def pointwise_backward(self, kind, fused, gates, tanh_c, zr_h, h_prev, c_prev, d_above, dh_carry,
+                           dc_carry, db=None):
+        """cells.hpp:349 through the unmodified reference; returns dict of outputs (db: in place)."""
+        H, B = d_above.shape
+        G = gate_count(kind)
+        o = {"dgw": fmat(G * H, B), "dh_local": fmat(H, B)}
+        if kind == 2:
+            o["dgr"] = fmat(G * H, B)
+        if kind == 3:
+            o["dc_prev"] = fmat(H, B)
+        self._call(self.lib.rwref_pointwise_backward, kind, int(fused), H, B, _fp(gates), _fp(tanh_c),
+                   _fp(zr_h), _fp(h_prev), _fp(c_prev), _fp(d_above), _fp(dh_carry), _fp(dc_carry),
+                   _fp(o["dgw"]), _fp(o.get("dgr")), _fp(o["dh_local"]), _fp(o.get("dc_prev")), _fp(db))
+        return o
 
     @staticmethod
     def _cfg(cfg, opt_level=6, batch_steps=None, workers=None):

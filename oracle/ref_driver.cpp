@@ -190,4 +190,57 @@ int rwref_time(const int* c, std::uint64_t seed, int pass, int reps, int warmup,
   }
 }
 
+// The reference's free pointwise stage (cells.hpp:181 pointwise_forward, 349
+// pointwise_backward) on dense column-major buffers (ld = rows); null save / optional pointers
+// as in the reference (gates == nullptr: inference). kind: CellKind.
+int rwref_pointwise_forward(int kind, int fused, int hidden, int batch, const float* zw, const float* zr,
+                            const float* bias, const float* h_prev, const float* c_prev, float* h_out,
+                            float* c_out, float* gates, float* tanh_c, float* zr_h, char* err, int errlen) {
+  try {
+    const CellKind k = static_cast<CellKind>(kind);
+    const int G = gate_count(k);
+    auto cs = [](const float* p, int r, int c) { return ConstSpan(Span{const_cast<float*>(p), r, c, r}); };
+    auto ms = [](float* p, int r, int c) { return p ? Span{p, r, c, r} : Span{}; };
+    CellSavedSlices save;
+    const bool rnn = k == CellKind::RnnTanh || k == CellKind::RnnRelu;
+    save.gates = rnn ? ms(h_out, hidden, batch) : ms(gates, G * hidden, batch);
+    save.tanh_c = ms(tanh_c, hidden, batch);
+    save.zr_h = ms(zr_h, hidden, batch);
+    CellWorkspace ws;
+    pointwise_forward(k, fused != 0, cs(zw, G * hidden, batch), cs(zr, G * hidden, batch), bias,
+                      cs(h_prev, hidden, batch), c_prev ? cs(c_prev, hidden, batch) : ConstSpan(),
+                      ms(h_out, hidden, batch), ms(c_out, hidden, batch), gates || rnn ? &save : nullptr, ws);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
+int rwref_pointwise_backward(int kind, int fused, int hidden, int batch, const float* gates, const float* tanh_c,
+                             const float* zr_h, const float* h_prev, const float* c_prev, const float* d_above,
+                             const float* dh_carry, const float* dc_carry, float* dgw, float* dgr, float* dh_local,
+                             float* dc_prev, float* db, char* err, int errlen) {
+  try {
+    const CellKind k = static_cast<CellKind>(kind);
+    const int G = gate_count(k);
+    const bool rnn = k == CellKind::RnnTanh || k == CellKind::RnnRelu;
+    auto cs = [](const float* p, int r, int c) {
+      return p ? ConstSpan(Span{const_cast<float*>(p), r, c, r}) : ConstSpan();
+    };
+    auto ms = [](float* p, int r, int c) { return p ? Span{p, r, c, r} : Span{}; };
+    CellSavedConst saved;
+    saved.gates = cs(gates, rnn ? hidden : G * hidden, batch);
+    saved.tanh_c = cs(tanh_c, hidden, batch);
+    saved.zr_h = cs(zr_h, hidden, batch);
+    CellWorkspace ws;
+    pointwise_backward(k, fused != 0, saved, cs(h_prev, hidden, batch), cs(c_prev, hidden, batch),
+                       cs(d_above, hidden, batch), cs(dh_carry, hidden, batch), cs(dc_carry, hidden, batch),
+                       ms(dgw, G * hidden, batch), dgr ? ms(dgr, G * hidden, batch) : ms(dgw, G * hidden, batch),
+                       ms(dh_local, hidden, batch), ms(dc_prev, hidden, batch), db, ws);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errlen);
+  }
+}
+
 }  // extern "C"

@@ -9,3 +9,4 @@ from .engine import (  # noqa: F401
     splitmix_symmetric,
 )
 from . import param_io  # noqa: F401  (reference parameter files, param_io.hpp)
+from .cells import gemm, pointwise_backward, pointwise_forward  # noqa: F401  (free functions)

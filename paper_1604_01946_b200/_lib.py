@@ -31,6 +31,7 @@ EXPORTS = [
     "rw_describe_precision", "rw_flop_count_cell",
     "rw_test_gemm", "rw_test_gemm_last_ms", "rw_pp_export", "rw_pp_link", "rw_pp_set_next_w",
     "rw_train_step", "rw_train_wait", "rw_trace_enable", "rw_trace_records", "rw_gemm", "rw_ladder_pass",
+    "rw_pointwise_forward", "rw_pointwise_backward",
 ]
 
 
@@ -125,6 +126,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.rw_ladder_pass.argtypes = [vp, C.c_int, vp]
     L.rw_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, _F, C.c_longlong, _F,
                           C.c_longlong, C.c_float, _F, C.c_longlong]
+    L.rw_pointwise_forward.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int] + [_F] * 10
+    L.rw_pointwise_backward.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int] + [_F] * 13
     L.rw_trace_records.argtypes = [vp, C.c_int, C.POINTER(rw_trace_record), C.c_int, C.POINTER(C.c_int)]
     L.rw_test_gemm_last_ms.argtypes = []
     L.rw_test_gemm_last_ms.restype = C.c_float

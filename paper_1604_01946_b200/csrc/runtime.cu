@@ -24,6 +24,7 @@
 #include "gemm_tc.cuh"
 #include "layout_kernels.cuh"
 #include "lstm_step.cuh"
+#include "pointwise.cuh"
 #include "kernel_ptrs.h"
 #include "rec_cluster.cuh"
 #include "sync_kernels.cuh"
@@ -2164,6 +2165,112 @@ void rw_destroy(rw_ctx* ctx) { delete ctx; }
 
 const char* rw_last_error(const rw_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 const char* rw_create_error(void) { return g_create_err.c_str(); }
+
+namespace {
+// host buffer <-> device scratch for the synchronous free functions
+struct HostIo {
+  std::vector<DevBuf> bufs;
+  float* in(const float* h, size_t n) {
+    if (!h) return nullptr;
+    bufs.emplace_back();
+    bufs.back().alloc(std::max<size_t>(n, 1) * 4);
+    RW_CUDA(cudaMemcpy(bufs.back().p, h, n * 4, cudaMemcpyHostToDevice));
+    return bufs.back().f();
+  }
+  float* out(float* h, size_t n) {
+    if (!h) return nullptr;
+    bufs.emplace_back();
+    bufs.back().alloc(std::max<size_t>(n, 1) * 4);
+    return bufs.back().f();
+  }
+};
+void pw_check(int kind, int hidden, int batch) {
+  if (kind < kCellRnnTanh || kind > kCellLstm) einval("cells: unknown cell kind " + std::to_string(kind));
+  if (hidden <= 0 || batch <= 0) einval("cells: hidden and batch must be positive");
+}
+}  // namespace
+
+int rw_pointwise_forward(int kind, int fused, int hidden, int batch, const float* zw, const float* zr,
+                         const float* bias, const float* h_prev, const float* c_prev, float* h_out, float* c_out,
+                         float* gates, float* tanh_c, float* zr_h) {
+  (void)fused;
+  return guarded(nullptr, [&] {
+    pw_check(kind, hidden, batch);
+    const int G = kind == kCellLstm ? 4 : kind == kCellGru ? 3 : 1;
+    const size_t hb = (size_t)hidden * batch, gb = hb * G;
+    if (!zw || !zr || !bias || !h_out) einval("cells: zw, zr, bias and h_out are required");
+    if (kind == kCellLstm && (!c_prev || !c_out)) einval("cells: LSTM needs c_prev and c_out");
+    if (kind != kCellLstm && c_prev) einval("cells: cell state supplied for a cell kind without one");
+    if (kind == kCellGru && !h_prev) einval("cells: GRU needs h_prev");
+    const bool rnn = kind == kCellRnnTanh || kind == kCellRnnRelu;
+    HostIo io;
+    float* dzw = io.in(zw, gb);
+    float* dzr = io.in(zr, gb);
+    float* db = io.in(bias, (size_t)G * hidden);
+    float* dhp = kind == kCellGru ? io.in(h_prev, hb) : nullptr;
+    float* dcp = kind == kCellLstm ? io.in(c_prev, hb) : nullptr;
+    float* dh = io.out(h_out, hb);
+    float* dc = kind == kCellLstm ? io.out(c_out, hb) : nullptr;
+    float* dg = rnn ? nullptr : io.out(gates, gb);
+    float* dtc = kind == kCellLstm ? io.out(tanh_c, hb) : nullptr;
+    float* dzh = kind == kCellGru ? io.out(zr_h, hb) : nullptr;
+    ++g_launches;
+    k_pointwise_fwd<<<grid_for((long long)hb), 256>>>(kind, hidden, batch, dzw, dzr, db, dhp, dcp, dh, dc, dg, dtc, dzh);
+    RW_CUDA(cudaGetLastError());
+    RW_CUDA(cudaDeviceSynchronize());
+    RW_CUDA(cudaMemcpy(h_out, dh, hb * 4, cudaMemcpyDeviceToHost));
+    if (dc) RW_CUDA(cudaMemcpy(c_out, dc, hb * 4, cudaMemcpyDeviceToHost));
+    if (dg) RW_CUDA(cudaMemcpy(gates, dg, gb * 4, cudaMemcpyDeviceToHost));
+    if (dtc) RW_CUDA(cudaMemcpy(tanh_c, dtc, hb * 4, cudaMemcpyDeviceToHost));
+    if (dzh) RW_CUDA(cudaMemcpy(zr_h, dzh, hb * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rw_pointwise_backward(int kind, int fused, int hidden, int batch, const float* gates, const float* tanh_c,
+                          const float* zr_h, const float* h_prev, const float* c_prev, const float* d_above,
+                          const float* dh_carry, const float* dc_carry, float* dgw, float* dgr, float* dh_local,
+                          float* dc_prev, float* db) {
+  (void)fused;
+  return guarded(nullptr, [&] {
+    pw_check(kind, hidden, batch);
+    const int G = kind == kCellLstm ? 4 : kind == kCellGru ? 3 : 1;
+    const size_t hb = (size_t)hidden * batch, gb = hb * G;
+    if (!gates) einval("cells: backward requires saved state from a training forward");
+    if (!d_above || !dh_carry || !dgw || !dh_local) einval("cells: d_above, dh_carry, dgw and dh_local are required");
+    if (kind == kCellLstm && (!tanh_c || !c_prev || !dc_carry || !dc_prev))
+      einval("cells: LSTM backward needs tanh_c, c_prev, dc_carry and dc_prev");
+    if (kind == kCellGru && (!zr_h || !h_prev || !dgr)) einval("cells: GRU backward needs zr_h, h_prev and dgr");
+    if (kind == kCellGru && dgr == dgw) einval("cells: GRU needs distinct dgw and dgr blocks");
+    HostIo io;
+    float* dgs = io.in(gates, kind == kCellLstm || kind == kCellGru ? gb : hb);
+    float* dtc = kind == kCellLstm ? io.in(tanh_c, hb) : nullptr;
+    float* dzh = kind == kCellGru ? io.in(zr_h, hb) : nullptr;
+    float* dhp = kind == kCellGru ? io.in(h_prev, hb) : nullptr;
+    float* dcp = kind == kCellLstm ? io.in(c_prev, hb) : nullptr;
+    float* dda = io.in(d_above, hb);
+    float* dhc = io.in(dh_carry, hb);
+    float* dcc = kind == kCellLstm ? io.in(dc_carry, hb) : nullptr;
+    float* ddgw = io.out(dgw, gb);
+    float* ddgr = kind == kCellGru ? io.out(dgr, gb) : nullptr;
+    float* dhl = io.out(dh_local, hb);
+    float* ddcp = kind == kCellLstm ? io.out(dc_prev, hb) : nullptr;
+    float* ddb = db ? io.in(db, (size_t)G * hidden) : nullptr;
+    ++g_launches;
+    k_pointwise_bwd<<<grid_for((long long)hb), 256>>>(kind, hidden, batch, dgs, dtc, dzh, dhp, dcp, dda, dhc, dcc, ddgw,
+                                                      ddgr, dhl, ddcp);
+    if (ddb) {
+      ++g_launches;
+      k_row_sums_add<<<ceil_div(G * hidden, 256), 256>>>(ddgw, G * hidden, batch, ddb);
+    }
+    RW_CUDA(cudaGetLastError());
+    RW_CUDA(cudaDeviceSynchronize());
+    RW_CUDA(cudaMemcpy(dgw, ddgw, gb * 4, cudaMemcpyDeviceToHost));
+    if (ddgr) RW_CUDA(cudaMemcpy(dgr, ddgr, gb * 4, cudaMemcpyDeviceToHost));
+    RW_CUDA(cudaMemcpy(dh_local, dhl, hb * 4, cudaMemcpyDeviceToHost));
+    if (ddcp) RW_CUDA(cudaMemcpy(dc_prev, ddcp, hb * 4, cudaMemcpyDeviceToHost));
+    if (ddb) RW_CUDA(cudaMemcpy(db, ddb, (size_t)G * hidden * 4, cudaMemcpyDeviceToHost));
+  });
+}
 
 int64_t rw_flop_count_cell(int hidden, int input, int batch) {
   return 2LL * 4 * hidden * ((int64_t)input + hidden) * batch;
