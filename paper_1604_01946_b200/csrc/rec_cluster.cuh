@@ -746,23 +746,32 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const int u = tile * kUnitsPerFwdTile + j;
       const long long Hp = p.Hp, G4 = 4 * Hp;
       const int own0 = m * nco;
+      // owned columns per thread: cl = cg + 8k, k < kK (nco = 16 kCC, so no bounds checks). All
+      // addressing is hoisted out of the step loop: per step only the block pointers advance
+      // (profiles/r02: the per-element 64-bit index math was ~45 % of the cell phase's
+      // instructions)
+      constexpr int kK = 2 * kCC;
       const float bi = Le.bias[u], bf = Le.bias[Hp + u], bo = Le.bias[2 * Hp + u], bc = Le.bias[3 * Hp + u];
-      // LSTM: c_{t-1} of owned columns cl = cg + 8k (c tape block 0 = c0); GRU: h_{t-1} (h0)
-      float creg[kClMaxN / 8];
+      // LSTM: c_{t-1} of owned columns (c tape block 0 = c0); GRU: h_{t-1} (h0)
+      float creg[kK];
 #pragma unroll
-      for (int k = 0; k < kClMaxN / 8; ++k) {
-        const int cl = cg + 8 * k;
+      for (int k = 0; k < kK; ++k) {
         const float* st = kKind == kCellGru ? Le.h : Le.c;
-        creg[k] = (cl < nco && kKind != kCellRnnTanh) ? st[(long long)(own0 + cl) * Hp + u] : 0.0f;
+        creg[k] = kKind != kCellRnnTanh ? st[(long long)(own0 + cg + 8 * k) * Hp + u] : 0.0f;
       }
-      const float* sum = reinterpret_cast<const float*>(S.b);
-      // h_t staging after the gate sums, in the B ring: idle between this step's MMA and the
-      // next step's loads, which wait for this CTA's own publish
-      const uint32_t hstg = smem_u32(S.b + (size_t)N * kTileM * 4);
-      // opt-in (RW_CL_DEBUG bit 16): measured at B forward 0.596 ms staged vs 0.589 scattered
-      // (bf16), cell phase 5.3 vs 3.3 us (fp16x2, profiles/r02)
-      const bool staged = (p.debug & 16) != 0 &&
-                          (size_t)p.stages * BR * kRowBytes >= (size_t)N * kTileM * 4 + (size_t)P::kPlanes * nco * 64;
+      const float* sum = reinterpret_cast<const float*>(S.b) + cg * kTileM + j;
+      // operand image of h_t (block t+1): column own0 + cg + 8k sits 8k rows of 128 B after column
+      // own0 + cg with the same 16-B chunk swizzle (it depends on the row mod 8 only); the fp16x2
+      // lo plane is N rows further
+      const long long blk_bytes = (long long)p.Hp * BR * 2;
+      uint8_t* hsw_t = Le.hsw + blk_bytes + sw_off(u, own0 + cg, BR);
+      const int lo_off = N * 128;
+      // tapes: element (col, u) at col * Hp + u (gates: col * 4Hp + u); col_new = (t + 1) N + own0 + cg + 8k
+      const long long kstride = 8 * Hp;
+      long long i_new = (long long)(N + own0 + cg) * Hp + u, i_prev = (long long)(own0 + cg) * Hp + u;
+      long long i_gate = (long long)(own0 + cg) * G4 + u;
+      const long long step_h = (long long)N * Hp, step_g = (long long)N * G4;
+      const bool tapes = !(p.debug & 1);
       uint32_t rxc = 0;
       if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
       for (int t = 0; t < p.T; ++t) {
@@ -778,34 +787,29 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           cl_rx_next(S, m, kc, nco);
         }
         // cell phase, operand store first (the critical output)
-        float hv[kClMaxN / 8], cv[kClMaxN / 8], iv[kClMaxN / 8], fv[kClMaxN / 8], ov[kClMaxN / 8],
-            cb[kClMaxN / 8], tcv[kClMaxN / 8];
-        const long long colp = (long long)t * N + own0;  // block t (c_{t-1}), owned base
-        uint8_t* hblk = Le.hsw + (size_t)(t + 1) * p.Hp * BR * 2;  // h_t: block t+1
+        float hv[kK], iv[kK], fv[kK], ov[kK], cb[kK], tcv[kK];
 #pragma unroll
-        for (int k = 0; k < kClMaxN / 8; ++k) {
-          const int cl = cg + 8 * k;
-          if (cl >= nco) break;
+        for (int k = 0; k < kK; ++k) {
+          const float* sk = sum + k * 8 * kTileM;
           if constexpr (kKind == kCellLstm) {
-            const float ai = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
-            const float af = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
-            const float ao = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j) + bo;
-            const float ac = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j) + bc;
+            const float ai = lds_f32(sk + 0 * 32) + bi;
+            const float af = lds_f32(sk + 1 * 32) + bf;
+            const float ao = lds_f32(sk + 2 * 32) + bo;
+            const float ac = lds_f32(sk + 3 * 32) + bc;
             iv[k] = act_sigmoid<P>(ai);
             fv[k] = act_sigmoid<P>(af);
             ov[k] = act_sigmoid<P>(ao);
             cb[k] = act_tanh<P>(ac);
             const float t1 = fv[k] * creg[k];
             const float t2 = iv[k] * cb[k];
-            cv[k] = t1 + t2;
-            tcv[k] = act_tanh<P>(cv[k]);
+            creg[k] = t1 + t2;  // c_t
+            tcv[k] = act_tanh<P>(creg[k]);
             hv[k] = ov[k] * tcv[k];
-            creg[k] = cv[k];
           } else if constexpr (kKind == kCellGru) {  // cells.hpp:294-313 operation order
-            const float ar = lds_f32(sum + (size_t)cl * kTileM + 0 * 32 + j) + bi;
-            const float au = lds_f32(sum + (size_t)cl * kTileM + 1 * 32 + j) + bf;
-            const float zwn = lds_f32(sum + (size_t)cl * kTileM + 2 * 32 + j);
-            const float zrn = lds_f32(sum + (size_t)cl * kTileM + 3 * 32 + j);
+            const float ar = lds_f32(sk + 0 * 32) + bi;
+            const float au = lds_f32(sk + 1 * 32) + bf;
+            const float zwn = lds_f32(sk + 2 * 32);
+            const float zrn = lds_f32(sk + 3 * 32);
             iv[k] = act_sigmoid<P>(ar);  // r
             fv[k] = act_sigmoid<P>(au);  // u
             const float t1 = zwn + bo;   // W_n x + b_n
@@ -819,34 +823,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             cb[k] = zrn;  // the zrh tape (R_n h_{t-1}, the backward's reset-gate input)
             creg[k] = hv[k];
           } else {  // RNN (cells.hpp:200-212)
-            const float a = lds_f32(sum + (size_t)cl * kTileM + j) + bi;
+            const float a = lds_f32(sk) + bi;
             hv[k] = p.kind == kCellRnnRelu ? (a > 0.0f ? a : 0.0f) : act_tanh<P>(a);
           }
           if constexpr (P::kPlanes == 2) {  // hi row n, lo row N + n of the k-block (scaled, common.cuh)
             __half hh, hl;
             f16x2_split(hv[k] * pow2f(kHScaleLog2), hh, hl);
-            if (staged) {  // [plane][cl][32 units]
-              asm volatile("st.shared.b16 [%0], %1;" ::"r"(hstg + (cl * 32 + j) * 2), "h"(__half_as_ushort(hh)));
-              asm volatile("st.shared.b16 [%0], %1;" ::"r"(hstg + nco * 64 + (cl * 32 + j) * 2), "h"(__half_as_ushort(hl)));
-            } else {
-              *reinterpret_cast<__half*>(hblk + sw_off(u, own0 + cl, BR)) = hh;
-              if (!(p.debug & 512))  // timing experiment (results invalid): hi plane only
-                *reinterpret_cast<__half*>(hblk + sw_off(u, N + own0 + cl, BR)) = hl;
-            }
-          } else if (staged) {
-            sts_bf16(hstg + (cl * 32 + j) * 2, hv[k]);
+            *reinterpret_cast<__half*>(hsw_t + k * 1024) = hh;
+            *reinterpret_cast<__half*>(hsw_t + k * 1024 + lo_off) = hl;
           } else {
-            *reinterpret_cast<__nv_bfloat16*>(hblk + sw_off(u, own0 + cl, N)) = __float2bfloat16_rn(hv[k]);
-          }
-        }
-        if (staged) {
-          // the CTA's 32 units x nco columns (x planes) as 16-byte chunks of the swizzled operand
-          // image: nco * 4 coalesced vector stores per plane instead of 32 * nco scattered 2-byte ones
-          named_bar_sync(1, kEpiThreads);
-          for (int i = et; i < P::kPlanes * nco * 4; i += kEpiThreads) {
-            const int pl = i >= nco * 4 ? 1 : 0, ii = i - pl * nco * 4;
-            const uint4 v = lds_v4(hstg + pl * nco * 64 + ii * 16);
-            *reinterpret_cast<uint4*>(hblk + sw_off(tile * kUnitsPerFwdTile + (ii & 3) * 8, pl * N + own0 + (ii >> 2), BR)) = v;
+            *reinterpret_cast<__nv_bfloat16*>(hsw_t + k * 1024) = __float2bfloat16_rn(hv[k]);
           }
         }
         if (et == 0) cl_trace(p, t, 3);
@@ -859,30 +845,33 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           red_relaxed_s(consumed, 1, sys);       // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
         }
-        // tapes (read only after the pass; the plain bf16 h feeds the weight-gradient GEMMs)
+        // tapes (read only after the pass; the plain h feeds the weight-gradient GEMMs)
+        if (tapes) {
 #pragma unroll
-        for (int k = 0; k < kClMaxN / 8; ++k) {
-          if (p.debug & 1) break;
-          const int cl = cg + 8 * k;
-          if (cl >= nco) break;
-          const long long col_prev = colp + cl, col_new = col_prev + N;
-          if constexpr (kKind == kCellLstm) Le.c[col_new * Hp + u] = cv[k];
-          Le.h[col_new * Hp + u] = hv[k];
-          store_operand<P>(Le.hop, col_new * Hp + u, P::kPlanes == 2 ? hv[k] * pow2f(kHScaleLog2) : hv[k]);
-          if (Le.gates && kKind != kCellRnnTanh) {
-            float* gp = Le.gates + col_prev * G4 + u;
-            gp[0] = iv[k];
-            gp[Hp] = fv[k];
-            gp[2 * Hp] = ov[k];
-            if constexpr (kKind == kCellLstm) {
-              gp[3 * Hp] = cb[k];
-              Le.tanhc[col_prev * Hp + u] = tcv[k];
-            } else {
-              Le.zrh[col_prev * Hp + u] = cb[k];
+          for (int k = 0; k < kK; ++k) {
+            const long long in = i_new + k * kstride, ip = i_prev + k * kstride;
+            if constexpr (kKind == kCellLstm) Le.c[in] = creg[k];
+            Le.h[in] = hv[k];
+            store_operand<P>(Le.hop, in, P::kPlanes == 2 ? hv[k] * pow2f(kHScaleLog2) : hv[k]);
+            if (Le.gates && kKind != kCellRnnTanh) {
+              float* gp = Le.gates + i_gate + k * 8 * G4;
+              gp[0] = iv[k];
+              gp[Hp] = fv[k];
+              gp[2 * Hp] = ov[k];
+              if constexpr (kKind == kCellLstm) {
+                gp[3 * Hp] = cb[k];
+                Le.tanhc[ip] = tcv[k];
+              } else {
+                Le.zrh[ip] = cb[k];
+              }
             }
           }
         }
         if (et == 0) cl_trace(p, t, 6);
+        hsw_t += blk_bytes;
+        i_new += step_h;
+        i_prev += step_h;
+        i_gate += step_g;
       }
     }
   }
