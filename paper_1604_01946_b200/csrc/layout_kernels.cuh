@@ -102,6 +102,139 @@ __global__ void k_pack_w0t(const float* __restrict__ W0, int H, int I, int Hp, i
   }
 }
 
+// ---- the whole K7 repack of a context in ONE launch (runtime.cu repack_params): a table of jobs
+// (every layer's forward [W|R] image, backward [W_{l+1}^T | R_l^T] image and padded bias, plus the
+// dx0 operand W_0^T), each cut into tiles of 32 destination rows x 128 K; block b finds its job by
+// the jobs' first-tile indices. Per tile the source is read once in 128-byte runs and the
+// destination planes are written 4 elements (8-16 bytes) per thread and plane.
+//   kRepackT ("transpose", the forward image): dest row rho (gate g, unit u), K = [W cols | R
+//     cols]; the source columns hold 32 consecutive units of one gate contiguously, the dest rows
+//     are K-contiguous -> through a 64 x 33 shared tile.
+//   kRepackC ("copy", backward image and W_0^T): dest row = source column (unit u / input i),
+//     K = rho order of one or two 4Hp halves; 4 consecutive rho are 4 consecutive units of one
+//     gate, i.e. 4 consecutive source elements of the same column -> direct float4 reads.
+//   kRepackB: the padded bias (4Hp fp32).
+enum RepackKind : int { kRepackT = 0, kRepackC = 1, kRepackB = 2 };
+constexpr int kRepackTileK = 128;
+struct RepackJob {
+  int kind, tile0, tiles_k;  // first tile of the job, tiles along K (kRepackB: 1024 elements / tile)
+  int rows, K;               // destination rows and K (elements)
+  int src_rows, k_split;     // valid source columns (kRepackC rows: H or I) / T: first R column (Ipl)
+  int src_k0;                // T: valid W columns (I or H); C: 4Hp, the width of one K half
+  const float* s0;           // T: W; C: first K half (W_{l+1} or W_0; null -> second half only); B: bias
+  const float* s1;           // T: R; C: second half (R_l)
+  void* p0;
+  void* p1;
+};
+
+__device__ __forceinline__ void store4_planes(int prec, void* p0, void* p1, long long idx, const float v[4],
+                                              float f16scale) {
+  if (prec == kBF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&a);
+    w.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p0) + idx) = w;
+  } else if (prec == kF16x2) {
+    __half hi[4], lo[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) f16x2_split(v[c] * f16scale, hi[c], lo[c]);
+    *reinterpret_cast<uint2*>(static_cast<__half*>(p0) + idx) = *reinterpret_cast<uint2*>(hi);
+    *reinterpret_cast<uint2*>(static_cast<__half*>(p1) + idx) = *reinterpret_cast<uint2*>(lo);
+  } else {
+    float4 hi, lo;
+    float* h = &hi.x;
+    float* l = &lo.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t b;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v[c]));
+      h[c] = __uint_as_float(b);
+      l[c] = v[c] - h[c];
+    }
+    *reinterpret_cast<float4*>(static_cast<float*>(p0) + idx) = hi;
+    *reinterpret_cast<float4*>(static_cast<float*>(p1) + idx) = lo;
+  }
+}
+
+// grid: total tiles of the job table, block 256. H, G: the cell's hidden size and gate count.
+__global__ void __launch_bounds__(256) k_repack(const RepackJob* __restrict__ jobs, int njobs, int H, int Hp, int G,
+                                                int prec) {
+  // transpose tile [k][row], rows XOR-swizzled by k / 4: conflict-free both when a warp writes one
+  // k (32 rows) and when it reads 4 consecutive k of one row per lane
+  __shared__ float tile[kRepackTileK * 32];
+  int ji = 0;
+  while (ji + 1 < njobs && (int)blockIdx.x >= jobs[ji + 1].tile0) ++ji;
+  const RepackJob J = jobs[ji];
+  const int tl = (int)blockIdx.x - J.tile0;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const float wsc = pow2f(kWScaleLog2);
+  if (J.kind == kRepackB) {
+    float* dst = static_cast<float*>(J.p0);
+    for (int e = tl * 1024 + tid; e < min(J.K, (tl + 1) * 1024); e += 256) {
+      const int g = e / Hp, u = e - g * Hp;
+      dst[e] = (u < H && g < G && J.s0) ? J.s0[g * H + u] : 0.0f;
+    }
+    return;
+  }
+  const int r0 = (tl / J.tiles_k) * 32, k0 = (tl % J.tiles_k) * kRepackTileK;
+  constexpr int kQ = kRepackTileK / 4;  // quads per destination row of a tile
+  const long long GH = (long long)G * H;
+  if (J.kind == kRepackT) {
+    const int g = rho_gate(r0), u = rho_unit(r0) + lane;
+    const bool rok = u < H && g < G;
+#pragma unroll
+    for (int i = 0; i < kRepackTileK / 8; ++i) {
+      const int kk = w + 8 * i, k = k0 + kk;
+      float v = 0.0f;
+      if (rok) {
+        if (k < J.k_split) {
+          if (k < J.src_k0) v = J.s0[(long long)k * GH + (long long)g * H + u];
+        } else if (k - J.k_split < H) {
+          v = J.s1[(long long)(k - J.k_split) * GH + (long long)g * H + u];
+        }
+      }
+      tile[kk * 32 + (lane ^ ((kk >> 2) & 31))] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32 * kQ / 256; ++i) {
+      const int idx = tid + 256 * i, r = idx / kQ, q = idx % kQ;
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] = tile[(q * 4 + c) * 32 + (r ^ (q & 31))];
+      if (k0 + q * 4 < J.K) store4_planes(prec, J.p0, J.p1, (long long)(r0 + r) * J.K + k0 + q * 4, v, wsc);
+    }
+    return;
+  }
+  // kRepackC
+#pragma unroll
+  for (int i = 0; i < 32 * kQ / 256; ++i) {
+    const int idx = tid + 256 * i, r = r0 + idx / kQ, k = k0 + (idx % kQ) * 4;
+    if (r >= J.rows || k >= J.K) continue;
+    const bool second = J.s0 == nullptr || k >= J.src_k0;
+    const float* M = second ? J.s1 : J.s0;
+    const int rho = second && J.s0 ? k - J.src_k0 : k;
+    const int g = rho_gate(rho), up = rho_unit(rho);
+    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (r < J.src_rows && g < G) {
+      const float* src = M + (long long)r * GH + (long long)g * H + up;
+      if (up + 3 < H && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(src));
+        v[0] = f.x;
+        v[1] = f.y;
+        v[2] = f.z;
+        v[3] = f.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (up + c < H) v[c] = src[c];
+      }
+    }
+    store4_planes(prec, J.p0, J.p1, (long long)r * J.K + k, v, wsc);
+  }
+}
+
 // Reference-order padded bias: dst[g*Hp + u] = b[g*H + u].
 __global__ void k_pack_bias(const float* __restrict__ b, int H, int Hp, float* dst, int G = 4) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

@@ -293,6 +293,8 @@ struct rw_ctx {
   bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
+  DevBuf repack_jobs;                        // k_repack's job table (built on the first repack)
+  int repack_njobs = 0, repack_tiles = 0;
   DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
   DevBuf pp_maps_dev;
@@ -1369,19 +1371,67 @@ struct PhaseTimer {
 void repack_params(rw_ctx* x, cudaStream_t s) {
   if (!x->dirty) return;
   const int L = x->L, H = x->H, I = x->I, Hp = x->Hp, Ip = x->Ip;
-  for (int l = 0; l < L; ++l) {
-    const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
-    ++g_launches;
-    k_pack_wf<<<dim3(ceil_div(Ipl + Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->W[l].f(), x->R[l].f(), H, Il, Hp,
-                                                                               Ipl, x->prec, x->wf[l].p(0),
-                                                                               x->wf[l].p(1), x->G);
-    const float* wup = l < L - 1 ? x->W[l + 1].f() : nullptr;
-    ++g_launches;
-    k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(wup, x->R[l].f(), H, Hp, x->prec,
-                                                             x->wb[l].p(0), x->wb[l].p(1), x->G);
-    ++g_launches;
-    k_pack_bias<<<ceil_div(4 * Hp, 256), 256, 0, s>>>(x->bias_raw[l].f(), H, Hp, x->bias[l].f(), x->G);
+  if (!x->repack_njobs) {
+    // one launch for every layer's forward / backward images and bias plus W_0^T (k_repack)
+    std::vector<RepackJob> jobs;
+    int tiles = 0;
+    auto add = [&](RepackJob j, int n) {
+      j.tile0 = tiles;
+      tiles += n;
+      jobs.push_back(j);
+    };
+    for (int l = 0; l < L; ++l) {
+      const int Il = l == 0 ? I : H, Ipl = l == 0 ? Ip : Hp;
+      RepackJob f{};
+      f.kind = kRepackT;
+      f.rows = 4 * Hp;
+      f.K = Ipl + Hp;
+      f.tiles_k = ceil_div(f.K, kRepackTileK);
+      f.k_split = Ipl;
+      f.src_k0 = Il;
+      f.s0 = x->W[l].f();
+      f.s1 = x->R[l].f();
+      f.p0 = x->wf[l].p(0);
+      f.p1 = x->wf[l].p(1);
+      add(f, (f.rows / 32) * f.tiles_k);
+      RepackJob b{};
+      b.kind = kRepackC;
+      b.rows = Hp;
+      b.K = (l < L - 1 ? 2 : 1) * 4 * Hp;
+      b.tiles_k = ceil_div(b.K, kRepackTileK);
+      b.src_rows = H;
+      b.src_k0 = 4 * Hp;
+      b.s0 = l < L - 1 ? x->W[l + 1].f() : nullptr;
+      b.s1 = x->R[l].f();
+      b.p0 = x->wb[l].p(0);
+      b.p1 = x->wb[l].p(1);
+      add(b, ceil_div(b.rows, 32) * b.tiles_k);
+      RepackJob c{};
+      c.kind = kRepackB;
+      c.K = 4 * Hp;
+      c.s0 = x->bias_raw[l].f();
+      c.p0 = x->bias[l].f();
+      add(c, ceil_div(c.K, 1024));
+    }
+    RepackJob t{};
+    t.kind = kRepackC;
+    t.rows = Ip;
+    t.K = 4 * Hp;
+    t.tiles_k = ceil_div(t.K, kRepackTileK);
+    t.src_rows = I;
+    t.src_k0 = 4 * Hp;
+    t.s0 = x->W[0].f();
+    t.p0 = x->w0t.p(0);
+    t.p1 = x->w0t.p(1);
+    add(t, ceil_div(t.rows, 32) * t.tiles_k);
+    x->repack_jobs.alloc(jobs.size() * sizeof(RepackJob));
+    RW_CUDA(cudaMemcpy(x->repack_jobs.p, jobs.data(), jobs.size() * sizeof(RepackJob), cudaMemcpyHostToDevice));
+    x->repack_njobs = (int)jobs.size();
+    x->repack_tiles = tiles;
   }
+  ++g_launches;
+  k_repack<<<x->repack_tiles, 256, 0, s>>>(static_cast<const RepackJob*>(x->repack_jobs.p), x->repack_njobs, H, Hp,
+                                           x->G, x->prec);
   if (x->pp_next && x->wn_raw.p) {  // forward boundary group: the next stage's W_first (rw_pp_set_next_w)
     ++g_launches;
     k_pack_wf<<<dim3(ceil_div(2 * Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->wn_raw.f(), x->wn_raw.f(), H, H, Hp,
@@ -1392,9 +1442,6 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
                                                              x->wb_prev.p, nullptr);
   }
-  ++g_launches;
-  k_pack_w0t<<<grid_for((long long)Ip * 4 * Hp), 256, 0, s>>>(x->W[0].f(), H, I, Hp, Ip, x->prec,
-                                                             x->w0t.p(0), x->w0t.p(1), x->G);
   RW_CUDA(cudaGetLastError());
   x->dirty = false;
 }
@@ -2628,7 +2675,10 @@ extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
     out->pid = (int64_t)getpid();
     out->device = x->dev;
     ClRing& r = dir == 0 ? x->ring_f_h[0] : x->ring_b_h[x->L - 1];
-    if (dir == 1) r.ko = ceil_div(4 * x->Hp / 64, kClKBlocks);  // written by the next stage
+    // written by the next stage's boundary group with the member count a single context gives
+    // this layer's off group (kc of the backward plan, runtime.cu planner), so the K split and
+    // the reduction order -- and the results, bit for bit -- match the unsplit stack
+    if (dir == 1) r.ko = x->cl_b.kc;
     r.sys = 1;
     out->ko = r.ko;
     export_region(out, 0, x->cl_offsum.p, r.ring);
@@ -2665,6 +2715,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.sys = 1;
     o.active = 1;
     o.unscale = 1.0f;  // bf16 only (above)
+    o.ko = peer->ko;   // the receiving ring's publication count (rw_pp_export)
     if (dir == 0) {
       if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
       x->wn_raw.alloc((size_t)x->G * H * H * 4);
