@@ -911,45 +911,70 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
   const bool staged = kKind != kCellGru && !(p.debug & 40) &&
                       (size_t)p.stages * BR * kRowBytes >= (size_t)8 * P::kPlanes * nco * 128;
   if (et == 0 && kc > 1) mbar_arrive_expect_tx(S.rx_full, (uint32_t)(kc - 1) * nco * kTileM * 4);
-  for (int it = 0; it <= p.T; ++it) {
+  // Addressing hoisted out of the step loop (as in the forward epilogue): per step only the tape
+  // offsets move back by one block; per column k a compile-time multiple of the column stride.
+  constexpr int kC = kChunks * 8;  // columns per thread (nco = 16 kChunks)
+  const long long col0 = (long long)(p.T - 1) * N + cbase;  // column of (t = T-1, k = 0)
+  long long o_g = col0 * G4 + u, o_h = col0 * Hp + u;       // gates / dG tapes, H-row tapes
+  const long long st_g = (long long)N * G4, st_h = (long long)N * Hp;
+  long long o_dy = ((long long)(p.T - 1) * p.B + cbase) * p.H + u;
+  const long long st_dy = (long long)p.B * p.H;
+  // staged dG image: gate g of unit u sits at K offset kk_g = q*128 + g*32 + lane of the tile's 8
+  // k-blocks; column n = cbase + k has n % 8 == k % 8 (cbase is a multiple of 8), so the 128B
+  // swizzle chunk is (kk_g / 8 % 8) ^ (k % 8)
+  uint32_t sbase[4];
+  int schunk[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int kk = q * 128 + g * 32 + lane;
+    const int rows = (P::kPlanes == 2 ? (kk >> 6) * 2 : (kk >> 6)) * nco + half * (nco >> 1);
+    sbase[g] = dstg + rows * 128 + (kk & 7) * 2;
+    schunk[g] = (kk >> 3) & 7;
+  }
+  int rg[4];  // operand row rho of each gate (the dG operand planes are rho-ordered)
+#pragma unroll
+  for (int g = 0; g < 4; ++g) rg[g] = rho_of(g, u);
+  for (int it = 0; it <= p.T; ++it, o_g -= st_g, o_h -= st_h, o_dy -= st_dy) {
     const int t = p.T - 1 - it;
     const bool off = ko > 0 && t >= 0;
     const bool have = t <= p.T - 2;  // an R^T.dG_{t+1} product was accumulated
-    float pi[8], pf[8], po[8], pcb[8], ptc[8], pcp[8], dyv[8];
+    // tapes of one chunk of 8 columns (registers bound the batch); chunk 0 is loaded before the
+    // wait for this step's GEMM, the others inside the cell loop
+    float pi[8], pf[8], po[8], pcb[8], pcp[8], ptc[8], dyv[8];
     auto load_tapes = [&](int i) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
+        const int k = i * 8 + j;
         pi[j] = pf[j] = po[j] = pcb[j] = ptc[j] = pcp[j] = dyv[j] = 0.0f;
-        const long long n = cbase + i * 8 + j;
         if (t < 0 || !uok || (p.debug & 4)) continue;
-        const long long col = (long long)t * N + n;
-        const float* gp = Ly.gates + col * G4 + u;
+        const float* gp = Ly.gates + o_g + k * G4;
+        const long long oh = o_h + k * Hp;
         if constexpr (kKind == kCellLstm) {
           pi[j] = gp[0];
           pf[j] = gp[Hp];
           po[j] = gp[2 * Hp];
           pcb[j] = gp[3 * Hp];
-          ptc[j] = Ly.tanhc[col * Hp + u];
-          pcp[j] = Ly.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+          ptc[j] = Ly.tanhc[oh];
+          pcp[j] = Ly.c[oh];  // c_{t-1}: block t of the c tape
         } else if constexpr (kKind == kCellGru) {
-          pi[j] = gp[0];                 // r
-          pf[j] = gp[Hp];                // u
-          po[j] = gp[2 * Hp];            // n
-          pcb[j] = Ly.zrh[col * Hp + u]; // R_n h_{t-1}
-          pcp[j] = Ly.h[col * Hp + u];   // h_{t-1}: block t of the h tape
+          pi[j] = gp[0];        // r
+          pf[j] = gp[Hp];       // u
+          po[j] = gp[2 * Hp];   // n
+          pcb[j] = Ly.zrh[oh];  // R_n h_{t-1}
+          pcp[j] = Ly.h[oh];    // h_{t-1}: block t of the h tape
         } else {
-          pcp[j] = Ly.h[(col + N) * Hp + u];  // h_t: block t + 1
+          pcp[j] = Ly.h[oh + st_h];  // h_t: block t + 1
         }
-        if (Ly.dy && u < p.H && n < p.B) dyv[j] = Ly.dy[((long long)t * p.B + n) * p.H + u];
+        if (Ly.dy && u < p.H && cbase + k < p.B) dyv[j] = Ly.dy[o_dy + (long long)k * p.H];
       }
     };
-    load_tapes(0);  // independent of this step's GEMM: in flight while we wait
+    load_tapes(0);
     if (kKind == kCellLstm && t >= 1) {
       // pull next step's tape lines (gates x4, tanh(c), c of this warp's 32 units and its
       // columns) from HBM into L2 now, so next step's loads are L2 hits
       const long long tn = t - 1;
       const int ub = tile * kTileM + q * 32;
-      for (int pi = lane; pi < kChunks * 8 * 6; pi += 32) {
+      for (int pi = lane; pi < kC * 6; pi += 32) {
         const long long col = tn * N + cbase + pi / 6;
         const int ty = pi % 6;
         const float* a = ty < 4 ? Ly.gates + col * G4 + ty * Hp + ub
@@ -960,15 +985,14 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     mbar_wait(&S.tmem_full[it & 1], (it >> 1) & 1);
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
-    float acc[kChunks * 8];
+    float acc[kC];
     cl_reduce<P, kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, p.unscale, &p);
     if (et == 0) cl_trace(p, it, 12);
-    float dab[kChunks * 8];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
+    float dab[kC];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
       mbar_wait(S.off_full, offc & 1);
 #pragma unroll
-      for (int i = 0; i < kChunks * 8; ++i)
-        dab[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
+      for (int i = 0; i < kC; ++i) dab[i] = lds_f32(S.rxoff + (size_t)(half * kC + i) * kTileM + row);
     }
     if (et == 0) cl_trace(p, it, 13);
     named_bar_sync(1, kEpiThreads);
@@ -981,7 +1005,7 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170); GRU: dh0 = R^T dgr_0 + the direct term dh_0 u_0
       if (uok) {
 #pragma unroll
-        for (int i = 0; i < kChunks * 8; ++i) {
+        for (int i = 0; i < kC; ++i) {
           const long long n = cbase + i;
           Ly.dh0[n * Hp + u] = kKind == kCellGru ? acc[i] + carry[i] : acc[i];
           if constexpr (kKind == kCellLstm) Ly.dc0[n * Hp + u] = carry[i];
@@ -989,111 +1013,104 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       }
       break;
     }
-    float g_i[kChunks * 8], g_f[kChunks * 8], g_o[kChunks * 8], g_c[kChunks * 8];
+    float g_i[kC], g_f[kC], g_o[kC], g_c[kC];
 #pragma unroll
-    for (int i = 0; i < kChunks; ++i) {
-      if (i > 0) load_tapes(i);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = i * 8 + j;
-        // dh = d_above + carry_h (GRU: carry_h = R^T dgr_{t+1} + the direct term dh_{t+1} u_{t+1})
-        const float ch = kKind == kCellGru ? acc[k] + carry[k] : acc[k];
-        const float dh = off ? dab[k] + ch : (Ly.dy ? dyv[j] + ch : ch);
-        if constexpr (kKind == kCellLstm) {  // cells.hpp:424-447 operation order
-          const float q1 = dh * po[j];
-          const float s0 = ptc[j] * ptc[j];
-          const float s1 = 1.0f - s0;
-          const float q2 = q1 * s1;
-          const float dc = carry[k] + q2;
-          const float a1 = dc * pcb[j], a2 = a1 * pi[j], a3 = 1.0f - pi[j];
-          const float b1 = dc * pcp[j], b2 = b1 * pf[j], b3 = 1.0f - pf[j];
-          const float c1 = dh * ptc[j], c2 = c1 * po[j], c3 = 1.0f - po[j];
-          const float d1 = dc * pi[j], d2 = pcb[j] * pcb[j], d3 = 1.0f - d2;
-          g_i[k] = a2 * a3;
-          g_f[k] = b2 * b3;
-          g_o[k] = c2 * c3;
-          g_c[k] = d1 * d3;
-          carry[k] = dc * pf[j];
-        } else if constexpr (kKind == kCellGru) {  // cells.hpp:514-538 operation order
-          const float om = 1.0f - pf[j];
-          const float dn = dh * om;
-          const float s = po[j] * po[j];
+    for (int k = 0; k < kC; ++k) {
+      const int j = k & 7;
+      if (j == 0 && k > 0) load_tapes(k >> 3);
+      // dh = d_above + carry_h (GRU: carry_h = R^T dgr_{t+1} + the direct term dh_{t+1} u_{t+1})
+      const float ch = kKind == kCellGru ? acc[k] + carry[k] : acc[k];
+      const float dh = off ? dab[k] + ch : (Ly.dy ? dyv[j] + ch : ch);
+      if constexpr (kKind == kCellLstm) {  // cells.hpp:424-447 operation order
+        const float q1 = dh * po[j];
+        const float s0 = ptc[j] * ptc[j];
+        const float s1 = 1.0f - s0;
+        const float q2 = q1 * s1;
+        const float dc = carry[k] + q2;
+        const float a1 = dc * pcb[j], a2 = a1 * pi[j], a3 = 1.0f - pi[j];
+        const float b1 = dc * pcp[j], b2 = b1 * pf[j], b3 = 1.0f - pf[j];
+        const float c1 = dh * ptc[j], c2 = c1 * po[j], c3 = 1.0f - po[j];
+        const float d1 = dc * pi[j], d2 = pcb[j] * pcb[j], d3 = 1.0f - d2;
+        g_i[k] = a2 * a3;
+        g_f[k] = b2 * b3;
+        g_o[k] = c2 * c3;
+        g_c[k] = d1 * d3;
+        carry[k] = dc * pf[j];
+      } else if constexpr (kKind == kCellGru) {  // cells.hpp:514-538 operation order
+        const float om = 1.0f - pf[j];
+        const float dn = dh * om;
+        const float s = po[j] * po[j];
+        const float s1 = 1.0f - s;
+        const float dnp = dn * s1;
+        const float tt = pcp[j] - po[j];
+        const float q = dh * tt;
+        const float q2 = q * pf[j];
+        const float dgu = q2 * om;
+        const float r0 = dnp * pcb[j];
+        const float r1 = r0 * pi[j];
+        const float r2 = 1.0f - pi[j];
+        g_i[k] = r1 * r2;     // dgw = dgr (reset gate)
+        g_f[k] = dgu;         // dgw = dgr (update gate)
+        g_o[k] = dnp;         // dgw (candidate); dgr = dnp r
+        g_c[k] = dnp * pi[j]; // slot 3 carries dgr of the candidate (slot 3 of dgw is zero)
+        carry[k] = dh * pf[j];
+      } else {  // RNN (cells.hpp:370-383)
+        if (p.kind == kCellRnnRelu) {
+          g_i[k] = pcp[j] > 0.0f ? dh : 0.0f;
+        } else {
+          const float s = pcp[j] * pcp[j];
           const float s1 = 1.0f - s;
-          const float dnp = dn * s1;
-          const float tt = pcp[j] - po[j];
-          const float q = dh * tt;
-          const float q2 = q * pf[j];
-          const float dgu = q2 * om;
-          const float r0 = dnp * pcb[j];
-          const float r1 = r0 * pi[j];
-          const float r2 = 1.0f - pi[j];
-          g_i[k] = r1 * r2;     // dgw = dgr (reset gate)
-          g_f[k] = dgu;         // dgw = dgr (update gate)
-          g_o[k] = dnp;         // dgw (candidate); dgr = dnp r
-          g_c[k] = dnp * pi[j]; // slot 3 carries dgr of the candidate (slot 3 of dgw is zero)
-          carry[k] = dh * pf[j];
-        } else {  // RNN (cells.hpp:370-383)
-          if (p.kind == kCellRnnRelu) {
-            g_i[k] = pcp[j] > 0.0f ? dh : 0.0f;
-          } else {
-            const float s = pcp[j] * pcp[j];
-            const float s1 = 1.0f - s;
-            g_i[k] = dh * s1;
-          }
-          g_f[k] = g_o[k] = g_c[k] = 0.0f;
+          g_i[k] = dh * s1;
         }
-        if (staged) {
-          // K offset within the tile's 8 k-blocks: rho_of(g, u) - 4 * tile * 128; staging rows
-          // (k-block, plane, owned column) -- fp16x2 keeps each k-block's hi and lo runs adjacent
-          const int n = cbase + k, nl = n - m * nco;
+        g_f[k] = g_o[k] = g_c[k] = 0.0f;
+      }
+      if (staged) {
+        // staging rows (k-block, plane, owned column): fp16x2 keeps each k-block's hi and lo runs adjacent
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int kk = q * 128 + g * 32 + lane;
-            const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
-            const uint32_t so = ((((kk >> 3) & 7) ^ (n & 7)) << 4) + (kk & 7) * 2;
+        for (int g = 0; g < 4; ++g) {
+          const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+          const uint32_t a = sbase[g] + k * 128 + ((schunk[g] ^ (k & 7)) << 4);
+          if constexpr (P::kPlanes == 2) {
+            __half hh, hl;
+            gmax = fmaxf(gmax, fabsf(gv));
+            f16x2_split(gv * kGS, hh, hl);
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(__half_as_ushort(hh)));
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(a + nco * 128), "h"(__half_as_ushort(hl)));
+          } else {
+            sts_bf16(a, gv);
+          }
+        }
+      } else if (uok && !(p.debug & 8)) {
+        uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
+        const int n = cbase + k;
+        if constexpr (kKind == kCellGru) {  // the W-side image (layer below): slots r, u, n, 0
+          uint8_t* wblk = Ly.dgwsw + (size_t)t * G4 * BR * 2;
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g_o[k];
             if constexpr (P::kPlanes == 2) {
               __half hh, hl;
-              gmax = fmaxf(gmax, fabsf(gv));
               f16x2_split(gv * kGS, hh, hl);
-              const uint32_t r0 = ((kk >> 6) * 2) * nco + nl;
-              asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + r0 * 128 + so), "h"(__half_as_ushort(hh)));
-              asm volatile("st.shared.b16 [%0], %1;" ::"r"(dstg + (r0 + nco) * 128 + so), "h"(__half_as_ushort(hl)));
+              *reinterpret_cast<__half*>(wblk + sw_off(rg[g], n, BR)) = hh;
+              *reinterpret_cast<__half*>(wblk + sw_off(rg[g], N + n, BR)) = hl;
             } else {
-              sts_bf16(dstg + ((kk >> 6) * nco + nl) * 128 + so, gv);
+              *reinterpret_cast<__nv_bfloat16*>(wblk + sw_off(rg[g], n, N)) = __float2bfloat16_rn(gv);
             }
           }
-        } else if (uok && !(p.debug & 8)) {
-          uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
-          const int n = cbase + k;
-          if constexpr (kKind == kCellGru) {  // the W-side image (layer below): slots r, u, n, 0
-            uint8_t* wblk = Ly.dgwsw + (size_t)t * G4 * BR * 2;
+        }
 #pragma unroll
-            for (int g = 0; g < 3; ++g) {
-              const float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g_o[k];
-              if constexpr (P::kPlanes == 2) {
-                __half hh, hl;
-                f16x2_split(gv * kGS, hh, hl);
-                *reinterpret_cast<__half*>(wblk + sw_off(rho_of(g, u), n, BR)) = hh;
-                *reinterpret_cast<__half*>(wblk + sw_off(rho_of(g, u), N + n, BR)) = hl;
-              } else {
-                *reinterpret_cast<__nv_bfloat16*>(wblk + sw_off(rho_of(g, u), n, N)) = __float2bfloat16_rn(gv);
-              }
-            }
-          }
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            // the R-side image (this layer's recurrence); GRU: slots r, u, n <- dgr (slot 3's value), 0
-            float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
-            if (kKind == kCellGru) gv = g == 2 ? g_c[k] : g == 3 ? 0.0f : gv;
-            if constexpr (P::kPlanes == 2) {
-              __half hh, hl;
-              gmax = fmaxf(gmax, fabsf(gv));
-              f16x2_split(gv * kGS, hh, hl);
-              *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), n, BR)) = hh;
-              *reinterpret_cast<__half*>(blk + sw_off(rho_of(g, u), N + n, BR)) = hl;
-            } else {
-              *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rho_of(g, u), n, N)) = __float2bfloat16_rn(gv);
-            }
+        for (int g = 0; g < 4; ++g) {
+          // the R-side image (this layer's recurrence); GRU: slots r, u, n <- dgr (slot 3's value), 0
+          float gv = g == 0 ? g_i[k] : g == 1 ? g_f[k] : g == 2 ? g_o[k] : g_c[k];
+          if (kKind == kCellGru) gv = g == 2 ? g_c[k] : g == 3 ? 0.0f : gv;
+          if constexpr (P::kPlanes == 2) {
+            __half hh, hl;
+            gmax = fmaxf(gmax, fabsf(gv));
+            f16x2_split(gv * kGS, hh, hl);
+            *reinterpret_cast<__half*>(blk + sw_off(rg[g], n, BR)) = hh;
+            *reinterpret_cast<__half*>(blk + sw_off(rg[g], N + n, BR)) = hl;
+          } else {
+            *reinterpret_cast<__nv_bfloat16*>(blk + sw_off(rg[g], n, N)) = __float2bfloat16_rn(gv);
           }
         }
       }
@@ -1103,7 +1120,8 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
       // run of the operand image (fp16x2: hi rows at m*nco, lo rows at N + m*nco of the k-block)
       named_bar_sync(1, kEpiThreads);
       uint8_t* blk = Ly.dgsw + (size_t)t * G4 * BR * 2;
-      const int kb0 = tile * 8, nkb = min(8, (int)(G4 / 64) - kb0), per = nco * 8;
+      const int kb0 = tile * 8, nkb = min(8, (int)(G4 / 64) - kb0);
+      constexpr int per = 16 * kChunks * 8;  // nco * 8 chunks of 16 B per (k-block, plane)
       for (int i = et; i < nkb * P::kPlanes * per; i += kEpiThreads) {
         const int kp = i / per, r = i - kp * per;  // kp = k-block * planes + plane
         const int kb = kp / P::kPlanes, pl = kp - kb * P::kPlanes;
@@ -1123,24 +1141,24 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     }
     if (uok) {
 #pragma unroll
-      for (int k = 0; k < kChunks * 8; ++k) {
-        const long long ob = ((long long)t * N + cbase + k) * G4;
+      for (int k = 0; k < kC; ++k) {
+        const long long ob = o_g - u + k * G4;  // column (t, cbase + k) of the rho-ordered planes
         const float wc = kKind == kCellGru ? 0.0f : g_c[k];  // slot 3 of dgw (GRU: holds dgr_n)
-        store_operand<P>(Ly.dgop, ob + rho_of(0, u), g_i[k] * kGS);
-        store_operand<P>(Ly.dgop, ob + rho_of(1, u), g_f[k] * kGS);
-        store_operand<P>(Ly.dgop, ob + rho_of(2, u), g_o[k] * kGS);
-        store_operand<P>(Ly.dgop, ob + rho_of(3, u), wc * kGS);
-        float* dgp = Ly.dg + ((long long)t * N + cbase + k) * G4 + u;
+        store_operand<P>(Ly.dgop, ob + rg[0], g_i[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rg[1], g_f[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rg[2], g_o[k] * kGS);
+        store_operand<P>(Ly.dgop, ob + rg[3], wc * kGS);
+        float* dgp = Ly.dg + o_g + k * G4;
         dgp[0] = g_i[k];
         dgp[Hp] = g_f[k];
         dgp[2 * Hp] = g_o[k];
         dgp[3 * Hp] = wc;
         if constexpr (kKind == kCellGru) {  // dgr: r, u as dgw, candidate dnp r (cells.hpp:527-529)
-          store_operand<P>(Ly.dgrop, ob + rho_of(0, u), g_i[k] * kGS);
-          store_operand<P>(Ly.dgrop, ob + rho_of(1, u), g_f[k] * kGS);
-          store_operand<P>(Ly.dgrop, ob + rho_of(2, u), g_c[k] * kGS);
-          store_operand<P>(Ly.dgrop, ob + rho_of(3, u), 0.0f);
-          float* dgq = Ly.dgr + ((long long)t * N + cbase + k) * G4 + u;
+          store_operand<P>(Ly.dgrop, ob + rg[0], g_i[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rg[1], g_f[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rg[2], g_c[k] * kGS);
+          store_operand<P>(Ly.dgrop, ob + rg[3], 0.0f);
+          float* dgq = Ly.dgr + o_g + k * G4;
           dgq[0] = g_i[k];
           dgq[Hp] = g_f[k];
           dgq[2 * Hp] = g_c[k];

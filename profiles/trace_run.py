@@ -51,6 +51,16 @@ def summarize(path):
             pub[key] = max(pub[key], int(r["end_ns"]))
         if r["span"] == "wait":
             seen[key].append(int(r["end_ns"]))
+    # skew between the critical CTAs of one (layer, step): first to last publish
+    pubs = defaultdict(list)
+    for r in rows:
+        if r["span"] == "publish":
+            pubs[(r["phase"], int(r["task_layer"]), int(r["task_block"]))].append(int(r["end_ns"]))
+    for ph in ("fwd", "bwd"):
+        sp = [max(v) - min(v) for k, v in pubs.items() if k[0] == ph and len(v) > 1]
+        if sp:
+            out[f"{ph}.publish_spread_median_ns"] = statistics.median(sp)
+            out[f"{ph}.publish_spread_p90_ns"] = sorted(sp)[int(0.9 * (len(sp) - 1))]
     for ph, d in (("fwd", -1), ("bwd", 1)):
         props = []
         for (p2, l, t), v in seen.items():
