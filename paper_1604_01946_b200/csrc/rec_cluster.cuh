@@ -91,7 +91,12 @@ struct ClParams {
   int kc;        // active critical members per tile
   int cs;        // cluster size = max(kc, ko over groups)
   int ncomax;    // Bp / min(kc, min ko): receive-slot size (columns) of the carve-up
-  int stages;    // B-operand TMA stages
+  int stages;    // B-operand TMA stages (critical CTAs; also the ring region's size)
+  int stages_off;   // off CTAs' stages (< stages when the critical CTAs alias their push staging)
+  int st_alias;     // backward: critical CTAs stage their split-K pushes inside the B ring (idle
+                    // between this step's MMAs and the next step's loads), at byte offset st_off;
+                    // off CTAs keep them after their stages_off stages
+  int st_off;
   int ring;      // off-partial ring depth (kRing; RW_PP_RING for the sequential pipeline test)
   int n_crit;    // critical layer groups (grid rows y < n_crit); rows may also carry off groups
   const ClRing* cring;   // [n_crit]
@@ -142,15 +147,17 @@ __host__ __device__ inline size_t cl_smem_bytes(int cs, int ncomax, int rows, in
 }
 
 template <class P>
-__device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p) {
+__device__ __forceinline__ ClSmem cl_carve(uint8_t* smem, const ClParams& p, bool crit = true) {
   ClSmem s;
   const size_t slot = cl_slot_bytes(p.ncomax);
   s.a = smem;
   s.b = s.a + kClKBlocks * kTileM * kRowBytes;
-  s.rx = reinterpret_cast<float*>(s.b + p.stages * P::kPlanes * p.Bp * kRowBytes);
+  const size_t stage = (size_t)P::kPlanes * p.Bp * kRowBytes;
+  s.rx = reinterpret_cast<float*>(s.b + p.stages * stage);
   s.rxoff = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rx) + (p.cs - 1) * slot);
-  s.st = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(s.rxoff) + slot);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s.st) + (p.cs - 1) * slot);
+  uint8_t* st_sep = reinterpret_cast<uint8_t*>(s.rxoff) + slot;
+  s.st = reinterpret_cast<float*>(!p.st_alias ? st_sep : crit ? s.b + p.st_off : s.b + p.stages_off * stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_sep + (p.st_alias ? 0 : (p.cs - 1) * slot));
   s.full = bars;
   s.empty = bars + p.stages;
   s.a_full = bars + 2 * p.stages;
@@ -328,8 +335,8 @@ __device__ __forceinline__ void cl_load_alo(const ClSmem& S, uint32_t tmem_alo, 
 // k-blocks travel in pairs (one 2 x N x 128-byte copy into two adjacent stages, completion on
 // the even stage's barrier) when the ring and the step's k-block count are even: >= 16 KB bulk
 // copies ingest ~62 B/cycle per SM vs ~50 for 8 KB ones (profiles/ubench/mma_ubench.cu).
-__device__ __forceinline__ bool cl_pair_kb(const ClParams& p, int nkb) {
-  return !(p.debug & 64) && (p.stages % 2 == 0) && (nkb % 2 == 0);
+__device__ __forceinline__ bool cl_pair_kb(const ClParams& p, int nkb, int stages) {
+  return !(p.debug & 64) && (stages % 2 == 0) && (nkb % 2 == 0);
 }
 // MMA issuers: warps 1 (j = 0) and 3 (j = 1), each converged; elect.sync inside the instruction
 // blocks picks the issuing lane (sm100_ptx.cuh umma_bf16_warp). Issuer j multiplies its half of
@@ -341,7 +348,7 @@ template <class P>
 __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, int it, uint32_t acc, int nkb,
                                             uint32_t idesc, uint32_t& pc, int stages, int N, int j,
                                             uint32_t tmem_alo) {
-  const bool pairs = cl_pair_kb(p, nkb);
+  const bool pairs = cl_pair_kb(p, nkb, stages);
   const int a_bytes = kTileM * kRowBytes, b_bytes = P::kPlanes * N * kRowBytes;
   const bool l0 = (threadIdx.x & 31) == 0;
   const uint64_t a0 = sdesc_sw128(smem_u32(S.a), 16, 1024), b0 = sdesc_sw128(smem_u32(S.b), 16, 1024);
@@ -697,7 +704,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (t > 0) wait_flag(&Ly.flags[t - 1], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 2));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
-        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR, cl_pair_kb(p, nkb));
+        cl_load_b(S, Ly.hsw + (size_t)t * p.Hp * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR, cl_pair_kb(p, nkb, p.stages));
         if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
         cl_trace(p, t, 14);  // task start: h_{t-1} and the off partial both available
       } else {
@@ -705,7 +712,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         fence_proxy_async_global();
         cl_trace(p, t, 1);
         cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, p.stages, BR,
-                  cl_pair_kb(p, nkb));
+                  cl_pair_kb(p, nkb, p.stages));
       }
     }
   } else if (active && (warp == 1 || warp == 3)) {
@@ -1237,7 +1244,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const ClSmem S = cl_carve<P>(smem, p);
+  const ClSmem S = cl_carve<P>(smem, p, crit);
+  const int stages = crit ? p.stages : p.stages_off;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem_need = 4 * N + (P::kPlanes == 2 ? nkb * 32 : 0);  // as k_cl_fwd
   uint32_t tmem_cols = 32;
@@ -1272,14 +1280,18 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           wait_flag(&Ly.flags[t + 1], flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 2));
         else if (Og.op_flags)
           wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(1, l, t, 1));
+        // aliased push staging: the peers consumed this CTA's previous pushes (implied by the flag
+        // -- every member published after reading them -- and made formal by the barrier) before
+        // the ring is refilled
+        if (crit && p.st_alias && kc > 1 && it > 0) mbar_wait(S.push_free, (it - 1) & 1);
         fence_proxy_async_global();
         cl_trace(p, it, 1);
         if (crit)
-          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * BR * 2, kb_lo, kb_hi, kofs, pc, p.stages, BR,
-                    cl_pair_kb(p, nkb));
+          cl_load_b(S, Ly.dgsw + (size_t)(t + 1) * G4p * BR * 2, kb_lo, kb_hi, kofs, pc, stages, BR,
+                    cl_pair_kb(p, nkb, stages));
         else
-          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, p.stages, BR,
-                    cl_pair_kb(p, nkb));
+          cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, stages, BR,
+                    cl_pair_kb(p, nkb, stages));
       }
       if (off && !early) cl_fetch_off(S, p, ring, done, done_target, it, m, nco, offc, wait_code(1, l, t, 3), sys);
       if (crit) cl_trace(p, it, 14);  // task start: dG_{t+1} and the off partial (d_above) both available
@@ -1299,7 +1311,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
       }
       if (!crit || t <= p.T - 2)
-        cl_mma_step<P>(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j, tmem_alo);
+        cl_mma_step<P>(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, stages, N, j, tmem_alo);
       umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {

@@ -193,6 +193,7 @@ constexpr int kNcclFloat32 = 7, kNcclSum = 0;
 
 struct ClPlan {
   int kc = 0, cs = 0, ncomax = 0, stages = 0;
+  int stages_off = 0, st_alias = 0, st_off = 0;  // ClParams (rec_cluster.cuh)
   size_t smem = 0;
   void* kern = nullptr;  // the k_cl_fwd / k_cl_bwd instantiation for Bp / kc owned columns
 };
@@ -491,13 +492,34 @@ bool plan_cluster(int prec, bool fwd, int kc, const std::vector<int>& ko, int ti
   // an even ring lets operand k-blocks travel in pairs (rec_cluster.cuh cl_pair_kb)
   if (stages % 2 && stages > min_stages) smem = cl_smem_bytes(cs, ncomax, rows, --stages);
   if (fwd && (size_t)stages * rows * kRowBytes < (size_t)(Bp / kc) * kTileM * 4) return false;
+  // backward with split-K pushes: the critical CTAs stage their pushes inside the B ring (after
+  // the dG staging image), which frees (cs-1) slots for more ring stages; the off CTAs keep a
+  // separate staging area after their (fewer) stages in the same region (rec_cluster.cuh)
+  int stages_off = stages, st_alias = 0, st_off = 0;
+  if (!fwd && cs > 1 && !(getenv("RW_CL_ST_ALIAS") && atoi(getenv("RW_CL_ST_ALIAS")) == 0)) {
+    const size_t stage = (size_t)rows * kRowBytes, slot = cl_slot_bytes(ncomax), st_bytes = (size_t)(cs - 1) * slot;
+    const size_t staging = (size_t)8 * prec_planes(prec) * (Bp / kc) * 128;
+    const size_t fixed = 1024 + (size_t)kClKBlocks * kTileM * kRowBytes + (size_t)cs * slot + 16;
+    int sc = kClKBlocks;
+    while (sc > 2 && fixed + sc * stage + (2 * sc + 12) * 8 > (size_t)kSmemLimit) --sc;
+    if (sc % 2) --sc;
+    int so = sc * stage > st_bytes ? (int)((sc * stage - st_bytes) / stage) : 0;
+    if (so % 2) --so;
+    if (sc > stages && so >= 2 && (size_t)sc * stage >= staging + st_bytes) {
+      stages = sc;
+      stages_off = so;
+      st_alias = 1;
+      st_off = (int)((staging + 1023) / 1024 * 1024);
+      smem = fixed + sc * stage + (2 * sc + 12) * 8;
+    }
+  }
   smem = std::max(smem, (size_t)116 * 1024);  // one CTA per SM
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
   if ((long long)max_active_clusters(kernel, cs, smem, L * tiles * 2 * cs) < (long long)L * tiles * 2) return false;
-  out = ClPlan{kc, cs, ncomax, stages, smem, kernel};
+  out = ClPlan{kc, cs, ncomax, stages, stages_off, st_alias, st_off, smem, kernel};
   return true;
 }
 
@@ -1546,6 +1568,9 @@ ClParams cl_params(rw_ctx* x, bool fwd) {
   p.cs = pl.cs;
   p.ncomax = pl.ncomax;
   p.stages = pl.stages;
+  p.stages_off = pl.stages_off;
+  p.st_alias = pl.st_alias;
+  p.st_off = pl.st_off;
   p.ring = x->cl_ring;
   p.n_crit = x->L;
   p.cring = static_cast<const ClRing*>((fwd ? x->cl_ring_f : x->cl_ring_b).p);
