@@ -242,15 +242,25 @@ __device__ __forceinline__ void red_relaxed_s(uint32_t* p, uint32_t v, bool sys)
 __device__ __forceinline__ int cl_slot(int s, int d) { return s < d ? s : s - 1; }
 
 // Load 8 accumulator columns of this thread's TMEM lane: acc0 (+ acc1, `two` accumulators N
-// columns apart, the two issuers' halves of K), or zeros if nothing was accumulated.
-__device__ __forceinline__ void cl_ld8(uint32_t taddr, bool have, float (&v)[8], bool two = false, int N = 0) {
+// columns apart, the two issuers' halves of K), or zeros if nothing was accumulated. `fz` (critical
+// CTAs, fp16x2 with fused hi planes): each issuer's accumulator is 2N wide -- [A_hi.B_hi +
+// A_lo.B_hi | A_hi.B_lo] -- so the parts are N apart and there are 2 (4 with `two`) of them.
+__device__ __forceinline__ void cl_ld8(uint32_t taddr, bool have, float (&v)[8], bool two = false, int N = 0,
+                                       bool fz = false) {
   if (have) {
     uint32_t r[8], r2[8];
     tmem_ld_32x32b_x8(taddr, r);
-    if (two) tmem_ld_32x32b_x8(taddr + N, r2);
+    if (two || fz) tmem_ld_32x32b_x8(taddr + N, r2);
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = two ? __uint_as_float(r[j]) + __uint_as_float(r2[j]) : __uint_as_float(r[j]);
+    for (int j = 0; j < 8; ++j) v[j] = (two || fz) ? __uint_as_float(r[j]) + __uint_as_float(r2[j]) : __uint_as_float(r[j]);
+    if (fz && two) {
+      tmem_ld_32x32b_x8(taddr + 2 * N, r);
+      tmem_ld_32x32b_x8(taddr + 3 * N, r2);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += __uint_as_float(r[j]) + __uint_as_float(r2[j]);
+    }
   } else {
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = 0.0f;
@@ -347,7 +357,7 @@ __device__ __forceinline__ int cl_half0(int nkb) { return (nkb + 1) >> 1; }
 template <class P>
 __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, int it, uint32_t acc, int nkb,
                                             uint32_t idesc, uint32_t& pc, int stages, int N, int j,
-                                            uint32_t tmem_alo) {
+                                            uint32_t tmem_alo, bool fz = false, uint32_t idesc2 = 0) {
   const bool pairs = cl_pair_kb(p, nkb, stages);
   const int a_bytes = kTileM * kRowBytes, b_bytes = P::kPlanes * N * kRowBytes;
   const bool l0 = (threadIdx.x & 31) == 0;
@@ -365,6 +375,14 @@ __device__ __forceinline__ void cl_mma_step(const ClSmem& S, const ClParams& p, 
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {  // 4 x K=16 per 64-element k-block (32 bytes along K)
       const uint32_t acc_on = (k != k_lo || kk) ? 1u : 0u;
+      if (P::kPlanes == 2 && fz) {
+        // one N = 2N MMA over the stage's [hi rows | lo rows]: columns [0, N) A_hi.B_hi, [N, 2N)
+        // A_hi.B_lo (an N = 128 MMA costs what an N = 64 one does, profiles/r01 ubench), then A_lo.B_hi
+        // into the first half
+        umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, kk * 32), idesc2, acc_on);
+        umma_ts_f16_warp(acc, tmem_alo + k * 32 + kk * 8, desc_add(bd, kk * 32), idesc, 1u);
+        continue;
+      }
       umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, kk * 32), idesc, acc_on);
       if constexpr (P::kPlanes == 2) {
         umma_bf16_warp(acc, desc_add(ad, kk * 32), desc_add(bd, N * kRowBytes + kk * 32), idesc, 1u);
@@ -410,7 +428,7 @@ __device__ __forceinline__ void cl_load_b(const ClSmem& S, const uint8_t* blk, i
 template <class P, int kChunks>
 __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool have, bool two, int N, int it, int m,
                                           int n_act, int nco, uint32_t& rxc, float (&v_out)[kChunks * 8],
-                                          float unscale, const ClParams* tp = nullptr) {
+                                          float unscale, const ClParams* tp = nullptr, bool fz = false) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const uint32_t taddr = tacc + (uint32_t(q * 32) << 16);
@@ -425,7 +443,7 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
       float* blk = S.st + (size_t)cl_slot(d, m) * nco * kTileM;
       for (int c0 = half * (nco >> 1); c0 < (half + 1) * (nco >> 1); c0 += 8) {
         float v[8];
-        cl_ld8(taddr + d * nco + c0, have, v, two, N);
+        cl_ld8(taddr + d * nco + c0, have, v, two, N, fz);
 #pragma unroll
         for (int j = 0; j < 8; ++j) sts_f32(blk + (size_t)(c0 + j) * kTileM + row, v[j]);
       }
@@ -445,16 +463,27 @@ __device__ __forceinline__ void cl_reduce(const ClSmem& S, uint32_t tacc, bool h
   if (have) {
     // every chunk's TMEM loads in flight before one wait
     uint32_t r[kChunks * 8], r2[kChunks * 8];
+    const bool pair01 = two || fz;  // a second part N columns after the first
 #pragma unroll
     for (int i = 0; i < kChunks; ++i) {
       uint32_t* ri = r + i * 8;
       tmem_ld_32x32b_x8(taddr + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(ri));
-      if (two) tmem_ld_32x32b_x8(taddr + N + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(r2 + i * 8));
+      if (pair01) tmem_ld_32x32b_x8(taddr + N + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(r2 + i * 8));
     }
     tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < kChunks * 8; ++i)
-      v_out[i] = two ? __uint_as_float(r[i]) + __uint_as_float(r2[i]) : __uint_as_float(r[i]);
+      v_out[i] = pair01 ? __uint_as_float(r[i]) + __uint_as_float(r2[i]) : __uint_as_float(r[i]);
+    if (fz && two) {  // the second issuer's two parts (2N, 3N)
+#pragma unroll
+      for (int i = 0; i < kChunks; ++i) {
+        tmem_ld_32x32b_x8(taddr + 2 * N + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(r + i * 8));
+        tmem_ld_32x32b_x8(taddr + 3 * N + own0 + half * (nco >> 1) + i * 8, *reinterpret_cast<uint32_t(*)[8]>(r2 + i * 8));
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < kChunks * 8; ++i) v_out[i] += __uint_as_float(r[i]) + __uint_as_float(r2[i]);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < kChunks * 8; ++i) v_out[i] = 0.0f;
@@ -587,11 +616,12 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // rows of gate slot 2 get W_n x, rows of the unused slot 3 get R_n h (written by the slot-2 threads).
 template <class P, int kChunks, int kKind = kCellLstm>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
-                                           int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp, float unscale) {
+                                           int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp, float unscale,
+                                           bool fz = false) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   float v[kChunks * 8];
-  cl_reduce<P, kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v, unscale);
+  cl_reduce<P, kChunks>(S, tacc, true, two, N, t, m, kc, nco, rxc, v, unscale, nullptr, fz);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 9);
   mbar_wait(S.off_full, offc & 1);
   if (tp && threadIdx.x == kEpiBase) cl_trace(*tp, t, 10);
@@ -666,6 +696,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int nkb = kb_hi - kb_lo;
   const bool two = nkb - cl_half0(nkb) > 0;  // the second issuer accumulated something
   const int nco = N / n_act;
+  // critical fp16x2 CTAs fuse A_hi.B_hi and A_hi.B_lo into one N = 2N MMA (cl_mma_step): each
+  // issuer's accumulator is 2N wide and there is one step buffer -- the next step's MMAs need this
+  // CTA's own publish, which follows its accumulator reads (RW_CL_DEBUG bit 128 disables)
+  const bool fz = crit && P::kPlanes == 2 && !(p.debug & 128);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -719,6 +753,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     // ================= MMA issuers (whole warps, elected lane issues); j = half of the k-blocks
     const int j = warp == 3 ? 1 : 0;
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
+    const uint32_t idesc2 = idesc_make(P::kFmt, false, false, kTileM, 2 * N);
     mbar_wait(S.a_full, 0);
     if constexpr (P::kPlanes == 2) mbar_wait(S.alo_full, 0);
     tc_fence_after();
@@ -729,7 +764,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_empty[ab], ((t >> 1) - 1) & 1);
         tc_fence_after();
       }
-      cl_mma_step<P>(S, p, t, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, p.stages, N, j, tmem_alo);
+      cl_mma_step<P>(S, p, t, tmem_base + (fz ? j * 2 * N : (ab * 2 + j) * N), nkb, idesc, pc, p.stages, N, j,
+                     tmem_alo, fz, idesc2);
       umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
@@ -785,8 +821,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         mbar_wait(&S.tmem_full[t & 1], (t >> 1) & 1);
         tc_fence_after();
         if (et == 0) cl_trace(p, t, 2);
-        const uint32_t tacc = tmem_base + (t & 1) * 2 * N;
-        cl_fwd_sum<P, kCC, kKind>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p, p.unscale);
+        const uint32_t tacc = tmem_base + (fz ? 0 : (t & 1) * 2 * N);
+        cl_fwd_sum<P, kCC, kKind>(S, tacc, two, N, t, m, kc, nco, rxc, (uint32_t)t, &p, p.unscale, fz);
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
           cl_trace(p, t, 4);
@@ -893,7 +929,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 template <class P, int kChunks, int kKind = kCellLstm>
 __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S, const ClParams& p,
                                             uint32_t tmem_base, bool two, int tile, int m, int ko, uint32_t* consumed,
-                                            bool sys, uint32_t flag_target) {
+                                            bool sys, uint32_t flag_target, bool fz) {
   const int et = threadIdx.x - kEpiBase, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = (warp - 4) >> 2, row = q * 32 + lane;
   const int N = p.Bp, kc = p.kc, nco = N / kc;
@@ -993,7 +1029,8 @@ __device__ __forceinline__ void cl_bwd_crit(const BwdLayer& Ly, const ClSmem& S,
     tc_fence_after();
     if (et == 0) cl_trace(p, it, 2);
     float acc[kC];
-    cl_reduce<P, kChunks>(S, tmem_base + (it & 1) * 2 * N, have, two, N, it, m, kc, nco, rxc, acc, p.unscale, &p);
+    cl_reduce<P, kChunks>(S, tmem_base + (fz ? 0 : (it & 1) * 2 * N), have, two, N, it, m, kc, nco, rxc, acc, p.unscale,
+                          &p, fz);
     if (et == 0) cl_trace(p, it, 12);
     float dab[kC];  // d_above: W_{l+1}^T dG_{l+1,t} (off cluster) or dy (top layer)
     if (off) {
@@ -1240,6 +1277,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int nkb = kb_hi - kb_lo;
   const bool two = nkb - cl_half0(nkb) > 0;  // the second issuer accumulated something
   const int nco = N / n_act;
+  // critical fp16x2 CTAs fuse A_hi.B_hi and A_hi.B_lo into one N = 2N MMA (cl_mma_step): each
+  // issuer's accumulator is 2N wide and there is one step buffer -- the next step's MMAs need this
+  // CTA's own publish, which follows its accumulator reads (RW_CL_DEBUG bit 128 disables)
+  const bool fz = crit && P::kPlanes == 2 && !(p.debug & 128);
   const int n_it = crit ? p.T + 1 : p.T;
 
   extern __shared__ uint8_t smem_raw[];
@@ -1299,6 +1340,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   } else if (active && (warp == 1 || warp == 3)) {
     const int j = warp == 3 ? 1 : 0;
     const uint32_t idesc = idesc_make(P::kFmt, false, false, kTileM, N);
+    const uint32_t idesc2 = idesc_make(P::kFmt, false, false, kTileM, 2 * N);
     mbar_wait(S.a_full, 0);
     if constexpr (P::kPlanes == 2) mbar_wait(S.alo_full, 0);
     tc_fence_after();
@@ -1311,7 +1353,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         tc_fence_after();
       }
       if (!crit || t <= p.T - 2)
-        cl_mma_step<P>(S, p, it, tmem_base + (ab * 2 + j) * N, nkb, idesc, pc, stages, N, j, tmem_alo);
+        cl_mma_step<P>(S, p, it, tmem_base + (fz ? j * 2 * N : (ab * 2 + j) * N), nkb, idesc, pc, stages, N, j,
+                       tmem_alo, fz, idesc2);
       umma_commit_warp(&S.tmem_full[ab]);
     }
   } else if (active && warp >= 4) {
@@ -1328,7 +1371,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         default: cl_off_loop<P, 1>(S, p, tmem_base, two, n_it, m, n_act, ring, done, consumed, sys, epoch, Og.unscale); break;
       }
     } else {
-      cl_bwd_crit<P, kCC, kKind>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target);
+      cl_bwd_crit<P, kCC, kKind>(Ly, S, p, tmem_base, two, tile, m, ko, consumed, sys, flag_target, fz);
     }
   }
   cl_teardown(tmem_base, tmem_cols);
