@@ -291,6 +291,11 @@ struct rw_ctx {
   bool pair_f = false;                       // stepwise forward as CTA pairs (k_lstm_fwd<bf16, true>)
   bool pair_b = false;                       // persistent backward as CTA pairs (k_lstm_bwd<bf16, true>)
   bool ls_pers_f = false, ls_pers_b = false;  // layer-sequential: one persistent launch per layer
+  // stepwise forward with batched input projections (large H): W_l . X_l for blocks of fwd_batch
+  // steps as one GEMM into the gates tape (layer 0: all steps at once), the step kernels then
+  // stream only R (FwdLayer::zx); descriptors [layer 0][layer l >= 1 x block]
+  int fwd_batch = 0;
+  DevBuf gemm_fb;
   bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
@@ -864,6 +869,16 @@ void build(rw_ctx* x) {
   }
   x->fwd_sched = pf.sched;
   x->ks_f = pf.ks;
+  if (pf.sched == RW_SCHED_STEPWISE && !ls && x->kind == kCellLstm) {
+    // measured default (profiles/r02/README.md): blocks of 4 steps from H = 1024 up at batch <= 64
+    // (C2048 forward 5.97 -> 5.84 ms). At config E's batch of 256 the fp32 W.x tape a block
+    // writes and the steps re-read (8 MB per layer-step) costs nearly what it saves in streamed W,
+    // and the GEMMs take the SMs the wavefront's step kernels need: 18.9 -> 33.0 ms, so off.
+    // RW_FWD_BATCH=s overrides, 0 disables
+    x->fwd_batch = Hp >= 1024 && Bp <= 64 ? 4 : 0;
+    if (const char* e = getenv("RW_FWD_BATCH")) x->fwd_batch = std::max(0, atoi(e));
+    x->fwd_batch = std::min(x->fwd_batch, T);
+  }
   x->res_f = pf.resident;
   x->st_f = pf.stages;
   x->smem_f = pf.smem;
@@ -997,7 +1012,7 @@ void build(rw_ctx* x) {
   int m_xK2 = 0;  // CTA-pair forward: Bp/2-row boxes (bf16: one plane)
   std::vector<int> m_hopK2(L), m_dgK2(L);
   // layer-sequential GEMMs: B operands (layer inputs / dG) as K-major boxes of bn_ls columns
-  x->bn_ls = x->prec == kBF16 ? 256 : 64;  // tf32: the chunked-promotion GEMM variant
+  x->bn_ls = x->prec == kBF16 ? 256 : x->prec == kF16x2 ? 128 : 64;  // tf32: the chunked-promotion GEMM variant
   int m_xLS[2] = {0, 0};
   std::vector<int> m_hopLS(2 * L), m_dgLS(2 * L);
   std::vector<int> m_dgT(2 * L), m_hT(2 * L);
@@ -1035,7 +1050,7 @@ void build(rw_ctx* x) {
     m_xMN[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, aK));
     m_w0t[p] = add_map(x, make_map(x->w0t.p(p), prec, G4p, Ip, aK, kTileM));
     m_dg0dx[p] = add_map(x, make_map(x->dgop[0].p(p), prec, G4p, colsT, aK, gemm_box_rows(x->bn_dx)));
-    if (ls) {
+    if (ls || x->fwd_batch) {
       m_xLS[p] = add_map(x, make_map(x->x_op.p(p), prec, Ip, colsT, aK, gemm_box_rows(x->bn_ls)));
       for (int l = 0; l < L; ++l) {
         m_hopLS[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, gemm_box_rows(x->bn_ls)));
@@ -1069,7 +1084,7 @@ void build(rw_ctx* x) {
     F.gates = x->gates[l].f();
     F.tanhc = x->tanhc[l].f();
     F.flags = ff + (size_t)l * T;
-    F.zx = ls ? x->gates[l].f() : nullptr;  // the input GEMM writes W.x into the gates tape
+    F.zx = ls || x->fwd_batch ? x->gates[l].f() : nullptr;  // the input GEMM writes W.x into the gates tape
     F.bx2 = x->pair_f ? MD + (l == 0 ? m_xK2 : m_hopK2[l - 1]) : nullptr;
     F.bh2 = x->pair_f ? MD + m_hopK2[l] : nullptr;
     F.alo = f16x2 ? static_cast<const uint16_t*>(x->wf[l].p(1)) : nullptr;
@@ -1301,6 +1316,43 @@ void build(rw_ctx* x) {
     x->gemm_lsb.alloc(sizeof(GemmDesc) * L);
     RW_CUDA(cudaMemcpy(x->gemm_lsf.p, lf.data(), sizeof(GemmDesc) * L, cudaMemcpyHostToDevice));
     RW_CUDA(cudaMemcpy(x->gemm_lsb.p, lb.data(), sizeof(GemmDesc) * L, cudaMemcpyHostToDevice));
+  }
+  if (x->fwd_batch) {  // batched input projections of the stepwise forward (run_forward_rec)
+    const int sb = x->fwd_batch, nb = ceil_div(T, sb);
+    std::vector<GemmDesc> fb;
+    for (int l = 0; l < L; ++l) {
+      const int Ipl = l == 0 ? Ip : Hp;
+      GemmDesc f{};
+      f.error = static_cast<int*>(x->errflag.p);
+      for (int p = 0; p < 2; ++p) {
+        const int q = p % x->planes;
+        f.a[p] = mp(m_wf[2 * l + q], p);
+        f.b[p] = l == 0 ? mp(m_xLS[q], p) : mp(m_hopLS[2 * (l - 1) + q], p);
+      }
+      f.M = (int)G4p;
+      f.K = Ipl;
+      f.ldd = G4p;
+      f.row_mode = kRowGatePad;
+      f.col_mode = kColIdentity;
+      f.H = H;
+      f.Hp = Hp;
+      f.B = B;
+      f.Bp = Bp;
+      f.m_valid = (int)G4p;
+      // fp16x2: the operand planes carry 2^kWScaleLog2 x (2^kXScaleLog2 | 2^kHScaleLog2)
+      f.alpha = x->prec == kF16x2 ? pow2f(-(kWScaleLog2 + (l == 0 ? kXScaleLog2 : kHScaleLog2))) : 1.0f;
+      for (int b = 0; b < (l == 0 ? 1 : nb); ++b) {
+        GemmDesc g = f;
+        const int c0 = l == 0 ? 0 : b * sb, nc = l == 0 ? T : std::min(sb, T - c0);
+        g.N = nc * Bp;
+        g.n_valid = nc * Bp;
+        g.b_n_off = (l == 0 ? 0 : Bp) + c0 * Bp;  // h_{l-1,t} is column block t+1
+        g.d = x->gates[l].f() + (size_t)c0 * Bp * G4p;
+        fb.push_back(g);
+      }
+    }
+    x->gemm_fb.alloc(sizeof(GemmDesc) * fb.size());
+    RW_CUDA(cudaMemcpy(x->gemm_fb.p, fb.data(), sizeof(GemmDesc) * fb.size(), cudaMemcpyHostToDevice));
   }
   x->gemm_wg.alloc(sizeof(GemmDesc) * wg.size());
   RW_CUDA(cudaMemcpy(x->gemm_wg.p, wg.data(), sizeof(GemmDesc) * wg.size(), cudaMemcpyHostToDevice));
@@ -1677,6 +1729,34 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
   rp.n_steps = 1;
   RW_CUDA(cudaEventRecord(x->fork_ev, s));
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->fork_ev, 0));
+  if (x->fwd_batch) {
+    // blocks of sb steps: layer l's input GEMM for block b waits for layer l-1's block b, then the
+    // block's step kernels (K = Hp: R only) follow on the layer's stream; layer 0's input
+    // projection covers every step in one GEMM
+    const int sb = x->fwd_batch, nb = ceil_div(x->T, sb);
+    const GemmDesc* FB = static_cast<const GemmDesc*>(x->gemm_fb.p);
+    const int st = gemm_stages(x->planes, x->bn_ls);
+    launch_gemm<P, false, false>(FB, 1, 4 * x->Hp, x->Bp * x->T, x->bn_ls, st, x->ls[0]);
+    for (int b = 0; b < nb; ++b) {
+      const int t0 = b * sb, t1 = std::min(x->T, t0 + sb);
+      for (int l = 0; l < x->L; ++l) {
+        if (l > 0) {
+          RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l - 1], 0));
+          launch_gemm<P, false, false>(FB + 1 + (size_t)(l - 1) * nb + b, 1, 4 * x->Hp, x->Bp * (t1 - t0), x->bn_ls, st,
+                                       x->ls[l]);
+        }
+        rp.layer_base = l;
+        for (int t = t0; t < t1; ++t) {
+          rp.t_first = t;
+          if (x->tracing) rp.trace = x->trace_f.u64() + (size_t)(l * x->T + t) * rp.tiles * rp.ksplit * 8;
+          launch_rec<P>(kern, x->fwd_layers.p, rp, rp.tiles * rp.ksplit, 1, x->smem_f, x->ls[l], x->pair_f ? 2 : 0);
+        }
+        RW_CUDA(cudaEventRecord(x->lev[l], x->ls[l]));
+      }
+    }
+    for (int l = 0; l < x->L; ++l) RW_CUDA(cudaStreamWaitEvent(s, x->lev[l], 0));
+    return;
+  }
   for (int t = 0; t < x->T; ++t) {
     for (int l = 0; l < x->L; ++l) {
       if (l > 0) RW_CUDA(cudaStreamWaitEvent(x->ls[l], x->lev[l - 1], 0));

@@ -306,3 +306,22 @@ def test_device_trace_honours_wavefront_edges(tmp_path, monkeypatch, schedule, p
         hdr = f.readline().strip()
     assert hdr == "task_layer,task_block,phase,worker,start_ns,end_ns"
     assert vt.validate(str(path), L, T, "fwd", slack_ns=64) is None
+
+
+# stepwise forward with batched input projections (runtime.cu fwd_batch: W_l . X_l for blocks of
+# s steps as one GEMM into the gates tape, the step kernels then stream only R); the default
+# switches it on from H = 1024, RW_FWD_BATCH forces it here at small shapes, incl. a block count
+# that does not divide T and a ragged batch
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("dims,s", [(Dims(3, 96, 40, 20, 10), 4), (Dims(2, 130, 70, 33, 5), 2),
+                                    (Dims(2, 256, 256, 64, 7), 3)],
+                         ids=["L3H96s4", "L2H130s2", "L2H256s3"])
+def test_stepwise_batched_input(reference, monkeypatch, precision, dims, s):
+    from paper_1604_01946_b200 import Engine
+    monkeypatch.setenv("RW_FWD_BATCH", str(s))
+    c, params, x, dy, h0, c0 = make_case(dims, seed=9, bias=True, state=True)
+    eng = Engine(c, precision=precision, schedule="stepwise")
+    assert eng.describe()["fwd_schedule"] == "stepwise"
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), precision)
