@@ -82,6 +82,36 @@ __device__ __forceinline__ void f16x2_split(float v, __half& hi, __half& lo) {
   lo = __float2half_rn(v - __half2float(hi));
 }
 
+// fp32-parity activations without libm's slow paths (cluster forward epilogue): 2^t by MUFU.EX2
+// (relative error ~2^-22, plus |t| 2^-24 from rounding t), the reciprocal by MUFU.RCP + one Newton
+// step; tanh below |x| = 0.6 by an odd polynomial (least-squares fit, 7.6e-8 relative in fp32),
+// where 1 - 2/(1+e^2x) would cancel. Within a few fp32 ulps of expf / tanhf.
+__device__ __forceinline__ float ex2_approx(float t) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
+  return y;
+}
+__device__ __forceinline__ float rcp_newton(float d) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  return fmaf(r, fmaf(-d, r, 1.0f), r);
+}
+__device__ __forceinline__ float sigmoid_fast(float x) {
+  return rcp_newton(1.0f + ex2_approx(fminf(-1.4426950408889634f * x, 126.0f)));
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float ax = fabsf(x);
+  const float z = x * x;
+  float p = -0.005984960589557886f;
+  p = fmaf(p, z, 0.020868148654699326f);
+  p = fmaf(p, z, -0.053803566843271255f);
+  p = fmaf(p, z, 0.13332132995128632f);
+  p = fmaf(p, z, -0.3333330452442169f);
+  const float small = fmaf(x * z, p, x);
+  const float r = 1.0f - 2.0f * rcp_newton(1.0f + ex2_approx(fminf(2.8853900817779268f * ax, 126.0f)));
+  return ax < 0.6f ? small : copysignf(r, x);
+}
+
 // Cell kinds (rw_config.cell_kind, the reference's CellKind order): the cluster kernels are
 // instantiated per class -- LSTM, GRU, RNN (tanh / relu selected at run time).
 enum CellKindDev : int { kCellRnnTanh = 0, kCellRnnRelu = 1, kCellGru = 2, kCellLstm = 3 };
