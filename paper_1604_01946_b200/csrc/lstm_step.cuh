@@ -183,11 +183,12 @@ __device__ __forceinline__ void store_operand(void* const* planes, long long idx
 
 // Activations (the reference's definitions: sigmoid = 1/(1+exp(-x)), cells.hpp:30; tanh).
 // bf16 mode: the SFU approximations (relative error ~2^-11, far below the bf16 operand rounding
-// it already carries). fp32-parity mode: the accurate libm chain (expf, IEEE division, tanhf),
-// as the reference computes it. Measured alternatives (profiles/r02/README.md): MUFU.EX2 on a
-// range-reduced argument with an rcp.approx + Newton reciprocal was accurate enough but the
-// cell phase got slower (4.9-5.3 vs 3.3 us at config B), and tanh(x) = 1 - 2/(1 + e^{2x}) without
-// a small-|x| branch broke the 1e-5 contract (2e-5 normwise).
+// it already carries). fp32-parity mode: MUFU.EX2 + MUFU.RCP with a Newton step and a polynomial
+// for |tanh| below 0.6 (common.cuh sigmoid_fast / tanh_fast, a few fp32 ulps from expf / tanhf):
+// libm's expf, IEEE division and tanhf cost ~150 instructions per cell element and were half the
+// cluster forward's cell phase (2.7 -> 1.3 us, profiles/r02/README.md). An earlier attempt kept
+// both paths in one binary and measured no gain -- the code size hid it. tanh(x) = 1 - 2/(1+e^2x)
+// without the small-|x| branch breaks the 1e-5 contract (2e-5 normwise).
 template <class P>
 __device__ __forceinline__ float act_sigmoid(float x) {
   if constexpr (P::kPlanes == 1) {
@@ -196,7 +197,7 @@ __device__ __forceinline__ float act_sigmoid(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(0.5f * x));
     return fmaf(0.5f, y, 0.5f);
   } else {
-    return 1.0f / (1.0f + expf(-x));
+    return sigmoid_fast(x);
   }
 }
 template <class P>
@@ -206,7 +207,7 @@ __device__ __forceinline__ float act_tanh(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
   } else {
-    return tanhf(x);
+    return tanh_fast(x);
   }
 }
 

@@ -839,28 +839,14 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             const float af = lds_f32(sk + 1 * 32) + bf;
             const float ao = lds_f32(sk + 2 * 32) + bo;
             const float ac = lds_f32(sk + 3 * 32) + bc;
-            // fp16x2 (fp32-parity): MUFU.EX2 + MUFU.RCP with a Newton step and a polynomial for
-            // small |tanh| (common.cuh sigmoid_fast / tanh_fast: a few fp32 ulps of expf / tanhf)
-            // -- libm's expf / division / tanhf cost ~150 instructions per cell element and
-            // dominated the cell phase (profiles/r02/README.md); bf16: MUFU.TANH
-            if constexpr (P::kPlanes == 2) {
-              iv[k] = sigmoid_fast(ai);
-              fv[k] = sigmoid_fast(af);
-              ov[k] = sigmoid_fast(ao);
-              cb[k] = tanh_fast(ac);
-            } else {
-              iv[k] = act_sigmoid<P>(ai);
-              fv[k] = act_sigmoid<P>(af);
-              ov[k] = act_sigmoid<P>(ao);
-              cb[k] = act_tanh<P>(ac);
-            }
+            iv[k] = act_sigmoid<P>(ai);  // fp32-parity: libm-free (lstm_step.cuh)
+            fv[k] = act_sigmoid<P>(af);
+            ov[k] = act_sigmoid<P>(ao);
+            cb[k] = act_tanh<P>(ac);
             const float t1 = fv[k] * creg[k];
             const float t2 = iv[k] * cb[k];
             creg[k] = t1 + t2;  // c_t
-            if constexpr (P::kPlanes == 2)
-              tcv[k] = tanh_fast(creg[k]);
-            else
-              tcv[k] = act_tanh<P>(creg[k]);
+            tcv[k] = act_tanh<P>(creg[k]);
             hv[k] = ov[k] * tcv[k];
           } else if constexpr (kKind == kCellGru) {  // cells.hpp:294-313 operation order
             const float ar = lds_f32(sk + 0 * 32) + bi;
