@@ -111,11 +111,10 @@ struct ClParams {
                   // 2^-(kWScaleLog2 + kGScaleLog2) backward (R^T.dG); off groups: ClOff::unscale
   unsigned* gmax; // backward: max |dG| of the pass (float bits; range check of the scaled dG planes)
   int kind;       // cell kind (CellKindDev): the RNN variants share one instantiation
-  int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 512 = fp16x2 forward
-              // without the lo-plane stores, 1 = skip fwd tapes,
+  int debug;  // RW_CL_DEBUG bits. Timing experiments (results invalid): 1 = skip fwd tapes,
               // 4 = skip bwd tape loads, 8 = skip bwd operand stores. Variants (results valid):
-              // 16 = forward h operand staged in smem, 32 = backward dG operand stored scattered,
-              // 64 = operand k-blocks copied one per bulk copy (not in pairs)
+              // 32 = backward dG operand stored scattered, 64 = operand k-blocks copied one per
+              // bulk copy (not in pairs), 128 = critical fp16x2 CTAs without the fused N = 2N MMA
 };
 
 // Shared-memory carve-up (identical for every CTA of a launch, so a local address mapped with
