@@ -324,6 +324,9 @@ struct rw_ctx {
   // as soon as that layer's weight-gradient GEMMs finish, while the lower layers' GEMMs and dx0 run
   bool dp_overlap = false;
   cudaStream_t comm_s = nullptr;
+  // the dx0 GEMM runs on its own stream beside the weight-gradient GEMMs (fills their last wave)
+  cudaStream_t tail_s = nullptr;
+  cudaEvent_t ev_tail_fork = nullptr, ev_tail_join = nullptr;
   std::vector<cudaEvent_t> ev_layer;
   cudaEvent_t ev_comm = nullptr;
   cudaEvent_t ev_fwd = nullptr, ev_x = nullptr, ev_y_staged = nullptr, ev_y_out = nullptr, ev_dy = nullptr,
@@ -1404,6 +1407,9 @@ void build(rw_ctx* x) {
     }
   }
   RW_CUDA(cudaEventCreateWithFlags(&x->fork_ev, cudaEventDisableTiming));
+  RW_CUDA(cudaStreamCreateWithFlags(&x->tail_s, cudaStreamNonBlocking));
+  RW_CUDA(cudaEventCreateWithFlags(&x->ev_tail_fork, cudaEventDisableTiming));
+  RW_CUDA(cudaEventCreateWithFlags(&x->ev_tail_join, cudaEventDisableTiming));
   if (const char* e = getenv("RW_NO_GRAPHS")) x->use_graphs = atoi(e) == 0;
   if (const char* e = getenv("RW_TRACE")) x->trace_path = e;
   if (const char* e = getenv("RW_TRACE_SPANS")) x->trace_spans_path = e;
@@ -2120,13 +2126,25 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
     PhaseTimer pt(x, 5, s);
     run_db(x, s);
   }
-  {
-    PhaseTimer pt(x, 3, s);
+  // dx0 and the weight gradients are independent: dx0 on its own stream fills the weight
+  // GEMMs' last wave (RW_SERIAL_TAIL=1, and profiling mode, keep them in sequence)
+  static const bool serial_tail = getenv("RW_SERIAL_TAIL") && atoi(getenv("RW_SERIAL_TAIL")) != 0;
+  if (!x->profiling && !serial_tail) {
+    RW_CUDA(cudaEventRecord(x->ev_tail_fork, s));
+    RW_CUDA(cudaStreamWaitEvent(x->tail_s, x->ev_tail_fork, 0));
+    run_dx0<P>(x, x->tail_s);
     run_weight_grads<P>(x, s);
-  }
-  {
-    PhaseTimer pt(x, 4, s);
-    run_dx0<P>(x, s);
+    RW_CUDA(cudaEventRecord(x->ev_tail_join, x->tail_s));
+    RW_CUDA(cudaStreamWaitEvent(s, x->ev_tail_join, 0));
+  } else {
+    {
+      PhaseTimer pt(x, 3, s);
+      run_weight_grads<P>(x, s);
+    }
+    {
+      PhaseTimer pt(x, 4, s);
+      run_dx0<P>(x, s);
+    }
   }
   if (!overlap) {
     PhaseTimer pt(x, 5, s);
@@ -2278,6 +2296,9 @@ rw_ctx::~rw_ctx() {
   for (auto s : ls) cudaStreamDestroy(s);
   for (auto e : lev) cudaEventDestroy(e);
   if (fork_ev) cudaEventDestroy(fork_ev);
+  if (tail_s) cudaStreamDestroy(tail_s);
+  if (ev_tail_fork) cudaEventDestroy(ev_tail_fork);
+  if (ev_tail_join) cudaEventDestroy(ev_tail_join);
   if (main) cudaStreamDestroy(main);
   if (cp_in) cudaStreamDestroy(cp_in);
   if (cp_out) cudaStreamDestroy(cp_out);
