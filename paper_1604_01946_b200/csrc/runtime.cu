@@ -2129,10 +2129,13 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
   // dx0 and the weight gradients are independent: dx0 on its own stream fills the weight
   // GEMMs' last wave (RW_SERIAL_TAIL=1, and profiling mode, keep them in sequence)
   static const bool serial_tail = getenv("RW_SERIAL_TAIL") && atoi(getenv("RW_SERIAL_TAIL")) != 0;
+  bool db_done = overlap;
   if (!x->profiling && !serial_tail) {
     RW_CUDA(cudaEventRecord(x->ev_tail_fork, s));
     RW_CUDA(cudaStreamWaitEvent(x->tail_s, x->ev_tail_fork, 0));
     run_dx0<P>(x, x->tail_s);
+    if (!db_done) run_db(x, x->tail_s);  // the bias-gradient reduction too
+    db_done = true;
     run_weight_grads<P>(x, s);
     RW_CUDA(cudaEventRecord(x->ev_tail_join, x->tail_s));
     RW_CUDA(cudaStreamWaitEvent(s, x->ev_tail_join, 0));
@@ -2147,8 +2150,10 @@ void enqueue_pass_body(rw_ctx* x, int pass, cudaStream_t s) {
     }
   }
   if (!overlap) {
-    PhaseTimer pt(x, 5, s);
-    run_db(x, s);
+    if (!db_done) {
+      PhaseTimer pt(x, 5, s);
+      run_db(x, s);
+    }
   } else {  // join: the pass completes when the last bucket is summed
     RW_CUDA(cudaEventRecord(x->ev_comm, x->comm_s));
     RW_CUDA(cudaStreamWaitEvent(s, x->ev_comm, 0));
