@@ -374,6 +374,42 @@ __global__ void k_pad_swizzle_bf16(const float* __restrict__ src, int R, int B, 
   }
 }
 
+// fp16x2 counterpart of k_pad_swizzle_bf16 (cluster schedule, fp32-parity): the layer-0 input
+// x (R x B*T, column-major fp32) -> both scaled operand planes (Rp x Bp*T) and their pre-swizzled
+// step image ([hi rows | lo rows] per k-block, as k_swizzle_op writes it) in one pass; records
+// max|x| for the range check of the scaled planes.
+__global__ void k_pad_swizzle_f16x2(const float* __restrict__ src, int R, int B, int T, int Rp, int Bp,
+                                    __half* __restrict__ hi, __half* __restrict__ lo, uint8_t* __restrict__ sw,
+                                    float f16scale, unsigned* amax) {
+  const int kc = Rp >> 3;
+  const long long total = (long long)kc * Bp * T;
+  float mx = 0.0f;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long col = e / kc;
+    const int k = (int)(e - col * kc) << 3;
+    const int t = (int)(col / Bp), b = (int)(col - (long long)t * Bp);
+    __align__(16) __half vh[8];
+    __align__(16) __half vl[8];
+    const float* sc = src + ((long long)t * B + b) * R;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float v = (b < B && k + j < R) ? sc[k + j] : 0.0f;
+      mx = fmaxf(mx, fabsf(v));
+      f16x2_split(v * f16scale, vh[j], vl[j]);
+    }
+    const uint4 qh = *reinterpret_cast<const uint4*>(vh), ql = *reinterpret_cast<const uint4*>(vl);
+    *reinterpret_cast<uint4*>(hi + col * Rp + k) = qh;
+    *reinterpret_cast<uint4*>(lo + col * Rp + k) = ql;
+    uint8_t* blk = sw + (long long)t * Rp * Bp * 2 * 2;
+    *reinterpret_cast<uint4*>(blk + sw_off(k, b, 2 * Bp)) = qh;
+    *reinterpret_cast<uint4*>(blk + sw_off(k, Bp + b, 2 * Bp)) = ql;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.0f && amax) atomicMax(amax, __float_as_uint(mx));
+}
+
 // All layers' bias-gradient reductions in one launch (blockIdx.y = layer within the group).
 constexpr int kDbGroup = 16;
 struct DbGroup {

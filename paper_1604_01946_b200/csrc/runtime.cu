@@ -1572,13 +1572,18 @@ void forward_prologue(rw_ctx* x, cudaStream_t s, const float* h0_dev, const floa
   if (x->prec == kF16x2 && (inputs || state))
     RW_CUDA(cudaMemsetAsync(static_cast<unsigned*>(x->errflag.p) + (inputs ? 3 : 4), 0, inputs && state ? 8 : 4, s));
   // cluster schedule (bf16): the plain operand and its swizzled image in one pass
-  const bool fused_x = inputs && !x->pp_prev && x->fwd_sched == RW_SCHED_CLUSTER && x->prec == kBF16 &&
-                       x->Ip % 8 == 0;
-  if (fused_x) {
+  const bool fused_x = inputs && !x->pp_prev && x->fwd_sched == RW_SCHED_CLUSTER &&
+                       (x->prec == kBF16 || x->prec == kF16x2) && x->Ip % 8 == 0;
+  if (fused_x && x->prec == kBF16) {
     ++g_launches;
     k_pad_swizzle_bf16<<<grid_for((long long)x->Ip / 8 * Bp * x->T), 256, 0, s>>>(
         x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, static_cast<__nv_bfloat16*>(x->x_op.p(0)),
         static_cast<uint8_t*>(x->xsw.p));
+  } else if (fused_x) {
+    ++g_launches;
+    k_pad_swizzle_f16x2<<<grid_for((long long)x->Ip / 8 * Bp * x->T), 256, 0, s>>>(
+        x->x_raw.f(), x->I, B, x->T, x->Ip, Bp, static_cast<__half*>(x->x_op.p(0)), static_cast<__half*>(x->x_op.p(1)),
+        static_cast<uint8_t*>(x->xsw.p), pow2f(kXScaleLog2), static_cast<unsigned*>(x->errflag.p) + 3);
   } else if (inputs && !x->pp_prev) {  // a pipeline stage's layer input is written by the previous stage
     ++g_launches;
     k_pad_cols<<<pad_grid((long long)x->Ip * Bp * x->T), 256, 0, s>>>(
