@@ -325,3 +325,21 @@ def test_stepwise_batched_input(reference, monkeypatch, precision, dims, s):
     dev = run_device(eng, params, x, dy, h0, c0)
     ref = run_reference(reference, c, params, x, dy, h0, c0)
     assert_within(compare(dev, ref, c), precision)
+
+
+# fp32-parity operand range (common.cuh: |x| < 4096 for the scaled fp16x2 planes): the pad kernels
+# record max|x| (incl. the fused pad + swizzle of the cluster schedule) and the sync reports it
+@pytest.mark.parametrize("schedule", ["cluster", "persistent"])
+def test_fp16x2_input_range_is_reported(schedule):
+    from paper_1604_01946_b200 import Engine
+    c, params, x, dy, h0, c0 = make_case(Dims(2, 64, 64, 16, 4), seed=3)
+    eng = make_engine(Engine, c, "fp32", schedule)
+    eng.set_params(params)
+    big = np.asfortranarray(x * np.float32(1e5))
+    with pytest.raises(RuntimeError, match="exceeds the fp16x2 operand range"):
+        eng.forward(params, big, True)
+        eng.sync()
+    # a pass within range is fine again afterwards
+    eng2 = make_engine(Engine, c, "fp32", schedule)
+    dev = run_device(eng2, params, x, dy, h0, c0)
+    assert np.isfinite(dev["y"]).all()
