@@ -182,17 +182,19 @@ __global__ void __launch_bounds__(256) k_repack(const RepackJob* __restrict__ jo
   const long long GH = (long long)G * H;
   if (J.kind == kRepackT) {
     const int g = rho_gate(r0), u = rho_unit(r0) + lane;
-    const bool rok = u < H && g < G;
+    // GRU (G = 3, linear before reset): the candidate gate's two halves go to different slots --
+    // W_n in slot 2 of the W columns, R_n in slot 3 of the R columns -- so any kernel that sums
+    // [W|R].[x;h] over K keeps W_n x (slot 2) and R_n h (slot 3) apart for the reset gate
+    const int gr = G == 3 ? (g == 3 ? 2 : g == 2 ? 3 : g) : g;  // source gate of the R columns
+    const bool wok = u < H && g < G, rok = u < H && gr < G && !(G == 3 && g == 2);
 #pragma unroll
     for (int i = 0; i < kRepackTileK / 8; ++i) {
       const int kk = w + 8 * i, k = k0 + kk;
       float v = 0.0f;
-      if (rok) {
-        if (k < J.k_split) {
-          if (k < J.src_k0) v = J.s0[(long long)k * GH + (long long)g * H + u];
-        } else if (k - J.k_split < H) {
-          v = J.s1[(long long)(k - J.k_split) * GH + (long long)g * H + u];
-        }
+      if (k < J.k_split) {
+        if (wok && k < J.src_k0) v = J.s0[(long long)k * GH + (long long)g * H + u];
+      } else if (rok && k - J.k_split < H) {
+        v = J.s1[(long long)(k - J.k_split) * GH + (long long)gr * H + u];
       }
       tile[kk * 32 + (lane ^ ((kk >> 2) & 31))] = v;
     }

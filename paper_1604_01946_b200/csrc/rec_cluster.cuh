@@ -612,7 +612,7 @@ __device__ __forceinline__ void cl_fetch_off(const ClSmem& S, const ClParams& p,
 // grid (tiles * 2 * cs, L), cluster (cs, 1, 1). Cluster c: tile c/2, role c%2 (0 critical
 // R.h_{t-1}, 1 off W.x_t). Member m < kc (critical) / m < ko_l (off) is active.
 // GRU (linear before reset, cells.hpp:283-333): the candidate gate keeps its two halves apart --
-// rows of gate slot 2 get W_n x, rows of the unused slot 3 get R_n h (written by the slot-2 threads).
+// slot 2 sums to W_n x and slot 3 to R_n h (the repacked image holds W_n and R_n in those slots).
 template <class P, int kChunks, int kKind = kCellLstm>
 __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool two, int N, int t, int m, int kc,
                                            int nco, uint32_t& rxc, uint32_t offc, const ClParams* tp, float unscale,
@@ -630,17 +630,8 @@ __device__ __forceinline__ void cl_fwd_sum(const ClSmem& S, uint32_t tacc, bool 
   float zw[kChunks * 8];
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i) zw[i] = lds_f32(S.rxoff + (size_t)(half * kChunks * 8 + i) * kTileM + row);
-  if constexpr (kKind == kCellGru) {
-    if (q == 3) return;
-    if (q == 2) {
-#pragma unroll
-      for (int i = 0; i < kChunks * 8; ++i) {
-        sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row, zw[i]);
-        sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row + 32, v[i]);
-      }
-      return;
-    }
-  }
+  // (GRU: the forward image keeps W_n in slot 2 of the W columns and R_n in slot 3 of the R
+  // columns -- layout_kernels.cuh k_repack -- so slot 2 sums to W_n x and slot 3 to R_n h)
 #pragma unroll
   for (int i = 0; i < kChunks * 8; ++i)
     sts_f32(sum + (size_t)(half * kChunks * 8 + i) * kTileM + row, zw[i] + v[i]);  // (zw + zr), cells.hpp:240
