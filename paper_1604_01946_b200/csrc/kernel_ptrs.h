@@ -14,8 +14,10 @@ void* cl_kernel_ptr(int prec, bool fwd, int nco, int kind = kCellLstm);
 void* cl_kernel_ptr_lstm(int prec, bool fwd, int nco);
 void* cl_kernel_ptr_gru(int prec, bool fwd, int nco);
 void* cl_kernel_ptr_rnn(int prec, bool fwd, int nco);
-// k_lstm_fwd / k_lstm_bwd<P, pair> (lstm_step.cuh); prec kBF16, kF16x2 or kTF32x3 (pair: bf16 only)
-void* lstm_kernel_ptr(int prec, bool fwd, bool pair);
+// k_lstm_fwd / k_lstm_bwd<P, pair, kind> (lstm_step.cuh); prec kBF16, kF16x2 or kTF32x3 (pair: bf16
+// LSTM only); GRU / RNN: bf16 or fp16x2, no pairs (kernels_lstm_cells.cu)
+void* lstm_kernel_ptr(int prec, bool fwd, bool pair, int kind = kCellLstm);
+void* lstm_kernel_ptr_cells(int prec, bool fwd, int kind);
 // k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh): bf16 BNV 0; two-plane formats BNV = tile width 64 / 128
 void* gemm_tc_ptr(int prec, bool amn, bool bmn, int bnv);
 // k_gemm_p<AMN, BMN, BN> / k_gemm_p2<AMN, BMN, BN> (bf16), BN 128 or 256

@@ -137,6 +137,7 @@ struct RecParams {
   unsigned long long timeout_ns;
   unsigned int* progress;     // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
   unsigned long long* trace;  // optional [cta][n_steps][8] %globaltimer stamps (RW_TRACE)
+  int kind;                   // cell kind (CellKindDev): the RNN variants share one instantiation
 };
 
 // Trace stamps per (CTA, step): 0 producer starts waiting for its inputs, 1 inputs ready
@@ -565,7 +566,7 @@ __device__ __forceinline__ void mma_kblock(uint32_t acc, uint32_t a_base, uint32
 // tcgen05.mma.cta_group::2 with M = 256; each CTA loads its own 128 A rows and half of the B
 // columns (Bp/2), so per SM a k-block moves 16 + Bp*64 bytes instead of 16K + Bp*128 -- the
 // per-SM operand ingress that bounds the step at large Bp (config E: 3 MB per CTA per step).
-template <class P, bool kPair = false>
+template <class P, bool kPair = false, int kKind = kCellLstm>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_fwd(const FwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
@@ -794,12 +795,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         xchg_publish(S, ks, xc);
         if (et == 0 && n0 == 0) trace_stamp(p, it, 4);
         // cell phase: owned columns cl = cg + 8k, unit j; loads first, then math
-        float cp[8];
+        float cp[8];  // LSTM: c_{t-1}; GRU: h_{t-1} (the direct term u h_{t-1}); RNN: unused
         const long long colb = (long long)t * p.Bp + n0 + rank * nco;  // block t, owned base
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int cl = cg + 8 * k;
-          cp[k] = cl < nco ? Le.c[(colb + cl) * Hp + u] : 0.0f;
+          const float* st = kKind == kCellGru ? Le.h : Le.c;
+          cp[k] = (cl < nco && kKind != kCellRnnTanh) ? st[(colb + cl) * Hp + u] : 0.0f;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -815,32 +817,61 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           }
           const float si = xchg_sum(S, ks, nco, cl, 0 * 32 + j), sf = xchg_sum(S, ks, nco, cl, 1 * 32 + j);
           const float so = xchg_sum(S, ks, nco, cl, 2 * 32 + j), sc = xchg_sum(S, ks, nco, cl, 3 * 32 + j);
-          const float ai = (zxm ? zi + si : si) + bi;
-          const float af = (zxm ? zf + sf : sf) + bf;
-          const float ao = (zxm ? zo + so : so) + bo;
-          const float ac = (zxm ? zc + sc : sc) + bc;
-          const float iv = act_sigmoid<P>(ai);
-          const float fv = act_sigmoid<P>(af);
-          const float ov = act_sigmoid<P>(ao);
-          const float cb = act_tanh<P>(ac);
-          const float t1 = fv * cp[k];
-          const float t2 = iv * cb;
-          const float cv = t1 + t2;
-          const float tcv = act_tanh<P>(cv);
-          const float hv = ov * tcv;
           const long long col_prev = colb + cl;       // block t   (c_{t-1})
           const long long col_new = col_prev + p.Bp;  // block t+1 (c_t, h_t)
-          Le.c[col_new * Hp + u] = cv;
+          float hv;
+          if constexpr (kKind == kCellLstm) {
+            const float ai = (zxm ? zi + si : si) + bi;
+            const float af = (zxm ? zf + sf : sf) + bf;
+            const float ao = (zxm ? zo + so : so) + bo;
+            const float ac = (zxm ? zc + sc : sc) + bc;
+            const float iv = act_sigmoid<P>(ai);
+            const float fv = act_sigmoid<P>(af);
+            const float ov = act_sigmoid<P>(ao);
+            const float cb = act_tanh<P>(ac);
+            const float t1 = fv * cp[k];
+            const float t2 = iv * cb;
+            const float cv = t1 + t2;
+            const float tcv = act_tanh<P>(cv);
+            hv = ov * tcv;
+            Le.c[col_new * Hp + u] = cv;
+            if (Le.gates) {
+              float* gp = Le.gates + col_prev * G4 + u;
+              gp[0] = iv;
+              gp[Hp] = fv;
+              gp[2 * Hp] = ov;
+              gp[3 * Hp] = cb;
+              Le.tanhc[col_prev * Hp + u] = tcv;
+            }
+          } else if constexpr (kKind == kCellGru) {
+            // cells.hpp:294-313; the forward image keeps W_n x in slot 2 and R_n h in slot 3
+            // (layout_kernels.cuh k_repack), so the K-summed accumulator holds both apart
+            const float ar = (zxm ? zi + si : si) + bi;
+            const float au = (zxm ? zf + sf : sf) + bf;
+            const float zwn = zxm ? zo + so : so;
+            const float zrn = zxm ? zc + sc : sc;
+            const float rv = act_sigmoid<P>(ar);
+            const float uv = act_sigmoid<P>(au);
+            const float t1 = zwn + bo;  // W_n x + b_n
+            const float t2 = rv * zrn;
+            const float nv = act_tanh<P>(t1 + t2);
+            const float t3 = uv * cp[k];
+            const float om = 1.0f - uv;
+            const float t4 = om * nv;
+            hv = t3 + t4;
+            if (Le.gates) {
+              float* gp = Le.gates + col_prev * G4 + u;
+              gp[0] = rv;
+              gp[Hp] = uv;
+              gp[2 * Hp] = nv;
+              Le.zrh[col_prev * Hp + u] = zrn;
+            }
+          } else {  // RNN (cells.hpp:200-212)
+            const float a = (zxm ? zi + si : si) + bi;
+            hv = p.kind == kCellRnnRelu ? (a > 0.0f ? a : 0.0f) : act_tanh<P>(a);
+          }
           Le.h[col_new * Hp + u] = hv;
           store_operand<P>(Le.hop, col_new * Hp + u, kF16Ops<P> ? hv * pow2f(kHScaleLog2) : hv);
-          if (Le.gates) {
-            float* gp = Le.gates + col_prev * G4 + u;
-            gp[0] = iv;
-            gp[Hp] = fv;
-            gp[2 * Hp] = ov;
-            gp[3 * Hp] = cb;
-            Le.tanhc[col_prev * Hp + u] = tcv;
-          }
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 5);
         xchg_release(S, ks);
@@ -869,7 +900,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
 // kPair (bf16, ksplit 1, streamed A): CTA pairs as in k_lstm_fwd<_, true>; the leader's
 // tmem_empty barrier collects one arrival per CTA before the next step's MMAs overwrite either
 // CTA's accumulator.
-template <class P, bool kPair = false>
+template <class P, bool kPair = false, int kKind = kCellLstm>
 __global__ void __launch_bounds__(kRecThreads, 1)
     k_lstm_bwd(const BwdLayer* __restrict__ layers, RecParams p) {
   const int l = p.layer_base + blockIdx.y;
@@ -1136,13 +1167,24 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               }
               const long long col = (long long)t * p.Bp + n;
               const float* gp = Le.gates + col * G4 + u;
-              pi[k] = gp[0];
-              pf[k] = gp[Hp];
-              po[k] = gp[2 * Hp];
-              pcb[k] = gp[3 * Hp];
-              ptc[k] = Le.tanhc[col * Hp + u];
-              pcp[k] = Le.c[col * Hp + u];  // c_{t-1}: block t of the c tape
-              dci[k] = (t == p.T - 1) ? 0.0f : Le.carry_c[n * Hp + u];
+              if constexpr (kKind == kCellLstm) {
+                pi[k] = gp[0];
+                pf[k] = gp[Hp];
+                po[k] = gp[2 * Hp];
+                pcb[k] = gp[3 * Hp];
+                ptc[k] = Le.tanhc[col * Hp + u];
+                pcp[k] = Le.c[col * Hp + u];  // c_{t-1}: block t of the c tape
+              } else if constexpr (kKind == kCellGru) {
+                pi[k] = gp[0];                 // r
+                pf[k] = gp[Hp];                // u
+                po[k] = gp[2 * Hp];            // n
+                pcb[k] = Le.zrh[col * Hp + u]; // R_n h_{t-1}
+                pcp[k] = Le.h[col * Hp + u];   // h_{t-1}: block t of the h tape
+              } else {
+                pcp[k] = Le.h[(col + p.Bp) * Hp + u];  // h_t: block t + 1
+              }
+              // LSTM: the cell-state carry dc f; GRU: the direct term dh u (cells.hpp:531)
+              dci[k] = (t == p.T - 1 || kKind == kCellRnnTanh) ? 0.0f : Le.carry_c[n * Hp + u];
               if (dam)
                 dyv[k] = Le.dabove[col * Hp + u];
               else if (Le.dy && u < p.H && n < p.B)
@@ -1153,23 +1195,61 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               const int cl = hh + 2 * (kb8 * 8 + k);
               if (cl >= nco) break;
               const long long n = cbase + cl;
-              if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170)
-                Le.dh0[n * Hp + u] = acc[k];
-                Le.dc0[n * Hp + u] = dci[k];
+              if (t < 0) {  // dh0 / dc0 (engine.hpp:163-170); GRU: dh0 = R^T dgr_0 + dh_0 u_0
+                if constexpr (kKind == kCellGru) {
+                  Le.dh0[n * Hp + u] = acc[k] + dci[k];
+                } else {
+                  Le.dh0[n * Hp + u] = acc[k];
+                  if constexpr (kKind == kCellLstm) Le.dc0[n * Hp + u] = dci[k];
+                }
                 continue;
               }
-              const float dh = (Le.dy || dam) ? dyv[k] + acc[k] : acc[k];  // d_above + carry_h
-              const float q1 = dh * po[k];
-              const float s0 = ptc[k] * ptc[k];
-              const float s1 = 1.0f - s0;
-              const float q2 = q1 * s1;
-              const float dc = dci[k] + q2;
-              const float a1 = dc * pcb[k], a2 = a1 * pi[k], a3 = 1.0f - pi[k];
-              const float b1 = dc * pcp[k], b2 = b1 * pf[k], b3 = 1.0f - pf[k];
-              const float c1 = dh * ptc[k], c2 = c1 * po[k], c3 = 1.0f - po[k];
-              const float d1 = dc * pi[k], d2 = pcb[k] * pcb[k], d3 = 1.0f - d2;
-              const float gi = a2 * a3, gf = b2 * b3, go = c2 * c3, gc = d1 * d3;
-              Le.carry_c[n * Hp + u] = dc * pf[k];
+              // d_above + carry_h (GRU: carry_h = R^T dgr_{t+1} + the direct term dh_{t+1} u_{t+1})
+              const float chh = kKind == kCellGru ? acc[k] + dci[k] : acc[k];
+              const float dh = (Le.dy || dam) ? dyv[k] + chh : chh;
+              float gi, gf = 0.0f, go = 0.0f, gc = 0.0f, rn = 0.0f;  // rn: GRU dgr of the candidate
+              if constexpr (kKind == kCellLstm) {  // cells.hpp:424-447
+                const float q1 = dh * po[k];
+                const float s0 = ptc[k] * ptc[k];
+                const float s1 = 1.0f - s0;
+                const float q2 = q1 * s1;
+                const float dc = dci[k] + q2;
+                const float a1 = dc * pcb[k], a2 = a1 * pi[k], a3 = 1.0f - pi[k];
+                const float b1 = dc * pcp[k], b2 = b1 * pf[k], b3 = 1.0f - pf[k];
+                const float c1 = dh * ptc[k], c2 = c1 * po[k], c3 = 1.0f - po[k];
+                const float d1 = dc * pi[k], d2 = pcb[k] * pcb[k], d3 = 1.0f - d2;
+                gi = a2 * a3;
+                gf = b2 * b3;
+                go = c2 * c3;
+                gc = d1 * d3;
+                Le.carry_c[n * Hp + u] = dc * pf[k];
+              } else if constexpr (kKind == kCellGru) {  // cells.hpp:514-538
+                const float om = 1.0f - pf[k];
+                const float dn = dh * om;
+                const float s = po[k] * po[k];
+                const float s1 = 1.0f - s;
+                const float dnp = dn * s1;
+                const float tt = pcp[k] - po[k];
+                const float q = dh * tt;
+                const float q2 = q * pf[k];
+                const float dgu = q2 * om;
+                const float r0 = dnp * pcb[k];
+                const float r1 = r0 * pi[k];
+                const float r2 = 1.0f - pi[k];
+                gi = r1 * r2;  // dgw = dgr (reset gate)
+                gf = dgu;      // dgw = dgr (update gate)
+                go = dnp;      // dgw (candidate)
+                rn = dnp * pi[k];
+                Le.carry_c[n * Hp + u] = dh * pf[k];
+              } else {  // RNN (cells.hpp:370-383)
+                if (p.kind == kCellRnnRelu) {
+                  gi = pcp[k] > 0.0f ? dh : 0.0f;
+                } else {
+                  const float s = pcp[k] * pcp[k];
+                  const float s1 = 1.0f - s;
+                  gi = dh * s1;
+                }
+              }
               const long long col = (long long)t * p.Bp + n;
               float* dgp = Le.dg + col * G4 + u;
               dgp[0] = gi;
@@ -1181,6 +1261,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               store_operand<P>(Le.dgop, ob + rho_of(1, u), gf * kGS);
               store_operand<P>(Le.dgop, ob + rho_of(2, u), go * kGS);
               store_operand<P>(Le.dgop, ob + rho_of(3, u), gc * kGS);
+              if constexpr (kKind == kCellGru) {  // dgr: r, u as dgw, candidate dnp r (cells.hpp:527-529)
+                float* dgq = Le.dgr + col * G4 + u;
+                dgq[0] = gi;
+                dgq[Hp] = gf;
+                dgq[2 * Hp] = rn;
+                store_operand<P>(Le.dgrop, ob + rho_of(0, u), gi * kGS);
+                store_operand<P>(Le.dgrop, ob + rho_of(1, u), gf * kGS);
+                store_operand<P>(Le.dgrop, ob + rho_of(2, u), rn * kGS);
+                store_operand<P>(Le.dgrop, ob + rho_of(3, u), 0.0f);
+              }
               if constexpr (kF16Ops<P>) gmax = fmaxf(gmax, fmaxf(fmaxf(fabsf(gi), fabsf(gf)), fmaxf(fabsf(go), fabsf(gc))));
               si += gi;
               sf += gf;

@@ -760,14 +760,14 @@ void build(rw_ctx* x) {
       if (!(cl_f && cl_b)) cl_f = cl_b = false;
     }
   }
-  // GRU and vanilla-RNN cells run on the cluster schedule only: their epilogues need the input and
-  // recurrent products apart (GRU's linear-before-reset candidate gate), which is that schedule's
-  // split of roles (rec_cluster.cuh); the other schedules fuse them into one accumulator
-  if (x->kind != kCellLstm && !(cl_f && cl_b))
+  // GRU and vanilla-RNN cells: the cluster schedule keeps the input and recurrent products in
+  // separate roles; the persistent / stepwise kernels sum [W|R].[x;h] over K, and GRU's
+  // linear-before-reset candidate stays apart there through the forward image's slot layout
+  // (W_n in slot 2, R_n in slot 3: layout_kernels.cuh k_repack). Not on the layer-sequential
+  // schedule and not with 3xTF32 operands (LSTM only).
+  if (x->kind != kCellLstm && x->prec == kTF32x3)
     einval(std::string("rnnwave_sm100: ") + (x->kind == kCellGru ? "GRU" : "RNN") +
-           " cells run on the cluster schedule, which does not fit this configuration (batch <= 64, owned "
-           "columns multiple of 16, CTAs and clusters co-resident" +
-           (c.schedule == RW_SCHED_AUTO || c.schedule == RW_SCHED_CLUSTER ? ")" : "; schedule must be auto or cluster)"));
+           " cells do not run on the layer-sequential schedule or with 3xTF32 operands");
   x->planes = prec_planes(x->prec);
   x->elem = prec_elem(x->prec);
   x->atomK = prec_atomk(x->prec);
@@ -837,8 +837,8 @@ void build(rw_ctx* x) {
 
   // ---- schedules
   const bool f16x2 = x->prec == kF16x2;
-  void* kf = lstm_kernel_ptr(x->prec, true, false);
-  void* kb = lstm_kernel_ptr(x->prec, false, false);
+  void* kf = lstm_kernel_ptr(x->prec, true, false, x->kind);
+  void* kb = lstm_kernel_ptr(x->prec, false, false, x->kind);
   const int kbf_max = (std::max(Ip, Hp) + Hp) / x->atomK;
   const int kbb_max = (int)((L > 1 ? 2 : 1) * G4p / x->atomK);
   const int tiles_f = Hp / kUnitsPerFwdTile, tiles_b = ceil_div(Hp, kTileM);
@@ -894,7 +894,7 @@ void build(rw_ctx* x) {
   x->slots_b = pb.a_slots;
   // stepwise forward as CTA pairs (cta_group::2, M = 256, each CTA half of the batch columns):
   // bf16, no split-K, an even tile count and Bp/2 a multiple of 16 (RW_FWD_PAIR=0 disables)
-  x->pair_f = x->prec == kBF16 && pf.sched == RW_SCHED_STEPWISE && !ls && !cl_f && pf.ks == 1 && tiles_f % 2 == 0 &&
+  x->pair_f = x->kind == kCellLstm && x->prec == kBF16 && pf.sched == RW_SCHED_STEPWISE && !ls && !cl_f && pf.ks == 1 && tiles_f % 2 == 0 &&
               Bp >= 64 && Bp % 32 == 0 && !(getenv("RW_FWD_PAIR") && atoi(getenv("RW_FWD_PAIR")) == 0);
   if (x->pair_f) {
     int st = 8;
@@ -912,7 +912,7 @@ void build(rw_ctx* x) {
   }
   // persistent backward as CTA pairs: bf16, no split-K, streamed weights, even tile count,
   // and the pairs co-resident (RW_BWD_PAIR=0 disables)
-  x->pair_b = x->prec == kBF16 && pb.sched == RW_SCHED_PERSISTENT && !ls && !cl_b && pb.ks == 1 && !pb.resident &&
+  x->pair_b = x->kind == kCellLstm && x->prec == kBF16 && pb.sched == RW_SCHED_PERSISTENT && !ls && !cl_b && pb.ks == 1 && !pb.resident &&
               tiles_b % 2 == 0 && Bp >= 64 && Bp % 32 == 0 &&
               !(getenv("RW_BWD_PAIR") && atoi(getenv("RW_BWD_PAIR")) == 0);
   if (x->pair_b) {
@@ -1009,6 +1009,7 @@ void build(rw_ctx* x) {
 
   // ---- tensor maps
   const int aK = x->atomK, prec = x->prec;
+  std::vector<int> m_dgrK(2 * L);  // GRU: the R-side dG operand (the persistent / stepwise recurrence)
   std::vector<int> m_wf(2 * L), m_wb(2 * L), m_hopK(2 * L), m_hopMN(2 * L), m_dgK(2 * L),
       m_dgMN(2 * L), m_dgrMN(2 * L);
   int m_xK[2], m_xMN[2], m_w0t[2], m_dg0dx[2], m_xT[2];
@@ -1035,6 +1036,8 @@ void build(rw_ctx* x) {
       if (x->pair_f) m_hopK2[l] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, Bp / 2));
       m_hopMN[2 * l + p] = add_map(x, make_map(x->hop[l].p(p), prec, Hp, colsT1, aK, aK));
       m_dgK[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp));
+      m_dgrK[2 * l + p] = x->kind == kCellGru ? add_map(x, make_map(x->dgrop[l].p(p), prec, G4p, colsT, aK, Bp))
+                                              : m_dgK[2 * l + p];
       if (x->pair_b) m_dgK2[l] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, Bp / 2));
       m_dgMN[2 * l + p] = add_map(x, make_map(x->dgop[l].p(p), prec, G4p, colsT, aK, aK));
       m_dgrMN[2 * l + p] = x->kind == kCellGru ? add_map(x, make_map(x->dgrop[l].p(p), prec, G4p, colsT, aK, aK))
@@ -1102,7 +1105,7 @@ void build(rw_ctx* x) {
     for (int p = 0; p < 2; ++p) {
       Bd.a[p] = mp(m_wb[2 * l + (p % x->planes)], p);
       Bd.bup[p] = l < L - 1 ? mp(m_dgK[2 * (l + 1) + (p % x->planes)], p) : nullptr;
-      Bd.bg[p] = mp(m_dgK[2 * l + (p % x->planes)], p);
+      Bd.bg[p] = mp(m_dgrK[2 * l + (p % x->planes)], p);  // GRU: R^T dgr (dgr != dgw in the candidate)
       Bd.bup2 = x->pair_b && l < L - 1 ? MD + m_dgK2[l + 1] : nullptr;
       Bd.bg2 = x->pair_b ? MD + m_dgK2[l] : nullptr;
       Bd.alo = f16x2 ? static_cast<const uint16_t*>(x->wb[l].p(1)) : nullptr;
@@ -1528,6 +1531,7 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
 
 RecParams rec_params(rw_ctx* x, bool fwd) {
   RecParams rp{};
+  rp.kind = x->kind;
   rp.L = x->L;
   rp.H = x->H;
   rp.Hp = x->Hp;
@@ -1698,7 +1702,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
   {
   if (x->fwd_sched == RW_SCHED_LAYERSEQ) {
     RecParams rp = rec_params(x, true);
-    void* kern = KernelSet<P>::fwd();
+    void* kern = lstm_kernel_ptr(x->prec, true, false, x->kind);
     rp.resident = 0;
     // one persistent launch per layer (its tiles x ksplit CTAs co-resident, flag-synchronised
     // steps, R streamed from L2 -- one layer's weights fit there) unless RW_LS_PERSISTENT=0:
@@ -1719,7 +1723,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
     return;
   }
   RecParams rp = rec_params(x, true);
-  void* kern = KernelSet<P>::fwd();
+  void* kern = lstm_kernel_ptr(x->prec, true, false, x->kind);
   // inference: no gate tapes (null gates pointer patched via a second descriptor table is
   // avoided by simply keeping the tapes; cost is HBM writes only)
   (void)training;
@@ -1793,7 +1797,7 @@ void run_backward_rec(rw_ctx* x, cudaStream_t s) {
   {
   if (x->prec == kF16x2) RW_CUDA(cudaMemsetAsync(static_cast<unsigned*>(x->errflag.p) + 2, 0, 4, s));  // max|dG|
   RecParams rp = rec_params(x, false);
-  void* kern = KernelSet<P>::bwd();
+  void* kern = lstm_kernel_ptr(x->prec, false, false, x->kind);
   if (x->bwd_sched == RW_SCHED_LAYERSEQ) {
     const bool pers = x->ls_pers_b;  // as in the forward
     rp.persistent = pers ? 1 : 0;

@@ -2,7 +2,8 @@
 row 2 -- against the unmodified reference CPU engine (oracle/_ref, cells.hpp:200-225, 283-333,
 365-400, 486-562) on identical SplitMix64 weights and inputs with nonzero bias and h0, through
 the reference-shaped API, in both precision modes. Tolerances: tests/parity.py. The device runs
-these cells on the cluster schedule (rec_cluster.cuh, per-class instantiations)."""
+these cells on the cluster schedule (rec_cluster.cuh) and on the persistent / stepwise schedules
+(lstm_step.cuh), per-class instantiations."""
 import numpy as np
 import pytest
 
@@ -70,3 +71,41 @@ def test_gru_tapes_and_errors(reference):
         assert e2 < 1e-5, e2
     with pytest.raises(ValueError, match="c0 supplied for a cell kind without cell state"):
         eng.forward(params, x, True, h0, h0)
+
+
+# GRU / RNN on the persistent and stepwise schedules (the large-H path): the kernels sum
+# [W|R].[x;h] over K and the GRU candidate's halves stay apart through the forward image's slots
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("kind", list(KINDS), ids=lambda k: KINDS[k])
+@pytest.mark.parametrize("schedule", ["persistent", "stepwise"])
+@pytest.mark.parametrize("shape", [(2, 64, 48, 16, 7), (2, 130, 70, 33, 5), (3, 96, 40, 20, 6)],
+                         ids=lambda s: "L{}H{}I{}B{}T{}".format(*s))
+def test_cell_parity_wavefront_schedules(reference, kind, shape, schedule, precision):
+    from paper_1604_01946_b200 import Engine
+    dims = Dims(*shape, kind=kind)
+    c, params, x, dy, h0, c0 = make_case(dims, seed=29, bias=True, state=True)
+    eng = Engine(c, precision=precision, schedule=schedule)
+    d = eng.describe()
+    assert d["fwd_schedule"] == d["bwd_schedule"] == schedule, d
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    rows = compare(dev, ref, c)
+    if kind == 1 and precision == "bf16":  # as test_cell_parity: ReLU backward in bf16
+        fwd = [r for r in rows if r[0] == "y" or r[0].startswith("hT")]
+        assert_within(fwd, precision)
+        assert not [r for r in rows if r not in fwd and not (r[1] <= 0.2 and r[2] <= 0.4)]
+        return
+    assert_within(rows, precision)
+
+
+@pytest.mark.parametrize("kind", [2, 0], ids=["gru", "rnn-tanh"])
+def test_cell_large_hidden_auto_schedule(reference, kind):
+    """H = 1024 does not fit the cluster schedule: AUTO picks the persistent kernels for GRU / RNN."""
+    from paper_1604_01946_b200 import Engine
+    dims = Dims(1, 1024, 256, 32, 5, kind=kind)
+    c, params, x, dy, h0, c0 = make_case(dims, seed=31, bias=True, state=True)
+    eng = Engine(c, precision="fp32")
+    assert eng.describe()["fwd_schedule"] != "cluster"
+    dev = run_device(eng, params, x, dy, h0, c0)
+    ref = run_reference(reference, c, params, x, dy, h0, c0)
+    assert_within(compare(dev, ref, c), "fp32")
