@@ -81,8 +81,8 @@ typedef struct {
   int input;
   int batch;
   int steps;
-  int cell_kind;   /* CellKind: 0 RnnTanh, 1 RnnRelu, 2 Gru, 3 Lstm (config.hpp:12); GRU / RNN run
-                     every schedule but the layer-sequential one */
+  int cell_kind;   /* CellKind: 0 RnnTanh, 1 RnnRelu, 2 Gru, 3 Lstm (config.hpp:12); all cell kinds run
+                     on every schedule */
   int opt_level;   /* validated 0..6 for API compatibility; selects no alternate path */
   int batch_steps; /* validated (1..steps) like the reference */
   int workers;     /* validated > 0; unused on the device */

@@ -15,7 +15,7 @@ void* cl_kernel_ptr_lstm(int prec, bool fwd, int nco);
 void* cl_kernel_ptr_gru(int prec, bool fwd, int nco);
 void* cl_kernel_ptr_rnn(int prec, bool fwd, int nco);
 // k_lstm_fwd / k_lstm_bwd<P, pair, kind> (lstm_step.cuh); prec kBF16, kF16x2 or kTF32x3 (pair: bf16
-// LSTM only); GRU / RNN: bf16 or fp16x2, no pairs (kernels_lstm_cells.cu)
+// LSTM only); GRU / RNN: no pairs (kernels_lstm_cells.cu)
 void* lstm_kernel_ptr(int prec, bool fwd, bool pair, int kind = kCellLstm);
 void* lstm_kernel_ptr_cells(int prec, bool fwd, int kind);
 // k_gemm_tc<P, AMN, BMN, BNV> (gemm_tc.cuh): bf16 BNV 0; two-plane formats BNV = tile width 64 / 128

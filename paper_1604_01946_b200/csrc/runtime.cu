@@ -243,7 +243,7 @@ struct rw_ctx {
   std::vector<Operand> hop, dgop;
   // tf32 only: K-major (time-batch contiguous) copies for the weight-gradient GEMMs, since
   // tcgen05 kind::tf32 cannot read these operands MN-major with the 128B swizzle we use
-  std::vector<Operand> dgT, hT;
+  std::vector<Operand> dgT, hT, dgrT;  // 3xTF32 weight gradients: K-major copies (GRU: dgr too)
   Operand xT;
   DevBuf dx0, y_raw, stage;  // unpadded outputs / staging
   std::vector<DevBuf> dW, dR, db;
@@ -761,13 +761,9 @@ void build(rw_ctx* x) {
     }
   }
   // GRU and vanilla-RNN cells: the cluster schedule keeps the input and recurrent products in
-  // separate roles; the persistent / stepwise kernels sum [W|R].[x;h] over K, and GRU's
-  // linear-before-reset candidate stays apart there through the forward image's slot layout
-  // (W_n in slot 2, R_n in slot 3: layout_kernels.cuh k_repack). Not on the layer-sequential
-  // schedule and not with 3xTF32 operands (LSTM only).
-  if (x->kind != kCellLstm && x->prec == kTF32x3)
-    einval(std::string("rnnwave_sm100: ") + (x->kind == kCellGru ? "GRU" : "RNN") +
-           " cells do not run on the layer-sequential schedule or with 3xTF32 operands");
+  // separate roles; the persistent / stepwise / layer-sequential kernels sum [W|R].[x;h] over K,
+  // and GRU's linear-before-reset candidate stays apart there through the forward image's slot
+  // layout (W_n in slot 2, R_n in slot 3: layout_kernels.cuh k_repack).
   x->planes = prec_planes(x->prec);
   x->elem = prec_elem(x->prec);
   x->atomK = prec_atomk(x->prec);
@@ -820,9 +816,11 @@ void build(rw_ctx* x) {
   if (kmajor_wg) {
     x->dgT.resize(L);
     x->hT.resize(L);
+    if (x->kind == kCellGru) x->dgrT.resize(L);
     for (int l = 0; l < L; ++l) {
       x->dgT[l].alloc(x->prec, (size_t)G4p * colsT);
       x->hT[l].alloc(x->prec, (size_t)Hp * colsT1);
+      if (x->kind == kCellGru) x->dgrT[l].alloc(x->prec, (size_t)G4p * colsT);
     }
     x->xT.alloc(x->prec, (size_t)Ip * colsT);
   }
@@ -1019,7 +1017,7 @@ void build(rw_ctx* x) {
   x->bn_ls = x->prec == kBF16 ? 256 : x->prec == kF16x2 ? 128 : 64;  // tf32: the chunked-promotion GEMM variant
   int m_xLS[2] = {0, 0};
   std::vector<int> m_hopLS(2 * L), m_dgLS(2 * L);
-  std::vector<int> m_dgT(2 * L), m_hT(2 * L);
+  std::vector<int> m_dgT(2 * L), m_hT(2 * L), m_dgrT(2 * L);
   x->bn_dx = x->prec == kBF16 ? (colsT >= 256 ? 256 : 128) : 128;
   if (const char* e = getenv("RW_BN_DX")) x->bn_dx = atoi(e);
   // two-plane formats: (hi,hi)+(hi,lo) as one N = 2 bn MMA, 2 x 2 bn TMEM columns (gemm_tc.cuh)
@@ -1046,6 +1044,8 @@ void build(rw_ctx* x) {
     if (kmajor_wg) {
       for (int l = 0; l < L; ++l) {
         m_dgT[2 * l + p] = add_map(x, make_map(x->dgT[l].p(p), prec, colsT, G4p, aK, kTileM));
+        m_dgrT[2 * l + p] = x->kind == kCellGru ? add_map(x, make_map(x->dgrT[l].p(p), prec, colsT, G4p, aK, kTileM))
+                                                : m_dgT[2 * l + p];
         m_hT[2 * l + p] = add_map(x, make_map(x->hT[l].p(p), prec, colsT1, Hp, aK, gemm_box_rows(x->bn_wg)));
       }
       m_xT[p] = add_map(x, make_map(x->xT.p(p), prec, colsT, Ip, aK, gemm_box_rows(x->bn_wg)));
@@ -1260,7 +1260,8 @@ void build(rw_ctx* x) {
     GemmDesc r = d;
     for (int p = 0; p < 2; ++p) {
       r.b[p] = kmajor_wg ? mp(m_hT[2 * l + (p % x->planes)], p) : mp(m_hopMN[2 * l + (p % x->planes)], p);
-      if (!kmajor_wg) r.a[p] = mp(m_dgrMN[2 * l + (p % x->planes)], p);  // dR = dgr h^T (GRU: dgr != dgw)
+      // dR = dgr h^T (GRU: dgr != dgw)
+      r.a[p] = kmajor_wg ? mp(m_dgrT[2 * l + (p % x->planes)], p) : mp(m_dgrMN[2 * l + (p % x->planes)], p);
     }
     r.N = Hp;
     r.b_k_off = 0;  // Hprev = blocks 0..T-1
@@ -2074,6 +2075,7 @@ void run_weight_grads(rw_ctx* x, cudaStream_t s) {
     const long long colsT = (long long)x->Bp * x->T;
     for (int l = 0; l < x->L; ++l) {
       transpose_planes(x, x->dgop[l], 4 * x->Hp, colsT, x->dgT[l], s);
+      if (x->kind == kCellGru) transpose_planes(x, x->dgrop[l], 4 * x->Hp, colsT, x->dgrT[l], s);
       transpose_planes(x, x->hop[l], x->Hp, colsT + x->Bp, x->hT[l], s);
     }
     transpose_planes(x, x->x_op, x->Ip, colsT, x->xT, s);

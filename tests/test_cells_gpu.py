@@ -73,11 +73,12 @@ def test_gru_tapes_and_errors(reference):
         eng.forward(params, x, True, h0, h0)
 
 
-# GRU / RNN on the persistent and stepwise schedules (the large-H path): the kernels sum
+# GRU / RNN on the persistent, stepwise and layer-sequential schedules (the large-H path; layerseq
+# fp32 = 3xTF32 operands): the kernels sum
 # [W|R].[x;h] over K and the GRU candidate's halves stay apart through the forward image's slots
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("kind", list(KINDS), ids=lambda k: KINDS[k])
-@pytest.mark.parametrize("schedule", ["persistent", "stepwise"])
+@pytest.mark.parametrize("schedule", ["persistent", "stepwise", "layerseq"])
 @pytest.mark.parametrize("shape", [(2, 64, 48, 16, 7), (2, 130, 70, 33, 5), (3, 96, 40, 20, 6)],
                          ids=lambda s: "L{}H{}I{}B{}T{}".format(*s))
 def test_cell_parity_wavefront_schedules(reference, kind, shape, schedule, precision):
