@@ -175,24 +175,28 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- shared
 def job_flops(args, world: int) -> int:
     """FLOPs of one step of the whole job: weak scaling runs `world` full minibatches, strong
-    scaling splits one across the ranks."""
-    f = pass_flops(CONFIGS[args.config])
+    scaling splits one across the ranks. `--pass fwd` (inference forward) counts 1x, both 3x
+    (bench.hpp:55-62)."""
+    f = pass_flops(CONFIGS[args.config], 1 if getattr(args, "pass_", "both") == "fwd" else 3)
     return f if args.scaling == "strong" else f * world
 
 
-def workload_name(key: str, c: dict) -> str:
-    base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM fwd+bwd"
-    return base + (" (BASELINE configs[1])" if key == "B" else f" (sweep config {key})")
+def workload_name(key: str, c: dict, pass_: str = "both") -> str:
+    base = f"{c['layers']}L h{c['hidden']} mb{c['batch']} T{c['steps']} LSTM " + (
+        "fwd+bwd" if pass_ == "both" else "forward (inference)")
+    return base + (" (BASELINE configs[1])" if key == "B" and pass_ == "both" else f" (sweep config {key})")
 
 
-def config_dict(key: str, c: dict, world: int) -> dict:
+def config_dict(key: str, c: dict, world: int, pass_: str = "both") -> dict:
     """The `config` object both arms print (identical keys, so the driver can match them)."""
-    return {"workload": workload_name(key, c), "model": f"lstm-{c['layers']}x{c['hidden']}",
+    return {"workload": workload_name(key, c, pass_), "model": f"lstm-{c['layers']}x{c['hidden']}",
             "global_batch": c["batch"] * world, "seq_len": c["steps"], "layers": c["layers"],
             "hidden": c["hidden"], "parallelism": f"dp{world}" if world > 1 else "single",
             "l2": "flushed (256 MiB write) between timed steps",
-            "per_step_work": "K7 repack (params updated in place) + forward (training) + "
-                             "backward_data + weight_update, like the reference's time_level pass"}
+            "per_step_work": ("K7 repack (params updated in place) + forward (training) + backward_data + "
+                              "weight_update, like the reference's time_level pass" if pass_ == "both" else
+                              "K7 repack (params updated in place) + inference forward, like the reference's "
+                              "time_level Forward pass")}
 
 
 def cpu_model() -> str:
@@ -216,13 +220,14 @@ def run_reference(args) -> None:
     c = dict(CONFIGS[args.config])  # the same workload as our arm's line
     d = oracle.Dims(**c)
     cores = os.cpu_count() or 1
-    flops = pass_flops(c)
+    pk = 0 if args.pass_ == "fwd" else 2  # bench::PassKind Forward / Both
+    flops = pass_flops(c, 1 if pk == 0 else 3)
     # one pass of the reference engine at O6 ~ seconds; bound the run to a few minutes
-    est = R.time(d, seed=42, pass_kind=2, reps=1, warmup=0, workers=cores)["median_us"] * 1e-6
+    est = R.time(d, seed=42, pass_kind=pk, reps=1, warmup=0, workers=cores)["median_us"] * 1e-6
     budget = 150.0
     reps = max(1, min(args.steps, int(budget / max(est, 1e-3))))
     warm = max(args.warmup, 3) if est * (reps + max(args.warmup, 3)) < 1.5 * budget else 1
-    t = R.time(d, seed=42, pass_kind=2, reps=reps, warmup=warm, workers=cores)
+    t = R.time(d, seed=42, pass_kind=pk, reps=reps, warmup=warm, workers=cores)
     sec = t["median_us"] * 1e-6
     tflops = flops / sec / 1e12
     line = {
@@ -232,7 +237,7 @@ def run_reference(args) -> None:
         "data": "synthetic (SplitMix64 seed 42, reference generators)",
         # the same job description as our arm's line (weak scaling: N minibatches, which the CPU
         # engine processes at its per-minibatch rate)
-        "config": config_dict(args.config, c, 1 if args.scaling == "strong" else args.gpus),
+        "config": config_dict(args.config, c, 1 if args.scaling == "strong" else args.gpus, args.pass_),
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "reference",
                          "sample": f"{reps} full config-{args.config} passes (median), O6, {cores} workers",
                          "cpu": cpu_model(), "lib": os.path.basename(R.path)},
@@ -274,10 +279,13 @@ def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: b
     # L2 flush buffer (> 126 MB L2) written between timed steps, outside the events
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
+    fwd_only = getattr(args, "pass_", "both") == "fwd"
+    pass_kind = 0 if fwd_only else 2  # 0: inference forward (config A's "forward" line), 2: fwd + bwd
+
     def step():
         eng.params_updated()  # the parameters changed (optimizer): K7 repack inside the pass
-        eng.run_pass(2, sh)
-        if world > 1:
+        eng.run_pass(pass_kind, sh)
+        if world > 1 and not fwd_only:
             eng.allreduce_grads(sh)
 
     with torch.cuda.stream(stream):
@@ -315,13 +323,36 @@ def measure(args, precision: str, world: int, rank: int, local: int, with_e2e: b
         for _ in range(nprof):
             flush.zero_()
             eng.params_updated()
-            eng.run_pass(2, sh)
+            eng.run_pass(pass_kind, sh)
         eng.sync()
         ph = eng.phase_times(reset=True)
         eng.set_profiling(False)
 
         e2e = None
-        if with_e2e:
+        if with_e2e and fwd_only:
+            # inference through the public API with host buffers: upload x (pinned), forward, read y
+            yh = torch.zeros(c["batch"] * c["steps"], c["hidden"], dtype=torch.float32).pin_memory().numpy().T
+            xh = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).pin_memory()
+            e2e_steps = max(10, min(args.steps, 50))
+
+            def infer():
+                eng.params_updated()
+                eng.upload_inputs_ptr(xh.data_ptr(), 0)
+                eng.run_pass(0)
+                eng.read_outputs(y=yh)
+
+            for _ in range(3):
+                infer()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                infer()
+            e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+            e2e = {"value": job_flops(args, world) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "ms_per_step": e2e_ms, "h2d_bytes_per_step": xh.numel() * 4, "d2h_bytes_per_step": yh.size * 4,
+                   "path": "C-ABI rw_upload_inputs (pinned host x) -> rw_run_pass(0) (K7 repack + inference "
+                           "forward) -> rw_read_outputs(y) on the host"}
+        elif with_e2e:
             def pinned(rows, cols=None):
                 """Column-major float32 host array in pinned (page-locked) memory."""
                 if cols is None:
@@ -388,7 +419,7 @@ def roofline(args, m: dict, precision: str) -> tuple[dict, dict]:
             "stepwise": ("k_lstm_fwd", "k_lstm_bwd")}
     kf = kern.get(desc["fwd_schedule"], ("k_lstm_fwd",))[0]
     kb = kern.get(desc["bwd_schedule"], ("", "k_lstm_bwd"))[1]
-    if bwd_ms >= fwd_ms:
+    if bwd_ms >= fwd_ms and getattr(args, "pass_", "both") != "fwd":
         dom, dom_ms, dom_fl = f"{kb} (fused recurrent backward, {desc['bwd_schedule']})", bwd_ms, bwd_fl
         dom_k, dom_by = kb, recurrent_bytes(c, False, planes)
     else:
@@ -449,12 +480,12 @@ def run_ours(args) -> None:
     rf, crit = roofline(args, m, args.precision)
     cpu_base = None
     if not args.no_cpu_baseline and args.config in ("A", "B"):
-        cpu_base = cpu_baseline(args.config)
+        cpu_base = cpu_baseline(args.config, args.pass_)
     value = job_flops(args, world) / (m["ms"] * 1e-3) / 1e12
     dtype = {"bf16": "bf16", "fp32": "tf32x3 (fp32-parity)"}
     operands = {"tf32x3": "3xTF32 split operands", "fp16x2": "fp16x2 split operands (hi + lo, 3 MMAs)",
                 "bf16": "bf16 operands"}
-    cfgd = config_dict(args.config, c, 1 if args.scaling == "strong" else world)
+    cfgd = config_dict(args.config, c, 1 if args.scaling == "strong" else world, args.pass_)
     cfgd.update({"precision": args.precision, "schedule": m["desc"],
                  "operands": operands.get(m["desc"]["operands"], m["desc"]["operands"]),
                  "pct_of_bf16_peak": 100.0 * value / world / peak_burst,
@@ -494,7 +525,7 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(key: str = "B") -> dict | None:
+def cpu_baseline(key: str = "B", pass_: str = "both") -> dict | None:
     """The reference CPU engine on the host cores, bounded sample of the same workload: P = all
     host threads and P = min(nproc, 2L) (the reference CLI's default worker count,
     rnnwave.cpp:30-37)."""
@@ -508,15 +539,17 @@ def cpu_baseline(key: str = "B") -> dict | None:
     c = CONFIGS[key]
     d = oracle.Dims(**c)
     cores = os.cpu_count() or 1
-    t = R.time(d, seed=42, pass_kind=2, reps=3, warmup=1, workers=cores)
+    pk, mult = (0, 1) if pass_ == "fwd" else (2, 3)
+    t = R.time(d, seed=42, pass_kind=pk, reps=3, warmup=1, workers=cores)
     sec = t["median_us"] * 1e-6
     p2 = min(cores, 2 * c["layers"])
-    t2 = R.time(d, seed=42, pass_kind=2, reps=3, warmup=1, workers=p2)
+    t2 = R.time(d, seed=42, pass_kind=pk, reps=3, warmup=1, workers=p2)
     sec2 = t2["median_us"] * 1e-6
-    return {"value": pass_flops(c) / sec / 1e12, "unit": "TFLOP/s", "cores": cores,
+    what = "fwd+bwd" if pass_ == "both" else "inference forward"
+    return {"value": pass_flops(c, mult) / sec / 1e12, "unit": "TFLOP/s", "cores": cores,
             "kind": kind, "ms_per_step": sec * 1e3, "cpu": cpu_model(),
-            "sample": f"3 full config-{key} fwd+bwd passes after 1 warm-up (median), O6, workers=cores",
-            "default_workers": {"workers": p2, "value": pass_flops(c) / sec2 / 1e12, "ms_per_step": sec2 * 1e3,
+            "sample": f"3 full config-{key} {what} passes after 1 warm-up (median), O6, workers=cores",
+            "default_workers": {"workers": p2, "value": pass_flops(c, mult) / sec2 / 1e12, "ms_per_step": sec2 * 1e3,
                                 "why": "min(nproc, 2L), the reference CLI default (rnnwave.cpp:30-37)"}}
 
 
@@ -627,6 +660,8 @@ def main():
     ap.add_argument("--single-precision", action="store_true", help="skip the secondary precision")
     ap.add_argument("--schedule", default="auto", choices=["auto", "stepwise", "persistent", "cluster", "layerseq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pass", dest="pass_", default="both", choices=["both", "fwd"],
+                    help="both: training step (the headline); fwd: inference forward (SURVEY 8d config A)")
     ap.add_argument("--ladder", action="store_true", help="the GPU optimisation ladder (O0-O6) in the "
                     "reference's run-ladder CSV schema instead of the bench line")
     ap.add_argument("--ladder-csv", default=None)
