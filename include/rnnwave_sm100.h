@@ -200,32 +200,33 @@ int rw_comm_overlap(rw_ctx* ctx, int on);
 /* ---- layer pipeline over NVLink (config E; SURVEY §8e "deep stacks split as a layer
  * pipeline that hands off h_t per timestep peer-to-peer") ----
  * Stage k is an ordinary context holding layers [l_k, l_k + L_k) (cfg.input = H for k > 0).
- * At the stage boundary the cluster schedule's off-critical group of a layer -- the GEMM
- * that does not depend on that layer's own recurrence -- runs on the stage that owns its
- * operand and writes its per-step partial sums straight into the neighbour's ring over
- * NVLink (system-scope release counters per step): forward, stage k computes
- * W_{l_{k+1}} . h_{last,t} for stage k+1; backward, stage k+1 computes W_{l_{k+1}}^T . dG_t for
- * stage k's last layer. After its forward, stage k also copies its last layer's h sequence
- * into stage k+1's layer-input buffer (for stage k+1's dW of its first layer).
+ * Forward: stage k's last layer writes each h_t (the bf16 operand image, H x B x 2 bytes per
+ * step) straight into stage k+1's layer-input image over NVLink and releases a system-scope
+ * per-step counter; stage k+1's first layer then runs exactly as on one GPU. Backward: the
+ * cluster schedule's off-critical group of stage k+1's first layer (W^T . dG_t, which does not
+ * depend on stage k's recurrence) runs on stage k+1 and writes its per-step partial sums into
+ * stage k's last-layer ring. After its forward, stage k also copies its last layer's h sequence
+ * into stage k+1's plain layer-input planes (for stage k+1's dW of its first layer).
  * Requires the cluster schedule (bf16) in both directions. Exported descriptors carry CUDA
  * IPC handles (cross-process) and raw pointers (same-process stages, tests). */
 typedef struct {
-  char handle[5][64];     /* cudaIpcMemHandle_t of ring data / done / consumed / layer-input
-                             buffer / input-ready counter */
+  char handle[5][64];     /* cudaIpcMemHandle_t of the regions: dir 0: input image / per-step
+                             input counters / (same) / plain layer-input planes / input-ready
+                             counter; dir 1: ring data / done / consumed */
   uint64_t offset[5];     /* byte offset of the region inside each exported allocation */
   uint64_t ptr[5];        /* device pointers in the exporting process */
   int64_t pid;            /* exporting process */
   int device;             /* exporting device */
   int ko;                 /* off members the ring expects per step */
 } rw_pp_ring;
-/* dir 0: the forward ring of my first layer (+ my layer-input buffer); dir 1: the backward
- * ring of my last layer. */
+/* dir 0: my layer-input image, its per-step counters and my plain layer-input buffer; dir 1:
+ * the backward ring of my last layer. */
 int rw_pp_export(rw_ctx* ctx, int dir, rw_pp_ring* out);
-/* dir 0: link to the NEXT stage's forward export; W_next is the next stage's first-layer W
- * (4H x H, reference layout, host). dir 1: link to the PREVIOUS stage's backward export. */
+/* dir 0: link to the NEXT stage's forward export (W_next: unused since the h_t hand-off, may be
+ * NULL). dir 1: link to the PREVIOUS stage's backward export. */
 int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next);
-/* The next stage's first-layer W (4H x H, reference layout) after a parameter update: the
- * forward boundary group re-packs it with this stage's next pass. */
+/* Kept for API compatibility: the forward hand-off sends h_t, so the next stage's weights
+ * need no refresh here after a parameter update (validates that a forward link exists). */
 int rw_pp_set_next_w(rw_ctx* ctx, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */

@@ -70,6 +70,10 @@ struct FwdLayer {
   const uint16_t* alo;
   int alo_ld, alo_rows;
   float* zrh;                // GRU: R-side candidate pre-activation R_n h_{t-1} tape (Hp x Bp T)
+  // layer pipeline (rw_pp_link, forward): the next stage's layer-input image and its per-step
+  // input counters -- the last layer of a stage also writes h_t there (block t) and releases it
+  uint8_t* hsw_peer;
+  uint32_t* peer_flags;
 };
 
 struct BwdLayer {

@@ -732,7 +732,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (!early) cl_fetch_off(S, p, ring, done, done_target, t, m, nco, offc, wait_code(0, l, t, 3), sys);
         cl_trace(p, t, 14);  // task start: h_{t-1} and the off partial both available
       } else {
-        if (Og.op_flags) wait_flag(&Og.op_flags[t], flag_target, p.error, p.timeout_ns, wait_code(0, l, t, 1));
+        // (system scope when the operand is written by another process: a pipeline stage's input)
+        if (Og.op_flags) wait_flag_s(&Og.op_flags[t], flag_target, sys, p.error, p.timeout_ns, wait_code(0, l, t, 1));
         fence_proxy_async_global();
         cl_trace(p, t, 1);
         cl_load_b(S, Og.op + (size_t)(Og.op_blk_off + t) * Og.kdim * BR * 2, kb_lo, kb_hi, 0, pc, p.stages, BR,
@@ -798,6 +799,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       // lo plane is N rows further
       const long long blk_bytes = (long long)p.Hp * BR * 2;
       uint8_t* hsw_t = Le.hsw + blk_bytes + sw_off(u, own0 + cg, BR);
+      // layer pipeline: the next stage's layer-input image (its block t = our h_t), over NVLink
+      uint8_t* peer_t = Le.hsw_peer ? Le.hsw_peer + sw_off(u, own0 + cg, BR) : nullptr;
       const int lo_off = N * 128;
       // tapes: element (col, u) at col * Hp + u (gates: col * 4Hp + u); col_new = (t + 1) N + own0 + cg + 8k
       const long long kstride = 8 * Hp;
@@ -864,8 +867,14 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             f16x2_split(hv[k] * pow2f(kHScaleLog2), hh, hl);
             *reinterpret_cast<__half*>(hsw_t + k * 1024) = hh;
             *reinterpret_cast<__half*>(hsw_t + k * 1024 + lo_off) = hl;
+            if (peer_t) {
+              *reinterpret_cast<__half*>(peer_t + k * 1024) = hh;
+              *reinterpret_cast<__half*>(peer_t + k * 1024 + lo_off) = hl;
+            }
           } else {
-            *reinterpret_cast<__nv_bfloat16*>(hsw_t + k * 1024) = __float2bfloat16_rn(hv[k]);
+            const __nv_bfloat16 hb = __float2bfloat16_rn(hv[k]);
+            *reinterpret_cast<__nv_bfloat16*>(hsw_t + k * 1024) = hb;
+            if (peer_t) *reinterpret_cast<__nv_bfloat16*>(peer_t + k * 1024) = hb;
           }
         }
         if (et == 0) cl_trace(p, t, 3);
@@ -875,6 +884,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (et == 0) {
           cl_trace(p, t, 15);  // task end, before the release
           red_release_gpu_add(&Le.flags[t], 1);  // cumulative over the CTA's stores (bar.sync above)
+          if (Le.peer_flags) red_release_s(Le.peer_flags + t, 1, true);  // the next stage's input
           red_relaxed_s(consumed, 1, sys);       // ring slot t was copied into rxoff
           cl_trace(p, t, 5);
         }
@@ -902,6 +912,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
         if (et == 0) cl_trace(p, t, 6);
         hsw_t += blk_bytes;
+        if (peer_t) peer_t += blk_bytes;
         i_new += step_h;
         i_prev += step_h;
         i_gate += step_g;

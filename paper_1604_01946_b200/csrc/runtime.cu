@@ -298,7 +298,8 @@ struct rw_ctx {
   DevBuf gemm_fb;
   bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
-  DevBuf wf_next, wb_prev;                   // packed W_next (forward boundary) / W_0^T (backward)
+  DevBuf wf_next, wb_prev;                   // (unused since the h_t hand-off) / packed W_0^T (backward)
+  DevBuf xin_flags;                          // pipeline stage > 0: per-step counters of its input h_t
   DevBuf repack_jobs;                        // k_repack's job table (built on the first repack)
   int repack_njobs = 0, repack_tiles = 0;
   DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
@@ -2816,23 +2817,32 @@ extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
     memset(out, 0, sizeof *out);
     out->pid = (int64_t)getpid();
     out->device = x->dev;
-    ClRing& r = dir == 0 ? x->ring_f_h[0] : x->ring_b_h[x->L - 1];
-    // written by the next stage's boundary group with the member count a single context gives
-    // this layer's off group (kc of the backward plan, runtime.cu planner), so the K split and
-    // the reduction order -- and the results, bit for bit -- match the unsplit stack
-    if (dir == 1) r.ko = x->cl_b.kc;
-    r.sys = 1;
-    out->ko = r.ko;
-    export_region(out, 0, x->cl_offsum.p, r.ring);
-    export_region(out, 1, x->cl_done.p, r.done);
-    export_region(out, 2, x->cl_consumed.p, r.consumed);
     if (dir == 0) {
+      // forward: the previous stage writes its last layer's h_t (bf16 operand image, H x B x 2 B
+      // per step) straight into this stage's layer-input image over NVLink and releases a
+      // per-step counter; this stage's first-layer W.x group then runs as on one GPU
+      x->xin_flags.alloc((size_t)x->T * 4);
+      export_region(out, 0, x->xsw.p, x->xsw.p);
+      export_region(out, 1, x->xin_flags.p, x->xin_flags.p);
+      export_region(out, 2, x->xin_flags.p, x->xin_flags.p);
       export_region(out, 3, x->x_op.p(0), x->x_op.p(0));
       export_region(out, 4, x->cl_epoch.p, static_cast<uint32_t*>(x->cl_epoch.p) + 2);
-      x->off_f_h[0].active = 0;  // the previous stage computes W_0 . x into this ring
+      ClOff& o = x->off_f_h[0];
+      o.op_flags = static_cast<const uint32_t*>(x->xin_flags.p);
+      o.sys = 1;  // written by another process: system-scope waits
       x->pp_prev = true;
       x->pp_exported_f = true;
     } else {
+      ClRing& r = x->ring_b_h[x->L - 1];
+      // written by the next stage's boundary group with the member count a single context gives
+      // this layer's off group (kc of the backward plan, runtime.cu planner), so the K split and
+      // the reduction order -- and the results, bit for bit -- match the unsplit stack
+      r.ko = x->cl_b.kc;
+      r.sys = 1;
+      out->ko = r.ko;
+      export_region(out, 0, x->cl_offsum.p, r.ring);
+      export_region(out, 1, x->cl_done.p, r.done);
+      export_region(out, 2, x->cl_consumed.p, r.consumed);
       x->pp_exported_b = true;
     }
     upload_cluster_tables(x);
@@ -2850,6 +2860,24 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
     const long long G4p = 4LL * Hp;
+    if (dir == 0) {
+      // forward: our last layer's critical CTAs also store h_t into the next stage's input image
+      // and release its per-step counter (rec_cluster.cuh k_cl_fwd); W_next is not needed
+      (void)W_next;
+      uint8_t* peer_xsw = static_cast<uint8_t*>(open_region(x, peer, 0));
+      uint32_t* peer_flags = static_cast<uint32_t*>(open_region(x, peer, 1));
+      FwdLayer top;
+      FwdLayer* dev_top = static_cast<FwdLayer*>(x->fwd_layers.p) + (L - 1);
+      RW_CUDA(cudaMemcpy(&top, dev_top, sizeof top, cudaMemcpyDeviceToHost));
+      top.hsw_peer = peer_xsw;
+      top.peer_flags = peer_flags;
+      RW_CUDA(cudaMemcpy(dev_top, &top, sizeof top, cudaMemcpyHostToDevice));
+      x->pp_next_xop = open_region(x, peer, 3);
+      x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
+      x->pp_next = true;
+      invalidate_graphs(x);
+      return;
+    }
     ClOff o{};
     o.ring = static_cast<float*>(open_region(x, peer, 0));
     o.done = static_cast<uint32_t*>(open_region(x, peer, 1));
@@ -2858,21 +2886,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.active = 1;
     o.unscale = 1.0f;  // bf16 only (above)
     o.ko = peer->ko;   // the receiving ring's publication count (rw_pp_export)
-    if (dir == 0) {
-      if (!W_next) einval("rw_pp_link: forward link needs the next stage's first-layer W (4H x H)");
-      x->wn_raw.alloc((size_t)x->G * H * H * 4);
-      RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, (size_t)x->G * H * H * 4, cudaMemcpyHostToDevice));
-      x->wf_next.alloc((size_t)G4p * (Hp + Hp) * 2);
-      x->dirty = true;  // repack_params packs W_next into wf_next (again after rw_pp_set_next_w)
-      o.kdim = Hp;
-      o.op = static_cast<const uint8_t*>(x->hsw[L - 1].p);
-      o.op_blk_off = 1;
-      o.op_flags = static_cast<const uint32_t*>(x->flags_f.p) + (size_t)(L - 1) * T;
-      x->pp_maps[0] = make_map(x->wf_next.p, x->prec, Hp + Hp, G4p, aK, kTileM);
-      x->pp_next_xop = open_region(x, peer, 3);
-      x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
-      x->pp_next = true;
-    } else {
+    {
       if (!x->pp_prev) einval("rw_pp_link: backward link needs this stage's forward ring exported first");
       x->wb_prev.alloc((size_t)Hp * 2 * G4p * 2);
       o.kdim = (int)G4p;
@@ -2904,15 +2918,12 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
 // debug: counters of the boundary rings (pipeline bring-up): out[0..1] epochs (fwd, bwd),
 // out[2..4] forward ring of layer 0: done[0..1], consumed; out[6..8] backward ring of the last
 // layer: done[0..1], consumed; out[10..11] rows_f, rows_b; out[12..15] ko/sys of those rings.
-// The next stage's first-layer W changed (its parameters were updated): the forward boundary
-// group of this stage multiplies with it, so it is re-packed with this stage's next pass.
 extern "C" int rw_pp_set_next_w(rw_ctx* x, const float* W_next) {
+  // the forward hand-off sends h_t; the next stage multiplies with its own W (which follows its
+  // own parameter updates), so there is nothing to refresh here -- kept for API compatibility
   return guarded(x, [&] {
-    if (!x->pp_next || !x->wn_raw.p) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
-    if (!W_next) einval("rw_pp_set_next_w: W_next is null");
-    RW_CUDA(cudaSetDevice(x->dev));
-    RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, (unsigned long long)x->G * x->H * x->H * 4, cudaMemcpyHostToDevice));
-    x->dirty = true;
+    if (!x->pp_next) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
+    (void)W_next;
   });
 }
 

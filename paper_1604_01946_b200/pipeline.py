@@ -2,12 +2,12 @@
 h_t per timestep peer-to-peer over NVLink following the paper's wavefront").
 
 Stage k of n owns layers [first_k, first_k + L_k) as an ordinary Engine (input width H for
-k > 0). The device side is rw_pp_export / rw_pp_link (include/rnnwave_sm100.h): at each stage
-boundary the off-critical GEMM of the boundary layer runs on the GPU that owns its operand and
-writes its per-step partial sums into the neighbour's ring over NVLink, so the cross-layer
-wavefront of the paper (PAPER Listing 4) continues across GPUs step by step:
+k > 0). The device side is rw_pp_export / rw_pp_link (include/rnnwave_sm100.h), and the
+cross-layer wavefront of the paper (PAPER Listing 4) continues across GPUs step by step:
 
-  forward : stage k computes W_{first_{k+1}} . h_{last_k, t} into stage k+1's first-layer ring;
+  forward : stage k's last layer writes each h_t (bf16 operand image, H x B x 2 bytes) into stage
+            k+1's layer-input image over NVLink and releases a per-step counter, so stage k+1's
+            first layer runs exactly as on one GPU;
   backward: stage k+1 computes W_{first_{k+1}}^T . dG_{first_{k+1}, t} into stage k's last-layer
             ring (its d_above), and stage k copies h_{last_k} into stage k+1's layer input
             (the operand of stage k+1's first-layer dW).
@@ -72,12 +72,9 @@ class PipelineStage:
         self.exports: dict[int, bytes] = {}
 
     def set_params(self, params) -> None:
-        """params: the full model's LayerParams; the stage takes its own slice, and -- once linked
-        to a next stage -- that stage's first-layer W, which its forward boundary group multiplies
-        with (rw_pp_set_next_w: repacked with this stage's next pass)."""
+        """params: the full model's LayerParams; the stage takes its own slice (the forward
+        hand-off sends h_t, so no neighbour's weights are needed)."""
         self.engine.set_params(params[self.first:self.first + self.count])
-        if self.plan.link_next and getattr(self, "_linked_next", False):
-            self.engine.pp_set_next_w(params[self.first + self.count].w)
 
     def export(self) -> dict[int, bytes]:
         if self.plan.export_fwd:
@@ -89,9 +86,7 @@ class PipelineStage:
     def link(self, next_exports: dict[int, bytes] | None, prev_exports: dict[int, bytes] | None,
              params) -> None:
         if self.plan.link_next:
-            w_next = params[self.first + self.count].w
-            self.engine.pp_link(0, next_exports[0], w_next)
-            self._linked_next = True
+            self.engine.pp_link(0, next_exports[0], None)
         if self.plan.link_prev:
             self.engine.pp_link(1, prev_exports[1])
 
