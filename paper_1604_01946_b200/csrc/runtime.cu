@@ -300,6 +300,8 @@ struct rw_ctx {
   bool pp_exported_f = false, pp_exported_b = false;
   DevBuf wf_next, wb_prev;                   // (unused since the h_t hand-off) / packed W_0^T (backward)
   DevBuf xin_flags;                          // pipeline stage > 0: per-step counters of its input h_t
+  DevBuf wb_prev_lo;                         // fp16x2: lo plane of wb_prev
+  void* pp_next_xop_lo = nullptr;            // fp16x2: next stage's layer-input lo plane (peer pointer)
   DevBuf repack_jobs;                        // k_repack's job table (built on the first repack)
   int repack_njobs = 0, repack_tiles = 0;
   DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
@@ -1525,7 +1527,7 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   if (x->pp_prev && x->wb_prev.p) {  // backward boundary group: [W_0^T | R_0^T] of this stage
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
-                                                             x->wb_prev.p, nullptr);
+                                                             x->wb_prev.p, x->wb_prev_lo.p);
   }
   RW_CUDA(cudaGetLastError());
   x->dirty = false;
@@ -1686,9 +1688,13 @@ void launch_cluster(rw_ctx* x, void* kernel, const void* layers, const ClParams&
 
 void run_forward_cluster(rw_ctx* x, cudaStream_t s) {
   launch_cluster(x, x->cl_f.kern, x->fwd_layers.p, cl_params(x, true), x->rows_f, x->cl_f.smem, s, true);
-  if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, bf16 plain
+  if (x->pp_next_xop) {  // next stage's layer input (its dW_0 operand): h_{last, 0..T-1}, plain planes
     RW_CUDA(cudaMemcpyAsync(x->pp_next_xop, static_cast<uint8_t*>(x->hop[x->L - 1].p(0)) + (size_t)x->Hp * x->Bp * 2,
                             (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
+    if (x->pp_next_xop_lo)
+      RW_CUDA(cudaMemcpyAsync(x->pp_next_xop_lo,
+                              static_cast<uint8_t*>(x->hop[x->L - 1].p(1)) + (size_t)x->Hp * x->Bp * 2,
+                              (size_t)x->Hp * x->Bp * x->T * 2, cudaMemcpyDefault, s));
     ++g_launches;
     k_pp_signal<<<1, 1, 0, s>>>(x->pp_next_ready, static_cast<const uint32_t*>(x->cl_epoch.p));
     RW_CUDA(cudaGetLastError());
@@ -2810,8 +2816,8 @@ static void* open_region(rw_ctx* x, const rw_pp_ring* peer, int i) {
 
 extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
   return guarded(x, [&] {
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16)
-      einval("rw_pp_export: the layer pipeline needs the cluster schedule in both directions (bf16)");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->kind != kCellLstm)
+      einval("rw_pp_export: the layer pipeline needs LSTM cells on the cluster schedule in both directions");
     if (dir != 0 && dir != 1) einval("rw_pp_export: dir must be 0 (forward) or 1 (backward)");
     RW_CUDA(cudaSetDevice(x->dev));
     memset(out, 0, sizeof *out);
@@ -2824,12 +2830,22 @@ extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
       x->xin_flags.alloc((size_t)x->T * 4);
       export_region(out, 0, x->xsw.p, x->xsw.p);
       export_region(out, 1, x->xin_flags.p, x->xin_flags.p);
-      export_region(out, 2, x->xin_flags.p, x->xin_flags.p);
+      // fp16x2: the plain layer-input lo plane (bf16: unused, the counters again)
+      export_region(out, 2, x->x_op.p(1) ? x->x_op.p(1) : x->xin_flags.p, x->x_op.p(1) ? x->x_op.p(1) : x->xin_flags.p);
       export_region(out, 3, x->x_op.p(0), x->x_op.p(0));
       export_region(out, 4, x->cl_epoch.p, static_cast<uint32_t*>(x->cl_epoch.p) + 2);
       ClOff& o = x->off_f_h[0];
       o.op_flags = static_cast<const uint32_t*>(x->xin_flags.p);
       o.sys = 1;  // written by another process: system-scope waits
+      if (x->prec == kF16x2) {
+        // this stage's layer input is an h (the previous stage's, 2^kHScaleLog2 planes), not x:
+        // the first layer's W.x unscale and its dW GEMM's alpha follow
+        o.unscale = pow2f(-(kWScaleLog2 + kHScaleLog2));
+        GemmDesc d0;
+        RW_CUDA(cudaMemcpy(&d0, x->gemm_wg.p, sizeof d0, cudaMemcpyDeviceToHost));
+        d0.alpha = pow2f(-(kGScaleLog2 + kHScaleLog2));
+        RW_CUDA(cudaMemcpy(x->gemm_wg.p, &d0, sizeof d0, cudaMemcpyHostToDevice));
+      }
       x->pp_prev = true;
       x->pp_exported_f = true;
     } else {
@@ -2854,9 +2870,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
   x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->prec != kBF16 ||
-        x->kind != kCellLstm)
-      einval("rw_pp_link: the layer pipeline needs LSTM cells on the cluster schedule in both directions (bf16)");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->kind != kCellLstm)
+      einval("rw_pp_link: the layer pipeline needs LSTM cells on the cluster schedule in both directions");
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
     const long long G4p = 4LL * Hp;
@@ -2873,6 +2888,7 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
       top.peer_flags = peer_flags;
       RW_CUDA(cudaMemcpy(dev_top, &top, sizeof top, cudaMemcpyHostToDevice));
       x->pp_next_xop = open_region(x, peer, 3);
+      if (x->prec == kF16x2) x->pp_next_xop_lo = open_region(x, peer, 2);
       x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
       x->pp_next = true;
       invalidate_graphs(x);
@@ -2884,11 +2900,17 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
     o.consumed = static_cast<const uint32_t*>(open_region(x, peer, 2));
     o.sys = 1;
     o.active = 1;
-    o.unscale = 1.0f;  // bf16 only (above)
+    o.unscale = x->prec == kF16x2 ? pow2f(-(kWScaleLog2 + kGScaleLog2)) : 1.0f;  // W^T.dG planes' scales
     o.ko = peer->ko;   // the receiving ring's publication count (rw_pp_export)
     {
       if (!x->pp_prev) einval("rw_pp_link: backward link needs this stage's forward ring exported first");
       x->wb_prev.alloc((size_t)Hp * 2 * G4p * 2);
+      if (x->prec == kF16x2) {  // fp16x2: the lo plane lives in tensor memory (the TMEM-A operand)
+        x->wb_prev_lo.alloc((size_t)Hp * 2 * G4p * 2);
+        o.alo = static_cast<const uint16_t*>(x->wb_prev_lo.p);
+        o.alo_ld = (int)(2 * G4p);
+        o.alo_rows = Hp;
+      }
       o.kdim = (int)G4p;
       o.op = static_cast<const uint8_t*>(x->dgsw[0].p);
       o.op_blk_off = 0;

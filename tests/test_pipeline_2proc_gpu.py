@@ -21,7 +21,7 @@ DIMS = Dims(4, 128, 96, 32, 6)
 SEED = 53
 
 
-def _stage_proc(k, n, conn):
+def _stage_proc(k, n, conn, precision):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -33,7 +33,7 @@ def _stage_proc(k, n, conn):
     try:
         c, params, x, dy, _, _ = mk(DIMS, seed=SEED, bias=True)
         H, B, T = c.hidden, c.batch, c.steps
-        st = PipelineStage(c, k, n)
+        st = PipelineStage(c, k, n, precision=precision)
         st.set_params(params)
         conn.send(("exports", st.export()))
         nxt, prv = conn.recv()
@@ -59,12 +59,13 @@ def _stage_proc(k, n, conn):
         conn.send(("error", repr(e)))
 
 
-def test_two_process_pipeline_matches_single_context():
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_two_process_pipeline_matches_single_context(precision):
     import multiprocessing as mp
     from paper_1604_01946_b200 import Engine
     c, params, x, dy, _, _ = make_case(DIMS, seed=SEED, bias=True)
     H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
-    ref = Engine(c, precision="bf16", schedule="cluster")
+    ref = Engine(c, precision=precision, schedule="cluster")
     ref.set_params(params)
     ref.upload_inputs(x, dy)
     ref.run_pass(2)
@@ -80,7 +81,7 @@ def test_two_process_pipeline_matches_single_context():
     pipes, procs = [], []
     for k in range(n):
         a, b = ctx.Pipe()
-        p = ctx.Process(target=_stage_proc, args=(k, n, b))
+        p = ctx.Process(target=_stage_proc, args=(k, n, b, precision))
         p.start()
         pipes.append(a)
         procs.append(p)

@@ -16,14 +16,15 @@ pytestmark = pytest.mark.gpu
 from oracle import Dims  # noqa: E402
 
 
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
 @pytest.mark.parametrize("dims,n", [(Dims(4, 128, 96, 32, 10), 2), (Dims(3, 64, 64, 16, 7), 3)],
                          ids=["L4H128x2", "L3H64x3"])
-def test_pipeline_matches_single_context(dims, n, monkeypatch):
+def test_pipeline_matches_single_context(dims, n, precision, monkeypatch):
     from paper_1604_01946_b200 import Engine
     from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process
     c, params, x, dy, _, _ = make_case(dims, seed=23, bias=True)
     H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
-    ref = Engine(c, precision="bf16", schedule="cluster")
+    ref = Engine(c, precision=precision, schedule="cluster")
     ref.set_params(params)
     ref.upload_inputs(x, dy)
     ref.run_pass(2)
@@ -36,7 +37,7 @@ def test_pipeline_matches_single_context(dims, n, monkeypatch):
     ref.read_outputs(y_r, dx_r, dw_r, dr_r, db_r)
 
     monkeypatch.setenv("RW_PP_RING", str(T))
-    stages = [PipelineStage(c, k, n) for k in range(n)]
+    stages = [PipelineStage(c, k, n, precision=precision) for k in range(n)]
     for s in stages:
         s.set_params(params)
     link_in_process(stages, params)
