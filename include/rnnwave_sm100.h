@@ -207,7 +207,7 @@ int rw_comm_overlap(rw_ctx* ctx, int on);
  * depend on stage k's recurrence) runs on stage k+1 and writes its per-step partial sums into
  * stage k's last-layer ring. After its forward, stage k also copies its last layer's h sequence
  * into stage k+1's plain layer-input planes (for stage k+1's dW of its first layer).
- * Requires LSTM cells on the cluster schedule in both directions (bf16 or fp32-parity fp16x2
+ * Requires the cluster schedule in both directions (any cell kind; bf16 or fp32-parity fp16x2
  * operands). Exported descriptors carry CUDA
  * IPC handles (cross-process) and raw pointers (same-process stages, tests). */
 typedef struct {

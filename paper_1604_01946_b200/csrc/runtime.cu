@@ -1527,7 +1527,7 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   if (x->pp_prev && x->wb_prev.p) {  // backward boundary group: [W_0^T | R_0^T] of this stage
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
-                                                             x->wb_prev.p, x->wb_prev_lo.p);
+                                                             x->wb_prev.p, x->wb_prev_lo.p, x->G);
   }
   RW_CUDA(cudaGetLastError());
   x->dirty = false;
@@ -2816,8 +2816,8 @@ static void* open_region(rw_ctx* x, const rw_pp_ring* peer, int i) {
 
 extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
   return guarded(x, [&] {
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->kind != kCellLstm)
-      einval("rw_pp_export: the layer pipeline needs LSTM cells on the cluster schedule in both directions");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+      einval("rw_pp_export: the layer pipeline needs the cluster schedule in both directions");
     if (dir != 0 && dir != 1) einval("rw_pp_export: dir must be 0 (forward) or 1 (backward)");
     RW_CUDA(cudaSetDevice(x->dev));
     memset(out, 0, sizeof *out);
@@ -2870,8 +2870,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
   x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER || x->kind != kCellLstm)
-      einval("rw_pp_link: the layer pipeline needs LSTM cells on the cluster schedule in both directions");
+    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
+      einval("rw_pp_link: the layer pipeline needs the cluster schedule in both directions");
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
     const long long G4p = 4LL * Hp;
@@ -2912,7 +2912,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
         o.alo_rows = Hp;
       }
       o.kdim = (int)G4p;
-      o.op = static_cast<const uint8_t*>(x->dgsw[0].p);
+      // W^T . dgw (GRU: the W-side image, dgw != dgr in the candidate gate)
+      o.op = static_cast<const uint8_t*>(x->kind == kCellGru ? x->dgwsw[0].p : x->dgsw[0].p);
       o.op_blk_off = 0;
       o.op_flags = static_cast<const uint32_t*>(x->flags_b.p);
       x->pp_maps[1] = make_map(x->wb_prev.p, x->prec, 2 * G4p, Hp, aK, kTileM);

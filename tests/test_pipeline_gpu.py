@@ -17,8 +17,9 @@ from oracle import Dims  # noqa: E402
 
 
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
-@pytest.mark.parametrize("dims,n", [(Dims(4, 128, 96, 32, 10), 2), (Dims(3, 64, 64, 16, 7), 3)],
-                         ids=["L4H128x2", "L3H64x3"])
+@pytest.mark.parametrize("dims,n", [(Dims(4, 128, 96, 32, 10), 2), (Dims(3, 64, 64, 16, 7), 3),
+                                    (Dims(3, 128, 96, 32, 8, kind=2), 3), (Dims(2, 64, 48, 16, 6, kind=0), 2)],
+                         ids=["L4H128x2", "L3H64x3", "gru-L3H128x3", "rnn-L2H64x2"])
 def test_pipeline_matches_single_context(dims, n, precision, monkeypatch):
     from paper_1604_01946_b200 import Engine
     from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process
@@ -31,9 +32,10 @@ def test_pipeline_matches_single_context(dims, n, precision, monkeypatch):
     ref.sync()
     y_r = np.zeros((H, B * T), np.float32, order="F")
     dx_r = np.zeros((I, B * T), np.float32, order="F")
-    dw_r = [np.zeros((4 * H, I if l == 0 else H), np.float32, order="F") for l in range(L)]
-    dr_r = [np.zeros((4 * H, H), np.float32, order="F") for _ in range(L)]
-    db_r = [np.zeros(4 * H, np.float32) for _ in range(L)]
+    G = {3: 4, 2: 3}.get(getattr(dims, "kind", 3), 1)  # gate count of the cell kind
+    dw_r = [np.zeros((G * H, I if l == 0 else H), np.float32, order="F") for l in range(L)]
+    dr_r = [np.zeros((G * H, H), np.float32, order="F") for _ in range(L)]
+    db_r = [np.zeros(G * H, np.float32) for _ in range(L)]
     ref.read_outputs(y_r, dx_r, dw_r, dr_r, db_r)
 
     monkeypatch.setenv("RW_PP_RING", str(T))
