@@ -207,8 +207,12 @@ int rw_comm_overlap(rw_ctx* ctx, int on);
  * depend on stage k's recurrence) runs on stage k+1 and writes its per-step partial sums into
  * stage k's last-layer ring. After its forward, stage k also copies its last layer's h sequence
  * into stage k+1's plain layer-input planes (for stage k+1's dW of its first layer).
- * Requires the cluster schedule in both directions (any cell kind; bf16 or fp32-parity fp16x2
- * operands). Exported descriptors carry CUDA
+ * That is the cluster schedule (mode 0). On the persistent / stepwise schedules (mode 1, config
+ * E) stage k's last layer stores h_t into stage k+1's plain layer-input planes, stage k+1's first
+ * layer stores its dG_t into stage k's dG-input planes, and stage k's top layer multiplies them
+ * by W_next^T (stage k+1's W_0, exported as region 3 of the forward descriptor) -- each with a
+ * system-scope per-step counter; a stage below the last then needs >= 2 layers. Any cell kind;
+ * bf16 or fp32-parity operands; both stages of a link in the same family. Exported descriptors carry CUDA
  * IPC handles (cross-process) and raw pointers (same-process stages, tests). */
 typedef struct {
   char handle[5][64];     /* cudaIpcMemHandle_t of the regions: dir 0: input image / per-step
@@ -219,15 +223,19 @@ typedef struct {
   int64_t pid;            /* exporting process */
   int device;             /* exporting device */
   int ko;                 /* off members the ring expects per step */
+  int mode;               /* schedule family of the exporting stage: 0 cluster, 1 persistent /
+                             stepwise (both stages of a link must agree) */
 } rw_pp_ring;
 /* dir 0: my layer-input image, its per-step counters and my plain layer-input buffer; dir 1:
  * the backward ring of my last layer. */
 int rw_pp_export(rw_ctx* ctx, int dir, rw_pp_ring* out);
-/* dir 0: link to the NEXT stage's forward export (W_next: unused since the h_t hand-off, may be
- * NULL). dir 1: link to the PREVIOUS stage's backward export. */
+/* dir 0: link to the NEXT stage's forward export (W_next: the next stage's first-layer W in the
+ * reference layout -- cluster: unused; persistent / stepwise: NULL = read it from the export).
+ * dir 1: link to the PREVIOUS stage's backward export. */
 int rw_pp_link(rw_ctx* ctx, int dir, const rw_pp_ring* peer, const float* W_next);
-/* Kept for API compatibility: the forward hand-off sends h_t, so the next stage's weights
- * need no refresh here after a parameter update (validates that a forward link exists). */
+/* After the next stage's parameters changed: cluster -- nothing to refresh (the forward hand-off
+ * sends h_t); persistent / stepwise -- re-pack W_next (optionally from a new pointer) into the
+ * top layer's backward image on the next pass. Validates that a forward link exists. */
 int rw_pp_set_next_w(rw_ctx* ctx, const float* W_next);
 
 /* cells.hpp:65-68: 2 * 4 * H * (I + H) * B multiply-add FLOPs per cell. */

@@ -44,7 +44,8 @@ class rw_config(C.Structure):
 
 class rw_pp_ring(C.Structure):
     _fields_ = [("handle", (C.c_char * 64) * 5), ("offset", C.c_uint64 * 5), ("ptr", C.c_uint64 * 5),
-                ("pid", C.c_int64), ("device", C.c_int), ("ko", C.c_int)]
+                ("pid", C.c_int64), ("device", C.c_int), ("ko", C.c_int),
+                ("mode", C.c_int)]
 
 
 _lib = None

@@ -74,6 +74,11 @@ struct FwdLayer {
   // input counters -- the last layer of a stage also writes h_t there (block t) and releases it
   uint8_t* hsw_peer;
   uint32_t* peer_flags;
+  // layer pipeline, persistent / stepwise schedules: the next stage's plain layer-input planes
+  // (x_op, row length peer_ld) -- the last layer stores h_t into block t there, then releases
+  // peer_flags[t] (system scope) once per CTA
+  void* xop_peer[2];
+  int peer_ld;
 };
 
 struct BwdLayer {
@@ -113,6 +118,11 @@ struct BwdLayer {
   float* dgr;
   void* dgrop[2];
   uint8_t* dgwsw;
+  // layer pipeline, persistent / stepwise schedules: the previous stage's dG-input planes (the
+  // layout of dgop) -- the first layer stores its W-side dG_t there too, then releases
+  // peer_flags[t] (system scope) once per CTA
+  void* dg_peer[2];
+  uint32_t* peer_flags;
 };
 
 struct RecParams {
@@ -142,7 +152,17 @@ struct RecParams {
   unsigned int* progress;     // debug only (RW_DEBUG_HANG_S): [cta][4] role progress words
   unsigned long long* trace;  // optional [cta][n_steps][8] %globaltimer stamps (RW_TRACE)
   int kind;                   // cell kind (CellKindDev): the RNN variants share one instantiation
+  // layer pipeline (persistent / stepwise): per-step counters a neighbouring stage releases at
+  // system scope -- forward: layer 0's input h_t; backward: the top layer's dG from above.
+  // Cumulative over passes: target = *pp_epoch (this context's pass count in that direction)
+  // x pp_in_flags[T] (the sender's CTAs per step, written at link time).
+  const uint32_t* pp_in_flags;
+  const uint32_t* pp_epoch;
 };
+
+__device__ __forceinline__ uint32_t pp_target(const RecParams& p) {
+  return p.pp_in_flags ? *p.pp_epoch * p.pp_in_flags[p.T] : 0u;
+}
 
 // Trace stamps per (CTA, step): 0 producer starts waiting for its inputs, 1 inputs ready
 // (flags acquired, loads issued), 2 accumulator ready in TMEM, 3 partials pushed, 4 exchange
@@ -249,6 +269,45 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
                                           const RecParams& p, int code) {
   wait_flag(flag, target, p.error, p.timeout_ns, code);
+}
+// Flag operations at gpu or system scope (system: the counter is shared with a peer GPU).
+__device__ __forceinline__ uint32_t ld_relaxed_s(const uint32_t* p, bool sys) {
+  uint32_t v;
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_flag_s(const uint32_t* flag, uint32_t target, bool sys, int* error,
+                                            unsigned long long timeout_ns, int code) {
+  if (!sys) {
+    wait_flag(flag, target, error, timeout_ns, code);
+    return;
+  }
+  const uint64_t t0 = globaltimer();
+#pragma unroll 1
+  while (!flag_reached(ld_relaxed_s(flag, true), target)) {
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicCAS(error, 0, code);
+      atomicMax(error + 1, (int)ld_relaxed_s(flag, true));
+      return;
+    }
+  }
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+}
+__device__ __forceinline__ void red_release_s(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    red_release_gpu_add(p, v);
+}
+__device__ __forceinline__ void red_relaxed_s(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    red_relaxed_gpu_add(p, v);
 }
 // error code: 1<<30 | dir<<28 | layer<<20 | (t+2)<<4 | which
 __device__ __forceinline__ int wait_code(int dir, int l, int t, int which) {
@@ -620,6 +679,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       prefetch_tmap(Ly.bx2);
       prefetch_tmap(Ly.bh2);
       const int t = p.t_first;
+      if (l == 0 && p.pp_in_flags) {  // pipeline stage: h_t of the previous stage
+        wait_flag_s(&p.pp_in_flags[t], pp_target(p), true, p.error, p.timeout_ns, wait_code(0, l, t, 1));
+        fence_proxy_async_global();
+      }
       uint32_t pc = 0;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++pc) {
         const int s = pc % p.stages;
@@ -681,6 +744,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (!p.resident && kb + p.a_prefetch < kb_hi && p.a_prefetch > 0)
           for (int pl = 0; pl < P::kPlanes; ++pl)
             tma_prefetch_2d(Ly.a[pl], (kb + p.a_prefetch + akofs) * P::kAtomK, row0);
+        if (seg0 && !x_ready && l == 0 && p.pp_in_flags) {  // pipeline stage (any schedule)
+          wait_flag_s(&p.pp_in_flags[t], pp_target(p), true, p.error, p.timeout_ns, wait_code(0, l, t, 1));
+          fence_proxy_async_global();
+          x_ready = true;
+        }
         if (p.persistent) {
           if (seg0 && !x_ready) {
             progress(p, 0, it, 2);
@@ -876,6 +944,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           }
           Le.h[col_new * Hp + u] = hv;
           store_operand<P>(Le.hop, col_new * Hp + u, kF16Ops<P> ? hv * pow2f(kHScaleLog2) : hv);
+          if (Le.xop_peer[0] && u < Le.peer_ld)  // pipeline: the next stage's layer input, block t
+            store_operand<P>(Le.xop_peer, col_prev * Le.peer_ld + u, kF16Ops<P> ? hv * pow2f(kHScaleLog2) : hv);
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 5);
         xchg_release(S, ks);
@@ -889,6 +959,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (et == 0) {
           __threadfence();
           red_release_gpu_add(&Le.flags[t], 1);
+        }
+      }
+      if (Le.xop_peer[0]) {  // pipeline: publish h_t to the next stage (system scope)
+        if (!p.persistent) {
+          fence_proxy_async_global();
+          named_bar_sync(1, kEpiThreads);
+        }
+        if (et == 0) {
+          __threadfence_system();
+          red_release_s(Le.peer_flags + t, 1, true);
         }
       }
       if (et == 0) trace_stamp(p, it, 7);
@@ -912,7 +992,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   __shared__ const uint32_t* up_flags;
   if (threadIdx.x == 0) {
     Ly = layers[l];
-    up_flags = Ly.has_up ? layers[l + 1].flags : nullptr;
+    up_flags = Ly.has_up && l + 1 < p.L ? layers[l + 1].flags : nullptr;  // top + pipeline: pp_in_flags
     set_wait_error(p.error);
   }
   __syncthreads();
@@ -982,6 +1062,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (!p.resident && p.a_prefetch > 0 && kb + p.a_prefetch < kb_hi && kb_active(kb + p.a_prefetch, t))
           for (int pl = 0; pl < P::kPlanes; ++pl)
             tma_prefetch_2d(Ly.a[pl], (kb + p.a_prefetch + akofs) * P::kAtomK, row0);
+        if (seg0 && !up_ready && l == p.L - 1 && p.pp_in_flags) {  // pipeline: dG_t from the next stage
+          wait_flag_s(&p.pp_in_flags[t], pp_target(p), true, p.error, p.timeout_ns, wait_code(1, l, t, 1));
+          fence_proxy_async_global();
+          up_ready = true;
+        }
         if (p.persistent) {
           if (seg0 && !up_ready) {
             progress(p, 0, it, 2);
@@ -1265,6 +1350,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
               store_operand<P>(Le.dgop, ob + rho_of(1, u), gf * kGS);
               store_operand<P>(Le.dgop, ob + rho_of(2, u), go * kGS);
               store_operand<P>(Le.dgop, ob + rho_of(3, u), gc * kGS);
+              if (Le.dg_peer[0]) {  // pipeline: the previous stage's dG input (W-side, as dgop)
+                store_operand<P>(Le.dg_peer, ob + rho_of(0, u), gi * kGS);
+                store_operand<P>(Le.dg_peer, ob + rho_of(1, u), gf * kGS);
+                store_operand<P>(Le.dg_peer, ob + rho_of(2, u), go * kGS);
+                store_operand<P>(Le.dg_peer, ob + rho_of(3, u), gc * kGS);
+              }
               if constexpr (kKind == kCellGru) {  // dgr: r, u as dgw, candidate dnp r (cells.hpp:527-529)
                 float* dgq = Le.dgr + col * G4 + u;
                 dgq[0] = gi;
@@ -1300,6 +1391,16 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         if (et == 0) {
           __threadfence();
           red_release_gpu_add(&Le.flags[t], 1);
+        }
+      }
+      if (Le.dg_peer[0] && t >= 0) {  // pipeline: publish dG_t to the previous stage
+        if (!p.persistent) {
+          fence_proxy_async_global();
+          named_bar_sync(1, kEpiThreads);
+        }
+        if (et == 0) {
+          __threadfence_system();
+          red_release_s(Le.peer_flags + t, 1, true);
         }
       }
       if (et == 0) trace_stamp(p, it, 7);

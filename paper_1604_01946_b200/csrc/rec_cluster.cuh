@@ -197,45 +197,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// Flag operations at gpu or system scope (system: the counter is shared with a peer GPU).
-__device__ __forceinline__ uint32_t ld_relaxed_s(const uint32_t* p, bool sys) {
-  uint32_t v;
-  if (sys)
-    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  else
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void wait_flag_s(const uint32_t* flag, uint32_t target, bool sys, int* error,
-                                            unsigned long long timeout_ns, int code) {
-  if (!sys) {
-    wait_flag(flag, target, error, timeout_ns, code);
-    return;
-  }
-  const uint64_t t0 = globaltimer();
-#pragma unroll 1
-  while (!flag_reached(ld_relaxed_s(flag, true), target)) {
-    if (globaltimer() - t0 > timeout_ns) {
-      atomicCAS(error, 0, code);
-      atomicMax(error + 1, (int)ld_relaxed_s(flag, true));
-      return;
-    }
-  }
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-}
-__device__ __forceinline__ void red_release_s(uint32_t* p, uint32_t v, bool sys) {
-  if (sys)
-    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-  else
-    red_release_gpu_add(p, v);
-}
-__device__ __forceinline__ void red_relaxed_s(uint32_t* p, uint32_t v, bool sys) {
-  if (sys)
-    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-  else
-    red_relaxed_gpu_add(p, v);
-}
 
 // Receive slot of sender s at owner d (senders = every member but d, in member order).
 __device__ __forceinline__ int cl_slot(int s, int d) { return s < d ? s : s - 1; }

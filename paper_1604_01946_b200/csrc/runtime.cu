@@ -305,11 +305,22 @@ struct rw_ctx {
   DevBuf repack_jobs;                        // k_repack's job table (built on the first repack)
   int repack_njobs = 0, repack_tiles = 0;
   DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
-  std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(2);
+  // [0] forward / [1] backward boundary group (cluster); [2..3] the top layer's [W_next^T | R^T]
+  // planes, [4..5] its dG-input planes, [6] the same as CTA-pair boxes (persistent / stepwise)
+  std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(8);
   DevBuf pp_maps_dev;
   void* pp_next_xop = nullptr;               // next stage's layer-input operand (peer pointer)
   uint32_t* pp_next_ready = nullptr;         // next stage's input-ready counter (peer pointer)
   std::vector<void*> pp_opened;              // IPC-opened peer allocations
+  // layer pipeline over the persistent / stepwise schedules: h_t stored straight into the next
+  // stage's layer-input planes; the next stage's first-layer dG_t stored into this stage's dgin
+  // planes, which its top layer multiplies by W_next^T (the peer's W_0, pp_wnext) exactly as one
+  // context's layer below would
+  bool pp_plain = false;
+  Operand dgin;
+  DevBuf dgin_flags;                         // [T] per-step counters + [T] the sender's CTAs per step
+  const float* pp_wnext = nullptr;
+  bool pp_up = false;                        // the top layer's backward reads dgin (has_up)
   std::vector<DevBuf> hsw, dgsw;  // pre-swizzled bf16 operand step blocks (sw_off)
   // GRU: zrh tapes, R-side gate gradients dgr (fp32 tape + operand planes), the W-side image dgwsw
   std::vector<DevBuf> zrh, dgr, dgwsw;
@@ -1484,11 +1495,12 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
       RepackJob b{};
       b.kind = kRepackC;
       b.rows = Hp;
-      b.K = (l < L - 1 ? 2 : 1) * 4 * Hp;
+      const bool up = l < L - 1 || x->pp_up;  // pipeline: the next stage's W_0 above the top layer
+      b.K = (up ? 2 : 1) * 4 * Hp;
       b.tiles_k = ceil_div(b.K, kRepackTileK);
       b.src_rows = H;
       b.src_k0 = 4 * Hp;
-      b.s0 = l < L - 1 ? x->W[l + 1].f() : nullptr;
+      b.s0 = l < L - 1 ? x->W[l + 1].f() : up ? x->pp_wnext : nullptr;
       b.s1 = x->R[l].f();
       b.p0 = x->wb[l].p(0);
       b.p1 = x->wb[l].p(1);
@@ -1557,6 +1569,15 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   }
   rp.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
+  if (fwd && x->pp_plain && x->pp_prev) {  // layer 0's input is the previous stage's h_t
+    rp.pp_in_flags = static_cast<const uint32_t*>(x->xin_flags.p);
+    rp.pp_epoch = static_cast<const uint32_t*>(x->cl_epoch.p);
+    rp.us_in0 = rp.us_in;  // fp16x2: h planes (2^kHScaleLog2), not x
+  }
+  if (!fwd && x->pp_up) {  // the top layer's d_above comes from the next stage
+    rp.pp_in_flags = static_cast<const uint32_t*>(x->dgin_flags.p);
+    rp.pp_epoch = static_cast<const uint32_t*>(x->cl_epoch.p) + 1;
+  }
   rp.a_prefetch = 0;  // measured: no gain at config E (0 4 8 16 32 -> 727 702 694 701 660 TFLOP/s)
   if (const char* e = getenv("RW_A_PREFETCH")) rp.a_prefetch = atoi(e);
   rp.error = static_cast<int*>(x->errflag.p);
@@ -1702,7 +1723,37 @@ void run_forward_cluster(rw_ctx* x, cudaStream_t s) {
 }
 
 template <class P>
+void run_forward_rec_body(rw_ctx* x, cudaStream_t s, bool training);
+template <class P>
+void run_backward_rec_body(rw_ctx* x, cudaStream_t s);
+
+// Pipeline stages on the persistent / stepwise schedules count their passes (the targets of the
+// cumulative peer counters) and, after the forward, tell the next stage its input landed.
+template <class P>
 void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
+  const bool pp = x->pp_plain && (x->pp_prev || x->pp_next);
+  if (pp) {
+    ++g_launches;
+    k_epoch_inc<<<1, 1, 0, s>>>(static_cast<uint32_t*>(x->cl_epoch.p));
+  }
+  run_forward_rec_body<P>(x, s, training);
+  if (pp && x->pp_next) {
+    ++g_launches;
+    k_pp_signal<<<1, 1, 0, s>>>(x->pp_next_ready, static_cast<const uint32_t*>(x->cl_epoch.p));
+  }
+  RW_CUDA(cudaGetLastError());
+}
+template <class P>
+void run_backward_rec(rw_ctx* x, cudaStream_t s) {
+  if (x->pp_plain && x->pp_up) {
+    ++g_launches;
+    k_epoch_inc<<<1, 1, 0, s>>>(static_cast<uint32_t*>(x->cl_epoch.p) + 1);
+  }
+  run_backward_rec_body<P>(x, s);
+}
+
+template <class P>
+void run_forward_rec_body(rw_ctx* x, cudaStream_t s, bool training) {
   if (x->fwd_sched == RW_SCHED_CLUSTER) {
     run_forward_cluster(x, s);
     return;
@@ -1796,7 +1847,7 @@ void run_forward_rec(rw_ctx* x, cudaStream_t s, bool training) {
 }
 
 template <class P>
-void run_backward_rec(rw_ctx* x, cudaStream_t s) {
+void run_backward_rec_body(rw_ctx* x, cudaStream_t s) {
   for (int l = 0; l < x->L; ++l) RW_CUDA(cudaMemsetAsync(x->dbp[l].p, 0, x->dbp[l].bytes, s));
   if (x->bwd_sched == RW_SCHED_CLUSTER) {
     launch_cluster(x, x->cl_b.kern, x->bwd_layers.p, cl_params(x, false), x->rows_b, x->cl_b.smem, s, false);
@@ -2814,15 +2865,118 @@ static void* open_region(rw_ctx* x, const rw_pp_ring* peer, int i) {
   return static_cast<uint8_t*>(base) + peer->offset[i];
 }
 
+// Schedule family of a pipeline stage: 0 cluster (boundary groups, swizzled images), 1 the
+// persistent / stepwise kernels (plain operand planes written per step by the neighbour).
+static int pp_family(rw_ctx* x, const char* fn) {
+  auto plain = [](int s) { return s == RW_SCHED_PERSISTENT || s == RW_SCHED_STEPWISE; };
+  if (x->fwd_sched == RW_SCHED_CLUSTER && x->bwd_sched == RW_SCHED_CLUSTER) return 0;
+  if (plain(x->fwd_sched) && plain(x->bwd_sched)) {
+    if (x->fwd_batch)
+      einval(std::string(fn) + ": the layer pipeline does not batch the input projections (set RW_FWD_BATCH=0)");
+    return 1;
+  }
+  einval(std::string(fn) + ": the layer pipeline needs the cluster schedule in both directions, or the "
+         "persistent / stepwise schedules in both");
+  return -1;
+}
+
+// fp16x2: a stage's layer input is an h (2^kHScaleLog2 planes), not x: its first layer's dW
+// GEMM alpha follows (the W.x unscale: ClOff::unscale / RecParams::us_in0)
+static void pp_input_is_h(rw_ctx* x) {
+  if (x->prec != kF16x2) return;
+  GemmDesc d0;
+  RW_CUDA(cudaMemcpy(&d0, x->gemm_wg.p, sizeof d0, cudaMemcpyDeviceToHost));
+  d0.alpha = pow2f(-(kGScaleLog2 + kHScaleLog2));
+  RW_CUDA(cudaMemcpy(x->gemm_wg.p, &d0, sizeof d0, cudaMemcpyHostToDevice));
+}
+
+static void pp_upload_maps(rw_ctx* x) {
+  if (!x->pp_maps_dev.p) x->pp_maps_dev.alloc(x->pp_maps.size() * sizeof(CUtensorMap));
+  RW_CUDA(cudaMemcpy(x->pp_maps_dev.p, x->pp_maps.data(), x->pp_maps.size() * sizeof(CUtensorMap),
+                     cudaMemcpyHostToDevice));
+}
+
+// Persistent / stepwise stage with a next stage: once both the dG input planes (rw_pp_export
+// dir 1) and the next stage's W_0 (rw_pp_link dir 0) are known, the top layer's backward
+// becomes an inner layer's: A = [W_next^T | R^T] (packed by k_repack), the up operand = dgin,
+// its per-step counter released by the next stage -- the same K order and accumulation as one
+// context holding both stages, so the results match it bit for bit.
+static void pp_plain_up(rw_ctx* x) {
+  if (x->pp_up || !x->pp_wnext || !x->dgin.p(0)) return;
+  const int L = x->L, Hp = x->Hp, aK = x->atomK;
+  const long long G4p = 4LL * Hp, colsT = (long long)x->Bp * x->T;
+  if (L == 1)  // the backward plan (k-blocks per accumulator, resident slots) covered R^T only
+    einval("rw_pp_link: on the persistent / stepwise schedules a stage below the last needs >= 2 layers");
+  x->wb[L - 1].alloc(x->prec, (size_t)Hp * 2 * G4p);
+  for (int p = 0; p < x->planes; ++p) {
+    x->pp_maps[2 + p] = make_map(x->wb[L - 1].p(p), x->prec, 2 * G4p, Hp, aK, kTileM);
+    x->pp_maps[4 + p] = make_map(x->dgin.p(p), x->prec, G4p, colsT, aK, x->Bp);
+  }
+  if (x->pair_b) x->pp_maps[6] = make_map(x->dgin.p(0), x->prec, G4p, colsT, aK, x->Bp / 2);
+  pp_upload_maps(x);
+  const CUtensorMap* MD = static_cast<const CUtensorMap*>(x->pp_maps_dev.p);
+  BwdLayer b;
+  BwdLayer* dev = static_cast<BwdLayer*>(x->bwd_layers.p) + (L - 1);
+  RW_CUDA(cudaMemcpy(&b, dev, sizeof b, cudaMemcpyDeviceToHost));
+  for (int p = 0; p < 2; ++p) {
+    b.a[p] = p < x->planes ? MD + 2 + p : nullptr;
+    b.bup[p] = p < x->planes ? MD + 4 + p : nullptr;
+  }
+  b.bup2 = x->pair_b ? MD + 6 : nullptr;
+  b.has_up = 1;
+  b.dy = nullptr;  // an inner layer of the whole stack: its output gradient is d_above only
+  RW_CUDA(cudaMemcpy(dev, &b, sizeof b, cudaMemcpyHostToDevice));
+  x->pp_up = true;
+  x->repack_njobs = 0;  // rebuild the repack table: the top layer's image now holds W_next^T too
+  x->dirty = true;
+}
+
+// CTAs of one layer that release a per-step counter (persistent / stepwise kernels)
+static uint32_t pp_senders(rw_ctx* x, bool fwd) {
+  const RecParams rp = rec_params(x, fwd);
+  return (uint32_t)(!fwd && x->pair_b ? rp.tiles : rp.tiles * rp.ksplit);
+}
+
 extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
   return guarded(x, [&] {
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
-      einval("rw_pp_export: the layer pipeline needs the cluster schedule in both directions");
+    const int fam = pp_family(x, "rw_pp_export");
     if (dir != 0 && dir != 1) einval("rw_pp_export: dir must be 0 (forward) or 1 (backward)");
     RW_CUDA(cudaSetDevice(x->dev));
     memset(out, 0, sizeof *out);
     out->pid = (int64_t)getpid();
     out->device = x->dev;
+    out->mode = fam;
+    if (fam == 1) {
+      x->pp_plain = true;
+      if (!x->cl_epoch.p) x->cl_epoch.alloc(16);
+      const size_t nf = (size_t)(x->T + 1) * 4;
+      if (dir == 0) {
+        // forward: the previous stage's last layer stores h_t into block t of these planes (the
+        // layer-0 input operand, read by the step kernels and by the dW_0 GEMM) and releases
+        // xin_flags[t]; it also reads our W_0 (region 3) for its top layer's backward
+        x->xin_flags.alloc(nf);
+        export_region(out, 0, x->x_op.p(0), x->x_op.p(0));
+        export_region(out, 1, x->xin_flags.p, x->xin_flags.p);
+        export_region(out, 2, x->x_op.p(1) ? x->x_op.p(1) : x->xin_flags.p, x->x_op.p(1) ? x->x_op.p(1) : x->xin_flags.p);
+        export_region(out, 3, x->W[0].p, x->W[0].p);
+        export_region(out, 4, x->cl_epoch.p, static_cast<uint32_t*>(x->cl_epoch.p) + 2);
+        pp_input_is_h(x);
+        x->pp_prev = true;
+        x->pp_exported_f = true;
+      } else {
+        // backward: the next stage's first layer stores its W-side dG_t here (dgop's layout)
+        const long long colsT = (long long)x->Bp * x->T;
+        x->dgin.alloc(x->prec, (size_t)4 * x->Hp * colsT);
+        x->dgin_flags.alloc(nf);
+        export_region(out, 0, x->dgin.p(0), x->dgin.p(0));
+        export_region(out, 1, x->dgin_flags.p, x->dgin_flags.p);
+        export_region(out, 2, x->dgin.p(1) ? x->dgin.p(1) : x->dgin_flags.p, x->dgin.p(1) ? x->dgin.p(1) : x->dgin_flags.p);
+        x->pp_exported_b = true;
+        pp_plain_up(x);
+      }
+      invalidate_graphs(x);
+      return;
+    }
     if (dir == 0) {
       // forward: the previous stage writes its last layer's h_t (bf16 operand image, H x B x 2 B
       // per step) straight into this stage's layer-input image over NVLink and releases a
@@ -2837,15 +2991,8 @@ extern "C" int rw_pp_export(rw_ctx* x, int dir, rw_pp_ring* out) {
       ClOff& o = x->off_f_h[0];
       o.op_flags = static_cast<const uint32_t*>(x->xin_flags.p);
       o.sys = 1;  // written by another process: system-scope waits
-      if (x->prec == kF16x2) {
-        // this stage's layer input is an h (the previous stage's, 2^kHScaleLog2 planes), not x:
-        // the first layer's W.x unscale and its dW GEMM's alpha follow
-        o.unscale = pow2f(-(kWScaleLog2 + kHScaleLog2));
-        GemmDesc d0;
-        RW_CUDA(cudaMemcpy(&d0, x->gemm_wg.p, sizeof d0, cudaMemcpyDeviceToHost));
-        d0.alpha = pow2f(-(kGScaleLog2 + kHScaleLog2));
-        RW_CUDA(cudaMemcpy(x->gemm_wg.p, &d0, sizeof d0, cudaMemcpyHostToDevice));
-      }
+      if (x->prec == kF16x2) o.unscale = pow2f(-(kWScaleLog2 + kHScaleLog2));  // h planes, not x
+      pp_input_is_h(x);
       x->pp_prev = true;
       x->pp_exported_f = true;
     } else {
@@ -2870,11 +3017,46 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
   x->state0_zero = false;  // conservatively re-stage the state blocks after relinking
   return guarded(x, [&] {
     if (!peer) einval("rw_pp_link: peer descriptor is null");
-    if (x->fwd_sched != RW_SCHED_CLUSTER || x->bwd_sched != RW_SCHED_CLUSTER)
-      einval("rw_pp_link: the layer pipeline needs the cluster schedule in both directions");
+    const int fam = pp_family(x, "rw_pp_link");
+    if (peer->mode != fam) einval("rw_pp_link: the two stages use different schedule families (cluster vs persistent/stepwise)");
+    if (dir != 0 && dir != 1) einval("rw_pp_link: dir must be 0 (forward) or 1 (backward)");
     RW_CUDA(cudaSetDevice(x->dev));
     const int L = x->L, H = x->H, Hp = x->Hp, T = x->T, aK = x->atomK;
     const long long G4p = 4LL * Hp;
+    if (fam == 1) {
+      x->pp_plain = true;
+      if (!x->cl_epoch.p) x->cl_epoch.alloc(16);
+      void* p0 = open_region(x, peer, 0);
+      uint32_t* flags = static_cast<uint32_t*>(open_region(x, peer, 1));
+      void* p1 = x->planes > 1 ? open_region(x, peer, 2) : nullptr;
+      // the receiver's per-pass target: our CTAs per step (slot T of its counters)
+      const uint32_t cnt = pp_senders(x, dir == 0);
+      RW_CUDA(cudaMemcpy(flags + T, &cnt, 4, cudaMemcpyDefault));
+      if (dir == 0) {  // forward: our last layer stores h_t into the next stage's input planes
+        FwdLayer top;
+        FwdLayer* dev = static_cast<FwdLayer*>(x->fwd_layers.p) + (L - 1);
+        RW_CUDA(cudaMemcpy(&top, dev, sizeof top, cudaMemcpyDeviceToHost));
+        top.xop_peer[0] = p0;
+        top.xop_peer[1] = p1;
+        top.peer_ld = Hp;  // the next stage's Ip = round_up(H, 64) = Hp
+        top.peer_flags = flags;
+        RW_CUDA(cudaMemcpy(dev, &top, sizeof top, cudaMemcpyHostToDevice));
+        x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
+        x->pp_wnext = W_next ? W_next : static_cast<const float*>(open_region(x, peer, 3));
+        x->pp_next = true;
+        pp_plain_up(x);
+      } else {  // backward: our first layer stores its W-side dG_t into the previous stage's planes
+        BwdLayer b0;
+        BwdLayer* dev = static_cast<BwdLayer*>(x->bwd_layers.p);
+        RW_CUDA(cudaMemcpy(&b0, dev, sizeof b0, cudaMemcpyDeviceToHost));
+        b0.dg_peer[0] = p0;
+        b0.dg_peer[1] = p1;
+        b0.peer_flags = flags;
+        RW_CUDA(cudaMemcpy(dev, &b0, sizeof b0, cudaMemcpyHostToDevice));
+      }
+      invalidate_graphs(x);
+      return;
+    }
     if (dir == 0) {
       // forward: our last layer's critical CTAs also store h_t into the next stage's input image
       // and release its per-step counter (rec_cluster.cuh k_cl_fwd); W_next is not needed
@@ -2919,9 +3101,8 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
       x->pp_maps[1] = make_map(x->wb_prev.p, x->prec, 2 * G4p, Hp, aK, kTileM);
       x->dirty = true;  // repack_params packs [W_0^T | R_0^T] into wb_prev
     }
-    // two fixed map slots [forward boundary, backward boundary], device copy allocated once
-    if (!x->pp_maps_dev.p) x->pp_maps_dev.alloc(2 * sizeof(CUtensorMap));
-    RW_CUDA(cudaMemcpy(x->pp_maps_dev.p, x->pp_maps.data(), 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    // fixed map slots [forward boundary, backward boundary, ...], device copy allocated once
+    pp_upload_maps(x);
     o.a = static_cast<const CUtensorMap*>(x->pp_maps_dev.p) + dir;
     std::vector<ClOff>& offs = dir == 0 ? x->off_f_h : x->off_b_h;
     offs.resize(L + 1);
@@ -2946,7 +3127,12 @@ extern "C" int rw_pp_set_next_w(rw_ctx* x, const float* W_next) {
   // own parameter updates), so there is nothing to refresh here -- kept for API compatibility
   return guarded(x, [&] {
     if (!x->pp_next) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
-    (void)W_next;
+    if (x->pp_plain) {  // persistent / stepwise: W_next is packed into the top layer's backward image
+      if (W_next) x->pp_wnext = W_next;
+      x->repack_njobs = 0;
+      x->dirty = true;
+      invalidate_graphs(x);
+    }
   });
 }
 

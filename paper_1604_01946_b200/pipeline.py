@@ -12,6 +12,14 @@ cross-layer wavefront of the paper (PAPER Listing 4) continues across GPUs step 
             ring (its d_above), and stage k copies h_{last_k} into stage k+1's layer input
             (the operand of stage k+1's first-layer dW).
 
+That is the cluster schedule. On the persistent / stepwise schedules (config E: deep stacks at
+batch 256, where the cluster schedule does not fit) the hand-off goes through plain operand
+planes instead: stage k's last layer stores h_t straight into stage k+1's layer-input planes;
+stage k+1's first layer stores its dG_t into stage k's dG-input planes, and stage k's top layer
+multiplies them by W_{first_{k+1}}^T (read from stage k+1's parameters over the link) exactly
+as the layer below does inside one context. Both directions release system-scope per-step
+counters, cumulative over passes.
+
 Exchange order (both the in-process and the torch.distributed variants):
   1. every stage k > 0 exports its forward ring (dir 0), every stage k < n-1 its backward ring
      (dir 1);
@@ -63,11 +71,15 @@ def link_plan(k: int, n: int) -> LinkPlan:
 class PipelineStage:
     """One stage: an Engine over the stage's layers plus the boundary links."""
 
-    def __init__(self, cfg: LadderConfig, k: int, n: int, device: int = 0, precision: str = "bf16"):
+    def __init__(self, cfg: LadderConfig, k: int, n: int, device: int = 0, precision: str = "bf16",
+                 schedule: str = "cluster"):
+        """schedule: "cluster" (boundary groups), or "persistent" / "stepwise" / "auto" resolving to
+        those two (config E's shape): every stage of one pipeline must use the same family, and
+        stages below the last need >= 2 layers there (the top layer's backward takes W_next)."""
         self.k, self.n = k, n
         self.first, self.count = split_layers(cfg.layers, n)[k]
         self.full_cfg = cfg
-        self.engine = Engine(stage_config(cfg, k, n), precision=precision, schedule="cluster", device=device)
+        self.engine = Engine(stage_config(cfg, k, n), precision=precision, schedule=schedule, device=device)
         self.plan = link_plan(k, n)
         self.exports: dict[int, bytes] = {}
 

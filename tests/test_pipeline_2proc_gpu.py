@@ -21,19 +21,20 @@ DIMS = Dims(4, 128, 96, 32, 6)
 SEED = 53
 
 
-def _stage_proc(k, n, conn, precision):
+def _stage_proc(k, n, conn, precision, schedule="cluster"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     sys.path.insert(0, os.path.join(root, "oracle"))
     sys.path.insert(0, os.path.join(root, "tests"))
     os.environ["RW_PP_RING"] = str(DIMS.steps)
+    os.environ["RW_FWD_KSPLIT"] = os.environ["RW_BWD_KSPLIT"] = "1"
     from parity import make_case as mk
     from paper_1604_01946_b200.pipeline import PipelineStage
     try:
         c, params, x, dy, _, _ = mk(DIMS, seed=SEED, bias=True)
         H, B, T = c.hidden, c.batch, c.steps
-        st = PipelineStage(c, k, n, precision=precision)
+        st = PipelineStage(c, k, n, precision=precision, schedule=schedule)
         st.set_params(params)
         conn.send(("exports", st.export()))
         nxt, prv = conn.recv()
@@ -59,13 +60,16 @@ def _stage_proc(k, n, conn, precision):
         conn.send(("error", repr(e)))
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp32"])
-def test_two_process_pipeline_matches_single_context(precision):
+@pytest.mark.parametrize("precision,schedule", [("bf16", "cluster"), ("fp32", "cluster"), ("bf16", "persistent"),
+                                                ("fp32", "stepwise")])
+def test_two_process_pipeline_matches_single_context(precision, schedule, monkeypatch):
     import multiprocessing as mp
     from paper_1604_01946_b200 import Engine
     c, params, x, dy, _, _ = make_case(DIMS, seed=SEED, bias=True)
     H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
-    ref = Engine(c, precision=precision, schedule="cluster")
+    monkeypatch.setenv("RW_FWD_KSPLIT", "1")  # the stages' k-split (the children set the same)
+    monkeypatch.setenv("RW_BWD_KSPLIT", "1")
+    ref = Engine(c, precision=precision, schedule=schedule)
     ref.set_params(params)
     ref.upload_inputs(x, dy)
     ref.run_pass(2)
@@ -81,7 +85,7 @@ def test_two_process_pipeline_matches_single_context(precision):
     pipes, procs = [], []
     for k in range(n):
         a, b = ctx.Pipe()
-        p = ctx.Process(target=_stage_proc, args=(k, n, b, precision))
+        p = ctx.Process(target=_stage_proc, args=(k, n, b, precision, schedule))
         p.start()
         pipes.append(a)
         procs.append(p)
