@@ -29,43 +29,6 @@ __device__ __forceinline__ void store_planes(int prec, void* p0, void* p1, long 
   }
 }
 
-// Forward operand of layer l: rows rho (4Hp), K = [0, Ipl) from W, [Ipl, Ipl+Hp) from R.
-// W and R are column-major (element (row, k) at k*4H + row), the operand is K-major (k
-// contiguous per rho row), so the kernel transposes through shared memory: a block moves a
-// tile of 32 rho rows (one gate of 32 consecutive units = 32 consecutive source rows) x 64 k,
-// reading 128-byte runs of the source columns and writing 64-element runs of the operand rows.
-// grid (ceil((Ipl + Hp) / 64), 4Hp / 32), block (32, 8).
-// G: the cell's gate count (LSTM 4, GRU 3, RNN 1); gate slots g >= G of the 4-slot rho layout
-// stay zero (W and R are G*H x I column-major, gate blocks of H rows, cells.hpp:24-28).
-__global__ void k_pack_wf(const float* __restrict__ W, const float* __restrict__ R, int H, int I,
-                          int Hp, int Ipl, int prec, void* p0, void* p1, int G = 4) {
-  __shared__ float tile[64][33];
-  const int K = Ipl + Hp;
-  const int k0 = blockIdx.x * 64, rho0 = blockIdx.y * 32;
-  const int g = rho_gate(rho0), u0 = rho_unit(rho0);
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int kk = ty; kk < 64; kk += 8) {
-    const int k = k0 + kk, u = u0 + tx;
-    float v = 0.0f;
-    if (u < H && k < K && g < G) {
-      const long long row = (long long)g * H + u;
-      if (k < Ipl) {
-        if (k < I) v = W[(long long)k * G * H + row];
-      } else if (k - Ipl < H) {
-        v = R[(long long)(k - Ipl) * G * H + row];
-      }
-    }
-    tile[kk][tx] = v;
-  }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    for (int kk = tx; kk < 64; kk += 32) {
-      const int k = k0 + kk;
-      if (k < K) store_planes(prec, p0, p1, (long long)(rho0 + r) * K + k, tile[kk][r], pow2f(kWScaleLog2));
-    }
-  }
-}
-
 // Backward operand of layer l: rows = units (Hp), K = [W_{l+1}^T (4Hp, rho order)] ++
 // [R_l^T (4Hp, rho order)]; Wup may be null (top layer). Both sources are 4H x H.
 __global__ void k_pack_wb(const float* __restrict__ Wup, const float* __restrict__ R, int H,

@@ -298,13 +298,13 @@ struct rw_ctx {
   DevBuf gemm_fb;
   bool state0_zero = false;                  // block 0 (h0 = c0 = 0) of the state tapes is current
   bool pp_exported_f = false, pp_exported_b = false;
-  DevBuf wf_next, wb_prev;                   // (unused since the h_t hand-off) / packed W_0^T (backward)
+  DevBuf wb_prev;                            // packed [W_0^T | R_0^T] (cluster backward boundary group)
   DevBuf xin_flags;                          // pipeline stage > 0: per-step counters of its input h_t
   DevBuf wb_prev_lo;                         // fp16x2: lo plane of wb_prev
   void* pp_next_xop_lo = nullptr;            // fp16x2: next stage's layer-input lo plane (peer pointer)
   DevBuf repack_jobs;                        // k_repack's job table (built on the first repack)
   int repack_njobs = 0, repack_tiles = 0;
-  DevBuf wn_raw;                             // the next stage's first-layer W (reference layout, fp32)
+  DevBuf wn_raw;                             // host-given copy of the next stage's W_0 (persistent / stepwise pipeline)
   // [0] forward / [1] backward boundary group (cluster); [2..3] the top layer's [W_next^T | R^T]
   // planes, [4..5] its dG-input planes, [6] the same as CTA-pair boxes (persistent / stepwise)
   std::vector<CUtensorMap> pp_maps = std::vector<CUtensorMap>(8);
@@ -1531,11 +1531,6 @@ void repack_params(rw_ctx* x, cudaStream_t s) {
   ++g_launches;
   k_repack<<<x->repack_tiles, 256, 0, s>>>(static_cast<const RepackJob*>(x->repack_jobs.p), x->repack_njobs, H, Hp,
                                            x->G, x->prec);
-  if (x->pp_next && x->wn_raw.p) {  // forward boundary group: the next stage's W_first (rw_pp_set_next_w)
-    ++g_launches;
-    k_pack_wf<<<dim3(ceil_div(2 * Hp, 64), 4 * Hp / 32), dim3(32, 8), 0, s>>>(x->wn_raw.f(), x->wn_raw.f(), H, H, Hp,
-                                                                           Hp, x->prec, x->wf_next.p, nullptr);
-  }
   if (x->pp_prev && x->wb_prev.p) {  // backward boundary group: [W_0^T | R_0^T] of this stage
     ++g_launches;
     k_pack_wb<<<grid_for((long long)Hp * 8 * Hp), 256, 0, s>>>(x->W[0].f(), x->R[0].f(), H, Hp, x->prec,
@@ -3042,7 +3037,13 @@ extern "C" int rw_pp_link(rw_ctx* x, int dir, const rw_pp_ring* peer, const floa
         top.peer_flags = flags;
         RW_CUDA(cudaMemcpy(dev, &top, sizeof top, cudaMemcpyHostToDevice));
         x->pp_next_ready = static_cast<uint32_t*>(open_region(x, peer, 4));
-        x->pp_wnext = W_next ? W_next : static_cast<const float*>(open_region(x, peer, 3));
+        if (W_next) {  // host copy given (reference layout, G H x H): keep it on the device
+          x->wn_raw.alloc((size_t)x->G * H * H * 4);
+          RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, x->wn_raw.bytes, cudaMemcpyHostToDevice));
+          x->pp_wnext = x->wn_raw.f();
+        } else {  // the next stage's live parameters over the link
+          x->pp_wnext = static_cast<const float*>(open_region(x, peer, 3));
+        }
         x->pp_next = true;
         pp_plain_up(x);
       } else {  // backward: our first layer stores its W-side dG_t into the previous stage's planes
@@ -3128,7 +3129,11 @@ extern "C" int rw_pp_set_next_w(rw_ctx* x, const float* W_next) {
   return guarded(x, [&] {
     if (!x->pp_next) einval("rw_pp_set_next_w: no forward link (rw_pp_link dir 0) on this stage");
     if (x->pp_plain) {  // persistent / stepwise: W_next is packed into the top layer's backward image
-      if (W_next) x->pp_wnext = W_next;
+      if (W_next) {  // a new host copy; NULL: re-read the linked one (the peer's live W_0)
+        x->wn_raw.alloc((size_t)x->G * x->H * x->H * 4);
+        RW_CUDA(cudaMemcpy(x->wn_raw.p, W_next, x->wn_raw.bytes, cudaMemcpyHostToDevice));
+        x->pp_wnext = x->wn_raw.f();
+      }
       x->repack_njobs = 0;
       x->dirty = true;
       invalidate_graphs(x);

@@ -531,15 +531,18 @@ class Engine:
         return bytes(r)
 
     def pp_link(self, direction: int, peer: bytes, w_next=None) -> None:
-        """0: link to the next stage's forward export (h_t hand-off; w_next unused, kept for
-        compatibility); 1: link to the previous stage's backward export."""
+        """0: link to the next stage's forward export (h_t hand-off; w_next: the next stage's
+        first-layer W as a host array -- cluster: unused; persistent / stepwise: packed into the
+        top layer's backward image, None = read the next stage's live W_0 over the link);
+        1: link to the previous stage's backward export."""
         r = _lib.rw_pp_ring.from_buffer_copy(peer)
         w = as_matrix(w_next) if w_next is not None else None
         self._check(self._L.rw_pp_link(self._ctx, direction, C.byref(r), _fp(w)))
 
     def pp_set_next_w(self, w_next) -> None:
-        """rw_pp_set_next_w: a validated no-op since the forward hand-off sends h_t."""
-        w = as_matrix(w_next)
+        """rw_pp_set_next_w: after the next stage's parameters changed (persistent / stepwise:
+        re-pack W_next, optionally from a new host array; cluster: a validated no-op)."""
+        w = as_matrix(w_next) if w_next is not None else None
         self._check(self._L.rw_pp_set_next_w(self._ctx, _fp(w)))
 
     def launch_count(self, reset: bool = False) -> int:

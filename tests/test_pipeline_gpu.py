@@ -256,3 +256,56 @@ def test_pipeline_stages_run_concurrently(schedule, precision, monkeypatch):
         for j in range(cnt):
             assert np.array_equal(dw[j], dw_r[lo + j]), ("dW", lo + j)
     assert elapsed < 20.0  # no flag wait ran into its timeout
+
+
+@pytest.mark.parametrize("host_w", [False, True], ids=["live-peer-W", "host-W_next"])
+def test_pipeline_plain_follows_parameter_updates(host_w, monkeypatch):
+    """Persistent family: the lower stage's top-layer backward multiplies by the next stage's
+    W_0. After an optimizer step it must use the new W_0 -- read live over the link (set_params
+    marks the image for re-packing) or, when the link was given a host copy, the copy handed to
+    rw_pp_set_next_w -- bitwise a fresh single context on the new parameters."""
+    from paper_1604_01946_b200 import Engine
+    from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process
+    monkeypatch.setenv("RW_FWD_KSPLIT", "1")
+    monkeypatch.setenv("RW_BWD_KSPLIT", "1")
+    c, params, x, dy, _, _ = make_case(Dims(4, 128, 128, 32, 6), seed=43, bias=True)
+    H, I, B, T, L, n = c.hidden, c.input, c.batch, c.steps, c.layers, 2
+    stages = [PipelineStage(c, k, n, schedule="persistent") for k in range(n)]
+    for s in stages:
+        s.set_params(params)
+    ex = [s.export() for s in stages]
+    stages[0].engine.pp_link(0, ex[1][0], params[2].w if host_w else None)
+    stages[1].engine.pp_link(1, ex[0][1])
+    zx = np.zeros((H, B * T), np.float32, order="F")
+    for k, s in enumerate(stages):
+        s.engine.upload_inputs(x if k == 0 else zx, dy if k == n - 1 else zx)
+
+    def run():
+        for s in stages:
+            s.engine.run_pass(3)
+            s.engine.sync()
+        for s in reversed(stages):
+            s.engine.run_pass(1)
+            s.engine.sync()
+        dr = [np.zeros((4 * H, H), np.float32, order="F") for _ in range(2)]
+        stages[0].engine.read_outputs(dr=dr)
+        return dr
+
+    run()
+    for p in params:  # "optimizer step"
+        p.w[:] = p.w * np.float32(0.9) + np.float32(0.01)
+        p.r[:] = p.r * np.float32(1.1)
+    stages[1].set_params(params)  # only the upper stage's parameters are re-sent ...
+    stages[0].set_params(params)
+    if host_w:  # ... and the lower stage gets the new W_next as a host copy
+        stages[0].engine.pp_set_next_w(params[2].w)
+    dr = run()
+    ref = Engine(c, precision="bf16", schedule="persistent")
+    ref.set_params(params)
+    ref.upload_inputs(x, dy)
+    ref.run_pass(2)
+    ref.sync()
+    dr_r = [np.zeros((4 * H, H), np.float32, order="F") for _ in range(L)]
+    ref.read_outputs(dr=dr_r)
+    for j in range(2):
+        assert np.array_equal(dr[j], dr_r[j]), j
