@@ -158,6 +158,7 @@ struct RecParams {
   // x pp_in_flags[T] (the sender's CTAs per step, written at link time).
   const uint32_t* pp_in_flags;
   const uint32_t* pp_epoch;
+  int tape_prefetch;  // backward: L2 bulk prefetch of the forward tapes ahead of the cell phase
 };
 
 __device__ __forceinline__ uint32_t pp_target(const RecParams& p) {
@@ -519,6 +520,8 @@ __device__ __forceinline__ uint32_t rec_setup_pair(const RecSmem& S, const RecPa
     mbar_init(S.a_full, 1);
     mbar_init(S.tmem_full, 1);
     mbar_init(S.tmem_empty, tmem_empty_count);
+    mbar_init(S.pfull, 1);                       // second accumulator buffer (k_lstm_bwd pair)
+    mbar_init(S.pempty, tmem_empty_count);
     mbar_init(S.xready, 1);
     mbar_init(S.xfree, 1);
     fence_barrier_init();
@@ -980,6 +983,31 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     rec_teardown(ks, tmem_base, tmem_cols);
 }
 
+// Backward epilogue: pull the forward tapes a chunk of batch columns will read (written long
+// before, so not in L2) into L2 ahead of the cell math -- per column the tile's 128-unit rows of
+// each tape are contiguous 512-byte runs, one bulk prefetch each. Without it the cell phase is
+// bound by dependent HBM loads (config E: ~96 us per step per CTA, profiles/r02/spans_E_bf16.txt).
+template <int kKind>
+__device__ __forceinline__ void bwd_tape_prefetch(const BwdLayer& Le, const RecParams& p, int t, long long nbase,
+                                                  int ncols, int row0, int et) {
+  if (t < 0 || ncols <= 0 || row0 >= p.Hp) return;
+  constexpr int kSeg = kKind == kCellLstm ? 6 : kKind == kCellGru ? 5 : 1;
+  const long long Hp = p.Hp, G4 = 4 * Hp;
+  const uint32_t bytes = (uint32_t)min(128, p.Hp - row0) * 4u;
+  for (int i = et; i < ncols * kSeg; i += kEpiThreads) {
+    const int c = i / kSeg, sg = i - c * kSeg;
+    const long long col = (long long)t * p.Bp + nbase + c;
+    const float* a;
+    if constexpr (kKind == kCellLstm)
+      a = sg < 4 ? Le.gates + col * G4 + sg * Hp + row0 : (sg == 4 ? Le.tanhc : Le.c) + col * Hp + row0;
+    else if constexpr (kKind == kCellGru)
+      a = sg < 3 ? Le.gates + col * G4 + sg * Hp + row0 : (sg == 3 ? Le.zrh : Le.h) + col * Hp + row0;
+    else
+      a = Le.h + (col + p.Bp) * Hp + row0;
+    bulk_prefetch_l2(a, bytes);
+  }
+}
+
 // ====================================================================== backward kernel
 // kPair (bf16, ksplit 1, streamed A): CTA pairs as in k_lstm_fwd<_, true>; the leader's
 // tmem_empty barrier collects one arrival per CTA before the next step's MMAs overwrite either
@@ -1018,8 +1046,15 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                                              ~uintptr_t(1023));
   const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // pair (one accumulator per step, no promotion): two accumulator buffers in tensor memory, so
+  // step t's MMAs (its W^T dG_up half first) run while the epilogue still drains step t+1 --
+  // with one buffer they waited for the drain of the last column chunk, i.e. most of the cell
+  // phase (config E: 269 us per step, profiles/r02/spans_E_bf16.txt)
+  const bool dbuf = kPair && p.n_acc == 1 && !p.promo && 2 * N <= 512;
+  uint64_t* const tfull[2] = {S.tmem_full, dbuf ? S.pfull : S.tmem_full};
+  uint64_t* const tempty[2] = {S.tmem_empty, dbuf ? S.pempty : S.tmem_empty};
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(N * (p.n_acc + p.promo))) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * (dbuf ? 2 : p.n_acc + p.promo))) tmem_cols <<= 1;
   // pair: the leader's tmem_empty takes one arrival per CTA (after its epilogue drained TMEM)
   const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols, 2) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
@@ -1121,10 +1156,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         uint32_t pc = 0;
         for (int it = 0; it < p.n_steps; ++it) {
           const int t = p.t_first - it;
-          if (it > 0) {
-            mbar_wait(S.tmem_empty, (it - 1) & 1);  // both CTAs drained their accumulators
+          const int bi = dbuf ? (it & 1) : 0;
+          const int use = dbuf ? (it >> 1) : it;  // earlier steps that used buffer bi
+          if (use > 0) {
+            mbar_wait(tempty[bi], (use - 1) & 1);  // both CTAs drained this buffer
             tc_fence_after();
           }
+          const uint32_t tacc = tmem_base + (uint32_t)(bi * N);
           bool first = true;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             if (!kb_active(kb, t)) continue;
@@ -1135,13 +1173,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             const uint64_t b0 = sdesc_sw128(smem_u32(S.b_st + s * b_stage), 16, 1024);
 #pragma unroll
             for (int kk = 0; kk < P::kAtomK / P::kUmmaK; ++kk)
-              g2::umma2_warp(tmem_base, desc_add(a0, kk * 32), desc_add(b0, kk * 32), idesc,
+              g2::umma2_warp(tacc, desc_add(a0, kk * 32), desc_add(b0, kk * 32), idesc,
                              (!first || kk) ? 1u : 0u);
             g2::commit2_warp(&S.empty[s]);
             first = false;
             ++pc;
           }
-          g2::commit2_warp(S.tmem_full);
+          g2::commit2_warp(tfull[bi]);
         }
       }
     }
@@ -1201,6 +1239,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     float gmax = 0.0f;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
+      if (p.tape_prefetch) {  // the first chunk's tapes, while this step's MMAs run
+        const int nc = min(kXChunk, N), nco = nc / ks;
+        bwd_tape_prefetch<kKind>(Le, p, t, rank * nco, nco, row0, et);
+      }
       int ns[2] = {0, 0};
       for (int kb = kb_lo; kb < kb_hi; ++kb) ns[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
       const int nact = ns[0] + ns[1];
@@ -1208,10 +1250,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const int n_chunks = (!kPair && p.promo) ? nc0 + (ns[1] + p.acc_kb - 1) / p.acc_kb : (nact + p.acc_kb - 1) / p.acc_kb;
       const int n_used = (!kPair && p.promo) ? (n_chunks > 0 ? 1 : 0) : n_chunks;
       if (et == 0) progress(p, 2, it, 1);
+      const int bi = dbuf ? (it & 1) : 0;
+      const uint32_t tacc = tmem_base + (uint32_t)(bi * N);
       if (!kPair && p.promo) {
         promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, p.us_in, p.us_rec);
       } else {
-        mbar_wait(S.tmem_full, it & 1);
+        mbar_wait(tfull[bi], (dbuf ? (it >> 1) : it) & 1);
         tc_fence_after();
       }
       if (et == 0) trace_stamp(p, it, 2);
@@ -1222,14 +1266,14 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         xchg_wait_free(S, ks, xc);
         for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
-          load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
+          load_acc_sum(tacc + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
           xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
         if (n0 + kXChunk >= N && (kPair || !p.promo)) {
           tc_fence_before();
           if constexpr (kPair) {
             named_bar_sync(1, kEpiThreads);  // the whole CTA drained its TMEM accumulator
-            if (et == 0) mbar_arrive_remote(S.tmem_empty, 0);
+            if (et == 0) mbar_arrive_remote(tempty[bi], 0);
           } else {
             mbar_arrive(S.tmem_empty);
           }
@@ -1238,6 +1282,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         xchg_publish(S, ks, xc);
         if (et == 0 && n0 == 0) trace_stamp(p, it, 4);
         const long long cbase = (long long)n0 + rank * nco;  // first owned batch column
+        if (p.tape_prefetch && n0 + kXChunk < N) {  // the next chunk's tapes, behind this chunk's math
+          const int nc2 = min(kXChunk, N - n0 - kXChunk), nco2 = nc2 / ks;
+          bwd_tape_prefetch<kKind>(Le, p, t, (long long)n0 + kXChunk + rank * nco2, nco2, row0, et);
+        }
         if (u < p.Hp) {
           float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
           // owned columns cl = hh + 2k, processed 8 at a time: all loads first, then math
