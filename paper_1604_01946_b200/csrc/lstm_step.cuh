@@ -1046,11 +1046,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                                              ~uintptr_t(1023));
   const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // pair (one accumulator per step, no promotion): two accumulator buffers in tensor memory, so
+  // one accumulator per step (no promotion): two accumulator buffers in tensor memory, so
   // step t's MMAs (its W^T dG_up half first) run while the epilogue still drains step t+1 --
   // with one buffer they waited for the drain of the last column chunk, i.e. most of the cell
   // phase (config E: 269 us per step, profiles/r02/spans_E_bf16.txt)
-  const bool dbuf = kPair && p.n_acc == 1 && !p.promo && 2 * N <= 512;
+  const bool dbuf = p.n_acc == 1 && !p.promo && 2 * N <= 512;
   uint64_t* const tfull[2] = {S.tmem_full, dbuf ? S.pfull : S.tmem_full};
   uint64_t* const tempty[2] = {S.tmem_empty, dbuf ? S.pempty : S.tmem_empty};
   uint32_t tmem_cols = 32;
@@ -1193,8 +1193,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
       progress(p, 1, it, 1);
-      if (it > 0 && !p.promo) {
-        mbar_wait(S.tmem_empty, (it - 1) & 1);
+      const int bi = dbuf ? (it & 1) : 0;
+      const int use = dbuf ? (it >> 1) : it;  // earlier steps that used accumulator buffer bi
+      if (use > 0 && !p.promo) {
+        mbar_wait(tempty[bi], (use - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
@@ -1207,7 +1209,8 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         const int s = pc % p.stages;
         const int sg = kb < nkb0 ? 0 : 1;
         const bool cstart = p.promo ? iseg[sg] % p.acc_kb == 0 : nact % p.acc_kb == 0;
-        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch) : tmem_base + (nact / p.acc_kb) * N;
+        const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch)
+                                     : tmem_base + (uint32_t)(bi * N) + (nact / p.acc_kb) * N;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
@@ -1222,7 +1225,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
         ++pc;
       }
-      if (!p.promo) umma_commit_warp(S.tmem_full);
+      if (!p.promo) umma_commit_warp(tfull[bi]);
     }
   } else if (warp >= 4) {
     const BwdLayer Le = Ly;  // register copy (see the forward epilogue)
@@ -1275,7 +1278,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             named_bar_sync(1, kEpiThreads);  // the whole CTA drained its TMEM accumulator
             if (et == 0) mbar_arrive_remote(tempty[bi], 0);
           } else {
-            mbar_arrive(S.tmem_empty);
+            mbar_arrive(tempty[bi]);
           }
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
