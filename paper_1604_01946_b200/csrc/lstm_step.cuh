@@ -667,8 +667,13 @@ __global__ void __launch_bounds__(kRecThreads, 1)
                                              ~uintptr_t(1023));
   const RecSmem S = carve(smem, a_total, b_stage, p.stages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // persistent, one accumulator per step (no promotion): two accumulator buffers, so step t's
+  // W.x half runs while the epilogue still drains step t-1 (as k_lstm_bwd)
+  const bool dbuf = !kPair && p.persistent && p.n_acc == 1 && !p.promo && 2 * N <= 512;
+  uint64_t* const tfull[2] = {S.tmem_full, dbuf ? S.pfull : S.tmem_full};
+  uint64_t* const tempty[2] = {S.tmem_empty, dbuf ? S.pempty : S.tmem_empty};
   uint32_t tmem_cols = 32;
-  while (tmem_cols < (uint32_t)(N * (p.n_acc + p.promo))) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)(N * (dbuf ? 2 : p.n_acc + p.promo))) tmem_cols <<= 1;
   const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols) : rec_setup(S, p, ks, tmem_cols);
   const int row0 = tile * kTileM;
 
@@ -795,8 +800,10 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     const int s0_hi = min(kb_hi, nkb0);  // this CTA's K segment 0 (W.x) is [kb_lo, s0_hi)
     for (int it = 0; it < p.n_steps; ++it) {
       progress(p, 1, it, 1);
-      if (it > 0 && !p.promo) {
-        mbar_wait(S.tmem_empty, (it - 1) & 1);
+      const int ab = dbuf ? (it & 1) : 0;  // accumulator buffer (not "bi": the bias below)
+      const int use = dbuf ? (it >> 1) : it;  // earlier steps that used buffer ab
+      if (use > 0 && !p.promo) {
+        mbar_wait(tempty[ab], (use - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
@@ -808,7 +815,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         const int nseg = kb < nkb0 ? s0_hi - kb_lo : kb_hi - max(kb_lo, nkb0);
         const bool cstart = p.promo ? iseg % p.acc_kb == 0 : nact % p.acc_kb == 0;
         const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch)
-                                     : tmem_base + (nact / p.acc_kb) * N;  // accumulator of this k-block
+                                     : tmem_base + (uint32_t)(ab * N) + (nact / p.acc_kb) * N;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(S.a_res + (p.resident ? (kb - kb_lo) : s) * a_stage);
@@ -820,7 +827,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           ++ch;
         }
       }
-      if (!p.promo) umma_commit_warp(S.tmem_full);
+      if (!p.promo) umma_commit_warp(tfull[ab]);
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
@@ -845,10 +852,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first + it;
       if (et == 0) progress(p, 2, it, 1);
+      const int ab = dbuf ? (it & 1) : 0;  // accumulator buffer (bi is the input-gate bias)
+      const uint32_t tacc = tmem_base + (uint32_t)(ab * N);
       if (p.promo) {
         promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, sc0, p.us_rec);
       } else {
-        mbar_wait(S.tmem_full, it & 1);
+        mbar_wait(tfull[ab], (dbuf ? (it >> 1) : it) & 1);
         tc_fence_after();
       }
       if (et == 0) trace_stamp(p, it, 2);
@@ -859,12 +868,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         xchg_wait_free(S, ks, xc);
         for (int c0 = half * (nc >> 1); c0 < (half + 1) * (nc >> 1); c0 += 8) {
           float a[8];
-          load_acc_sum(tmem_base + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
+          load_acc_sum(tacc + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
           xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
         if (n0 + kXChunk >= N && !p.promo) {
           tc_fence_before();
-          mbar_arrive(S.tmem_empty);
+          mbar_arrive(tempty[ab]);
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
         xchg_publish(S, ks, xc);
