@@ -158,7 +158,6 @@ struct RecParams {
   // x pp_in_flags[T] (the sender's CTAs per step, written at link time).
   const uint32_t* pp_in_flags;
   const uint32_t* pp_epoch;
-  int tape_prefetch;  // backward: L2 bulk prefetch of the forward tapes ahead of the cell phase
 };
 
 __device__ __forceinline__ uint32_t pp_target(const RecParams& p) {
@@ -992,31 +991,6 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     rec_teardown(ks, tmem_base, tmem_cols);
 }
 
-// Backward epilogue: pull the forward tapes a chunk of batch columns will read (written long
-// before, so not in L2) into L2 ahead of the cell math -- per column the tile's 128-unit rows of
-// each tape are contiguous 512-byte runs, one bulk prefetch each. Without it the cell phase is
-// bound by dependent HBM loads (config E: ~96 us per step per CTA, profiles/r02/spans_E_bf16.txt).
-template <int kKind>
-__device__ __forceinline__ void bwd_tape_prefetch(const BwdLayer& Le, const RecParams& p, int t, long long nbase,
-                                                  int ncols, int row0, int et) {
-  if (t < 0 || ncols <= 0 || row0 >= p.Hp) return;
-  constexpr int kSeg = kKind == kCellLstm ? 6 : kKind == kCellGru ? 5 : 1;
-  const long long Hp = p.Hp, G4 = 4 * Hp;
-  const uint32_t bytes = (uint32_t)min(128, p.Hp - row0) * 4u;
-  for (int i = et; i < ncols * kSeg; i += kEpiThreads) {
-    const int c = i / kSeg, sg = i - c * kSeg;
-    const long long col = (long long)t * p.Bp + nbase + c;
-    const float* a;
-    if constexpr (kKind == kCellLstm)
-      a = sg < 4 ? Le.gates + col * G4 + sg * Hp + row0 : (sg == 4 ? Le.tanhc : Le.c) + col * Hp + row0;
-    else if constexpr (kKind == kCellGru)
-      a = sg < 3 ? Le.gates + col * G4 + sg * Hp + row0 : (sg == 3 ? Le.zrh : Le.h) + col * Hp + row0;
-    else
-      a = Le.h + (col + p.Bp) * Hp + row0;
-    bulk_prefetch_l2(a, bytes);
-  }
-}
-
 // ====================================================================== backward kernel
 // kPair (bf16, ksplit 1, streamed A): CTA pairs as in k_lstm_fwd<_, true>; the leader's
 // tmem_empty barrier collects one arrival per CTA before the next step's MMAs overwrite either
@@ -1251,10 +1225,6 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     float gmax = 0.0f;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
-      if (p.tape_prefetch) {  // the first chunk's tapes, while this step's MMAs run
-        const int nc = min(kXChunk, N), nco = nc / ks;
-        bwd_tape_prefetch<kKind>(Le, p, t, rank * nco, nco, row0, et);
-      }
       int ns[2] = {0, 0};
       for (int kb = kb_lo; kb < kb_hi; ++kb) ns[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
       const int nact = ns[0] + ns[1];
@@ -1294,10 +1264,6 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         xchg_publish(S, ks, xc);
         if (et == 0 && n0 == 0) trace_stamp(p, it, 4);
         const long long cbase = (long long)n0 + rank * nco;  // first owned batch column
-        if (p.tape_prefetch && n0 + kXChunk < N) {  // the next chunk's tapes, behind this chunk's math
-          const int nc2 = min(kXChunk, N - n0 - kXChunk), nco2 = nc2 / ks;
-          bwd_tape_prefetch<kKind>(Le, p, t, (long long)n0 + kXChunk + rank * nco2, nco2, row0, et);
-        }
         if (u < p.Hp) {
           float si = 0.0f, sf = 0.0f, so = 0.0f, sc = 0.0f;  // db partials (cells.hpp:163-168)
           // owned columns cl = hh + 2k, processed 8 at a time: all loads first, then math

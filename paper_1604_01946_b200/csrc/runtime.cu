@@ -1564,8 +1564,6 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   }
   rp.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
-  rp.tape_prefetch = 1;  // RW_TAPE_PREFETCH=0 disables (measurement)
-  if (const char* e = getenv("RW_TAPE_PREFETCH")) rp.tape_prefetch = atoi(e);
   if (fwd && x->pp_plain && x->pp_prev) {  // layer 0's input is the previous stage's h_t
     rp.pp_in_flags = static_cast<const uint32_t*>(x->xin_flags.p);
     rp.pp_epoch = static_cast<const uint32_t*>(x->cl_epoch.p);

@@ -103,10 +103,6 @@ RW_DEVICE void mbar_wait_bounded(uint64_t* bar, uint32_t phase) { mbar_wait(bar,
 RW_DEVICE void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
-// L2 prefetch of a contiguous global range (16-byte aligned, size a multiple of 16).
-RW_DEVICE void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 // L2 prefetch of one 2-D box (no shared-memory destination, no completion).
 RW_DEVICE void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
