@@ -158,6 +158,7 @@ struct RecParams {
   // x pp_in_flags[T] (the sender's CTAs per step, written at link time).
   const uint32_t* pp_in_flags;
   const uint32_t* pp_epoch;
+  int acc_dbuf;  // persistent kernels: two accumulator buffers when a step fits one (RW_ACC_DBUF)
 };
 
 __device__ __forceinline__ uint32_t pp_target(const RecParams& p) {
@@ -393,6 +394,7 @@ struct RecSmem {
   uint32_t* tmem_slot;
 };
 constexpr int kMaxPromoSlots = 8;
+__device__ __forceinline__ uint64_t* acc_bar(int b, uint64_t* b0, uint64_t* b1) { return b ? b1 : b0; }
 
 __device__ __forceinline__ RecSmem carve(uint8_t* smem, int a_bytes_total, int b_stage_bytes,
                                          int stages) {
@@ -668,9 +670,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // persistent, one accumulator per step (no promotion): two accumulator buffers, so step t's
   // W.x half runs while the epilogue still drains step t-1 (as k_lstm_bwd)
-  const bool dbuf = !kPair && p.persistent && p.n_acc == 1 && !p.promo && 2 * N <= 512;
-  uint64_t* const tfull[2] = {S.tmem_full, dbuf ? S.pfull : S.tmem_full};
-  uint64_t* const tempty[2] = {S.tmem_empty, dbuf ? S.pempty : S.tmem_empty};
+  const bool dbuf = p.acc_dbuf && !kPair && p.persistent && p.n_acc == 1 && !p.promo && 2 * N <= 512;
+  // accumulator buffer 1's barriers (selected with acc_bar, not a dynamically indexed array,
+  // which would live on the stack)
+  uint64_t* const tfull1 = dbuf ? S.pfull : S.tmem_full;
+  uint64_t* const tempty1 = dbuf ? S.pempty : S.tmem_empty;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * (dbuf ? 2 : p.n_acc + p.promo))) tmem_cols <<= 1;
   const uint32_t tmem_base = kPair ? rec_setup_pair(S, p, tmem_cols) : rec_setup(S, p, ks, tmem_cols);
@@ -802,7 +806,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const int ab = dbuf ? (it & 1) : 0;  // accumulator buffer (not "bi": the bias below)
       const int use = dbuf ? (it >> 1) : it;  // earlier steps that used buffer ab
       if (use > 0 && !p.promo) {
-        mbar_wait(tempty[ab], (use - 1) & 1);
+        mbar_wait(acc_bar(ab, S.tmem_empty, tempty1), (use - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
@@ -826,7 +830,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           ++ch;
         }
       }
-      if (!p.promo) umma_commit_warp(tfull[ab]);
+      if (!p.promo) umma_commit_warp(acc_bar(ab, S.tmem_full, tfull1));
     }
   } else if (warp >= 4) {
     // ================= epilogue: split-K exchange + LSTM cell (cells.hpp:227-260)
@@ -856,7 +860,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       if (p.promo) {
         promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, sc0, p.us_rec);
       } else {
-        mbar_wait(tfull[ab], (dbuf ? (it >> 1) : it) & 1);
+        mbar_wait(acc_bar(ab, S.tmem_full, tfull1), (dbuf ? (it >> 1) : it) & 1);
         tc_fence_after();
       }
       if (et == 0) trace_stamp(p, it, 2);
@@ -872,7 +876,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         }
         if (n0 + kXChunk >= N && !p.promo) {
           tc_fence_before();
-          mbar_arrive(tempty[ab]);
+          mbar_arrive(acc_bar(ab, S.tmem_empty, tempty1));
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 3);
         xchg_publish(S, ks, xc);
@@ -1033,9 +1037,11 @@ __global__ void __launch_bounds__(kRecThreads, 1)
   // step t's MMAs (its W^T dG_up half first) run while the epilogue still drains step t+1 --
   // with one buffer they waited for the drain of the last column chunk, i.e. most of the cell
   // phase (config E: 269 us per step, profiles/r02/spans_E_bf16.txt)
-  const bool dbuf = p.n_acc == 1 && !p.promo && 2 * N <= 512;
-  uint64_t* const tfull[2] = {S.tmem_full, dbuf ? S.pfull : S.tmem_full};
-  uint64_t* const tempty[2] = {S.tmem_empty, dbuf ? S.pempty : S.tmem_empty};
+  const bool dbuf = p.acc_dbuf && p.n_acc == 1 && !p.promo && 2 * N <= 512;
+  // accumulator buffer 1's barriers (selected with acc_bar, not a dynamically indexed array,
+  // which would live on the stack)
+  uint64_t* const tfull1 = dbuf ? S.pfull : S.tmem_full;
+  uint64_t* const tempty1 = dbuf ? S.pempty : S.tmem_empty;
   uint32_t tmem_cols = 32;
   while (tmem_cols < (uint32_t)(N * (dbuf ? 2 : p.n_acc + p.promo))) tmem_cols <<= 1;
   // pair: the leader's tmem_empty takes one arrival per CTA (after its epilogue drained TMEM)
@@ -1142,7 +1148,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           const int bi = dbuf ? (it & 1) : 0;
           const int use = dbuf ? (it >> 1) : it;  // earlier steps that used buffer bi
           if (use > 0) {
-            mbar_wait(tempty[bi], (use - 1) & 1);  // both CTAs drained this buffer
+            mbar_wait(acc_bar(bi, S.tmem_empty, tempty1), (use - 1) & 1);  // both CTAs drained this buffer
             tc_fence_after();
           }
           const uint32_t tacc = tmem_base + (uint32_t)(bi * N);
@@ -1162,7 +1168,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
             first = false;
             ++pc;
           }
-          g2::commit2_warp(tfull[bi]);
+          g2::commit2_warp(acc_bar(bi, S.tmem_full, tfull1));
         }
       }
     }
@@ -1179,19 +1185,22 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       const int bi = dbuf ? (it & 1) : 0;
       const int use = dbuf ? (it >> 1) : it;  // earlier steps that used accumulator buffer bi
       if (use > 0 && !p.promo) {
-        mbar_wait(tempty[bi], (use - 1) & 1);
+        mbar_wait(acc_bar(bi, S.tmem_empty, tempty1), (use - 1) & 1);
         tc_fence_after();
       }
       progress(p, 1, it, 2);
       // active k-blocks of this step per K segment (the ring closes a chunk on each segment's last)
-      int nseg[2] = {0, 0};
-      for (int kb = kb_lo; kb < kb_hi; ++kb) nseg[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
-      int nact = 0, iseg[2] = {0, 0};  // active k-blocks so far this step (overall, per segment)
+      // (scalars, not [2] arrays indexed by segment: those would live on the stack)
+      int nseg0 = 0, nseg1 = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb)
+        if (kb_active(kb, t)) ++(kb < nkb0 ? nseg0 : nseg1);
+      int nact = 0, nact0 = 0;  // active k-blocks so far this step (overall, in segment 0)
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         if (!kb_active(kb, t)) continue;
         const int s = pc % p.stages;
-        const int sg = kb < nkb0 ? 0 : 1;
-        const bool cstart = p.promo ? iseg[sg] % p.acc_kb == 0 : nact % p.acc_kb == 0;
+        const bool sg0 = kb < nkb0;
+        const int iseg = sg0 ? nact0 : nact - nact0;  // position inside this k-block's segment
+        const bool cstart = p.promo ? iseg % p.acc_kb == 0 : nact % p.acc_kb == 0;
         const uint32_t acc = p.promo ? promo_slot(S, p, tmem_base, N, cstart, ch)
                                      : tmem_base + (uint32_t)(bi * N) + (nact / p.acc_kb) * N;
         mbar_wait(&S.full[s], (pc / p.stages) & 1);
@@ -1200,15 +1209,15 @@ __global__ void __launch_bounds__(kRecThreads, 1)
         const uint32_t b_base = smem_u32(S.b_st + s * b_stage);
         mma_kblock<P>(acc, a_base, b_base, a_bytes, b_bytes, idesc, cstart);
         ++nact;
-        ++iseg[sg];
+        nact0 += sg0 ? 1 : 0;
         umma_commit_warp(&S.empty[s]);
-        if (p.promo && (iseg[sg] % p.acc_kb == 0 || iseg[sg] == nseg[sg])) {
+        if (p.promo && ((iseg + 1) % p.acc_kb == 0 || iseg + 1 == (sg0 ? nseg0 : nseg1))) {
           umma_commit_warp(&S.pfull[ch % (uint32_t)p.n_acc]);
           ++ch;
         }
         ++pc;
       }
-      if (!p.promo) umma_commit_warp(tfull[bi]);
+      if (!p.promo) umma_commit_warp(acc_bar(bi, S.tmem_full, tfull1));
     }
   } else if (warp >= 4) {
     const BwdLayer Le = Ly;  // register copy (see the forward epilogue)
@@ -1225,11 +1234,12 @@ __global__ void __launch_bounds__(kRecThreads, 1)
     float gmax = 0.0f;
     for (int it = 0; it < p.n_steps; ++it) {
       const int t = p.t_first - it;
-      int ns[2] = {0, 0};
-      for (int kb = kb_lo; kb < kb_hi; ++kb) ns[kb < nkb0 ? 0 : 1] += kb_active(kb, t) ? 1 : 0;
-      const int nact = ns[0] + ns[1];
-      const int nc0 = (ns[0] + p.acc_kb - 1) / p.acc_kb;
-      const int n_chunks = (!kPair && p.promo) ? nc0 + (ns[1] + p.acc_kb - 1) / p.acc_kb : (nact + p.acc_kb - 1) / p.acc_kb;
+      int ns0 = 0, ns1 = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb)
+        if (kb_active(kb, t)) ++(kb < nkb0 ? ns0 : ns1);
+      const int nact = ns0 + ns1;
+      const int nc0 = (ns0 + p.acc_kb - 1) / p.acc_kb;
+      const int n_chunks = (!kPair && p.promo) ? nc0 + (ns1 + p.acc_kb - 1) / p.acc_kb : (nact + p.acc_kb - 1) / p.acc_kb;
       const int n_used = (!kPair && p.promo) ? (n_chunks > 0 ? 1 : 0) : n_chunks;
       if (et == 0) progress(p, 2, it, 1);
       const int bi = dbuf ? (it & 1) : 0;
@@ -1237,7 +1247,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       if (!kPair && p.promo) {
         promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, p.us_in, p.us_rec);
       } else {
-        mbar_wait(tfull[bi], (dbuf ? (it >> 1) : it) & 1);
+        mbar_wait(acc_bar(bi, S.tmem_full, tfull1), (dbuf ? (it >> 1) : it) & 1);
         tc_fence_after();
       }
       if (et == 0) trace_stamp(p, it, 2);
@@ -1255,9 +1265,9 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           tc_fence_before();
           if constexpr (kPair) {
             named_bar_sync(1, kEpiThreads);  // the whole CTA drained its TMEM accumulator
-            if (et == 0) mbar_arrive_remote(tempty[bi], 0);
+            if (et == 0) mbar_arrive_remote(acc_bar(bi, S.tmem_empty, tempty1), 0);
           } else {
-            mbar_arrive(tempty[bi]);
+            mbar_arrive(acc_bar(bi, S.tmem_empty, tempty1));
           }
         }
         if (et == 0 && n0 == 0) trace_stamp(p, it, 3);

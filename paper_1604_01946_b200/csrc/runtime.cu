@@ -1564,6 +1564,8 @@ RecParams rec_params(rw_ctx* x, bool fwd) {
   }
   rp.gmax = fwd ? nullptr : static_cast<unsigned*>(x->errflag.p) + 2;
   rp.flag_target = (uint32_t)(rp.tiles * rp.ksplit);
+  rp.acc_dbuf = 1;
+  if (const char* e = getenv("RW_ACC_DBUF")) rp.acc_dbuf = atoi(e);
   if (fwd && x->pp_plain && x->pp_prev) {  // layer 0's input is the previous stage's h_t
     rp.pp_in_flags = static_cast<const uint32_t*>(x->xin_flags.p);
     rp.pp_epoch = static_cast<const uint32_t*>(x->cl_epoch.p);
