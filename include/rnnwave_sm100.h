@@ -215,9 +215,13 @@ int rw_comm_overlap(rw_ctx* ctx, int on);
  * bf16 or fp32-parity operands; both stages of a link in the same family. Exported descriptors carry CUDA
  * IPC handles (cross-process) and raw pointers (same-process stages, tests). */
 typedef struct {
-  char handle[5][64];     /* cudaIpcMemHandle_t of the regions: dir 0: input image / per-step
-                             input counters / (same) / plain layer-input planes / input-ready
-                             counter; dir 1: ring data / done / consumed */
+  char handle[5][64];     /* cudaIpcMemHandle_t of the regions. mode 0 (cluster): dir 0: input
+                             image / per-step input counters / lo plane of the plain layer input
+                             / plain layer-input planes / input-ready counter; dir 1: ring data /
+                             done / consumed. mode 1 (persistent / stepwise): dir 0: layer-input
+                             plane 0 / per-step counters (+ senders per step at [T]) / plane 1 /
+                             W_0 (reference layout) / input-ready counter; dir 1: dG-input
+                             plane 0 / per-step counters / plane 1 */
   uint64_t offset[5];     /* byte offset of the region inside each exported allocation */
   uint64_t ptr[5];        /* device pointers in the exporting process */
   int64_t pid;            /* exporting process */
