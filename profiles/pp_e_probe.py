@@ -7,7 +7,9 @@ persistent / stepwise hand-off at full scale, not a multi-GPU speed-up. (Both st
 at once on ONE GPU deadlock at this size: the later stage's step kernels fill the SMs while
 spinning on counters the earlier stage can then not get SMs to release -- the flag timeout
 ends it with an error. On separate GPUs, the deployment, each stage has its own SMs.)
-Usage: python profiles/pp_e_probe.py [layers,hidden,input,batch,steps] [precision] [reps]"""
+Usage: python profiles/pp_e_probe.py [layers,hidden,input,batch,steps] [precision] [reps] [seq|conc]
+conc: both stages in flight at once on their own streams (no host sync between the stages) --
+for shapes whose two stages fit on the GPU together (e.g. C1024: 2 x 2 layers, persistent)."""
 import json
 import os
 import sys
@@ -26,6 +28,7 @@ from paper_1604_01946_b200.pipeline import PipelineStage, link_in_process  # noq
 dims = Dims(*[int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "8,2048,2048,256,100").split(",")])
 prec = sys.argv[2] if len(sys.argv) > 2 else "bf16"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+mode = sys.argv[4] if len(sys.argv) > 4 else "seq"
 n = 2
 c, params, x, dy, _, _ = make_case(dims, seed=41, bias=True)
 H, I, B, T, L = c.hidden, c.input, c.batch, c.steps, c.layers
@@ -78,9 +81,13 @@ for k, s in enumerate(stages):
 def pipelined():
     for s in stages:
         s.engine.run_pass(3)
-        s.engine.sync()
+        if mode == "seq":
+            s.engine.sync()
     for s in reversed(stages):
         s.engine.run_pass(1)
+        if mode == "seq":
+            s.engine.sync()
+    for s in stages:
         s.engine.sync()
 
 
@@ -99,8 +106,8 @@ for s in stages:
         same["db"] &= bool(np.array_equal(db[j], db_r[l]))
         worst = max(worst, float(np.abs(dw[j] - dw_r[l]).max()))
 flops = 3 * 2 * 4 * H * (I + H) * B * T * L  # forward + backward_data + weight_update
-print(json.dumps({"config": dict(layers=L, hidden=H, input=I, batch=B, steps=T), "precision": prec,
-                  "single_ms": round(ms_single, 2), "pipeline_2stage_sequential_ms": round(ms_pp, 2),
+print(json.dumps({"config": dict(layers=L, hidden=H, input=I, batch=B, steps=T), "precision": prec, "mode": mode,
+                  "single_ms": round(ms_single, 2), "pipeline_2stage_ms": round(ms_pp, 2),
                   "single_tflops": round(flops / ms_single / 1e9, 1),
                   "pipeline_tflops": round(flops / ms_pp / 1e9, 1),
                   "bitwise_equal": same, "max_abs_diff": worst,
