@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
       if (et == 0) progress(p, 2, it, 1);
       const int ab = dbuf ? (it & 1) : 0;  // accumulator buffer (bi is the input-gate bias)
       const uint32_t tacc = tmem_base + (uint32_t)(ab * N);
-      if (p.promo) {
+      if (!kPair && p.promo) {  // (the CTA-pair kernel never promotes: keep it out of its code)
         promo_drain(S, p, tmem_base, N, n_chunks, ech, nc0, sc0, p.us_rec);
       } else {
         mbar_wait(acc_bar(ab, S.tmem_full, tfull1), (dbuf ? (it >> 1) : it) & 1);
@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(kRecThreads, 1)
           load_acc_sum(tacc + (uint32_t(q * 32) << 16) + n0 + c0, N, n_used, a);
           xchg_push8(S, ks, rank, nco, q, lane, c0, a, inv);
         }
-        if (n0 + kXChunk >= N && !p.promo) {
+        if (n0 + kXChunk >= N && (kPair || !p.promo)) {
           tc_fence_before();
           mbar_arrive(acc_bar(ab, S.tmem_empty, tempty1));
         }
