@@ -79,7 +79,9 @@ constexpr unsigned long long kWaitNs = 20ULL * 1000000000ULL;
 constexpr int kWaitTimeoutCode = (1 << 30) | (3 << 28) | 15;
 static __shared__ int* rw_wait_err;
 RW_DEVICE void set_wait_error(int* e) { rw_wait_err = e; }
-RW_DEVICE bool mbar_wait_slow(uint64_t* bar, uint32_t phase) {
+// out of line: inlined at every wait site it would add its timer / error-word code to each
+// producer, MMA and epilogue loop
+static __device__ __noinline__ bool mbar_wait_slow(uint64_t* bar, uint32_t phase) {
   const uint64_t t0 = globaltimer();
   int* const err = rw_wait_err;
 #pragma unroll 1
