@@ -244,6 +244,22 @@ __device__ __forceinline__ bool flag_reached(uint32_t v, uint32_t target) { retu
 
 // Spin until *flag reaches target (gpu-scope acquire), bounded by a timeout that records an
 // error instead of hanging the device. `code` identifies the wait for the host message.
+// the timed back-off of wait_flag, out of line (as mbar_wait_slow): only long waits get here
+static __device__ __noinline__ void wait_flag_slow(const uint32_t* flag, uint32_t target, int* error,
+                                                   unsigned long long timeout_ns, int code) {
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
+#pragma unroll 1
+  while (!flag_reached(ld_relaxed_gpu(flag), target)) {
+    nanosleep(ns);
+    if (ns < 128) ns <<= 1;
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicCAS(error, 0, code);
+      atomicMax(error + 1, (int)ld_relaxed_gpu(flag));
+      return;
+    }
+  }
+}
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target, int* error,
                                           unsigned long long timeout_ns, int code) {
   // Poll with relaxed loads (an acquire load per iteration would invalidate the SM's L1 each
@@ -251,20 +267,7 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
   bool ok = flag_reached(ld_relaxed_gpu(flag), target);
 #pragma unroll 1
   for (int i = 0; i < 65536 && !ok; ++i) ok = flag_reached(ld_relaxed_gpu(flag), target);
-  if (!ok) {
-    const uint64_t t0 = globaltimer();
-    uint32_t ns = 32;
-#pragma unroll 1
-    while (!flag_reached(ld_relaxed_gpu(flag), target)) {
-      nanosleep(ns);
-      if (ns < 128) ns <<= 1;
-      if (globaltimer() - t0 > timeout_ns) {
-        atomicCAS(error, 0, code);
-        atomicMax(error + 1, (int)ld_relaxed_gpu(flag));
-        return;
-      }
-    }
-  }
+  if (!ok) wait_flag_slow(flag, target, error, timeout_ns, code);
   (void)ld_acquire_gpu(flag);
 }
 __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t target,
